@@ -1,0 +1,258 @@
+/* oracle.c -- fp64 CPU oracle for the Artificial Retina hot path.
+ *
+ * TEST INFRASTRUCTURE ONLY.  Only tests/, __graft_entry__.smoke() and
+ * bench.py's cpu_baseline / --impl reference legs may load this library.
+ * The product path (paper_1709_08610_b200/) never imports, links or calls it,
+ * and this file shares no code, header, table or constant with it.
+ *
+ * What it computes is the plain definition, in double precision, on the same
+ * fp32 input arrays the GPU receives (promoted exactly to double):
+ *
+ *   Eq. (1)  (Sec. 2)   R(theta) = sum_k exp(-s(x_k, theta)^2 / sigma^2)
+ *   Eq. (2)              R_ij = R(theta_ij) on a lattice of units
+ *   grad R    chain rule through s^2 (derivation below)
+ *   step iii             "select clusters of activated units" read as
+ *                                       strict local maxima over existing neighbours
+ *                                       with R >= R0 (reading Z6)
+ *   Alg. 1         multi-start: theta^0 = seeds, q fixed updates
+ *                                       theta <- clamp(theta + eta grad R) (reading Z7),
+ *                                       cluster, per cluster keep the highest R >= R0
+ *                                       (readings Z9, Z10)
+ *
+ * Distance s ("the distance between hit x and the line defined by
+ * parameters theta"; PAPER.md:74 / 195 "euclidean distance in corresponding
+ * detector planes"):
+ *   model 0  LINE2D  theta = (a, b),        hit (x, y):    s   = y - (a x + b)
+ *   model 1  SLOPE2  theta = (tx, ty),      hit (x, y, z): s^2 = (x - tx d)^2 + (y - ty d)^2, d = z - z_ref
+ *   model 2  SLOPE3  theta = (tx, ty, z0),  hit (x, y, z): s^2 = (x - tx d)^2 + (y - ty d)^2, d = z - z0
+ *
+ * Sums run sequentially in hit-array order.  No cutoff on far hits.
+ */
+#define _GNU_SOURCE
+#include <math.h>
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+#ifdef _OPENMP
+#include <omp.h>
+#endif
+
+enum { ORA_LINE2D = 0, ORA_SLOPE2 = 1, ORA_SLOPE3 = 2 };
+
+static int model_P(int model) { return model == ORA_SLOPE3 ? 3 : 2; }
+
+int ora_num_threads(void) {
+#ifdef _OPENMP
+    return omp_get_max_threads();
+#else
+    return 1;
+#endif
+}
+
+/* R, grad R and A_i = sum_k |d_i t_k| at one theta (Eq. 1 and its gradient).
+ *
+ * With t_k = exp(-s_k^2 / sigma^2):
+ *   LINE2D: s = y - a x - b;  dR/da = (2/sigma^2) sum t s x;  dR/db = (2/sigma^2) sum t s
+ *   SLOPE2/3: s_x = x - tx d, s_y = y - ty d
+ *           dR/dtx = (2/sigma^2) sum t s_x d;  dR/dty = (2/sigma^2) sum t s_y d
+ *   SLOPE3:   dR/dz0 = -(2/sigma^2) sum t (s_x tx + s_y ty)      (d = z - z0, dd/dz0 = -1)
+ * grad and A may be NULL. */
+void ora_point(int model, const float *hits, int n, double z_ref, const double *theta,
+               double sigma, double *R_out, double *grad, double *A) {
+    const double inv_s2 = 1.0 / (sigma * sigma);
+    const int P = model_P(model);
+    double R = 0.0, g[3] = {0, 0, 0}, a[3] = {0, 0, 0};
+    for (int k = 0; k < n; ++k) {
+        const double x = hits[4 * k + 0], y = hits[4 * k + 1], z = hits[4 * k + 2];
+        double s2, dg[3] = {0, 0, 0};
+        if (model == ORA_LINE2D) {
+            const double s = y - (theta[0] * x + theta[1]);
+            s2 = s * s;
+            dg[0] = s * x;
+            dg[1] = s;
+        } else {
+            const double d = (model == ORA_SLOPE3) ? z - theta[2] : z - z_ref;
+            const double sx = x - theta[0] * d, sy = y - theta[1] * d;
+            s2 = sx * sx + sy * sy;
+            dg[0] = sx * d;
+            dg[1] = sy * d;
+            if (model == ORA_SLOPE3) dg[2] = -(sx * theta[0] + sy * theta[1]);
+        }
+        const double t = exp(-s2 * inv_s2);
+        R += t;
+        for (int i = 0; i < P; ++i) {
+            g[i] += t * dg[i];
+            a[i] += fabs(t * dg[i]);
+        }
+    }
+    *R_out = R;
+    for (int i = 0; i < P; ++i) {
+        if (grad) grad[i] = 2.0 * inv_s2 * g[i];
+        if (A) A[i] = 2.0 * inv_s2 * a[i];
+    }
+}
+
+/* Eq. (2): R at every node tuple of every event.  out is [E][n0][n1]([n2]),
+ * last axis fastest.  nodes_k are fp32 node tables (reading Z4). */
+void ora_grid(int model, int n_events, const int32_t *offsets, const float *hits, double z_ref,
+              double sigma, const int32_t *axis_len, const float *nodes0, const float *nodes1,
+              const float *nodes2, double *out) {
+    const int P = model_P(model);
+    const int64_t n0 = axis_len[0], n1 = axis_len[1], n2 = (P == 3) ? axis_len[2] : 1;
+    const int64_t per_event = n0 * n1 * n2;
+#pragma omp parallel for collapse(2) schedule(dynamic)
+    for (int64_t e = 0; e < n_events; ++e) {
+        for (int64_t i = 0; i < n0; ++i) {
+            const float *h = hits + 4 * (int64_t)offsets[e];
+            const int n = offsets[e + 1] - offsets[e];
+            for (int64_t j = 0; j < n1; ++j) {
+                for (int64_t l = 0; l < n2; ++l) {
+                    double th[3] = {nodes0[i], nodes1[j], P == 3 ? nodes2[l] : 0.0};
+                    double R;
+                    ora_point(model, h, n, z_ref, th, sigma, &R, NULL, NULL);
+                    out[e * per_event + (i * n1 + j) * n2 + l] = R;
+                }
+            }
+        }
+    }
+}
+
+/* Step (iii), reading Z6: cell c is a peak iff R_c >= R0 and
+ * R_c > R_n for every EXISTING neighbour n (3^P - 1 of them in the interior;
+ * boundary cells have fewer).  Peaks are listed in ascending linear index;
+ * count is the true count, entries past `capacity` are dropped. */
+void ora_peaks(const double *grid, int n_events, int P, const int32_t *axis_len, double threshold,
+               int capacity, int32_t *peak_index, double *peak_value, int32_t *peak_count) {
+    const int64_t n0 = axis_len[0], n1 = axis_len[1], n2 = (P == 3) ? axis_len[2] : 1;
+    const int64_t per_event = n0 * n1 * n2;
+#pragma omp parallel for schedule(dynamic)
+    for (int e = 0; e < n_events; ++e) {
+        const double *g = grid + e * per_event;
+        int32_t cnt = 0;
+        for (int64_t i = 0; i < n0; ++i)
+            for (int64_t j = 0; j < n1; ++j)
+                for (int64_t l = 0; l < n2; ++l) {
+                    const int64_t c = (i * n1 + j) * n2 + l;
+                    const double v = g[c];
+                    int is_peak = v >= threshold;
+                    for (int di = -1; di <= 1 && is_peak; ++di)
+                        for (int dj = -1; dj <= 1 && is_peak; ++dj)
+                            for (int dl = (P == 3 ? -1 : 0); dl <= (P == 3 ? 1 : 0) && is_peak; ++dl) {
+                                if (di == 0 && dj == 0 && dl == 0) continue;
+                                const int64_t ii = i + di, jj = j + dj, ll = l + dl;
+                                if (ii < 0 || ii >= n0 || jj < 0 || jj >= n1 || ll < 0 || ll >= n2) continue;
+                                if (!(v > g[(ii * n1 + jj) * n2 + ll])) is_peak = 0;
+                            }
+                    if (is_peak) {
+                        if (cnt < capacity) {
+                            peak_index[(int64_t)e * capacity + cnt] = (int32_t)c;
+                            peak_value[(int64_t)e * capacity + cnt] = v;
+                        }
+                        ++cnt;
+                    }
+                }
+        peak_count[e] = cnt;
+    }
+}
+
+/* Algorithm 1, lines "for j = 1..q: compute R, grad R; theta^j := update[...]"
+ * with update = fixed-step ascent clamped to the prior box
+ * (reading Z7): theta^{j+1} = clamp(theta^j + eta grad R(theta^j)).  Returns
+ * theta^n, R(theta^n) and grad R(theta^n) (grad_out may be NULL). */
+void ora_multistart(int model, int n_events, const int32_t *offsets, const float *hits,
+                    double z_ref, double sigma, int n_seeds, const float *seeds, int n_iters,
+                    double step, const double *box_lo, const double *box_hi, double *theta_out,
+                    double *R_out, double *grad_out) {
+    const int P = model_P(model);
+#pragma omp parallel for collapse(2) schedule(dynamic, 16)
+    for (int64_t e = 0; e < n_events; ++e) {
+        for (int64_t s = 0; s < n_seeds; ++s) {
+            const float *h = hits + 4 * (int64_t)offsets[e];
+            const int n = offsets[e + 1] - offsets[e];
+            const int64_t id = (int64_t)e * n_seeds + s;
+            double th[3] = {0, 0, 0}, g[3], R;
+            for (int i = 0; i < P; ++i) th[i] = seeds[id * P + i];
+            for (int j = 0; j < n_iters; ++j) {
+                ora_point(model, h, n, z_ref, th, sigma, &R, g, NULL);
+                for (int i = 0; i < P; ++i) {
+                    double v = th[i] + step * g[i];
+                    if (v < box_lo[i]) v = box_lo[i];
+                    if (v > box_hi[i]) v = box_hi[i];
+                    th[i] = v;
+                }
+            }
+            ora_point(model, h, n, z_ref, th, sigma, &R, g, NULL);
+            for (int i = 0; i < P; ++i) theta_out[id * P + i] = th[i];
+            R_out[id] = R;
+            if (grad_out)
+                for (int i = 0; i < P; ++i) grad_out[id * P + i] = g[i];
+        }
+    }
+}
+
+/* Algorithm 1, "cluster solutions; for each cluster select solution with
+ * highest response and above threshold R0", readings Z9/Z10:
+ *   keep items with R >= R0; order them by (R desc, theta lexicographic asc,
+ *   seed index asc); scan that order: an item joins the EARLIEST-created leader
+ *   L with max_i |theta_i - L_i| <= r_i, else it founds a new leader.  Leaders
+ *   are emitted in creation order with their cluster sizes. */
+typedef struct { const double *theta; const double *R; int P; } merge_ctx;
+
+static int merge_cmp(const void *pa, const void *pb, void *vctx) {
+    const merge_ctx *c = (const merge_ctx *)vctx;
+    const int32_t a = *(const int32_t *)pa, b = *(const int32_t *)pb;
+    if (c->R[a] > c->R[b]) return -1;
+    if (c->R[a] < c->R[b]) return 1;
+    for (int i = 0; i < c->P; ++i) {
+        if (c->theta[(int64_t)a * c->P + i] < c->theta[(int64_t)b * c->P + i]) return -1;
+        if (c->theta[(int64_t)a * c->P + i] > c->theta[(int64_t)b * c->P + i]) return 1;
+    }
+    return (a < b) ? -1 : (a > b);
+}
+
+void ora_merge(int n_events, int n_seeds, int P, const double *theta, const double *R,
+               const double *radius, double threshold, int capacity, double *track_theta,
+               double *track_R, int32_t *track_seed, int32_t *track_size, int32_t *track_count) {
+#pragma omp parallel for schedule(dynamic)
+    for (int e = 0; e < n_events; ++e) {
+        const double *th = theta + (int64_t)e * n_seeds * P;
+        const double *r = R + (int64_t)e * n_seeds;
+        int32_t *items = (int32_t *)malloc(sizeof(int32_t) * (n_seeds > 0 ? n_seeds : 1));
+        int32_t *leader = (int32_t *)malloc(sizeof(int32_t) * (n_seeds > 0 ? n_seeds : 1));
+        int32_t *size = (int32_t *)malloc(sizeof(int32_t) * (n_seeds > 0 ? n_seeds : 1));
+        int m = 0;
+        for (int s = 0; s < n_seeds; ++s)
+            if (r[s] >= threshold) items[m++] = s;
+        merge_ctx ctx = {th, r, P};
+        qsort_r(items, m, sizeof(int32_t), merge_cmp, &ctx);
+        int L = 0;
+        for (int q = 0; q < m; ++q) {
+            const int s = items[q];
+            int found = -1;
+            for (int l = 0; l < L && found < 0; ++l) {
+                int inside = 1;
+                for (int i = 0; i < P; ++i)
+                    if (!(fabs(th[(int64_t)s * P + i] - th[(int64_t)leader[l] * P + i]) <= radius[i])) inside = 0;
+                if (inside) found = l;
+            }
+            if (found >= 0) {
+                size[found] += 1;
+            } else {
+                leader[L] = s;
+                size[L] = 1;
+                ++L;
+            }
+        }
+        for (int l = 0; l < L && l < capacity; ++l) {
+            const int64_t o = (int64_t)e * capacity + l;
+            for (int i = 0; i < P; ++i) track_theta[o * P + i] = th[(int64_t)leader[l] * P + i];
+            track_R[o] = r[leader[l]];
+            track_seed[o] = leader[l];
+            track_size[o] = size[l];
+        }
+        track_count[e] = L;
+        free(items);
+        free(leader);
+        free(size);
+    }
+}

@@ -1,0 +1,146 @@
+"""ctypes front end of the fp64 C oracle (oracle.c).
+
+TEST INFRASTRUCTURE ONLY: imported by tests/, __graft_entry__.smoke() and
+bench.py's cpu_baseline / --impl reference legs, never by the product package.
+Every function takes the same fp32 arrays the CUDA path receives and returns
+float64 results; the arithmetic lives in oracle.c (see its header for the
+PAPER.md passages each function follows).
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+from typing import Optional, Sequence
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SRC = os.path.join(_HERE, "oracle.c")
+_LIB = os.path.join(_HERE, "liboracle.so")
+_lib = None
+
+LINE2D, SLOPE2, SLOPE3 = 0, 1, 2
+
+
+def build(force: bool = False) -> str:
+    """Compile oracle.c (plain C, -O2, no fast-math, OpenMP)."""
+    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
+        subprocess.check_call(["gcc", "-O2", "-fopenmp", "-fPIC", "-shared", "-o", _LIB, _SRC, "-lm"])
+    return _LIB
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        build()
+        L = ctypes.CDLL(_LIB)
+        P = ctypes.c_void_p
+        i, d = ctypes.c_int, ctypes.c_double
+        L.ora_num_threads.restype = i
+        L.ora_point.argtypes = [i, P, i, d, P, d, P, P, P]
+        L.ora_grid.argtypes = [i, i, P, P, d, d, P, P, P, P, P]
+        L.ora_peaks.argtypes = [P, i, i, P, d, i, P, P, P]
+        L.ora_multistart.argtypes = [i, i, P, P, d, d, i, P, i, d, P, P, P, P, P]
+        L.ora_merge.argtypes = [i, i, i, P, P, P, d, i, P, P, P, P, P]
+        for f in (L.ora_point, L.ora_grid, L.ora_peaks, L.ora_multistart, L.ora_merge):
+            f.restype = None
+        _lib = L
+    return _lib
+
+
+def _p(a: Optional[np.ndarray]):
+    return None if a is None else a.ctypes.data_as(ctypes.c_void_p)
+
+
+def _f32(a) -> np.ndarray:
+    return np.ascontiguousarray(np.asarray(a, dtype=np.float32))
+
+
+def _f(v) -> float:
+    """Reading Z18: scalars reach the GPU as fp32; the oracle uses that fp32 value promoted."""
+    return float(np.float32(v))
+
+
+def _P(model: int) -> int:
+    return 3 if model == SLOPE3 else 2
+
+
+def num_threads() -> int:
+    return int(lib().ora_num_threads())
+
+
+def point(model: int, hits, theta, sigma: float, z_ref: float = 0.0):
+    """Eq. (1) and its gradient at one theta: returns (R, grad[P], A[P])."""
+    h = _f32(hits).reshape(-1, 4)
+    th = np.ascontiguousarray(np.asarray(theta, np.float64))
+    R = np.zeros(1)
+    g = np.zeros(_P(model))
+    A = np.zeros(_P(model))
+    lib().ora_point(model, _p(h), len(h), _f(z_ref), _p(th), _f(sigma), _p(R), _p(g), _p(A))
+    return float(R[0]), g, A
+
+
+def grid(model: int, offsets, hits, nodes: Sequence[np.ndarray], sigma: float,
+         z_ref: float = 0.0) -> np.ndarray:
+    """Eq. (2): float64 [E, n0, n1(, n2)]."""
+    off = np.ascontiguousarray(np.asarray(offsets, np.int32))
+    h = _f32(hits).reshape(-1, 4)
+    nd = [_f32(n) for n in nodes]
+    P = _P(model)
+    assert len(nd) == P
+    alen = np.array([len(n) for n in nd], np.int32)
+    E = len(off) - 1
+    out = np.zeros((E,) + tuple(alen), np.float64)
+    lib().ora_grid(model, E, _p(off), _p(h), _f(z_ref), _f(sigma), _p(alen),
+                   _p(nd[0]), _p(nd[1]), _p(nd[2]) if P == 3 else None, _p(out))
+    return out
+
+
+def peaks(grid_values: np.ndarray, P: int, threshold: float, capacity: int):
+    """Reading Z6 peaks of a [E, n0, n1(, n2)] grid: (index[E,cap], value[E,cap], count[E])."""
+    g = np.ascontiguousarray(np.asarray(grid_values, np.float64))
+    E = g.shape[0]
+    alen = np.array(g.shape[1:], np.int32)
+    assert len(alen) == P
+    idx = np.full((E, max(capacity, 1)), -1, np.int32)
+    val = np.zeros((E, max(capacity, 1)), np.float64)
+    cnt = np.zeros(E, np.int32)
+    lib().ora_peaks(_p(g), E, P, _p(alen), _f(threshold), int(capacity), _p(idx), _p(val), _p(cnt))
+    return idx[:, :capacity], val[:, :capacity], cnt
+
+
+def multistart(model: int, offsets, hits, seeds, sigma: float, n_iters: int, step: float,
+               box_lo, box_hi, z_ref: float = 0.0, want_grad: bool = True):
+    """Algorithm 1 update loop (reading Z7): (theta[E,S,P], R[E,S], grad[E,S,P] or None)."""
+    off = np.ascontiguousarray(np.asarray(offsets, np.int32))
+    h = _f32(hits).reshape(-1, 4)
+    sd = _f32(seeds)
+    E, S, P = sd.shape
+    assert P == _P(model) and E == len(off) - 1
+    lo = np.ascontiguousarray(np.asarray(box_lo, np.float32).astype(np.float64))
+    hi = np.ascontiguousarray(np.asarray(box_hi, np.float32).astype(np.float64))
+    th = np.zeros((E, S, P))
+    R = np.zeros((E, S))
+    g = np.zeros((E, S, P)) if want_grad else None
+    lib().ora_multistart(model, E, _p(off), _p(h), _f(z_ref), _f(sigma), S, _p(sd),
+                         int(n_iters), _f(step), _p(lo), _p(hi), _p(th), _p(R), _p(g))
+    return th, R, g
+
+
+def merge(theta, R, radius, threshold: float, capacity: int):
+    """Algorithm 1 "cluster ... select highest response above R0" (readings Z9/Z10).
+    Returns (track_theta[E,cap,P], track_R[E,cap], seed[E,cap], size[E,cap], count[E])."""
+    th = np.ascontiguousarray(np.asarray(theta, np.float64))
+    r = np.ascontiguousarray(np.asarray(R, np.float64))
+    E, S, P = th.shape
+    rad = np.ascontiguousarray(np.asarray(radius, np.float32).astype(np.float64))
+    cap = max(capacity, 1)
+    tt = np.zeros((E, cap, P))
+    tr = np.zeros((E, cap))
+    ts = np.full((E, cap), -1, np.int32)
+    tz = np.zeros((E, cap), np.int32)
+    tc = np.zeros(E, np.int32)
+    lib().ora_merge(E, S, P, _p(th), _p(r), _p(rad), _f(threshold), int(capacity),
+                    _p(tt), _p(tr), _p(ts), _p(tz), _p(tc))
+    return tt[:, :capacity], tr[:, :capacity], ts[:, :capacity], tz[:, :capacity], tc

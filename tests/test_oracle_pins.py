@@ -1,0 +1,404 @@
+"""Pins of the fp64 oracle against what the paper and mathematics fix (CPU only).
+
+Each test names the pin id of DESIGN.md §5 (P1..P13) and the passage it
+follows.  None of them re-types oracle.c's formula: they use closed forms,
+invariants, special cases, independent numerical differentiation, library
+routines (scipy.ndimage) and brute force on tiny inputs.
+"""
+import itertools
+import math
+import os
+
+import numpy as np
+import pytest
+from scipy import ndimage
+
+from oracle import brute
+from oracle import oracle as ora
+from synth import configs as C
+from synth import events as G
+
+GOLDEN = os.path.join(os.path.dirname(__file__), "golden", "closed_forms.txt")
+
+
+def golden():
+    out = {}
+    for line in open(GOLDEN):
+        line = line.strip()
+        if not line or line.startswith("#"):
+            continue
+        k, v = line.split()
+        out[k] = float(v)
+    return out
+
+
+def h4(rows):
+    a = np.zeros((len(rows), 4), np.float32)
+    for i, r in enumerate(rows):
+        a[i, :len(r)] = r
+    return a
+
+
+# ---------------------------------------------------------------- P1
+def test_P1_hit_on_pattern_contributes_exactly_one():
+    # tx = k / 2^10, integer z: x = tx z is exact, so s = 0 exactly in every model.
+    tx, ty = 77 / 1024, -301 / 1024
+    rows = [(tx * z, ty * z, z) for z in (30.0, 60.0, 450.0, 750.0)]
+    R, g, _ = ora.point(C.SLOPE2, h4(rows), (tx, ty), 0.44)
+    assert R == 4.0 and np.all(g == 0.0)
+    z0 = -37.0
+    rows3 = [(tx * (z - z0), ty * (z - z0), z) for z in (30.0, 60.0, 750.0)]
+    R3, g3, _ = ora.point(C.SLOPE3, h4(rows3), (tx, ty, z0), 0.88)
+    assert R3 == 3.0 and np.all(g3 == 0.0)
+    a, b = 0.25, -0.375
+    rows2 = [(x, a * x + b) for x in (1.0, 2.0, 7.0)]
+    R2, g2, _ = ora.point(C.LINE2D, h4(rows2), (a, b), 0.005)
+    assert R2 == 3.0 and np.all(g2 == 0.0)
+
+
+# ---------------------------------------------------------------- P2
+def test_P2_bounds_0_le_R_le_N():
+    rng = np.random.default_rng(0)
+    for model in (C.LINE2D, C.SLOPE2, C.SLOPE3):
+        for _ in range(20):
+            n = int(rng.integers(0, 40))
+            h = rng.normal(0, 3, (n, 4)).astype(np.float32)
+            h[:, 2] = np.abs(h[:, 2]) * 100
+            th = rng.normal(0, 0.2, 3)[: 3 if model == C.SLOPE3 else 2]
+            R, _, _ = ora.point(model, h, th, float(rng.uniform(0.05, 5)))
+            assert 0.0 <= R <= n
+
+
+# ---------------------------------------------------------------- P3
+def test_P3_closed_form_distances():
+    gv = golden()
+    sig = float(np.float32(0.44031311))
+    # SLOPE2, theta = 0: s = |(x, y)| in the plane
+    assert ora.point(C.SLOPE2, h4([]), (0, 0), sig)[0] == 0.0
+    assert ora.point(C.SLOPE2, h4([(0, 0, 100)]), (0, 0), sig)[0] == gv["one_hit_s0"]
+    R1 = ora.point(C.SLOPE2, h4([(sig, 0, 100)]), (0, 0), sig)[0]
+    assert abs(R1 - gv["one_hit_s_sigma"]) <= 1e-15
+    # distance 2 sigma along y -- also pins that s^2 = s_x^2 + s_y^2 (no sqrt, no 1/2)
+    R2 = ora.point(C.SLOPE2, h4([(0, -sig, 30), (0, 2 * sig, 30)]), (0, 0), sig)[0]
+    assert abs(R2 - gv["hits_sigma_2sigma"]) <= 1e-15
+    # 3 sigma split over both coordinates as a 3-4-5 triangle: sigma = 5/8,
+    # (s_x, s_y) = (9/8, 3/2) are exact binaries with s_x^2 + s_y^2 = 9 sigma^2
+    R3 = ora.point(C.SLOPE2, h4([(1.125, 1.5, 1)]), (0, 0), 0.625)[0]
+    assert abs(R3 - gv["one_hit_s_3sigma"]) <= 1e-15
+    # LINE2D: vertical residual y - (a x + b)
+    RL = ora.point(C.LINE2D, h4([(3.0, 1.0 + 0.25), (5.0, 1.0 - 0.5)]), (0.0, 1.0), 0.25)[0]
+    assert abs(RL - gv["hits_sigma_2sigma"]) <= 1e-15
+
+
+# ---------------------------------------------------------------- P4 (north star: brute force)
+@pytest.mark.parametrize("model", [C.LINE2D, C.SLOPE2, C.SLOPE3])
+def test_P4_brute_force_mpmath(model):
+    rng = np.random.default_rng(10 + model)
+    for _ in range(6):
+        n = int(rng.integers(1, 16))
+        P = 3 if model == C.SLOPE3 else 2
+        th_true = np.array([rng.uniform(-0.3, 0.3), rng.uniform(-0.3, 0.3), rng.uniform(-20, 20)])[:P]
+        z = np.sort(rng.choice(C.VELO_PLANES[1:], n))
+        if model == C.LINE2D:
+            x = rng.integers(1, 11, n).astype(float)
+            rows = [(xi, th_true[0] * xi + th_true[1] + rng.normal(0, 0.01)) for xi in x]
+        else:
+            d = z - (th_true[2] if model == C.SLOPE3 else 0.0)
+            rows = [(th_true[0] * di + rng.normal(0, .05), th_true[1] * di + rng.normal(0, .05), zi)
+                    for di, zi in zip(d, z)]
+        h = h4(rows)
+        sigma = float(np.float32(0.05 if model == C.LINE2D else 0.3))
+        th = th_true + rng.normal(0, [1e-3, 1e-3, 0.1][:P])
+        R, g, A = ora.point(model, h, th, sigma)
+        Rb = float(brute.response(model, h, th, sigma))
+        gb = [float(v) for v in brute.gradient(model, h, th, sigma)]
+        assert abs(R - Rb) <= 1e-13 * max(Rb, 1e-300)
+        for i in range(P):
+            assert abs(g[i] - gb[i]) <= 1e-12 * max(A[i], 1e-300)
+
+
+# ---------------------------------------------------------------- P5
+@pytest.mark.parametrize("model", [C.LINE2D, C.SLOPE2, C.SLOPE3])
+def test_P5_gradient_vs_central_differences(model):
+    cfg = {C.LINE2D: C.CFG0, C.SLOPE2: C.CFG2, C.SLOPE3: C.CFG4}[model]
+    b = G.make_batch(cfg, [0])
+    h = b.event_hits(0)
+    rng = np.random.default_rng(5)
+    P = cfg.P
+    for k in range(8):
+        t0 = b.truth[0][k % len(b.truth[0])]
+        th = np.array(t0, float) + rng.normal(0, [2e-3, 2e-3, 0.5][:P])
+        _, g, A = ora.point(model, h, th, cfg.sigma)
+        scale = np.array([1e-6, 1e-6, 1e-4][:P])
+        for i in range(P):
+            e = np.zeros(P)
+            e[i] = scale[i]
+            # Richardson-extrapolated central difference: O(h^4)
+            d1 = (ora.point(model, h, th + e, cfg.sigma)[0] - ora.point(model, h, th - e, cfg.sigma)[0]) / (2 * e[i])
+            d2 = (ora.point(model, h, th + 2 * e, cfg.sigma)[0] - ora.point(model, h, th - 2 * e, cfg.sigma)[0]) / (4 * e[i])
+            fd = (4 * d1 - d2) / 3
+            assert abs(g[i] - fd) <= 1e-5 * max(A[i], 1e-9), (i, g[i], fd, A[i])
+
+
+# ---------------------------------------------------------------- P6
+def test_P6_mirror_pair_zero_gradient():
+    tx, ty, d = 0.1, -0.05, 300.0
+    cx, cy = tx * d, ty * d
+    for dx, dy, axis in ((0.2, 0.0, 0), (0.0, 0.3, 1)):
+        h = h4([(cx + dx, cy + dy, d), (cx - dx, cy - dy, d)])
+        _, g, A = ora.point(C.SLOPE2, h, (tx, ty), 0.44)
+        assert abs(g[axis]) <= 1e-12 * A[axis]
+        assert A[axis] > 0
+    # LINE2D: hits mirrored about the line in y at the same x -> dR/db = 0
+    h = h4([(4.0, 2.125 + 0.015625), (4.0, 2.125 - 0.015625)])  # exact binaries
+    _, g, A = ora.point(C.LINE2D, h, (0.5, 0.125), 0.03125)
+    assert abs(g[1]) <= 1e-12 * A[1] and abs(g[0]) <= 1e-12 * A[0]
+
+
+# ---------------------------------------------------------------- P7
+def test_P7_invariants():
+    b = G.make_batch(C.CFG2, [3])
+    h = b.event_hits(0)
+    th = b.truth[0][0] + 1e-3
+    s = C.CFG2.sigma
+    RA = ora.point(C.SLOPE2, h[:400], th, s)[0]
+    RB = ora.point(C.SLOPE2, h[400:], th, s)[0]
+    R = ora.point(C.SLOPE2, h, th, s)[0]
+    assert abs(R - (RA + RB)) <= 1e-13 * R  # additivity
+    Rs = [ora.point(C.SLOPE2, h, th, sg)[0] for sg in (0.1, 0.2, 0.44, 1.0, 3.0)]
+    assert all(a <= b for a, b in zip(Rs, Rs[1:]))  # non-decreasing in sigma
+    # LINE2D translation: y -> y + delta and b -> b + delta leaves R unchanged
+    b0 = G.make_batch(C.CFG0, [0])
+    h0 = b0.event_hits(0).copy()
+    h0[:, 1] = np.round(h0[:, 1] * 2.0 ** 16) / 2.0 ** 16  # so that y + delta is exact in fp32
+    delta = 0.5
+    h1 = h0.copy()
+    h1[:, 1] += np.float32(delta)
+    for a_, b_ in ((0.1, 0.2), (-0.3, 0.7)):
+        r0 = ora.point(C.LINE2D, h0, (a_, b_), 0.02)[0]
+        r1 = ora.point(C.LINE2D, h1, (a_, b_ + delta), 0.02)[0]
+        assert abs(r0 - r1) <= 1e-12 * max(r0, 1e-3)
+    # special-case reductions between models: SLOPE3 with z0 = c == SLOPE2 with z_ref = c
+    for c in (0.0, -42.5, 17.25):
+        r2, g2, _ = ora.point(C.SLOPE2, h, th, s, z_ref=c)
+        r3, g3, _ = ora.point(C.SLOPE3, h, (th[0], th[1], c), s)
+        assert r2 == r3 and np.all(g2 == g3[:2])
+
+
+# ---------------------------------------------------------------- P8 (derived from PAPER.md:38)
+def test_P8_single_hit_closed_form_and_grid_argmax():
+    sig = 0.44031311
+    x, y, d = 7.3, -4.1, 270.0
+    h = h4([(x, y, d)])
+    rng = np.random.default_rng(1)
+    for _ in range(10):
+        t = rng.uniform(-0.3, 0.3, 2)
+        # R(t) = exp(-d^2 |t - h/d|^2 / sigma^2)
+        u = np.array([x, y]) / d
+        closed = math.exp(-d * d * float(np.sum((t - u) ** 2)) / (sig * sig))
+        R, g, _ = ora.point(C.SLOPE2, h, t, float(np.float32(sig)))
+        sig32 = float(np.float32(sig))
+        closed32 = math.exp(-d * d * float(np.sum((t - np.array([np.float32(x), np.float32(y)]) / d) ** 2)) / sig32 ** 2)
+        assert abs(R - closed32) <= 1e-12
+        gc = 2 * d * d / sig32 ** 2 * closed32 * (np.array([np.float32(x), np.float32(y)]) / d - t)
+        assert np.allclose(g, gc, rtol=1e-9, atol=1e-300)
+    # the grid argmax is the node nearest h/d (per axis, the grid is separable)
+    nodes = G.axis_nodes(C.CFG1)
+    Rg = ora.grid(C.SLOPE2, [0, 1], h, nodes, 0.05)
+    i, j = np.unravel_index(np.argmax(Rg[0]), Rg[0].shape)
+    assert i == np.argmin(np.abs(nodes[0].astype(float) - np.float32(x) / d))
+    assert j == np.argmin(np.abs(nodes[1].astype(float) - np.float32(y) / d))
+
+
+# ---------------------------------------------------------------- P9
+def test_P9_noiseless_recovery_grid_and_multistart():
+    nodes = [np.linspace(-0.3, 0.3, 61).astype(np.float32)] * 2
+    truth_ij = [(10, 12), (30, 45), (50, 20)]
+    rows = []
+    nh = []
+    for (i, j) in truth_ij:
+        tx, ty = float(nodes[0][i]), float(nodes[1][j])
+        k = 0
+        for z in C.VELO_PLANES[1:]:
+            r = math.hypot(tx * z, ty * z)
+            if 5 < r < 40:
+                rows.append((np.float32(tx) * z, np.float32(ty) * z, z))
+                k += 1
+        nh.append(k)
+    rows.sort(key=lambda r: r[2])
+    h = h4(rows)
+    sig = 0.05
+    Rg = ora.grid(C.SLOPE2, [0, len(h)], h, nodes, sig)
+    idx, val, cnt = ora.peaks(Rg, 2, 2.5, 64)
+    found = sorted(int(v) for v in idx[0, :cnt[0]])
+    assert found == sorted(i * 61 + j for i, j in truth_ij)
+    for (i, j), n in zip(truth_ij, nh):
+        # each own hit contributes 1 up to the fp32 rounding of its coordinates (s ~ 1e-6 mm)
+        assert Rg[0, i, j] >= n * (1 - 1e-7)
+    # multi-start from seeds inside a basin converges monotonically toward theta_true
+    tt = np.array([[nodes[0][i], nodes[1][j]] for i, j in truth_ij], np.float64)
+    seeds = (tt + np.array([[2e-5, -1.5e-5]])).astype(np.float32)[None]
+    step = C.step_slope2(sig)
+    prev = first = np.abs(seeds[0].astype(float) - tt).max(axis=1)
+    for n_it in (1, 2, 5, 20, 100, 2000):
+        th, R, _ = ora.multistart(C.SLOPE2, [0, len(h)], h, seeds, sig, n_it, step, (-.3, -.3), (.3, .3))
+        dist = np.abs(th[0] - tt).max(axis=1)
+        assert np.all(dist <= prev + 1e-12)
+        prev = dist
+    assert np.all(prev < 0.01 * first)
+
+
+# ---------------------------------------------------------------- P10
+def _strict_max_scipy(g, thr):
+    P = g.ndim
+    fp = np.ones((3,) * P, bool)
+    fp[(1,) * P] = False
+    nb = ndimage.maximum_filter(g, footprint=fp, mode="constant", cval=-np.inf)
+    return np.flatnonzero((g > nb) & (g >= thr))
+
+
+@pytest.mark.parametrize("P", [2, 3])
+def test_P10_peak_rule(P):
+    rng = np.random.default_rng(P)
+    shape = (9, 13) if P == 2 else (7, 6, 9)
+    for trial in range(30):
+        g = rng.integers(0, 4, shape).astype(np.float64)  # many planted ties
+        thr = float(rng.choice([0.0, 1.0, 2.5]))
+        idx, val, cnt = ora.peaks(g[None], P, thr, 10_000)
+        exp = _strict_max_scipy(g, thr)
+        assert cnt[0] == len(exp) and np.array_equal(idx[0, :cnt[0]], exp)
+        assert np.array_equal(val[0, :cnt[0]], g.ravel()[exp])
+        # adding a constant to grid and R0 leaves the peaks unchanged
+        idx2, _, cnt2 = ora.peaks(g[None] + 8.0, P, thr + 8.0, 10_000)
+        assert cnt2[0] == cnt[0] and np.array_equal(idx2[0, :cnt[0]], idx[0, :cnt[0]])
+    # constant grid -> none; single peak -> argmax
+    assert ora.peaks(np.ones((1,) + shape), P, 0.0, 10)[2][0] == 0
+    g = np.zeros(shape)
+    c = tuple(s // 2 for s in shape)
+    g[c] = 3.0
+    idx, _, cnt = ora.peaks(g[None], P, 0.0, 10)
+    assert cnt[0] == 1 and idx[0, 0] == np.ravel_multi_index(c, shape)
+    # capacity: the true count is reported, only `cap` entries written
+    g = rng.random(shape)
+    idx, _, cnt = ora.peaks(g[None], P, 0.0, 2)
+    assert cnt[0] == len(_strict_max_scipy(g, 0.0)) and idx.shape[1] == 2
+
+
+# ---------------------------------------------------------------- P11 (Z7)
+def test_P11_multistart_identities():
+    cfg = C.CFG2
+    b = G.make_batch(cfg, [0, 1])
+    seeds = G.make_seeds(cfg, [0, 1], n_seeds=64)
+    th, R, g = ora.multistart(cfg.model, b.offsets, b.hits, seeds, cfg.sigma, 0, cfg.step,
+                              cfg.box_lo, cfg.box_hi)
+    assert np.array_equal(th, seeds.astype(np.float64))
+    for e in range(2):
+        for s in (0, 17, 63):
+            R1, g1, _ = ora.point(cfg.model, b.event_hits(e), seeds[e, s], cfg.sigma)
+            assert R[e, s] == R1 and np.array_equal(g[e, s], g1)
+    th0, _, _ = ora.multistart(cfg.model, b.offsets, b.hits, seeds, cfg.sigma, 7, 0.0, cfg.box_lo, cfg.box_hi)
+    assert np.array_equal(th0, seeds.astype(np.float64))
+    thb, _, _ = ora.multistart(cfg.model, b.offsets, b.hits, seeds, cfg.sigma, 10, cfg.step * 1e4,
+                               cfg.box_lo, cfg.box_hi)
+    assert np.all(thb >= np.float32(-0.3)) and np.all(thb <= np.float32(0.3))
+
+
+def test_P11_single_hit_trajectory_is_a_straight_contraction():
+    # one hit: grad R is parallel to (h/d - t) so ascent moves t straight toward h/d
+    x, y, d = 9.0, -3.0, 300.0
+    h = h4([(x, y, d)])
+    u = np.array([x, y]) / d
+    sig = 2.0
+    seeds = np.array([[[0.02, -0.015], [0.035, 0.0]]], np.float32)
+    th, R, _ = ora.multistart(C.SLOPE2, [0, 1], h, seeds, sig, 3, C.step_slope2(sig) * 30,
+                              (-.3, -.3), (.3, .3))
+    for s in range(2):
+        v0 = seeds[0, s].astype(float) - u
+        v1 = th[0, s] - u
+        assert abs(v0[0] * v1[1] - v0[1] * v1[0]) <= 1e-12 * np.linalg.norm(v0) ** 2
+        assert 0 < np.linalg.norm(v1) < np.linalg.norm(v0)
+        assert np.dot(v0, v1) > 0
+
+
+# ---------------------------------------------------------------- P12
+def _merge_cluster_all_then_select(theta, R, radius, thr):
+    """Alternative formulation of PAPER.md:154-155: greedy leader clustering of
+    ALL solutions in order (R desc, theta lex, index), then keep clusters whose
+    leader (= highest R member) is >= R0."""
+    n, P = theta.shape
+    order = sorted(range(n), key=lambda s: (-R[s],) + tuple(theta[s]) + (s,))
+    leaders, members = [], []
+    for s in order:
+        for li, l in enumerate(leaders):
+            if all(abs(theta[s, i] - theta[l, i]) <= radius[i] for i in range(P)):
+                members[li].append(s)
+                break
+        else:
+            leaders.append(s)
+            members.append([s])
+    return [(l, sum(1 for m in mem if R[m] >= thr)) for l, mem in zip(leaders, members) if R[l] >= thr]
+
+
+def test_P12_merge_examples_and_equivalence():
+    rad = (6e-4, 6e-4)
+    r32 = np.float32(6e-4).astype(float)
+    th = np.array([[[0.1, 0.1], [0.1, 0.1], [0.1, 0.1]]])
+    _, _, seed, size, cnt = ora.merge(th, np.array([[6.0, 6.0, 6.0]]), rad, 5.0, 8)
+    assert cnt[0] == 1 and size[0, 0] == 3 and seed[0, 0] == 0
+    th = np.array([[[0.1, 0.1], [0.1 + 10 * r32, 0.1]]])
+    _, _, _, _, cnt = ora.merge(th, np.array([[6.0, 7.0]]), rad, 5.0, 8)
+    assert cnt[0] == 2
+    _, _, _, _, cnt = ora.merge(th, np.array([[4.0, 4.9]]), rad, 5.0, 8)
+    assert cnt[0] == 0
+    # equal R: the theta-lexicographically smaller one leads
+    th = np.array([[[0.2, 0.1], [0.2, 0.0999], [0.1998, 0.3]]])
+    _, _, seed, _, cnt = ora.merge(th, np.array([[6.0, 6.0, 6.0]]), rad, 5.0, 8)
+    assert list(seed[0, :cnt[0]]) == [2, 1]
+    # random sets vs the cluster-all formulation, and permutation invariance
+    rng = np.random.default_rng(3)
+    for trial in range(20):
+        n = 300
+        centers = rng.uniform(-0.3, 0.3, (12, 2))
+        theta = centers[rng.integers(0, 12, n)] + rng.normal(0, 3e-4, (n, 2))
+        R = rng.uniform(0, 12, n).round(1)  # planted R ties
+        tt, tr, seed, size, cnt = ora.merge(theta[None], R[None], rad, 5.0, n)
+        rad64 = np.array(rad, np.float32).astype(float)
+        ref = _merge_cluster_all_then_select(theta, R, rad64, 5.0)
+        assert [(int(a), int(b)) for a, b in zip(seed[0, :cnt[0]], size[0, :cnt[0]])] == ref
+        perm = rng.permutation(n)
+        _, _, seed2, size2, cnt2 = ora.merge(theta[perm][None], R[perm][None], rad, 5.0, n)
+        assert cnt2[0] == cnt[0]
+        assert list(perm[seed2[0, :cnt2[0]]]) == list(seed[0, :cnt[0]])
+        assert np.array_equal(size2[0, :cnt2[0]], size[0, :cnt[0]])
+
+
+# ---------------------------------------------------------------- P13
+def test_P13_determinism_and_shard_invariance():
+    cfg = C.CFG3
+    full = G.make_batch(cfg, range(6))
+    part = G.make_batch(cfg, [4, 5])
+    assert np.array_equal(full.hits[full.offsets[4]:], part.hits)
+    s_full = G.make_seeds(cfg, range(6), n_seeds=32)
+    s_part = G.make_seeds(cfg, [4, 5], n_seeds=32)
+    assert np.array_equal(s_full[4:], s_part)
+    cfg2 = C.CFG2
+    b = G.make_batch(cfg2, range(3))
+    sd = G.make_seeds(cfg2, range(3), n_seeds=16)
+    a1 = ora.multistart(cfg2.model, b.offsets, b.hits, sd, cfg2.sigma, 3, cfg2.step, cfg2.box_lo, cfg2.box_hi)
+    a2 = ora.multistart(cfg2.model, b.offsets, b.hits, sd, cfg2.sigma, 3, cfg2.step, cfg2.box_lo, cfg2.box_hi)
+    for x, y in zip(a1, a2):
+        assert np.array_equal(x, y)
+
+
+def test_generator_shapes_and_sorting():
+    for name in ("cfg0", "cfg1", "cfg2", "cfg3", "cfg4"):
+        cfg = C.CONFIGS[name]
+        b = G.make_batch(cfg, range(min(cfg.n_events, 3)))
+        assert b.hits.dtype == np.float32 and b.hits.shape[1] == 4
+        for e in range(b.n_events):
+            h = b.event_hits(e)
+            key = h[:, 0] if cfg.model == C.LINE2D else h[:, 2]
+            assert np.all(np.diff(key) >= 0)
+        if cfg.n_seeds:
+            s = G.make_seeds(cfg, [0], n_seeds=100)
+            assert np.all(s >= np.float32(np.array(cfg.box_lo))) and np.all(s <= np.float32(np.array(cfg.box_hi)))
