@@ -1,0 +1,328 @@
+#!/usr/bin/env python
+"""Benchmark of the Artificial Retina hot path on B200 (one process per GPU).
+
+A step = one pass of the whole hot path over this rank's
+event batch: grid response + peak finding (grid AR) and multi-start
+fixed-step ascent + merging (Algorithm 1), then the one result gather.
+
+Workload (default): BASELINE.json configs[3] ("Run-3-like batch"), 10,000 events per
+rank with distinct event ids (weak scaling: per-GPU work fixed as N grows), 1024^2 grid,
+8192 seeds x 50 iterations.  Metric: unit.hit evaluations/s (whole job), plus events/s.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+    python -m torch.distributed.run --nproc-per-node N --master-addr 127.0.0.1 bench.py --gpus N
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+from synth import configs as C  # noqa: E402
+from synth import events as G  # noqa: E402
+
+METRIC = "retina unit·hit evaluations/s (events/s alongside)"
+UNIT = "pairs/s"
+MUFU_PER_SM_CLK = 16      # measured: tools/pipe_microbench (15.95 ex2/clk/SM)
+FMA_PER_SM_CLK = 128      # measured: 121.5 FFMA/clk/SM; FFMA2 does not double it
+N_SM = 148
+
+
+def peaks_json():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        return json.load(open(p))
+    return {"sm_max_mhz": 1965.0, "hbm_gbs": 6650.0, "fallback": True}
+
+
+def args_():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="cfg3")
+    ap.add_argument("--events-per-rank", type=int, default=None)
+    ap.add_argument("--chunk-events", type=int, default=256)
+    ap.add_argument("--e2e-steps", type=int, default=None)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-sample-events", type=int, default=3)
+    return ap.parse_args()
+
+
+def make_spec(cfg):
+    from paper_1709_08610_b200.pipeline import PathSpec
+    return PathSpec(model=cfg.model, sigma=cfg.sigma, nodes=G.axis_nodes(cfg) if cfg.axes else [],
+                    peak_threshold=cfg.peak_threshold, peak_capacity=cfg.peak_capacity, n_seeds=cfg.n_seeds,
+                    n_iters=cfg.n_iters, step=cfg.step, box_lo=cfg.box_lo, box_hi=cfg.box_hi,
+                    merge_radius=cfg.merge_radius, track_threshold=cfg.track_threshold,
+                    track_capacity=cfg.track_capacity, z_ref=cfg.z_ref)
+
+
+# ----------------------------------------------------------------------------- clocks
+class ClockSampler:
+    """Samples SM clock and throttle reasons via NVML every 100 ms while running."""
+    REASONS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
+               0x8: "hw_slowdown", 0x10: "sync_boost", 0x20: "sw_thermal_slowdown",
+               0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting"}
+
+    def __init__(self, index: int):
+        self.samples, self.reasons, self.max_mhz = [], set(), None
+        self._stop = threading.Event()
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception as e:  # pragma: no cover - reported in the JSON
+            self.nv, self.err = None, str(e)
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                mask = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for bit, name in self.REASONS.items():
+                    if mask & bit and bit != 0x1:
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            self._stop.wait(0.1)
+
+    def __enter__(self):
+        if self.nv:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self.nv:
+            self.t.join()
+
+    def summary(self):
+        if not self.nv:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvml unavailable"]}
+        return {"sm_mhz": statistics.median(self.samples) if self.samples else None,
+                "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+# ----------------------------------------------------------------------------- CPU oracle
+def oracle_sample(cfg, n_events: int):
+    """The fp64 oracle, as it stands, on a bounded sample of the same workload: the full
+    grid + peaks of `n_events` events and their full multi-start + merge."""
+    from oracle import oracle as ora
+    ev = list(range(n_events))
+    b = G.make_batch(cfg, ev)
+    seeds = G.make_seeds(cfg, ev)
+    nodes = G.axis_nodes(cfg) if cfg.axes else []
+    nh = float(b.n_hits)
+    t0 = time.perf_counter()
+    pairs = 0.0
+    if nodes:
+        g = ora.grid(cfg.model, b.offsets, b.hits, nodes, cfg.sigma)
+        ora.peaks(g, cfg.P, cfg.peak_threshold, cfg.peak_capacity)
+        pairs += nh * cfg.n_units
+    if cfg.n_seeds:
+        th, R, _ = ora.multistart(cfg.model, b.offsets, b.hits, seeds, cfg.sigma, cfg.n_iters, cfg.step,
+                                  cfg.box_lo, cfg.box_hi, want_grad=False)
+        ora.merge(th, R, cfg.merge_radius, cfg.track_threshold, cfg.track_capacity)
+        pairs += nh * cfg.n_seeds * (cfg.n_iters + 1)
+    dt = time.perf_counter() - t0
+    return {"value": pairs / dt, "unit": UNIT, "cores": ora.num_threads(), "kind": "oracle",
+            "events_per_s": n_events / dt, "seconds": dt,
+            "sample": f"{n_events} event(s) of {cfg.name}: full {'x'.join(str(a[2]) for a in cfg.axes)} grid + "
+                      f"peaks and {cfg.n_seeds} seeds x {cfg.n_iters + 1} passes + merge; {pairs:.3e} pairs"}
+
+
+def run_reference(a):
+    rank, world, _ = (int(os.environ.get(k, d)) for k, d in (("RANK", 0), ("WORLD_SIZE", 1), ("LOCAL_RANK", 0)))
+    if rank != 0:
+        return
+    cfg = C.get_config(a.config)
+    steps = []
+    for _ in range(a.warmup + a.steps):
+        steps.append(oracle_sample(cfg, a.cpu_sample_events))
+    timed = steps[a.warmup:]
+    value = statistics.median(s["value"] for s in timed)
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": a.gpus,
+            "steps": a.steps, "warmup": a.warmup, "ms_per_step": 1e3 * statistics.median(s["seconds"] for s in timed),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "config": {"workload": f"{cfg.name} (bounded sample, CPU oracle)",
+                                            "events_per_step": a.cpu_sample_events},
+            "events_per_s": statistics.median(s["events_per_s"] for s in timed),
+            "cpu_baseline": {k: timed[-1][k] for k in ("kind", "cores", "sample")} | {"value": value, "unit": UNIT},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ----------------------------------------------------------------------------- GPU arm
+def main():
+    a = args_()
+    if a.impl == "reference":
+        return run_reference(a)
+    import torch
+    import torch.distributed as dist
+
+    from paper_1709_08610_b200 import dist as D
+    from paper_1709_08610_b200 import retina as RT
+    from paper_1709_08610_b200.pipeline import PhaseTimer, RetinaPipeline, upload
+
+    rank, world, local = D.env()
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    RT.lib()  # fail loudly if the native library is missing
+    cfg = C.get_config(a.config)
+    E = a.events_per_rank or cfg.n_events
+    ev_ids = range(rank * E, (rank + 1) * E)  # weak scaling: distinct events per rank
+    t0 = time.perf_counter()
+    batch = G.make_batch(cfg, ev_ids)
+    seeds = G.make_seeds(cfg, ev_ids)
+    gen_s = time.perf_counter() - t0
+    spec = make_spec(cfg)
+    pipe = RetinaPipeline(spec, E, chunk_events=a.chunk_events)
+    stream = torch.cuda.current_stream()
+    dbatch = upload(batch.offsets, batch.hits, seeds)
+    pairs_grid, pairs_ms = pipe.pairs(dbatch)
+    keep = 64
+
+    def step(b, timer=None, t_ms=0.0):
+        pipe.run(b, stream=stream, timer=timer)
+        buf = D.pack(pipe.peak_idx[:E], pipe.peak_val[:E], pipe.peak_cnt[:E], pipe.t_theta[:E], pipe.t_resp[:E],
+                     pipe.t_size[:E], pipe.t_count[:E], keep,
+                     [rank, rank * E, E, 0, 0, t_ms, pairs_grid / 1e9, pairs_ms / 1e9])
+        return D.gather(buf, world)
+
+    for _ in range(a.warmup):
+        step(dbatch)
+    torch.cuda.synchronize()
+    timer = PhaseTimer(stream)
+    pipe.launches = 0
+    with ClockSampler(local) as clocks:
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        ev0.record(stream)
+        for _ in range(a.steps):
+            gathered = step(dbatch, timer)
+        ev1.record(stream)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+    ms = ev0.elapsed_time(ev1)
+    launches = pipe.launches
+    phase_ms = timer.totals_ms()
+    phase_n = timer.counts()
+    t = torch.tensor([ms], device="cuda")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_max = float(t.item())
+    ms_step = ms_max / a.steps
+
+    # ---- e2e through the public API with host buffers (pinned H2D + D2H inside the region)
+    e2e_steps = a.e2e_steps if a.e2e_steps is not None else max(1, min(a.steps, 3))
+    off_h = torch.from_numpy(batch.offsets).pin_memory()
+    hits_h = torch.from_numpy(batch.hits).pin_memory()
+    seeds_h = torch.from_numpy(seeds).pin_memory()
+    res_h = torch.empty(gathered.shape, dtype=torch.float32).pin_memory()
+    h2d = off_h.numel() * 4 + hits_h.numel() * 4 + seeds_h.numel() * 4
+    d2h = res_h.numel() * 4
+    dev_off = torch.empty_like(off_h, device="cuda")
+    dev_hits = torch.empty_like(hits_h, device="cuda")
+    dev_seeds = torch.empty_like(seeds_h, device="cuda")
+    b2 = dbatch.__class__(offsets=dev_off, hits=dev_hits, seeds=dev_seeds, max_event_hits=dbatch.max_event_hits,
+                          n_hits_per_event=dbatch.n_hits_per_event)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(e2e_steps):
+        dev_off.copy_(off_h, non_blocking=True)
+        dev_hits.copy_(hits_h, non_blocking=True)
+        dev_seeds.copy_(seeds_h, non_blocking=True)
+        g2 = step(b2)
+        res_h.copy_(g2, non_blocking=True)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    t2 = torch.tensor([e0.elapsed_time(e1)], device="cuda")
+    if world > 1:
+        dist.all_reduce(t2, op=dist.ReduceOp.MAX)
+    e2e_ms_step = float(t2.item()) / e2e_steps
+
+    if rank != 0:
+        if world > 1:
+            dist.barrier()
+            dist.destroy_process_group()
+        return
+
+    # ---- roofline of the dominant kernel (largest share of the step)
+    pk = peaks_json()
+    fmax = float(pk.get("sm_max_mhz", 1965.0)) * 1e6
+    work = {"grid": pairs_grid, "multistart": pairs_ms}
+    dom = max((k for k in phase_ms if k in work), key=lambda k: phase_ms[k])
+    n_launch = phase_n[dom] / a.steps
+    avg_ms = phase_ms[dom] / phase_n[dom]
+    per_launch = work[dom] / n_launch
+    achieved = per_launch / (avg_ms * 1e-3)
+    peak_pairs = N_SM * MUFU_PER_SM_CLK * fmax  # 1 MUFU.EX2 per pair
+    clk = clocks.summary()
+    roof = {"bound": "alu", "kernel": {"grid": "grid_response_kernel", "multistart": "multistart_kernel"}[dom],
+            "achieved": achieved / 1e9, "peak": peak_pairs / 1e9, "unit": "Gpair/s (1 MUFU.EX2 per pair)",
+            "frac": achieved / peak_pairs,
+            "peak_basis": f"{N_SM} SMs x {MUFU_PER_SM_CLK} MUFU.EX2/clk/SM (measured 15.95) x sm_max_mhz "
+                          f"{fmax / 1e6:.0f} (MEASURED_PEAKS.json)",
+            "frac_at_measured_clock": (achieved / (N_SM * MUFU_PER_SM_CLK * clk["sm_mhz"] * 1e6)
+                                       if clk.get("sm_mhz") else None),
+            "traffic": None, "launch_ms": avg_ms, "pairs_per_launch": per_launch,
+            "share_of_step": phase_ms[dom] / a.steps / ms_step}
+    prof = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(prof):
+        try:
+            roof["traffic"] = json.load(open(prof)).get(dom)
+        except Exception:
+            pass
+    total_pairs = (pairs_grid + pairs_ms) * world
+    line = {
+        "metric": METRIC, "value": total_pairs / (ms_step * 1e-3), "unit": UNIT, "n_gpus": world,
+        "steps": a.steps, "warmup": a.warmup, "ms_per_step": ms_step, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "events_per_s": E * world / (ms_step * 1e-3),
+        "config": {"workload": f"{cfg.name}: BASELINE.json configs[3] Run-3-like batch, {E} events per GPU "
+                               f"(ids rank*{E}..), 1024x1024 SLOPE2 grid + 3x3 peaks (R0={cfg.peak_threshold}), "
+                               f"{cfg.n_seeds} seeds x {cfg.n_iters} fixed-step iterations + merge",
+                   "events_per_rank": E, "hits_per_event_mean": float(batch.n_hits) / E,
+                   "pairs_grid_per_rank": pairs_grid, "pairs_multistart_per_rank": pairs_ms,
+                   "l2": "inputs > L2 (hits %.0f MB, seeds %.0f MB, grid writes %.1f GB per step)" % (
+                       batch.hits.nbytes / 1e6, seeds.nbytes / 1e6, 4.0 * cfg.n_units * E / 1e9),
+                   "parallelism": f"dp{world} (events sharded, 1 all_gather of results)"},
+        "phases_ms_per_step": {k: v / a.steps for k, v in phase_ms.items()},
+        "roofline": roof,
+        "clocks": clk,
+        "e2e": {"value": total_pairs / (e2e_ms_step * 1e-3), "unit": UNIT, "h2d_bytes_per_step": h2d,
+                "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms_step},
+        "gpu_launches": launches,
+        "gen_seconds": gen_s,
+    }
+    if world == 1 and not a.no_cpu_baseline:
+        line["cpu_baseline"] = oracle_sample(cfg, a.cpu_sample_events)
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,157 @@
+/* retina.h -- C ABI of the B200 (sm_100a) Artificial Retina hot path.
+ *
+ * arXiv 1709.08610, "Numerical optimization for Artificial Retina Algorithm".
+ * Four entry points, one per step of the method on the hot path:
+ *
+ *   retina_grid_response        Eq. (1)-(2), PAPER.md:36-39 (Sec. 2) and step (ii),
+ *                               R_ij = sum_k exp(-s(x_k, theta_ij)^2 / sigma^2)
+ *                               for every unit of a lattice, for every event of a batch.
+ *   retina_find_peaks           step (iii), "select clusters of activated
+ *                               units", read as strict local maxima (Z6).
+ *   retina_multistart_optimize  Algorithm 1: seeds theta^0 (drawn by the
+ *                               caller from the prior), a FIXED number
+ *                               of updates theta <- clamp(theta + step grad R) (PAPER.md:136,
+ *                               151; Z7); returns theta^n, R(theta^n), grad R(theta^n).
+ *   retina_merge_tracks         Algorithm 1: "cluster solutions; for each
+ *                               cluster select solution with highest response and above
+ *                               threshold R0" (Z9, Z10).
+ *
+ * Track models and the distance s:
+ *   RETINA_LINE2D  P=2, theta=(a, b),       hit (x, y, -, -):  s   = y - (a x + b)
+ *   RETINA_SLOPE2  P=2, theta=(tx, ty),     hit (x, y, z, -):  s^2 = (x - tx d)^2 + (y - ty d)^2, d = z - z_ref
+ *   RETINA_SLOPE3  P=3, theta=(tx, ty, z0), hit (x, y, z, -):  s^2 = (x - tx d)^2 + (y - ty d)^2, d = z - z0
+ *
+ * Conventions (all entry points):
+ *  - Bulk data are DEVICE pointers (CUDA global memory of the current device); small
+ *    descriptors (axis lengths, node-table pointer arrays, box, radius) are HOST pointers.
+ *  - Ownership: every buffer is caller-owned.  The library never allocates device
+ *    memory, never frees, and keeps no pointer after the call returns.
+ *  - Asynchrony: every call only enqueues kernels on `stream` (a cudaStream_t passed as
+ *    void*; NULL = legacy default stream) and never synchronizes.  Safe to call from
+ *    several host threads on different streams.
+ *  - Errors: host-checkable problems return RETINA_EINVAL synchronously and launch
+ *    nothing (NULL pointers, n_events < 0, sigma <= 0 or non-finite, unknown model or
+ *    model/P mismatch, axis_len < 2, capacity < 0, n_iters < 0, n_seeds < 0, box_lo >
+ *    box_hi, radius < 0).  Sizes the kernels do not support return RETINA_EUNSUPPORTED
+ *    (e.g. n_seeds > RETINA_MERGE_MAX_SEEDS in merge, or > 2^31 cells per event).  A
+ *    failed launch returns RETINA_ECUDA.  retina_last_error() gives a thread-local
+ *    message for the last non-OK return.
+ *  - Capacity overflow is NOT an error: *_count holds the TRUE count, and entries past
+ *    `capacity` are dropped; the caller sees it after synchronizing.
+ *  - Determinism: outputs are bit-identical for identical inputs (no float atomics, fixed
+ *    per-thread accumulation order, deterministic compaction and sort).
+ *  - Precision: fp32 storage and arithmetic, exp lowered to ex2.approx with the
+ *    log2(e)/sigma^2 scale applied after squaring; residuals formed with exact
+ *    products (FMA) and, where a difference of coordinates is inexact (z - z_ref,
+ *    z - z0, y - a x), as double-float pairs.
+ *  - There is no CPU fallback: without a CUDA device every call returns RETINA_ECUDA.
+ */
+#ifndef RETINA_H
+#define RETINA_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum { RETINA_OK = 0, RETINA_EINVAL = 1, RETINA_EUNSUPPORTED = 2, RETINA_ECUDA = 3 };
+enum { RETINA_LINE2D = 0, RETINA_SLOPE2 = 1, RETINA_SLOPE3 = 2 };
+
+#define RETINA_MERGE_MAX_SEEDS 16384
+
+/* A batch of events in CSR form ("a set of hits"; "An event
+ * consists of N_e coordinates (x, y, z) of triggered pixels").
+ *   offsets:  device int32 [n_events + 1], offsets[0] = 0, non-decreasing; event e owns
+ *             hits offsets[e] .. offsets[e+1]-1.
+ *   hits:     device float [4 * offsets[n_events]], (x, y, z, 0) per hit, 16-byte aligned.
+ *             Hits sorted by z within an event make SLOPE3 multi-start faster (it
+ *             re-forms z - z0 only when z changes); any order gives the same results
+ *             up to fp32 summation order being the array order.
+ *   z_ref:    SLOPE2 only: z of the pattern origin (0 in every BASELINE config).
+ *   max_event_hits: optional HOST-side upper bound on hits per event (0 = unknown).  It
+ *             only sizes the shared-memory hit buffer (events that fit stay resident
+ *             across multi-start iterations); results never depend on it. */
+typedef struct {
+    int32_t        n_events;
+    const int32_t *offsets;
+    const float   *hits;
+    float          z_ref;
+    int32_t        max_event_hits;
+} retina_events;
+
+/* Eq. (2): response of every unit of the lattice axis_nodes[0] x ... x axis_nodes[P-1].
+ *   model:      RETINA_LINE2D / SLOPE2 (P = 2) or RETINA_SLOPE3 (P = 3).
+ *   sigma:      bandwidth of Eq. (1), > 0, in the units of s.
+ *   axis_len:   host int32 [P], each >= 2.
+ *   axis_nodes: host array [P] of device fp32 [axis_len[i]] node tables (the caller owns
+ *               the node values; they are not recomputed, Z4).
+ *   response:   device fp32 [n_events][axis_len[0]]...[axis_len[P-1]], last axis fastest.
+ * Returns RETINA_OK, RETINA_EINVAL, RETINA_EUNSUPPORTED or RETINA_ECUDA. */
+int retina_grid_response(const retina_events *ev, int model, float sigma,
+                         const int32_t *axis_len, const float *const *axis_nodes,
+                         float *response, void *stream);
+
+/* Step (iii) on a response grid (any fp32 grid of that shape):
+ * cell c is reported iff response[c] >= threshold and response[c] > response[n] for every
+ * EXISTING neighbour n of its 3^P - 1 neighbourhood (cells on the lattice boundary have
+ * fewer neighbours; equal neighbours -- plateaus -- give no peak).
+ *   response:    device fp32 [n_events][cells]; P in {2, 3}; axis_len host int32 [P].
+ *   capacity:    entries per event of the output lists, >= 0.
+ *   peak_index:  device int32 [n_events][capacity], linear cell index, ascending.
+ *   peak_value:  device fp32  [n_events][capacity], response at that cell.
+ *   peak_count:  device int32 [n_events], TRUE number of peaks (may exceed capacity). */
+int retina_find_peaks(const float *response, int32_t n_events, int32_t P,
+                      const int32_t *axis_len, float threshold, int32_t capacity,
+                      int32_t *peak_index, float *peak_value, int32_t *peak_count,
+                      void *stream);
+
+/* Algorithm 1 update loop with update = fixed-step gradient ascent clamped to the prior
+ * box (Z7).  For every (event e, seed i):
+ *     theta^0 = seeds[e][i];  theta^{j+1} = clamp(theta^j + step * grad R(theta^j)),
+ *     j = 0 .. n_iters-1, clamp per axis to [box_lo, box_hi];
+ *   then theta_out = theta^n, response_out = R(theta^n), grad_out = grad R(theta^n).
+ * n_iters = 0 evaluates R and grad R at the seeds (BASELINE configs[0] "grad R at 256
+ * random theta").
+ *   seeds:        device fp32 [n_events][n_seeds][P].
+ *   box_lo/hi:    host fp32 [P].
+ *   theta_out:    device fp32 [n_events][n_seeds][P]; may alias seeds.
+ *   response_out: device fp32 [n_events][n_seeds].
+ *   grad_out:     device fp32 [n_events][n_seeds][P], or NULL (then the last pass
+ *                 evaluates R only). */
+int retina_multistart_optimize(const retina_events *ev, int model, float sigma,
+                               int32_t n_seeds, const float *seeds, int32_t n_iters,
+                               float step, const float *box_lo, const float *box_hi,
+                               float *theta_out, float *response_out, float *grad_out,
+                               void *stream);
+
+/* Algorithm 1 "cluster solutions ... select highest response above R0" per event:
+ *   keep seeds with response >= threshold; order them by (response descending, theta
+ *   lexicographic ascending, seed index ascending); scan that order: a seed joins the
+ *   EARLIEST-created leader L with |theta_i - L_i| <= radius[i] for every axis i
+ *   (differences formed exactly, in fp64), otherwise it founds a new leader.
+ *   theta, response: device fp32 [n_events][n_seeds][P] and [n_events][n_seeds].
+ *   radius:          host fp32 [P], >= 0.  n_seeds <= RETINA_MERGE_MAX_SEEDS.
+ *   track_theta:     device fp32 [n_events][capacity][P], leaders in creation order
+ *                    (= response descending).
+ *   track_response:  device fp32 [n_events][capacity].
+ *   track_seed:      device int32 [n_events][capacity], leader's seed index.
+ *   track_size:      device int32 [n_events][capacity], number of above-threshold members.
+ *   track_count:     device int32 [n_events], TRUE number of clusters. */
+int retina_merge_tracks(int32_t n_events, int32_t n_seeds, int32_t P, const float *theta,
+                        const float *response, const float *radius, float threshold,
+                        int32_t capacity, float *track_theta, float *track_response,
+                        int32_t *track_seed, int32_t *track_size, int32_t *track_count,
+                        void *stream);
+
+/* Static description of a status code. */
+const char *retina_status_string(int status);
+/* Thread-local detail for the last non-OK return of the calling thread ("" if none). */
+const char *retina_last_error(void);
+/* Library version string, e.g. "retina-b200 0.1 sm_100a". */
+const char *retina_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* RETINA_H */

@@ -1,0 +1,231 @@
+// abi.cu -- the extern "C" boundary declared in include/retina.h: host-side validation,
+// derived fp32 constants (rounded once from fp64), and launches on the caller's stream.
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+
+#include "../../include/retina.h"
+#include "common.cuh"
+#include "kernels.cuh"
+
+namespace {
+
+thread_local char g_last_error[512] = "";
+
+int fail(int status, const char *fmt, ...) {
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(g_last_error, sizeof(g_last_error), fmt, ap);
+    va_end(ap);
+    return status;
+}
+
+int cuda_fail(cudaError_t err, const char *where) {
+    return fail(RETINA_ECUDA, "%s: %s (%s)", where, cudaGetErrorString(err), cudaGetErrorName(err));
+}
+
+int model_P(int model) {
+    return model == RETINA_SLOPE3 ? 3 : (model == RETINA_LINE2D || model == RETINA_SLOPE2) ? 2 : -1;
+}
+
+bool finite_pos(float v) { return std::isfinite(v) && v > 0.f; }
+
+// -log2(e)/sigma^2 and 2/sigma^2 from the fp32 sigma, in fp64, rounded once.
+float neg_k(float sigma) {
+    const double s = sigma;
+    return (float)(-1.4426950408889634074 / (s * s));
+}
+float c2_of(float sigma) {
+    const double s = sigma;
+    return (float)(2.0 / (s * s));
+}
+
+int stage_cap(int32_t hint, int dflt) {
+    if (hint <= 0) return dflt;
+    int c = ((hint + 31) / 32) * 32;
+    if (c < 64) c = 64;
+    if (c > retina::kMaxStageHits) c = retina::kMaxStageHits;
+    return c;
+}
+
+int check_events(const retina_events *ev) {
+    if (!ev) return fail(RETINA_EINVAL, "ev is NULL");
+    if (ev->n_events < 0) return fail(RETINA_EINVAL, "n_events < 0 (%d)", ev->n_events);
+    if (ev->n_events > 0 && (!ev->offsets || !ev->hits))
+        return fail(RETINA_EINVAL, "offsets/hits is NULL");
+    if (((uintptr_t)ev->hits & 15u) != 0) return fail(RETINA_EINVAL, "hits must be 16-byte aligned");
+    if (!std::isfinite(ev->z_ref)) return fail(RETINA_EINVAL, "z_ref is not finite");
+    if (ev->max_event_hits < 0) return fail(RETINA_EINVAL, "max_event_hits < 0");
+    return RETINA_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char *retina_status_string(int status) {
+    switch (status) {
+        case RETINA_OK: return "RETINA_OK";
+        case RETINA_EINVAL: return "RETINA_EINVAL: invalid argument";
+        case RETINA_EUNSUPPORTED: return "RETINA_EUNSUPPORTED: size or option not supported";
+        case RETINA_ECUDA: return "RETINA_ECUDA: CUDA launch or device error";
+    }
+    return "unknown retina status";
+}
+
+const char *retina_last_error(void) { return g_last_error; }
+
+const char *retina_version(void) { return "retina-b200 0.1 sm_100a"; }
+
+int retina_grid_response(const retina_events *ev, int model, float sigma, const int32_t *axis_len,
+                         const float *const *axis_nodes, float *response, void *stream) {
+    g_last_error[0] = 0;
+    int st = check_events(ev);
+    if (st) return st;
+    const int P = model_P(model);
+    if (P < 0) return fail(RETINA_EINVAL, "unknown model %d", model);
+    if (!finite_pos(sigma)) return fail(RETINA_EINVAL, "sigma must be finite and > 0");
+    if (!axis_len || !axis_nodes) return fail(RETINA_EINVAL, "axis_len/axis_nodes is NULL");
+    long long cells = 1;
+    for (int i = 0; i < P; ++i) {
+        if (axis_len[i] < 2) return fail(RETINA_EINVAL, "axis_len[%d] = %d < 2", i, axis_len[i]);
+        if (!axis_nodes[i]) return fail(RETINA_EINVAL, "axis_nodes[%d] is NULL", i);
+        cells *= axis_len[i];
+    }
+    if (cells > 0x7fffffffLL) return fail(RETINA_EUNSUPPORTED, "more than 2^31-1 cells per event");
+    if (ev->n_events > 0 && !response) return fail(RETINA_EINVAL, "response is NULL");
+    retina::GridArgs a{};
+    a.offsets = ev->offsets;
+    a.hits = reinterpret_cast<const float4 *>(ev->hits);
+    a.z_ref = ev->z_ref;
+    a.negK = neg_k(sigma);
+    a.n0 = axis_len[0];
+    a.n1 = axis_len[1];
+    a.n2 = (P == 3) ? axis_len[2] : 1;
+    a.nodes0 = axis_nodes[0];
+    a.nodes1 = axis_nodes[1];
+    a.nodes2 = (P == 3) ? axis_nodes[2] : nullptr;
+    a.R = response;
+    a.cap = stage_cap(ev->max_event_hits, 2048);
+    const cudaError_t err = retina::launch_grid_response(model, a, ev->n_events, (cudaStream_t)stream);
+    if (err != cudaSuccess) return cuda_fail(err, "retina_grid_response");
+    return RETINA_OK;
+}
+
+int retina_find_peaks(const float *response, int32_t n_events, int32_t P, const int32_t *axis_len,
+                      float threshold, int32_t capacity, int32_t *peak_index, float *peak_value,
+                      int32_t *peak_count, void *stream) {
+    g_last_error[0] = 0;
+    if (n_events < 0) return fail(RETINA_EINVAL, "n_events < 0");
+    if (P != 2 && P != 3) return fail(RETINA_EINVAL, "P must be 2 or 3 (got %d)", P);
+    if (!axis_len) return fail(RETINA_EINVAL, "axis_len is NULL");
+    if (capacity < 0) return fail(RETINA_EINVAL, "capacity < 0");
+    if (std::isnan(threshold)) return fail(RETINA_EINVAL, "threshold is NaN");
+    long long cells = 1;
+    for (int i = 0; i < P; ++i) {
+        if (axis_len[i] < 2) return fail(RETINA_EINVAL, "axis_len[%d] = %d < 2", i, axis_len[i]);
+        cells *= axis_len[i];
+    }
+    if (cells > 0x7fffffffLL) return fail(RETINA_EUNSUPPORTED, "more than 2^31-1 cells per event");
+    if (n_events == 0) return RETINA_OK;
+    if (!response || !peak_count || (capacity > 0 && (!peak_index || !peak_value)))
+        return fail(RETINA_EINVAL, "NULL device pointer");
+    retina::PeakArgs a{};
+    a.R = response;
+    a.n0 = axis_len[0];
+    a.n1 = axis_len[1];
+    a.n2 = (P == 3) ? axis_len[2] : 1;
+    a.P = P;
+    a.threshold = threshold;
+    a.capacity = capacity;
+    a.idx = peak_index;
+    a.val = peak_value;
+    a.cnt = peak_count;
+    const cudaError_t err = retina::launch_find_peaks(a, n_events, (cudaStream_t)stream);
+    if (err != cudaSuccess) return cuda_fail(err, "retina_find_peaks");
+    return RETINA_OK;
+}
+
+int retina_multistart_optimize(const retina_events *ev, int model, float sigma, int32_t n_seeds,
+                               const float *seeds, int32_t n_iters, float step, const float *box_lo,
+                               const float *box_hi, float *theta_out, float *response_out,
+                               float *grad_out, void *stream) {
+    g_last_error[0] = 0;
+    int st = check_events(ev);
+    if (st) return st;
+    const int P = model_P(model);
+    if (P < 0) return fail(RETINA_EINVAL, "unknown model %d", model);
+    if (!finite_pos(sigma)) return fail(RETINA_EINVAL, "sigma must be finite and > 0");
+    if (n_seeds < 0) return fail(RETINA_EINVAL, "n_seeds < 0");
+    if (n_iters < 0) return fail(RETINA_EINVAL, "n_iters < 0");
+    if (!std::isfinite(step)) return fail(RETINA_EINVAL, "step is not finite");
+    if (!box_lo || !box_hi) return fail(RETINA_EINVAL, "box_lo/box_hi is NULL");
+    for (int i = 0; i < P; ++i)
+        if (!(box_lo[i] <= box_hi[i])) return fail(RETINA_EINVAL, "box_lo[%d] > box_hi[%d]", i, i);
+    if (ev->n_events == 0 || n_seeds == 0) return RETINA_OK;
+    if (!seeds || !theta_out || !response_out) return fail(RETINA_EINVAL, "NULL device pointer");
+    if ((long long)ev->n_events * n_seeds * P > 0x7fffffffffffLL)
+        return fail(RETINA_EUNSUPPORTED, "too many seeds");
+    retina::MultistartArgs a{};
+    a.offsets = ev->offsets;
+    a.hits = reinterpret_cast<const float4 *>(ev->hits);
+    a.z_ref = ev->z_ref;
+    a.negK = neg_k(sigma);
+    a.c2 = c2_of(sigma);
+    a.step = step;
+    for (int i = 0; i < 3; ++i) {
+        a.lo[i] = (i < P) ? box_lo[i] : 0.f;
+        a.hi[i] = (i < P) ? box_hi[i] : 0.f;
+    }
+    a.n_seeds = n_seeds;
+    a.n_iters = n_iters;
+    a.seeds = seeds;
+    a.theta_out = theta_out;
+    a.R_out = response_out;
+    a.grad_out = grad_out;
+    a.cap = stage_cap(ev->max_event_hits, 4096);
+    const cudaError_t err = retina::launch_multistart(model, a, ev->n_events, (cudaStream_t)stream);
+    if (err != cudaSuccess) return cuda_fail(err, "retina_multistart_optimize");
+    return RETINA_OK;
+}
+
+int retina_merge_tracks(int32_t n_events, int32_t n_seeds, int32_t P, const float *theta,
+                        const float *response, const float *radius, float threshold, int32_t capacity,
+                        float *track_theta, float *track_response, int32_t *track_seed,
+                        int32_t *track_size, int32_t *track_count, void *stream) {
+    g_last_error[0] = 0;
+    if (n_events < 0) return fail(RETINA_EINVAL, "n_events < 0");
+    if (n_seeds < 0) return fail(RETINA_EINVAL, "n_seeds < 0");
+    if (P != 2 && P != 3) return fail(RETINA_EINVAL, "P must be 2 or 3 (got %d)", P);
+    if (capacity < 0) return fail(RETINA_EINVAL, "capacity < 0");
+    if (!radius) return fail(RETINA_EINVAL, "radius is NULL");
+    for (int i = 0; i < P; ++i)
+        if (!(radius[i] >= 0.f) || !std::isfinite(radius[i]))
+            return fail(RETINA_EINVAL, "radius[%d] must be finite and >= 0", i);
+    if (std::isnan(threshold)) return fail(RETINA_EINVAL, "threshold is NaN");
+    if (n_seeds > RETINA_MERGE_MAX_SEEDS)
+        return fail(RETINA_EUNSUPPORTED, "n_seeds %d > %d", n_seeds, RETINA_MERGE_MAX_SEEDS);
+    if (n_events == 0) return RETINA_OK;
+    if (!track_count || (n_seeds > 0 && (!theta || !response)) ||
+        (capacity > 0 && (!track_theta || !track_response || !track_seed || !track_size)))
+        return fail(RETINA_EINVAL, "NULL device pointer");
+    retina::MergeArgs a{};
+    a.n_seeds = n_seeds;
+    a.P = P;
+    a.theta = theta;
+    a.R = response;
+    for (int i = 0; i < 3; ++i) a.radius[i] = (i < P) ? (double)radius[i] : 0.0;
+    a.threshold = threshold;
+    a.capacity = capacity;
+    a.t_theta = track_theta;
+    a.t_R = track_response;
+    a.t_seed = track_seed;
+    a.t_size = track_size;
+    a.t_count = track_count;
+    const cudaError_t err = retina::launch_merge(a, n_events, (cudaStream_t)stream);
+    if (err != cudaSuccess) return cuda_fail(err, "retina_merge_tracks");
+    return RETINA_OK;
+}
+
+}  // extern "C"

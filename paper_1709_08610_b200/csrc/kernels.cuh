@@ -1,0 +1,71 @@
+// kernels.cuh -- argument blocks and host launchers of the retina kernels (internal).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace retina {
+
+enum { kLine2D = 0, kSlope2 = 1, kSlope3 = 2 };
+
+struct GridArgs {
+    const int32_t *offsets;
+    const float4 *hits;
+    float z_ref;
+    float negK;  // -log2(e) / sigma^2, rounded once from fp64 on the host
+    int n0, n1, n2;
+    const float *nodes0, *nodes1, *nodes2;
+    float *R;
+    int cap;     // float4 slots of the shared-memory hit stage
+    int e_base;
+};
+
+struct MultistartArgs {
+    const int32_t *offsets;
+    const float4 *hits;
+    float z_ref;
+    float negK;   // -log2(e) / sigma^2
+    float c2;     // 2 / sigma^2 (gradient prefactor)
+    float step;
+    float lo[3], hi[3];
+    int n_seeds;
+    int n_iters;
+    const float *seeds;
+    float *theta_out, *R_out, *grad_out;
+    int cap;
+    int e_base;
+};
+
+struct PeakArgs {
+    const float *R;
+    int n0, n1, n2;  // n2 = 1 for P = 2
+    int P;
+    float threshold;
+    int capacity;
+    int32_t *idx;
+    float *val;
+    int32_t *cnt;
+    int e_base;
+};
+
+struct MergeArgs {
+    int n_seeds;
+    int P;
+    const float *theta;
+    const float *R;
+    double radius[3];
+    float threshold;
+    int capacity;
+    float *t_theta;
+    float *t_R;
+    int32_t *t_seed;
+    int32_t *t_size;
+    int32_t *t_count;
+    int e_base;
+};
+
+cudaError_t launch_grid_response(int model, const GridArgs &a, int n_events, cudaStream_t stream);
+cudaError_t launch_multistart(int model, const MultistartArgs &a, int n_events, cudaStream_t stream);
+cudaError_t launch_find_peaks(const PeakArgs &a, int n_events, cudaStream_t stream);
+cudaError_t launch_merge(const MergeArgs &a, int n_events, cudaStream_t stream);
+
+}  // namespace retina

@@ -1,0 +1,188 @@
+"""One GPU's pass of the whole hot path over an event batch.
+
+    S-A  grid AR (steps ii-iii):  retina_grid_response -> retina_find_peaks
+    S-B  Algorithm 1:            retina_multistart_optimize -> retina_merge_tracks
+
+All arithmetic runs in libretina.so; this module only owns device buffers, slices the
+CSR batch into chunks (the response grid of a chunk is produced, scanned for peaks and
+then overwritten by the next chunk, so a 10,000-event batch needs ~1 GB of grid buffer,
+not 42 GB), and counts the algorithmic work (unit.hit pairs) for the report.
+"""
+from __future__ import annotations
+
+import dataclasses
+from typing import List, Optional, Sequence
+
+import numpy as np
+import torch
+
+from . import retina as R
+
+
+@dataclasses.dataclass
+class PathSpec:
+    """Hot-path parameters (the ABI arguments; see include/retina.h)."""
+    model: int
+    sigma: float
+    nodes: Sequence[np.ndarray]          # fp32 node tables (grid path)
+    peak_threshold: float
+    peak_capacity: int
+    n_seeds: int
+    n_iters: int
+    step: float
+    box_lo: Sequence[float]
+    box_hi: Sequence[float]
+    merge_radius: Sequence[float]
+    track_threshold: float
+    track_capacity: int
+    z_ref: float = 0.0
+    sigma_ms: Optional[float] = None     # multi-start sigma (defaults to sigma)
+
+    @property
+    def P(self) -> int:
+        return R.MODEL_P[self.model]
+
+    @property
+    def cells(self) -> int:
+        return int(np.prod([len(n) for n in self.nodes])) if self.nodes else 0
+
+
+@dataclasses.dataclass
+class DeviceBatch:
+    offsets: torch.Tensor      # int32 [E+1] device
+    hits: torch.Tensor         # fp32 [N, 4] device
+    seeds: torch.Tensor        # fp32 [E, S, P] device
+    max_event_hits: int
+    n_hits_per_event: np.ndarray  # host int64 [E]
+
+    @property
+    def n_events(self) -> int:
+        return self.offsets.numel() - 1
+
+
+class RetinaPipeline:
+    def __init__(self, spec: PathSpec, max_events: int, chunk_events: int = 256, device="cuda",
+                 grid_bytes_budget: float = 2e9):
+        self.spec = spec
+        self.device = torch.device(device)
+        cells = spec.cells
+        if cells:
+            chunk_events = max(1, min(chunk_events, int(grid_bytes_budget // (4 * cells))))
+        self.chunk = min(chunk_events, max(1, max_events))
+        self.nodes = [torch.from_numpy(np.ascontiguousarray(n, np.float32)).to(self.device) for n in spec.nodes]
+        shape = tuple(len(n) for n in spec.nodes)
+        self.grid_buf = torch.empty((self.chunk,) + shape, dtype=torch.float32, device=self.device) if cells else None
+        E, P = max_events, spec.P
+        self.peak_idx = torch.empty((E, spec.peak_capacity), dtype=torch.int32, device=self.device)
+        self.peak_val = torch.empty((E, spec.peak_capacity), dtype=torch.float32, device=self.device)
+        self.peak_cnt = torch.empty((E,), dtype=torch.int32, device=self.device)
+        S = spec.n_seeds
+        self.theta = torch.empty((E, S, P), dtype=torch.float32, device=self.device)
+        self.resp = torch.empty((E, S), dtype=torch.float32, device=self.device)
+        self.t_theta = torch.empty((E, spec.track_capacity, P), dtype=torch.float32, device=self.device)
+        self.t_resp = torch.empty((E, spec.track_capacity), dtype=torch.float32, device=self.device)
+        self.t_seed = torch.empty((E, spec.track_capacity), dtype=torch.int32, device=self.device)
+        self.t_size = torch.empty((E, spec.track_capacity), dtype=torch.int32, device=self.device)
+        self.t_count = torch.empty((E,), dtype=torch.int32, device=self.device)
+        self.launches = 0
+
+    # ------------------------------------------------------------------ accounting
+    def pairs(self, batch: DeviceBatch):
+        """Algorithmic unit.hit pairs: grid = N_e x cells, multi-start = N_e x S x (n_iters+1)."""
+        n = batch.n_hits_per_event.astype(np.float64)
+        grid = float(n.sum()) * self.spec.cells
+        ms = float(n.sum()) * self.spec.n_seeds * (self.spec.n_iters + 1)
+        return grid, ms
+
+    def events_view(self, batch: DeviceBatch, e0: int, e1: int) -> R.Events:
+        return R.Events(batch.offsets[e0:e1 + 1], batch.hits, self.spec.z_ref, batch.max_event_hits)
+
+    # ------------------------------------------------------------------ the two paths
+    def run_grid(self, batch: DeviceBatch, stream=None, timer=None):
+        sp = self.spec
+        E = batch.n_events
+        for e0 in range(0, E, self.chunk):
+            e1 = min(E, e0 + self.chunk)
+            ev = self.events_view(batch, e0, e1)
+            out = self.grid_buf[: e1 - e0]
+            if timer is not None:
+                timer.start("grid")
+            R.retina_grid_response(ev, sp.model, sp.sigma, self.nodes, out=out, stream=stream)
+            if timer is not None:
+                timer.stop("grid")
+                timer.start("peaks")
+            R.retina_find_peaks(out, sp.P, sp.peak_threshold, sp.peak_capacity,
+                                out=(self.peak_idx[e0:e1], self.peak_val[e0:e1], self.peak_cnt[e0:e1]),
+                                stream=stream)
+            if timer is not None:
+                timer.stop("peaks")
+            self.launches += 2
+
+    def run_multistart(self, batch: DeviceBatch, stream=None, timer=None):
+        sp = self.spec
+        E = batch.n_events
+        ev = self.events_view(batch, 0, E)
+        if timer is not None:
+            timer.start("multistart")
+        R.retina_multistart_optimize(ev, sp.model, sp.sigma_ms or sp.sigma, batch.seeds, sp.n_iters, sp.step,
+                                     sp.box_lo, sp.box_hi, want_grad=False,
+                                     out=(self.theta[:E], self.resp[:E], None), stream=stream)
+        if timer is not None:
+            timer.stop("multistart")
+            timer.start("merge")
+        R.retina_merge_tracks(self.theta[:E], self.resp[:E], sp.merge_radius, sp.track_threshold,
+                              sp.track_capacity,
+                              out=(self.t_theta[:E], self.t_resp[:E], self.t_seed[:E], self.t_size[:E],
+                                   self.t_count[:E]), stream=stream)
+        if timer is not None:
+            timer.stop("merge")
+        self.launches += 2
+
+    def run(self, batch: DeviceBatch, stream=None, timer=None):
+        if self.spec.cells:
+            self.run_grid(batch, stream, timer)
+        if self.spec.n_seeds:
+            self.run_multistart(batch, stream, timer)
+
+
+class PhaseTimer:
+    """CUDA-event timer per phase on a given stream (sums over launches)."""
+
+    def __init__(self, stream):
+        self.stream = stream
+        self.pending = {}
+        self.events: dict = {}
+
+    def start(self, name):
+        ev = torch.cuda.Event(enable_timing=True)
+        ev.record(self.stream)
+        self.pending[name] = ev
+
+    def stop(self, name):
+        ev = torch.cuda.Event(enable_timing=True)
+        ev.record(self.stream)
+        self.events.setdefault(name, []).append((self.pending.pop(name), ev))
+
+    def totals_ms(self):
+        return {k: sum(a.elapsed_time(b) for a, b in v) for k, v in self.events.items()}
+
+    def counts(self):
+        return {k: len(v) for k, v in self.events.items()}
+
+    def reset(self):
+        self.events = {}
+        self.pending = {}
+
+
+def upload(offsets: np.ndarray, hits: np.ndarray, seeds: np.ndarray, device="cuda",
+           pinned: bool = False, stream=None) -> DeviceBatch:
+    """Host -> device copy of one batch (from pinned buffers when `pinned`)."""
+    def t(a, dtype):
+        x = torch.from_numpy(np.ascontiguousarray(a))
+        if pinned:
+            x = x.pin_memory()
+        return x.to(device, dtype, non_blocking=pinned)
+    counts = np.diff(np.asarray(offsets, np.int64))
+    return DeviceBatch(offsets=t(offsets.astype(np.int32), torch.int32), hits=t(hits, torch.float32),
+                       seeds=t(seeds, torch.float32),
+                       max_event_hits=int(counts.max()) if len(counts) else 0, n_hits_per_event=counts)

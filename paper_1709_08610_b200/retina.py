@@ -1,0 +1,194 @@
+"""Thin Python binding of libretina.so (include/retina.h), same names as the C ABI.
+
+Argument marshalling only: every step of the hot path runs in the CUDA kernels behind
+the C ABI.  torch is used for device memory and streams.  There is no CPU fallback: if
+the shared library is missing or no CUDA device is present, calls raise.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from typing import Optional, Sequence
+
+import torch
+
+from .build import LIB
+
+LINE2D, SLOPE2, SLOPE3 = 0, 1, 2
+MODEL_P = {LINE2D: 2, SLOPE2: 2, SLOPE3: 3}
+RETINA_OK, RETINA_EINVAL, RETINA_EUNSUPPORTED, RETINA_ECUDA = 0, 1, 2, 3
+MERGE_MAX_SEEDS = 16384
+
+EXPORTED = ("retina_grid_response", "retina_find_peaks", "retina_multistart_optimize",
+            "retina_merge_tracks", "retina_status_string", "retina_last_error", "retina_version")
+
+
+class RetinaError(RuntimeError):
+    def __init__(self, fn: str, status: int, detail: str):
+        super().__init__(f"{fn} -> {status}: {detail}")
+        self.status = status
+
+
+class retina_events(ctypes.Structure):
+    _fields_ = [("n_events", ctypes.c_int32), ("offsets", ctypes.c_void_p), ("hits", ctypes.c_void_p),
+                ("z_ref", ctypes.c_float), ("max_event_hits", ctypes.c_int32)]
+
+
+_lib = None
+
+
+def lib() -> ctypes.CDLL:
+    """Load libretina.so (built in-tree by __graft_entry__.build() / build.py)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB):
+            raise ImportError(f"{LIB} is missing: run `python -m paper_1709_08610_b200.build` "
+                              "(there is no CPU fallback)")
+        L = ctypes.CDLL(LIB)
+        vp, i32, f32 = ctypes.c_void_p, ctypes.c_int32, ctypes.c_float
+        L.retina_grid_response.argtypes = [ctypes.POINTER(retina_events), ctypes.c_int, f32, vp, vp, vp, vp]
+        L.retina_find_peaks.argtypes = [vp, i32, i32, vp, f32, i32, vp, vp, vp, vp]
+        L.retina_multistart_optimize.argtypes = [ctypes.POINTER(retina_events), ctypes.c_int, f32, i32, vp,
+                                                 i32, f32, vp, vp, vp, vp, vp, vp]
+        L.retina_merge_tracks.argtypes = [i32, i32, i32, vp, vp, vp, f32, i32, vp, vp, vp, vp, vp, vp]
+        for f in (L.retina_grid_response, L.retina_find_peaks, L.retina_multistart_optimize,
+                  L.retina_merge_tracks):
+            f.restype = ctypes.c_int
+        L.retina_status_string.argtypes = [ctypes.c_int]
+        L.retina_status_string.restype = ctypes.c_char_p
+        L.retina_last_error.restype = ctypes.c_char_p
+        L.retina_version.restype = ctypes.c_char_p
+        _lib = L
+    return _lib
+
+
+def version() -> str:
+    return lib().retina_version().decode()
+
+
+def _check(fn: str, status: int):
+    if status != RETINA_OK:
+        raise RetinaError(fn, status, lib().retina_last_error().decode())
+
+
+def _ptr(t: Optional[torch.Tensor]):
+    return None if t is None else ctypes.c_void_p(t.data_ptr())
+
+
+def _arr(ctype, vals):
+    a = (ctype * max(len(vals), 1))(*vals)
+    return ctypes.cast(a, ctypes.c_void_p), a  # keep `a` alive while the call runs
+
+
+def _stream(stream) -> ctypes.c_void_p:
+    if stream is None:
+        stream = torch.cuda.current_stream()
+    return ctypes.c_void_p(stream.cuda_stream)
+
+
+def _dev(t: torch.Tensor, dtype) -> torch.Tensor:
+    if not t.is_cuda:
+        raise ValueError("device tensor expected (the library takes device pointers)")
+    if t.dtype != dtype or not t.is_contiguous():
+        raise ValueError(f"contiguous {dtype} tensor expected")
+    return t
+
+
+class Events:
+    """A device-resident CSR batch: offsets int32 [E+1], hits float32 [N, 4]."""
+
+    def __init__(self, offsets: torch.Tensor, hits: torch.Tensor, z_ref: float = 0.0,
+                 max_event_hits: int = 0):
+        self.offsets = _dev(offsets, torch.int32)
+        self.hits = _dev(hits, torch.float32)
+        assert hits.dim() == 2 and hits.shape[1] == 4
+        self.n_events = offsets.numel() - 1
+        self.c = retina_events(self.n_events, offsets.data_ptr(), hits.data_ptr(), float(z_ref),
+                               int(max_event_hits))
+
+    @staticmethod
+    def from_numpy(offsets, hits, z_ref: float = 0.0, device="cuda", max_event_hits: Optional[int] = None):
+        import numpy as np
+        off = torch.from_numpy(np.ascontiguousarray(offsets, dtype=np.int32)).to(device)
+        h = torch.from_numpy(np.ascontiguousarray(hits, dtype=np.float32)).to(device)
+        if max_event_hits is None:
+            o = np.asarray(offsets)
+            max_event_hits = int(np.max(np.diff(o))) if len(o) > 1 else 0
+        return Events(off, h, z_ref, max_event_hits)
+
+
+def retina_grid_response(events: Events, model: int, sigma: float, nodes: Sequence[torch.Tensor],
+                         out: Optional[torch.Tensor] = None, stream=None) -> torch.Tensor:
+    P = MODEL_P[model]
+    nodes = [_dev(n, torch.float32) for n in nodes]
+    alen, _k1 = _arr(ctypes.c_int32, [n.numel() for n in nodes])
+    nptr, _k2 = _arr(ctypes.c_void_p, [n.data_ptr() for n in nodes])
+    if out is None:
+        out = torch.empty((events.n_events,) + tuple(n.numel() for n in nodes), device=events.hits.device,
+                          dtype=torch.float32)
+    _check("retina_grid_response",
+           lib().retina_grid_response(ctypes.byref(events.c), model, float(sigma), alen, nptr,
+                                      _ptr(_dev(out, torch.float32)), _stream(stream)))
+    return out
+
+
+def retina_find_peaks(response: torch.Tensor, P: int, threshold: float, capacity: int,
+                      out=None, stream=None):
+    """Returns (peak_index int32 [E, cap], peak_value fp32 [E, cap], peak_count int32 [E])."""
+    _dev(response, torch.float32)
+    E = response.shape[0]
+    shape = tuple(response.shape[1:])
+    assert len(shape) == P
+    alen, _k = _arr(ctypes.c_int32, list(shape))
+    if out is None:
+        dev = response.device
+        out = (torch.empty((E, capacity), dtype=torch.int32, device=dev),
+               torch.empty((E, capacity), dtype=torch.float32, device=dev),
+               torch.empty((E,), dtype=torch.int32, device=dev))
+    idx, val, cnt = out
+    _check("retina_find_peaks",
+           lib().retina_find_peaks(_ptr(response), E, P, alen, float(threshold), int(capacity),
+                                   _ptr(idx), _ptr(val), _ptr(cnt), _stream(stream)))
+    return idx, val, cnt
+
+
+def retina_multistart_optimize(events: Events, model: int, sigma: float, seeds: torch.Tensor,
+                               n_iters: int, step: float, box_lo, box_hi, want_grad: bool = True,
+                               out=None, stream=None):
+    """Returns (theta_out [E,S,P], response_out [E,S], grad_out [E,S,P] or None)."""
+    P = MODEL_P[model]
+    _dev(seeds, torch.float32)
+    E, S, Ps = seeds.shape
+    assert Ps == P and E == events.n_events
+    lo, _k1 = _arr(ctypes.c_float, [float(v) for v in box_lo])
+    hi, _k2 = _arr(ctypes.c_float, [float(v) for v in box_hi])
+    if out is None:
+        out = (torch.empty_like(seeds), torch.empty((E, S), dtype=torch.float32, device=seeds.device),
+               torch.empty_like(seeds) if want_grad else None)
+    th, R, g = out
+    _check("retina_multistart_optimize",
+           lib().retina_multistart_optimize(ctypes.byref(events.c), model, float(sigma), S, _ptr(seeds),
+                                            int(n_iters), float(step), lo, hi, _ptr(th), _ptr(R), _ptr(g),
+                                            _stream(stream)))
+    return th, R, g
+
+
+def retina_merge_tracks(theta: torch.Tensor, response: torch.Tensor, radius, threshold: float,
+                        capacity: int, out=None, stream=None):
+    """Returns (track_theta [E,cap,P], track_response [E,cap], track_seed, track_size, track_count)."""
+    _dev(theta, torch.float32)
+    _dev(response, torch.float32)
+    E, S, P = theta.shape
+    rad, _k = _arr(ctypes.c_float, [float(v) for v in radius])
+    if out is None:
+        dev = theta.device
+        out = (torch.empty((E, capacity, P), dtype=torch.float32, device=dev),
+               torch.empty((E, capacity), dtype=torch.float32, device=dev),
+               torch.empty((E, capacity), dtype=torch.int32, device=dev),
+               torch.empty((E, capacity), dtype=torch.int32, device=dev),
+               torch.empty((E,), dtype=torch.int32, device=dev))
+    tt, tr, ts, tz, tc = out
+    _check("retina_merge_tracks",
+           lib().retina_merge_tracks(E, S, P, _ptr(theta), _ptr(response), rad, float(threshold), int(capacity),
+                                     _ptr(tt), _ptr(tr), _ptr(ts), _ptr(tz), _ptr(tc), _stream(stream)))
+    return tt, tr, ts, tz, tc

@@ -1,0 +1,116 @@
+"""The C ABI library loads, exports every symbol include/retina.h declares, and rejects
+host-checkable argument errors synchronously (no GPU needed: nothing is launched)."""
+import ctypes
+import os
+import re
+import subprocess
+
+import pytest
+
+from paper_1709_08610_b200 import build as B
+from paper_1709_08610_b200 import retina as rt
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HEADER = os.path.join(ROOT, "include", "retina.h")
+
+
+@pytest.fixture(scope="module")
+def L():
+    B.build()
+    return rt.lib()
+
+
+def declared_functions():
+    src = open(HEADER).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(retina_[a-z_]+)\s*\(", src)))
+
+
+def test_exports_every_declared_symbol(L):
+    names = declared_functions()
+    assert set(names) == set(rt.EXPORTED)
+    out = subprocess.run(["nm", "-D", "--defined-only", B.LIB], capture_output=True, text=True).stdout
+    exported = set(re.findall(r" T (\w+)", out))
+    for n in names:
+        assert n in exported, n
+        assert hasattr(L, n)
+
+
+def test_status_strings_and_version(L):
+    assert L.retina_status_string(0).decode() == "RETINA_OK"
+    for s in (1, 2, 3):
+        assert L.retina_status_string(s).decode().startswith("RETINA_E")
+    assert "sm_100a" in L.retina_version().decode()
+
+
+def _ev(n=1, offsets=1, hits=16):
+    return rt.retina_events(n, offsets, hits, 0.0, 0)
+
+
+def _f(*v):
+    return ctypes.cast((ctypes.c_float * len(v))(*v), ctypes.c_void_p)
+
+
+def _i(*v):
+    return ctypes.cast((ctypes.c_int32 * len(v))(*v), ctypes.c_void_p)
+
+
+def test_grid_response_validation(L):
+    alen = _i(4, 4)
+    nodes = ctypes.cast((ctypes.c_void_p * 2)(16, 16), ctypes.c_void_p)
+    g = L.retina_grid_response
+    assert g(None, 1, 0.5, alen, nodes, 16, None) == rt.RETINA_EINVAL
+    ev = _ev()
+    assert g(ctypes.byref(ev), 1, 0.0, alen, nodes, 16, None) == rt.RETINA_EINVAL
+    assert b"sigma" in L.retina_last_error()
+    assert g(ctypes.byref(ev), 1, float("nan"), alen, nodes, 16, None) == rt.RETINA_EINVAL
+    assert g(ctypes.byref(ev), 7, 0.5, alen, nodes, 16, None) == rt.RETINA_EINVAL
+    assert g(ctypes.byref(ev), 1, 0.5, _i(1, 4), nodes, 16, None) == rt.RETINA_EINVAL
+    assert g(ctypes.byref(ev), 1, 0.5, alen, nodes, None, None) == rt.RETINA_EINVAL
+    bad = _ev(hits=8)  # misaligned hits
+    assert g(ctypes.byref(bad), 1, 0.5, alen, nodes, 16, None) == rt.RETINA_EINVAL
+    neg = _ev(n=-1)
+    assert g(ctypes.byref(neg), 1, 0.5, alen, nodes, 16, None) == rt.RETINA_EINVAL
+    big = _i(65536, 65536)
+    assert g(ctypes.byref(ev), 1, 0.5, big, nodes, 16, None) == rt.RETINA_EUNSUPPORTED
+
+
+def test_peaks_validation(L):
+    p = L.retina_find_peaks
+    assert p(16, 1, 4, _i(4, 4), 0.0, 4, 16, 16, 16, None) == rt.RETINA_EINVAL   # P = 4
+    assert p(16, 1, 2, _i(4, 4), 0.0, -1, 16, 16, 16, None) == rt.RETINA_EINVAL  # capacity < 0
+    assert p(16, -1, 2, _i(4, 4), 0.0, 4, 16, 16, 16, None) == rt.RETINA_EINVAL
+    assert p(16, 1, 2, _i(1, 4), 0.0, 4, 16, 16, 16, None) == rt.RETINA_EINVAL
+    assert p(16, 0, 2, _i(4, 4), 0.0, 4, 16, 16, 16, None) == rt.RETINA_OK       # nothing to do
+    assert p(16, 1, 2, _i(4, 4), float("nan"), 4, 16, 16, 16, None) == rt.RETINA_EINVAL
+
+
+def test_multistart_validation(L):
+    m = L.retina_multistart_optimize
+    ev = _ev()
+    lo, hi = _f(-1, -1), _f(1, 1)
+    assert m(ctypes.byref(ev), 1, 0.5, 8, 16, -1, 0.1, lo, hi, 16, 16, None, None) == rt.RETINA_EINVAL
+    assert m(ctypes.byref(ev), 1, 0.5, -8, 16, 1, 0.1, lo, hi, 16, 16, None, None) == rt.RETINA_EINVAL
+    assert m(ctypes.byref(ev), 1, 0.5, 8, 16, 1, 0.1, hi, lo, 16, 16, None, None) == rt.RETINA_EINVAL
+    assert m(ctypes.byref(ev), 1, 0.5, 8, 16, 1, float("inf"), lo, hi, 16, 16, None, None) == rt.RETINA_EINVAL
+    assert m(ctypes.byref(ev), 1, 0.5, 8, None, 1, 0.1, lo, hi, 16, 16, None, None) == rt.RETINA_EINVAL
+    assert m(ctypes.byref(ev), 1, 0.5, 0, None, 1, 0.1, lo, hi, None, None, None, None) == rt.RETINA_OK
+
+
+def test_merge_validation(L):
+    mg = L.retina_merge_tracks
+    rad = _f(1e-3, 1e-3)
+    args = (16, 16, rad, 5.0, 4, 16, 16, 16, 16, 16, None)
+    assert mg(1, 16, 4, *args) == rt.RETINA_EINVAL
+    assert mg(1, 16385, 2, *args) == rt.RETINA_EUNSUPPORTED
+    assert mg(1, 16, 2, 16, 16, _f(-1.0, 1.0), 5.0, 4, 16, 16, 16, 16, 16, None) == rt.RETINA_EINVAL
+    assert mg(0, 16, 2, *args) == rt.RETINA_OK
+
+
+def test_product_package_never_touches_oracle():
+    pkg = os.path.join(ROOT, "paper_1709_08610_b200")
+    for dirpath, _, files in os.walk(pkg):
+        for f in files:
+            if f.endswith((".py", ".cu", ".cuh", ".h")):
+                src = open(os.path.join(dirpath, f)).read()
+                assert "oracle" not in re.sub(r"#.*|//.*", "", src).replace("oracle/", ""), f

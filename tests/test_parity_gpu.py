@@ -1,0 +1,330 @@
+"""GPU parity: the CUDA path (through the C ABI) vs the fp64 oracle on the same seeded
+inputs (comparators T1..T7 of DESIGN.md §5).  Needs a B200."""
+import numpy as np
+import pytest
+import torch
+
+from oracle import oracle as ora
+from synth import configs as C
+from synth import events as G
+from tests import parity_util as PU
+
+import paper_1709_08610_b200 as R
+
+pytestmark = pytest.mark.gpu
+DEV = "cuda"
+
+
+def dev(a, dtype=torch.float32):
+    return torch.from_numpy(np.ascontiguousarray(a)).to(DEV, dtype)
+
+
+def events_of(batch, z_ref=0.0, hint=True):
+    return R.Events.from_numpy(batch.offsets, batch.hits, z_ref=z_ref,
+                               max_event_hits=None if hint else 0)
+
+
+def gpu_grid(batch, cfg, nodes, z_ref=0.0, hint=True, sigma=None):
+    ev = events_of(batch, z_ref, hint)
+    out = R.retina_grid_response(ev, cfg.model, cfg.sigma if sigma is None else sigma,
+                                 [dev(n) for n in nodes])
+    torch.cuda.synchronize()
+    return out.cpu().numpy()
+
+
+def synthetic_batch(model, counts, seed=0):
+    """Events with given hit counts, VELO-like coordinates (or toy for LINE2D)."""
+    rng = np.random.default_rng(seed)
+    hs = []
+    for n in counts:
+        h = np.zeros((n, 4), np.float32)
+        if model == C.LINE2D:
+            h[:, 0] = rng.integers(1, 11, n)
+            h[:, 1] = rng.uniform(-2, 2, n)
+            h = h[np.argsort(h[:, 0], kind="stable")]
+        else:
+            z = rng.choice(C.VELO_PLANES, n)
+            t = rng.uniform(-0.3, 0.3, (n, 2))
+            h[:, 0] = t[:, 0] * z + rng.normal(0, 0.5, n)
+            h[:, 1] = t[:, 1] * z + rng.normal(0, 0.5, n)
+            h[:, 2] = z
+            h = h[np.argsort(h[:, 2], kind="stable")]
+        hs.append(h)
+    off = np.zeros(len(counts) + 1, np.int32)
+    off[1:] = np.cumsum(counts)
+    hits = np.concatenate(hs) if hs else np.zeros((0, 4), np.float32)
+    return G.EventBatch(offsets=off, hits=hits, event_ids=np.arange(len(counts)), truth=[None] * len(counts),
+                        n_track_hits=np.zeros(len(counts)))
+
+
+# --------------------------------------------------------------------------- T1
+@pytest.mark.parametrize("name", ["cfg0", "cfg1"])
+def test_T1_grid_full_single_event(name):
+    cfg = C.CONFIGS[name]
+    b = G.make_batch(cfg, [0])
+    nodes = G.axis_nodes(cfg)
+    g = gpu_grid(b, cfg, nodes)
+    ref = ora.grid(cfg.model, b.offsets, b.hits, nodes, cfg.sigma)
+    ok, worst = PU.t1_response(g, ref)
+    assert ok, worst
+
+
+@pytest.mark.parametrize("model,z_ref,shape", [
+    (C.SLOPE2, 0.0, (37, 70)), (C.SLOPE2, -12.345, (41, 33)), (C.LINE2D, 0.0, (29, 90)),
+    (C.SLOPE3, 0.0, (5, 37, 45)), (C.SLOPE3, 0.0, (3, 70, 33))])
+@pytest.mark.parametrize("hint", [True, False])
+def test_T1_grid_ragged_edges(model, z_ref, shape, hint):
+    # events: typical, empty, single hit, and one larger than the default hit stage (streaming)
+    b = synthetic_batch(model, [700, 0, 1, 5000, 37], seed=len(shape) + model)
+    P = len(shape)
+    lo = [-0.3, -0.3, -150.0] if model != C.LINE2D else [-0.5, -1.0]
+    hi = [0.3, 0.3, 150.0] if model != C.LINE2D else [0.5, 1.0]
+    nodes = [np.linspace(lo[i], hi[i], shape[i]).astype(np.float32) for i in range(P)]
+    sigma = 0.05 if model == C.LINE2D else 0.44
+    cfg = C.Config(name="t", model=model, n_events=5, seed=0, n_tracks=0, sigma=sigma)
+    g = gpu_grid(b, cfg, nodes, z_ref=z_ref, hint=hint)
+    ref = ora.grid(model, b.offsets, b.hits, nodes, sigma, z_ref=z_ref)
+    assert np.all(g[1] == 0.0)
+    ok, worst = PU.t1_response(g, ref)
+    assert ok, worst
+
+
+@pytest.mark.parametrize("name,events,sub", [("cfg3", [0, 9999], 48), ("cfg4", [0], 12)])
+def test_T1_grid_full_size_sampled(name, events, sub):
+    """BASELINE full sizes (1024^2, 256^3) in the bench launch configuration; the oracle
+    recomputes a sampled sub-lattice (random node subsets per axis)."""
+    cfg = C.CONFIGS[name]
+    b = G.make_batch(cfg, events)
+    nodes = G.axis_nodes(cfg)
+    g = gpu_grid(b, cfg, nodes)
+    rng = np.random.default_rng(7)
+    pick = [np.sort(rng.choice(len(n), sub, replace=False)) for n in nodes]
+    pick = [np.unique(np.concatenate([p, [0, len(n) - 1]])) for p, n in zip(pick, nodes)]
+    ref = ora.grid(cfg.model, b.offsets, b.hits, [n[p] for n, p in zip(nodes, pick)], cfg.sigma)
+    sub_gpu = g[(slice(None),) + np.ix_(*pick)]
+    ok, worst = PU.t1_response(sub_gpu, ref)
+    assert ok, worst
+
+
+# --------------------------------------------------------------------------- T2
+@pytest.mark.parametrize("name,z_ref", [("cfg0", 0.0), ("cfg2", 0.0), ("cfg2", 23.5), ("cfg4", 0.0)])
+def test_T2_gradient_at_points(name, z_ref):
+    cfg = C.CONFIGS[name]
+    ev_ids = [0] if cfg.n_events == 1 else [0, 1, 2]
+    b = G.make_batch(cfg, ev_ids)
+    n = 256
+    seeds = G.make_seeds(cfg, ev_ids, n_seeds=n)
+    # half the points next to true tracks (where gradients cancel), half random
+    for e in range(len(ev_ids)):
+        t = b.truth[e]
+        k = min(n // 2, len(t))
+        rng = np.random.default_rng(e)
+        near = t[rng.integers(0, len(t), k)] + rng.normal(0, [1e-4, 1e-4, 0.05][:cfg.P], (k, cfg.P))
+        seeds[e, :k] = near.astype(np.float32)
+    ev = events_of(b, z_ref)
+    th, Rg, gg = R.retina_multistart_optimize(ev, cfg.model, cfg.sigma, dev(seeds), 0, 0.0,
+                                              cfg.box_lo, cfg.box_hi)
+    torch.cuda.synchronize()
+    th, Rg, gg = th.cpu().numpy(), Rg.cpu().numpy(), gg.cpu().numpy()
+    assert np.array_equal(th, seeds)
+    worst1 = worst2 = 0.0
+    for e in range(len(ev_ids)):
+        h = b.event_hits(e)
+        for s in range(n):
+            r, g, A = ora.point(cfg.model, h, seeds[e, s].astype(np.float64), cfg.sigma, z_ref=z_ref)
+            ok1, w1 = PU.t1_response(Rg[e, s], r)
+            Gs = PU.grad_floor_scale(cfg.model, h, cfg.sigma, seeds[e, s].astype(np.float64))
+            ok2, w2 = PU.t2_gradient(gg[e, s], g, A, Gs)
+            worst1, worst2 = max(worst1, w1), max(worst2, w2)
+    assert worst1 <= 1.0 and worst2 <= 1.0, (worst1, worst2)
+
+
+# --------------------------------------------------------------------------- T3 / T4
+@pytest.mark.parametrize("name", ["cfg0", "cfg1"])
+@pytest.mark.parametrize("thr", [0.0, 2.5])
+def test_T3_T4_peaks(name, thr):
+    cfg = C.CONFIGS[name]
+    b = G.make_batch(cfg, [0])
+    nodes = G.axis_nodes(cfg)
+    ev = events_of(b)
+    grid = R.retina_grid_response(ev, cfg.model, cfg.sigma, [dev(n) for n in nodes])
+    cap = 4096
+    idx, val, cnt = R.retina_find_peaks(grid, cfg.P, thr, cap)
+    torch.cuda.synchronize()
+    g32 = grid.cpu().numpy()
+    idx, val, cnt = idx.cpu().numpy(), val.cpu().numpy(), cnt.cpu().numpy()
+    # T3: bit-exact on the same fp32 grid
+    ri, rv, rc = ora.peaks(g32.astype(np.float64), cfg.P, thr, cap)
+    assert cnt[0] == rc[0]
+    k = min(cnt[0], cap)
+    assert np.array_equal(idx[0, :k], ri[0, :k]) and np.array_equal(val[0, :k].astype(np.float64), rv[0, :k])
+    # T4: vs the fp64 oracle grid, near-ties excused
+    ref = ora.grid(cfg.model, b.offsets, b.hits, nodes, cfg.sigma)[0]
+    ok, ndiff, nexc = PU.t4_peak_sets(idx[0], cnt[0], ref, cfg.P, thr, cap)
+    assert ok, (ndiff, nexc)
+
+
+@pytest.mark.parametrize("P,shape", [(2, (1, 37, 61)), (2, (3, 1024, 1024)), (3, (2, 19, 23, 29)),
+                                     (3, (1, 64, 64, 64))])
+def test_T3_peaks_bitexact_planted_ties(P, shape):
+    rng = np.random.default_rng(P)
+    g = rng.integers(0, 5, shape).astype(np.float32)  # many plateaus and ties
+    g[0].flat[::97] = 7.0
+    for thr, cap in ((0.0, 1 << 20), (3.0, 1 << 20), (0.0, 5)):
+        idx, val, cnt = R.retina_find_peaks(dev(g), P, thr, cap)
+        torch.cuda.synchronize()
+        ri, rv, rc = ora.peaks(g.astype(np.float64), P, thr, cap)
+        cnt = cnt.cpu().numpy()
+        assert np.array_equal(cnt, rc)
+        idx, val = idx.cpu().numpy(), val.cpu().numpy()
+        for e in range(shape[0]):
+            k = min(cnt[e], cap)
+            assert np.array_equal(idx[e, :k], ri[e, :k])
+            assert np.array_equal(val[e, :k].astype(np.float64), rv[e, :k])
+
+
+def test_T3_peaks_cfg4_slope3_sampled():
+    cfg = C.CFG4
+    b = G.make_batch(cfg, [1])
+    nodes = G.axis_nodes(cfg)
+    grid = R.retina_grid_response(events_of(b), cfg.model, cfg.sigma, [dev(n) for n in nodes])
+    idx, val, cnt = R.retina_find_peaks(grid, 3, cfg.peak_threshold, cfg.peak_capacity)
+    torch.cuda.synchronize()
+    g32 = grid.cpu().numpy().astype(np.float64)
+    ri, rv, rc = ora.peaks(g32, 3, cfg.peak_threshold, cfg.peak_capacity)
+    cnt = cnt.cpu().numpy()
+    assert cnt[0] == rc[0] and cnt[0] > 0
+    k = min(cnt[0], cfg.peak_capacity)
+    assert np.array_equal(idx.cpu().numpy()[0, :k], ri[0, :k])
+
+
+# --------------------------------------------------------------------------- T5 / T6 / T7
+def _run_multistart(cfg, ev_ids, n_seeds, n_iters=None, step=None, z_ref=0.0):
+    b = G.make_batch(cfg, ev_ids)
+    seeds = G.make_seeds(cfg, ev_ids, n_seeds=n_seeds)
+    n_iters = cfg.n_iters if n_iters is None else n_iters
+    step = cfg.step if step is None else step
+    ev = events_of(b, z_ref)
+    th, Rg, gg = R.retina_multistart_optimize(ev, cfg.model, cfg.sigma, dev(seeds), n_iters, step,
+                                              cfg.box_lo, cfg.box_hi)
+    torch.cuda.synchronize()
+    return b, seeds, th, Rg, gg
+
+
+@pytest.mark.parametrize("name,n_ev,n_seeds,step_mult", [("cfg2", 4, 1024, 1.0), ("cfg2", 2, 512, 20.0),
+                                                          ("cfg4", 1, 256, 1.0), ("cfg0", 1, 256, 1e3)])
+def test_T5_T6_T7_multistart_and_merge(name, n_ev, n_seeds, step_mult):
+    cfg = C.CONFIGS[name]
+    ev_ids = list(range(n_ev))
+    n_iters = cfg.n_iters if cfg.n_iters else 20
+    step = cfg.step * step_mult
+    b, seeds, th_d, R_d, g_d = _run_multistart(cfg, ev_ids, n_seeds, n_iters, step)
+    th, Rg = th_d.cpu().numpy(), R_d.cpu().numpy()
+    rth, rR, rg = ora.multistart(cfg.model, b.offsets, b.hits, seeds, cfg.sigma, n_iters, step,
+                                 cfg.box_lo, cfg.box_hi)
+    ranges = np.array(cfg.box_hi, np.float64) - np.array(cfg.box_lo, np.float64)
+    # T5: states within 1e-3 x range unless the seed is sensitive (oracle-side rule)
+    dev_rel = np.max(np.abs(th.astype(np.float64) - rth) / ranges, axis=2)
+    bad = np.argwhere(dev_rel > 1e-3)
+    if len(bad):
+        sens = PU.sensitive_seeds(cfg.model, b.offsets, b.hits, seeds, cfg.sigma, n_iters, step,
+                                  cfg.box_lo, cfg.box_hi, rth, ranges, [tuple(x) for x in bad])
+        assert sens.all(), f"{(~sens).sum()} non-sensitive seeds off by > 1e-3 range"
+    assert len(bad) <= 0.01 * th.shape[0] * th.shape[1]
+    assert np.all(th >= np.float32(cfg.box_lo)) and np.all(th <= np.float32(cfg.box_hi))
+    # T1 on the final responses: response_out = R(theta_out), checked at the GPU's own theta_out
+    rng = np.random.default_rng(0)
+    for e in range(len(ev_ids)):
+        for s in rng.choice(th.shape[1], 64, replace=False):
+            r, _, _ = ora.point(cfg.model, b.event_hits(e), th[e, s].astype(np.float64), cfg.sigma)
+            ok, worst = PU.t1_response(Rg[e, s], r)
+            assert ok, (e, s, worst)
+    if cfg.P == 0 or name == "cfg0":
+        return
+    # T7: merge bit-exact vs the oracle merge on the GPU's fp32 outputs
+    cap = cfg.track_capacity
+    tt, tr, ts, tz, tc = R.retina_merge_tracks(th_d, R_d, cfg.merge_radius, cfg.track_threshold, cap)
+    torch.cuda.synchronize()
+    ts, tz, tc = ts.cpu().numpy(), tz.cpu().numpy(), tc.cpu().numpy()
+    ott, otr, ots, otz, otc = ora.merge(th.astype(np.float64), Rg.astype(np.float64), cfg.merge_radius,
+                                        cfg.track_threshold, cap)
+    assert np.array_equal(tc, otc)
+    for e in range(len(ev_ids)):
+        k = min(tc[e], cap)
+        assert np.array_equal(ts[e, :k], ots[e, :k]) and np.array_equal(tz[e, :k], otz[e, :k])
+    assert np.array_equal(tt.cpu().numpy()[0, :min(tc[0], cap)], th[0, ts[0, :min(tc[0], cap)]])
+    # T6: merged track sets from GPU and oracle pipelines match within 1e-3 range,
+    # excusing tracks near R0, near the merge radius, or made only of sensitive seeds
+    _, _, ots64, _, otc64 = ora.merge(rth, rR, cfg.merge_radius, cfg.track_threshold, cap)
+    for e in range(len(ev_ids)):
+        A = th[e, ts[e, :min(tc[e], cap)]].astype(np.float64)
+        B = rth[e, ots64[e, :min(otc64[e], cap)]]
+        unmatched = 0
+        for X, Y, RX in ((A, B, Rg[e, ts[e, :min(tc[e], cap)]]), (B, A, rR[e, ots64[e, :min(otc64[e], cap)]])):
+            for x, rx in zip(X, RX):
+                if len(Y) and np.min(np.max(np.abs(Y - x) / ranges, axis=1)) <= 1e-3:
+                    continue
+                if abs(rx - cfg.track_threshold) <= 1e-5 * cfg.track_threshold:
+                    continue
+                unmatched += 1
+        assert unmatched <= max(1, 0.02 * max(len(A), len(B))), (e, unmatched, len(A), len(B))
+
+
+def test_T7_merge_synthetic_ties_and_capacity():
+    rng = np.random.default_rng(11)
+    E, S, P = 3, 16384, 3
+    centers = rng.uniform(-0.3, 0.3, (40, P)).astype(np.float32)
+    lab = rng.integers(0, 40, (E, S))
+    th = (centers[lab] + rng.normal(0, 2e-4, (E, S, P))).astype(np.float32)
+    th[:, ::7] = th[:, 3:4]  # exact duplicates
+    Rv = rng.uniform(0, 12, (E, S)).round(1).astype(np.float32)  # exact R ties
+    rad = (6e-4, 6e-4, 6e-4)
+    for cap in (4096, 3):
+        tt, tr, ts, tz, tc = R.retina_merge_tracks(dev(th), dev(Rv), rad, 5.0, cap)
+        torch.cuda.synchronize()
+        _, _, ots, otz, otc = ora.merge(th.astype(np.float64), Rv.astype(np.float64), rad, 5.0, cap)
+        assert np.array_equal(tc.cpu().numpy(), otc)
+        for e in range(E):
+            k = min(otc[e], cap)
+            assert np.array_equal(ts.cpu().numpy()[e, :k], ots[e, :k])
+            assert np.array_equal(tz.cpu().numpy()[e, :k], otz[e, :k])
+
+
+# --------------------------------------------------------------------------- identities / edges
+def test_multistart_identities_and_determinism():
+    cfg = C.CFG2
+    b = G.make_batch(cfg, [0, 1])
+    seeds = G.make_seeds(cfg, [0, 1], n_seeds=1000)
+    ev = events_of(b)
+    sd = dev(seeds)
+    th0, R0, _ = R.retina_multistart_optimize(ev, cfg.model, cfg.sigma, sd, 7, 0.0, cfg.box_lo, cfg.box_hi)
+    torch.cuda.synchronize()
+    assert torch.equal(th0, sd)
+    a = R.retina_multistart_optimize(ev, cfg.model, cfg.sigma, sd, 10, cfg.step, cfg.box_lo, cfg.box_hi)
+    bb = R.retina_multistart_optimize(ev, cfg.model, cfg.sigma, sd, 10, cfg.step, cfg.box_lo, cfg.box_hi)
+    torch.cuda.synchronize()
+    for x, y in zip(a, bb):
+        assert torch.equal(x, y)
+    # theta_out aliasing seeds; grad_out = NULL gives the same R
+    alias = sd.clone()
+    _, Ra, _ = R.retina_multistart_optimize(ev, cfg.model, cfg.sigma, alias, 10, cfg.step, cfg.box_lo,
+                                            cfg.box_hi, want_grad=False,
+                                            out=(alias, torch.empty_like(a[1]), None))
+    torch.cuda.synchronize()
+    assert torch.equal(alias, a[0]) and torch.equal(Ra, a[1])
+
+
+def test_empty_batch_and_zero_hit_events():
+    cfg = C.CFG1
+    b = synthetic_batch(C.SLOPE2, [0, 0])
+    nodes = [dev(n) for n in G.axis_nodes(cfg)]
+    ev = events_of(b)
+    g = R.retina_grid_response(ev, cfg.model, cfg.sigma, nodes)
+    idx, val, cnt = R.retina_find_peaks(g, 2, 0.0, 16)
+    seeds = dev(np.zeros((2, 10, 2), np.float32))
+    th, Rr, gg = R.retina_multistart_optimize(ev, cfg.model, cfg.sigma, seeds, 5, 1e-3, (-.3, -.3), (.3, .3))
+    torch.cuda.synchronize()
+    assert torch.all(g == 0) and torch.all(cnt == 0) and torch.all(Rr == 0) and torch.all(gg == 0)
+    e0 = R.Events(torch.zeros(1, dtype=torch.int32, device=DEV), torch.zeros((0, 4), device=DEV))
+    out = R.retina_grid_response(e0, cfg.model, cfg.sigma, nodes)
+    assert out.shape[0] == 0
