@@ -291,7 +291,9 @@ def main():
     prof = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(prof):
         try:
-            roof["traffic"] = json.load(open(prof)).get(dom)
+            per_ev = json.load(open(prof))[dom]["dram_bytes_per_event"]
+            roof["traffic"] = per_ev * E / n_launch  # bytes per launch (events per launch x per-event capture)
+            roof["traffic_unit"] = "bytes/launch (ncu dram read+write, scaled per event)"
         except Exception:
             pass
     total_pairs = (pairs_grid + pairs_ms) * world

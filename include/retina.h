@@ -64,7 +64,8 @@ enum { RETINA_LINE2D = 0, RETINA_SLOPE2 = 1, RETINA_SLOPE3 = 2 };
  * consists of N_e coordinates (x, y, z) of triggered pixels").
  *   offsets:  device int32 [n_events + 1], offsets[0] = 0, non-decreasing; event e owns
  *             hits offsets[e] .. offsets[e+1]-1.
- *   hits:     device float [4 * offsets[n_events]], (x, y, z, 0) per hit, 16-byte aligned.
+ *   hits:     device float [4 * offsets[n_events]], (x, y, z, 0) per hit, 16-byte aligned
+ *             (may be NULL only when the batch holds no hit).
  *             Hits sorted by z within an event make SLOPE3 multi-start faster (it
  *             re-forms z - z0 only when z changes); any order gives the same results
  *             up to fp32 summation order being the array order.
@@ -91,6 +92,18 @@ typedef struct {
 int retina_grid_response(const retina_events *ev, int model, float sigma,
                          const int32_t *axis_len, const float *const *axis_nodes,
                          float *response, void *stream);
+
+/* Same as retina_grid_response with an explicit kernel choice:
+ *   RETINA_GRID_AUTO       separable for SLOPE2/SLOPE3, direct for LINE2D (what
+ *                          retina_grid_response uses);
+ *   RETINA_GRID_DIRECT     one MUFU.EX2 per (unit, hit) pair (all models);
+ *   RETINA_GRID_SEPARABLE  SLOPE2/SLOPE3 only: exp(-s^2/sigma^2) = e_x(tx, hit) e_y(ty, hit)
+ *                          exactly, so the grid is a dense contraction over hits
+ *                          (RETINA_EUNSUPPORTED for LINE2D, whose residual does not split). */
+enum { RETINA_GRID_AUTO = 0, RETINA_GRID_DIRECT = 1, RETINA_GRID_SEPARABLE = 2 };
+int retina_grid_response_ex(const retina_events *ev, int model, float sigma,
+                            const int32_t *axis_len, const float *const *axis_nodes,
+                            float *response, int algorithm, void *stream);
 
 /* Step (iii) on a response grid (any fp32 grid of that shape):
  * cell c is reported iff response[c] >= threshold and response[c] > response[n] for every

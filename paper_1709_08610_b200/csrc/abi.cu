@@ -52,8 +52,7 @@ int stage_cap(int32_t hint, int dflt) {
 int check_events(const retina_events *ev) {
     if (!ev) return fail(RETINA_EINVAL, "ev is NULL");
     if (ev->n_events < 0) return fail(RETINA_EINVAL, "n_events < 0 (%d)", ev->n_events);
-    if (ev->n_events > 0 && (!ev->offsets || !ev->hits))
-        return fail(RETINA_EINVAL, "offsets/hits is NULL");
+    if (ev->n_events > 0 && !ev->offsets) return fail(RETINA_EINVAL, "offsets is NULL");
     if (((uintptr_t)ev->hits & 15u) != 0) return fail(RETINA_EINVAL, "hits must be 16-byte aligned");
     if (!std::isfinite(ev->z_ref)) return fail(RETINA_EINVAL, "z_ref is not finite");
     if (ev->max_event_hits < 0) return fail(RETINA_EINVAL, "max_event_hits < 0");
@@ -80,6 +79,11 @@ const char *retina_version(void) { return "retina-b200 0.1 sm_100a"; }
 
 int retina_grid_response(const retina_events *ev, int model, float sigma, const int32_t *axis_len,
                          const float *const *axis_nodes, float *response, void *stream) {
+    return retina_grid_response_ex(ev, model, sigma, axis_len, axis_nodes, response, RETINA_GRID_AUTO, stream);
+}
+
+int retina_grid_response_ex(const retina_events *ev, int model, float sigma, const int32_t *axis_len,
+                            const float *const *axis_nodes, float *response, int algorithm, void *stream) {
     g_last_error[0] = 0;
     int st = check_events(ev);
     if (st) return st;
@@ -95,6 +99,12 @@ int retina_grid_response(const retina_events *ev, int model, float sigma, const 
     }
     if (cells > 0x7fffffffLL) return fail(RETINA_EUNSUPPORTED, "more than 2^31-1 cells per event");
     if (ev->n_events > 0 && !response) return fail(RETINA_EINVAL, "response is NULL");
+    if (algorithm < RETINA_GRID_AUTO || algorithm > RETINA_GRID_SEPARABLE)
+        return fail(RETINA_EINVAL, "unknown grid algorithm %d", algorithm);
+    if (algorithm == RETINA_GRID_SEPARABLE && model == RETINA_LINE2D)
+        return fail(RETINA_EUNSUPPORTED, "LINE2D residual does not factorise: no separable grid");
+    const bool separable = (algorithm == RETINA_GRID_SEPARABLE) ||
+                           (algorithm == RETINA_GRID_AUTO && model != RETINA_LINE2D);
     retina::GridArgs a{};
     a.offsets = ev->offsets;
     a.hits = reinterpret_cast<const float4 *>(ev->hits);
@@ -108,7 +118,9 @@ int retina_grid_response(const retina_events *ev, int model, float sigma, const 
     a.nodes2 = (P == 3) ? axis_nodes[2] : nullptr;
     a.R = response;
     a.cap = stage_cap(ev->max_event_hits, 2048);
-    const cudaError_t err = retina::launch_grid_response(model, a, ev->n_events, (cudaStream_t)stream);
+    const cudaError_t err = separable
+                                ? retina::launch_grid_separable(model, a, ev->n_events, (cudaStream_t)stream)
+                                : retina::launch_grid_response(model, a, ev->n_events, (cudaStream_t)stream);
     if (err != cudaSuccess) return cuda_fail(err, "retina_grid_response");
     return RETINA_OK;
 }

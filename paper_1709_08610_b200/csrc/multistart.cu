@@ -4,7 +4,7 @@
 // then R(theta^n) and (optionally) grad R(theta^n).
 //
 // Mapping (K4): grid = (seed blocks, events), 128 threads per CTA, each thread
-// owns S = 2 seeds (lanes over consecutive seeds: coalesced seed loads / stores).  The event's
+// owns S = 4 seeds (lanes over consecutive seeds: coalesced seed loads / stores).  The event's
 // hits are staged ONCE in shared memory by a TMA bulk copy and stay resident for all
 // n_iters + 1 passes when they fit (HitStage); otherwise they stream per pass.  Each pass
 // accumulates, per seed, R = sum w and the raw gradient sums in registers, in hit-array order;
@@ -25,27 +25,54 @@ constexpr int kMsThreads = 128;
 template <int MODEL, int S, bool ZREF, bool GRAD>
 __device__ __forceinline__ void ms_pass(HitStage &st, const float (&th)[S][3], float negK, float zref,
                                         float (&R)[S], float (&G)[S][4]) {
+    // G[s][0..1]: sum w s_x d, sum w s_y d;  G[s][2..3] (SLOPE3): sum w s_x, sum w s_y.
+    // SLOPE2/3 gradients are accumulated per detector plane (hits with equal z, which are
+    // contiguous when hits are sorted by z): Q = sum_{k in plane} w s, then G += d_plane Q at
+    // each plane change.  This saves the per-pair w*d multiply (the FMA pipe is the binding
+    // unit of this loop); unsorted hits only make planes shorter, never wrong.
 #pragma unroll
     for (int s = 0; s < S; ++s) {
         R[s] = 0.f;
 #pragma unroll
         for (int i = 0; i < 4; ++i) G[s][i] = 0.f;
     }
-    float dh[S], dl[S];
-    float zprev = __int_as_float(0x7fc00000);  // NaN: the first hit always re-forms d
+    float dh[S], dl[S], qx[S], qy[S];
+#pragma unroll
+    for (int s = 0; s < S; ++s) dh[s] = dl[s] = qx[s] = qy[s] = 0.f;
+    float zprev = __int_as_float(0x7fc00000);  // NaN: the first hit always opens a plane
+    float dprev = 0.f, dlprev = 0.f;           // SLOPE2: d of the open plane (hi, lo)
+    auto flush = [&]() {
+#pragma unroll
+        for (int s = 0; s < S; ++s) {
+            const float d = (MODEL == kSlope3) ? dh[s] : dprev;
+            G[s][0] = __fmaf_rn(d, qx[s], G[s][0]);
+            G[s][1] = __fmaf_rn(d, qy[s], G[s][1]);
+            if (MODEL == kSlope3) {
+                G[s][2] = __fadd_rn(G[s][2], qx[s]);
+                G[s][3] = __fadd_rn(G[s][3], qy[s]);
+            }
+            qx[s] = qy[s] = 0.f;
+        }
+    };
     st.pass([&](const float4 *h, int len) {
 #pragma unroll 2
         for (int k = 0; k < len; ++k) {
             const float4 hk = h[k];
             if (MODEL == kSlope2) {
-                float hdh = hk.z, hdl = 0.f;
-                if (ZREF) two_sum(hk.z, -zref, hdh, hdl);
+                if (hk.z != zprev) {  // warp-uniform: every thread reads the same hit
+                    if (GRAD) flush();
+                    zprev = hk.z;
+                    if (ZREF)
+                        two_sum(hk.z, -zref, dprev, dlprev);
+                    else
+                        dprev = hk.z;
+                }
 #pragma unroll
                 for (int s = 0; s < S; ++s) {
                     float sx, sy;
                     if (ZREF) {
-                        sx = __fmaf_rn(-th[s][0], hdl, __fmaf_rn(-th[s][0], hdh, hk.x));
-                        sy = __fmaf_rn(-th[s][1], hdl, __fmaf_rn(-th[s][1], hdh, hk.y));
+                        sx = __fmaf_rn(-th[s][0], dlprev, __fmaf_rn(-th[s][0], dprev, hk.x));
+                        sy = __fmaf_rn(-th[s][1], dlprev, __fmaf_rn(-th[s][1], dprev, hk.y));
                     } else {
                         sx = __fmaf_rn(-th[s][0], hk.z, hk.x);
                         sy = __fmaf_rn(-th[s][1], hk.z, hk.y);
@@ -54,13 +81,13 @@ __device__ __forceinline__ void ms_pass(HitStage &st, const float (&th)[S][3], f
                     const float w = ex2_approx(__fmul_rn(q, negK));
                     R[s] = __fadd_rn(R[s], w);
                     if (GRAD) {
-                        const float wd = __fmul_rn(w, hdh);
-                        G[s][0] = __fmaf_rn(wd, sx, G[s][0]);
-                        G[s][1] = __fmaf_rn(wd, sy, G[s][1]);
+                        qx[s] = __fmaf_rn(w, sx, qx[s]);
+                        qy[s] = __fmaf_rn(w, sy, qy[s]);
                     }
                 }
             } else if (MODEL == kSlope3) {
-                if (hk.z != zprev) {  // warp-uniform: every thread reads the same hit
+                if (hk.z != zprev) {
+                    if (GRAD) flush();
                     zprev = hk.z;
 #pragma unroll
                     for (int s = 0; s < S; ++s) two_sum(hk.z, -th[s][2], dh[s], dl[s]);
@@ -73,11 +100,8 @@ __device__ __forceinline__ void ms_pass(HitStage &st, const float (&th)[S][3], f
                     const float w = ex2_approx(__fmul_rn(q, negK));
                     R[s] = __fadd_rn(R[s], w);
                     if (GRAD) {
-                        const float wd = __fmul_rn(w, dh[s]);
-                        G[s][0] = __fmaf_rn(wd, sx, G[s][0]);
-                        G[s][1] = __fmaf_rn(wd, sy, G[s][1]);
-                        G[s][2] = __fmaf_rn(w, sx, G[s][2]);
-                        G[s][3] = __fmaf_rn(w, sy, G[s][3]);
+                        qx[s] = __fmaf_rn(w, sx, qx[s]);
+                        qy[s] = __fmaf_rn(w, sy, qy[s]);
                     }
                 }
             } else {  // LINE2D
@@ -99,6 +123,111 @@ __device__ __forceinline__ void ms_pass(HitStage &st, const float (&th)[S][3], f
             }
         }
     });
+    if (GRAD && MODEL != kLine2D) flush();
+}
+
+// SLOPE2 / SLOPE3 pass on seed PAIRS with packed f32x2 arithmetic (FFMA2 / FMUL2 / FADD2):
+// every instruction of the per-pair chain serves two seeds, halving issue slots.  Each half
+// is an independent IEEE round-to-nearest operation, so results are bit-identical to the
+// scalar ms_pass.  Per (seed, hit): 8 FMA-pipe lane-ops + 1 MUFU.EX2, i.e. the loop is
+// balanced between the FMA pipe (128 lanes/clk/SM) and MUFU (16/clk/SM).
+template <int MODEL, int S, bool ZREF, bool GRAD>
+__device__ __forceinline__ void ms_pass_x2(HitStage &st, const float (&th)[S][3], float negK, float zref,
+                                           float (&R)[S], float (&G)[S][4]) {
+    static_assert(S % 2 == 0, "seed pairs");
+    constexpr int NP = S / 2;
+    float2 mtx[NP], mty[NP], r2[NP], qx[NP], qy[NP], gx[NP], gy[NP], ax[NP], ay[NP], dh[NP], dl[NP];
+    const float2 zero = make_float2(0.f, 0.f);
+#pragma unroll
+    for (int p = 0; p < NP; ++p) {
+        mtx[p] = make_float2(-th[2 * p][0], -th[2 * p + 1][0]);
+        mty[p] = make_float2(-th[2 * p][1], -th[2 * p + 1][1]);
+        r2[p] = qx[p] = qy[p] = gx[p] = gy[p] = ax[p] = ay[p] = dh[p] = dl[p] = zero;
+    }
+    const float2 nk = make_float2(negK, negK);
+    float zprev = __int_as_float(0x7fc00000);
+    float dprev = 0.f, dlprev = 0.f;
+    auto flush = [&]() {
+#pragma unroll
+        for (int p = 0; p < NP; ++p) {
+            const float2 d = (MODEL == kSlope3) ? dh[p] : make_float2(dprev, dprev);
+            gx[p] = __ffma2_rn(d, qx[p], gx[p]);
+            gy[p] = __ffma2_rn(d, qy[p], gy[p]);
+            if (MODEL == kSlope3) {
+                ax[p] = __fadd2_rn(ax[p], qx[p]);
+                ay[p] = __fadd2_rn(ay[p], qy[p]);
+            }
+            qx[p] = qy[p] = zero;
+        }
+    };
+    st.pass([&](const float4 *h, int len) {
+#pragma unroll 2
+        for (int k = 0; k < len; ++k) {
+            const float4 hk = h[k];
+            if (hk.z != zprev) {  // warp-uniform plane change
+                if (GRAD) flush();
+                zprev = hk.z;
+                if (MODEL == kSlope3) {
+#pragma unroll
+                    for (int p = 0; p < NP; ++p) {
+                        two_sum(hk.z, -th[2 * p][2], dh[p].x, dl[p].x);
+                        two_sum(hk.z, -th[2 * p + 1][2], dh[p].y, dl[p].y);
+                    }
+                } else if (ZREF) {
+                    two_sum(hk.z, -zref, dprev, dlprev);
+                } else {
+                    dprev = hk.z;
+                }
+            }
+            const float2 X = make_float2(hk.x, hk.x), Y = make_float2(hk.y, hk.y);
+#pragma unroll
+            for (int p = 0; p < NP; ++p) {
+                float2 sx, sy;
+                if (MODEL == kSlope3) {
+                    sx = __ffma2_rn(mtx[p], dl[p], __ffma2_rn(mtx[p], dh[p], X));
+                    sy = __ffma2_rn(mty[p], dl[p], __ffma2_rn(mty[p], dh[p], Y));
+                } else if (ZREF) {
+                    const float2 D = make_float2(dprev, dprev), DL = make_float2(dlprev, dlprev);
+                    sx = __ffma2_rn(mtx[p], DL, __ffma2_rn(mtx[p], D, X));
+                    sy = __ffma2_rn(mty[p], DL, __ffma2_rn(mty[p], D, Y));
+                } else {
+                    const float2 Z = make_float2(hk.z, hk.z);
+                    sx = __ffma2_rn(mtx[p], Z, X);
+                    sy = __ffma2_rn(mty[p], Z, Y);
+                }
+                const float2 a = __fmul2_rn(__ffma2_rn(sx, sx, __fmul2_rn(sy, sy)), nk);
+                const float2 w = make_float2(ex2_approx(a.x), ex2_approx(a.y));
+                r2[p] = __fadd2_rn(r2[p], w);
+                if (GRAD) {
+                    qx[p] = __ffma2_rn(w, sx, qx[p]);
+                    qy[p] = __ffma2_rn(w, sy, qy[p]);
+                }
+            }
+        }
+    });
+    if (GRAD) flush();
+#pragma unroll
+    for (int p = 0; p < NP; ++p) {
+        R[2 * p] = r2[p].x;
+        R[2 * p + 1] = r2[p].y;
+        G[2 * p][0] = gx[p].x;
+        G[2 * p + 1][0] = gx[p].y;
+        G[2 * p][1] = gy[p].x;
+        G[2 * p + 1][1] = gy[p].y;
+        G[2 * p][2] = ax[p].x;
+        G[2 * p + 1][2] = ax[p].y;
+        G[2 * p][3] = ay[p].x;
+        G[2 * p + 1][3] = ay[p].y;
+    }
+}
+
+template <int MODEL, int S, bool ZREF, bool GRAD>
+__device__ __forceinline__ void ms_eval(HitStage &st, const float (&th)[S][3], float negK, float zref,
+                                        float (&R)[S], float (&G)[S][4]) {
+    if constexpr (MODEL == kLine2D)
+        ms_pass<MODEL, S, ZREF, GRAD>(st, th, negK, zref, R, G);
+    else
+        ms_pass_x2<MODEL, S, ZREF, GRAD>(st, th, negK, zref, R, G);
 }
 
 template <int MODEL, int S>
@@ -137,7 +266,7 @@ __global__ void __launch_bounds__(kMsThreads) multistart_kernel(MultistartArgs a
 
     float R[S], G[S][4], g[S][3];
     for (int it = 0; it < a.n_iters; ++it) {
-        ms_pass<MODEL, S, ZREF, true>(st, th, a.negK, a.z_ref, R, G);
+        ms_eval<MODEL, S, ZREF, true>(st, th, a.negK, a.z_ref, R, G);
         ms_gradient<MODEL, S>(th, G, a.c2, g);
 #pragma unroll
         for (int s = 0; s < S; ++s)
@@ -146,10 +275,10 @@ __global__ void __launch_bounds__(kMsThreads) multistart_kernel(MultistartArgs a
                 th[s][i] = fminf(fmaxf(__fmaf_rn(a.step, g[s][i], th[s][i]), a.lo[i]), a.hi[i]);
     }
     if (a.grad_out) {
-        ms_pass<MODEL, S, ZREF, true>(st, th, a.negK, a.z_ref, R, G);
+        ms_eval<MODEL, S, ZREF, true>(st, th, a.negK, a.z_ref, R, G);
         ms_gradient<MODEL, S>(th, G, a.c2, g);
     } else {
-        ms_pass<MODEL, S, ZREF, false>(st, th, a.negK, a.z_ref, R, G);
+        ms_eval<MODEL, S, ZREF, false>(st, th, a.negK, a.z_ref, R, G);
     }
 #pragma unroll
     for (int s = 0; s < S; ++s) {
@@ -167,7 +296,7 @@ __global__ void __launch_bounds__(kMsThreads) multistart_kernel(MultistartArgs a
 
 template <int MODEL, bool ZREF>
 static cudaError_t launch_ms(const MultistartArgs &a0, int n_events, cudaStream_t stream) {
-    constexpr int S = 2;
+    constexpr int S = 4;
     auto kern = multistart_kernel<MODEL, S, ZREF>;
     const size_t smem = (size_t)a0.cap * sizeof(float4);
     cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);

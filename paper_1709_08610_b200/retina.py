@@ -19,7 +19,9 @@ MODEL_P = {LINE2D: 2, SLOPE2: 2, SLOPE3: 3}
 RETINA_OK, RETINA_EINVAL, RETINA_EUNSUPPORTED, RETINA_ECUDA = 0, 1, 2, 3
 MERGE_MAX_SEEDS = 16384
 
-EXPORTED = ("retina_grid_response", "retina_find_peaks", "retina_multistart_optimize",
+GRID_AUTO, GRID_DIRECT, GRID_SEPARABLE = 0, 1, 2
+
+EXPORTED = ("retina_grid_response", "retina_grid_response_ex", "retina_find_peaks", "retina_multistart_optimize",
             "retina_merge_tracks", "retina_status_string", "retina_last_error", "retina_version")
 
 
@@ -47,11 +49,13 @@ def lib() -> ctypes.CDLL:
         L = ctypes.CDLL(LIB)
         vp, i32, f32 = ctypes.c_void_p, ctypes.c_int32, ctypes.c_float
         L.retina_grid_response.argtypes = [ctypes.POINTER(retina_events), ctypes.c_int, f32, vp, vp, vp, vp]
+        L.retina_grid_response_ex.argtypes = [ctypes.POINTER(retina_events), ctypes.c_int, f32, vp, vp, vp,
+                                              ctypes.c_int, vp]
         L.retina_find_peaks.argtypes = [vp, i32, i32, vp, f32, i32, vp, vp, vp, vp]
         L.retina_multistart_optimize.argtypes = [ctypes.POINTER(retina_events), ctypes.c_int, f32, i32, vp,
                                                  i32, f32, vp, vp, vp, vp, vp, vp]
         L.retina_merge_tracks.argtypes = [i32, i32, i32, vp, vp, vp, f32, i32, vp, vp, vp, vp, vp, vp]
-        for f in (L.retina_grid_response, L.retina_find_peaks, L.retina_multistart_optimize,
+        for f in (L.retina_grid_response, L.retina_grid_response_ex, L.retina_find_peaks, L.retina_multistart_optimize,
                   L.retina_merge_tracks):
             f.restype = ctypes.c_int
         L.retina_status_string.argtypes = [ctypes.c_int]
@@ -118,7 +122,8 @@ class Events:
 
 
 def retina_grid_response(events: Events, model: int, sigma: float, nodes: Sequence[torch.Tensor],
-                         out: Optional[torch.Tensor] = None, stream=None) -> torch.Tensor:
+                         out: Optional[torch.Tensor] = None, stream=None, algorithm: int = GRID_AUTO
+                         ) -> torch.Tensor:
     P = MODEL_P[model]
     nodes = [_dev(n, torch.float32) for n in nodes]
     alen, _k1 = _arr(ctypes.c_int32, [n.numel() for n in nodes])
@@ -126,9 +131,9 @@ def retina_grid_response(events: Events, model: int, sigma: float, nodes: Sequen
     if out is None:
         out = torch.empty((events.n_events,) + tuple(n.numel() for n in nodes), device=events.hits.device,
                           dtype=torch.float32)
-    _check("retina_grid_response",
-           lib().retina_grid_response(ctypes.byref(events.c), model, float(sigma), alen, nptr,
-                                      _ptr(_dev(out, torch.float32)), _stream(stream)))
+    _check("retina_grid_response_ex",
+           lib().retina_grid_response_ex(ctypes.byref(events.c), model, float(sigma), alen, nptr,
+                                         _ptr(_dev(out, torch.float32)), int(algorithm), _stream(stream)))
     return out
 
 
