@@ -31,21 +31,28 @@ def stale() -> bool:
     return any(os.path.getmtime(p) > t for p in _deps())
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not stale():
+def build(force: bool = False, verbose: bool = False, out: str = LIB, defines=()) -> str:
+    """Compile every csrc/*.cu into one shared library (`defines` only for experiments)."""
+    if out == LIB and not defines and not force and not stale():
         return LIB
-    cmd = [NVCC, *ARCH, *FLAGS, "-shared", "-o", LIB, *sources()]
+    cmd = [NVCC, *ARCH, *FLAGS, *[f"-D{d}" for d in defines], "-shared", "-o", out, *sources()]
     res = subprocess.run(cmd, capture_output=True, text=True)
     if res.returncode != 0:
         sys.stderr.write(res.stdout + res.stderr)
         raise RuntimeError("nvcc failed building libretina.so")
-    with open(os.path.join(PKG, "ptxas.log"), "w") as f:
-        f.write(res.stderr)
+    if out == LIB:
+        with open(os.path.join(PKG, "ptxas.log"), "w") as f:
+            f.write(res.stderr)
     if verbose:
         sys.stderr.write(res.stderr)
-    return LIB
+    return out
 
 
 if __name__ == "__main__":
-    build(force="--force" in sys.argv, verbose=True)
-    print(LIB)
+    import argparse
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--force", action="store_true")
+    ap.add_argument("--out", default=LIB)
+    ap.add_argument("-D", dest="defines", action="append", default=[])
+    a = ap.parse_args()
+    print(build(force=a.force, verbose=True, out=a.out, defines=a.defines))

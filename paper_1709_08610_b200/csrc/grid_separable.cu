@@ -16,8 +16,9 @@
 // Tiling: CTA = 256 threads computes a 128 (axis 0, tx) x 128 (axis 1, ty) tile of one event
 // (and one z0 for SLOPE3).  Hits are staged in shared memory by TMA bulk copies (HitStage);
 // per 32-hit chunk the CTA generates EX[32][128] and EY[32][128] into shared memory (one
-// MUFU.EX2 each), then every thread accumulates an 8x8 register micro-tile with 64 FFMA per
-// 4 LDS.128.
+// MUFU.EX2 each), then every thread accumulates an 8x8 register micro-tile with 32 FFMA2
+// (row value broadcast) per 4 LDS.128.  (A variant that interleaved the next chunk's
+// generation with this chunk's FFMA2s spilled at 128 registers and measured slower.)
 #include "common.cuh"
 #include "kernels.cuh"
 
@@ -52,11 +53,13 @@ __global__ void __launch_bounds__(256, 2) grid_separable_kernel(GridArgs a) {
     const float z0 = (MODEL == kSlope3) ? __ldg(a.nodes2 + l) : a.z_ref;
     const float negK = a.negK;
 
-    float acc[8][8];
+    // 8 x 8 micro-tile as 8 x 4 column PAIRS: one FFMA2 (row value broadcast to both halves)
+    // updates two units, halving issue slots; each half is an IEEE fma.rn, same as FFMA.
+    float2 acc[8][4];
 #pragma unroll
     for (int r = 0; r < 8; ++r)
 #pragma unroll
-        for (int c = 0; c < 8; ++c) acc[r][c] = 0.f;
+        for (int c = 0; c < 4; ++c) acc[r][c] = make_float2(0.f, 0.f);
 
     st.pass([&](const float4 *h, int len) {
         for (int k0 = 0; k0 < len; k0 += SB_K) {
@@ -90,16 +93,19 @@ __global__ void __launch_bounds__(256, 2) grid_separable_kernel(GridArgs a) {
                 const float4 b0 = *reinterpret_cast<const float4 *>(&sB[k][tc * 4]);
                 const float4 b1 = *reinterpret_cast<const float4 *>(&sB[k][64 + tc * 4]);
                 const float av[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
-                const float bv[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
+                const float2 bv[4] = {make_float2(b0.x, b0.y), make_float2(b0.z, b0.w), make_float2(b1.x, b1.y),
+                                      make_float2(b1.z, b1.w)};
 #pragma unroll
                 for (int r = 0; r < 8; ++r)
 #pragma unroll
-                    for (int c = 0; c < 8; ++c) acc[r][c] = __fmaf_rn(av[r], bv[c], acc[r][c]);
+                    for (int c = 0; c < 4; ++c)
+                        acc[r][c] = __ffma2_rn(make_float2(av[r], av[r]), bv[c], acc[r][c]);
             }
             __syncthreads();
         }
     });
 
+#define ACC(r, c) (((c) & 1) ? acc[r][(c) >> 1].y : acc[r][(c) >> 1].x)
     const int64_t cells = (int64_t)a.n0 * a.n1 * (MODEL == kSlope3 ? a.n2 : 1);
     float *out = a.R + (int64_t)e * cells;
 #pragma unroll
@@ -112,21 +118,23 @@ __global__ void __launch_bounds__(256, 2) grid_separable_kernel(GridArgs a) {
             if (MODEL == kSlope3) {
 #pragma unroll
                 for (int c = 0; c < 4; ++c)
-                    if (j0 + c < a.n1) out[((int64_t)i * a.n1 + j0 + c) * a.n2 + l] = acc[r][half * 4 + c];
+                    if (j0 + c < a.n1) out[((int64_t)i * a.n1 + j0 + c) * a.n2 + l] = ACC(r, half * 4 + c);
             } else {
                 float *p = out + (int64_t)i * a.n1 + j0;
                 if (j0 + 3 < a.n1 && ((reinterpret_cast<uintptr_t>(p) & 15u) == 0)) {
                     *reinterpret_cast<float4 *>(p) =
-                        make_float4(acc[r][half * 4], acc[r][half * 4 + 1], acc[r][half * 4 + 2], acc[r][half * 4 + 3]);
+                        make_float4(ACC(r, half * 4), ACC(r, half * 4 + 1), ACC(r, half * 4 + 2), ACC(r, half * 4 + 3));
                 } else {
 #pragma unroll
                     for (int c = 0; c < 4; ++c)
-                        if (j0 + c < a.n1) p[c] = acc[r][half * 4 + c];
+                        if (j0 + c < a.n1) p[c] = ACC(r, half * 4 + c);
                 }
             }
         }
     }
 }
+
+#undef ACC
 
 template <int MODEL, bool ZREF>
 static cudaError_t launch_sep(const GridArgs &a0, int n_events, cudaStream_t stream) {

@@ -4,7 +4,7 @@
 // then R(theta^n) and (optionally) grad R(theta^n).
 //
 // Mapping (K4): grid = (seed blocks, events), 128 threads per CTA, each thread
-// owns S = 4 seeds (lanes over consecutive seeds: coalesced seed loads / stores).  The event's
+// owns S = 8 seeds (lanes over consecutive seeds: coalesced seed loads / stores).  The event's
 // hits are staged ONCE in shared memory by a TMA bulk copy and stay resident for all
 // n_iters + 1 passes when they fit (HitStage); otherwise they stream per pass.  Each pass
 // accumulates, per seed, R = sum w and the raw gradient sums in registers, in hit-array order;
@@ -131,7 +131,7 @@ __device__ __forceinline__ void ms_pass(HitStage &st, const float (&th)[S][3], f
 // is an independent IEEE round-to-nearest operation, so results are bit-identical to the
 // scalar ms_pass.  Per (seed, hit): 8 FMA-pipe lane-ops + 1 MUFU.EX2, i.e. the loop is
 // balanced between the FMA pipe (128 lanes/clk/SM) and MUFU (16/clk/SM).
-template <int MODEL, int S, bool ZREF, bool GRAD>
+template <int MODEL, int S, bool ZREF, bool GRAD, bool WANT_R>
 __device__ __forceinline__ void ms_pass_x2(HitStage &st, const float (&th)[S][3], float negK, float zref,
                                            float (&R)[S], float (&G)[S][4]) {
     static_assert(S % 2 == 0, "seed pairs");
@@ -197,7 +197,7 @@ __device__ __forceinline__ void ms_pass_x2(HitStage &st, const float (&th)[S][3]
                 }
                 const float2 a = __fmul2_rn(__ffma2_rn(sx, sx, __fmul2_rn(sy, sy)), nk);
                 const float2 w = make_float2(ex2_approx(a.x), ex2_approx(a.y));
-                r2[p] = __fadd2_rn(r2[p], w);
+                if (WANT_R) r2[p] = __fadd2_rn(r2[p], w);  // iterations only need grad R
                 if (GRAD) {
                     qx[p] = __ffma2_rn(w, sx, qx[p]);
                     qy[p] = __ffma2_rn(w, sy, qy[p]);
@@ -221,13 +221,13 @@ __device__ __forceinline__ void ms_pass_x2(HitStage &st, const float (&th)[S][3]
     }
 }
 
-template <int MODEL, int S, bool ZREF, bool GRAD>
+template <int MODEL, int S, bool ZREF, bool GRAD, bool WANT_R>
 __device__ __forceinline__ void ms_eval(HitStage &st, const float (&th)[S][3], float negK, float zref,
                                         float (&R)[S], float (&G)[S][4]) {
     if constexpr (MODEL == kLine2D)
         ms_pass<MODEL, S, ZREF, GRAD>(st, th, negK, zref, R, G);
     else
-        ms_pass_x2<MODEL, S, ZREF, GRAD>(st, th, negK, zref, R, G);
+        ms_pass_x2<MODEL, S, ZREF, GRAD, WANT_R>(st, th, negK, zref, R, G);
 }
 
 template <int MODEL, int S>
@@ -266,7 +266,7 @@ __global__ void __launch_bounds__(kMsThreads) multistart_kernel(MultistartArgs a
 
     float R[S], G[S][4], g[S][3];
     for (int it = 0; it < a.n_iters; ++it) {
-        ms_eval<MODEL, S, ZREF, true>(st, th, a.negK, a.z_ref, R, G);
+        ms_eval<MODEL, S, ZREF, true, false>(st, th, a.negK, a.z_ref, R, G);
         ms_gradient<MODEL, S>(th, G, a.c2, g);
 #pragma unroll
         for (int s = 0; s < S; ++s)
@@ -275,10 +275,10 @@ __global__ void __launch_bounds__(kMsThreads) multistart_kernel(MultistartArgs a
                 th[s][i] = fminf(fmaxf(__fmaf_rn(a.step, g[s][i], th[s][i]), a.lo[i]), a.hi[i]);
     }
     if (a.grad_out) {
-        ms_eval<MODEL, S, ZREF, true>(st, th, a.negK, a.z_ref, R, G);
+        ms_eval<MODEL, S, ZREF, true, true>(st, th, a.negK, a.z_ref, R, G);
         ms_gradient<MODEL, S>(th, G, a.c2, g);
     } else {
-        ms_eval<MODEL, S, ZREF, false>(st, th, a.negK, a.z_ref, R, G);
+        ms_eval<MODEL, S, ZREF, false, true>(st, th, a.negK, a.z_ref, R, G);
     }
 #pragma unroll
     for (int s = 0; s < S; ++s) {
@@ -296,7 +296,10 @@ __global__ void __launch_bounds__(kMsThreads) multistart_kernel(MultistartArgs a
 
 template <int MODEL, bool ZREF>
 static cudaError_t launch_ms(const MultistartArgs &a0, int n_events, cudaStream_t stream) {
-    constexpr int S = 4;
+#ifndef RETINA_MS_SEEDS
+#define RETINA_MS_SEEDS 8
+#endif
+    constexpr int S = RETINA_MS_SEEDS;
     auto kern = multistart_kernel<MODEL, S, ZREF>;
     const size_t smem = (size_t)a0.cap * sizeof(float4);
     cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);

@@ -43,10 +43,11 @@ def lib() -> ctypes.CDLL:
     """Load libretina.so (built in-tree by __graft_entry__.build() / build.py)."""
     global _lib
     if _lib is None:
-        if not os.path.exists(LIB):
-            raise ImportError(f"{LIB} is missing: run `python -m paper_1709_08610_b200.build` "
+        path = os.environ.get("RETINA_LIB", LIB)  # experiments may point at a variant build
+        if not os.path.exists(path):
+            raise ImportError(f"{path} is missing: run `python -m paper_1709_08610_b200.build` "
                               "(there is no CPU fallback)")
-        L = ctypes.CDLL(LIB)
+        L = ctypes.CDLL(path)
         vp, i32, f32 = ctypes.c_void_p, ctypes.c_int32, ctypes.c_float
         L.retina_grid_response.argtypes = [ctypes.POINTER(retina_events), ctypes.c_int, f32, vp, vp, vp, vp]
         L.retina_grid_response_ex.argtypes = [ctypes.POINTER(retina_events), ctypes.c_int, f32, vp, vp, vp,
