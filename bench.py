@@ -268,34 +268,52 @@ def main():
             dist.destroy_process_group()
         return
 
-    # ---- roofline of the dominant kernel (largest share of the step)
+    # ---- roofline of every hot kernel; the dominant one (largest share of the step) on top
     pk = peaks_json()
     fmax = float(pk.get("sm_max_mhz", 1965.0)) * 1e6
-    work = {"grid": pairs_grid, "multistart": pairs_ms}
-    dom = max((k for k in phase_ms if k in work), key=lambda k: phase_ms[k])
-    n_launch = phase_n[dom] / a.steps
-    avg_ms = phase_ms[dom] / phase_n[dom]
-    per_launch = work[dom] / n_launch
-    achieved = per_launch / (avg_ms * 1e-3)
-    peak_pairs = N_SM * MUFU_PER_SM_CLK * fmax  # 1 MUFU.EX2 per pair
     clk = clocks.summary()
-    roof = {"bound": "alu", "kernel": {"grid": "grid_response_kernel", "multistart": "multistart_kernel"}[dom],
-            "achieved": achieved / 1e9, "peak": peak_pairs / 1e9, "unit": "Gpair/s (1 MUFU.EX2 per pair)",
-            "frac": achieved / peak_pairs,
-            "peak_basis": f"{N_SM} SMs x {MUFU_PER_SM_CLK} MUFU.EX2/clk/SM (measured 15.95) x sm_max_mhz "
-                          f"{fmax / 1e6:.0f} (MEASURED_PEAKS.json)",
-            "frac_at_measured_clock": (achieved / (N_SM * MUFU_PER_SM_CLK * clk["sm_mhz"] * 1e6)
-                                       if clk.get("sm_mhz") else None),
-            "traffic": None, "launch_ms": avg_ms, "pairs_per_launch": per_launch,
-            "share_of_step": phase_ms[dom] / a.steps / ms_step}
+    traffic = {}
     prof = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(prof):
         try:
-            per_ev = json.load(open(prof))[dom]["dram_bytes_per_event"]
-            roof["traffic"] = per_ev * E / n_launch  # bytes per launch (events per launch x per-event capture)
-            roof["traffic_unit"] = "bytes/launch (ncu dram read+write, scaled per event)"
+            traffic = json.load(open(prof))
         except Exception:
-            pass
+            traffic = {}
+    work = {"grid": pairs_grid, "multistart": pairs_ms}
+    roofs = {}
+    for ph in (k for k in phase_ms if k in work):
+        n_launch = phase_n[ph] / a.steps
+        avg_ms = phase_ms[ph] / phase_n[ph]
+        per_launch = work[ph] / n_launch
+        pairs_s = per_launch / (avg_ms * 1e-3)
+        if ph == "grid" and cfg.model == C.SLOPE2:
+            # tcgen05 3xTF32 contraction: 2 algorithmic flops per (unit, hit) pair; the fp32-accurate
+            # tensor peak is the TF32 peak (measured bf16 burst x nominal tf32/bf16 = 0.5) / 3 passes
+            peak = float(pk.get("bf16_tflops", 1590.0)) * 1e12 * 0.5 / 3.0
+            r = {"bound": "tensor", "kernel": "grid_tensor_kernel (tcgen05.mma kind::tf32, 3xTF32)",
+                 "achieved": 2.0 * pairs_s / 1e12, "peak": peak / 1e12, "unit": "TFLOP/s",
+                 "frac": 2.0 * pairs_s / peak,
+                 "peak_basis": "MEASURED_PEAKS.json bf16_tflops (burst) x 0.5 (tf32/bf16 nominal) / 3 (3xTF32 split); "
+                               "algorithmic flops = 2 per unit.hit pair",
+                 "executed_tf32_frac": 6.0 * pairs_s / (peak * 3.0)}
+        else:
+            peak = N_SM * MUFU_PER_SM_CLK * fmax  # 1 MUFU.EX2 per pair
+            r = {"bound": "alu", "kernel": {"grid": "grid_separable/direct", "multistart": "multistart_kernel"}[ph],
+                 "achieved": pairs_s / 1e9, "peak": peak / 1e9, "unit": "Gpair/s (1 MUFU.EX2 per pair)",
+                 "frac": pairs_s / peak,
+                 "peak_basis": f"{N_SM} SMs x {MUFU_PER_SM_CLK} MUFU.EX2/clk/SM (measured 15.95) x sm_max_mhz "
+                               f"{fmax / 1e6:.0f} (MEASURED_PEAKS.json); FMA pipe gives the same 16 pairs/clk/SM "
+                               "at 8 lane-ops per pair",
+                 "frac_at_measured_clock": (pairs_s / (N_SM * MUFU_PER_SM_CLK * clk["sm_mhz"] * 1e6)
+                                            if clk.get("sm_mhz") else None)}
+        r.update({"launch_ms": avg_ms, "pairs_per_launch": per_launch, "pairs_per_s": pairs_s,
+                  "share_of_step": phase_ms[ph] / a.steps / ms_step, "traffic": None})
+        if ph in traffic:
+            r["traffic"] = traffic[ph]["dram_bytes_per_event"] * E / n_launch
+            r["traffic_unit"] = "bytes/launch (ncu dram read+write per event x events per launch)"
+        roofs[ph] = r
+    dom = max(roofs, key=lambda k: roofs[k]["share_of_step"])
+    roof = dict(roofs[dom])
     total_pairs = (pairs_grid + pairs_ms) * world
     line = {
         "metric": METRIC, "value": total_pairs / (ms_step * 1e-3), "unit": UNIT, "n_gpus": world,
@@ -312,6 +330,7 @@ def main():
                    "parallelism": f"dp{world} (events sharded, 1 all_gather of results)"},
         "phases_ms_per_step": {k: v / a.steps for k, v in phase_ms.items()},
         "roofline": roof,
+        "roofline_kernels": roofs,
         "clocks": clk,
         "e2e": {"value": total_pairs / (e2e_ms_step * 1e-3), "unit": UNIT, "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms_step},

@@ -94,13 +94,16 @@ int retina_grid_response(const retina_events *ev, int model, float sigma,
                          float *response, void *stream);
 
 /* Same as retina_grid_response with an explicit kernel choice:
- *   RETINA_GRID_AUTO       separable for SLOPE2/SLOPE3, direct for LINE2D (what
- *                          retina_grid_response uses);
+ *   RETINA_GRID_AUTO       tensor for SLOPE2, separable for SLOPE3, direct for LINE2D
+ *                          (what retina_grid_response uses);
  *   RETINA_GRID_DIRECT     one MUFU.EX2 per (unit, hit) pair (all models);
  *   RETINA_GRID_SEPARABLE  SLOPE2/SLOPE3 only: exp(-s^2/sigma^2) = e_x(tx, hit) e_y(ty, hit)
- *                          exactly, so the grid is a dense contraction over hits
- *                          (RETINA_EUNSUPPORTED for LINE2D, whose residual does not split). */
-enum { RETINA_GRID_AUTO = 0, RETINA_GRID_DIRECT = 1, RETINA_GRID_SEPARABLE = 2 };
+ *                          exactly, so the grid is a dense contraction over hits, done with
+ *                          FFMA2 on the CUDA cores (RETINA_EUNSUPPORTED for LINE2D, whose
+ *                          residual does not split);
+ *   RETINA_GRID_TENSOR     SLOPE2 only: the same contraction on the tcgen05 tensor cores with a
+ *                          3xTF32 split (fp32-level accuracy), accumulators in TMEM. */
+enum { RETINA_GRID_AUTO = 0, RETINA_GRID_DIRECT = 1, RETINA_GRID_SEPARABLE = 2, RETINA_GRID_TENSOR = 3 };
 int retina_grid_response_ex(const retina_events *ev, int model, float sigma,
                             const int32_t *axis_len, const float *const *axis_nodes,
                             float *response, int algorithm, void *stream);

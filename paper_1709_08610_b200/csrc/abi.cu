@@ -99,12 +99,16 @@ int retina_grid_response_ex(const retina_events *ev, int model, float sigma, con
     }
     if (cells > 0x7fffffffLL) return fail(RETINA_EUNSUPPORTED, "more than 2^31-1 cells per event");
     if (ev->n_events > 0 && !response) return fail(RETINA_EINVAL, "response is NULL");
-    if (algorithm < RETINA_GRID_AUTO || algorithm > RETINA_GRID_SEPARABLE)
+    if (algorithm < RETINA_GRID_AUTO || algorithm > RETINA_GRID_TENSOR)
         return fail(RETINA_EINVAL, "unknown grid algorithm %d", algorithm);
     if (algorithm == RETINA_GRID_SEPARABLE && model == RETINA_LINE2D)
         return fail(RETINA_EUNSUPPORTED, "LINE2D residual does not factorise: no separable grid");
-    const bool separable = (algorithm == RETINA_GRID_SEPARABLE) ||
-                           (algorithm == RETINA_GRID_AUTO && model != RETINA_LINE2D);
+    if (algorithm == RETINA_GRID_TENSOR && model != RETINA_SLOPE2)
+        return fail(RETINA_EUNSUPPORTED, "tensor-core grid is implemented for SLOPE2 only");
+    if (algorithm == RETINA_GRID_AUTO)
+        algorithm = (model == RETINA_LINE2D)   ? RETINA_GRID_DIRECT
+                    : (model == RETINA_SLOPE2) ? RETINA_GRID_TENSOR
+                                               : RETINA_GRID_SEPARABLE;
     retina::GridArgs a{};
     a.offsets = ev->offsets;
     a.hits = reinterpret_cast<const float4 *>(ev->hits);
@@ -118,9 +122,13 @@ int retina_grid_response_ex(const retina_events *ev, int model, float sigma, con
     a.nodes2 = (P == 3) ? axis_nodes[2] : nullptr;
     a.R = response;
     a.cap = stage_cap(ev->max_event_hits, 2048);
-    const cudaError_t err = separable
-                                ? retina::launch_grid_separable(model, a, ev->n_events, (cudaStream_t)stream)
-                                : retina::launch_grid_response(model, a, ev->n_events, (cudaStream_t)stream);
+    cudaError_t err;
+    if (algorithm == RETINA_GRID_TENSOR)
+        err = retina::launch_grid_tensor(model, a, ev->n_events, (cudaStream_t)stream);
+    else if (algorithm == RETINA_GRID_SEPARABLE)
+        err = retina::launch_grid_separable(model, a, ev->n_events, (cudaStream_t)stream);
+    else
+        err = retina::launch_grid_response(model, a, ev->n_events, (cudaStream_t)stream);
     if (err != cudaSuccess) return cuda_fail(err, "retina_grid_response");
     return RETINA_OK;
 }

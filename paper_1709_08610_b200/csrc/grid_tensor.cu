@@ -1,0 +1,251 @@
+// grid_tensor.cu -- K1t: Eq. (2) for SLOPE2 as a dense contraction on the 5th-generation tensor
+// cores (tcgen05.mma, accumulators in TMEM).
+//
+// Same exact factorisation as K1s (grid_separable.cu):
+//     R[i][j] = sum_k EX[i][k] * EY[j][k],  EX = 2^(-K (x - tx z)^2),  EY = 2^(-K (y - ty z)^2).
+// fp32 accuracy on TF32 tensor cores by the 3xTF32 split: every factor v is written as
+// v = hi + lo with hi = v truncated to TF32 (exact) and lo = v - hi (exact in fp32, then seen
+// with TF32's 11 significant bits), and the K dimension is concatenated three times,
+//     [EX_hi | EX_hi | EX_lo] . [EY_hi | EY_lo | EY_hi]^T,
+// so one accumulator receives hi.hi + hi.lo + lo.hi (the dropped lo.lo term is ~2^-22 relative).
+// All terms are positive (no cancellation), so the relative error of R stays ~1e-6 (T1).
+//
+// CTA = 256 threads, one 128 (tx) x 256 (ty) output tile of one event, 1 CTA per SM (~200 KB
+// smem).  Hits are staged once in shared memory by TMA bulk copies (HitStage).  Per 32-hit
+// chunk all 8 warps GENERATE the split operands (one MUFU.EX2 per factor) into one of two
+// operand stages (K-major, no-swizzle UMMA canonical layout), then thread 0 issues
+// 4 k-steps x 3 parts = 12 tcgen05.mma (M=128, N=256, K=8, kind::tf32) and commits them to the
+// stage's mbarrier; the next chunk is generated into the other stage while the tensor core
+// works.  Epilogue: tcgen05.ld (32x32b.x16) TMEM -> registers -> coalesced-by-row stores.
+#include "common.cuh"
+#include "kernels.cuh"
+
+namespace retina {
+
+constexpr int TC_M = 128, TC_N = 256, TC_KC = 32;        // tile and hits per chunk
+constexpr int TC_A_BYTES = TC_M * TC_KC * 4;             // one part (hi or lo) of A: 16 KB
+constexpr int TC_B_BYTES = TC_N * TC_KC * 4;             // one part of B: 32 KB
+constexpr int TC_STAGE_BYTES = 2 * TC_A_BYTES + 2 * TC_B_BYTES;  // 96 KB
+constexpr int TC_TMEM_COLS = 256;
+
+__device__ __forceinline__ uint64_t umma_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+    // SM100 shared-memory matrix descriptor, K-major, SWIZZLE_NONE (layout type 0):
+    // start>>4 [0,14), LBO>>4 [16,30), SBO>>4 [32,46), version 1 [46,48).
+    return (uint64_t)((saddr >> 4) & 0x3FFFu) | ((uint64_t)((lbo >> 4) & 0x3FFFu) << 16) |
+           ((uint64_t)((sbo >> 4) & 0x3FFFu) << 32) | (1ull << 46);
+}
+
+// kind::tf32 instruction descriptor: D f32 (bits 4-5 = 1), A/B tf32 (2 at bits 7-9, 10-12),
+// both K-major, N >> 3 at bits 17-22, M >> 4 at bits 24-28.
+constexpr uint32_t kTcIdesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(TC_N >> 3) << 17) |
+                              ((uint32_t)(TC_M >> 4) << 24);
+
+__device__ __forceinline__ void tc_mma(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+        "l"(da), "l"(db), "r"(kTcIdesc), "r"(accumulate));
+}
+
+__device__ __forceinline__ void tc_commit(uint64_t *bar) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                     smem_u32(bar))
+                 : "memory");
+}
+
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+
+__device__ __forceinline__ float tf32_trunc(float v) { return __uint_as_float(__float_as_uint(v) & 0xFFFFE000u); }
+
+template <bool ZREF>
+__global__ void __launch_bounds__(256, 1) grid_tensor_kernel(GridArgs a) {
+    extern __shared__ __align__(1024) uint8_t s_raw[];
+    __shared__ __align__(8) uint64_t s_bar[2];     // hit stage
+    __shared__ __align__(8) uint64_t s_empty[2];   // operand stage s free (MMAs done)
+    __shared__ uint32_t s_tmem;
+
+    uint8_t *stage_base = s_raw;                                           // 2 x 96 KB operands
+    float4 *s_hits = reinterpret_cast<float4 *>(s_raw + 2 * TC_STAGE_BYTES);  // hit stage after
+
+    const int e = a.e_base + blockIdx.y;
+    const int tn = (a.n1 + TC_N - 1) / TC_N;
+    const int t_n = blockIdx.x % tn, t_m = blockIdx.x / tn;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+
+    if (warp == 0) {  // TMEM accumulator: 128 lanes x 256 fp32 columns
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&s_tmem)),
+                     "r"(TC_TMEM_COLS));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+        tc_fence_before();
+    }
+    if (tid == 0) {
+        mbar_init(&s_empty[0], 1);
+        mbar_init(&s_empty[1], 1);
+    }
+    const int start = a.offsets[e], nh = a.offsets[e + 1] - start;
+    HitStage st;
+    st.init(s_hits, s_bar, a.hits + start, nh, a.cap);  // contains __syncthreads (+ mbarrier fence)
+    tc_fence_after();
+    const uint32_t tmem = s_tmem;
+
+    // generation roles: warp = k-block (4 hits) of the chunk, lane + 32 t = operand row
+    float pa[4], pb[8];
+#pragma unroll
+    for (int t = 0; t < 4; ++t) pa[t] = __ldg(a.nodes0 + min(t_m * TC_M + lane + 32 * t, a.n0 - 1));
+#pragma unroll
+    for (int t = 0; t < 8; ++t) pb[t] = __ldg(a.nodes1 + min(t_n * TC_N + lane + 32 * t, a.n1 - 1));
+    const float negK = a.negK, zref = a.z_ref;
+    const uint32_t stage_saddr = smem_u32(stage_base);
+
+    int chunk = 0;  // global chunk counter (uniform)
+    st.pass([&](const float4 *h, int len) {
+        for (int k0 = 0; k0 < len; k0 += TC_KC, ++chunk) {
+            const int s = chunk & 1;
+            if (chunk >= 2) mbar_wait(&s_empty[s], ((chunk - 2) >> 1) & 1);  // MMAs of chunk-2 done
+            uint8_t *sb = stage_base + s * TC_STAGE_BYTES;
+            // ---- generate this warp's k-block (4 hits) for 4 A rows and 8 B rows per lane
+            float hx[4], hy[4], hz[4], hzl[4];
+            bool ok[4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const int k = k0 + warp * 4 + q;
+                ok[q] = k < len;
+                const float4 hk = h[ok[q] ? k : 0];
+                hx[q] = hk.x;
+                hy[q] = hk.y;
+                if (ZREF)
+                    two_sum(hk.z, -zref, hz[q], hzl[q]);
+                else {
+                    hz[q] = hk.z;
+                    hzl[q] = 0.f;
+                }
+            }
+            float *Ahi = reinterpret_cast<float *>(sb);
+            float *Alo = reinterpret_cast<float *>(sb + TC_A_BYTES);
+            float *Bhi = reinterpret_cast<float *>(sb + 2 * TC_A_BYTES);
+            float *Blo = reinterpret_cast<float *>(sb + 2 * TC_A_BYTES + TC_B_BYTES);
+#pragma unroll
+            for (int t = 0; t < 12; ++t) {
+                const bool isA = t < 4;
+                const float p = isA ? pa[t] : pb[t - 4];
+                float vh[4], vl[4];
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    const float c = isA ? hx[q] : hy[q];
+                    const float sres = ZREF ? __fmaf_rn(-p, hzl[q], __fmaf_rn(-p, hz[q], c)) : __fmaf_rn(-p, hz[q], c);
+                    const float v = ok[q] ? ex2_approx(__fmul_rn(__fmul_rn(sres, sres), negK)) : 0.f;
+                    vh[q] = tf32_trunc(v);
+                    vl[q] = __fsub_rn(v, vh[q]);
+                }
+                // K-major no-swizzle canonical layout: k-block kb of 4 elements, row r at 16 B
+                const int r = lane + 32 * (isA ? t : t - 4);
+                const int rows = isA ? TC_M : TC_N;
+                float *dh = (isA ? Ahi : Bhi) + (warp * rows + r) * 4;
+                float *dl = (isA ? Alo : Blo) + (warp * rows + r) * 4;
+                *reinterpret_cast<float4 *>(dh) = make_float4(vh[0], vh[1], vh[2], vh[3]);
+                *reinterpret_cast<float4 *>(dl) = make_float4(vl[0], vl[1], vl[2], vl[3]);
+            }
+            fence_proxy_async();  // generic-proxy smem writes -> visible to the tensor core
+            __syncthreads();
+            if (tid == 0) {
+                tc_fence_after();
+                const uint32_t base = stage_saddr + s * TC_STAGE_BYTES;
+                const uint32_t aH = base, aL = base + TC_A_BYTES, bH = base + 2 * TC_A_BYTES,
+                               bL = bH + TC_B_BYTES;
+#pragma unroll
+                for (int j = 0; j < TC_KC / 8; ++j) {  // K = 8 tf32 per MMA = 2 k-blocks
+                    const uint32_t oa = j * 2 * (TC_M * 16), ob = j * 2 * (TC_N * 16);
+                    const uint32_t acc0 = (chunk > 0 || j > 0) ? 1u : 0u;
+                    // LBO = distance between the two 4-element k-blocks, SBO = 8 rows x 16 B
+                    tc_mma(tmem, umma_desc(aH + oa, TC_M * 16, 128), umma_desc(bH + ob, TC_N * 16, 128), acc0);
+                    tc_mma(tmem, umma_desc(aH + oa, TC_M * 16, 128), umma_desc(bL + ob, TC_N * 16, 128), 1u);
+                    tc_mma(tmem, umma_desc(aL + oa, TC_M * 16, 128), umma_desc(bH + ob, TC_N * 16, 128), 1u);
+                }
+                tc_commit(&s_empty[s]);
+            }
+        }
+    });
+
+    const int n_chunks = chunk;
+    if (n_chunks > 0) {
+        const int s = (n_chunks - 1) & 1;
+        mbar_wait(&s_empty[s], ((n_chunks - 1) >> 1) & 1);  // last MMAs (and all before) done
+    }
+    tc_fence_after();
+
+    // ---- epilogue: warp w reads TMEM lanes 32 (w % 4) .. +31 (= tile rows), columns half w / 4
+    const int q = warp & 3, half = warp >> 2;
+    const int i = t_m * TC_M + q * 32 + lane;
+    const int64_t cells = (int64_t)a.n0 * a.n1;
+    float *out = a.R + (int64_t)e * cells + (int64_t)i * a.n1;
+#pragma unroll 1
+    for (int cc = 0; cc < 8; ++cc) {
+        const int col = half * 128 + cc * 16;
+        uint32_t v[16];
+        if (n_chunks > 0) {
+            const uint32_t taddr = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)col;
+            asm volatile(
+                "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, "
+                "[%16];"
+                : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
+                  "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]),
+                  "=r"(v[14]), "=r"(v[15])
+                : "r"(taddr));
+            asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+        } else {
+#pragma unroll
+            for (int x = 0; x < 16; ++x) v[x] = 0u;
+        }
+        const int j0 = t_n * TC_N + col;
+        if (i < a.n0) {
+            if (j0 + 15 < a.n1 && (((uintptr_t)(out + j0)) & 15u) == 0) {
+#pragma unroll
+                for (int x = 0; x < 16; x += 4)
+                    *reinterpret_cast<float4 *>(out + j0 + x) =
+                        make_float4(__uint_as_float(v[x]), __uint_as_float(v[x + 1]), __uint_as_float(v[x + 2]),
+                                    __uint_as_float(v[x + 3]));
+            } else {
+#pragma unroll
+                for (int x = 0; x < 16; ++x)
+                    if (j0 + x < a.n1) out[j0 + x] = __uint_as_float(v[x]);
+            }
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 0)
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TC_TMEM_COLS));
+}
+
+int tensor_max_stage_hits() {
+    return (227 * 1024 - 2 * TC_STAGE_BYTES - 1024) / 16;  // hit slots left after the operand stages
+}
+
+template <bool ZREF>
+static cudaError_t launch_tc(const GridArgs &a0, int n_events, cudaStream_t stream) {
+    auto kern = grid_tensor_kernel<ZREF>;
+    GridArgs a = a0;
+    a.cap = min(a.cap, tensor_max_stage_hits()) & ~1;
+    const size_t smem = 2 * (size_t)TC_STAGE_BYTES + (size_t)a.cap * sizeof(float4);
+    cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (err != cudaSuccess) return err;
+    const long long tiles = (long long)((a.n0 + TC_M - 1) / TC_M) * ((a.n1 + TC_N - 1) / TC_N);
+    for (int e0 = 0; e0 < n_events; e0 += 65535) {
+        a.e_base = e0;
+        const int ne = min(65535, n_events - e0);
+        kern<<<dim3((unsigned)tiles, ne), 256, smem, stream>>>(a);
+        err = cudaGetLastError();
+        if (err != cudaSuccess) return err;
+    }
+    return cudaSuccess;
+}
+
+cudaError_t launch_grid_tensor(int model, const GridArgs &a, int n_events, cudaStream_t stream) {
+    if (n_events == 0) return cudaSuccess;
+    if (model != kSlope2) return cudaErrorInvalidValue;
+    return (a.z_ref == 0.f) ? launch_tc<false>(a, n_events, stream) : launch_tc<true>(a, n_events, stream);
+}
+
+}  // namespace retina

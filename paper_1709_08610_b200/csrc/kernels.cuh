@@ -65,6 +65,7 @@ struct MergeArgs {
 
 cudaError_t launch_grid_response(int model, const GridArgs &a, int n_events, cudaStream_t stream);
 cudaError_t launch_grid_separable(int model, const GridArgs &a, int n_events, cudaStream_t stream);
+cudaError_t launch_grid_tensor(int model, const GridArgs &a, int n_events, cudaStream_t stream);
 cudaError_t launch_multistart(int model, const MultistartArgs &a, int n_events, cudaStream_t stream);
 cudaError_t launch_find_peaks(const PeakArgs &a, int n_events, cudaStream_t stream);
 cudaError_t launch_merge(const MergeArgs &a, int n_events, cudaStream_t stream);

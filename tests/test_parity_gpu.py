@@ -353,3 +353,58 @@ def test_direct_and_separable_agree_cfg3_batch():
         idx, _, cnt = R.retina_find_peaks(dev(gs[e:e + 1]), 2, 2.5, 4096)
         ok, nd, ne = PU.t4_peak_sets(idx.cpu().numpy()[0], int(cnt[0]), gd[e].astype(np.float64), 2, 2.5, 4096)
         assert ok, (nd, ne)
+
+
+# --------------------------------------------------------------------------- tensor-core grid (SLOPE2)
+TENSOR = R.retina.GRID_TENSOR
+
+
+def test_T1_tensor_grid_cfg1_full():
+    cfg = C.CFG1
+    b = G.make_batch(cfg, [0])
+    nodes = G.axis_nodes(cfg)
+    g = gpu_grid(b, cfg, nodes, algo=TENSOR)
+    ref = ora.grid(cfg.model, b.offsets, b.hits, nodes, cfg.sigma)
+    ok, worst = PU.t1_response(g, ref)
+    assert ok, worst
+
+
+@pytest.mark.parametrize("z_ref,shape", [(0.0, (37, 70)), (-12.345, (41, 33)), (0.0, (130, 300)),
+                                         (0.0, (256, 512))])
+@pytest.mark.parametrize("hint", [True, False])
+def test_T1_tensor_grid_ragged_edges(z_ref, shape, hint):
+    b = synthetic_batch(C.SLOPE2, [700, 0, 1, 5000, 37, 33], seed=3)
+    nodes = [np.linspace(-0.3, 0.3, n).astype(np.float32) for n in shape]
+    cfg = C.Config(name="t", model=C.SLOPE2, n_events=6, seed=0, n_tracks=0, sigma=0.44)
+    g = gpu_grid(b, cfg, nodes, z_ref=z_ref, hint=hint, algo=TENSOR)
+    ref = ora.grid(C.SLOPE2, b.offsets, b.hits, nodes, 0.44, z_ref=z_ref)
+    assert np.all(g[1] == 0.0)
+    ok, worst = PU.t1_response(g, ref)
+    assert ok, worst
+
+
+def test_T1_tensor_grid_cfg3_full_size_sampled():
+    cfg = C.CFG3
+    b = G.make_batch(cfg, [0, 5000, 9999])
+    nodes = G.axis_nodes(cfg)
+    g = gpu_grid(b, cfg, nodes, algo=TENSOR)
+    rng = np.random.default_rng(9)
+    pick = [np.unique(np.concatenate([np.sort(rng.choice(len(n), 48, replace=False)), [0, len(n) - 1]]))
+            for n in nodes]
+    ref = ora.grid(cfg.model, b.offsets, b.hits, [n[p] for n, p in zip(nodes, pick)], cfg.sigma)
+    ok, worst = PU.t1_response(g[(slice(None),) + np.ix_(*pick)], ref)
+    assert ok, worst
+
+
+def test_tensor_vs_separable_cfg3_batch_and_peaks():
+    cfg = C.CFG3
+    b = G.make_batch(cfg, range(32))
+    nodes = G.axis_nodes(cfg)
+    gt = gpu_grid(b, cfg, nodes, algo=TENSOR)
+    gs = gpu_grid(b, cfg, nodes, algo=R.retina.GRID_SEPARABLE)
+    err = np.abs(gt.astype(np.float64) - gs) / (2e-5 * np.maximum(gs, 1e-6))
+    assert err.max() <= 1.0, err.max()
+    for e in (0, 17, 31):
+        idx, _, cnt = R.retina_find_peaks(dev(gt[e:e + 1]), 2, 2.5, 4096)
+        ok, nd, ne = PU.t4_peak_sets(idx.cpu().numpy()[0], int(cnt[0]), gs[e].astype(np.float64), 2, 2.5, 4096)
+        assert ok, (nd, ne)
