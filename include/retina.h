@@ -122,6 +122,21 @@ int retina_find_peaks(const float *response, int32_t n_events, int32_t P,
                       int32_t *peak_index, float *peak_value, int32_t *peak_count,
                       void *stream);
 
+/* Step (iv), "for each cluster estimate track parameters" (Z21):
+ * for every listed peak, per axis i, the vertex of the parabola through the peak cell and its
+ * two neighbours along i,
+ *     delta = (R- - R+) / (2 (R- - 2 R0 + R+)),  theta_i = node_i[c_i] + delta (node_i[c_i+1] - node_i[c_i-1]) / 2,
+ * falling back to the cell centre on the lattice boundary (a neighbour missing) or when the
+ * curvature is not negative; |delta| <= 1/2 (a strict maximum keeps the vertex in its cell).
+ *   response:    device fp32 grid, as given to retina_find_peaks.
+ *   axis_len, axis_nodes: as in retina_grid_response (host arrays; device node tables).
+ *   peak_index, peak_count, capacity: the outputs of retina_find_peaks.
+ *   peak_theta:  device fp32 [n_events][capacity][P]; entries >= min(count, capacity) untouched. */
+int retina_estimate_peaks(const float *response, int32_t n_events, int32_t P,
+                          const int32_t *axis_len, const float *const *axis_nodes,
+                          const int32_t *peak_index, const int32_t *peak_count, int32_t capacity,
+                          float *peak_theta, void *stream);
+
 /* Algorithm 1 update loop with update = fixed-step gradient ascent clamped to the prior
  * box (Z7).  For every (event e, seed i):
  *     theta^0 = seeds[e][i];  theta^{j+1} = clamp(theta^j + step * grad R(theta^j)),

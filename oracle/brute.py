@@ -42,3 +42,22 @@ def gradient(model, hits, theta, sigma, z_ref=0.0):
             return mp.fsum(mp.exp(-_s2(model, h, th, z_ref) / (sg * sg)) for h in hits)
         out.append(mp.diff(f, mp.mpf(float(theta[i]))))
     return out
+
+
+def hessian(model, hits, theta, sigma, z_ref=0.0):
+    """Second partial derivatives of Eq. (1) by mpmath numerical differentiation."""
+    P = len(theta)
+    sg = mp.mpf(float(sigma))
+
+    def f(*t):
+        return mp.fsum(mp.exp(-_s2(model, h, list(t), z_ref) / (sg * sg)) for h in hits)
+
+    x0 = [mp.mpf(float(v)) for v in theta]
+    H = [[None] * P for _ in range(P)]
+    for a in range(P):
+        for b in range(P):
+            orders = [0] * P
+            orders[a] += 1
+            orders[b] += 1
+            H[a][b] = mp.diff(f, x0, tuple(orders))
+    return H

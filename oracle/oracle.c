@@ -256,3 +256,196 @@ void ora_merge(int n_events, int n_seeds, int P, const double *theta, const doub
         free(size);
     }
 }
+
+/* Step (iv) ("for each cluster estimate track parameters"), reading Z21
+ * (SPEC.md:292-300): per peak and per axis, the vertex of the parabola through the values at
+ * the peak cell and its two neighbours along that axis, in units of the local half-spacing
+ * (node[c+1] - node[c-1]) / 2; the cell centre when a neighbour is missing (lattice
+ * boundary) or the three points are not strictly concave.  The vertex of a parabola through
+ * (-1, a), (0, b), (1, c) is at (a - c) / (2 (a - 2 b + c)). */
+void ora_estimate(const double *grid, int n_events, int P, const int32_t *axis_len, const float *nodes0,
+                  const float *nodes1, const float *nodes2, const int32_t *peak_index,
+                  const int32_t *peak_count, int capacity, double *theta) {
+    const int64_t n[3] = {axis_len[0], axis_len[1], P == 3 ? axis_len[2] : 1};
+    const int64_t per_event = n[0] * n[1] * n[2];
+    const int64_t stride[3] = {n[1] * n[2], n[2], 1};
+    const float *nodes[3] = {nodes0, nodes1, nodes2};
+    for (int e = 0; e < n_events; ++e) {
+        const int cnt = peak_count[e] < capacity ? peak_count[e] : capacity;
+        for (int p = 0; p < cnt; ++p) {
+            const int64_t c = peak_index[(int64_t)e * capacity + p];
+            const int64_t ci[3] = {c / stride[0], (c / stride[1]) % n[1], c % n[2]};
+            const double *g = grid + e * per_event;
+            for (int i = 0; i < P; ++i) {
+                double t = nodes[i][ci[i]];
+                if (ci[i] > 0 && ci[i] < n[i] - 1) {
+                    const double a = g[c - stride[i]], b = g[c], cc = g[c + stride[i]];
+                    const double den = 2.0 * (a - 2.0 * b + cc);
+                    if (den < 0.0) {
+                        double delta = (a - cc) / den;
+                        if (delta > 0.5) delta = 0.5;
+                        if (delta < -0.5) delta = -0.5;
+                        t += delta * 0.5 * ((double)nodes[i][ci[i] + 1] - (double)nodes[i][ci[i] - 1]);
+                    }
+                }
+                theta[((int64_t)e * capacity + p) * P + i] = t;
+            }
+        }
+    }
+}
+
+/* ------------------------------------------------------------------------------------------
+ * NEXT #1: the paper's own update: Truncated Newton steps on R with the
+ * Hessian (Algorithm 1 line "compute response R, gradient grad R and Hessian H R",
+ * PAPER.md:150) and a per-step bandwidth schedule sigma_1..sigma_q.
+ *
+ * R, gradient and Hessian at one theta, by the chain rule through f = s^2 / sigma^2 with the
+ * residual vector r(theta) = (s) (LINE2D) or (s_x, s_y) (SLOPE2/3):
+ *     t_k = exp(-f_k),  d_a f = (2/sigma^2) sum_c r_c d_a r_c,
+ *     d_ab f = (2/sigma^2) sum_c (d_a r_c d_b r_c + r_c d_ab r_c),
+ *     dR/d_a = -sum_k t_k d_a f_k,   H_ab = sum_k t_k (d_a f_k d_b f_k - d_ab f_k).
+ * Residual derivatives: LINE2D r = y - a x - b: dr = (-x, -1).  SLOPE2 r = (x - tx d, y - ty d),
+ * d = z - z_ref: d r_x/d tx = -d, d r_y/d ty = -d.  SLOPE3 d = z - z0: additionally
+ * d r_x/d z0 = tx, d r_y/d z0 = ty, d2 r_x/(d tx d z0) = 1, d2 r_y/(d ty d z0) = 1.
+ * H is row-major P x P; grad, H may be NULL. */
+void ora_point_hess(int model, const float *hits, int n, double z_ref, const double *theta, double sigma,
+                    double *R_out, double *grad, double *H) {
+    const int P = model_P(model);
+    const double c = 2.0 / (sigma * sigma);
+    double R = 0.0, g[3] = {0, 0, 0}, h[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
+    for (int k = 0; k < n; ++k) {
+        const double x = hits[4 * k + 0], y = hits[4 * k + 1], z = hits[4 * k + 2];
+        double r[2] = {0, 0}, J[2][3] = {{0, 0, 0}, {0, 0, 0}}, K2[2][3][3];
+        memset(K2, 0, sizeof(K2));
+        int nr;
+        if (model == ORA_LINE2D) {
+            nr = 1;
+            r[0] = y - (theta[0] * x + theta[1]);
+            J[0][0] = -x;
+            J[0][1] = -1.0;
+        } else {
+            nr = 2;
+            const double d = (model == ORA_SLOPE3) ? z - theta[2] : z - z_ref;
+            r[0] = x - theta[0] * d;
+            r[1] = y - theta[1] * d;
+            J[0][0] = -d;
+            J[1][1] = -d;
+            if (model == ORA_SLOPE3) {
+                J[0][2] = theta[0];
+                J[1][2] = theta[1];
+                K2[0][0][2] = K2[0][2][0] = 1.0;
+                K2[1][1][2] = K2[1][2][1] = 1.0;
+            }
+        }
+        double f = 0.0;
+        for (int q = 0; q < nr; ++q) f += r[q] * r[q];
+        f /= sigma * sigma;
+        const double t = exp(-f);
+        double df[3] = {0, 0, 0};
+        for (int a = 0; a < P; ++a)
+            for (int q = 0; q < nr; ++q) df[a] += c * r[q] * J[q][a];
+        R += t;
+        for (int a = 0; a < P; ++a) {
+            g[a] -= t * df[a];
+            for (int b = 0; b < P; ++b) {
+                double d2f = 0.0;
+                for (int q = 0; q < nr; ++q) d2f += c * (J[q][a] * J[q][b] + r[q] * K2[q][a][b]);
+                h[a * 3 + b] += t * (df[a] * df[b] - d2f);
+            }
+        }
+    }
+    *R_out = R;
+    for (int a = 0; a < P; ++a) {
+        if (grad) grad[a] = g[a];
+        if (H)
+            for (int b = 0; b < P; ++b) H[a * P + b] = h[a * 3 + b];
+    }
+}
+
+/* Truncated-Newton direction for MAXIMISING R (reading Z23): conjugate gradients on
+ * (-H) p = g, at most P iterations (exact for a positive-definite -H), stopped at a direction
+ * of non-positive curvature d^T (-H) d <= 0: the iterate built so far is kept, or, at the first
+ * iteration, the fixed-step gradient direction p = eta g (reading Z24). */
+static void tn_direction(int P, const double *g, const double *H, double eta, double *p) {
+    double x[3] = {0, 0, 0}, r[3], d[3], Ad[3];
+    double rr = 0.0;
+    for (int a = 0; a < P; ++a) {
+        r[a] = g[a];
+        d[a] = g[a];
+        rr += g[a] * g[a];
+    }
+    const double rr0 = rr;
+    int it;
+    for (it = 0; it < P && rr > 0.0; ++it) {
+        double curv = 0.0;
+        for (int a = 0; a < P; ++a) {
+            Ad[a] = 0.0;
+            for (int b = 0; b < P; ++b) Ad[a] -= H[a * P + b] * d[b];
+            curv += d[a] * Ad[a];
+        }
+        if (!(curv > 0.0)) {
+            if (it == 0)
+                for (int a = 0; a < P; ++a) x[a] = eta * g[a];
+            break;
+        }
+        const double alpha = rr / curv;
+        double rr_new = 0.0;
+        for (int a = 0; a < P; ++a) {
+            x[a] += alpha * d[a];
+            r[a] -= alpha * Ad[a];
+            rr_new += r[a] * r[a];
+        }
+        if (rr_new <= 1e-24 * rr0) break;
+        const double beta = rr_new / rr;
+        for (int a = 0; a < P; ++a) d[a] = r[a] + beta * d[a];
+        rr = rr_new;
+    }
+    for (int a = 0; a < P; ++a) p[a] = x[a];
+}
+
+/* Algorithm 1 with update[.] = one Truncated-Newton step per
+ * optimisation step j = 1..q at bandwidth sigma_j, with Armijo
+ * backtracking on R (reading Z25: c1 = 1e-4, alpha = 1, 1/2, ..., at most max_halvings
+ * halvings; theta is clamped to the prior box at every trial; no accepted trial leaves theta
+ * unchanged).  Returns theta^q, R(theta^q) and grad R(theta^q) at final_sigma. */
+void ora_newton(int model, int n_events, const int32_t *offsets, const float *hits, double z_ref, int n_seeds,
+                const float *seeds, int n_steps, const double *sigmas, const double *etas, double final_sigma,
+                int max_halvings, const double *box_lo, const double *box_hi, double *theta_out,
+                double *R_out, double *grad_out) {
+    const int P = model_P(model);
+#pragma omp parallel for collapse(2) schedule(dynamic, 16)
+    for (int64_t e = 0; e < n_events; ++e) {
+        for (int64_t s = 0; s < n_seeds; ++s) {
+            const float *h = hits + 4 * (int64_t)offsets[e];
+            const int n = offsets[e + 1] - offsets[e];
+            const int64_t id = e * n_seeds + s;
+            double th[3] = {0, 0, 0}, g[3], H[9], p[3], R0, Rt, tt[3];
+            for (int a = 0; a < P; ++a) th[a] = seeds[id * P + a];
+            for (int j = 0; j < n_steps; ++j) {
+                ora_point_hess(model, h, n, z_ref, th, sigmas[j], &R0, g, H);
+                tn_direction(P, g, H, etas[j], p);
+                double slope = 0.0;
+                for (int a = 0; a < P; ++a) slope += g[a] * p[a];
+                double alpha = 1.0;
+                for (int k = 0; k <= max_halvings; ++k, alpha *= 0.5) {
+                    for (int a = 0; a < P; ++a) {
+                        double v = th[a] + alpha * p[a];
+                        if (v < box_lo[a]) v = box_lo[a];
+                        if (v > box_hi[a]) v = box_hi[a];
+                        tt[a] = v;
+                    }
+                    ora_point_hess(model, h, n, z_ref, tt, sigmas[j], &Rt, NULL, NULL);
+                    if (Rt >= R0 + 1e-4 * alpha * slope) {
+                        for (int a = 0; a < P; ++a) th[a] = tt[a];
+                        break;
+                    }
+                }
+            }
+            ora_point_hess(model, h, n, z_ref, th, final_sigma, &R0, g, NULL);
+            for (int a = 0; a < P; ++a) theta_out[id * P + a] = th[a];
+            R_out[id] = R0;
+            if (grad_out)
+                for (int a = 0; a < P; ++a) grad_out[id * P + a] = g[a];
+        }
+    }
+}

@@ -43,7 +43,11 @@ def lib():
         L.ora_peaks.argtypes = [P, i, i, P, d, i, P, P, P]
         L.ora_multistart.argtypes = [i, i, P, P, d, d, i, P, i, d, P, P, P, P, P]
         L.ora_merge.argtypes = [i, i, i, P, P, P, d, i, P, P, P, P, P]
-        for f in (L.ora_point, L.ora_grid, L.ora_peaks, L.ora_multistart, L.ora_merge):
+        L.ora_estimate.argtypes = [P, i, i, P, P, P, P, P, P, i, P]
+        L.ora_point_hess.argtypes = [i, P, i, d, P, d, P, P, P]
+        L.ora_newton.argtypes = [i, i, P, P, d, i, P, i, P, P, d, i, P, P, P, P, P]
+        for f in (L.ora_point, L.ora_grid, L.ora_peaks, L.ora_multistart, L.ora_merge, L.ora_estimate,
+                  L.ora_point_hess, L.ora_newton):
             f.restype = None
         _lib = L
     return _lib
@@ -144,3 +148,50 @@ def merge(theta, R, radius, threshold: float, capacity: int):
     lib().ora_merge(E, S, P, _p(th), _p(r), _p(rad), _f(threshold), int(capacity),
                     _p(tt), _p(tr), _p(ts), _p(tz), _p(tc))
     return tt[:, :capacity], tr[:, :capacity], ts[:, :capacity], tz[:, :capacity], tc
+
+
+def estimate(grid_values, nodes: Sequence[np.ndarray], peak_index, peak_count, capacity: int):
+    """Step (iv) quadratic sub-cell estimate (reading Z21): float64 [E, capacity, P]."""
+    g = np.ascontiguousarray(np.asarray(grid_values, np.float64))
+    E = g.shape[0]
+    P = g.ndim - 1
+    nd = [_f32(n) for n in nodes]
+    alen = np.array([len(n) for n in nd], np.int32)
+    idx = np.ascontiguousarray(np.asarray(peak_index, np.int32))
+    cnt = np.ascontiguousarray(np.asarray(peak_count, np.int32))
+    out = np.zeros((E, max(capacity, 1), P))
+    lib().ora_estimate(_p(g), E, P, _p(alen), _p(nd[0]), _p(nd[1]), _p(nd[2]) if P == 3 else None,
+                       _p(idx), _p(cnt), int(capacity), _p(out))
+    return out[:, :capacity]
+
+
+def point_hess(model: int, hits, theta, sigma: float, z_ref: float = 0.0):
+    """R, grad R and the Hessian (P x P) at one theta (chain rule through s^2; oracle.c)."""
+    h = _f32(hits).reshape(-1, 4)
+    th = np.ascontiguousarray(np.asarray(theta, np.float64))
+    P = _P(model)
+    R = np.zeros(1)
+    g = np.zeros(P)
+    H = np.zeros((P, P))
+    lib().ora_point_hess(model, _p(h), len(h), _f(z_ref), _p(th), _f(sigma), _p(R), _p(g), _p(H))
+    return float(R[0]), g, H
+
+
+def newton(model: int, offsets, hits, seeds, sigmas, etas, final_sigma: float, max_halvings: int,
+           box_lo, box_hi, z_ref: float = 0.0, want_grad: bool = True):
+    """Algorithm 1 with Truncated-Newton updates and a sigma schedule (readings Z22-Z25)."""
+    off = np.ascontiguousarray(np.asarray(offsets, np.int32))
+    h = _f32(hits).reshape(-1, 4)
+    sd = _f32(seeds)
+    E, S, P = sd.shape
+    sg = np.ascontiguousarray(np.asarray(sigmas, np.float32).astype(np.float64))
+    et = np.ascontiguousarray(np.asarray(etas, np.float32).astype(np.float64))
+    assert len(sg) == len(et)
+    lo = np.ascontiguousarray(np.asarray(box_lo, np.float32).astype(np.float64))
+    hi = np.ascontiguousarray(np.asarray(box_hi, np.float32).astype(np.float64))
+    th = np.zeros((E, S, P))
+    R = np.zeros((E, S))
+    g = np.zeros((E, S, P)) if want_grad else None
+    lib().ora_newton(model, E, _p(off), _p(h), _f(z_ref), S, _p(sd), len(sg), _p(sg), _p(et), _f(final_sigma),
+                     int(max_halvings), _p(lo), _p(hi), _p(th), _p(R), _p(g))
+    return th, R, g

@@ -167,6 +167,42 @@ int retina_find_peaks(const float *response, int32_t n_events, int32_t P, const 
     return RETINA_OK;
 }
 
+int retina_estimate_peaks(const float *response, int32_t n_events, int32_t P, const int32_t *axis_len,
+                          const float *const *axis_nodes, const int32_t *peak_index, const int32_t *peak_count,
+                          int32_t capacity, float *peak_theta, void *stream) {
+    g_last_error[0] = 0;
+    if (n_events < 0) return fail(RETINA_EINVAL, "n_events < 0");
+    if (P != 2 && P != 3) return fail(RETINA_EINVAL, "P must be 2 or 3 (got %d)", P);
+    if (!axis_len || !axis_nodes) return fail(RETINA_EINVAL, "axis_len/axis_nodes is NULL");
+    if (capacity < 0) return fail(RETINA_EINVAL, "capacity < 0");
+    long long cells = 1;
+    for (int i = 0; i < P; ++i) {
+        if (axis_len[i] < 2) return fail(RETINA_EINVAL, "axis_len[%d] = %d < 2", i, axis_len[i]);
+        if (!axis_nodes[i]) return fail(RETINA_EINVAL, "axis_nodes[%d] is NULL", i);
+        cells *= axis_len[i];
+    }
+    if (cells > 0x7fffffffLL) return fail(RETINA_EUNSUPPORTED, "more than 2^31-1 cells per event");
+    if (n_events == 0 || capacity == 0) return RETINA_OK;
+    if (!response || !peak_index || !peak_count || !peak_theta) return fail(RETINA_EINVAL, "NULL device pointer");
+    retina::EstimateArgs a{};
+    a.R = response;
+    a.n0 = axis_len[0];
+    a.n1 = axis_len[1];
+    a.n2 = (P == 3) ? axis_len[2] : 1;
+    a.P = P;
+    a.n_events = n_events;
+    a.capacity = capacity;
+    a.idx = peak_index;
+    a.cnt = peak_count;
+    a.nodes0 = axis_nodes[0];
+    a.nodes1 = axis_nodes[1];
+    a.nodes2 = (P == 3) ? axis_nodes[2] : nullptr;
+    a.theta = peak_theta;
+    const cudaError_t err = retina::launch_estimate(a, (cudaStream_t)stream);
+    if (err != cudaSuccess) return cuda_fail(err, "retina_estimate_peaks");
+    return RETINA_OK;
+}
+
 int retina_multistart_optimize(const retina_events *ev, int model, float sigma, int32_t n_seeds,
                                const float *seeds, int32_t n_iters, float step, const float *box_lo,
                                const float *box_hi, float *theta_out, float *response_out,

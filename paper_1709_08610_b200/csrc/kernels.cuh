@@ -63,6 +63,19 @@ struct MergeArgs {
     int e_base;
 };
 
+struct EstimateArgs {
+    const float *R;
+    int n0, n1, n2;  // n2 = 1 for P = 2
+    int P;
+    int n_events;
+    int capacity;
+    const int32_t *idx;
+    const int32_t *cnt;
+    const float *nodes0, *nodes1, *nodes2;
+    float *theta;
+};
+
+cudaError_t launch_estimate(const EstimateArgs &a, cudaStream_t stream);
 cudaError_t launch_grid_response(int model, const GridArgs &a, int n_events, cudaStream_t stream);
 cudaError_t launch_grid_separable(int model, const GridArgs &a, int n_events, cudaStream_t stream);
 cudaError_t launch_grid_tensor(int model, const GridArgs &a, int n_events, cudaStream_t stream);

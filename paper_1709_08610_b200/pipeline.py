@@ -1,6 +1,7 @@
 """One GPU's pass of the whole hot path over an event batch.
 
-    S-A  grid AR (steps ii-iii):  retina_grid_response -> retina_find_peaks
+    S-A  grid AR (steps ii-iv):  retina_grid_response -> retina_find_peaks
+                                                   -> retina_estimate_peaks
     S-B  Algorithm 1:            retina_multistart_optimize -> retina_merge_tracks
 
 All arithmetic runs in libretina.so; this module only owns device buffers, slices the
@@ -76,6 +77,7 @@ class RetinaPipeline:
         self.peak_idx = torch.empty((E, spec.peak_capacity), dtype=torch.int32, device=self.device)
         self.peak_val = torch.empty((E, spec.peak_capacity), dtype=torch.float32, device=self.device)
         self.peak_cnt = torch.empty((E,), dtype=torch.int32, device=self.device)
+        self.peak_theta = torch.empty((E, spec.peak_capacity, spec.P), dtype=torch.float32, device=self.device)
         S = spec.n_seeds
         self.theta = torch.empty((E, S, P), dtype=torch.float32, device=self.device)
         self.resp = torch.empty((E, S), dtype=torch.float32, device=self.device)
@@ -114,9 +116,12 @@ class RetinaPipeline:
             R.retina_find_peaks(out, sp.P, sp.peak_threshold, sp.peak_capacity,
                                 out=(self.peak_idx[e0:e1], self.peak_val[e0:e1], self.peak_cnt[e0:e1]),
                                 stream=stream)
+            # step (iv): sub-cell parameter estimate of every peak
+            R.retina_estimate_peaks(out, self.nodes, self.peak_idx[e0:e1], self.peak_cnt[e0:e1],
+                                    out=self.peak_theta[e0:e1], stream=stream)
             if timer is not None:
                 timer.stop("peaks")
-            self.launches += 2
+            self.launches += 3
 
     def run_multistart(self, batch: DeviceBatch, stream=None, timer=None):
         sp = self.spec

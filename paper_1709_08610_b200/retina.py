@@ -21,7 +21,7 @@ MERGE_MAX_SEEDS = 16384
 
 GRID_AUTO, GRID_DIRECT, GRID_SEPARABLE, GRID_TENSOR = 0, 1, 2, 3
 
-EXPORTED = ("retina_grid_response", "retina_grid_response_ex", "retina_find_peaks", "retina_multistart_optimize",
+EXPORTED = ("retina_grid_response", "retina_grid_response_ex", "retina_estimate_peaks", "retina_find_peaks", "retina_multistart_optimize",
             "retina_merge_tracks", "retina_status_string", "retina_last_error", "retina_version")
 
 
@@ -53,10 +53,11 @@ def lib() -> ctypes.CDLL:
         L.retina_grid_response_ex.argtypes = [ctypes.POINTER(retina_events), ctypes.c_int, f32, vp, vp, vp,
                                               ctypes.c_int, vp]
         L.retina_find_peaks.argtypes = [vp, i32, i32, vp, f32, i32, vp, vp, vp, vp]
+        L.retina_estimate_peaks.argtypes = [vp, i32, i32, vp, vp, vp, vp, i32, vp, vp]
         L.retina_multistart_optimize.argtypes = [ctypes.POINTER(retina_events), ctypes.c_int, f32, i32, vp,
                                                  i32, f32, vp, vp, vp, vp, vp, vp]
         L.retina_merge_tracks.argtypes = [i32, i32, i32, vp, vp, vp, f32, i32, vp, vp, vp, vp, vp, vp]
-        for f in (L.retina_grid_response, L.retina_grid_response_ex, L.retina_find_peaks, L.retina_multistart_optimize,
+        for f in (L.retina_grid_response, L.retina_grid_response_ex, L.retina_find_peaks, L.retina_estimate_peaks, L.retina_multistart_optimize,
                   L.retina_merge_tracks):
             f.restype = ctypes.c_int
         L.retina_status_string.argtypes = [ctypes.c_int]
@@ -156,6 +157,23 @@ def retina_find_peaks(response: torch.Tensor, P: int, threshold: float, capacity
            lib().retina_find_peaks(_ptr(response), E, P, alen, float(threshold), int(capacity),
                                    _ptr(idx), _ptr(val), _ptr(cnt), _stream(stream)))
     return idx, val, cnt
+
+
+def retina_estimate_peaks(response: torch.Tensor, nodes: Sequence[torch.Tensor], peak_index: torch.Tensor,
+                          peak_count: torch.Tensor, out: Optional[torch.Tensor] = None, stream=None) -> torch.Tensor:
+    """Step (iv): per-peak quadratic sub-cell estimate, fp32 [E, capacity, P]."""
+    _dev(response, torch.float32)
+    nodes = [_dev(n, torch.float32) for n in nodes]
+    P = len(nodes)
+    E, cap = peak_index.shape
+    alen, _k1 = _arr(ctypes.c_int32, [n.numel() for n in nodes])
+    nptr, _k2 = _arr(ctypes.c_void_p, [n.data_ptr() for n in nodes])
+    if out is None:
+        out = torch.zeros((E, cap, P), dtype=torch.float32, device=response.device)
+    _check("retina_estimate_peaks",
+           lib().retina_estimate_peaks(_ptr(response), E, P, alen, nptr, _ptr(_dev(peak_index, torch.int32)),
+                                       _ptr(_dev(peak_count, torch.int32)), int(cap), _ptr(out), _stream(stream)))
+    return out
 
 
 def retina_multistart_optimize(events: Events, model: int, sigma: float, seeds: torch.Tensor,

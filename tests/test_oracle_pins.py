@@ -402,3 +402,152 @@ def test_generator_shapes_and_sorting():
         if cfg.n_seeds:
             s = G.make_seeds(cfg, [0], n_seeds=100)
             assert np.all(s >= np.float32(np.array(cfg.box_lo))) and np.all(s <= np.float32(np.array(cfg.box_hi)))
+
+
+# ---------------------------------------------------------------- P14 step (iv)
+@pytest.mark.parametrize("P", [2, 3])
+def test_P14_estimate_exact_on_quadratics(P):
+    """3-point quadratic interpolation is exact on a parabola: a quadratic bump centred between
+    nodes is recovered to rounding, per axis, in parameter units."""
+    rng = np.random.default_rng(40 + P)
+    shape = (21, 17, 13)[:P]
+    nodes = [np.linspace(-0.3, 0.3, n).astype(np.float32) for n in shape]
+    for trial in range(10):
+        c = [int(rng.integers(2, n - 2)) for n in shape]
+        off = rng.uniform(-0.45, 0.45, P)
+        curv = rng.uniform(0.5, 3.0, P)
+        grids = np.meshgrid(*[np.arange(n, dtype=np.float64) for n in shape], indexing="ij")
+        g = 100.0 - sum(curv[i] * (grids[i] - (c[i] + off[i])) ** 2 for i in range(P))
+        idx, _, cnt = ora.peaks(g[None], P, 0.0, 16)
+        assert cnt[0] == 1 and idx[0, 0] == np.ravel_multi_index(c, shape)
+        th = ora.estimate(g[None], nodes, idx, cnt, 16)[0, 0]
+        for i in range(P):
+            step = float(nodes[i][c[i] + 1]) - float(nodes[i][c[i]])
+            truth = float(nodes[i][c[i]]) + off[i] * 0.5 * (float(nodes[i][c[i] + 1]) - float(nodes[i][c[i] - 1]))
+            assert abs(th[i] - truth) <= 1e-9 * abs(step), (i, th[i], truth)
+
+
+def test_P14_estimate_centre_boundary_and_single_track():
+    nodes = [np.linspace(-0.3, 0.3, 31).astype(np.float32)] * 2
+    g = np.zeros((31, 31))
+    g[10, 12] = 5.0
+    g[9, 12] = g[11, 12] = 2.0   # symmetric along axis 0
+    g[10, 11], g[10, 13] = 1.0, 1.0  # symmetric along axis 1
+    g[0, 5] = 4.0                # boundary peak along axis 0
+    g[1, 5] = 1.0
+    idx, _, cnt = ora.peaks(g[None], 2, 0.5, 8)
+    th = ora.estimate(g[None], nodes, idx, cnt, 8)[0]
+    k = {int(v): i for i, v in enumerate(idx[0, :cnt[0]])}
+    assert th[k[10 * 31 + 12]][0] == float(nodes[0][10]) and th[k[10 * 31 + 12]][1] == float(nodes[1][12])
+    assert th[k[0 * 31 + 5]][0] == float(nodes[0][0])  # falls back to the cell centre
+    # noiseless single track: the estimate is within half a step of the truth per axis and
+    # at least as close as the peak cell's node (PAPER.md:48 "maximal activation in the unit
+    # with pattern parameters closest to the tracks parameters")
+    cfg = C.CFG1
+    nd = G.axis_nodes(cfg)
+    tx, ty = 0.1234, -0.0567
+    rows = [(tx * z, ty * z, z) for z in C.VELO_PLANES[1:] if 5 < np.hypot(tx * z, ty * z) < 40]
+    h = h4(rows)
+    grid = ora.grid(C.SLOPE2, [0, len(h)], h, nd, cfg.sigma)
+    idx, _, cnt = ora.peaks(grid, 2, 2.5, 8)
+    assert cnt[0] == 1
+    th = ora.estimate(grid, nd, idx, cnt, 8)[0, 0]
+    i, j = np.unravel_index(idx[0, 0], grid.shape[1:])
+    step = float(nd[0][1] - nd[0][0])
+    assert abs(th[0] - tx) <= 0.5 * step and abs(th[1] - ty) <= 0.5 * step
+    assert abs(th[0] - tx) <= abs(float(nd[0][i]) - tx) + 1e-12
+    assert abs(th[1] - ty) <= abs(float(nd[1][j]) - ty) + 1e-12
+
+
+# ---------------------------------------------------------------- P15 Hessian (PAPER.md:128, 150)
+@pytest.mark.parametrize("model", [C.LINE2D, C.SLOPE2, C.SLOPE3])
+def test_P15_hessian_vs_mpmath_and_fd(model):
+    rng = np.random.default_rng(70 + model)
+    P = 3 if model == C.SLOPE3 else 2
+    for _ in range(4):
+        n = int(rng.integers(2, 8))
+        tt = np.array([rng.uniform(-0.3, 0.3), rng.uniform(-0.3, 0.3), rng.uniform(-20, 20)])[:P]
+        z = np.sort(rng.choice(C.VELO_PLANES[1:], n))
+        if model == C.LINE2D:
+            rows = [(float(xi), tt[0] * xi + tt[1] + rng.normal(0, 0.01)) for xi in rng.integers(1, 11, n)]
+            sigma = float(np.float32(0.05))
+        else:
+            d = z - (tt[2] if model == C.SLOPE3 else 0.0)
+            rows = [(tt[0] * di + rng.normal(0, .05), tt[1] * di + rng.normal(0, .05), zi) for di, zi in zip(d, z)]
+            sigma = float(np.float32(0.3))
+        h = h4(rows)
+        th = tt + rng.normal(0, [1e-3, 1e-3, 0.2][:P])
+        R, g, H = ora.point_hess(model, h, th, sigma)
+        Rp, gp, _ = ora.point(model, h, th, sigma)
+        assert abs(R - Rp) <= 1e-14 * R and np.allclose(g, gp, rtol=1e-12, atol=0)  # = ora_point
+        assert np.allclose(H, H.T, rtol=1e-12, atol=0)
+        Hb = np.array([[float(v) for v in row] for row in brute.hessian(model, h, th, sigma)])
+        scale = np.abs(Hb).max()
+        assert np.abs(H - Hb).max() <= 1e-9 * scale, (H, Hb)
+        # central differences of the (independently pinned) gradient
+        for a in range(P):
+            e = np.zeros(P)
+            e[a] = [1e-7, 1e-7, 1e-5][a]
+            fd = (ora.point(model, h, th + e, sigma)[1] - ora.point(model, h, th - e, sigma)[1]) / (2 * e[a])
+            assert np.abs(fd - H[:, a]).max() <= 1e-5 * scale
+
+
+# ---------------------------------------------------------------- P16 Truncated Newton (PAPER.md:213-216)
+def _velo_track_hits(t, z0=0.0, smear=0.0, seed=0):
+    rng = np.random.default_rng(seed)
+    rows = []
+    for z in C.VELO_PLANES:
+        if z <= z0:
+            continue
+        x, y = t[0] * (z - z0), t[1] * (z - z0)
+        if 5 < np.hypot(x, y) < 40:
+            rows.append((x + rng.normal(0, smear) if smear else x, y + rng.normal(0, smear) if smear else y, z))
+    return rows
+
+
+def test_P16_newton_converges_to_the_maximiser_found_by_scipy():
+    from scipy.optimize import minimize
+    rows = _velo_track_hits((0.11, -0.07), smear=0.012, seed=1) + _velo_track_hits((-0.2, 0.15), smear=0.012, seed=2)
+    rows.sort(key=lambda r: r[2])
+    h = h4(rows)
+    sig = float(np.float32(0.44))
+    res = minimize(lambda t: -ora.point(C.SLOPE2, h, t, sig)[0], x0=[0.1105, -0.0695],
+                   jac=lambda t: -ora.point(C.SLOPE2, h, t, sig)[1], method="BFGS",
+                   options={"gtol": 1e-12, "maxiter": 500})
+    seeds = np.array([[[0.1108, -0.0703], [0.1097, -0.0690]]], np.float32)
+    th, R, g = ora.newton(C.SLOPE2, [0, len(h)], h, seeds, [sig] * 4, [C.step_slope2(sig)] * 4, sig, 8,
+                          (-.3, -.3), (.3, .3))
+    for s in range(2):
+        assert np.abs(th[0, s] - res.x).max() <= 1e-9, (th[0, s], res.x)
+        assert R[0, s] >= -res.fun - 1e-12
+
+
+def test_P16_newton_ascent_identities_and_fallback():
+    cfg = C.CFG2
+    b = G.make_batch(cfg, [0])
+    seeds = G.make_seeds(cfg, [0], n_seeds=64)
+    sig = cfg.sigma
+    # n_steps = 0: identity
+    th, R, _ = ora.newton(cfg.model, b.offsets, b.hits, seeds, [], [], sig, 8, cfg.box_lo, cfg.box_hi)
+    assert np.array_equal(th, seeds.astype(np.float64))
+    # R is non-decreasing step by step at fixed sigma (Armijo acceptance or no move)
+    prev = np.array([ora.point(cfg.model, b.event_hits(0), s, sig)[0] for s in seeds[0].astype(np.float64)])
+    cur = seeds
+    for j in range(4):
+        th, R, _ = ora.newton(cfg.model, b.offsets, b.hits, cur, [sig], [cfg.step], sig, 8, cfg.box_lo, cfg.box_hi)
+        assert np.all(R[0] >= prev - 1e-12)
+        assert np.all(th >= np.float32(-0.3)) and np.all(th <= np.float32(0.3))
+        prev, cur = R[0], th.astype(np.float32)
+    # single hit far outside the Gaussian core: -H is not positive definite there, the first CG
+    # iteration falls back to the gradient direction, which points straight at the hit
+    x, y, d = 6.0, -3.0, 300.0
+    h = h4([(x, y, d)])
+    u = np.array([x, y]) / d
+    s0 = np.array([[[0.02 + 0.004, -0.01 + 0.003]]], np.float32)  # 1.5 mm = 1.5 sigma from the hit
+    sig1 = 1.0
+    Rh, gh, Hh = ora.point_hess(C.SLOPE2, h, s0[0, 0].astype(np.float64), sig1)
+    assert np.linalg.eigvalsh(-Hh).min() < 0  # indefinite: fallback path exercised
+    th, R, _ = ora.newton(C.SLOPE2, [0, 1], h, s0, [sig1], [C.step_slope2(sig1) * 50], sig1, 30, (-.3, -.3), (.3, .3))
+    v0, v1 = s0[0, 0].astype(float) - u, th[0, 0] - u
+    assert abs(v0[0] * v1[1] - v0[1] * v1[0]) <= 1e-9 * np.dot(v0, v0)
+    assert R[0, 0] > Rh

@@ -408,3 +408,33 @@ def test_tensor_vs_separable_cfg3_batch_and_peaks():
         idx, _, cnt = R.retina_find_peaks(dev(gt[e:e + 1]), 2, 2.5, 4096)
         ok, nd, ne = PU.t4_peak_sets(idx.cpu().numpy()[0], int(cnt[0]), gs[e].astype(np.float64), 2, 2.5, 4096)
         assert ok, (nd, ne)
+
+
+# --------------------------------------------------------------------------- step (iv) estimate
+@pytest.mark.parametrize("name,ev", [("cfg1", [0]), ("cfg3", [0, 1, 2]), ("cfg4", [0]), ("cfg0", [0])])
+def test_estimate_peaks_vs_oracle(name, ev):
+    cfg = C.CONFIGS[name]
+    b = G.make_batch(cfg, ev)
+    nodes = G.axis_nodes(cfg)
+    dnodes = [dev(n) for n in nodes]
+    grid = R.retina_grid_response(events_of(b), cfg.model, cfg.sigma, dnodes)
+    cap = cfg.peak_capacity
+    idx, val, cnt = R.retina_find_peaks(grid, cfg.P, cfg.peak_threshold, cap)
+    th = R.retina_estimate_peaks(grid, dnodes, idx, cnt)
+    torch.cuda.synchronize()
+    g64 = grid.cpu().numpy().astype(np.float64)
+    idx, cnt, th = idx.cpu().numpy(), cnt.cpu().numpy(), th.cpu().numpy()
+    ref = ora.estimate(g64, nodes, idx, cnt, cap)
+    steps = np.array([float(n[1] - n[0]) for n in nodes])
+    n_checked = 0
+    for e in range(len(ev)):
+        k = min(cnt[e], cap)
+        assert k > 0
+        err = np.abs(th[e, :k].astype(np.float64) - ref[e, :k]) / steps
+        assert err.max() <= 1e-3, err.max()  # fp32 vertex arithmetic vs fp64, in grid steps
+        # every estimate stays inside its peak's cell (|delta| <= 1/2)
+        cells = np.array(np.unravel_index(idx[e, :k], g64.shape[1:])).T
+        centre = np.stack([nodes[i][cells[:, i]] for i in range(cfg.P)], 1)
+        assert np.all(np.abs(th[e, :k] - centre) <= 0.5 * steps * (1 + 1e-5))
+        n_checked += k
+    assert n_checked > 0
