@@ -56,6 +56,8 @@ def args_():
     ap.add_argument("--e2e-steps", type=int, default=None)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample-events", type=int, default=3)
+    ap.add_argument("--update", default="gradient", choices=["gradient", "newton"],
+                    help="multi-start update: BASELINE fixed-step ascent, or the paper's Truncated Newton")
     return ap.parse_args()
 
 
@@ -191,10 +193,14 @@ def main():
     seeds = G.make_seeds(cfg, ev_ids)
     gen_s = time.perf_counter() - t0
     spec = make_spec(cfg)
+    if a.update == "newton":
+        spec.newton = C.newton_schedule(cfg)
     pipe = RetinaPipeline(spec, E, chunk_events=a.chunk_events)
     stream = torch.cuda.current_stream()
     dbatch = upload(batch.offsets, batch.hits, seeds)
     pairs_grid, pairs_ms = pipe.pairs(dbatch)
+    if a.update == "newton":  # lower bound: q Hessian passes + final pass (line-search trials not counted)
+        pairs_ms = pairs_ms / (cfg.n_iters + 1) * (len(spec.newton[0]) + 1)
     keep = 64
 
     def step(b, timer=None, t_ms=0.0):
@@ -322,7 +328,9 @@ def main():
         "events_per_s": E * world / (ms_step * 1e-3),
         "config": {"workload": f"{cfg.name}: BASELINE.json configs[3] Run-3-like batch, {E} events per GPU "
                                f"(ids rank*{E}..), 1024x1024 SLOPE2 grid + 3x3 peaks (R0={cfg.peak_threshold}), "
-                               f"{cfg.n_seeds} seeds x {cfg.n_iters} fixed-step iterations + merge",
+                               + (f"{cfg.n_seeds} seeds x {cfg.n_iters} fixed-step iterations + merge"
+                                  if a.update == "gradient" else
+                                  f"{cfg.n_seeds} seeds x q=3 Truncated-Newton steps (sigma schedule) + merge"),
                    "events_per_rank": E, "hits_per_event_mean": float(batch.n_hits) / E,
                    "pairs_grid_per_rank": pairs_grid, "pairs_multistart_per_rank": pairs_ms,
                    "l2": "inputs > L2 (hits %.0f MB, seeds %.0f MB, grid writes %.1f GB per step)" % (

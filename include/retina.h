@@ -156,6 +156,20 @@ int retina_multistart_optimize(const retina_events *ev, int model, float sigma,
                                float *theta_out, float *response_out, float *grad_out,
                                void *stream);
 
+/* Algorithm 1 with the paper's own update (Z22-Z25): q = n_steps
+ * Truncated-Newton steps, step j at bandwidth sigmas[j] with R, grad R and the Hessian H R from
+ * one pass over the hits, direction by conjugate gradients on (-H) p = grad R
+ * (<= P iterations; stopped at non-positive curvature, or p = etas[j] grad R at the first
+ * iteration), then backtracking alpha = 1, 1/2, ... (<= max_halvings halvings) accepting the
+ * first clamp(theta + alpha p) with R >= R(theta) + 1e-4 alpha grad R . p (else theta stays).
+ * Returns theta^q, R(theta^q) and grad R(theta^q) at final_sigma.  SLOPE2 / SLOPE3 only
+ * (RETINA_EUNSUPPORTED for LINE2D); n_steps <= 16.
+ *   sigmas, etas: host fp32 [n_steps]; other arguments as retina_multistart_optimize. */
+int retina_multistart_newton(const retina_events *ev, int model, int32_t n_seeds, const float *seeds,
+                             int32_t n_steps, const float *sigmas, const float *etas, float final_sigma,
+                             int32_t max_halvings, const float *box_lo, const float *box_hi,
+                             float *theta_out, float *response_out, float *grad_out, void *stream);
+
 /* Algorithm 1 "cluster solutions ... select highest response above R0" per event:
  *   keep seeds with response >= threshold; order them by (response descending, theta
  *   lexicographic ascending, seed index ascending); scan that order: a seed joins the

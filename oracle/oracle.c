@@ -366,8 +366,10 @@ void ora_point_hess(int model, const float *hits, int n, double z_ref, const dou
  * (-H) p = g, at most P iterations (exact for a positive-definite -H), stopped at a direction
  * of non-positive curvature d^T (-H) d <= 0: the iterate built so far is kept, or, at the first
  * iteration, the fixed-step gradient direction p = eta g (reading Z24). */
-static void tn_direction(int P, const double *g, const double *H, double eta, double *p) {
+static void tn_direction(int P, const double *g, const double *H, double eta, double *p, double *margin) {
     double x[3] = {0, 0, 0}, r[3], d[3], Ad[3];
+    double hs = 0.0;  /* scale of H for the curvature-decision margin (diagnostic only) */
+    for (int a = 0; a < P * P; ++a) hs = fabs(H[a]) > hs ? fabs(H[a]) : hs;
     double rr = 0.0;
     for (int a = 0; a < P; ++a) {
         r[a] = g[a];
@@ -382,6 +384,12 @@ static void tn_direction(int P, const double *g, const double *H, double eta, do
             Ad[a] = 0.0;
             for (int b = 0; b < P; ++b) Ad[a] -= H[a * P + b] * d[b];
             curv += d[a] * Ad[a];
+        }
+        {
+            double dd = 0.0;
+            for (int a = 0; a < P; ++a) dd += d[a] * d[a];
+            const double m = (dd > 0.0 && hs > 0.0) ? fabs(curv) / (dd * hs) : 1.0;
+            if (m < *margin) *margin = m;
         }
         if (!(curv > 0.0)) {
             if (it == 0)
@@ -407,11 +415,14 @@ static void tn_direction(int P, const double *g, const double *H, double eta, do
  * optimisation step j = 1..q at bandwidth sigma_j, with Armijo
  * backtracking on R (reading Z25: c1 = 1e-4, alpha = 1, 1/2, ..., at most max_halvings
  * halvings; theta is clamped to the prior box at every trial; no accepted trial leaves theta
- * unchanged).  Returns theta^q, R(theta^q) and grad R(theta^q) at final_sigma. */
+ * unchanged).  Returns theta^q, R(theta^q) and grad R(theta^q) at final_sigma.
+ * margin_out (nullable; diagnostic for the T5 near-tie rule, no effect on the result): per seed,
+ * the smallest relative margin of any discrete decision taken -- |R_t - (R_0 + c1 alpha g.p)| /
+ * R_0 for the Armijo tests and |d^T H d| / (|d|^2 max|H|) for the CG curvature tests. */
 void ora_newton(int model, int n_events, const int32_t *offsets, const float *hits, double z_ref, int n_seeds,
                 const float *seeds, int n_steps, const double *sigmas, const double *etas, double final_sigma,
                 int max_halvings, const double *box_lo, const double *box_hi, double *theta_out,
-                double *R_out, double *grad_out) {
+                double *R_out, double *grad_out, double *margin_out) {
     const int P = model_P(model);
 #pragma omp parallel for collapse(2) schedule(dynamic, 16)
     for (int64_t e = 0; e < n_events; ++e) {
@@ -419,11 +430,11 @@ void ora_newton(int model, int n_events, const int32_t *offsets, const float *hi
             const float *h = hits + 4 * (int64_t)offsets[e];
             const int n = offsets[e + 1] - offsets[e];
             const int64_t id = e * n_seeds + s;
-            double th[3] = {0, 0, 0}, g[3], H[9], p[3], R0, Rt, tt[3];
+            double th[3] = {0, 0, 0}, g[3], H[9], p[3], R0, Rt, tt[3], margin = 1.0;
             for (int a = 0; a < P; ++a) th[a] = seeds[id * P + a];
             for (int j = 0; j < n_steps; ++j) {
                 ora_point_hess(model, h, n, z_ref, th, sigmas[j], &R0, g, H);
-                tn_direction(P, g, H, etas[j], p);
+                tn_direction(P, g, H, etas[j], p, &margin);
                 double slope = 0.0;
                 for (int a = 0; a < P; ++a) slope += g[a] * p[a];
                 double alpha = 1.0;
@@ -435,6 +446,10 @@ void ora_newton(int model, int n_events, const int32_t *offsets, const float *hi
                         tt[a] = v;
                     }
                     ora_point_hess(model, h, n, z_ref, tt, sigmas[j], &Rt, NULL, NULL);
+                    {
+                        const double m = fabs(Rt - (R0 + 1e-4 * alpha * slope)) / (R0 > 1e-6 ? R0 : 1e-6);
+                        if (m < margin) margin = m;
+                    }
                     if (Rt >= R0 + 1e-4 * alpha * slope) {
                         for (int a = 0; a < P; ++a) th[a] = tt[a];
                         break;
@@ -446,6 +461,7 @@ void ora_newton(int model, int n_events, const int32_t *offsets, const float *hi
             R_out[id] = R0;
             if (grad_out)
                 for (int a = 0; a < P; ++a) grad_out[id * P + a] = g[a];
+            if (margin_out) margin_out[id] = margin;
         }
     }
 }

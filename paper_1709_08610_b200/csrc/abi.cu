@@ -246,6 +246,59 @@ int retina_multistart_optimize(const retina_events *ev, int model, float sigma, 
     return RETINA_OK;
 }
 
+int retina_multistart_newton(const retina_events *ev, int model, int32_t n_seeds, const float *seeds,
+                             int32_t n_steps, const float *sigmas, const float *etas, float final_sigma,
+                             int32_t max_halvings, const float *box_lo, const float *box_hi, float *theta_out,
+                             float *response_out, float *grad_out, void *stream) {
+    g_last_error[0] = 0;
+    int st = check_events(ev);
+    if (st) return st;
+    const int P = model_P(model);
+    if (P < 0) return fail(RETINA_EINVAL, "unknown model %d", model);
+    if (model == RETINA_LINE2D) return fail(RETINA_EUNSUPPORTED, "Newton update implemented for SLOPE2/SLOPE3");
+    if (n_seeds < 0) return fail(RETINA_EINVAL, "n_seeds < 0");
+    if (n_steps < 0) return fail(RETINA_EINVAL, "n_steps < 0");
+    if (n_steps > retina::kMaxNewtonSteps) return fail(RETINA_EUNSUPPORTED, "n_steps > %d", retina::kMaxNewtonSteps);
+    if (max_halvings < 0) return fail(RETINA_EINVAL, "max_halvings < 0");
+    if (n_steps > 0 && (!sigmas || !etas)) return fail(RETINA_EINVAL, "sigmas/etas is NULL");
+    for (int j = 0; j < n_steps; ++j) {
+        if (!finite_pos(sigmas[j])) return fail(RETINA_EINVAL, "sigmas[%d] must be finite and > 0", j);
+        if (!std::isfinite(etas[j])) return fail(RETINA_EINVAL, "etas[%d] is not finite", j);
+    }
+    if (!finite_pos(final_sigma)) return fail(RETINA_EINVAL, "final_sigma must be finite and > 0");
+    if (!box_lo || !box_hi) return fail(RETINA_EINVAL, "box_lo/box_hi is NULL");
+    for (int i = 0; i < P; ++i)
+        if (!(box_lo[i] <= box_hi[i])) return fail(RETINA_EINVAL, "box_lo[%d] > box_hi[%d]", i, i);
+    if (ev->n_events == 0 || n_seeds == 0) return RETINA_OK;
+    if (!seeds || !theta_out || !response_out) return fail(RETINA_EINVAL, "NULL device pointer");
+    retina::NewtonArgs a{};
+    a.offsets = ev->offsets;
+    a.hits = reinterpret_cast<const float4 *>(ev->hits);
+    a.z_ref = ev->z_ref;
+    a.n_seeds = n_seeds;
+    a.seeds = seeds;
+    a.n_steps = n_steps;
+    for (int j = 0; j < n_steps; ++j) {
+        a.negK[j] = neg_k(sigmas[j]);
+        a.c2[j] = c2_of(sigmas[j]);
+        a.eta[j] = etas[j];
+    }
+    a.final_negK = neg_k(final_sigma);
+    a.final_c2 = c2_of(final_sigma);
+    a.max_halvings = max_halvings;
+    for (int i = 0; i < 3; ++i) {
+        a.lo[i] = (i < P) ? box_lo[i] : 0.f;
+        a.hi[i] = (i < P) ? box_hi[i] : 0.f;
+    }
+    a.theta_out = theta_out;
+    a.R_out = response_out;
+    a.grad_out = grad_out;
+    a.cap = stage_cap(ev->max_event_hits, 4096);
+    const cudaError_t err = retina::launch_newton(model, a, ev->n_events, (cudaStream_t)stream);
+    if (err != cudaSuccess) return cuda_fail(err, "retina_multistart_newton");
+    return RETINA_OK;
+}
+
 int retina_merge_tracks(int32_t n_events, int32_t n_seeds, int32_t P, const float *theta,
                         const float *response, const float *radius, float threshold, int32_t capacity,
                         float *track_theta, float *track_response, int32_t *track_seed,

@@ -35,6 +35,26 @@ struct MultistartArgs {
     int e_base;
 };
 
+constexpr int kMaxNewtonSteps = 16;
+
+struct NewtonArgs {
+    const int32_t *offsets;
+    const float4 *hits;
+    float z_ref;
+    int n_seeds;
+    const float *seeds;
+    int n_steps;
+    float negK[kMaxNewtonSteps];  // -log2(e)/sigma_j^2
+    float c2[kMaxNewtonSteps];    // 2/sigma_j^2
+    float eta[kMaxNewtonSteps];   // gradient fallback step per optimisation step
+    float final_negK, final_c2;
+    int max_halvings;
+    float lo[3], hi[3];
+    float *theta_out, *R_out, *grad_out;
+    int cap;
+    int e_base;
+};
+
 struct PeakArgs {
     const float *R;
     int n0, n1, n2;  // n2 = 1 for P = 2
@@ -79,6 +99,7 @@ cudaError_t launch_estimate(const EstimateArgs &a, cudaStream_t stream);
 cudaError_t launch_grid_response(int model, const GridArgs &a, int n_events, cudaStream_t stream);
 cudaError_t launch_grid_separable(int model, const GridArgs &a, int n_events, cudaStream_t stream);
 cudaError_t launch_grid_tensor(int model, const GridArgs &a, int n_events, cudaStream_t stream);
+cudaError_t launch_newton(int model, const NewtonArgs &a, int n_events, cudaStream_t stream);
 cudaError_t launch_multistart(int model, const MultistartArgs &a, int n_events, cudaStream_t stream);
 cudaError_t launch_find_peaks(const PeakArgs &a, int n_events, cudaStream_t stream);
 cudaError_t launch_merge(const MergeArgs &a, int n_events, cudaStream_t stream);

@@ -1,0 +1,360 @@
+// newton.cu -- K6: the paper's own update (NEXT #1): Algorithm 1 with
+// update[.] = one Truncated-Newton step per optimisation step j = 1..q at bandwidth sigma_j,
+// using R, grad R and the Hessian H R computed in ONE pass over the hits.
+//
+// Per seed and step j (readings Z22-Z25, oracle.c ora_newton):
+//   R0, g, H = eval(theta, sigma_j)                                   (1 pass, Hessian mode)
+//   p = truncated CG on (-H) p = g, <= P iterations; non-positive curvature stops it, or at the
+//       first iteration falls back to p = eta_j g
+//   alpha = 1, 1/2, ... (<= max_halvings halvings): theta_t = clamp(theta + alpha p);
+//       accept the first theta_t with R(theta_t) >= R0 + 1e-4 alpha g.p  (1 R-only pass each;
+//       the CTA keeps passing while any of its seeds is still searching)
+// then R (and grad R) at final_sigma.
+//
+// Hessian accumulation (SLOPE2 / SLOPE3; A = s_x, B = s_y, c = 2/sigma^2, d = z - z_ref or z - z0):
+// per detector plane the loop sums W = sum w, wA, wB, wA^2, wAB, wB^2 (8 FMA-pipe ops per pair
+// on top of the residual/exponent), and at each plane change folds them into accumulators
+// weighted by 1, d and d^2, from which
+//   g_tx = c sum d wA,  g_ty = c sum d wB,  g_z0 = -c (tx sum wA + ty sum wB)
+//   H_txtx = c^2 sum d^2 wA^2 - c sum d^2 w,  H_tyty = c^2 sum d^2 wB^2 - c sum d^2 w,
+//   H_txty = c^2 sum d^2 wAB,
+//   H_txz0 = -c^2 (tx sum d wA^2 + ty sum d wAB) + c tx sum d w - c sum wA,
+//   H_tyz0 = -c^2 (tx sum d wAB + ty sum d wB^2) + c ty sum d w - c sum wB,
+//   H_z0z0 = c^2 (tx^2 sum wA^2 + 2 tx ty sum wAB + ty^2 sum wB^2) - c (tx^2 + ty^2) sum w.
+#include "common.cuh"
+#include "kernels.cuh"
+
+namespace retina {
+
+constexpr int kNtThreads = 128;
+
+// Plane-weighted sums for one seed.  Index: [0] w [1] wA [2] wB [3] wA2 [4] wAB [5] wB2.
+struct HessSums {
+    float p[6];    // current plane
+    float s1[6];   // weight 1 (s1[0] = R)
+    float sd[6];   // weight d
+    float sd2[6];  // weight d^2
+};
+
+template <int MODEL, int S, bool ZREF>
+__device__ __forceinline__ void nt_pass_hess(HitStage &st, const float (&th)[S][3], float negK, float zref,
+                                             HessSums (&hs)[S]) {
+#pragma unroll
+    for (int s = 0; s < S; ++s)
+#pragma unroll
+        for (int q = 0; q < 6; ++q) hs[s].p[q] = hs[s].s1[q] = hs[s].sd[q] = hs[s].sd2[q] = 0.f;
+    float dh[S], dl[S];
+#pragma unroll
+    for (int s = 0; s < S; ++s) dh[s] = dl[s] = 0.f;
+    float zprev = __int_as_float(0x7fc00000);
+    auto flush = [&]() {
+#pragma unroll
+        for (int s = 0; s < S; ++s) {
+            const float d = dh[s], d2 = __fmul_rn(dh[s], dh[s]);
+#pragma unroll
+            for (int q = 0; q < 6; ++q) {
+                hs[s].s1[q] = __fadd_rn(hs[s].s1[q], hs[s].p[q]);
+                hs[s].sd[q] = __fmaf_rn(d, hs[s].p[q], hs[s].sd[q]);
+                hs[s].sd2[q] = __fmaf_rn(d2, hs[s].p[q], hs[s].sd2[q]);
+                hs[s].p[q] = 0.f;
+            }
+        }
+    };
+    st.pass([&](const float4 *h, int len) {
+#pragma unroll 2
+        for (int k = 0; k < len; ++k) {
+            const float4 hk = h[k];
+            if (hk.z != zprev) {  // warp-uniform plane change
+                flush();
+                zprev = hk.z;
+#pragma unroll
+                for (int s = 0; s < S; ++s) {
+                    if (MODEL == kSlope3)
+                        two_sum(hk.z, -th[s][2], dh[s], dl[s]);
+                    else if (ZREF)
+                        two_sum(hk.z, -zref, dh[s], dl[s]);
+                    else {
+                        dh[s] = hk.z;
+                        dl[s] = 0.f;
+                    }
+                }
+            }
+#pragma unroll
+            for (int s = 0; s < S; ++s) {
+                float A, B;
+                if (MODEL == kSlope3 || ZREF) {
+                    A = __fmaf_rn(-th[s][0], dl[s], __fmaf_rn(-th[s][0], dh[s], hk.x));
+                    B = __fmaf_rn(-th[s][1], dl[s], __fmaf_rn(-th[s][1], dh[s], hk.y));
+                } else {
+                    A = __fmaf_rn(-th[s][0], hk.z, hk.x);
+                    B = __fmaf_rn(-th[s][1], hk.z, hk.y);
+                }
+                const float w = ex2_approx(__fmul_rn(__fmaf_rn(A, A, __fmul_rn(B, B)), negK));
+                const float wA = __fmul_rn(w, A), wB = __fmul_rn(w, B);
+                hs[s].p[0] = __fadd_rn(hs[s].p[0], w);
+                hs[s].p[1] = __fadd_rn(hs[s].p[1], wA);
+                hs[s].p[2] = __fadd_rn(hs[s].p[2], wB);
+                hs[s].p[3] = __fmaf_rn(wA, A, hs[s].p[3]);
+                hs[s].p[4] = __fmaf_rn(wA, B, hs[s].p[4]);
+                hs[s].p[5] = __fmaf_rn(wB, B, hs[s].p[5]);
+            }
+        }
+    });
+    flush();
+}
+
+// R only (line-search trials and the final pass); grad too when GRAD.
+template <int MODEL, int S, bool ZREF, bool GRAD>
+__device__ __forceinline__ void nt_pass_r(HitStage &st, const float (&th)[S][3], float negK, float zref,
+                                          float (&R)[S], float (&G)[S][4]) {
+#pragma unroll
+    for (int s = 0; s < S; ++s) {
+        R[s] = 0.f;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) G[s][q] = 0.f;
+    }
+    float dh[S], dl[S], qa[S], qb[S];
+#pragma unroll
+    for (int s = 0; s < S; ++s) dh[s] = dl[s] = qa[s] = qb[s] = 0.f;
+    float zprev = __int_as_float(0x7fc00000);
+    auto flush = [&]() {
+        if (!GRAD) return;
+#pragma unroll
+        for (int s = 0; s < S; ++s) {
+            G[s][0] = __fmaf_rn(dh[s], qa[s], G[s][0]);
+            G[s][1] = __fmaf_rn(dh[s], qb[s], G[s][1]);
+            G[s][2] = __fadd_rn(G[s][2], qa[s]);
+            G[s][3] = __fadd_rn(G[s][3], qb[s]);
+            qa[s] = qb[s] = 0.f;
+        }
+    };
+    st.pass([&](const float4 *h, int len) {
+#pragma unroll 2
+        for (int k = 0; k < len; ++k) {
+            const float4 hk = h[k];
+            if (hk.z != zprev) {
+                flush();
+                zprev = hk.z;
+#pragma unroll
+                for (int s = 0; s < S; ++s) {
+                    if (MODEL == kSlope3)
+                        two_sum(hk.z, -th[s][2], dh[s], dl[s]);
+                    else if (ZREF)
+                        two_sum(hk.z, -zref, dh[s], dl[s]);
+                    else {
+                        dh[s] = hk.z;
+                        dl[s] = 0.f;
+                    }
+                }
+            }
+#pragma unroll
+            for (int s = 0; s < S; ++s) {
+                float A, B;
+                if (MODEL == kSlope3 || ZREF) {
+                    A = __fmaf_rn(-th[s][0], dl[s], __fmaf_rn(-th[s][0], dh[s], hk.x));
+                    B = __fmaf_rn(-th[s][1], dl[s], __fmaf_rn(-th[s][1], dh[s], hk.y));
+                } else {
+                    A = __fmaf_rn(-th[s][0], hk.z, hk.x);
+                    B = __fmaf_rn(-th[s][1], hk.z, hk.y);
+                }
+                const float w = ex2_approx(__fmul_rn(__fmaf_rn(A, A, __fmul_rn(B, B)), negK));
+                R[s] = __fadd_rn(R[s], w);
+                if (GRAD) {
+                    qa[s] = __fmaf_rn(w, A, qa[s]);
+                    qb[s] = __fmaf_rn(w, B, qb[s]);
+                }
+            }
+        }
+    });
+    flush();
+}
+
+// Truncated CG on (-H) p = g (maximisation), <= P iterations, fallback eta g (oracle tn_direction).
+template <int P>
+__device__ __forceinline__ void nt_direction(const float (&g)[3], const float (&H)[3][3], float eta, float (&p)[3]) {
+    float x[3] = {0.f, 0.f, 0.f}, r[3], d[3], Ad[3];
+    float rr = 0.f;
+#pragma unroll
+    for (int a = 0; a < P; ++a) {
+        r[a] = g[a];
+        d[a] = g[a];
+        rr = __fmaf_rn(g[a], g[a], rr);
+    }
+    const float rr0 = rr;
+#pragma unroll
+    for (int it = 0; it < P; ++it) {
+        if (!(rr > 0.f)) break;
+        float curv = 0.f;
+#pragma unroll
+        for (int a = 0; a < P; ++a) {
+            float v = 0.f;
+#pragma unroll
+            for (int b = 0; b < P; ++b) v = __fmaf_rn(-H[a][b], d[b], v);
+            Ad[a] = v;
+            curv = __fmaf_rn(d[a], v, curv);
+        }
+        if (!(curv > 0.f)) {
+            if (it == 0) {
+#pragma unroll
+                for (int a = 0; a < P; ++a) x[a] = __fmul_rn(eta, g[a]);
+            }
+            break;
+        }
+        const float alpha = __fdiv_rn(rr, curv);
+        float rr_new = 0.f;
+#pragma unroll
+        for (int a = 0; a < P; ++a) {
+            x[a] = __fmaf_rn(alpha, d[a], x[a]);
+            r[a] = __fmaf_rn(-alpha, Ad[a], r[a]);
+            rr_new = __fmaf_rn(r[a], r[a], rr_new);
+        }
+        if (rr_new <= 1e-14f * rr0) break;
+        const float beta = __fdiv_rn(rr_new, rr);
+#pragma unroll
+        for (int a = 0; a < P; ++a) d[a] = __fmaf_rn(beta, d[a], r[a]);
+        rr = rr_new;
+    }
+#pragma unroll
+    for (int a = 0; a < 3; ++a) p[a] = (a < P) ? x[a] : 0.f;
+}
+
+template <int MODEL, int S, bool ZREF>
+__global__ void __launch_bounds__(kNtThreads) newton_kernel(NewtonArgs a) {
+    extern __shared__ __align__(16) float4 s_hits[];
+    __shared__ __align__(8) uint64_t s_bar[2];
+    constexpr int P = (MODEL == kSlope3) ? 3 : 2;
+
+    const int e = a.e_base + blockIdx.y;
+    const int start = a.offsets[e], nh = a.offsets[e + 1] - start;
+    HitStage st;
+    st.init(s_hits, s_bar, a.hits + start, nh, a.cap);
+
+    int sid[S];
+    float th[S][3];
+#pragma unroll
+    for (int s = 0; s < S; ++s) {
+        sid[s] = blockIdx.x * (kNtThreads * S) + s * kNtThreads + threadIdx.x;
+        const int64_t src = ((int64_t)e * a.n_seeds + min(sid[s], a.n_seeds - 1)) * P;
+#pragma unroll
+        for (int i = 0; i < 3; ++i) th[s][i] = (i < P) ? __ldg(a.seeds + src + i) : 0.f;
+    }
+
+    HessSums hs[S];
+    float R[S], G[S][4];
+    for (int j = 0; j < a.n_steps; ++j) {
+        const float c = a.c2[j], negK = a.negK[j];
+        nt_pass_hess<MODEL, S, ZREF>(st, th, negK, a.z_ref, hs);
+        float R0[S], p[S][3], slope[S], tt[S][3];
+        bool active[S];
+#pragma unroll
+        for (int s = 0; s < S; ++s) {
+            const float tx = th[s][0], ty = th[s][1];
+            const float c2 = __fmul_rn(c, c);
+            float g[3], H[3][3];
+            R0[s] = hs[s].s1[0];
+            const float *s1 = hs[s].s1, *sd = hs[s].sd, *sd2 = hs[s].sd2;
+            g[0] = __fmul_rn(c, sd[1]);
+            g[1] = __fmul_rn(c, sd[2]);
+            H[0][0] = __fmaf_rn(c2, sd2[3], -__fmul_rn(c, sd2[0]));
+            H[1][1] = __fmaf_rn(c2, sd2[5], -__fmul_rn(c, sd2[0]));
+            H[0][1] = H[1][0] = __fmul_rn(c2, sd2[4]);
+            if (MODEL == kSlope3) {
+                g[2] = -__fmul_rn(c, __fmaf_rn(tx, s1[1], __fmul_rn(ty, s1[2])));
+                H[0][2] = H[2][0] = __fmaf_rn(-c2, __fmaf_rn(tx, sd[3], __fmul_rn(ty, sd[4])),
+                                              __fmul_rn(c, __fmaf_rn(tx, sd[0], -s1[1])));
+                H[1][2] = H[2][1] = __fmaf_rn(-c2, __fmaf_rn(tx, sd[4], __fmul_rn(ty, sd[5])),
+                                              __fmul_rn(c, __fmaf_rn(ty, sd[0], -s1[2])));
+                const float q = __fmaf_rn(tx * tx, s1[3], __fmaf_rn(2.f * tx * ty, s1[4], __fmul_rn(ty * ty, s1[5])));
+                H[2][2] = __fmaf_rn(c2, q, -__fmul_rn(c, __fmul_rn(__fmaf_rn(tx, tx, ty * ty), s1[0])));
+            } else {
+                g[2] = 0.f;
+                H[0][2] = H[2][0] = H[1][2] = H[2][1] = H[2][2] = 0.f;
+            }
+            nt_direction<P>(g, H, a.eta[j], p[s]);
+            slope[s] = 0.f;
+#pragma unroll
+            for (int i = 0; i < P; ++i) slope[s] = __fmaf_rn(g[i], p[s][i], slope[s]);
+            active[s] = sid[s] < a.n_seeds;
+        }
+        float alpha = 1.f;
+        for (int k = 0; k <= a.max_halvings; ++k, alpha *= 0.5f) {
+            bool any = false;
+#pragma unroll
+            for (int s = 0; s < S; ++s) any |= active[s];
+            if (!__syncthreads_or(any)) break;
+#pragma unroll
+            for (int s = 0; s < S; ++s)
+#pragma unroll
+                for (int i = 0; i < 3; ++i)
+                    tt[s][i] = (i < P) ? fminf(fmaxf(__fmaf_rn(alpha, p[s][i], th[s][i]), a.lo[i]), a.hi[i]) : 0.f;
+            float Rt[S], Gd[S][4];
+            nt_pass_r<MODEL, S, ZREF, false>(st, tt, negK, a.z_ref, Rt, Gd);
+#pragma unroll
+            for (int s = 0; s < S; ++s) {
+                if (active[s] && Rt[s] >= __fmaf_rn(1e-4f * alpha, slope[s], R0[s])) {
+#pragma unroll
+                    for (int i = 0; i < 3; ++i) th[s][i] = tt[s][i];
+                    active[s] = false;
+                }
+            }
+        }
+    }
+    float g[S][3];
+    if (a.grad_out) {
+        nt_pass_r<MODEL, S, ZREF, true>(st, th, a.final_negK, a.z_ref, R, G);
+#pragma unroll
+        for (int s = 0; s < S; ++s) {
+            g[s][0] = __fmul_rn(a.final_c2, G[s][0]);
+            g[s][1] = __fmul_rn(a.final_c2, G[s][1]);
+            g[s][2] = (MODEL == kSlope3)
+                          ? -__fmul_rn(a.final_c2, __fmaf_rn(th[s][0], G[s][2], __fmul_rn(th[s][1], G[s][3])))
+                          : 0.f;
+        }
+    } else {
+        nt_pass_r<MODEL, S, ZREF, false>(st, th, a.final_negK, a.z_ref, R, G);
+    }
+#pragma unroll
+    for (int s = 0; s < S; ++s) {
+        if (sid[s] < a.n_seeds) {
+            const int64_t o = (int64_t)e * a.n_seeds + sid[s];
+            a.R_out[o] = R[s];
+#pragma unroll
+            for (int i = 0; i < P; ++i) {
+                a.theta_out[o * P + i] = th[s][i];
+                if (a.grad_out) a.grad_out[o * P + i] = g[s][i];
+            }
+        }
+    }
+}
+
+template <int MODEL, bool ZREF>
+static cudaError_t launch_nt(const NewtonArgs &a0, int n_events, cudaStream_t stream) {
+    constexpr int S = (MODEL == kSlope3) ? 2 : 4;
+    auto kern = newton_kernel<MODEL, S, ZREF>;
+    const size_t smem = (size_t)a0.cap * sizeof(float4);
+    cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (err != cudaSuccess) return err;
+    const int blocks = (a0.n_seeds + kNtThreads * S - 1) / (kNtThreads * S);
+    for (int e0 = 0; e0 < n_events; e0 += 65535) {
+        NewtonArgs a = a0;
+        a.e_base = e0;
+        const int ne = min(65535, n_events - e0);
+        kern<<<dim3(blocks, ne), kNtThreads, smem, stream>>>(a);
+        err = cudaGetLastError();
+        if (err != cudaSuccess) return err;
+    }
+    return cudaSuccess;
+}
+
+cudaError_t launch_newton(int model, const NewtonArgs &a, int n_events, cudaStream_t stream) {
+    if (n_events == 0 || a.n_seeds == 0) return cudaSuccess;
+    switch (model) {
+        case kSlope2:
+            return (a.z_ref == 0.f) ? launch_nt<kSlope2, false>(a, n_events, stream)
+                                    : launch_nt<kSlope2, true>(a, n_events, stream);
+        case kSlope3: return launch_nt<kSlope3, false>(a, n_events, stream);
+    }
+    return cudaErrorInvalidValue;
+}
+
+}  // namespace retina

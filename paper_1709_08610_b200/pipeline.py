@@ -38,6 +38,7 @@ class PathSpec:
     track_capacity: int
     z_ref: float = 0.0
     sigma_ms: Optional[float] = None     # multi-start sigma (defaults to sigma)
+    newton: Optional[tuple] = None       # (sigmas, etas, final_sigma, max_halvings): Newton update
 
     @property
     def P(self) -> int:
@@ -129,9 +130,14 @@ class RetinaPipeline:
         ev = self.events_view(batch, 0, E)
         if timer is not None:
             timer.start("multistart")
-        R.retina_multistart_optimize(ev, sp.model, sp.sigma_ms or sp.sigma, batch.seeds, sp.n_iters, sp.step,
-                                     sp.box_lo, sp.box_hi, want_grad=False,
-                                     out=(self.theta[:E], self.resp[:E], None), stream=stream)
+        if sp.newton is not None:  # the paper's update: Truncated Newton with a sigma schedule
+            sig, eta, fsig, mh = sp.newton
+            R.retina_multistart_newton(ev, sp.model, batch.seeds, sig, eta, fsig, mh, sp.box_lo, sp.box_hi,
+                                       want_grad=False, out=(self.theta[:E], self.resp[:E], None), stream=stream)
+        else:  # BASELINE configs[2..4]: fixed-step gradient ascent
+            R.retina_multistart_optimize(ev, sp.model, sp.sigma_ms or sp.sigma, batch.seeds, sp.n_iters, sp.step,
+                                         sp.box_lo, sp.box_hi, want_grad=False,
+                                         out=(self.theta[:E], self.resp[:E], None), stream=stream)
         if timer is not None:
             timer.stop("multistart")
             timer.start("merge")

@@ -21,8 +21,9 @@ MERGE_MAX_SEEDS = 16384
 
 GRID_AUTO, GRID_DIRECT, GRID_SEPARABLE, GRID_TENSOR = 0, 1, 2, 3
 
-EXPORTED = ("retina_grid_response", "retina_grid_response_ex", "retina_estimate_peaks", "retina_find_peaks", "retina_multistart_optimize",
-            "retina_merge_tracks", "retina_status_string", "retina_last_error", "retina_version")
+EXPORTED = ("retina_grid_response", "retina_grid_response_ex", "retina_estimate_peaks", "retina_find_peaks",
+            "retina_multistart_optimize", "retina_multistart_newton", "retina_merge_tracks",
+            "retina_status_string", "retina_last_error", "retina_version")
 
 
 class RetinaError(RuntimeError):
@@ -56,9 +57,11 @@ def lib() -> ctypes.CDLL:
         L.retina_estimate_peaks.argtypes = [vp, i32, i32, vp, vp, vp, vp, i32, vp, vp]
         L.retina_multistart_optimize.argtypes = [ctypes.POINTER(retina_events), ctypes.c_int, f32, i32, vp,
                                                  i32, f32, vp, vp, vp, vp, vp, vp]
+        L.retina_multistart_newton.argtypes = [ctypes.POINTER(retina_events), ctypes.c_int, i32, vp, i32, vp, vp,
+                                               f32, i32, vp, vp, vp, vp, vp, vp]
         L.retina_merge_tracks.argtypes = [i32, i32, i32, vp, vp, vp, f32, i32, vp, vp, vp, vp, vp, vp]
-        for f in (L.retina_grid_response, L.retina_grid_response_ex, L.retina_find_peaks, L.retina_estimate_peaks, L.retina_multistart_optimize,
-                  L.retina_merge_tracks):
+        for f in (L.retina_grid_response, L.retina_grid_response_ex, L.retina_find_peaks, L.retina_estimate_peaks,
+                  L.retina_multistart_optimize, L.retina_multistart_newton, L.retina_merge_tracks):
             f.restype = ctypes.c_int
         L.retina_status_string.argtypes = [ctypes.c_int]
         L.retina_status_string.restype = ctypes.c_char_p
@@ -194,6 +197,28 @@ def retina_multistart_optimize(events: Events, model: int, sigma: float, seeds: 
            lib().retina_multistart_optimize(ctypes.byref(events.c), model, float(sigma), S, _ptr(seeds),
                                             int(n_iters), float(step), lo, hi, _ptr(th), _ptr(R), _ptr(g),
                                             _stream(stream)))
+    return th, R, g
+
+
+def retina_multistart_newton(events: Events, model: int, seeds: torch.Tensor, sigmas, etas, final_sigma: float,
+                             max_halvings: int, box_lo, box_hi, want_grad: bool = True, out=None, stream=None):
+    """Truncated-Newton multi-start: (theta_out, response_out, grad_out or None)."""
+    P = MODEL_P[model]
+    _dev(seeds, torch.float32)
+    E, S, Ps = seeds.shape
+    assert Ps == P and E == events.n_events and len(sigmas) == len(etas)
+    sg, _k1 = _arr(ctypes.c_float, [float(v) for v in sigmas])
+    et, _k2 = _arr(ctypes.c_float, [float(v) for v in etas])
+    lo, _k3 = _arr(ctypes.c_float, [float(v) for v in box_lo])
+    hi, _k4 = _arr(ctypes.c_float, [float(v) for v in box_hi])
+    if out is None:
+        out = (torch.empty_like(seeds), torch.empty((E, S), dtype=torch.float32, device=seeds.device),
+               torch.empty_like(seeds) if want_grad else None)
+    th, R, g = out
+    _check("retina_multistart_newton",
+           lib().retina_multistart_newton(ctypes.byref(events.c), model, S, _ptr(seeds), len(sigmas), sg, et,
+                                          float(final_sigma), int(max_halvings), lo, hi, _ptr(th), _ptr(R),
+                                          _ptr(g), _stream(stream)))
     return th, R, g
 
 

@@ -169,3 +169,29 @@ def describe(cfg: Config) -> dict:
     d["model"] = MODEL_NAME[cfg.model]
     d["P"] = cfg.P
     return d
+
+
+# ---------------------------------------------------------------------------------------------
+# NEXT #1: the paper's own update.  Readings:
+# Z22 the schedule sigma = 0.3, 0.175, 0.05 (q = 3) is applied as RATIOS to the config's sigma,
+#     which is the last (finest) value: sigma_j = sigma_cfg x (6, 3.5, 1); final R at sigma_cfg.
+# Z23 Truncated Newton = conjugate gradients on (-H) p = grad R, <= P iterations, stopped at
+#     non-positive curvature.
+# Z24 the negative-curvature fallback at the first CG iteration is the fixed-step ascent step
+#     of reading Z7 at sigma_j: p = eta_j grad R, eta_j = sigma_j^2 / (2 lambda_max).
+# Z25 Armijo backtracking on R, c1 = 1e-4, alpha = 1, 1/2, ..., at most 8 halvings
+#     (SPEC.md:396), trial points clamped to the prior box; no accepted trial = no move.
+PAPER_SIGMA_SCHEDULE = (0.3, 0.175, 0.05)
+
+
+def newton_schedule(cfg: Config):
+    """(sigmas, etas, final_sigma, max_halvings) for the Truncated-Newton path of `cfg`."""
+    ratios = [s / PAPER_SIGMA_SCHEDULE[-1] for s in PAPER_SIGMA_SCHEDULE]
+    sigmas = [cfg.sigma * r for r in ratios]
+    if cfg.model == SLOPE3:
+        etas = [step_slope3(s) for s in sigmas]
+    elif cfg.model == SLOPE2:
+        etas = [step_slope2(s) for s in sigmas]
+    else:
+        etas = [step_line2d(s) for s in sigmas]
+    return sigmas, etas, cfg.sigma, 8
