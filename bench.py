@@ -292,7 +292,7 @@ def main():
         avg_ms = phase_ms[ph] / phase_n[ph]
         per_launch = work[ph] / n_launch
         pairs_s = per_launch / (avg_ms * 1e-3)
-        if ph == "grid" and cfg.model == C.SLOPE2:
+        if ph == "grid" and cfg.model in (C.SLOPE2, C.SLOPE3):
             # tcgen05 3xTF32 contraction: 2 algorithmic flops per (unit, hit) pair; the fp32-accurate
             # tensor peak is the TF32 peak (measured bf16 burst x nominal tf32/bf16 = 0.5) / 3 passes
             peak = float(pk.get("bf16_tflops", 1590.0)) * 1e12 * 0.5 / 3.0
@@ -326,8 +326,10 @@ def main():
         "steps": a.steps, "warmup": a.warmup, "ms_per_step": ms_step, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
         "events_per_s": E * world / (ms_step * 1e-3),
-        "config": {"workload": f"{cfg.name}: BASELINE.json configs[3] Run-3-like batch, {E} events per GPU "
-                               f"(ids rank*{E}..), 1024x1024 SLOPE2 grid + 3x3 peaks (R0={cfg.peak_threshold}), "
+        "config": {"workload": f"{cfg.name}: BASELINE.json configs[{cfg.name[-1]}], {E} events per GPU "
+                               f"(ids rank*{E}..), {'x'.join(str(x[2]) for x in cfg.axes)} "
+                               f"{C.MODEL_NAME[cfg.model].upper()} grid + {'x'.join(['3'] * cfg.P)} peaks "
+                               f"(R0={cfg.peak_threshold}) + sub-cell estimates, "
                                + (f"{cfg.n_seeds} seeds x {cfg.n_iters} fixed-step iterations + merge"
                                   if a.update == "gradient" else
                                   f"{cfg.n_seeds} seeds x q=3 Truncated-Newton steps (sigma schedule) + merge"),

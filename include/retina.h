@@ -49,6 +49,7 @@
 #ifndef RETINA_H
 #define RETINA_H
 
+#include <stddef.h>
 #include <stdint.h>
 
 #ifdef __cplusplus
@@ -94,14 +95,14 @@ int retina_grid_response(const retina_events *ev, int model, float sigma,
                          float *response, void *stream);
 
 /* Same as retina_grid_response with an explicit kernel choice:
- *   RETINA_GRID_AUTO       tensor for SLOPE2, separable for SLOPE3, direct for LINE2D
+ *   RETINA_GRID_AUTO       tensor for SLOPE2 and SLOPE3, direct for LINE2D
  *                          (what retina_grid_response uses);
  *   RETINA_GRID_DIRECT     one MUFU.EX2 per (unit, hit) pair (all models);
  *   RETINA_GRID_SEPARABLE  SLOPE2/SLOPE3 only: exp(-s^2/sigma^2) = e_x(tx, hit) e_y(ty, hit)
  *                          exactly, so the grid is a dense contraction over hits, done with
  *                          FFMA2 on the CUDA cores (RETINA_EUNSUPPORTED for LINE2D, whose
  *                          residual does not split);
- *   RETINA_GRID_TENSOR     SLOPE2 only: the same contraction on the tcgen05 tensor cores with a
+ *   RETINA_GRID_TENSOR     SLOPE2 / SLOPE3 (one GEMM per z0): the same contraction on the tcgen05 tensor cores with a
  *                          3xTF32 split (fp32-level accuracy), accumulators in TMEM. */
 enum { RETINA_GRID_AUTO = 0, RETINA_GRID_DIRECT = 1, RETINA_GRID_SEPARABLE = 2, RETINA_GRID_TENSOR = 3 };
 int retina_grid_response_ex(const retina_events *ev, int model, float sigma,
@@ -121,6 +122,15 @@ int retina_find_peaks(const float *response, int32_t n_events, int32_t P,
                       const int32_t *axis_len, float threshold, int32_t capacity,
                       int32_t *peak_index, float *peak_value, int32_t *peak_count,
                       void *stream);
+
+/* Same result as retina_find_peaks, computed by many CTAs per event (slabs of cells: count
+ * pass, then write pass at the deterministic prefix of the slab counts) using a caller-owned
+ * DEVICE workspace of at least retina_find_peaks_workspace_size() bytes.  Use it when events
+ * are few or grids large (e.g. 256^3).  workspace_bytes too small -> RETINA_EINVAL. */
+size_t retina_find_peaks_workspace_size(int32_t n_events, int32_t P, const int32_t *axis_len);
+int retina_find_peaks_ws(const float *response, int32_t n_events, int32_t P, const int32_t *axis_len,
+                         float threshold, int32_t capacity, int32_t *peak_index, float *peak_value,
+                         int32_t *peak_count, void *workspace, size_t workspace_bytes, void *stream);
 
 /* Step (iv), "for each cluster estimate track parameters" (Z21):
  * for every listed peak, per axis i, the vertex of the parabola through the peak cell and its

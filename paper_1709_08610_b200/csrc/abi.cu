@@ -103,12 +103,11 @@ int retina_grid_response_ex(const retina_events *ev, int model, float sigma, con
         return fail(RETINA_EINVAL, "unknown grid algorithm %d", algorithm);
     if (algorithm == RETINA_GRID_SEPARABLE && model == RETINA_LINE2D)
         return fail(RETINA_EUNSUPPORTED, "LINE2D residual does not factorise: no separable grid");
-    if (algorithm == RETINA_GRID_TENSOR && model != RETINA_SLOPE2)
-        return fail(RETINA_EUNSUPPORTED, "tensor-core grid is implemented for SLOPE2 only");
+    if (algorithm == RETINA_GRID_TENSOR && model == RETINA_LINE2D)
+        return fail(RETINA_EUNSUPPORTED, "LINE2D residual does not factorise: no tensor-core grid");
     if (algorithm == RETINA_GRID_AUTO)
         algorithm = (model == RETINA_LINE2D)   ? RETINA_GRID_DIRECT
-                    : (model == RETINA_SLOPE2) ? RETINA_GRID_TENSOR
-                                               : RETINA_GRID_SEPARABLE;
+                                               : RETINA_GRID_TENSOR;
     retina::GridArgs a{};
     a.offsets = ev->offsets;
     a.hits = reinterpret_cast<const float4 *>(ev->hits);
@@ -164,6 +163,52 @@ int retina_find_peaks(const float *response, int32_t n_events, int32_t P, const 
     a.cnt = peak_count;
     const cudaError_t err = retina::launch_find_peaks(a, n_events, (cudaStream_t)stream);
     if (err != cudaSuccess) return cuda_fail(err, "retina_find_peaks");
+    return RETINA_OK;
+}
+
+size_t retina_find_peaks_workspace_size(int32_t n_events, int32_t P, const int32_t *axis_len) {
+    if (n_events <= 0 || (P != 2 && P != 3) || !axis_len) return 0;
+    long long cells = 1;
+    for (int i = 0; i < P; ++i) cells *= (axis_len[i] > 0 ? axis_len[i] : 0);
+    if (cells <= 0 || cells > 0x7fffffffLL) return 0;
+    return (size_t)n_events * (size_t)retina::peaks_slabs((int)cells) * sizeof(int32_t);
+}
+
+int retina_find_peaks_ws(const float *response, int32_t n_events, int32_t P, const int32_t *axis_len,
+                         float threshold, int32_t capacity, int32_t *peak_index, float *peak_value,
+                         int32_t *peak_count, void *workspace, size_t workspace_bytes, void *stream) {
+    g_last_error[0] = 0;
+    if (n_events < 0) return fail(RETINA_EINVAL, "n_events < 0");
+    if (P != 2 && P != 3) return fail(RETINA_EINVAL, "P must be 2 or 3 (got %d)", P);
+    if (!axis_len) return fail(RETINA_EINVAL, "axis_len is NULL");
+    if (capacity < 0) return fail(RETINA_EINVAL, "capacity < 0");
+    if (std::isnan(threshold)) return fail(RETINA_EINVAL, "threshold is NaN");
+    long long cells = 1;
+    for (int i = 0; i < P; ++i) {
+        if (axis_len[i] < 2) return fail(RETINA_EINVAL, "axis_len[%d] = %d < 2", i, axis_len[i]);
+        cells *= axis_len[i];
+    }
+    if (cells > 0x7fffffffLL) return fail(RETINA_EUNSUPPORTED, "more than 2^31-1 cells per event");
+    if (n_events == 0) return RETINA_OK;
+    if (!response || !peak_count || (capacity > 0 && (!peak_index || !peak_value)))
+        return fail(RETINA_EINVAL, "NULL device pointer");
+    const size_t need = retina_find_peaks_workspace_size(n_events, P, axis_len);
+    if (!workspace || workspace_bytes < need)
+        return fail(RETINA_EINVAL, "workspace of %zu bytes needed (got %zu)", need, workspace_bytes);
+    retina::PeakArgs a{};
+    a.R = response;
+    a.n0 = axis_len[0];
+    a.n1 = axis_len[1];
+    a.n2 = (P == 3) ? axis_len[2] : 1;
+    a.P = P;
+    a.threshold = threshold;
+    a.capacity = capacity;
+    a.idx = peak_index;
+    a.val = peak_value;
+    a.cnt = peak_count;
+    const cudaError_t err =
+        retina::launch_find_peaks_ws(a, n_events, static_cast<int32_t *>(workspace), (cudaStream_t)stream);
+    if (err != cudaSuccess) return cuda_fail(err, "retina_find_peaks_ws");
     return RETINA_OK;
 }
 

@@ -1,5 +1,5 @@
-// grid_tensor.cu -- K1t: Eq. (2) for SLOPE2 as a dense contraction on the 5th-generation tensor
-// cores (tcgen05.mma, accumulators in TMEM).
+// grid_tensor.cu -- K1t: Eq. (2) for SLOPE2 and SLOPE3 (one GEMM per z0 value) as a dense
+// contraction on the 5th-generation tensor cores (tcgen05.mma, accumulators in TMEM).
 //
 // Same exact factorisation as K1s (grid_separable.cu):
 //     R[i][j] = sum_k EX[i][k] * EY[j][k],  EX = 2^(-K (x - tx z)^2),  EY = 2^(-K (y - ty z)^2).
@@ -59,7 +59,7 @@ __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence:
 
 __device__ __forceinline__ float tf32_trunc(float v) { return __uint_as_float(__float_as_uint(v) & 0xFFFFE000u); }
 
-template <bool ZREF>
+template <int MODEL, bool ZREF>
 __global__ void __launch_bounds__(256, 1) grid_tensor_kernel(GridArgs a) {
     extern __shared__ __align__(1024) uint8_t s_raw[];
     __shared__ __align__(8) uint64_t s_bar[2];     // hit stage
@@ -70,8 +70,12 @@ __global__ void __launch_bounds__(256, 1) grid_tensor_kernel(GridArgs a) {
     float4 *s_hits = reinterpret_cast<float4 *>(s_raw + 2 * TC_STAGE_BYTES);  // hit stage after
 
     const int e = a.e_base + blockIdx.y;
+    // block order: z0 index fastest (SLOPE3), so the CTAs resident at once write neighbouring
+    // z0 values of the same (tx, ty) cells and L2 merges their 4-byte stores into full sectors
     const int tn = (a.n1 + TC_N - 1) / TC_N;
-    const int t_n = blockIdx.x % tn, t_m = blockIdx.x / tn;
+    const int nl = (MODEL == kSlope3) ? a.n2 : 1;
+    const int l = blockIdx.x % nl, tile = blockIdx.x / nl;
+    const int t_n = tile % tn, t_m = tile / tn;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
 
     if (warp == 0) {  // TMEM accumulator: 128 lanes x 256 fp32 columns
@@ -96,7 +100,8 @@ __global__ void __launch_bounds__(256, 1) grid_tensor_kernel(GridArgs a) {
     for (int t = 0; t < 4; ++t) pa[t] = __ldg(a.nodes0 + min(t_m * TC_M + lane + 32 * t, a.n0 - 1));
 #pragma unroll
     for (int t = 0; t < 8; ++t) pb[t] = __ldg(a.nodes1 + min(t_n * TC_N + lane + 32 * t, a.n1 - 1));
-    const float negK = a.negK, zref = a.z_ref;
+    const float negK = a.negK;
+    const float zref = (MODEL == kSlope3) ? __ldg(a.nodes2 + l) : a.z_ref;  // d = z - z0 or z - z_ref
     const uint32_t stage_saddr = smem_u32(stage_base);
 
     int chunk = 0;  // global chunk counter (uniform)
@@ -115,7 +120,7 @@ __global__ void __launch_bounds__(256, 1) grid_tensor_kernel(GridArgs a) {
                 const float4 hk = h[ok[q] ? k : 0];
                 hx[q] = hk.x;
                 hy[q] = hk.y;
-                if (ZREF)
+                if (ZREF || MODEL == kSlope3)
                     two_sum(hk.z, -zref, hz[q], hzl[q]);
                 else {
                     hz[q] = hk.z;
@@ -134,7 +139,8 @@ __global__ void __launch_bounds__(256, 1) grid_tensor_kernel(GridArgs a) {
 #pragma unroll
                 for (int q = 0; q < 4; ++q) {
                     const float c = isA ? hx[q] : hy[q];
-                    const float sres = ZREF ? __fmaf_rn(-p, hzl[q], __fmaf_rn(-p, hz[q], c)) : __fmaf_rn(-p, hz[q], c);
+                    const float sres = (ZREF || MODEL == kSlope3) ? __fmaf_rn(-p, hzl[q], __fmaf_rn(-p, hz[q], c))
+                                                                   : __fmaf_rn(-p, hz[q], c);
                     const float v = ok[q] ? ex2_approx(__fmul_rn(__fmul_rn(sres, sres), negK)) : 0.f;
                     vh[q] = tf32_trunc(v);
                     vl[q] = __fsub_rn(v, vh[q]);
@@ -178,8 +184,8 @@ __global__ void __launch_bounds__(256, 1) grid_tensor_kernel(GridArgs a) {
     // ---- epilogue: warp w reads TMEM lanes 32 (w % 4) .. +31 (= tile rows), columns half w / 4
     const int q = warp & 3, half = warp >> 2;
     const int i = t_m * TC_M + q * 32 + lane;
-    const int64_t cells = (int64_t)a.n0 * a.n1;
-    float *out = a.R + (int64_t)e * cells + (int64_t)i * a.n1;
+    const int64_t cells = (int64_t)a.n0 * a.n1 * nl;
+    float *out = a.R + (int64_t)e * cells + (int64_t)i * a.n1 * nl;
 #pragma unroll 1
     for (int cc = 0; cc < 8; ++cc) {
         const int col = half * 128 + cc * 16;
@@ -199,7 +205,11 @@ __global__ void __launch_bounds__(256, 1) grid_tensor_kernel(GridArgs a) {
             for (int x = 0; x < 16; ++x) v[x] = 0u;
         }
         const int j0 = t_n * TC_N + col;
-        if (i < a.n0) {
+        if (i < a.n0 && MODEL == kSlope3) {
+#pragma unroll
+            for (int x = 0; x < 16; ++x)
+                if (j0 + x < a.n1) out[(int64_t)(j0 + x) * nl + l] = __uint_as_float(v[x]);
+        } else if (i < a.n0) {
             if (j0 + 15 < a.n1 && (((uintptr_t)(out + j0)) & 15u) == 0) {
 #pragma unroll
                 for (int x = 0; x < 16; x += 4)
@@ -223,15 +233,17 @@ int tensor_max_stage_hits() {
     return (227 * 1024 - 2 * TC_STAGE_BYTES - 1024) / 16;  // hit slots left after the operand stages
 }
 
-template <bool ZREF>
+template <int MODEL, bool ZREF>
 static cudaError_t launch_tc(const GridArgs &a0, int n_events, cudaStream_t stream) {
-    auto kern = grid_tensor_kernel<ZREF>;
+    auto kern = grid_tensor_kernel<MODEL, ZREF>;
     GridArgs a = a0;
     a.cap = min(a.cap, tensor_max_stage_hits()) & ~1;
     const size_t smem = 2 * (size_t)TC_STAGE_BYTES + (size_t)a.cap * sizeof(float4);
     cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (err != cudaSuccess) return err;
-    const long long tiles = (long long)((a.n0 + TC_M - 1) / TC_M) * ((a.n1 + TC_N - 1) / TC_N);
+    const long long tiles =
+        (long long)((a.n0 + TC_M - 1) / TC_M) * ((a.n1 + TC_N - 1) / TC_N) * (MODEL == kSlope3 ? a.n2 : 1);
+    if (tiles > 0x7fffffffLL) return cudaErrorInvalidConfiguration;
     for (int e0 = 0; e0 < n_events; e0 += 65535) {
         a.e_base = e0;
         const int ne = min(65535, n_events - e0);
@@ -244,8 +256,10 @@ static cudaError_t launch_tc(const GridArgs &a0, int n_events, cudaStream_t stre
 
 cudaError_t launch_grid_tensor(int model, const GridArgs &a, int n_events, cudaStream_t stream) {
     if (n_events == 0) return cudaSuccess;
+    if (model == kSlope3) return launch_tc<kSlope3, false>(a, n_events, stream);
     if (model != kSlope2) return cudaErrorInvalidValue;
-    return (a.z_ref == 0.f) ? launch_tc<false>(a, n_events, stream) : launch_tc<true>(a, n_events, stream);
+    return (a.z_ref == 0.f) ? launch_tc<kSlope2, false>(a, n_events, stream)
+                            : launch_tc<kSlope2, true>(a, n_events, stream);
 }
 
 }  // namespace retina

@@ -102,6 +102,8 @@ cudaError_t launch_grid_tensor(int model, const GridArgs &a, int n_events, cudaS
 cudaError_t launch_newton(int model, const NewtonArgs &a, int n_events, cudaStream_t stream);
 cudaError_t launch_multistart(int model, const MultistartArgs &a, int n_events, cudaStream_t stream);
 cudaError_t launch_find_peaks(const PeakArgs &a, int n_events, cudaStream_t stream);
+cudaError_t launch_find_peaks_ws(const PeakArgs &a, int n_events, int32_t *ws, cudaStream_t stream);
+int peaks_slabs(int cells);
 cudaError_t launch_merge(const MergeArgs &a, int n_events, cudaStream_t stream);
 
 }  // namespace retina

@@ -20,7 +20,19 @@
 
 namespace retina {
 
-constexpr int kMsThreads = 128;
+#ifndef RETINA_MS_THREADS
+#define RETINA_MS_THREADS 128
+#endif
+#ifndef RETINA_MS_MINB
+#define RETINA_MS_MINB 6  // caps registers at 80: 6 CTAs (24 warps) per SM, measured +3 % over 94 registers
+#endif
+#ifndef RETINA_MS3_SEEDS  // SLOPE3 carries z0 and the exact d = z - z0 per seed: fewer seeds per thread
+#define RETINA_MS3_SEEDS 4
+#endif
+#ifndef RETINA_MS3_MINB
+#define RETINA_MS3_MINB 6
+#endif
+constexpr int kMsThreads = RETINA_MS_THREADS;
 
 template <int MODEL, int S, bool ZREF, bool GRAD>
 __device__ __forceinline__ void ms_pass(HitStage &st, const float (&th)[S][3], float negK, float zref,
@@ -244,7 +256,8 @@ __device__ __forceinline__ void ms_gradient(const float (&th)[S][3], const float
 }
 
 template <int MODEL, int S, bool ZREF>
-__global__ void __launch_bounds__(kMsThreads) multistart_kernel(MultistartArgs a) {
+__global__ void __launch_bounds__(kMsThreads, (MODEL == kSlope3) ? RETINA_MS3_MINB : RETINA_MS_MINB)
+multistart_kernel(MultistartArgs a) {
     extern __shared__ __align__(16) float4 s_hits[];
     __shared__ __align__(8) uint64_t s_bar[2];
     constexpr int P = (MODEL == kSlope3) ? 3 : 2;
@@ -299,7 +312,7 @@ static cudaError_t launch_ms(const MultistartArgs &a0, int n_events, cudaStream_
 #ifndef RETINA_MS_SEEDS
 #define RETINA_MS_SEEDS 8
 #endif
-    constexpr int S = RETINA_MS_SEEDS;
+    constexpr int S = (MODEL == kSlope3) ? RETINA_MS3_SEEDS : RETINA_MS_SEEDS;
     auto kern = multistart_kernel<MODEL, S, ZREF>;
     const size_t smem = (size_t)a0.cap * sizeof(float4);
     cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);

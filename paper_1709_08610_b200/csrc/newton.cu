@@ -118,14 +118,15 @@ __device__ __forceinline__ void nt_pass_r(HitStage &st, const float (&th)[S][3],
     for (int s = 0; s < S; ++s) dh[s] = dl[s] = qa[s] = qb[s] = 0.f;
     float zprev = __int_as_float(0x7fc00000);
     auto flush = [&]() {
-        if (!GRAD) return;
+        if constexpr (GRAD) {
 #pragma unroll
-        for (int s = 0; s < S; ++s) {
-            G[s][0] = __fmaf_rn(dh[s], qa[s], G[s][0]);
-            G[s][1] = __fmaf_rn(dh[s], qb[s], G[s][1]);
-            G[s][2] = __fadd_rn(G[s][2], qa[s]);
-            G[s][3] = __fadd_rn(G[s][3], qb[s]);
-            qa[s] = qb[s] = 0.f;
+            for (int s = 0; s < S; ++s) {
+                G[s][0] = __fmaf_rn(dh[s], qa[s], G[s][0]);
+                G[s][1] = __fmaf_rn(dh[s], qb[s], G[s][1]);
+                G[s][2] = __fadd_rn(G[s][2], qa[s]);
+                G[s][3] = __fadd_rn(G[s][3], qb[s]);
+                qa[s] = qb[s] = 0.f;
+            }
         }
     };
     st.pass([&](const float4 *h, int len) {

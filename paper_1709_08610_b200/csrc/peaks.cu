@@ -15,6 +15,7 @@ namespace retina {
 
 constexpr int kPeakThreads = 512;
 constexpr int kPeakV = 4;
+constexpr int kSlabCells = 131072;  // cells per CTA in the workspace (two-pass) variant
 
 __device__ __forceinline__ int warp_incl_scan(int v) {
     const int lane = threadIdx.x & 31;
@@ -62,23 +63,20 @@ __device__ __forceinline__ bool is_peak(const float *__restrict__ g, int c, int 
     return true;
 }
 
-template <int P>
-__global__ void __launch_bounds__(kPeakThreads) find_peaks_kernel(PeakArgs a) {
-    __shared__ int s_warp[kPeakThreads / 32];
-    const int e = a.e_base + blockIdx.x;
-    const int cells = a.n0 * a.n1 * a.n2;
-    const float *g = a.R + (int64_t)e * cells;
-    int32_t *oi = a.idx + (int64_t)e * a.capacity;
-    float *ov = a.val + (int64_t)e * a.capacity;
+// Flags and (when WRITE) compacts the peaks of cells [c_begin, c_end) of one event, writing the
+// i-th peak found at output position pos0 + i.  Returns the number of peaks in the range.
+template <int P, bool WRITE>
+__device__ __forceinline__ int scan_range(const PeakArgs &a, const float *g, int32_t *oi, float *ov, int c_begin,
+                                          int c_end, int pos0, int *s_warp) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     int total = 0;
-    for (int base = 0; base < cells; base += kPeakThreads * kPeakV) {
+    for (int base = c_begin; base < c_end; base += kPeakThreads * kPeakV) {
         const int c0 = base + threadIdx.x * kPeakV;
         unsigned mask = 0;
 #pragma unroll
         for (int v = 0; v < kPeakV; ++v) {
             const int c = c0 + v;
-            if (c < cells && is_peak<P>(g, c, a.n0, a.n1, a.n2, a.threshold)) mask |= 1u << v;
+            if (c < c_end && is_peak<P>(g, c, a.n0, a.n1, a.n2, a.threshold)) mask |= 1u << v;
         }
         const int cnt = __popc(mask);
         const int incl = warp_incl_scan(cnt);
@@ -90,33 +88,99 @@ __global__ void __launch_bounds__(kPeakThreads) find_peaks_kernel(PeakArgs a) {
             if (lane < kPeakThreads / 32) s_warp[lane] = w;
         }
         __syncthreads();
-        int pos = total + incl - cnt + (warp > 0 ? s_warp[warp - 1] : 0);
-        const int chunk_total = s_warp[kPeakThreads / 32 - 1];
+        if (WRITE) {
+            int pos = pos0 + total + incl - cnt + (warp > 0 ? s_warp[warp - 1] : 0);
 #pragma unroll
-        for (int v = 0; v < kPeakV; ++v) {
-            if (mask & (1u << v)) {
-                if (pos < a.capacity) {
-                    oi[pos] = c0 + v;
-                    ov[pos] = __ldg(g + c0 + v);
+            for (int v = 0; v < kPeakV; ++v) {
+                if (mask & (1u << v)) {
+                    if (pos < a.capacity) {
+                        oi[pos] = c0 + v;
+                        ov[pos] = __ldg(g + c0 + v);
+                    }
+                    ++pos;
                 }
-                ++pos;
             }
         }
-        total += chunk_total;
+        total += s_warp[kPeakThreads / 32 - 1];
         __syncthreads();  // s_warp is rewritten by the next chunk
     }
+    return total;
+}
+
+// Single pass, one CTA per event (no workspace).
+template <int P>
+__global__ void __launch_bounds__(kPeakThreads) find_peaks_kernel(PeakArgs a) {
+    __shared__ int s_warp[kPeakThreads / 32];
+    const int e = a.e_base + blockIdx.x;
+    const int cells = a.n0 * a.n1 * a.n2;
+    const float *g = a.R + (int64_t)e * cells;
+    const int total = scan_range<P, true>(a, g, a.idx + (int64_t)e * a.capacity, a.val + (int64_t)e * a.capacity,
+                                          0, cells, 0, s_warp);
     if (threadIdx.x == 0) a.cnt[e] = total;
 }
 
+// Two passes over slabs of kSlabCells cells, grid (slabs, events), with a caller-owned int32
+// workspace [events][slabs]: (1) count per slab; (2) each slab sums the counts of the slabs
+// before it (fixed order: deterministic) and writes its peaks there; the last slab writes the
+// event's true count.  Same output as the single pass, many CTAs per event.
+template <int P>
+__global__ void __launch_bounds__(kPeakThreads) count_peaks_slab_kernel(PeakArgs a, int32_t *ws, int n_slabs) {
+    __shared__ int s_warp[kPeakThreads / 32];
+    const int e = a.e_base + blockIdx.y, b = blockIdx.x;
+    const int cells = a.n0 * a.n1 * a.n2;
+    const int c_begin = b * kSlabCells, c_end = min(cells, c_begin + kSlabCells);
+    const int n = scan_range<P, false>(a, a.R + (int64_t)e * cells, nullptr, nullptr, c_begin, c_end, 0, s_warp);
+    if (threadIdx.x == 0) ws[(int64_t)blockIdx.y * n_slabs + b] = n;
+}
+
+template <int P>
+__global__ void __launch_bounds__(kPeakThreads) write_peaks_slab_kernel(PeakArgs a, const int32_t *ws, int n_slabs) {
+    __shared__ int s_warp[kPeakThreads / 32];
+    __shared__ int s_off;
+    const int e = a.e_base + blockIdx.y, b = blockIdx.x;
+    const int cells = a.n0 * a.n1 * a.n2;
+    const int32_t *w = ws + (int64_t)blockIdx.y * n_slabs;
+    if (threadIdx.x == 0) {
+        int off = 0;
+        for (int i = 0; i < b; ++i) off += w[i];
+        s_off = off;
+    }
+    __syncthreads();
+    const int off = s_off;
+    const int c_begin = b * kSlabCells, c_end = min(cells, c_begin + kSlabCells);
+    if (off < a.capacity)
+        scan_range<P, true>(a, a.R + (int64_t)e * cells, a.idx + (int64_t)e * a.capacity,
+                            a.val + (int64_t)e * a.capacity, c_begin, c_end, off, s_warp);
+    if (b == n_slabs - 1 && threadIdx.x == 0) a.cnt[e] = off + w[b];
+}
+
 cudaError_t launch_find_peaks(const PeakArgs &a0, int n_events, cudaStream_t stream) {
-    for (int e0 = 0; e0 < n_events; e0 += 0x7fffffff) {
+    PeakArgs a = a0;
+    a.e_base = 0;
+    if (a.P == 3)
+        find_peaks_kernel<3><<<n_events, kPeakThreads, 0, stream>>>(a);
+    else
+        find_peaks_kernel<2><<<n_events, kPeakThreads, 0, stream>>>(a);
+    return cudaGetLastError();
+}
+
+int peaks_slabs(int cells) { return (cells + kSlabCells - 1) / kSlabCells; }
+
+cudaError_t launch_find_peaks_ws(const PeakArgs &a0, int n_events, int32_t *ws, cudaStream_t stream) {
+    const int cells = a0.n0 * a0.n1 * a0.n2;
+    const int n_slabs = peaks_slabs(cells);
+    for (int e0 = 0; e0 < n_events; e0 += 65535) {
         PeakArgs a = a0;
         a.e_base = e0;
-        const int ne = n_events - e0;
-        if (a.P == 3)
-            find_peaks_kernel<3><<<ne, kPeakThreads, 0, stream>>>(a);
-        else
-            find_peaks_kernel<2><<<ne, kPeakThreads, 0, stream>>>(a);
+        const int ne = min(65535, n_events - e0);
+        const dim3 grid(n_slabs, ne);
+        if (a.P == 3) {
+            count_peaks_slab_kernel<3><<<grid, kPeakThreads, 0, stream>>>(a, ws, n_slabs);
+            write_peaks_slab_kernel<3><<<grid, kPeakThreads, 0, stream>>>(a, ws, n_slabs);
+        } else {
+            count_peaks_slab_kernel<2><<<grid, kPeakThreads, 0, stream>>>(a, ws, n_slabs);
+            write_peaks_slab_kernel<2><<<grid, kPeakThreads, 0, stream>>>(a, ws, n_slabs);
+        }
         const cudaError_t err = cudaGetLastError();
         if (err != cudaSuccess) return err;
     }

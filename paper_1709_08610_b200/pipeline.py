@@ -74,6 +74,12 @@ class RetinaPipeline:
         self.nodes = [torch.from_numpy(np.ascontiguousarray(n, np.float32)).to(self.device) for n in spec.nodes]
         shape = tuple(len(n) for n in spec.nodes)
         self.grid_buf = torch.empty((self.chunk,) + shape, dtype=torch.float32, device=self.device) if cells else None
+        # many-CTA peak finder when a chunk has too few events to fill the GPU with one CTA per
+        # event (large grids, e.g. 256^3); one CTA per event otherwise (single read of the grid)
+        self.peak_ws = None
+        if cells and self.chunk < 2 * 148:
+            ws = R.find_peaks_workspace_size(self.chunk, shape)
+            self.peak_ws = torch.empty((max(ws, 4) // 4,), dtype=torch.int32, device=self.device)
         E, P = max_events, spec.P
         self.peak_idx = torch.empty((E, spec.peak_capacity), dtype=torch.int32, device=self.device)
         self.peak_val = torch.empty((E, spec.peak_capacity), dtype=torch.float32, device=self.device)
@@ -116,7 +122,7 @@ class RetinaPipeline:
                 timer.start("peaks")
             R.retina_find_peaks(out, sp.P, sp.peak_threshold, sp.peak_capacity,
                                 out=(self.peak_idx[e0:e1], self.peak_val[e0:e1], self.peak_cnt[e0:e1]),
-                                stream=stream)
+                                stream=stream, workspace=self.peak_ws)
             # step (iv): sub-cell parameter estimate of every peak
             R.retina_estimate_peaks(out, self.nodes, self.peak_idx[e0:e1], self.peak_cnt[e0:e1],
                                     out=self.peak_theta[e0:e1], stream=stream)

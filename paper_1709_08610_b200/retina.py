@@ -22,6 +22,7 @@ MERGE_MAX_SEEDS = 16384
 GRID_AUTO, GRID_DIRECT, GRID_SEPARABLE, GRID_TENSOR = 0, 1, 2, 3
 
 EXPORTED = ("retina_grid_response", "retina_grid_response_ex", "retina_estimate_peaks", "retina_find_peaks",
+            "retina_find_peaks_ws", "retina_find_peaks_workspace_size",
             "retina_multistart_optimize", "retina_multistart_newton", "retina_merge_tracks",
             "retina_status_string", "retina_last_error", "retina_version")
 
@@ -55,6 +56,10 @@ def lib() -> ctypes.CDLL:
                                               ctypes.c_int, vp]
         L.retina_find_peaks.argtypes = [vp, i32, i32, vp, f32, i32, vp, vp, vp, vp]
         L.retina_estimate_peaks.argtypes = [vp, i32, i32, vp, vp, vp, vp, i32, vp, vp]
+        L.retina_find_peaks_ws.argtypes = [vp, i32, i32, vp, f32, i32, vp, vp, vp, vp, ctypes.c_size_t, vp]
+        L.retina_find_peaks_ws.restype = ctypes.c_int
+        L.retina_find_peaks_workspace_size.argtypes = [i32, i32, vp]
+        L.retina_find_peaks_workspace_size.restype = ctypes.c_size_t
         L.retina_multistart_optimize.argtypes = [ctypes.POINTER(retina_events), ctypes.c_int, f32, i32, vp,
                                                  i32, f32, vp, vp, vp, vp, vp, vp]
         L.retina_multistart_newton.argtypes = [ctypes.POINTER(retina_events), ctypes.c_int, i32, vp, i32, vp, vp,
@@ -142,9 +147,16 @@ def retina_grid_response(events: Events, model: int, sigma: float, nodes: Sequen
     return out
 
 
+def find_peaks_workspace_size(n_events: int, shape) -> int:
+    alen, _k = _arr(ctypes.c_int32, list(shape))
+    return int(lib().retina_find_peaks_workspace_size(int(n_events), len(shape), alen))
+
+
 def retina_find_peaks(response: torch.Tensor, P: int, threshold: float, capacity: int,
-                      out=None, stream=None):
-    """Returns (peak_index int32 [E, cap], peak_value fp32 [E, cap], peak_count int32 [E])."""
+                      out=None, stream=None, workspace: Optional[torch.Tensor] = None):
+    """Returns (peak_index int32 [E, cap], peak_value fp32 [E, cap], peak_count int32 [E]).
+    With a device `workspace` (>= find_peaks_workspace_size bytes) the many-CTA path
+    (retina_find_peaks_ws) is used; the results are identical."""
     _dev(response, torch.float32)
     E = response.shape[0]
     shape = tuple(response.shape[1:])
@@ -156,9 +168,16 @@ def retina_find_peaks(response: torch.Tensor, P: int, threshold: float, capacity
                torch.empty((E, capacity), dtype=torch.float32, device=dev),
                torch.empty((E,), dtype=torch.int32, device=dev))
     idx, val, cnt = out
-    _check("retina_find_peaks",
-           lib().retina_find_peaks(_ptr(response), E, P, alen, float(threshold), int(capacity),
-                                   _ptr(idx), _ptr(val), _ptr(cnt), _stream(stream)))
+    if workspace is not None:
+        nbytes = workspace.numel() * workspace.element_size()
+        _check("retina_find_peaks_ws",
+               lib().retina_find_peaks_ws(_ptr(response), E, P, alen, float(threshold), int(capacity), _ptr(idx),
+                                          _ptr(val), _ptr(cnt), _ptr(workspace), ctypes.c_size_t(nbytes),
+                                          _stream(stream)))
+    else:
+        _check("retina_find_peaks",
+               lib().retina_find_peaks(_ptr(response), E, P, alen, float(threshold), int(capacity),
+                                       _ptr(idx), _ptr(val), _ptr(cnt), _stream(stream)))
     return idx, val, cnt
 
 

@@ -85,6 +85,22 @@ def test_peaks_validation(L):
     assert p(16, 1, 2, _i(4, 4), float("nan"), 4, 16, 16, 16, None) == rt.RETINA_EINVAL
 
 
+def test_peaks_workspace_size_and_validation(L):
+    sz = L.retina_find_peaks_workspace_size
+    sz.restype = ctypes.c_size_t
+    # 1024^2 cells -> 8 slabs of 131072 cells, 4 bytes each per event
+    assert sz(10, 2, _i(1024, 1024)) == 10 * 8 * 4
+    assert sz(3, 3, _i(256, 256, 256)) == 3 * 128 * 4
+    assert sz(0, 2, _i(4, 4)) == 0 and sz(1, 4, _i(4, 4)) == 0
+    p = L.retina_find_peaks_ws
+    p.argtypes = [ctypes.c_void_p, ctypes.c_int32, ctypes.c_int32, ctypes.c_void_p, ctypes.c_float, ctypes.c_int32,
+                  ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p]
+    assert p(16, 2, 2, _i(1024, 1024), 0.0, 4, 16, 16, 16, 16, 8, None) == rt.RETINA_EINVAL  # too small
+    assert b"workspace" in L.retina_last_error()
+    assert p(16, 2, 2, _i(1024, 1024), 0.0, 4, 16, 16, 16, None, 1 << 20, None) == rt.RETINA_EINVAL
+    assert p(16, 0, 2, _i(1024, 1024), 0.0, 4, 16, 16, 16, None, 0, None) == rt.RETINA_OK
+
+
 def test_multistart_validation(L):
     m = L.retina_multistart_optimize
     ev = _ev()

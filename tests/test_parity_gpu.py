@@ -191,6 +191,29 @@ def test_T3_peaks_bitexact_planted_ties(P, shape):
             assert np.array_equal(val[e, :k].astype(np.float64), rv[e, :k])
 
 
+@pytest.mark.parametrize("P,shape", [(2, (3, 1024, 1024)), (2, (5, 37, 61)), (3, (2, 64, 64, 64)),
+                                     (3, (1, 256, 256, 256)), (2, (2, 700, 900))])
+def test_T3_peaks_workspace_path_identical(P, shape):
+    """retina_find_peaks_ws (many CTAs per event) == retina_find_peaks (one CTA per event) ==
+    the oracle rule, bit for bit, including ties and capacity overflow."""
+    rng = np.random.default_rng(P + shape[1])
+    g = rng.integers(0, 6, shape).astype(np.float32)
+    dg = dev(g)
+    ws = torch.empty((R.retina.find_peaks_workspace_size(shape[0], shape[1:]) // 4 + 1,), dtype=torch.int32,
+                     device=DEV)
+    for thr, cap in ((0.0, 1 << 21), (4.0, 1 << 20), (0.0, 7)):
+        a = R.retina_find_peaks(dg, P, thr, cap)
+        b = R.retina_find_peaks(dg, P, thr, cap, workspace=ws)
+        torch.cuda.synchronize()
+        assert torch.equal(a[2], b[2])
+        for e in range(shape[0]):
+            k = min(int(a[2][e]), cap)
+            assert torch.equal(a[0][e, :k], b[0][e, :k]) and torch.equal(a[1][e, :k], b[1][e, :k])
+        if shape[1] <= 256:
+            ri, rv, rc = ora.peaks(g.astype(np.float64), P, thr, cap)
+            assert np.array_equal(b[2].cpu().numpy(), rc)
+
+
 def test_T3_peaks_cfg4_slope3_sampled():
     cfg = C.CFG4
     b = G.make_batch(cfg, [1])
@@ -501,3 +524,71 @@ def test_newton_identities():
     torch.cuda.synchronize()
     assert torch.equal(th, seeds)
     assert torch.allclose(Rn, R2, rtol=2e-6, atol=1e-6)
+
+
+# --------------------------------------------------------------------------- tensor-core grid (SLOPE3)
+@pytest.mark.parametrize("shape", [(5, 37, 45), (3, 70, 33), (130, 260, 3)])
+@pytest.mark.parametrize("hint", [True, False])
+def test_T1_tensor_grid_slope3_ragged(shape, hint):
+    b = synthetic_batch(C.SLOPE3, [700, 0, 1, 5000, 37], seed=11)
+    nodes = [np.linspace(lo, hi, n).astype(np.float32) for (lo, hi), n in
+             zip([(-0.3, 0.3), (-0.3, 0.3), (-150.0, 150.0)], shape)]
+    cfg = C.Config(name="t", model=C.SLOPE3, n_events=5, seed=0, n_tracks=0, sigma=0.88)
+    g = gpu_grid(b, cfg, nodes, hint=hint, algo=TENSOR)
+    ref = ora.grid(C.SLOPE3, b.offsets, b.hits, nodes, 0.88)
+    assert np.all(g[1] == 0.0)
+    ok, worst = PU.t1_response(g, ref)
+    assert ok, worst
+
+
+def test_T1_tensor_grid_cfg4_full_size_sampled_and_peaks():
+    cfg = C.CFG4
+    b = G.make_batch(cfg, [0, 1])
+    nodes = G.axis_nodes(cfg)
+    g = gpu_grid(b, cfg, nodes, algo=TENSOR)
+    rng = np.random.default_rng(12)
+    pick = [np.unique(np.concatenate([np.sort(rng.choice(len(n), 12, replace=False)), [0, len(n) - 1]]))
+            for n in nodes]
+    ref = ora.grid(cfg.model, b.offsets, b.hits, [n[p] for n, p in zip(nodes, pick)], cfg.sigma)
+    ok, worst = PU.t1_response(g[(slice(None),) + np.ix_(*pick)], ref)
+    assert ok, worst
+    gs = gpu_grid(b, cfg, nodes, algo=R.retina.GRID_SEPARABLE)
+    err = np.abs(g.astype(np.float64) - gs) / (2e-5 * np.maximum(gs, 1e-6))
+    assert err.max() <= 1.0, err.max()
+    idx, _, cnt = R.retina_find_peaks(dev(g[:1]), 3, cfg.peak_threshold, cfg.peak_capacity)
+    ok, nd, ne = PU.t4_peak_sets(idx.cpu().numpy()[0], int(cnt[0]), gs[0].astype(np.float64), 3,
+                                 cfg.peak_threshold, cfg.peak_capacity)
+    assert ok, (nd, ne)
+
+
+def test_many_events_launch_chunking():
+    """More than 65,535 events: the launchers split gridDim.y; tiny grid so the test stays small."""
+    E = 70_000
+    rng = np.random.default_rng(5)
+    counts = rng.integers(0, 4, E)
+    off = np.zeros(E + 1, np.int32)
+    off[1:] = np.cumsum(counts)
+    hits = np.zeros((int(off[-1]), 4), np.float32)
+    hits[:, 2] = rng.choice(C.VELO_PLANES[1:], len(hits))
+    hits[:, 0] = rng.uniform(-0.3, 0.3, len(hits)) * hits[:, 2]
+    hits[:, 1] = rng.uniform(-0.3, 0.3, len(hits)) * hits[:, 2]
+    b = G.EventBatch(offsets=off, hits=hits, event_ids=np.arange(E), truth=[None] * E, n_track_hits=counts)
+    nodes = [np.linspace(-0.3, 0.3, 3).astype(np.float32)] * 2
+    cfg = C.Config(name="t", model=C.SLOPE2, n_events=E, seed=0, n_tracks=0, sigma=0.44)
+    for algo in (R.retina.GRID_DIRECT, R.retina.GRID_SEPARABLE, TENSOR):
+        g = gpu_grid(b, cfg, nodes, algo=algo)
+        sel = np.r_[0:5, 65530:65540, E - 5:E]
+        sub = G.EventBatch(offsets=np.concatenate([[0], np.cumsum(counts[sel])]).astype(np.int32),
+                           hits=np.concatenate([hits[off[e]:off[e + 1]] for e in sel]), event_ids=sel,
+                           truth=[None] * len(sel), n_track_hits=counts[sel])
+        ref = ora.grid(C.SLOPE2, sub.offsets, sub.hits, nodes, 0.44)
+        ok, worst = PU.t1_response(g[sel], ref)
+        assert ok, (algo, worst)
+    seeds = np.zeros((E, 3, 2), np.float32)
+    seeds[:, :, 0] = rng.uniform(-0.3, 0.3, (E, 3))
+    th, Rr, _ = R.retina_multistart_optimize(events_of(b), C.SLOPE2, 0.44, dev(seeds), 0, 0.0, (-.3, -.3), (.3, .3))
+    torch.cuda.synchronize()
+    e = E - 1
+    for s in range(3):
+        r, _, _ = ora.point(C.SLOPE2, hits[off[e]:off[e + 1]], seeds[e, s].astype(np.float64), 0.44)
+        assert PU.t1_response(float(Rr[e, s]), r)[0]
