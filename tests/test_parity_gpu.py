@@ -561,6 +561,35 @@ def test_T1_tensor_grid_cfg4_full_size_sampled_and_peaks():
     assert ok, (nd, ne)
 
 
+@pytest.mark.parametrize("model,z_ref", [(C.SLOPE2, 0.0), (C.SLOPE2, 17.5), (C.SLOPE3, 0.0)])
+def test_multistart_and_newton_streaming_hits(model, z_ref):
+    """Events larger than the shared-memory hit stage (no size hint -> 4096-hit stage, 5000-hit
+    event) stream their hits through the double buffer on every pass; results must equal the
+    resident path bit for bit (same hit order, same arithmetic)."""
+    b = synthetic_batch(model, [5000, 300, 0], seed=21)
+    P = 3 if model == C.SLOPE3 else 2
+    lo = (-0.3, -0.3, -150.0)[:P]
+    hi = (0.3, 0.3, 150.0)[:P]
+    rng = np.random.default_rng(4)
+    seeds = np.stack([rng.uniform(l, h, (3, 700)) for l, h in zip(lo, hi)], axis=-1).astype(np.float32)
+    sigma = 0.44
+    step = C.step_slope3(sigma) if model == C.SLOPE3 else C.step_slope2(sigma)
+    res = []
+    for hint in (True, False):
+        ev = events_of(b, z_ref, hint)
+        a = R.retina_multistart_optimize(ev, model, sigma, dev(seeds), 5, step * 10, lo, hi)
+        n = R.retina_multistart_newton(ev, model, dev(seeds), [sigma * 3, sigma], [step * 9, step], sigma, 8, lo, hi)
+        torch.cuda.synchronize()
+        res.append([x.cpu().numpy() for x in a + n])
+    for x, y in zip(*res):
+        assert np.array_equal(x, y)
+    # and the streaming result is right: R at theta_out vs the oracle
+    th, Rr = res[1][0], res[1][1]
+    for s in range(0, 700, 97):
+        r, _, _ = ora.point(model, b.event_hits(0), th[0, s].astype(np.float64), sigma, z_ref=z_ref)
+        assert PU.t1_response(Rr[0, s], r)[0]
+
+
 def test_many_events_launch_chunking():
     """More than 65,535 events: the launchers split gridDim.y; tiny grid so the test stays small."""
     E = 70_000
