@@ -1,0 +1,55 @@
+"""sVELO evaluation (NEXT #2): Eq. (3) seed budget, epsilon-matching and efficiency, and the
+paper's experiment shape (efficiency vs reconstructible tracks at alpha = 1/3 and 1/10,
+PAPER.md:197-241).  Harness code: runs the CUDA path through the public binding.
+"""
+from __future__ import annotations
+
+import math
+
+import numpy as np
+
+from synth.svelo import SVELO, SveloConfig
+
+
+def direction_from_slopes(tx, ty):
+    """Unit direction (x, y, z) of the line x = tx z, y = ty z (z > 0)."""
+    tx = np.asarray(tx, np.float64)
+    ty = np.asarray(ty, np.float64)
+    n = np.sqrt(tx * tx + ty * ty + 1.0)
+    return np.stack([tx / n, ty / n, 1.0 / n], axis=-1)
+
+
+def angle_between(a_tx, a_ty, b_tx, b_ty):
+    """Angle (rad) between the directions of two lines through the origin (matching metric,
+    PAPER.md:197 'within epsilon = 1e-3 radians'), computed stably with atan2(|a x b|, a . b)."""
+    a = direction_from_slopes(a_tx, a_ty)
+    b = direction_from_slopes(b_tx, b_ty)
+    cross = np.linalg.norm(np.cross(a, b), axis=-1)
+    dot = np.sum(a * b, axis=-1)
+    return np.arctan2(cross, dot)
+
+
+def grid_cells_for_resolution(eps: float = 1e-3, cfg: SveloConfig = SVELO) -> int:
+    """n_grid of Eq. (3): cells of a slope lattice with step eps covering the
+    prior, |tx|, |ty| <= tan(max polar) (reading Z32: the kernels' lattice is in slopes)."""
+    t = math.tan(cfg.max_polar)
+    n = int(math.ceil(2.0 * t / eps)) + 1
+    return n * n
+
+
+def seed_budget(alpha: float, n_grid: int, C0: float = 30.0, q: int = 3) -> int:
+    """Eq. (3): n = alpha * n_grid * (1/C0) * (1/q)."""
+    return int(math.floor(alpha * n_grid / (C0 * q)))
+
+
+def match_efficiency(found_tx, found_ty, truth: np.ndarray, eps: float = 1e-3):
+    """a true track is reconstructed if some reported candidate lies within
+    eps radians of it.  Returns (efficiency, n_matched, n_true)."""
+    if len(truth) == 0:
+        return 1.0, 0, 0
+    if len(found_tx) == 0:
+        return 0.0, 0, len(truth)
+    ang = angle_between(truth[:, 0][:, None], truth[:, 1][:, None], np.asarray(found_tx)[None, :],
+                        np.asarray(found_ty)[None, :])
+    matched = int(np.sum(ang.min(axis=1) <= eps))
+    return matched / len(truth), matched, len(truth)

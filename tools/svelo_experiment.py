@@ -1,0 +1,170 @@
+#!/usr/bin/env python
+"""The paper's experiment shape on B200 (NEXT #2; Fig. 3): efficiency of the
+accelerated AR (Algorithm 1 with Truncated Newton and the sigma schedule 0.3 / 0.175 / 0.05 mm,
+PAPER.md:213-216) vs the number of reconstructible tracks, at seed budgets alpha = 1/3 and 1/10
+of the grid-search compute (Eq. (3)), beside the grid-search AR itself (lattice at the
+epsilon = 1e-3 resolution, peaks + sub-cell estimates) -- efficiency and measured GPU time.
+
+Readings: Z26-Z31 in synth/svelo.py; Z32 the grid lattice is in slope space
+(step eps over the prior); Z33 candidates above R0 = 1.5 at the final sigma (between the 2-hit
+floor N_min = 2 x ~0.9 and one hit); Z34 the grid-search sigma is the lattice step mapped to mm at
+the middle of the detector (Z2: eps x 350 mm) and its peaks need R >= 1.5 too; Z35 merge radius
+1e-3 per slope axis.  The figure values are placeholders in the paper: parity unpinned.
+
+    python tools/svelo_experiment.py [--events 20] [--mults 50,100,...]
+"""
+import argparse
+import json
+import math
+import os
+import sys
+import time
+
+import numpy as np
+import torch
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+from synth import configs as C  # noqa: E402
+from synth import svelo as S  # noqa: E402
+from tools import svelo_eval as EV  # noqa: E402
+import paper_1709_08610_b200 as R  # noqa: E402
+
+SIGMAS = [0.3, 0.175, 0.05]  # PAPER.md:215-216 (mm)
+R0 = 1.5                     # Z33
+EPS = 1e-3
+
+
+def timed(fn):
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    out = fn()
+    e1.record()
+    torch.cuda.synchronize()
+    return out, e0.elapsed_time(e1)
+
+
+def run(mults, n_events, alphas, C0, out_prefix):
+    cfg = S.SVELO
+    t_max = math.tan(cfg.max_polar)
+    box_lo, box_hi = (-t_max, -t_max), (t_max, t_max)
+    etas = [C.step_slope2(s, planes=cfg.layers) for s in SIGMAS]
+    n_grid = EV.grid_cells_for_resolution(EPS, cfg)
+    n_axis = int(round(math.sqrt(n_grid)))
+    nodes = [torch.linspace(-t_max, t_max, n_axis, device="cuda") for _ in range(2)]
+    sigma_grid = EPS * 350.0  # Z34
+    rows = []
+    for m in mults:
+        ids = list(range(n_events))
+        b = S.make_svelo_batch(m, ids)
+        ev = R.Events.from_numpy(b.offsets, b.hits)
+        # ---- grid-search AR: response on the eps lattice, peaks, sub-cell estimates (per event)
+        grid = torch.empty((1, n_axis, n_axis), device="cuda")
+        eff_g, t_g = [], 0.0
+        for e in range(n_events):
+            sub = R.Events(ev.offsets[e:e + 2], ev.hits, 0.0, ev.c.max_event_hits)
+
+            def grid_path():
+                R.retina_grid_response(sub, C.SLOPE2, sigma_grid, nodes, out=grid)
+                idx, val, cnt = R.retina_find_peaks(grid, 2, R0, 4096)
+                th = R.retina_estimate_peaks(grid, nodes, idx, cnt)
+                return th, cnt
+            (th, cnt), ms = timed(grid_path)
+            t_g += ms
+            k = min(int(cnt[0]), 4096)
+            est = th[0, :k].cpu().numpy().astype(np.float64)
+            eff_g.append(EV.match_efficiency(est[:, 0], est[:, 1], b.truth[e], EPS)[0])
+        row = {"n_reco": m, "events": n_events, "hits_per_event": float(b.n_hits) / n_events,
+               "grid": {"cells": n_axis * n_axis, "sigma_mm": sigma_grid, "efficiency": float(np.mean(eff_g)),
+                        "ms_per_event": t_g / n_events}}
+        for alpha in alphas:
+            n_seeds = EV.seed_budget(alpha, n_grid, C0=C0, q=len(SIGMAS))
+            seeds = torch.from_numpy(S.svelo_seeds(m, ids, n_seeds)).cuda()
+
+            def ms_path():
+                th, Rr, _ = R.retina_multistart_newton(ev, C.SLOPE2, seeds, SIGMAS, etas, SIGMAS[-1], 8, box_lo,
+                                                       box_hi, want_grad=False)
+                out = R.retina_merge_tracks(th, Rr, (EPS, EPS), R0, 2048)
+                return out
+            (tt, tr, ts, tz, tc), ms = timed(ms_path)
+            tt, tc = tt.cpu().numpy(), tc.cpu().numpy()
+            effs = []
+            for e in range(n_events):
+                k = min(int(tc[e]), 2048)
+                effs.append(EV.match_efficiency(tt[e, :k, 0], tt[e, :k, 1], b.truth[e], EPS)[0])
+            row[f"alpha_{alpha:.4f}"] = {"n_seeds": n_seeds, "efficiency": float(np.mean(effs)),
+                                         "ms_per_event": ms / n_events,
+                                         "tracks_per_event": float(np.mean(tc))}
+        rows.append(row)
+        print(json.dumps(row), flush=True)
+    res = {"readings": "Z26-Z35 (DESIGN.md §3)", "sigmas_mm": SIGMAS, "R0": R0, "eps": EPS, "C0": C0,
+           "n_grid": n_grid, "rows": rows}
+    json.dump(res, open(out_prefix + ".json", "w"), indent=1)
+    with open(out_prefix + ".md", "w") as f:
+        f.write("# sVELO experiment (PAPER.md Fig. 3 shape) on one B200\n\n")
+        f.write(f"n_grid = {n_grid} slope cells at eps = {EPS}; seeds by Eq. (3) with C0 = {C0}, q = 3; "
+                f"sigma schedule {SIGMAS} mm; R0 = {R0}; {n_events} events per multiplicity.\n\n")
+        hdr = "| reconstructible tracks | hits/event | grid eff | grid ms/event |"
+        sep = "|---|---|---|---|"
+        for alpha in alphas:
+            hdr += f" alpha={alpha:.3g} seeds | eff | ms/event |"
+            sep += "---|---|---|"
+        f.write(hdr + "\n" + sep + "\n")
+        for r in rows:
+            line = (f"| {r['n_reco']} | {r['hits_per_event']:.0f} | {r['grid']['efficiency']:.3f} | "
+                    f"{r['grid']['ms_per_event']:.3f} |")
+            for alpha in alphas:
+                a = r[f"alpha_{alpha:.4f}"]
+                line += f" {a['n_seeds']} | {a['efficiency']:.3f} | {a['ms_per_event']:.3f} |"
+            f.write(line + "\n")
+    return res
+
+
+def sweep(m, n_events, alphas, C0, out_prefix):
+    """Efficiency and time vs seed budget at one multiplicity: where does the accelerated AR
+    reach the grid's efficiency?  Candidates = converged seeds with R >= R0 (no merge, so
+    budgets above the merge kernel's 16,384-seed limit can be run); efficiency counts a true
+    track as found if any candidate is within eps (the merge would keep one of them)."""
+    cfg = S.SVELO
+    t_max = math.tan(cfg.max_polar)
+    etas = [C.step_slope2(s, planes=cfg.layers) for s in SIGMAS]
+    n_grid = EV.grid_cells_for_resolution(EPS, cfg)
+    ids = list(range(n_events))
+    b = S.make_svelo_batch(m, ids)
+    ev = R.Events.from_numpy(b.offsets, b.hits)
+    rows = []
+    for alpha in alphas:
+        n_seeds = EV.seed_budget(alpha, n_grid, C0=C0, q=len(SIGMAS))
+        seeds = torch.from_numpy(S.svelo_seeds(m, ids, n_seeds)).cuda()
+        (th, Rr, _), ms = timed(lambda: R.retina_multistart_newton(
+            ev, C.SLOPE2, seeds, SIGMAS, etas, SIGMAS[-1], 8, (-t_max, -t_max), (t_max, t_max), want_grad=False))
+        th, Rr = th.cpu().numpy(), Rr.cpu().numpy()
+        effs = []
+        for e in range(n_events):
+            keep = Rr[e] >= R0
+            effs.append(EV.match_efficiency(th[e, keep, 0], th[e, keep, 1], b.truth[e], EPS)[0])
+        rows.append({"alpha": alpha, "n_seeds": n_seeds, "efficiency": float(np.mean(effs)),
+                     "ms_per_event": ms / n_events})
+        print(json.dumps(rows[-1]), flush=True)
+    json.dump({"n_reco": m, "events": n_events, "C0": C0, "rows": rows}, open(out_prefix + ".json", "w"), indent=1)
+    with open(out_prefix + ".md", "w") as f:
+        f.write(f"# sVELO seed-budget sweep, {m} reconstructible tracks, {n_events} events\n\n"
+                "| alpha (Eq. 3, C0 = %g, q = 3) | seeds | efficiency | ms/event |\n|---|---|---|---|\n" % C0)
+        for r in rows:
+            f.write(f"| {r['alpha']:.3g} | {r['n_seeds']} | {r['efficiency']:.3f} | {r['ms_per_event']:.3f} |\n")
+    return rows
+
+
+if __name__ == "__main__":
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--events", type=int, default=20)
+    ap.add_argument("--mults", default="50,100,150,200,250,300,350")
+    ap.add_argument("--C0", type=float, default=30.0)
+    ap.add_argument("--out", default=os.path.join(ROOT, "profiles", "r1_svelo_experiment"))
+    ap.add_argument("--sweep", action="store_true", help="seed-budget sweep at 150 tracks instead")
+    a = ap.parse_args()
+    if a.sweep:
+        sweep(150, a.events, [0.1, 1 / 3, 1.0, 3.0, 10.0, 30.0], a.C0, a.out + "_sweep")
+    else:
+        run([int(x) for x in a.mults.split(",")], a.events, [1 / 3, 1 / 10], a.C0, a.out)
