@@ -40,18 +40,70 @@ __global__ void k_ffma2(float *out, int iters) {
     if (s == 1234.5f) out[0] = s;
 }
 
+// 3 distinct register operands per FMA (no immediates, no repeated registers)
+__global__ void k_ffma_3reg(float *out, int iters) {
+    float a[8], b[8], c[8];
+    for (int i = 0; i < 8; ++i) {  // runtime values: no immediate forms
+        a[i] = threadIdx.x + i;
+        b[i] = 1.0f + out[1 + i] * (i + 1);
+        c[i] = out[9 + i] * (i + threadIdx.x);
+    }
+    for (int it = 0; it < iters; ++it) {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) a[i] = __fmaf_rn(a[i], b[i], c[i]);
+    }
+    float s = 0; for (int i = 0; i < 8; ++i) s += a[i] + b[i] + c[i];
+    if (s == 1234.5f) out[0] = s;
+}
+
+// FFMA2 with three distinct register pairs
+__global__ void k_ffma2_3pair(float *out, int iters) {
+    float2 a[8], b[8], c[8];
+    for (int i = 0; i < 8; ++i) {
+        a[i] = make_float2(threadIdx.x + i, i);
+        b[i] = make_float2(1.0f + out[1 + i], 1.0f - out[1 + i]);
+        c[i] = make_float2(out[9 + i] * (i + threadIdx.x), out[9 + i] * i);
+    }
+    for (int it = 0; it < iters; ++it) {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) a[i] = __ffma2_rn(a[i], b[i], c[i]);
+    }
+    float s = 0; for (int i = 0; i < 8; ++i) s += a[i].x + a[i].y + b[i].x + c[i].y;
+    if (s == 1234.5f) out[0] = s;
+}
+
+// FFMA2 with a broadcast scalar (per-i) and two register pairs
+__global__ void k_ffma2_bcast(float *out, int iters) {
+    float2 a[8], c[8];
+    float b[8];
+    for (int i = 0; i < 8; ++i) {
+        a[i] = make_float2(threadIdx.x + i, i);
+        b[i] = 1.0f + out[1 + i] * (i + threadIdx.x);
+        c[i] = make_float2(out[9 + i] * (i + threadIdx.x), out[9 + i] * i);
+    }
+    for (int it = 0; it < iters; ++it) {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) a[i] = __ffma2_rn(a[i], make_float2(b[i], b[i]), c[i]);
+    }
+    float s = 0; for (int i = 0; i < 8; ++i) s += a[i].x + a[i].y + b[i] + c[i].y;
+    if (s == 1234.5f) out[0] = s;
+}
+
 int main() {
     int dev = 0, sms = 0, clk = 0;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     cudaDeviceGetAttribute(&clk, cudaDevAttrClockRate, dev);
     float *out;
-    cudaMalloc(&out, 4);
+    cudaMalloc(&out, 64 * sizeof(float));
+    cudaMemset(out, 0, 64 * sizeof(float));
     const int iters = 20000, threads = 512, blocks = sms * 4;
     cudaEvent_t a, b;
     cudaEventCreate(&a);
     cudaEventCreate(&b);
     struct { const char *name; void (*k)(float *, int); double ops_per_elem; } ks[] = {
-        {"ex2 (+1 FMUL)", k_ex2, 1.0}, {"ffma", k_ffma, 1.0}, {"ffma2 (2 FMA each)", k_ffma2, 2.0}};
+        {"ex2 (+1 FMUL)", k_ex2, 1.0}, {"ffma", k_ffma, 1.0}, {"ffma2 (2 FMA each)", k_ffma2, 2.0},
+        {"ffma 3 distinct regs", k_ffma_3reg, 1.0}, {"ffma2 3 distinct pairs", k_ffma2_3pair, 2.0},
+        {"ffma2 broadcast scalar", k_ffma2_bcast, 2.0}};
     for (auto &kk : ks) {
         kk.k<<<blocks, threads>>>(out, 100);
         cudaEventRecord(a);
