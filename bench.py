@@ -56,6 +56,8 @@ def args_():
     ap.add_argument("--e2e-steps", type=int, default=None)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample-events", type=int, default=3)
+    ap.add_argument("--no-graph", dest="graph", action="store_false",
+                    help="skip the CUDA-graph replay measurement")
     ap.add_argument("--update", default="gradient", choices=["gradient", "newton"],
                     help="multi-start update: BASELINE fixed-step ascent, or the paper's Truncated Newton")
     return ap.parse_args()
@@ -237,6 +239,24 @@ def main():
     ms_max = float(t.item())
     ms_step = ms_max / a.steps
 
+    # ---- the same hot path replayed from a CUDA graph (all kernel launches of one pass)
+    graph_ms = None
+    if a.graph:
+        graph = pipe.capture(dbatch)
+        graph.replay()
+        torch.cuda.synchronize()
+        g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        g0.record(stream)
+        for _ in range(a.steps):
+            graph.replay()
+        g1.record(stream)
+        torch.cuda.synchronize()
+        tg = torch.tensor([g0.elapsed_time(g1) / a.steps], device="cuda")
+        if world > 1:
+            dist.all_reduce(tg, op=dist.ReduceOp.MAX)
+        graph_ms = float(tg.item())
+        del graph
+
     # ---- e2e through the public API with host buffers (pinned H2D + D2H inside the region)
     e2e_steps = a.e2e_steps if a.e2e_steps is not None else max(1, min(a.steps, 3))
     off_h = torch.from_numpy(batch.offsets).pin_memory()
@@ -345,6 +365,10 @@ def main():
         "e2e": {"value": total_pairs / (e2e_ms_step * 1e-3), "unit": UNIT, "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms_step},
         "gpu_launches": launches,
+        "cuda_graph": (None if graph_ms is None else
+                       {"ms_per_step_without_gather": graph_ms,
+                        "value": (pairs_grid + pairs_ms) * world / (graph_ms * 1e-3),
+                        "note": "the pass replayed from one captured CUDA graph (no result pack/gather)"}),
         "gen_seconds": gen_s,
     }
     if world == 1 and not a.no_cpu_baseline:

@@ -9,6 +9,10 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <map>
+#include <mutex>
+#include <utility>
+
 #if defined(__CUDA_ARCH__) && (__CUDA_ARCH__ < 1000)
 #error "retina kernels target sm_100a only"
 #endif
@@ -16,6 +20,29 @@
 namespace retina {
 
 constexpr int kMaxStageHits = 12288;  // 192 KiB of float4 hits per CTA at most
+
+// Raises a kernel's dynamic shared-memory limit once per (device, kernel, size): the only state
+// the library keeps is this attribute cache, keyed by the kernel's address.  Skipping the call
+// when the limit is already high enough keeps launches free of non-stream API calls, so a
+// sequence of retina calls can be captured into a CUDA graph.
+inline cudaError_t ensure_dynamic_smem_impl(const void *kern, size_t bytes) {
+    static std::mutex mu;
+    static std::map<std::pair<int, const void *>, int> granted;
+    int dev = 0;
+    cudaError_t err = cudaGetDevice(&dev);
+    if (err != cudaSuccess) return err;
+    std::lock_guard<std::mutex> lock(mu);
+    auto it = granted.find({dev, kern});
+    if (it != granted.end() && (int)bytes <= it->second) return cudaSuccess;
+    err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+    if (err == cudaSuccess) granted[{dev, kern}] = (int)bytes;
+    return err;
+}
+
+template <class Kernel>
+inline cudaError_t ensure_dynamic_smem(Kernel kern, size_t bytes) {
+    return ensure_dynamic_smem_impl(reinterpret_cast<const void *>(kern), bytes);
+}
 
 __device__ __forceinline__ float ex2_approx(float x) {
     float y;

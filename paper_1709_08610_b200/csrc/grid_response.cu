@@ -141,7 +141,7 @@ template <int MODEL, int U, bool ZREF>
 static cudaError_t launch_grid(const GridArgs &a0, int n_events, cudaStream_t stream) {
     auto kern = grid_response_kernel<MODEL, U, ZREF>;
     const size_t smem = (size_t)a0.cap * sizeof(float4);
-    cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaError_t err = ensure_dynamic_smem(kern, smem);
     if (err != cudaSuccess) return err;
     long long tiles;
     if (MODEL == kSlope3)

@@ -140,7 +140,7 @@ template <int MODEL, bool ZREF>
 static cudaError_t launch_sep(const GridArgs &a0, int n_events, cudaStream_t stream) {
     auto kern = grid_separable_kernel<MODEL, ZREF>;
     const size_t smem = (size_t)a0.cap * sizeof(float4);
-    cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaError_t err = ensure_dynamic_smem(kern, smem);
     if (err != cudaSuccess) return err;
     const long long tiles = (long long)((a0.n0 + SB_M - 1) / SB_M) * ((a0.n1 + SB_N - 1) / SB_N) *
                             (MODEL == kSlope3 ? a0.n2 : 1);

@@ -239,7 +239,7 @@ static cudaError_t launch_tc(const GridArgs &a0, int n_events, cudaStream_t stre
     GridArgs a = a0;
     a.cap = min(a.cap, tensor_max_stage_hits()) & ~1;
     const size_t smem = 2 * (size_t)TC_STAGE_BYTES + (size_t)a.cap * sizeof(float4);
-    cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaError_t err = ensure_dynamic_smem(kern, smem);
     if (err != cudaSuccess) return err;
     const long long tiles =
         (long long)((a.n0 + TC_M - 1) / TC_M) * ((a.n1 + TC_N - 1) / TC_N) * (MODEL == kSlope3 ? a.n2 : 1);

@@ -179,8 +179,7 @@ cudaError_t launch_merge(const MergeArgs &a0, int n_events, cudaStream_t stream)
     int M = 1;
     while (M < a0.n_seeds) M <<= 1;
     const size_t smem = (size_t)M * sizeof(uint64_t);
-    cudaError_t err =
-        cudaFuncSetAttribute(merge_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaError_t err = ensure_dynamic_smem(merge_kernel, smem);
     if (err != cudaSuccess) return err;
     MergeArgs a = a0;
     a.e_base = 0;

@@ -315,7 +315,7 @@ static cudaError_t launch_ms(const MultistartArgs &a0, int n_events, cudaStream_
     constexpr int S = (MODEL == kSlope3) ? RETINA_MS3_SEEDS : RETINA_MS_SEEDS;
     auto kern = multistart_kernel<MODEL, S, ZREF>;
     const size_t smem = (size_t)a0.cap * sizeof(float4);
-    cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaError_t err = ensure_dynamic_smem(kern, smem);
     if (err != cudaSuccess) return err;
     const int blocks = (a0.n_seeds + kMsThreads * S - 1) / (kMsThreads * S);
     for (int e0 = 0; e0 < n_events; e0 += 65535) {

@@ -333,7 +333,7 @@ static cudaError_t launch_nt(const NewtonArgs &a0, int n_events, cudaStream_t st
     constexpr int S = (MODEL == kSlope3) ? 2 : 4;
     auto kern = newton_kernel<MODEL, S, ZREF>;
     const size_t smem = (size_t)a0.cap * sizeof(float4);
-    cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaError_t err = ensure_dynamic_smem(kern, smem);
     if (err != cudaSuccess) return err;
     const int blocks = (a0.n_seeds + kNtThreads * S - 1) / (kNtThreads * S);
     for (int e0 = 0; e0 < n_events; e0 += 65535) {

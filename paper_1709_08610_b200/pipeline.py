@@ -128,7 +128,7 @@ class RetinaPipeline:
                                     out=self.peak_theta[e0:e1], stream=stream)
             if timer is not None:
                 timer.stop("peaks")
-            self.launches += 3
+            self.launches += 3 + (1 if self.peak_ws is not None else 0)  # slab peaks = 2 kernels
 
     def run_multistart(self, batch: DeviceBatch, stream=None, timer=None):
         sp = self.spec
@@ -160,6 +160,21 @@ class RetinaPipeline:
             self.run_grid(batch, stream, timer)
         if self.spec.n_seeds:
             self.run_multistart(batch, stream, timer)
+
+    def capture(self, batch: DeviceBatch) -> "torch.cuda.CUDAGraph":
+        """Records one whole pass (every kernel launch of run()) into a CUDA graph; replaying it
+        re-runs the hot path on whatever is in `batch`'s device buffers, with no host work per
+        launch.  The library keeps no launch-time state besides its smem-attribute cache, which
+        the eager warm-up pass fills, so capture contains kernel launches only."""
+        side = torch.cuda.Stream(self.device)
+        side.wait_stream(torch.cuda.current_stream(self.device))
+        with torch.cuda.stream(side):
+            self.run(batch)  # warm-up outside capture (attribute cache, lazy module loading)
+        torch.cuda.current_stream(self.device).wait_stream(side)
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph):
+            self.run(batch)
+        return graph
 
 
 class PhaseTimer:

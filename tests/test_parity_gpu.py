@@ -590,6 +590,55 @@ def test_multistart_and_newton_streaming_hits(model, z_ref):
         assert PU.t1_response(Rr[0, s], r)[0]
 
 
+@pytest.mark.parametrize("name", ["cfg2", "cfg3", "cfg4"])
+def test_pipeline_cuda_graph_replay_bitwise(name):
+    """The whole pass captured in a CUDA graph and replayed gives the eager results bit for bit;
+    replaying after new inputs are copied into the batch buffers recomputes them."""
+    from paper_1709_08610_b200.pipeline import RetinaPipeline, upload
+    import bench
+    cfg = C.CONFIGS[name]
+    if name == "cfg2":
+        cfg = cfg.replace(axes=((-0.3, 0.3, 64), (-0.3, 0.3, 64)))
+    if name == "cfg4":
+        cfg = cfg.replace(n_seeds=1024)
+    E = 3
+    b = G.make_batch(cfg, range(E))
+    sd = G.make_seeds(cfg, range(E))
+    spec = bench.make_spec(cfg)
+    pipe = RetinaPipeline(spec, E, chunk_events=2)
+    db = upload(b.offsets, b.hits, sd)
+    pipe.run(db)
+    torch.cuda.synchronize()
+    outs = [pipe.peak_cnt, pipe.peak_idx, pipe.peak_theta, pipe.theta, pipe.resp, pipe.t_count, pipe.t_seed]
+    eager = [x[:E].clone() for x in outs]
+    for x in outs:
+        x.zero_()
+    g = pipe.capture(db)
+    for x in outs:
+        x.zero_()
+    g.replay()
+    torch.cuda.synchronize()
+    pc, tc = eager[0].cpu().numpy(), eager[5].cpu().numpy()
+    assert torch.equal(outs[0][:E], eager[0]) and torch.equal(outs[5][:E], eager[5])
+    assert torch.equal(outs[3][:E], eager[3]) and torch.equal(outs[4][:E], eager[4])
+    for e in range(E):  # list entries past the true counts are unspecified
+        k = min(int(pc[e]), spec.peak_capacity)
+        assert torch.equal(outs[1][e, :k], eager[1][e, :k]) and torch.equal(outs[2][e, :k], eager[2][e, :k])
+        k = min(int(tc[e]), spec.track_capacity)
+        assert torch.equal(outs[6][e, :k], eager[6][e, :k])
+    # new inputs into the same device buffers: the replay follows them
+    b2 = G.make_batch(cfg, range(E, 2 * E))
+    if b2.n_hits <= db.hits.shape[0]:
+        db.offsets.copy_(torch.from_numpy(b2.offsets))
+        db.hits[:b2.n_hits].copy_(torch.from_numpy(b2.hits))
+        g.replay()
+        torch.cuda.synchronize()
+        ref = RetinaPipeline(spec, E, chunk_events=2)
+        ref.run(upload(b2.offsets, b2.hits, sd))
+        torch.cuda.synchronize()
+        assert torch.equal(pipe.theta[:E], ref.theta[:E]) and torch.equal(pipe.peak_cnt[:E], ref.peak_cnt[:E])
+
+
 def test_many_events_launch_chunking():
     """More than 65,535 events: the launchers split gridDim.y; tiny grid so the test stays small."""
     E = 70_000
