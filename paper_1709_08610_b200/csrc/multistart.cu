@@ -33,6 +33,9 @@ namespace retina {
 #define RETINA_MS3_MINB 6
 #endif
 constexpr int kMsThreads = RETINA_MS_THREADS;
+#ifndef RETINA_MS3_CX
+#define RETINA_MS3_CX 1  // SLOPE3: per-plane -t d_lo folded by FADD2 (+3 % measured on cfg4)
+#endif
 
 template <int MODEL, int S, bool ZREF, bool GRAD>
 __device__ __forceinline__ void ms_pass(HitStage &st, const float (&th)[S][3], float negK, float zref,
@@ -150,6 +153,11 @@ __device__ __forceinline__ void ms_pass_x2(HitStage &st, const float (&th)[S][3]
     constexpr int NP = S / 2;
     float2 mtx[NP], mty[NP], r2[NP], qx[NP], qy[NP], gx[NP], gy[NP], ax[NP], ay[NP], dh[NP], dl[NP];
     const float2 zero = make_float2(0.f, 0.f);
+#if RETINA_MS3_CX
+    float2 cx[NP], cy[NP];
+#pragma unroll
+    for (int p = 0; p < NP; ++p) cx[p] = cy[p] = zero;
+#endif
 #pragma unroll
     for (int p = 0; p < NP; ++p) {
         mtx[p] = make_float2(-th[2 * p][0], -th[2 * p + 1][0]);
@@ -184,6 +192,10 @@ __device__ __forceinline__ void ms_pass_x2(HitStage &st, const float (&th)[S][3]
                     for (int p = 0; p < NP; ++p) {
                         two_sum(hk.z, -th[2 * p][2], dh[p].x, dl[p].x);
                         two_sum(hk.z, -th[2 * p + 1][2], dh[p].y, dl[p].y);
+#if RETINA_MS3_CX
+                        cx[p] = __fmul2_rn(mtx[p], dl[p]);  // -t d_lo: constant over the plane
+                        cy[p] = __fmul2_rn(mty[p], dl[p]);
+#endif
                     }
                 } else if (ZREF) {
                     two_sum(hk.z, -zref, dprev, dlprev);
@@ -196,8 +208,15 @@ __device__ __forceinline__ void ms_pass_x2(HitStage &st, const float (&th)[S][3]
             for (int p = 0; p < NP; ++p) {
                 float2 sx, sy;
                 if (MODEL == kSlope3) {
+#if RETINA_MS3_CX
+                    // (x - t d_hi) rounded once (error relative to |s + t d_lo| ~ |s|), then the
+                    // per-plane constant -t d_lo: an FADD2 of two pairs instead of a 3-pair FFMA2
+                    sx = __fadd2_rn(__ffma2_rn(mtx[p], dh[p], X), cx[p]);
+                    sy = __fadd2_rn(__ffma2_rn(mty[p], dh[p], Y), cy[p]);
+#else
                     sx = __ffma2_rn(mtx[p], dl[p], __ffma2_rn(mtx[p], dh[p], X));
                     sy = __ffma2_rn(mty[p], dl[p], __ffma2_rn(mty[p], dh[p], Y));
+#endif
                 } else if (ZREF) {
                     const float2 D = make_float2(dprev, dprev), DL = make_float2(dlprev, dlprev);
                     sx = __ffma2_rn(mtx[p], DL, __ffma2_rn(mtx[p], D, X));
