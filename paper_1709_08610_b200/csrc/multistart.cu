@@ -33,6 +33,10 @@ namespace retina {
 #define RETINA_MS3_MINB 6
 #endif
 constexpr int kMsThreads = RETINA_MS_THREADS;
+#ifndef RETINA_MS_POLY  // bit u*NP+p: seed pair p of the u-th hit of each two takes ex2_poly2 (FMA pipe)
+#define RETINA_MS_POLY 0
+#endif
+constexpr unsigned kPolyMask = RETINA_MS_POLY;
 #ifndef RETINA_MS3_CX
 #define RETINA_MS3_CX 1  // SLOPE3: per-plane -t d_lo folded by FADD2 (+3 % measured on cfg4)
 #endif
@@ -146,6 +150,11 @@ __device__ __forceinline__ void ms_pass(HitStage &st, const float (&th)[S][3], f
 // is an independent IEEE round-to-nearest operation, so results are bit-identical to the
 // scalar ms_pass.  Per (seed, hit): 8 FMA-pipe lane-ops + 1 MUFU.EX2, i.e. the loop is
 // balanced between the FMA pipe (128 lanes/clk/SM) and MUFU (16/clk/SM).
+template <int V>
+struct IC {
+    static constexpr int v = V;
+};
+
 template <int MODEL, int S, bool ZREF, bool GRAD, bool WANT_R>
 __device__ __forceinline__ void ms_pass_x2(HitStage &st, const float (&th)[S][3], float negK, float zref,
                                            float (&R)[S], float (&G)[S][4]) {
@@ -180,61 +189,68 @@ __device__ __forceinline__ void ms_pass_x2(HitStage &st, const float (&th)[S][3]
             qx[p] = qy[p] = zero;
         }
     };
-    st.pass([&](const float4 *h, int len) {
-#pragma unroll 2
-        for (int k = 0; k < len; ++k) {
-            const float4 hk = h[k];
-            if (hk.z != zprev) {  // warp-uniform plane change
-                if (GRAD) flush();
-                zprev = hk.z;
-                if (MODEL == kSlope3) {
+    // one hit; U = position of the hit in its group of two (selects the FMA-pipe exponentials)
+    auto hit = [&](const float4 hk, auto U) {
+        if (hk.z != zprev) {  // warp-uniform plane change
+            if (GRAD) flush();
+            zprev = hk.z;
+            if (MODEL == kSlope3) {
 #pragma unroll
-                    for (int p = 0; p < NP; ++p) {
-                        two_sum(hk.z, -th[2 * p][2], dh[p].x, dl[p].x);
-                        two_sum(hk.z, -th[2 * p + 1][2], dh[p].y, dl[p].y);
+                for (int p = 0; p < NP; ++p) {
+                    two_sum(hk.z, -th[2 * p][2], dh[p].x, dl[p].x);
+                    two_sum(hk.z, -th[2 * p + 1][2], dh[p].y, dl[p].y);
 #if RETINA_MS3_CX
-                        cx[p] = __fmul2_rn(mtx[p], dl[p]);  // -t d_lo: constant over the plane
-                        cy[p] = __fmul2_rn(mty[p], dl[p]);
+                    cx[p] = __fmul2_rn(mtx[p], dl[p]);  // -t d_lo: constant over the plane
+                    cy[p] = __fmul2_rn(mty[p], dl[p]);
 #endif
-                    }
-                } else if (ZREF) {
-                    two_sum(hk.z, -zref, dprev, dlprev);
-                } else {
-                    dprev = hk.z;
                 }
-            }
-            const float2 X = make_float2(hk.x, hk.x), Y = make_float2(hk.y, hk.y);
-#pragma unroll
-            for (int p = 0; p < NP; ++p) {
-                float2 sx, sy;
-                if (MODEL == kSlope3) {
-#if RETINA_MS3_CX
-                    // (x - t d_hi) rounded once (error relative to |s + t d_lo| ~ |s|), then the
-                    // per-plane constant -t d_lo: an FADD2 of two pairs instead of a 3-pair FFMA2
-                    sx = __fadd2_rn(__ffma2_rn(mtx[p], dh[p], X), cx[p]);
-                    sy = __fadd2_rn(__ffma2_rn(mty[p], dh[p], Y), cy[p]);
-#else
-                    sx = __ffma2_rn(mtx[p], dl[p], __ffma2_rn(mtx[p], dh[p], X));
-                    sy = __ffma2_rn(mty[p], dl[p], __ffma2_rn(mty[p], dh[p], Y));
-#endif
-                } else if (ZREF) {
-                    const float2 D = make_float2(dprev, dprev), DL = make_float2(dlprev, dlprev);
-                    sx = __ffma2_rn(mtx[p], DL, __ffma2_rn(mtx[p], D, X));
-                    sy = __ffma2_rn(mty[p], DL, __ffma2_rn(mty[p], D, Y));
-                } else {
-                    const float2 Z = make_float2(hk.z, hk.z);
-                    sx = __ffma2_rn(mtx[p], Z, X);
-                    sy = __ffma2_rn(mty[p], Z, Y);
-                }
-                const float2 a = __fmul2_rn(__ffma2_rn(sx, sx, __fmul2_rn(sy, sy)), nk);
-                const float2 w = make_float2(ex2_approx(a.x), ex2_approx(a.y));
-                if (WANT_R) r2[p] = __fadd2_rn(r2[p], w);  // iterations only need grad R
-                if (GRAD) {
-                    qx[p] = __ffma2_rn(w, sx, qx[p]);
-                    qy[p] = __ffma2_rn(w, sy, qy[p]);
-                }
+            } else if (ZREF) {
+                two_sum(hk.z, -zref, dprev, dlprev);
+            } else {
+                dprev = hk.z;
             }
         }
+        const float2 X = make_float2(hk.x, hk.x), Y = make_float2(hk.y, hk.y);
+#pragma unroll
+        for (int p = 0; p < NP; ++p) {
+            float2 sx, sy;
+            if (MODEL == kSlope3) {
+#if RETINA_MS3_CX
+                // (x - t d_hi) rounded once (error relative to |s + t d_lo| ~ |s|), then the
+                // per-plane constant -t d_lo: an FADD2 of two pairs instead of a 3-pair FFMA2
+                sx = __fadd2_rn(__ffma2_rn(mtx[p], dh[p], X), cx[p]);
+                sy = __fadd2_rn(__ffma2_rn(mty[p], dh[p], Y), cy[p]);
+#else
+                sx = __ffma2_rn(mtx[p], dl[p], __ffma2_rn(mtx[p], dh[p], X));
+                sy = __ffma2_rn(mty[p], dl[p], __ffma2_rn(mty[p], dh[p], Y));
+#endif
+            } else if (ZREF) {
+                const float2 D = make_float2(dprev, dprev), DL = make_float2(dlprev, dlprev);
+                sx = __ffma2_rn(mtx[p], DL, __ffma2_rn(mtx[p], D, X));
+                sy = __ffma2_rn(mty[p], DL, __ffma2_rn(mty[p], D, Y));
+            } else {
+                const float2 Z = make_float2(hk.z, hk.z);
+                sx = __ffma2_rn(mtx[p], Z, X);
+                sy = __ffma2_rn(mty[p], Z, Y);
+            }
+            const float2 a = __fmul2_rn(__ffma2_rn(sx, sx, __fmul2_rn(sy, sy)), nk);
+            const float2 w = ((kPolyMask >> (decltype(U)::v * NP + p)) & 1)
+                                 ? ex2_poly2(a)
+                                 : make_float2(ex2_approx(a.x), ex2_approx(a.y));
+            if (WANT_R) r2[p] = __fadd2_rn(r2[p], w);  // iterations only need grad R
+            if (GRAD) {
+                qx[p] = __ffma2_rn(w, sx, qx[p]);
+                qy[p] = __ffma2_rn(w, sy, qy[p]);
+            }
+        }
+    };
+    st.pass([&](const float4 *h, int len) {
+        int k = 0;
+        for (; k + 1 < len; k += 2) {
+            hit(h[k], IC<0>{});
+            hit(h[k + 1], IC<1>{});
+        }
+        if (k < len) hit(h[k], IC<0>{});
     });
     if (GRAD) flush();
 #pragma unroll
