@@ -219,8 +219,99 @@ __device__ __forceinline__ void nt_direction(const float (&g)[3], const float (&
     for (int a = 0; a < 3; ++a) p[a] = (a < P) ? x[a] : 0.f;
 }
 
+// Shared state of the compacted line search: per seed slot (owner thread t, seed s -> slot
+// s * kNtThreads + t) the base point, direction, R0 and Armijo slope, and two queues of slots.
+template <int S, int P>
+struct LineSearchSmem {
+    float base[kNtThreads * S][P];  // theta before the step; the accepted trial overwrites it
+    float dir[kNtThreads * S][P];
+    float R0[kNtThreads * S], slope[kNtThreads * S];
+    int q[2][kNtThreads * S];
+    int nq[2];
+};
+
+// Halvings k = 1 .. max_halvings for the seeds still active after the alpha = 1 trial.
+// Worker thread (warp w, lane l) takes queue entries w * 32 SQ + s * 32 + l, s < SQ; warps past
+// the queue's end skip the pass.  Needs the hits resident (pass() then has no barrier).
+#ifndef RETINA_NT_SQ
+#define RETINA_NT_SQ 1  // queue entries per worker thread (1 measured best: C0 5.3 vs 6.0 (2), 7.8 (4) on cfg3)
+#endif
 template <int MODEL, int S, bool ZREF>
-__global__ void __launch_bounds__(kNtThreads) newton_kernel(NewtonArgs a) {
+__device__ __forceinline__ void nt_line_search_queue(HitStage &st, const NewtonArgs &a, float negK, float (&th)[S][3],
+                                                     const float (&p)[S][3], const float (&R0)[S],
+                                                     const float (&slope)[S], const bool (&active)[S],
+                                                     LineSearchSmem<S, (MODEL == kSlope3) ? 3 : 2> &ls) {
+    constexpr int P = (MODEL == kSlope3) ? 3 : 2;
+    constexpr int SQ = RETINA_NT_SQ < S ? RETINA_NT_SQ : S;
+    const int tid = threadIdx.x, lane = tid & 31, wbase = (tid >> 5) * 32 * SQ;
+    __syncthreads();  // previous users of ls are done
+    if (tid == 0) ls.nq[0] = ls.nq[1] = 0;
+    __syncthreads();
+#pragma unroll
+    for (int s = 0; s < S; ++s) {
+        if (!active[s]) continue;
+        const int slot = s * kNtThreads + tid;
+#pragma unroll
+        for (int i = 0; i < P; ++i) {
+            ls.base[slot][i] = th[s][i];
+            ls.dir[slot][i] = p[s][i];
+        }
+        ls.R0[slot] = R0[s];
+        ls.slope[slot] = slope[s];
+        ls.q[0][atomicAdd(&ls.nq[0], 1)] = slot;
+    }
+    __syncthreads();
+    int cur = 0;
+    float alpha = 1.f;
+    for (int k = 1; k <= a.max_halvings; ++k) {
+        alpha *= 0.5f;
+        const int n = ls.nq[cur];  // final: written before the last barrier
+        if (n == 0) break;
+        for (int wb = wbase; wb < n; wb += kNtThreads * SQ) {  // n may exceed one sweep of the CTA
+            int slot[SQ];
+            float tt[SQ][3];
+#pragma unroll
+            for (int s = 0; s < SQ; ++s) {
+                const int e = wb + s * 32 + lane;
+                slot[s] = (e < n) ? ls.q[cur][e] : -1;
+                const int src = (e < n) ? slot[s] : ls.q[cur][0];  // padding lanes repeat entry 0
+#pragma unroll
+                for (int i = 0; i < 3; ++i)
+                    tt[s][i] = (i < P) ? fminf(fmaxf(__fmaf_rn(alpha, ls.dir[src][i], ls.base[src][i]), a.lo[i]),
+                                               a.hi[i])
+                                       : 0.f;
+            }
+            float Rt[SQ], Gd[SQ][4];
+            nt_pass_r<MODEL, SQ, ZREF, false>(st, tt, negK, a.z_ref, Rt, Gd);
+#pragma unroll
+            for (int s = 0; s < SQ; ++s) {
+                if (slot[s] < 0) continue;
+                const int sl = slot[s];
+                if (Rt[s] >= __fmaf_rn(1e-4f * alpha, ls.slope[sl], ls.R0[sl])) {
+#pragma unroll
+                    for (int i = 0; i < P; ++i) ls.base[sl][i] = tt[s][i];
+                } else {
+                    ls.q[cur ^ 1][atomicAdd(&ls.nq[cur ^ 1], 1)] = sl;
+                }
+            }
+        }
+        __syncthreads();  // all reads of queue cur and all pushes to cur ^ 1 are done
+        if (tid == 0) ls.nq[cur] = 0;
+        cur ^= 1;
+        __syncthreads();
+    }
+    __syncthreads();
+#pragma unroll
+    for (int s = 0; s < S; ++s) {
+        if (!active[s]) continue;
+        const int slot = s * kNtThreads + tid;
+#pragma unroll
+        for (int i = 0; i < P; ++i) th[s][i] = ls.base[slot][i];
+    }
+}
+
+template <int MODEL, int S, bool ZREF>
+__global__ void __launch_bounds__(kNtThreads, 5) newton_kernel(NewtonArgs a) {
     extern __shared__ __align__(16) float4 s_hits[];
     __shared__ __align__(8) uint64_t s_bar[2];
     constexpr int P = (MODEL == kSlope3) ? 3 : 2;
@@ -240,6 +331,7 @@ __global__ void __launch_bounds__(kNtThreads) newton_kernel(NewtonArgs a) {
         for (int i = 0; i < 3; ++i) th[s][i] = (i < P) ? __ldg(a.seeds + src + i) : 0.f;
     }
 
+    __shared__ LineSearchSmem<S, P> ls;
     HessSums hs[S];
     float R[S], G[S][4];
     for (int j = 0; j < a.n_steps; ++j) {
@@ -277,8 +369,15 @@ __global__ void __launch_bounds__(kNtThreads) newton_kernel(NewtonArgs a) {
             for (int i = 0; i < P; ++i) slope[s] = __fmaf_rn(g[i], p[s][i], slope[s]);
             active[s] = sid[s] < a.n_seeds;
         }
+        // Trial alpha = 1 for every seed of the CTA (all owners pass over the hits together).
+        // With the hits resident in shared memory, the seeds still searching after it are
+        // compacted into a queue and later trials run only on the warps that hold queue
+        // entries, so a halving costs ~ceil(active / (32 S)) warp passes instead of a whole CTA
+        // pass (the oracle's per-seed loop, evaluated in a different thread: bit-identical).
+        // Streaming events (hits > smem stage) keep the CTA-wide loop for every trial.
+        const int kmax_cta = st.resident ? 0 : a.max_halvings;
         float alpha = 1.f;
-        for (int k = 0; k <= a.max_halvings; ++k, alpha *= 0.5f) {
+        for (int k = 0; k <= kmax_cta; ++k, alpha *= 0.5f) {
             bool any = false;
 #pragma unroll
             for (int s = 0; s < S; ++s) any |= active[s];
@@ -299,6 +398,8 @@ __global__ void __launch_bounds__(kNtThreads) newton_kernel(NewtonArgs a) {
                 }
             }
         }
+        if (st.resident && a.max_halvings > 0)
+            nt_line_search_queue<MODEL, S, ZREF>(st, a, negK, th, p, R0, slope, active, ls);
     }
     float g[S][3];
     if (a.grad_out) {
