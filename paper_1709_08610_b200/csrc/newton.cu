@@ -170,6 +170,190 @@ __device__ __forceinline__ void nt_pass_r(HitStage &st, const float (&th)[S][3],
     flush();
 }
 
+// Packed variants of the two passes above for seed PAIRS (FFMA2 / FMUL2 / FADD2): the same
+// operation sequence per seed, each half an independent IEEE round-to-nearest operation, so
+// the results are bit-identical to nt_pass_hess / nt_pass_r with half the issue slots.
+template <int MODEL, int S, bool ZREF>
+__device__ __forceinline__ void nt_pass_hess_x2(HitStage &st, const float (&th)[S][3], float negK, float zref,
+                                                HessSums (&hs)[S]) {
+    static_assert(S % 2 == 0, "seed pairs");
+    constexpr int NP = S / 2;
+    const float2 zero = make_float2(0.f, 0.f), nk = make_float2(negK, negK);
+    float2 mtx[NP], mty[NP], dh[NP], dl[NP], pp[NP][6], s1[NP][6], sd[NP][6], sd2[NP][6];
+#pragma unroll
+    for (int p = 0; p < NP; ++p) {
+        mtx[p] = make_float2(-th[2 * p][0], -th[2 * p + 1][0]);
+        mty[p] = make_float2(-th[2 * p][1], -th[2 * p + 1][1]);
+        dh[p] = dl[p] = zero;
+#pragma unroll
+        for (int q = 0; q < 6; ++q) pp[p][q] = s1[p][q] = sd[p][q] = sd2[p][q] = zero;
+    }
+    float zprev = __int_as_float(0x7fc00000);
+    auto flush = [&]() {
+#pragma unroll
+        for (int p = 0; p < NP; ++p) {
+            const float2 d = dh[p], d2 = __fmul2_rn(dh[p], dh[p]);
+#pragma unroll
+            for (int q = 0; q < 6; ++q) {
+                s1[p][q] = __fadd2_rn(s1[p][q], pp[p][q]);
+                sd[p][q] = __ffma2_rn(d, pp[p][q], sd[p][q]);
+                sd2[p][q] = __ffma2_rn(d2, pp[p][q], sd2[p][q]);
+                pp[p][q] = zero;
+            }
+        }
+    };
+    st.pass([&](const float4 *h, int len) {
+#pragma unroll 2
+        for (int k = 0; k < len; ++k) {
+            const float4 hk = h[k];
+            if (hk.z != zprev) {  // warp-uniform plane change
+                flush();
+                zprev = hk.z;
+#pragma unroll
+                for (int p = 0; p < NP; ++p) {
+                    if (MODEL == kSlope3) {
+                        two_sum(hk.z, -th[2 * p][2], dh[p].x, dl[p].x);
+                        two_sum(hk.z, -th[2 * p + 1][2], dh[p].y, dl[p].y);
+                    } else if (ZREF) {
+                        float hi, lo;
+                        two_sum(hk.z, -zref, hi, lo);
+                        dh[p] = make_float2(hi, hi);
+                        dl[p] = make_float2(lo, lo);
+                    } else {
+                        dh[p] = make_float2(hk.z, hk.z);
+                    }
+                }
+            }
+            const float2 X = make_float2(hk.x, hk.x), Y = make_float2(hk.y, hk.y);
+#pragma unroll
+            for (int p = 0; p < NP; ++p) {
+                float2 A, B;
+                if (MODEL == kSlope3 || ZREF) {
+                    A = __ffma2_rn(mtx[p], dl[p], __ffma2_rn(mtx[p], dh[p], X));
+                    B = __ffma2_rn(mty[p], dl[p], __ffma2_rn(mty[p], dh[p], Y));
+                } else {
+                    const float2 Z = make_float2(hk.z, hk.z);
+                    A = __ffma2_rn(mtx[p], Z, X);
+                    B = __ffma2_rn(mty[p], Z, Y);
+                }
+                const float2 a = __fmul2_rn(__ffma2_rn(A, A, __fmul2_rn(B, B)), nk);
+                const float2 w = make_float2(ex2_approx(a.x), ex2_approx(a.y));
+                const float2 wA = __fmul2_rn(w, A), wB = __fmul2_rn(w, B);
+                pp[p][0] = __fadd2_rn(pp[p][0], w);
+                pp[p][1] = __fadd2_rn(pp[p][1], wA);
+                pp[p][2] = __fadd2_rn(pp[p][2], wB);
+                pp[p][3] = __ffma2_rn(wA, A, pp[p][3]);
+                pp[p][4] = __ffma2_rn(wA, B, pp[p][4]);
+                pp[p][5] = __ffma2_rn(wB, B, pp[p][5]);
+            }
+        }
+    });
+    flush();
+#pragma unroll
+    for (int p = 0; p < NP; ++p)
+#pragma unroll
+        for (int q = 0; q < 6; ++q) {
+            hs[2 * p].s1[q] = s1[p][q].x;
+            hs[2 * p + 1].s1[q] = s1[p][q].y;
+            hs[2 * p].sd[q] = sd[p][q].x;
+            hs[2 * p + 1].sd[q] = sd[p][q].y;
+            hs[2 * p].sd2[q] = sd2[p][q].x;
+            hs[2 * p + 1].sd2[q] = sd2[p][q].y;
+        }
+}
+
+template <int MODEL, int S, bool ZREF, bool GRAD>
+__device__ __forceinline__ void nt_pass_r_x2(HitStage &st, const float (&th)[S][3], float negK, float zref,
+                                             float (&R)[S], float (&G)[S][4]) {
+    static_assert(S % 2 == 0, "seed pairs");
+    constexpr int NP = S / 2;
+    const float2 zero = make_float2(0.f, 0.f), nk = make_float2(negK, negK);
+    float2 mtx[NP], mty[NP], dh[NP], dl[NP], r2[NP], qa[NP], qb[NP], g[NP][4];
+#pragma unroll
+    for (int p = 0; p < NP; ++p) {
+        mtx[p] = make_float2(-th[2 * p][0], -th[2 * p + 1][0]);
+        mty[p] = make_float2(-th[2 * p][1], -th[2 * p + 1][1]);
+        dh[p] = dl[p] = r2[p] = qa[p] = qb[p] = zero;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) g[p][q] = zero;
+    }
+    float zprev = __int_as_float(0x7fc00000);
+    auto flush = [&]() {
+        if constexpr (GRAD) {
+#pragma unroll
+            for (int p = 0; p < NP; ++p) {
+                g[p][0] = __ffma2_rn(dh[p], qa[p], g[p][0]);
+                g[p][1] = __ffma2_rn(dh[p], qb[p], g[p][1]);
+                g[p][2] = __fadd2_rn(g[p][2], qa[p]);
+                g[p][3] = __fadd2_rn(g[p][3], qb[p]);
+                qa[p] = qb[p] = zero;
+            }
+        }
+    };
+    st.pass([&](const float4 *h, int len) {
+#pragma unroll 2
+        for (int k = 0; k < len; ++k) {
+            const float4 hk = h[k];
+            if (hk.z != zprev) {
+                flush();
+                zprev = hk.z;
+#pragma unroll
+                for (int p = 0; p < NP; ++p) {
+                    if (MODEL == kSlope3) {
+                        two_sum(hk.z, -th[2 * p][2], dh[p].x, dl[p].x);
+                        two_sum(hk.z, -th[2 * p + 1][2], dh[p].y, dl[p].y);
+                    } else if (ZREF) {
+                        float hi, lo;
+                        two_sum(hk.z, -zref, hi, lo);
+                        dh[p] = make_float2(hi, hi);
+                        dl[p] = make_float2(lo, lo);
+                    } else {
+                        dh[p] = make_float2(hk.z, hk.z);
+                    }
+                }
+            }
+            const float2 X = make_float2(hk.x, hk.x), Y = make_float2(hk.y, hk.y);
+#pragma unroll
+            for (int p = 0; p < NP; ++p) {
+                float2 A, B;
+                if (MODEL == kSlope3 || ZREF) {
+                    A = __ffma2_rn(mtx[p], dl[p], __ffma2_rn(mtx[p], dh[p], X));
+                    B = __ffma2_rn(mty[p], dl[p], __ffma2_rn(mty[p], dh[p], Y));
+                } else {
+                    const float2 Z = make_float2(hk.z, hk.z);
+                    A = __ffma2_rn(mtx[p], Z, X);
+                    B = __ffma2_rn(mty[p], Z, Y);
+                }
+                const float2 a = __fmul2_rn(__ffma2_rn(A, A, __fmul2_rn(B, B)), nk);
+                const float2 w = make_float2(ex2_approx(a.x), ex2_approx(a.y));
+                r2[p] = __fadd2_rn(r2[p], w);
+                if (GRAD) {
+                    qa[p] = __ffma2_rn(w, A, qa[p]);
+                    qb[p] = __ffma2_rn(w, B, qb[p]);
+                }
+            }
+        }
+    });
+    flush();
+#pragma unroll
+    for (int p = 0; p < NP; ++p) {
+        R[2 * p] = r2[p].x;
+        R[2 * p + 1] = r2[p].y;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            G[2 * p][q] = g[p][q].x;
+            G[2 * p + 1][q] = g[p][q].y;
+        }
+    }
+}
+
+#ifndef RETINA_NT_MINB
+#define RETINA_NT_MINB 5  // CTAs per SM the register allocation must allow
+#endif
+#ifndef RETINA_NT_X2
+#define RETINA_NT_X2 1  // packed seed-pair passes (0: scalar reference passes)
+#endif
+
 // Truncated CG on (-H) p = g (maximisation), <= P iterations, fallback eta g (oracle tn_direction).
 template <int P>
 __device__ __forceinline__ void nt_direction(const float (&g)[3], const float (&H)[3][3], float eta, float (&p)[3]) {
@@ -311,7 +495,7 @@ __device__ __forceinline__ void nt_line_search_queue(HitStage &st, const NewtonA
 }
 
 template <int MODEL, int S, bool ZREF>
-__global__ void __launch_bounds__(kNtThreads, 5) newton_kernel(NewtonArgs a) {
+__global__ void __launch_bounds__(kNtThreads, RETINA_NT_MINB) newton_kernel(NewtonArgs a) {
     extern __shared__ __align__(16) float4 s_hits[];
     __shared__ __align__(8) uint64_t s_bar[2];
     constexpr int P = (MODEL == kSlope3) ? 3 : 2;
@@ -336,7 +520,10 @@ __global__ void __launch_bounds__(kNtThreads, 5) newton_kernel(NewtonArgs a) {
     float R[S], G[S][4];
     for (int j = 0; j < a.n_steps; ++j) {
         const float c = a.c2[j], negK = a.negK[j];
-        nt_pass_hess<MODEL, S, ZREF>(st, th, negK, a.z_ref, hs);
+        if constexpr (RETINA_NT_X2 && S % 2 == 0)
+            nt_pass_hess_x2<MODEL, S, ZREF>(st, th, negK, a.z_ref, hs);
+        else
+            nt_pass_hess<MODEL, S, ZREF>(st, th, negK, a.z_ref, hs);
         float R0[S], p[S][3], slope[S], tt[S][3];
         bool active[S];
 #pragma unroll
@@ -388,7 +575,10 @@ __global__ void __launch_bounds__(kNtThreads, 5) newton_kernel(NewtonArgs a) {
                 for (int i = 0; i < 3; ++i)
                     tt[s][i] = (i < P) ? fminf(fmaxf(__fmaf_rn(alpha, p[s][i], th[s][i]), a.lo[i]), a.hi[i]) : 0.f;
             float Rt[S], Gd[S][4];
-            nt_pass_r<MODEL, S, ZREF, false>(st, tt, negK, a.z_ref, Rt, Gd);
+            if constexpr (RETINA_NT_X2 && S % 2 == 0)
+                nt_pass_r_x2<MODEL, S, ZREF, false>(st, tt, negK, a.z_ref, Rt, Gd);
+            else
+                nt_pass_r<MODEL, S, ZREF, false>(st, tt, negK, a.z_ref, Rt, Gd);
 #pragma unroll
             for (int s = 0; s < S; ++s) {
                 if (active[s] && Rt[s] >= __fmaf_rn(1e-4f * alpha, slope[s], R0[s])) {
@@ -403,7 +593,10 @@ __global__ void __launch_bounds__(kNtThreads, 5) newton_kernel(NewtonArgs a) {
     }
     float g[S][3];
     if (a.grad_out) {
-        nt_pass_r<MODEL, S, ZREF, true>(st, th, a.final_negK, a.z_ref, R, G);
+        if constexpr (RETINA_NT_X2 && S % 2 == 0)
+            nt_pass_r_x2<MODEL, S, ZREF, true>(st, th, a.final_negK, a.z_ref, R, G);
+        else
+            nt_pass_r<MODEL, S, ZREF, true>(st, th, a.final_negK, a.z_ref, R, G);
 #pragma unroll
         for (int s = 0; s < S; ++s) {
             g[s][0] = __fmul_rn(a.final_c2, G[s][0]);
@@ -413,7 +606,10 @@ __global__ void __launch_bounds__(kNtThreads, 5) newton_kernel(NewtonArgs a) {
                           : 0.f;
         }
     } else {
-        nt_pass_r<MODEL, S, ZREF, false>(st, th, a.final_negK, a.z_ref, R, G);
+        if constexpr (RETINA_NT_X2 && S % 2 == 0)
+            nt_pass_r_x2<MODEL, S, ZREF, false>(st, th, a.final_negK, a.z_ref, R, G);
+        else
+            nt_pass_r<MODEL, S, ZREF, false>(st, th, a.final_negK, a.z_ref, R, G);
     }
 #pragma unroll
     for (int s = 0; s < S; ++s) {
