@@ -200,9 +200,10 @@ def main():
     pipe = RetinaPipeline(spec, E, chunk_events=a.chunk_events)
     stream = torch.cuda.current_stream()
     dbatch = upload(batch.offsets, batch.hits, seeds)
+    if a.update == "newton":  # the pairs count comes from the kernel's per-seed evaluation counts
+        pipe.run(dbatch, stream=stream)
+        torch.cuda.synchronize()
     pairs_grid, pairs_ms = pipe.pairs(dbatch)
-    if a.update == "newton":  # lower bound: q Hessian passes + final pass (line-search trials not counted)
-        pairs_ms = pairs_ms / (cfg.n_iters + 1) * (len(spec.newton[0]) + 1)
     keep = 64
 
     def step(b, timer=None, t_ms=0.0):
@@ -324,7 +325,9 @@ def main():
                  "executed_tf32_frac": 6.0 * pairs_s / (peak * 3.0)}
         else:
             peak = N_SM * MUFU_PER_SM_CLK * fmax  # 1 MUFU.EX2 per pair
-            r = {"bound": "alu", "kernel": {"grid": "grid_separable/direct", "multistart": "multistart_kernel"}[ph],
+            kname = {"grid": "grid_separable/direct",
+                     "multistart": "newton_kernel" if a.update == "newton" else "multistart_kernel"}[ph]
+            r = {"bound": "alu", "kernel": kname,
                  "achieved": pairs_s / 1e9, "peak": peak / 1e9, "unit": "Gpair/s (1 MUFU.EX2 per pair)",
                  "frac": pairs_s / peak,
                  "peak_basis": f"{N_SM} SMs x {MUFU_PER_SM_CLK} MUFU.EX2/clk/SM (measured 15.95) x sm_max_mhz "
@@ -334,7 +337,10 @@ def main():
                                             if clk.get("sm_mhz") else None)}
         r.update({"launch_ms": avg_ms, "pairs_per_launch": per_launch, "pairs_per_s": pairs_s,
                   "share_of_step": phase_ms[ph] / a.steps / ms_step, "traffic": None})
-        if ph in traffic:
+        if ph == "multistart" and a.update == "newton":
+            r["work_basis"] = ("pairs = sum over seeds of response evaluations (q Hessian-mode + line-search "
+                               "trials + final; counted by the kernel, PAPER.md:200-201 cost unit) x event hits")
+        if ph in traffic and not (ph == "multistart" and a.update == "newton"):
             r["traffic"] = traffic[ph]["dram_bytes_per_event"] * E / n_launch
             r["traffic_unit"] = "bytes/launch (ncu dram read+write per event x events per launch)"
         roofs[ph] = r

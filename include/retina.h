@@ -180,6 +180,17 @@ int retina_multistart_newton(const retina_events *ev, int model, int32_t n_seeds
                              int32_t max_halvings, const float *box_lo, const float *box_hi,
                              float *theta_out, float *response_out, float *grad_out, void *stream);
 
+/* retina_multistart_newton plus the paper's cost accounting (cost in
+ * units of one response evaluation): evals_out, device int32 [n_events][n_seeds] or NULL,
+ * receives per seed the response evaluations Algorithm 1 spent on it -- n_steps evaluations
+ * with gradient and Hessian, every line-search trial, and the final evaluation
+ * (= n_steps + sum_j trials_j + 1).  Identical results otherwise. */
+int retina_multistart_newton_ex(const retina_events *ev, int model, int32_t n_seeds, const float *seeds,
+                                int32_t n_steps, const float *sigmas, const float *etas, float final_sigma,
+                                int32_t max_halvings, const float *box_lo, const float *box_hi,
+                                float *theta_out, float *response_out, float *grad_out, int32_t *evals_out,
+                                void *stream);
+
 /* Algorithm 1 "cluster solutions ... select highest response above R0" per event:
  *   keep seeds with response >= threshold; order them by (response descending, theta
  *   lexicographic ascending, seed index ascending); scan that order: a seed joins the

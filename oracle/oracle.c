@@ -418,11 +418,14 @@ static void tn_direction(int P, const double *g, const double *H, double eta, do
  * unchanged).  Returns theta^q, R(theta^q) and grad R(theta^q) at final_sigma.
  * margin_out (nullable; diagnostic for the T5 near-tie rule, no effect on the result): per seed,
  * the smallest relative margin of any discrete decision taken -- |R_t - (R_0 + c1 alpha g.p)| /
- * R_0 for the Armijo tests and |d^T H d| / (|d|^2 max|H|) for the CG curvature tests. */
+ * R_0 for the Armijo tests and |d^T H d| / (|d|^2 max|H|) for the CG curvature tests.
+ * evals_out (nullable): per seed, the response evaluations Algorithm 1 spent on it, in the
+ * paper's cost unit: q evaluations with gradient and Hessian, every line-search
+ * trial, and the final evaluation, i.e. q + sum_j (trials of step j) + 1. */
 void ora_newton(int model, int n_events, const int32_t *offsets, const float *hits, double z_ref, int n_seeds,
                 const float *seeds, int n_steps, const double *sigmas, const double *etas, double final_sigma,
                 int max_halvings, const double *box_lo, const double *box_hi, double *theta_out,
-                double *R_out, double *grad_out, double *margin_out) {
+                double *R_out, double *grad_out, double *margin_out, int32_t *evals_out) {
     const int P = model_P(model);
 #pragma omp parallel for collapse(2) schedule(dynamic, 16)
     for (int64_t e = 0; e < n_events; ++e) {
@@ -431,9 +434,11 @@ void ora_newton(int model, int n_events, const int32_t *offsets, const float *hi
             const int n = offsets[e + 1] - offsets[e];
             const int64_t id = e * n_seeds + s;
             double th[3] = {0, 0, 0}, g[3], H[9], p[3], R0, Rt, tt[3], margin = 1.0;
+            int32_t evals = 0;
             for (int a = 0; a < P; ++a) th[a] = seeds[id * P + a];
             for (int j = 0; j < n_steps; ++j) {
                 ora_point_hess(model, h, n, z_ref, th, sigmas[j], &R0, g, H);
+                ++evals;
                 tn_direction(P, g, H, etas[j], p, &margin);
                 double slope = 0.0;
                 for (int a = 0; a < P; ++a) slope += g[a] * p[a];
@@ -446,6 +451,7 @@ void ora_newton(int model, int n_events, const int32_t *offsets, const float *hi
                         tt[a] = v;
                     }
                     ora_point_hess(model, h, n, z_ref, tt, sigmas[j], &Rt, NULL, NULL);
+                    ++evals;
                     {
                         const double m = fabs(Rt - (R0 + 1e-4 * alpha * slope)) / (R0 > 1e-6 ? R0 : 1e-6);
                         if (m < margin) margin = m;
@@ -462,6 +468,7 @@ void ora_newton(int model, int n_events, const int32_t *offsets, const float *hi
             if (grad_out)
                 for (int a = 0; a < P; ++a) grad_out[id * P + a] = g[a];
             if (margin_out) margin_out[id] = margin;
+            if (evals_out) evals_out[id] = evals + 1;
         }
     }
 }

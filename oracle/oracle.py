@@ -45,7 +45,7 @@ def lib():
         L.ora_merge.argtypes = [i, i, i, P, P, P, d, i, P, P, P, P, P]
         L.ora_estimate.argtypes = [P, i, i, P, P, P, P, P, P, i, P]
         L.ora_point_hess.argtypes = [i, P, i, d, P, d, P, P, P]
-        L.ora_newton.argtypes = [i, i, P, P, d, i, P, i, P, P, d, i, P, P, P, P, P, P]
+        L.ora_newton.argtypes = [i, i, P, P, d, i, P, i, P, P, d, i, P, P, P, P, P, P, P]
         for f in (L.ora_point, L.ora_grid, L.ora_peaks, L.ora_multistart, L.ora_merge, L.ora_estimate,
                   L.ora_point_hess, L.ora_newton):
             f.restype = None
@@ -178,9 +178,11 @@ def point_hess(model: int, hits, theta, sigma: float, z_ref: float = 0.0):
 
 
 def newton(model: int, offsets, hits, seeds, sigmas, etas, final_sigma: float, max_halvings: int,
-           box_lo, box_hi, z_ref: float = 0.0, want_grad: bool = True, want_margin: bool = False):
+           box_lo, box_hi, z_ref: float = 0.0, want_grad: bool = True, want_margin: bool = False,
+           want_evals: bool = False):
     """Algorithm 1 with Truncated-Newton updates and a sigma schedule (readings Z22-Z25).
-    Returns (theta, R, grad) or, with want_margin, (theta, R, grad, margin)."""
+    Returns (theta, R, grad), plus margin with want_margin, plus the per-seed response
+    evaluation count (q + line-search trials + 1) with want_evals."""
     off = np.ascontiguousarray(np.asarray(offsets, np.int32))
     h = _f32(hits).reshape(-1, 4)
     sd = _f32(seeds)
@@ -194,6 +196,8 @@ def newton(model: int, offsets, hits, seeds, sigmas, etas, final_sigma: float, m
     R = np.zeros((E, S))
     g = np.zeros((E, S, P)) if want_grad else None
     m = np.zeros((E, S)) if want_margin else None
+    ne = np.zeros((E, S), np.int32) if want_evals else None
     lib().ora_newton(model, E, _p(off), _p(h), _f(z_ref), S, _p(sd), len(sg), _p(sg), _p(et), _f(final_sigma),
-                     int(max_halvings), _p(lo), _p(hi), _p(th), _p(R), _p(g), _p(m))
-    return (th, R, g, m) if want_margin else (th, R, g)
+                     int(max_halvings), _p(lo), _p(hi), _p(th), _p(R), _p(g), _p(m), _p(ne))
+    res = (th, R, g) + ((m,) if want_margin else ()) + ((ne,) if want_evals else ())
+    return res

@@ -295,6 +295,14 @@ int retina_multistart_newton(const retina_events *ev, int model, int32_t n_seeds
                              int32_t n_steps, const float *sigmas, const float *etas, float final_sigma,
                              int32_t max_halvings, const float *box_lo, const float *box_hi, float *theta_out,
                              float *response_out, float *grad_out, void *stream) {
+    return retina_multistart_newton_ex(ev, model, n_seeds, seeds, n_steps, sigmas, etas, final_sigma, max_halvings,
+                                       box_lo, box_hi, theta_out, response_out, grad_out, nullptr, stream);
+}
+
+int retina_multistart_newton_ex(const retina_events *ev, int model, int32_t n_seeds, const float *seeds,
+                                int32_t n_steps, const float *sigmas, const float *etas, float final_sigma,
+                                int32_t max_halvings, const float *box_lo, const float *box_hi, float *theta_out,
+                                float *response_out, float *grad_out, int32_t *evals_out, void *stream) {
     g_last_error[0] = 0;
     int st = check_events(ev);
     if (st) return st;
@@ -338,6 +346,7 @@ int retina_multistart_newton(const retina_events *ev, int model, int32_t n_seeds
     a.theta_out = theta_out;
     a.R_out = response_out;
     a.grad_out = grad_out;
+    a.evals_out = evals_out;
     a.cap = stage_cap(ev->max_event_hits, 4096);
     const cudaError_t err = retina::launch_newton(model, a, ev->n_events, (cudaStream_t)stream);
     if (err != cudaSuccess) return cuda_fail(err, "retina_multistart_newton");

@@ -51,6 +51,7 @@ struct NewtonArgs {
     int max_halvings;
     float lo[3], hi[3];
     float *theta_out, *R_out, *grad_out;
+    int32_t *evals_out;  // nullable: response evaluations per seed (q + line-search trials + 1)
     int cap;
     int e_base;
 };

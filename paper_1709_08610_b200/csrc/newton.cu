@@ -410,6 +410,7 @@ struct LineSearchSmem {
     float base[kNtThreads * S][P];  // theta before the step; the accepted trial overwrites it
     float dir[kNtThreads * S][P];
     float R0[kNtThreads * S], slope[kNtThreads * S];
+    int ntrial[kNtThreads * S];  // halvings tried (k of the accepted trial, else max_halvings)
     int q[2][kNtThreads * S];
     int nq[2];
 };
@@ -423,7 +424,7 @@ struct LineSearchSmem {
 template <int MODEL, int S, bool ZREF>
 __device__ __forceinline__ void nt_line_search_queue(HitStage &st, const NewtonArgs &a, float negK, float (&th)[S][3],
                                                      const float (&p)[S][3], const float (&R0)[S],
-                                                     const float (&slope)[S], const bool (&active)[S],
+                                                     const float (&slope)[S], const bool (&active)[S], int (&nev)[S],
                                                      LineSearchSmem<S, (MODEL == kSlope3) ? 3 : 2> &ls) {
     constexpr int P = (MODEL == kSlope3) ? 3 : 2;
     constexpr int SQ = RETINA_NT_SQ < S ? RETINA_NT_SQ : S;
@@ -442,6 +443,7 @@ __device__ __forceinline__ void nt_line_search_queue(HitStage &st, const NewtonA
         }
         ls.R0[slot] = R0[s];
         ls.slope[slot] = slope[s];
+        ls.ntrial[slot] = a.max_halvings;
         ls.q[0][atomicAdd(&ls.nq[0], 1)] = slot;
     }
     __syncthreads();
@@ -474,6 +476,7 @@ __device__ __forceinline__ void nt_line_search_queue(HitStage &st, const NewtonA
                 if (Rt[s] >= __fmaf_rn(1e-4f * alpha, ls.slope[sl], ls.R0[sl])) {
 #pragma unroll
                     for (int i = 0; i < P; ++i) ls.base[sl][i] = tt[s][i];
+                    ls.ntrial[sl] = k;
                 } else {
                     ls.q[cur ^ 1][atomicAdd(&ls.nq[cur ^ 1], 1)] = sl;
                 }
@@ -491,6 +494,7 @@ __device__ __forceinline__ void nt_line_search_queue(HitStage &st, const NewtonA
         const int slot = s * kNtThreads + tid;
 #pragma unroll
         for (int i = 0; i < P; ++i) th[s][i] = ls.base[slot][i];
+        nev[s] += ls.ntrial[slot];
     }
 }
 
@@ -518,6 +522,9 @@ __global__ void __launch_bounds__(kNtThreads, RETINA_NT_MINB) newton_kernel(Newt
     __shared__ LineSearchSmem<S, P> ls;
     HessSums hs[S];
     float R[S], G[S][4];
+    int nev[S];  // response evaluations per seed (PAPER.md:200-201 cost unit)
+#pragma unroll
+    for (int s = 0; s < S; ++s) nev[s] = a.n_steps + 1;  // q Hessian-mode passes + the final one
     for (int j = 0; j < a.n_steps; ++j) {
         const float c = a.c2[j], negK = a.negK[j];
         if constexpr (RETINA_NT_X2 && S % 2 == 0)
@@ -574,6 +581,8 @@ __global__ void __launch_bounds__(kNtThreads, RETINA_NT_MINB) newton_kernel(Newt
 #pragma unroll
                 for (int i = 0; i < 3; ++i)
                     tt[s][i] = (i < P) ? fminf(fmaxf(__fmaf_rn(alpha, p[s][i], th[s][i]), a.lo[i]), a.hi[i]) : 0.f;
+#pragma unroll
+            for (int s = 0; s < S; ++s) nev[s] += active[s] ? 1 : 0;
             float Rt[S], Gd[S][4];
             if constexpr (RETINA_NT_X2 && S % 2 == 0)
                 nt_pass_r_x2<MODEL, S, ZREF, false>(st, tt, negK, a.z_ref, Rt, Gd);
@@ -589,7 +598,7 @@ __global__ void __launch_bounds__(kNtThreads, RETINA_NT_MINB) newton_kernel(Newt
             }
         }
         if (st.resident && a.max_halvings > 0)
-            nt_line_search_queue<MODEL, S, ZREF>(st, a, negK, th, p, R0, slope, active, ls);
+            nt_line_search_queue<MODEL, S, ZREF>(st, a, negK, th, p, R0, slope, active, nev, ls);
     }
     float g[S][3];
     if (a.grad_out) {
@@ -616,6 +625,7 @@ __global__ void __launch_bounds__(kNtThreads, RETINA_NT_MINB) newton_kernel(Newt
         if (sid[s] < a.n_seeds) {
             const int64_t o = (int64_t)e * a.n_seeds + sid[s];
             a.R_out[o] = R[s];
+            if (a.evals_out) a.evals_out[o] = nev[s];
 #pragma unroll
             for (int i = 0; i < P; ++i) {
                 a.theta_out[o * P + i] = th[s][i];

@@ -88,6 +88,8 @@ class RetinaPipeline:
         S = spec.n_seeds
         self.theta = torch.empty((E, S, P), dtype=torch.float32, device=self.device)
         self.resp = torch.empty((E, S), dtype=torch.float32, device=self.device)
+        # Newton path: response evaluations per seed (the paper's cost unit), counted by the kernel
+        self.evals = torch.empty((E, S), dtype=torch.int32, device=self.device) if spec.newton is not None else None
         self.t_theta = torch.empty((E, spec.track_capacity, P), dtype=torch.float32, device=self.device)
         self.t_resp = torch.empty((E, spec.track_capacity), dtype=torch.float32, device=self.device)
         self.t_seed = torch.empty((E, spec.track_capacity), dtype=torch.int32, device=self.device)
@@ -97,9 +99,15 @@ class RetinaPipeline:
 
     # ------------------------------------------------------------------ accounting
     def pairs(self, batch: DeviceBatch):
-        """Algorithmic unit.hit pairs: grid = N_e x cells, multi-start = N_e x S x (n_iters+1)."""
+        """Algorithmic unit.hit pairs: grid = N_e x cells, multi-start = N_e x S x (n_iters+1);
+        for the Newton update, N_e x (response evaluations of the event's seeds), read from the
+        kernel's per-seed counts of the last pass (call after one run())."""
         n = batch.n_hits_per_event.astype(np.float64)
         grid = float(n.sum()) * self.spec.cells
+        if self.spec.newton is not None:
+            E = batch.n_events
+            ev = self.evals[:E].to(torch.float64).sum(dim=1).cpu().numpy()
+            return grid, float((n * ev).sum())
         ms = float(n.sum()) * self.spec.n_seeds * (self.spec.n_iters + 1)
         return grid, ms
 
@@ -138,8 +146,9 @@ class RetinaPipeline:
             timer.start("multistart")
         if sp.newton is not None:  # the paper's update: Truncated Newton with a sigma schedule
             sig, eta, fsig, mh = sp.newton
-            R.retina_multistart_newton(ev, sp.model, batch.seeds, sig, eta, fsig, mh, sp.box_lo, sp.box_hi,
-                                       want_grad=False, out=(self.theta[:E], self.resp[:E], None), stream=stream)
+            R.retina_multistart_newton_ex(ev, sp.model, batch.seeds, sig, eta, fsig, mh, sp.box_lo, sp.box_hi,
+                                          want_grad=False, out=(self.theta[:E], self.resp[:E], None, self.evals[:E]),
+                                          stream=stream)
         else:  # BASELINE configs[2..4]: fixed-step gradient ascent
             R.retina_multistart_optimize(ev, sp.model, sp.sigma_ms or sp.sigma, batch.seeds, sp.n_iters, sp.step,
                                          sp.box_lo, sp.box_hi, want_grad=False,

@@ -23,7 +23,8 @@ GRID_AUTO, GRID_DIRECT, GRID_SEPARABLE, GRID_TENSOR = 0, 1, 2, 3
 
 EXPORTED = ("retina_grid_response", "retina_grid_response_ex", "retina_estimate_peaks", "retina_find_peaks",
             "retina_find_peaks_ws", "retina_find_peaks_workspace_size",
-            "retina_multistart_optimize", "retina_multistart_newton", "retina_merge_tracks",
+            "retina_multistart_optimize", "retina_multistart_newton", "retina_multistart_newton_ex",
+            "retina_merge_tracks",
             "retina_status_string", "retina_last_error", "retina_version")
 
 
@@ -64,9 +65,12 @@ def lib() -> ctypes.CDLL:
                                                  i32, f32, vp, vp, vp, vp, vp, vp]
         L.retina_multistart_newton.argtypes = [ctypes.POINTER(retina_events), ctypes.c_int, i32, vp, i32, vp, vp,
                                                f32, i32, vp, vp, vp, vp, vp, vp]
+        L.retina_multistart_newton_ex.argtypes = [ctypes.POINTER(retina_events), ctypes.c_int, i32, vp, i32, vp,
+                                                  vp, f32, i32, vp, vp, vp, vp, vp, vp, vp]
         L.retina_merge_tracks.argtypes = [i32, i32, i32, vp, vp, vp, f32, i32, vp, vp, vp, vp, vp, vp]
         for f in (L.retina_grid_response, L.retina_grid_response_ex, L.retina_find_peaks, L.retina_estimate_peaks,
-                  L.retina_multistart_optimize, L.retina_multistart_newton, L.retina_merge_tracks):
+                  L.retina_multistart_optimize, L.retina_multistart_newton, L.retina_multistart_newton_ex,
+                  L.retina_merge_tracks):
             f.restype = ctypes.c_int
         L.retina_status_string.argtypes = [ctypes.c_int]
         L.retina_status_string.restype = ctypes.c_char_p
@@ -222,6 +226,20 @@ def retina_multistart_optimize(events: Events, model: int, sigma: float, seeds: 
 def retina_multistart_newton(events: Events, model: int, seeds: torch.Tensor, sigmas, etas, final_sigma: float,
                              max_halvings: int, box_lo, box_hi, want_grad: bool = True, out=None, stream=None):
     """Truncated-Newton multi-start: (theta_out, response_out, grad_out or None)."""
+    return _newton(False, events, model, seeds, sigmas, etas, final_sigma, max_halvings, box_lo, box_hi, want_grad,
+                   out, stream)[:3]
+
+
+def retina_multistart_newton_ex(events: Events, model: int, seeds: torch.Tensor, sigmas, etas, final_sigma: float,
+                                max_halvings: int, box_lo, box_hi, want_grad: bool = True, out=None, stream=None):
+    """As retina_multistart_newton, plus the per-seed response-evaluation counts (int32 [E, S]):
+    (theta_out, response_out, grad_out or None, evals_out)."""
+    return _newton(True, events, model, seeds, sigmas, etas, final_sigma, max_halvings, box_lo, box_hi, want_grad,
+                   out, stream)
+
+
+def _newton(ex, events, model, seeds, sigmas, etas, final_sigma, max_halvings, box_lo, box_hi, want_grad, out,
+            stream):
     P = MODEL_P[model]
     _dev(seeds, torch.float32)
     E, S, Ps = seeds.shape
@@ -233,7 +251,16 @@ def retina_multistart_newton(events: Events, model: int, seeds: torch.Tensor, si
     if out is None:
         out = (torch.empty_like(seeds), torch.empty((E, S), dtype=torch.float32, device=seeds.device),
                torch.empty_like(seeds) if want_grad else None)
-    th, R, g = out
+        if ex:
+            out = out + (torch.empty((E, S), dtype=torch.int32, device=seeds.device),)
+    th, R, g = out[:3]
+    if ex:
+        ne = out[3]
+        _check("retina_multistart_newton_ex",
+               lib().retina_multistart_newton_ex(ctypes.byref(events.c), model, S, _ptr(seeds), len(sigmas), sg, et,
+                                                 float(final_sigma), int(max_halvings), lo, hi, _ptr(th), _ptr(R),
+                                                 _ptr(g), _ptr(ne), _stream(stream)))
+        return th, R, g, ne
     _check("retina_multistart_newton",
            lib().retina_multistart_newton(ctypes.byref(events.c), model, S, _ptr(seeds), len(sigmas), sg, et,
                                           float(final_sigma), int(max_halvings), lo, hi, _ptr(th), _ptr(R),

@@ -551,3 +551,31 @@ def test_P16_newton_ascent_identities_and_fallback():
     v0, v1 = s0[0, 0].astype(float) - u, th[0, 0] - u
     assert abs(v0[0] * v1[1] - v0[1] * v1[0]) <= 1e-9 * np.dot(v0, v0)
     assert R[0, 0] > Rh
+
+
+def test_P17_newton_evaluation_count():
+    """Cost accounting of Algorithm 1 in response evaluations:
+    q Hessian-mode evaluations + every line-search trial + the final evaluation."""
+    cfg = C.CFG2
+    b = G.make_batch(cfg, [0])
+    seeds = G.make_seeds(cfg, [0], n_seeds=16)
+    # no optimisation step: only the final evaluation
+    *_, ne = ora.newton(cfg.model, b.offsets, b.hits, seeds, [], [], cfg.sigma, 8, cfg.box_lo, cfg.box_hi,
+                        want_evals=True)
+    assert np.all(ne == 1)
+    # empty event: R = 0, grad = 0, p = 0, the first trial is accepted -> 2q + 1
+    sig = [cfg.sigma * 3, cfg.sigma]
+    eta = [cfg.step * 9, cfg.step]
+    *_, ne = ora.newton(cfg.model, [0, 0], np.zeros((0, 4), np.float32), seeds, sig, eta, cfg.sigma, 8,
+                        cfg.box_lo, cfg.box_hi, want_evals=True)
+    assert np.all(ne == 2 * 2 + 1)
+    # seed on the box edge with the (fallback) ascent direction pointing out of the box: every
+    # clamped trial equals the start, Armijo fails at every halving -> q (M + 1) + q + 1
+    d = 300.0
+    h = h4([(0.35 * d, 0.0, d)])  # the hit's slope lies outside the prior box in tx
+    s0 = np.array([[[0.3, 0.0]]], np.float32)
+    M = 8
+    th, R, _, ne = ora.newton(C.SLOPE2, [0, 1], h, s0, [10.0, 10.0], [1e-6, 1e-6], 10.0, M, (-.3, -.3), (.3, .3),
+                              want_evals=True)
+    assert ne[0, 0] == 2 * (M + 1) + 2 + 1
+    assert np.array_equal(th[0, 0], s0[0, 0].astype(np.float64))

@@ -471,12 +471,17 @@ def test_newton_multistart_vs_oracle(name, n_ev, n_seeds):
     b = G.make_batch(cfg, ev_ids)
     seeds = G.make_seeds(cfg, ev_ids, n_seeds=n_seeds)
     sig, eta, fsig, mh = C.newton_schedule(cfg)
-    th_d, R_d, g_d = R.retina_multistart_newton(events_of(b), cfg.model, dev(seeds), sig, eta, fsig, mh,
-                                                cfg.box_lo, cfg.box_hi)
+    th_d, R_d, g_d, ne_d = R.retina_multistart_newton_ex(events_of(b), cfg.model, dev(seeds), sig, eta, fsig, mh,
+                                                         cfg.box_lo, cfg.box_hi)
     torch.cuda.synchronize()
     th, Rg = th_d.cpu().numpy(), R_d.cpu().numpy()
-    rth, rR, _, margin = ora.newton(cfg.model, b.offsets, b.hits, seeds, sig, eta, fsig, mh, cfg.box_lo,
-                                    cfg.box_hi, want_margin=True)
+    rth, rR, _, margin, rne = ora.newton(cfg.model, b.offsets, b.hits, seeds, sig, eta, fsig, mh, cfg.box_lo,
+                                         cfg.box_hi, want_margin=True, want_evals=True)
+    # the paper's cost accounting (response evaluations per seed) is an integer: identical to the
+    # oracle's for every seed whose discrete decisions were not oracle near-ties
+    ne = ne_d.cpu().numpy()
+    assert np.array_equal(ne[margin > 1e-4], rne[margin > 1e-4])
+    assert np.all(ne >= 2 * len(sig) + 1) and np.all(ne <= len(sig) * (mh + 2) + 1)
     ranges = np.array(cfg.box_hi, np.float64) - np.array(cfg.box_lo, np.float64)
     dev_rel = np.max(np.abs(th.astype(np.float64) - rth) / ranges, axis=2)
     bad = np.argwhere(dev_rel > 1e-3)
