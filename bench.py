@@ -53,6 +53,8 @@ def args_():
     ap.add_argument("--config", default="cfg3")
     ap.add_argument("--events-per-rank", type=int, default=None)
     ap.add_argument("--chunk-events", type=int, default=256)
+    ap.add_argument("--overlap-peaks", action="store_true",
+                    help="peak scan of grid chunk c on a second stream while chunk c+1 is computed")
     ap.add_argument("--e2e-steps", type=int, default=None)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample-events", type=int, default=3)
@@ -197,7 +199,7 @@ def main():
     spec = make_spec(cfg)
     if a.update == "newton":
         spec.newton = C.newton_schedule(cfg)
-    pipe = RetinaPipeline(spec, E, chunk_events=a.chunk_events)
+    pipe = RetinaPipeline(spec, E, chunk_events=a.chunk_events, overlap_peaks=a.overlap_peaks)
     stream = torch.cuda.current_stream()
     dbatch = upload(batch.offsets, batch.hits, seeds)
     if a.update == "newton":  # the pairs count comes from the kernel's per-seed evaluation counts

@@ -64,7 +64,7 @@ class DeviceBatch:
 
 class RetinaPipeline:
     def __init__(self, spec: PathSpec, max_events: int, chunk_events: int = 256, device="cuda",
-                 grid_bytes_budget: float = 2e9):
+                 grid_bytes_budget: float = 2e9, overlap_peaks: bool = False):
         self.spec = spec
         self.device = torch.device(device)
         cells = spec.cells
@@ -74,6 +74,15 @@ class RetinaPipeline:
         self.nodes = [torch.from_numpy(np.ascontiguousarray(n, np.float32)).to(self.device) for n in spec.nodes]
         shape = tuple(len(n) for n in spec.nodes)
         self.grid_buf = torch.empty((self.chunk,) + shape, dtype=torch.float32, device=self.device) if cells else None
+        # With several chunks, the peak scan of chunk c (HBM-bound, small CTAs) runs on a second,
+        # higher-priority stream while the tensor-core grid kernel computes chunk c+1 into a second
+        # buffer: the two kernels co-reside on the SMs (the grid CTA leaves registers and threads free).
+        self.overlap = bool(cells) and overlap_peaks and max_events > self.chunk
+        self.grid_bufs = [self.grid_buf]
+        self.side = None
+        if self.overlap:
+            self.grid_bufs.append(torch.empty_like(self.grid_buf))
+            self.side = torch.cuda.Stream(self.device, priority=-1)
         # many-CTA peak finder when a chunk has too few events to fill the GPU with one CTA per
         # event (large grids, e.g. 256^3); one CTA per event otherwise (single read of the grid)
         self.peak_ws = None
@@ -118,25 +127,43 @@ class RetinaPipeline:
     def run_grid(self, batch: DeviceBatch, stream=None, timer=None):
         sp = self.spec
         E = batch.n_events
-        for e0 in range(0, E, self.chunk):
+        main = stream if stream is not None else torch.cuda.current_stream(self.device)
+        side = self.side if self.overlap else main
+        if side is not main:
+            side.wait_stream(main)
+        freed = [None] * len(self.grid_bufs)  # event: the peak scan of the buffer's last chunk is done
+        for ci, e0 in enumerate(range(0, E, self.chunk)):
             e1 = min(E, e0 + self.chunk)
+            b = ci % len(self.grid_bufs)
+            if freed[b] is not None:
+                main.wait_event(freed[b])
             ev = self.events_view(batch, e0, e1)
-            out = self.grid_buf[: e1 - e0]
+            out = self.grid_bufs[b][: e1 - e0]
             if timer is not None:
-                timer.start("grid")
-            R.retina_grid_response(ev, sp.model, sp.sigma, self.nodes, out=out, stream=stream)
+                timer.start("grid", main)
+            R.retina_grid_response(ev, sp.model, sp.sigma, self.nodes, out=out, stream=main)
             if timer is not None:
-                timer.stop("grid")
-                timer.start("peaks")
+                timer.stop("grid", main)
+            if side is not main:
+                done = torch.cuda.Event()
+                done.record(main)
+                side.wait_event(done)
+            if timer is not None:
+                timer.start("peaks", side)
             R.retina_find_peaks(out, sp.P, sp.peak_threshold, sp.peak_capacity,
                                 out=(self.peak_idx[e0:e1], self.peak_val[e0:e1], self.peak_cnt[e0:e1]),
-                                stream=stream, workspace=self.peak_ws)
+                                stream=side, workspace=self.peak_ws)
             # step (iv): sub-cell parameter estimate of every peak
             R.retina_estimate_peaks(out, self.nodes, self.peak_idx[e0:e1], self.peak_cnt[e0:e1],
-                                    out=self.peak_theta[e0:e1], stream=stream)
+                                    out=self.peak_theta[e0:e1], stream=side)
             if timer is not None:
-                timer.stop("peaks")
+                timer.stop("peaks", side)
+            if side is not main:
+                freed[b] = torch.cuda.Event()
+                freed[b].record(side)
             self.launches += 3 + (1 if self.peak_ws is not None else 0)  # slab peaks = 2 kernels
+        if side is not main:
+            main.wait_stream(side)
 
     def run_multistart(self, batch: DeviceBatch, stream=None, timer=None):
         sp = self.spec
@@ -194,14 +221,14 @@ class PhaseTimer:
         self.pending = {}
         self.events: dict = {}
 
-    def start(self, name):
+    def start(self, name, stream=None):
         ev = torch.cuda.Event(enable_timing=True)
-        ev.record(self.stream)
+        ev.record(stream or self.stream)
         self.pending[name] = ev
 
-    def stop(self, name):
+    def stop(self, name, stream=None):
         ev = torch.cuda.Event(enable_timing=True)
-        ev.record(self.stream)
+        ev.record(stream or self.stream)
         self.events.setdefault(name, []).append((self.pending.pop(name), ev))
 
     def totals_ms(self):
