@@ -316,15 +316,16 @@ def main():
         per_launch = work[ph] / n_launch
         pairs_s = per_launch / (avg_ms * 1e-3)
         if ph == "grid" and cfg.model in (C.SLOPE2, C.SLOPE3):
-            # tcgen05 3xTF32 contraction: 2 algorithmic flops per (unit, hit) pair; the fp32-accurate
-            # tensor peak is the TF32 peak (measured bf16 burst x nominal tf32/bf16 = 0.5) / 3 passes
-            peak = float(pk.get("bf16_tflops", 1590.0)) * 1e12 * 0.5 / 3.0
-            r = {"bound": "tensor", "kernel": "grid_tensor_kernel (tcgen05.mma kind::tf32, 3xTF32)",
+            # tcgen05 fp16-split contraction (RETINA_GRID_AUTO = RETINA_GRID_TENSOR_F16): 2 algorithmic
+            # flops per (unit, hit) pair, executed as 3 kind::f16 products (hi.hi, hi.lo, lo.hi); the
+            # fp32-accurate tensor peak is the measured dense bf16/f16 peak / 3
+            peak = float(pk.get("bf16_tflops", 1590.0)) * 1e12 / 3.0
+            r = {"bound": "tensor", "kernel": "grid_tensor16_kernel (tcgen05.mma kind::f16, fp16 hi/lo split)",
                  "achieved": 2.0 * pairs_s / 1e12, "peak": peak / 1e12, "unit": "TFLOP/s",
                  "frac": 2.0 * pairs_s / peak,
-                 "peak_basis": "MEASURED_PEAKS.json bf16_tflops (burst) x 0.5 (tf32/bf16 nominal) / 3 (3xTF32 split); "
-                               "algorithmic flops = 2 per unit.hit pair",
-                 "executed_tf32_frac": 6.0 * pairs_s / (peak * 3.0)}
+                 "peak_basis": "MEASURED_PEAKS.json bf16_tflops (burst; f16 = bf16 rate) / 3 (three f16 products "
+                               "per pair); algorithmic flops = 2 per unit.hit pair",
+                 "executed_f16_frac": 6.0 * pairs_s / (peak * 3.0)}
         else:
             peak = N_SM * MUFU_PER_SM_CLK * fmax  # 1 MUFU.EX2 per pair
             kname = {"grid": "grid_separable/direct",

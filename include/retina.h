@@ -95,7 +95,7 @@ int retina_grid_response(const retina_events *ev, int model, float sigma,
                          float *response, void *stream);
 
 /* Same as retina_grid_response with an explicit kernel choice:
- *   RETINA_GRID_AUTO       tensor for SLOPE2 and SLOPE3, direct for LINE2D
+ *   RETINA_GRID_AUTO       tensor (fp16 split) for SLOPE2 and SLOPE3, direct for LINE2D
  *                          (what retina_grid_response uses);
  *   RETINA_GRID_DIRECT     one MUFU.EX2 per (unit, hit) pair (all models);
  *   RETINA_GRID_SEPARABLE  SLOPE2/SLOPE3 only: exp(-s^2/sigma^2) = e_x(tx, hit) e_y(ty, hit)
@@ -103,8 +103,12 @@ int retina_grid_response(const retina_events *ev, int model, float sigma,
  *                          FFMA2 on the CUDA cores (RETINA_EUNSUPPORTED for LINE2D, whose
  *                          residual does not split);
  *   RETINA_GRID_TENSOR     SLOPE2 / SLOPE3 (one GEMM per z0): the same contraction on the tcgen05 tensor cores with a
- *                          3xTF32 split (fp32-level accuracy), accumulators in TMEM. */
-enum { RETINA_GRID_AUTO = 0, RETINA_GRID_DIRECT = 1, RETINA_GRID_SEPARABLE = 2, RETINA_GRID_TENSOR = 3 };
+ *                          3xTF32 split (fp32-level accuracy), accumulators in TMEM;
+ *   RETINA_GRID_TENSOR_F16 SLOPE2 / SLOPE3: the same contraction on kind::f16 with an exact scaled fp16 hi/lo split
+ *                          of every factor (hi.hi and hi.lo + lo.hi in two TMEM accumulators, fp32-level accuracy,
+ *                          half the MMA work of 3xTF32). */
+enum { RETINA_GRID_AUTO = 0, RETINA_GRID_DIRECT = 1, RETINA_GRID_SEPARABLE = 2, RETINA_GRID_TENSOR = 3,
+       RETINA_GRID_TENSOR_F16 = 4 };
 int retina_grid_response_ex(const retina_events *ev, int model, float sigma,
                             const int32_t *axis_len, const float *const *axis_nodes,
                             float *response, int algorithm, void *stream);

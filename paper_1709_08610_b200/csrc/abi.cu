@@ -99,15 +99,15 @@ int retina_grid_response_ex(const retina_events *ev, int model, float sigma, con
     }
     if (cells > 0x7fffffffLL) return fail(RETINA_EUNSUPPORTED, "more than 2^31-1 cells per event");
     if (ev->n_events > 0 && !response) return fail(RETINA_EINVAL, "response is NULL");
-    if (algorithm < RETINA_GRID_AUTO || algorithm > RETINA_GRID_TENSOR)
+    if (algorithm < RETINA_GRID_AUTO || algorithm > RETINA_GRID_TENSOR_F16)
         return fail(RETINA_EINVAL, "unknown grid algorithm %d", algorithm);
     if (algorithm == RETINA_GRID_SEPARABLE && model == RETINA_LINE2D)
         return fail(RETINA_EUNSUPPORTED, "LINE2D residual does not factorise: no separable grid");
-    if (algorithm == RETINA_GRID_TENSOR && model == RETINA_LINE2D)
+    if ((algorithm == RETINA_GRID_TENSOR || algorithm == RETINA_GRID_TENSOR_F16) && model == RETINA_LINE2D)
         return fail(RETINA_EUNSUPPORTED, "LINE2D residual does not factorise: no tensor-core grid");
     if (algorithm == RETINA_GRID_AUTO)
         algorithm = (model == RETINA_LINE2D)   ? RETINA_GRID_DIRECT
-                                               : RETINA_GRID_TENSOR;
+                                               : RETINA_GRID_TENSOR_F16;
     retina::GridArgs a{};
     a.offsets = ev->offsets;
     a.hits = reinterpret_cast<const float4 *>(ev->hits);
@@ -124,6 +124,8 @@ int retina_grid_response_ex(const retina_events *ev, int model, float sigma, con
     cudaError_t err;
     if (algorithm == RETINA_GRID_TENSOR)
         err = retina::launch_grid_tensor(model, a, ev->n_events, (cudaStream_t)stream);
+    else if (algorithm == RETINA_GRID_TENSOR_F16)
+        err = retina::launch_grid_tensor16(model, a, ev->n_events, (cudaStream_t)stream);
     else if (algorithm == RETINA_GRID_SEPARABLE)
         err = retina::launch_grid_separable(model, a, ev->n_events, (cudaStream_t)stream);
     else

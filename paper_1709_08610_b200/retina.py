@@ -19,7 +19,7 @@ MODEL_P = {LINE2D: 2, SLOPE2: 2, SLOPE3: 3}
 RETINA_OK, RETINA_EINVAL, RETINA_EUNSUPPORTED, RETINA_ECUDA = 0, 1, 2, 3
 MERGE_MAX_SEEDS = 16384
 
-GRID_AUTO, GRID_DIRECT, GRID_SEPARABLE, GRID_TENSOR = 0, 1, 2, 3
+GRID_AUTO, GRID_DIRECT, GRID_SEPARABLE, GRID_TENSOR, GRID_TENSOR_F16 = 0, 1, 2, 3, 4
 
 EXPORTED = ("retina_grid_response", "retina_grid_response_ex", "retina_estimate_peaks", "retina_find_peaks",
             "retina_find_peaks_ws", "retina_find_peaks_workspace_size",

@@ -380,13 +380,15 @@ def test_direct_and_separable_agree_cfg3_batch():
 
 # --------------------------------------------------------------------------- tensor-core grid (SLOPE2)
 TENSOR = R.retina.GRID_TENSOR
+TENSORS = [R.retina.GRID_TENSOR, R.retina.GRID_TENSOR_F16]  # 3xTF32 and fp16-split kernels
 
 
-def test_T1_tensor_grid_cfg1_full():
+@pytest.mark.parametrize("tensor", TENSORS)
+def test_T1_tensor_grid_cfg1_full(tensor):
     cfg = C.CFG1
     b = G.make_batch(cfg, [0])
     nodes = G.axis_nodes(cfg)
-    g = gpu_grid(b, cfg, nodes, algo=TENSOR)
+    g = gpu_grid(b, cfg, nodes, algo=tensor)
     ref = ora.grid(cfg.model, b.offsets, b.hits, nodes, cfg.sigma)
     ok, worst = PU.t1_response(g, ref)
     assert ok, worst
@@ -395,22 +397,24 @@ def test_T1_tensor_grid_cfg1_full():
 @pytest.mark.parametrize("z_ref,shape", [(0.0, (37, 70)), (-12.345, (41, 33)), (0.0, (130, 300)),
                                          (0.0, (256, 512))])
 @pytest.mark.parametrize("hint", [True, False])
-def test_T1_tensor_grid_ragged_edges(z_ref, shape, hint):
+@pytest.mark.parametrize("tensor", TENSORS)
+def test_T1_tensor_grid_ragged_edges(z_ref, shape, hint, tensor):
     b = synthetic_batch(C.SLOPE2, [700, 0, 1, 5000, 37, 33], seed=3)
     nodes = [np.linspace(-0.3, 0.3, n).astype(np.float32) for n in shape]
     cfg = C.Config(name="t", model=C.SLOPE2, n_events=6, seed=0, n_tracks=0, sigma=0.44)
-    g = gpu_grid(b, cfg, nodes, z_ref=z_ref, hint=hint, algo=TENSOR)
+    g = gpu_grid(b, cfg, nodes, z_ref=z_ref, hint=hint, algo=tensor)
     ref = ora.grid(C.SLOPE2, b.offsets, b.hits, nodes, 0.44, z_ref=z_ref)
     assert np.all(g[1] == 0.0)
     ok, worst = PU.t1_response(g, ref)
     assert ok, worst
 
 
-def test_T1_tensor_grid_cfg3_full_size_sampled():
+@pytest.mark.parametrize("tensor", TENSORS)
+def test_T1_tensor_grid_cfg3_full_size_sampled(tensor):
     cfg = C.CFG3
     b = G.make_batch(cfg, [0, 5000, 9999])
     nodes = G.axis_nodes(cfg)
-    g = gpu_grid(b, cfg, nodes, algo=TENSOR)
+    g = gpu_grid(b, cfg, nodes, algo=tensor)
     rng = np.random.default_rng(9)
     pick = [np.unique(np.concatenate([np.sort(rng.choice(len(n), 48, replace=False)), [0, len(n) - 1]]))
             for n in nodes]
@@ -419,11 +423,12 @@ def test_T1_tensor_grid_cfg3_full_size_sampled():
     assert ok, worst
 
 
-def test_tensor_vs_separable_cfg3_batch_and_peaks():
+@pytest.mark.parametrize("tensor", TENSORS)
+def test_tensor_vs_separable_cfg3_batch_and_peaks(tensor):
     cfg = C.CFG3
     b = G.make_batch(cfg, range(32))
     nodes = G.axis_nodes(cfg)
-    gt = gpu_grid(b, cfg, nodes, algo=TENSOR)
+    gt = gpu_grid(b, cfg, nodes, algo=tensor)
     gs = gpu_grid(b, cfg, nodes, algo=R.retina.GRID_SEPARABLE)
     err = np.abs(gt.astype(np.float64) - gs) / (2e-5 * np.maximum(gs, 1e-6))
     assert err.max() <= 1.0, err.max()
@@ -534,23 +539,25 @@ def test_newton_identities():
 # --------------------------------------------------------------------------- tensor-core grid (SLOPE3)
 @pytest.mark.parametrize("shape", [(5, 37, 45), (3, 70, 33), (130, 260, 3)])
 @pytest.mark.parametrize("hint", [True, False])
-def test_T1_tensor_grid_slope3_ragged(shape, hint):
+@pytest.mark.parametrize("tensor", TENSORS)
+def test_T1_tensor_grid_slope3_ragged(shape, hint, tensor):
     b = synthetic_batch(C.SLOPE3, [700, 0, 1, 5000, 37], seed=11)
     nodes = [np.linspace(lo, hi, n).astype(np.float32) for (lo, hi), n in
              zip([(-0.3, 0.3), (-0.3, 0.3), (-150.0, 150.0)], shape)]
     cfg = C.Config(name="t", model=C.SLOPE3, n_events=5, seed=0, n_tracks=0, sigma=0.88)
-    g = gpu_grid(b, cfg, nodes, hint=hint, algo=TENSOR)
+    g = gpu_grid(b, cfg, nodes, hint=hint, algo=tensor)
     ref = ora.grid(C.SLOPE3, b.offsets, b.hits, nodes, 0.88)
     assert np.all(g[1] == 0.0)
     ok, worst = PU.t1_response(g, ref)
     assert ok, worst
 
 
-def test_T1_tensor_grid_cfg4_full_size_sampled_and_peaks():
+@pytest.mark.parametrize("tensor", TENSORS)
+def test_T1_tensor_grid_cfg4_full_size_sampled_and_peaks(tensor):
     cfg = C.CFG4
     b = G.make_batch(cfg, [0, 1])
     nodes = G.axis_nodes(cfg)
-    g = gpu_grid(b, cfg, nodes, algo=TENSOR)
+    g = gpu_grid(b, cfg, nodes, algo=tensor)
     rng = np.random.default_rng(12)
     pick = [np.unique(np.concatenate([np.sort(rng.choice(len(n), 12, replace=False)), [0, len(n) - 1]]))
             for n in nodes]
@@ -658,7 +665,7 @@ def test_many_events_launch_chunking():
     b = G.EventBatch(offsets=off, hits=hits, event_ids=np.arange(E), truth=[None] * E, n_track_hits=counts)
     nodes = [np.linspace(-0.3, 0.3, 3).astype(np.float32)] * 2
     cfg = C.Config(name="t", model=C.SLOPE2, n_events=E, seed=0, n_tracks=0, sigma=0.44)
-    for algo in (R.retina.GRID_DIRECT, R.retina.GRID_SEPARABLE, TENSOR):
+    for algo in (R.retina.GRID_DIRECT, R.retina.GRID_SEPARABLE, *TENSORS):
         g = gpu_grid(b, cfg, nodes, algo=algo)
         sel = np.r_[0:5, 65530:65540, E - 5:E]
         sub = G.EventBatch(offsets=np.concatenate([[0], np.cumsum(counts[sel])]).astype(np.int32),
