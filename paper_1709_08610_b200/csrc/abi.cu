@@ -82,6 +82,10 @@ int retina_grid_response(const retina_events *ev, int model, float sigma, const 
     return retina_grid_response_ex(ev, model, sigma, axis_len, axis_nodes, response, RETINA_GRID_AUTO, stream);
 }
 
+#ifndef RETINA_T16_PERSISTENT
+#define RETINA_T16_PERSISTENT 0  // 1: experimental persistent fp16 kernel (measured slower, grid_tensor16p.cu)
+#endif
+
 int retina_grid_response_ex(const retina_events *ev, int model, float sigma, const int32_t *axis_len,
                             const float *const *axis_nodes, float *response, int algorithm, void *stream) {
     g_last_error[0] = 0;
@@ -125,7 +129,8 @@ int retina_grid_response_ex(const retina_events *ev, int model, float sigma, con
     if (algorithm == RETINA_GRID_TENSOR)
         err = retina::launch_grid_tensor(model, a, ev->n_events, (cudaStream_t)stream);
     else if (algorithm == RETINA_GRID_TENSOR_F16)
-        err = retina::launch_grid_tensor16(model, a, ev->n_events, (cudaStream_t)stream);
+        err = RETINA_T16_PERSISTENT ? retina::launch_grid_tensor16p(model, a, ev->n_events, (cudaStream_t)stream)
+                                    : retina::launch_grid_tensor16(model, a, ev->n_events, (cudaStream_t)stream);
     else if (algorithm == RETINA_GRID_SEPARABLE)
         err = retina::launch_grid_separable(model, a, ev->n_events, (cudaStream_t)stream);
     else
