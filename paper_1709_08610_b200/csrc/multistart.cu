@@ -34,7 +34,7 @@ namespace retina {
 #endif
 constexpr int kMsThreads = RETINA_MS_THREADS;
 #ifndef RETINA_MS_POLY  // bit u*NP+p: seed pair p of the u-th hit of each two takes ex2_poly2 (FMA pipe)
-#define RETINA_MS_POLY 0
+#define RETINA_MS_POLY 0   // measured slower (profiles/r1_k4_fma_exp_offload.jsonl): off
 #endif
 constexpr unsigned kPolyMask = RETINA_MS_POLY;
 #ifndef RETINA_MS3_CX
@@ -189,7 +189,8 @@ __device__ __forceinline__ void ms_pass_x2(HitStage &st, const float (&th)[S][3]
             qx[p] = qy[p] = zero;
         }
     };
-    // one hit; U = position of the hit in its group of two (selects the FMA-pipe exponentials)
+    // one hit; U = position of the hit in its group of two (selects the FMA-pipe exponentials of
+    // the opt-in RETINA_MS_POLY variant; with the mask 0 every exponential is MUFU.EX2)
     auto hit = [&](const float4 hk, auto U) {
         if (hk.z != zprev) {  // warp-uniform plane change
             if (GRAD) flush();
@@ -245,12 +246,17 @@ __device__ __forceinline__ void ms_pass_x2(HitStage &st, const float (&th)[S][3]
         }
     };
     st.pass([&](const float4 *h, int len) {
-        int k = 0;
-        for (; k + 1 < len; k += 2) {
-            hit(h[k], IC<0>{});
-            hit(h[k + 1], IC<1>{});
+        if constexpr (kPolyMask == 0) {
+#pragma unroll 2
+            for (int k = 0; k < len; ++k) hit(h[k], IC<0>{});
+        } else {
+            int k = 0;
+            for (; k + 1 < len; k += 2) {
+                hit(h[k], IC<0>{});
+                hit(h[k + 1], IC<1>{});
+            }
+            if (k < len) hit(h[k], IC<0>{});
         }
-        if (k < len) hit(h[k], IC<0>{});
     });
     if (GRAD) flush();
 #pragma unroll
