@@ -73,6 +73,14 @@ def test_grid_response_validation(L):
     assert g(ctypes.byref(neg), 1, 0.5, alen, nodes, 16, None) == rt.RETINA_EINVAL
     big = _i(65536, 65536)
     assert g(ctypes.byref(ev), 1, 0.5, big, nodes, 16, None) == rt.RETINA_EUNSUPPORTED
+    gx = L.retina_grid_response_ex
+    assert gx(ctypes.byref(ev), 1, 0.5, alen, nodes, 16, 5, None) == rt.RETINA_EINVAL  # unknown algorithm
+    assert gx(ctypes.byref(ev), 1, 0.5, alen, nodes, 16, -1, None) == rt.RETINA_EINVAL
+    for algo in (rt.GRID_TENSOR, rt.GRID_TENSOR_F16, rt.GRID_SEPARABLE):  # LINE2D does not factorise
+        assert gx(ctypes.byref(ev), 0, 0.5, alen, nodes, 16, algo, None) == rt.RETINA_EUNSUPPORTED
+    e0 = _ev(n=0)  # nothing to launch: every algorithm accepts an empty batch
+    for algo in (rt.GRID_AUTO, rt.GRID_DIRECT, rt.GRID_SEPARABLE, rt.GRID_TENSOR, rt.GRID_TENSOR_F16):
+        assert gx(ctypes.byref(e0), 1, 0.5, alen, nodes, 16, algo, None) == rt.RETINA_OK
 
 
 def test_peaks_validation(L):
@@ -111,6 +119,33 @@ def test_multistart_validation(L):
     assert m(ctypes.byref(ev), 1, 0.5, 8, 16, 1, float("inf"), lo, hi, 16, 16, None, None) == rt.RETINA_EINVAL
     assert m(ctypes.byref(ev), 1, 0.5, 8, None, 1, 0.1, lo, hi, 16, 16, None, None) == rt.RETINA_EINVAL
     assert m(ctypes.byref(ev), 1, 0.5, 0, None, 1, 0.1, lo, hi, None, None, None, None) == rt.RETINA_OK
+
+
+def test_newton_validation(L):
+    for fn in (L.retina_multistart_newton, L.retina_multistart_newton_ex):
+        ex = fn is L.retina_multistart_newton_ex
+        ev = _ev()
+        lo, hi = _f(-1, -1), _f(1, 1)
+        sg, et = _f(0.5, 0.2), _f(1e-3, 1e-3)
+
+        def call(model=1, S=8, steps=2, sig=sg, eta=et, fs=0.2, mh=8, lo_=lo, hi_=hi, th=16, R=16):
+            args = [ctypes.byref(ev), model, S, 16, steps, sig, eta, fs, mh, lo_, hi_, th, R, None]
+            if ex:
+                args.append(None)
+            return fn(*args, None)
+
+        assert call(model=0) == rt.RETINA_EUNSUPPORTED          # LINE2D has no Newton kernel
+        assert call(model=9) == rt.RETINA_EINVAL
+        assert call(S=-1) == rt.RETINA_EINVAL
+        assert call(steps=-1) == rt.RETINA_EINVAL
+        assert call(steps=17) == rt.RETINA_EUNSUPPORTED          # > kMaxNewtonSteps
+        assert call(sig=_f(0.0, 0.2)) == rt.RETINA_EINVAL
+        assert call(eta=_f(float("nan"), 1.0)) == rt.RETINA_EINVAL
+        assert call(fs=-1.0) == rt.RETINA_EINVAL
+        assert call(mh=-1) == rt.RETINA_EINVAL
+        assert call(lo_=hi, hi_=lo) == rt.RETINA_EINVAL
+        assert call(th=None) == rt.RETINA_EINVAL
+        assert call(S=0, th=None, R=None) == rt.RETINA_OK        # nothing to do
 
 
 def test_merge_validation(L):
