@@ -178,7 +178,7 @@ size_t retina_find_peaks_workspace_size(int32_t n_events, int32_t P, const int32
     long long cells = 1;
     for (int i = 0; i < P; ++i) cells *= (axis_len[i] > 0 ? axis_len[i] : 0);
     if (cells <= 0 || cells > 0x7fffffffLL) return 0;
-    return (size_t)n_events * (size_t)retina::peaks_slabs((int)cells) * sizeof(int32_t);
+    return retina::peaks_workspace_bytes(n_events, (int)cells);
 }
 
 int retina_find_peaks_ws(const float *response, int32_t n_events, int32_t P, const int32_t *axis_len,

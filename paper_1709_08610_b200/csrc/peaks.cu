@@ -16,6 +16,7 @@ namespace retina {
 constexpr int kPeakThreads = 512;
 constexpr int kPeakV = 4;
 constexpr int kSlabCells = 131072;  // cells per CTA in the workspace (two-pass) variant
+constexpr int kSlabList = 256;      // peaks a slab keeps from pass 1 (more: pass 2 rescans it)
 
 __device__ __forceinline__ int warp_incl_scan(int v) {
     const int lane = threadIdx.x & 31;
@@ -67,7 +68,7 @@ __device__ __forceinline__ bool is_peak(const float *__restrict__ g, int c, int 
 // i-th peak found at output position pos0 + i.  Returns the number of peaks in the range.
 template <int P, bool WRITE>
 __device__ __forceinline__ int scan_range(const PeakArgs &a, const float *g, int32_t *oi, float *ov, int c_begin,
-                                          int c_end, int pos0, int *s_warp) {
+                                          int c_end, int pos0, int *s_warp, int cap) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     int total = 0;
     for (int base = c_begin; base < c_end; base += kPeakThreads * kPeakV) {
@@ -93,7 +94,7 @@ __device__ __forceinline__ int scan_range(const PeakArgs &a, const float *g, int
 #pragma unroll
             for (int v = 0; v < kPeakV; ++v) {
                 if (mask & (1u << v)) {
-                    if (pos < a.capacity) {
+                    if (pos < cap) {
                         oi[pos] = c0 + v;
                         ov[pos] = __ldg(g + c0 + v);
                     }
@@ -115,22 +116,43 @@ __global__ void __launch_bounds__(kPeakThreads) find_peaks_kernel(PeakArgs a) {
     const int cells = a.n0 * a.n1 * a.n2;
     const float *g = a.R + (int64_t)e * cells;
     const int total = scan_range<P, true>(a, g, a.idx + (int64_t)e * a.capacity, a.val + (int64_t)e * a.capacity,
-                                          0, cells, 0, s_warp);
+                                          0, cells, 0, s_warp, a.capacity);
     if (threadIdx.x == 0) a.cnt[e] = total;
 }
 
-// Two passes over slabs of kSlabCells cells, grid (slabs, events), with a caller-owned int32
-// workspace [events][slabs]: (1) count per slab; (2) each slab sums the counts of the slabs
-// before it (fixed order: deterministic) and writes its peaks there; the last slab writes the
-// event's true count.  Same output as the single pass, many CTAs per event.
+// Two passes over slabs of kSlabCells cells, grid (slabs, events), with a caller-owned
+// workspace: int32 counts [events][slabs], then per slab a list of its first kSlabList peaks
+// (int32 index [events][slabs][kSlabList], fp32 value [events][slabs][kSlabList]).
+// (1) each slab scans its cells once, counts its peaks and keeps the first kSlabList of them
+// (ascending index); (2) each slab sums the counts of the slabs before it (fixed order:
+// deterministic) and copies its list to that offset -- only a slab with more than kSlabList
+// peaks scans its cells again.  The last slab writes the event's true count.  Same output as
+// the single pass, many CTAs per event, and (for sparse peaks) one read of the grid.
+struct SlabWs {
+    int32_t *count;
+    int32_t *idx;
+    float *val;
+    __device__ __forceinline__ static SlabWs at(int32_t *ws, int n_ev, int n_slabs) {
+        SlabWs w;
+        const int64_t lists = (int64_t)n_ev * n_slabs;
+        w.count = ws;
+        w.idx = ws + lists;
+        w.val = reinterpret_cast<float *>(ws + lists + lists * kSlabList);
+        return w;
+    }
+};
+
 template <int P>
 __global__ void __launch_bounds__(kPeakThreads) count_peaks_slab_kernel(PeakArgs a, int32_t *ws, int n_slabs) {
     __shared__ int s_warp[kPeakThreads / 32];
     const int e = a.e_base + blockIdx.y, b = blockIdx.x;
     const int cells = a.n0 * a.n1 * a.n2;
     const int c_begin = b * kSlabCells, c_end = min(cells, c_begin + kSlabCells);
-    const int n = scan_range<P, false>(a, a.R + (int64_t)e * cells, nullptr, nullptr, c_begin, c_end, 0, s_warp);
-    if (threadIdx.x == 0) ws[(int64_t)blockIdx.y * n_slabs + b] = n;
+    const SlabWs w = SlabWs::at(ws, gridDim.y, n_slabs);
+    const int64_t slab = (int64_t)blockIdx.y * n_slabs + b;
+    const int n = scan_range<P, true>(a, a.R + (int64_t)e * cells, w.idx + slab * kSlabList,
+                                      w.val + slab * kSlabList, c_begin, c_end, 0, s_warp, kSlabList);
+    if (threadIdx.x == 0) w.count[slab] = n;
 }
 
 template <int P>
@@ -139,19 +161,31 @@ __global__ void __launch_bounds__(kPeakThreads) write_peaks_slab_kernel(PeakArgs
     __shared__ int s_off;
     const int e = a.e_base + blockIdx.y, b = blockIdx.x;
     const int cells = a.n0 * a.n1 * a.n2;
-    const int32_t *w = ws + (int64_t)blockIdx.y * n_slabs;
+    const SlabWs w = SlabWs::at(const_cast<int32_t *>(ws), gridDim.y, n_slabs);
+    const int32_t *cnt = w.count + (int64_t)blockIdx.y * n_slabs;
     if (threadIdx.x == 0) {
         int off = 0;
-        for (int i = 0; i < b; ++i) off += w[i];
+        for (int i = 0; i < b; ++i) off += cnt[i];
         s_off = off;
     }
     __syncthreads();
-    const int off = s_off;
-    const int c_begin = b * kSlabCells, c_end = min(cells, c_begin + kSlabCells);
-    if (off < a.capacity)
-        scan_range<P, true>(a, a.R + (int64_t)e * cells, a.idx + (int64_t)e * a.capacity,
-                            a.val + (int64_t)e * a.capacity, c_begin, c_end, off, s_warp);
-    if (b == n_slabs - 1 && threadIdx.x == 0) a.cnt[e] = off + w[b];
+    const int off = s_off, n = cnt[b];
+    int32_t *oi = a.idx + (int64_t)e * a.capacity;
+    float *ov = a.val + (int64_t)e * a.capacity;
+    if (off < a.capacity) {
+        if (n <= kSlabList) {  // pass 1 kept every peak of this slab: copy, no grid read
+            const int64_t slab = (int64_t)blockIdx.y * n_slabs + b;
+            const int m = min(n, a.capacity - off);
+            for (int i = threadIdx.x; i < m; i += kPeakThreads) {
+                oi[off + i] = w.idx[slab * kSlabList + i];
+                ov[off + i] = w.val[slab * kSlabList + i];
+            }
+        } else {
+            const int c_begin = b * kSlabCells, c_end = min(cells, c_begin + kSlabCells);
+            scan_range<P, true>(a, a.R + (int64_t)e * cells, oi, ov, c_begin, c_end, off, s_warp, a.capacity);
+        }
+    }
+    if (b == n_slabs - 1 && threadIdx.x == 0) a.cnt[e] = off + n;
 }
 
 cudaError_t launch_find_peaks(const PeakArgs &a0, int n_events, cudaStream_t stream) {
@@ -165,6 +199,11 @@ cudaError_t launch_find_peaks(const PeakArgs &a0, int n_events, cudaStream_t str
 }
 
 int peaks_slabs(int cells) { return (cells + kSlabCells - 1) / kSlabCells; }
+
+size_t peaks_workspace_bytes(long long n_events, int cells) {
+    const long long lists = n_events * peaks_slabs(cells);
+    return (size_t)lists * (sizeof(int32_t) + (size_t)kSlabList * (sizeof(int32_t) + sizeof(float)));
+}
 
 cudaError_t launch_find_peaks_ws(const PeakArgs &a0, int n_events, int32_t *ws, cudaStream_t stream) {
     const int cells = a0.n0 * a0.n1 * a0.n2;

@@ -96,9 +96,11 @@ def test_peaks_validation(L):
 def test_peaks_workspace_size_and_validation(L):
     sz = L.retina_find_peaks_workspace_size
     sz.restype = ctypes.c_size_t
-    # 1024^2 cells -> 8 slabs of 131072 cells, 4 bytes each per event
-    assert sz(10, 2, _i(1024, 1024)) == 10 * 8 * 4
-    assert sz(3, 3, _i(256, 256, 256)) == 3 * 128 * 4
+    # 1024^2 cells -> 8 slabs of 131072 cells per event; per slab a count (4 B) and a list of
+    # 256 (index, value) pairs (8 B each)
+    per_slab = 4 + 256 * 8
+    assert sz(10, 2, _i(1024, 1024)) == 10 * 8 * per_slab
+    assert sz(3, 3, _i(256, 256, 256)) == 3 * 128 * per_slab
     assert sz(0, 2, _i(4, 4)) == 0 and sz(1, 4, _i(4, 4)) == 0
     p = L.retina_find_peaks_ws
     p.argtypes = [ctypes.c_void_p, ctypes.c_int32, ctypes.c_int32, ctypes.c_void_p, ctypes.c_float, ctypes.c_int32,

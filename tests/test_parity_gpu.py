@@ -214,6 +214,38 @@ def test_T3_peaks_workspace_path_identical(P, shape):
             assert np.array_equal(b[2].cpu().numpy(), rc)
 
 
+@pytest.mark.parametrize("P,shape", [(2, (3, 1024, 1024)), (3, (2, 96, 96, 96))])
+def test_T3_peaks_workspace_slab_lists_and_rescans(P, shape):
+    """Sparse peaks (kept in the per-slab lists of pass 1 and copied) next to a dense region
+    (more than 256 peaks in a slab: pass 2 rescans it), in the same event: the workspace path
+    equals the single-CTA path and the oracle bit for bit, for several capacities."""
+    rng = np.random.default_rng(40 + P)
+    g = rng.uniform(0.0, 1.0, shape).astype(np.float32)          # below threshold everywhere
+    flat = g.reshape(shape[0], -1)
+    cells = flat.shape[1]
+    for e in range(shape[0]):
+        pk = rng.choice(cells, 300, replace=False)                 # isolated planted peaks
+        flat[e, pk] = rng.uniform(3.0, 9.0, 300).astype(np.float32)
+        d0 = 131072 * (e % max(1, cells // 131072))                # one dense slab per event
+        flat[e, d0:d0 + 20000] = rng.integers(2, 9, 20000).astype(np.float32)
+    g = flat.reshape(shape)
+    dg = dev(g)
+    ws = torch.empty((R.retina.find_peaks_workspace_size(shape[0], shape[1:]) // 4 + 1,), dtype=torch.int32,
+                     device=DEV)
+    for thr, cap in ((2.5, 1 << 20), (2.5, 100), (2.5, 4000)):
+        a = R.retina_find_peaks(dg, P, thr, cap)
+        b = R.retina_find_peaks(dg, P, thr, cap, workspace=ws)
+        torch.cuda.synchronize()
+        assert torch.equal(a[2], b[2])
+        ri, rv, rc = ora.peaks(g.astype(np.float64), P, thr, cap)
+        assert np.array_equal(b[2].cpu().numpy(), rc)
+        for e in range(shape[0]):
+            k = min(int(rc[e]), cap)
+            assert np.array_equal(b[0][e, :k].cpu().numpy(), ri[e, :k])
+            assert np.array_equal(b[1][e, :k].cpu().numpy().astype(np.float64), rv[e, :k])
+            assert torch.equal(a[0][e, :k], b[0][e, :k])
+
+
 def test_T3_peaks_cfg4_slope3_sampled():
     cfg = C.CFG4
     b = G.make_batch(cfg, [1])
