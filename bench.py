@@ -320,7 +320,8 @@ def main():
             # flops per (unit, hit) pair, executed as 3 kind::f16 products (hi.hi, hi.lo, lo.hi); the
             # fp32-accurate tensor peak is the measured dense bf16/f16 peak / 3
             peak = float(pk.get("bf16_tflops", 1590.0)) * 1e12 / 3.0
-            r = {"bound": "tensor", "kernel": "grid_tensor16_kernel (tcgen05.mma kind::f16, fp16 hi/lo split)",
+            r = {"bound": "tensor",
+                 "kernel": "grid_tensor16x2_kernel (tcgen05.mma cta_group::2 kind::f16, fp16 hi/lo split)",
                  "achieved": 2.0 * pairs_s / 1e12, "peak": peak / 1e12, "unit": "TFLOP/s",
                  "frac": 2.0 * pairs_s / peak,
                  "peak_basis": "MEASURED_PEAKS.json bf16_tflops (burst; f16 = bf16 rate) / 3 (three f16 products "

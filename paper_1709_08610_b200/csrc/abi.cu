@@ -86,6 +86,10 @@ int retina_grid_response(const retina_events *ev, int model, float sigma, const 
 #define RETINA_T16_PERSISTENT 0  // 1: experimental persistent fp16 kernel (measured slower, grid_tensor16p.cu)
 #endif
 
+#ifndef RETINA_T16_PAIR
+#define RETINA_T16_PAIR 1  // CTA-pair (cta_group::2) fp16 kernel (0: one CTA per 128x256 tile)
+#endif
+
 int retina_grid_response_ex(const retina_events *ev, int model, float sigma, const int32_t *axis_len,
                             const float *const *axis_nodes, float *response, int algorithm, void *stream) {
     g_last_error[0] = 0;
@@ -130,6 +134,7 @@ int retina_grid_response_ex(const retina_events *ev, int model, float sigma, con
         err = retina::launch_grid_tensor(model, a, ev->n_events, (cudaStream_t)stream);
     else if (algorithm == RETINA_GRID_TENSOR_F16)
         err = RETINA_T16_PERSISTENT ? retina::launch_grid_tensor16p(model, a, ev->n_events, (cudaStream_t)stream)
+              : RETINA_T16_PAIR     ? retina::launch_grid_tensor16x2(model, a, ev->n_events, (cudaStream_t)stream)
                                     : retina::launch_grid_tensor16(model, a, ev->n_events, (cudaStream_t)stream);
     else if (algorithm == RETINA_GRID_SEPARABLE)
         err = retina::launch_grid_separable(model, a, ev->n_events, (cudaStream_t)stream);

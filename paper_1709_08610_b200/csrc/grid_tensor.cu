@@ -608,6 +608,257 @@ __global__ void __launch_bounds__(32 * (T16_WARPS + 1), 1) grid_tensor16_kernel(
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(2 * TC_N));
 }
 
+// ------------------------------------------------------------------------------------------------
+// CTA-pair variant of the fp16-split kernel (cta_group::2): a cluster of two CTAs on one TPC
+// computes a 256 (tx) x 256 (ty) tile with M = 256 MMAs issued by the even CTA.  CTA r holds
+// the A rows (tx) 128 r .. 128 r + 127 of the pair tile and HALF of the B operand (ty rows
+// 128 r .. 128 r + 127); its TMEM receives its own 128 rows x 256 columns.  Each CTA therefore
+// generates 128 + 128 factor rows per hit for 32,768 pairs instead of 128 + 256: a third less
+// generation work, which is what limits the one-CTA kernel.  The odd CTA's generating warps
+// arrive on the even CTA's full barrier (mapa + mbarrier.arrive.release.cluster); the MMA
+// commit is multicast to both CTAs' empty barriers.
+#ifndef RETINA_X2_NS
+#define RETINA_X2_NS 2
+#endif
+#ifndef RETINA_X2_KC
+#define RETINA_X2_KC 64
+#endif
+constexpr int X2_KC = RETINA_X2_KC;                    // hits per chunk
+constexpr int X2_NS = RETINA_X2_NS;
+constexpr int X2_KB = X2_KC / 8;                       // 8-hit k-blocks per chunk
+constexpr int X2_PART = 128 * X2_KC * 2;               // one fp16 part (hi or lo) of A or of B-half
+constexpr int X2_STAGE = 4 * X2_PART;                  // A hi, A lo, B hi, B lo: 64 KB
+constexpr int X2_WARPS = 16;                           // generating warps (+1 MMA warp)
+constexpr int X2_NR = X2_WARPS / X2_KB;                // row sets per k-block (2)
+constexpr int X2_NA = 4 / X2_NR, X2_NB = 4 / X2_NR;   // A and B rows per lane per chunk (2, 2)
+constexpr uint32_t kTcIdescF16M256 =
+    (1u << 4) | ((uint32_t)(TC_N >> 3) << 17) | ((uint32_t)(256 >> 4) << 24);  // M = 256 (pair)
+static_assert(X2_NS * X2_STAGE + 1024 + 64 * 16 <= 227 * 1024, "operand ring must leave room for hits");
+
+__device__ __forceinline__ uint32_t cluster_rank() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ uint32_t mapa_rank0(uint32_t saddr) {
+    uint32_t r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, 0;" : "=r"(r) : "r"(saddr));
+    return r;
+}
+__device__ __forceinline__ void mbar_arrive_remote(uint32_t cluster_addr) {
+    asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+}
+__device__ __forceinline__ void mbar_wait_cluster(uint64_t *bar, uint32_t parity) {
+    uint32_t done;
+    do {
+        asm volatile(
+            "{\n\t.reg .pred p;\n\t"
+            "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2;\n\t"
+            "selp.u32 %0, 1, 0, p;\n\t}"
+            : "=r"(done)
+            : "r"(smem_u32(bar)), "r"(parity)
+            : "memory");
+    } while (!done);
+}
+__device__ __forceinline__ void tc2_mma_f16(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+        "l"(da), "l"(db), "r"(kTcIdescF16M256), "r"(accumulate));
+}
+__device__ __forceinline__ void tc2_commit_both(uint64_t *bar) {
+    asm volatile(
+        "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+            smem_u32(bar)),
+        "h"((unsigned short)3)
+        : "memory");
+}
+
+template <int MODEL, bool ZREF>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(32 * (X2_WARPS + 1), 1)
+    grid_tensor16x2_kernel(GridArgs a) {
+    extern __shared__ __align__(1024) uint8_t s_raw[];
+    __shared__ __align__(8) uint64_t s_bar[2];
+    __shared__ __align__(8) uint64_t s_full[X2_NS];   // used in the even CTA: 2 x 16 warps arrive
+    __shared__ __align__(8) uint64_t s_empty[X2_NS];  // both CTAs: the multicast MMA commit arrives
+    __shared__ __align__(8) uint64_t s_done;
+    __shared__ uint32_t s_tmem;
+
+    uint8_t *stage_base = s_raw;
+    float4 *s_hits = reinterpret_cast<float4 *>(s_raw + X2_NS * X2_STAGE);
+
+    const uint32_t rank = cluster_rank();
+    const int e = a.e_base + blockIdx.y;
+    const int tn = (a.n1 + TC_N - 1) / TC_N;
+    const int nl = (MODEL == kSlope3) ? a.n2 : 1;
+    const int pair = blockIdx.x >> 1;  // one pair tile per cluster
+    const int l = pair % nl, tile = pair / nl;
+    const int t_n = tile % tn, p_m = tile / tn;
+    const int t_m = 2 * p_m + (int)rank;  // this CTA's 128-row block of tx
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const bool mma_warp = warp == X2_WARPS;
+
+    if (warp == 0) {  // both CTAs: 2 accumulators (hi.hi and hi.lo + lo.hi) x 256 columns
+        asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&s_tmem)),
+                     "r"(2 * TC_N));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+        tc_fence_before();
+    }
+    if (tid == 0) {
+        for (int i = 0; i < X2_NS; ++i) {
+            mbar_init(&s_full[i], 2 * X2_WARPS);
+            mbar_init(&s_empty[i], 1);
+        }
+        mbar_init(&s_done, 1);
+        fence_mbar_init();
+    }
+    const int start = a.offsets[e], nh = a.offsets[e + 1] - start;
+    HitStage st;
+    st.init(s_hits, s_bar, a.hits + start, nh, a.cap);  // __syncthreads inside
+    cluster_sync_all();                                 // peer barriers initialised before remote arrives
+    tc_fence_after();
+    const uint32_t tmem = s_tmem;
+
+    const int kb = warp % X2_KB, rset = (warp / X2_KB) % X2_NR;
+    float pa[X2_NA], pb[X2_NB];
+    if (!mma_warp) {
+#pragma unroll
+        for (int t = 0; t < X2_NA; ++t)
+            pa[t] = __ldg(a.nodes0 + min(t_m * 128 + lane + 32 * (t * X2_NR + rset), a.n0 - 1));
+#pragma unroll
+        for (int t = 0; t < X2_NB; ++t)  // this CTA's half of the pair tile's 256 ty columns
+            pb[t] = __ldg(a.nodes1 + min(t_n * TC_N + (int)rank * 128 + lane + 32 * (t * X2_NR + rset), a.n1 - 1));
+    }
+    const float negK = a.negK;
+    const float zref = (MODEL == kSlope3) ? __ldg(a.nodes2 + l) : a.z_ref;
+    const uint32_t stage_saddr = smem_u32(stage_base);
+    constexpr bool EXACT_D = ZREF || MODEL == kSlope3;
+
+    int chunk = 0;
+    st.pass([&](const float4 *h, int len) {
+        for (int k0 = 0; k0 < len; k0 += X2_KC, ++chunk) {
+            const int s = chunk % X2_NS;
+            const uint32_t round = (uint32_t)(chunk / X2_NS);
+            if (mma_warp) {
+                if (rank == 0 && lane == 0) {
+                    mbar_wait_cluster(&s_full[s], round & 1u);
+                    tc_fence_after();
+                    const uint32_t base = stage_saddr + s * X2_STAGE;
+                    const uint32_t aH = base, aL = base + X2_PART, bH = base + 2 * X2_PART, bL = base + 3 * X2_PART;
+#pragma unroll
+                    for (int j = 0; j < X2_KC / 16; ++j) {  // K = 16 fp16 per MMA = 2 k-blocks
+                        const uint32_t o = j * 2 * (128 * 16);
+                        const uint32_t acc0 = (chunk > 0 || j > 0) ? 1u : 0u;
+                        tc2_mma_f16(tmem, umma_desc(aH + o, 128 * 16, 128), umma_desc(bH + o, 128 * 16, 128), acc0);
+                        tc2_mma_f16(tmem + TC_N, umma_desc(aH + o, 128 * 16, 128), umma_desc(bL + o, 128 * 16, 128),
+                                    acc0);
+                        tc2_mma_f16(tmem + TC_N, umma_desc(aL + o, 128 * 16, 128), umma_desc(bH + o, 128 * 16, 128),
+                                    1u);
+                    }
+                    tc2_commit_both(&s_empty[s]);
+                }
+                __syncwarp();
+                continue;
+            }
+            if (chunk >= X2_NS) mbar_wait(&s_empty[s], (round - 1) & 1u);  // MMAs of chunk - NS done
+            uint8_t *sb = stage_base + s * X2_STAGE;
+            float2 hx[4], hy[4], hz[4], hzl[4];
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+                const int k = k0 + kb * 8 + q;
+                const bool ok = k < len;
+                const float4 hk = h[ok ? k : 0];
+                float zh = hk.z, zl = 0.f;
+                if (EXACT_D) two_sum(hk.z, -zref, zh, zl);
+                const float xv = ok ? hk.x : 1e30f, yv = ok ? hk.y : 1e30f;
+                if (q & 1) {
+                    hx[q >> 1].y = xv; hy[q >> 1].y = yv; hz[q >> 1].y = zh; hzl[q >> 1].y = zl;
+                } else {
+                    hx[q >> 1].x = xv; hy[q >> 1].x = yv; hz[q >> 1].x = zh; hzl[q >> 1].x = zl;
+                }
+            }
+            const float2 nk2 = make_float2(negK, negK);
+#pragma unroll
+            for (int t = 0; t < X2_NA + X2_NB; ++t) {
+                const bool isA = t < X2_NA;
+                const float p = isA ? pa[t] : pb[t - X2_NA];
+                const float2 mp = make_float2(-p, -p);
+                uint32_t wh[4], wl[4];
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    const float2 c = isA ? hx[q] : hy[q];
+                    const float2 sres =
+                        EXACT_D ? __ffma2_rn(mp, hzl[q], __ffma2_rn(mp, hz[q], c)) : __ffma2_rn(mp, hz[q], c);
+                    const float2 arg = __fmul2_rn(__fmul2_rn(sres, sres), nk2);
+                    const float2 v = make_float2(ex2_approx(arg.x), ex2_approx(arg.y));
+                    const float2 vs = __fmul2_rn(v, make_float2(0x1p15f, 0x1p15f));
+                    const __half2 hh = __floats2half2_rn(vs.x, vs.y);
+                    const float2 hf = __half22float2(hh);                                    // exact
+                    const float2 lo = __ffma2_rn(hf, make_float2(-0x1p-15f, -0x1p-15f), v);  // exact
+                    const float2 ls = __fmul2_rn(lo, make_float2(0x1p26f, 0x1p26f));
+                    wh[q] = *reinterpret_cast<const uint32_t *>(&hh);
+                    wl[q] = pack_h2(ls.x, ls.y);
+                }
+                const int r = lane + 32 * ((isA ? t : t - X2_NA) * X2_NR + rset);
+                uint8_t *dh = sb + (isA ? 0 : 2 * X2_PART) + (size_t)(kb * 128 + r) * 16;
+                *reinterpret_cast<uint4 *>(dh) = make_uint4(wh[0], wh[1], wh[2], wh[3]);
+                *reinterpret_cast<uint4 *>(dh + X2_PART) = make_uint4(wl[0], wl[1], wl[2], wl[3]);
+            }
+            fence_proxy_async();
+            __syncwarp();
+            if (lane == 0) mbar_arrive_remote(mapa_rank0(smem_u32(&s_full[s])));
+        }
+    });
+
+    const int n_chunks = chunk;
+    if (mma_warp && rank == 0 && lane == 0) {
+        if (n_chunks > 0) tc2_commit_both(&s_done);  // every MMA of the pair tile complete, both CTAs told
+    }
+    if (n_chunks > 0) mbar_wait(&s_done, 0u);
+    tc_fence_after();
+    if (!mma_warp) tc_epilogue<MODEL, true>(a, e, t_m, t_n, l, nl, tmem, n_chunks, warp, lane);
+    tc_fence_before();
+    __syncthreads();
+    cluster_sync_all();  // the peer is done with its TMEM before the pair deallocates
+    if (warp == 0)
+        asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(2 * TC_N));
+}
+
+int tensor16x2_max_stage_hits() { return (227 * 1024 - X2_NS * X2_STAGE - 1024) / 16; }
+
+template <int MODEL, bool ZREF>
+static cudaError_t launch_tc16x2(const GridArgs &a0, int n_events, cudaStream_t stream) {
+    auto kern = grid_tensor16x2_kernel<MODEL, ZREF>;
+    GridArgs a = a0;
+    a.cap = min(a.cap, tensor16x2_max_stage_hits()) & ~1;
+    const size_t smem = X2_NS * (size_t)X2_STAGE + (size_t)a.cap * sizeof(float4);
+    cudaError_t err = ensure_dynamic_smem(kern, smem);
+    if (err != cudaSuccess) return err;
+    const long long pairs =
+        (long long)((a.n0 + 255) / 256) * ((a.n1 + TC_N - 1) / TC_N) * (MODEL == kSlope3 ? a.n2 : 1);
+    if (2 * pairs > 0x7fffffffLL) return cudaErrorInvalidConfiguration;
+    for (int e0 = 0; e0 < n_events; e0 += 65535) {
+        a.e_base = e0;
+        const int ne = min(65535, n_events - e0);
+        kern<<<dim3((unsigned)(2 * pairs), ne), 32 * (X2_WARPS + 1), smem, stream>>>(a);
+        err = cudaGetLastError();
+        if (err != cudaSuccess) return err;
+    }
+    return cudaSuccess;
+}
+
+cudaError_t launch_grid_tensor16x2(int model, const GridArgs &a, int n_events, cudaStream_t stream) {
+    if (n_events == 0) return cudaSuccess;
+    if (model == kSlope3) return launch_tc16x2<kSlope3, false>(a, n_events, stream);
+    if (model != kSlope2) return cudaErrorInvalidValue;
+    return (a.z_ref == 0.f) ? launch_tc16x2<kSlope2, false>(a, n_events, stream)
+                            : launch_tc16x2<kSlope2, true>(a, n_events, stream);
+}
+
 int tensor16_max_stage_hits() { return (227 * 1024 - T16_NS * T16_STAGE_BYTES - 1024) / 16; }
 
 template <int MODEL, bool ZREF>

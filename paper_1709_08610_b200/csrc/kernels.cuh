@@ -102,6 +102,7 @@ cudaError_t launch_grid_separable(int model, const GridArgs &a, int n_events, cu
 cudaError_t launch_grid_tensor(int model, const GridArgs &a, int n_events, cudaStream_t stream);
 cudaError_t launch_grid_tensor16(int model, const GridArgs &a, int n_events, cudaStream_t stream);
 cudaError_t launch_grid_tensor16p(int model, const GridArgs &a, int n_events, cudaStream_t stream);
+cudaError_t launch_grid_tensor16x2(int model, const GridArgs &a, int n_events, cudaStream_t stream);
 cudaError_t launch_newton(int model, const NewtonArgs &a, int n_events, cudaStream_t stream);
 cudaError_t launch_multistart(int model, const MultistartArgs &a, int n_events, cudaStream_t stream);
 cudaError_t launch_find_peaks(const PeakArgs &a, int n_events, cudaStream_t stream);
