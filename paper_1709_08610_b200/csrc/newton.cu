@@ -411,6 +411,7 @@ struct LineSearchSmem {
     float dir[kNtThreads * S][P];
     float R0[kNtThreads * S], slope[kNtThreads * S];
     int ntrial[kNtThreads * S];  // halvings tried (k of the accepted trial, else max_halvings)
+    int kmin[kNtThreads * S];    // smallest halving k of the current round that passed Armijo
     int q[2][kNtThreads * S];
     int nq[2];
 };
@@ -421,6 +422,10 @@ struct LineSearchSmem {
 #ifndef RETINA_NT_SQ
 #define RETINA_NT_SQ 1  // queue entries per worker thread (1 measured best: C0 5.3 vs 6.0 (2), 7.8 (4) on cfg3)
 #endif
+#ifndef RETINA_NT_LSB
+#define RETINA_NT_LSB 4  // halvings evaluated together per queue round (measured: C0 4.9 / 4.0 / 3.8 / 3.8 for 1 / 2 / 4 / 8)
+#endif
+constexpr int kNtLsBatch = RETINA_NT_LSB;
 template <int MODEL, int S, bool ZREF>
 __device__ __forceinline__ void nt_line_search_queue(HitStage &st, const NewtonArgs &a, float negK, float (&th)[S][3],
                                                      const float (&p)[S][3], const float (&R0)[S],
@@ -444,23 +449,31 @@ __device__ __forceinline__ void nt_line_search_queue(HitStage &st, const NewtonA
         ls.R0[slot] = R0[s];
         ls.slope[slot] = slope[s];
         ls.ntrial[slot] = a.max_halvings;
+        ls.kmin[slot] = 0x7fffffff;
         ls.q[0][atomicAdd(&ls.nq[0], 1)] = slot;
     }
     __syncthreads();
+    // Rounds of LB halvings: every (queued seed, k) pair of the round is one entry, all evaluated
+    // in the same pass; the seed takes the smallest k whose trial passes Armijo (exactly the
+    // sequential rule's choice -- the later trials of the round are speculative work).
     int cur = 0;
-    float alpha = 1.f;
-    for (int k = 1; k <= a.max_halvings; ++k) {
-        alpha *= 0.5f;
+    for (int k0 = 1; k0 <= a.max_halvings; k0 += kNtLsBatch) {
+        const int nb = min(kNtLsBatch, a.max_halvings - k0 + 1);
         const int n = ls.nq[cur];  // final: written before the last barrier
         if (n == 0) break;
-        for (int wb = wbase; wb < n; wb += kNtThreads * SQ) {  // n may exceed one sweep of the CTA
-            int slot[SQ];
+        const int ne = n * nb;
+        for (int wb = wbase; wb < ne; wb += kNtThreads * SQ) {  // ne may exceed one sweep of the CTA
+            int slot[SQ], kk[SQ];
             float tt[SQ][3];
 #pragma unroll
             for (int s = 0; s < SQ; ++s) {
                 const int e = wb + s * 32 + lane;
-                slot[s] = (e < n) ? ls.q[cur][e] : -1;
-                const int src = (e < n) ? slot[s] : ls.q[cur][0];  // padding lanes repeat entry 0
+                const bool valid = e < ne;
+                const int qi = valid ? e / nb : 0;  // padding lanes repeat entry 0
+                kk[s] = k0 + (valid ? e - qi * nb : 0);
+                const int src = ls.q[cur][qi];
+                slot[s] = valid ? src : -1;
+                const float alpha = __int_as_float((127 - kk[s]) << 23);  // 2^-k, exact
 #pragma unroll
                 for (int i = 0; i < 3; ++i)
                     tt[s][i] = (i < P) ? fminf(fmaxf(__fmaf_rn(alpha, ls.dir[src][i], ls.base[src][i]), a.lo[i]),
@@ -473,13 +486,21 @@ __device__ __forceinline__ void nt_line_search_queue(HitStage &st, const NewtonA
             for (int s = 0; s < SQ; ++s) {
                 if (slot[s] < 0) continue;
                 const int sl = slot[s];
-                if (Rt[s] >= __fmaf_rn(1e-4f * alpha, ls.slope[sl], ls.R0[sl])) {
+                const float alpha = __int_as_float((127 - kk[s]) << 23);
+                if (Rt[s] >= __fmaf_rn(1e-4f * alpha, ls.slope[sl], ls.R0[sl])) atomicMin(&ls.kmin[sl], kk[s]);
+            }
+        }
+        __syncthreads();  // every trial of the round is decided
+        for (int i = tid; i < n; i += kNtThreads) {
+            const int sl = ls.q[cur][i], km = ls.kmin[sl];
+            if (km < k0 + nb) {  // accepted: recompute the trial point (same operations, same bits)
+                const float alpha = __int_as_float((127 - km) << 23);
 #pragma unroll
-                    for (int i = 0; i < P; ++i) ls.base[sl][i] = tt[s][i];
-                    ls.ntrial[sl] = k;
-                } else {
-                    ls.q[cur ^ 1][atomicAdd(&ls.nq[cur ^ 1], 1)] = sl;
-                }
+                for (int d = 0; d < P; ++d)
+                    ls.base[sl][d] = fminf(fmaxf(__fmaf_rn(alpha, ls.dir[sl][d], ls.base[sl][d]), a.lo[d]), a.hi[d]);
+                ls.ntrial[sl] = km;
+            } else {
+                ls.q[cur ^ 1][atomicAdd(&ls.nq[cur ^ 1], 1)] = sl;
             }
         }
         __syncthreads();  // all reads of queue cur and all pushes to cur ^ 1 are done
