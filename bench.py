@@ -261,28 +261,50 @@ def main():
         del graph
 
     # ---- e2e through the public API with host buffers (pinned H2D + D2H inside the region)
-    e2e_steps = a.e2e_steps if a.e2e_steps is not None else max(1, min(a.steps, 3))
+    e2e_steps = a.e2e_steps if a.e2e_steps is not None else max(1, min(a.steps, 5))
     off_h = torch.from_numpy(batch.offsets).pin_memory()
     hits_h = torch.from_numpy(batch.hits).pin_memory()
     seeds_h = torch.from_numpy(seeds).pin_memory()
     res_h = torch.empty(gathered.shape, dtype=torch.float32).pin_memory()
     h2d = off_h.numel() * 4 + hits_h.numel() * 4 + seeds_h.numel() * 4
     d2h = res_h.numel() * 4
-    dev_off = torch.empty_like(off_h, device="cuda")
-    dev_hits = torch.empty_like(hits_h, device="cuda")
-    dev_seeds = torch.empty_like(seeds_h, device="cuda")
-    b2 = dbatch.__class__(offsets=dev_off, hits=dev_hits, seeds=dev_seeds, max_event_hits=dbatch.max_event_hits,
-                          n_hits_per_event=dbatch.n_hits_per_event)
+    # two device copies of the inputs: the H2D copy of step i+1 (copy stream) overlaps the
+    # compute of step i; every step still moves its own inputs host -> device inside the region
+    bufs = []
+    for _ in range(2):
+        d_off, d_hits, d_seeds = (torch.empty_like(x, device="cuda") for x in (off_h, hits_h, seeds_h))
+        bufs.append((d_off, d_hits, d_seeds,
+                     dbatch.__class__(offsets=d_off, hits=d_hits, seeds=d_seeds,
+                                      max_event_hits=dbatch.max_event_hits,
+                                      n_hits_per_event=dbatch.n_hits_per_event)))
+    copy_stream = torch.cuda.Stream()
+    ready = [torch.cuda.Event() for _ in range(2)]
+    done = [None, None]
+
+    def h2d_into(i):
+        d_off, d_hits, d_seeds, _ = bufs[i % 2]
+        with torch.cuda.stream(copy_stream):
+            if done[i % 2] is not None:
+                copy_stream.wait_event(done[i % 2])  # the step that last read this buffer is done
+            d_off.copy_(off_h, non_blocking=True)
+            d_hits.copy_(hits_h, non_blocking=True)
+            d_seeds.copy_(seeds_h, non_blocking=True)
+            ready[i % 2].record(copy_stream)
+
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
-    for _ in range(e2e_steps):
-        dev_off.copy_(off_h, non_blocking=True)
-        dev_hits.copy_(hits_h, non_blocking=True)
-        dev_seeds.copy_(seeds_h, non_blocking=True)
-        g2 = step(b2)
+    copy_stream.wait_stream(stream)
+    h2d_into(0)
+    for i in range(e2e_steps):
+        stream.wait_event(ready[i % 2])
+        g2 = step(bufs[i % 2][3])
+        done[i % 2] = torch.cuda.Event()
+        done[i % 2].record(stream)
+        if i + 1 < e2e_steps:
+            h2d_into(i + 1)
         res_h.copy_(g2, non_blocking=True)
     e1.record(stream)
     torch.cuda.synchronize()
