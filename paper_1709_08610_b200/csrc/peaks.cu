@@ -14,7 +14,11 @@
 namespace retina {
 
 constexpr int kPeakThreads = 512;
-constexpr int kPeakV = 4;
+#ifndef RETINA_PEAK_V
+#define RETINA_PEAK_V 16
+#endif
+constexpr int kPeakV = RETINA_PEAK_V;  // consecutive cells per thread per sweep (multiple of 4, <= 32)
+static_assert(kPeakV % 4 == 0 && kPeakV <= 32, "cells per thread");
 constexpr int kSlabCells = 131072;  // cells per CTA in the workspace (two-pass) variant
 constexpr int kSlabList = 256;      // peaks a slab keeps from pass 1 (more: pass 2 rescans it)
 
@@ -28,11 +32,10 @@ __device__ __forceinline__ int warp_incl_scan(int v) {
     return v;
 }
 
+// Neighbour test of cell c whose value v (>= threshold) is already loaded.
 template <int P>
-__device__ __forceinline__ bool is_peak(const float *__restrict__ g, int c, int n0, int n1, int n2,
-                                        float thr) {
-    const float v = __ldg(g + c);
-    if (!(v >= thr)) return false;
+__device__ __forceinline__ bool beats_neighbours(const float *__restrict__ g, int c, float v, int n0, int n1,
+                                                 int n2) {
     int l = 0, j, i;
     if (P == 3) {
         l = c % n2;
@@ -64,6 +67,13 @@ __device__ __forceinline__ bool is_peak(const float *__restrict__ g, int c, int 
     return true;
 }
 
+template <int P>
+__device__ __forceinline__ bool is_peak(const float *__restrict__ g, int c, int n0, int n1, int n2,
+                                        float thr) {
+    const float v = __ldg(g + c);
+    return v >= thr && beats_neighbours<P>(g, c, v, n0, n1, n2);
+}
+
 // Flags and (when WRITE) compacts the peaks of cells [c_begin, c_end) of one event, writing the
 // i-th peak found at output position pos0 + i.  Returns the number of peaks in the range.
 template <int P, bool WRITE>
@@ -74,10 +84,27 @@ __device__ __forceinline__ int scan_range(const PeakArgs &a, const float *g, int
     for (int base = c_begin; base < c_end; base += kPeakThreads * kPeakV) {
         const int c0 = base + threadIdx.x * kPeakV;
         unsigned mask = 0;
+        if (c0 + kPeakV <= c_end && ((reinterpret_cast<uintptr_t>(g + c0) & 15u) == 0)) {
+            // 16-byte loads for the thread's cells, all in flight together (most cells fail the
+            // threshold right here)
+            float vv[kPeakV];
 #pragma unroll
-        for (int v = 0; v < kPeakV; ++v) {
-            const int c = c0 + v;
-            if (c < c_end && is_peak<P>(g, c, a.n0, a.n1, a.n2, a.threshold)) mask |= 1u << v;
+            for (int u = 0; u < kPeakV; u += 4) {
+                const float4 q = __ldg(reinterpret_cast<const float4 *>(g + c0 + u));
+                vv[u] = q.x;
+                vv[u + 1] = q.y;
+                vv[u + 2] = q.z;
+                vv[u + 3] = q.w;
+            }
+#pragma unroll
+            for (int v = 0; v < kPeakV; ++v)
+                if (vv[v] >= a.threshold && beats_neighbours<P>(g, c0 + v, vv[v], a.n0, a.n1, a.n2)) mask |= 1u << v;
+        } else {
+#pragma unroll
+            for (int v = 0; v < kPeakV; ++v) {
+                const int c = c0 + v;
+                if (c < c_end && is_peak<P>(g, c, a.n0, a.n1, a.n2, a.threshold)) mask |= 1u << v;
+            }
         }
         const int cnt = __popc(mask);
         const int incl = warp_incl_scan(cnt);
