@@ -14,11 +14,13 @@
 namespace retina {
 
 constexpr int kPeakThreads = 512;
-#ifndef RETINA_PEAK_V
-#define RETINA_PEAK_V 16
-#endif
-constexpr int kPeakV = RETINA_PEAK_V;  // consecutive cells per thread per sweep (multiple of 4, <= 32)
-static_assert(kPeakV % 4 == 0 && kPeakV <= 32, "cells per thread");
+// Consecutive cells per thread per sweep: 16 (four float4 loads in flight) for P = 2; 4 for P = 3,
+// whose wider peaks put more cells above threshold, each with 26 neighbour reads, so fewer cells per
+// thread keep the warps balanced (cfg4 peaks 22 ms with 4 vs 78 with 16; cfg3 9.5 with 16 vs 15 with 4).
+template <int P>
+struct PeakV {
+    static constexpr int v = (P == 3) ? 4 : 16;
+};
 constexpr int kSlabCells = 131072;  // cells per CTA in the workspace (two-pass) variant
 constexpr int kSlabList = 256;      // peaks a slab keeps from pass 1 (more: pass 2 rescans it)
 
@@ -81,6 +83,7 @@ __device__ __forceinline__ int scan_range(const PeakArgs &a, const float *g, int
                                           int c_end, int pos0, int *s_warp, int cap) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     int total = 0;
+    constexpr int kPeakV = PeakV<P>::v;
     for (int base = c_begin; base < c_end; base += kPeakThreads * kPeakV) {
         const int c0 = base + threadIdx.x * kPeakV;
         unsigned mask = 0;
