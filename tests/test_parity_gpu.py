@@ -555,6 +555,26 @@ def test_newton_multistart_vs_oracle(name, n_ev, n_seeds):
         assert np.all(otc > 0)
 
 
+def test_newton_line_search_queue_deterministic():
+    """The line-search queue is filled with shared-memory atomics (entry order varies run to
+    run); every seed's result and evaluation count must not: two runs agree bit for bit, and
+    the run exercises the queue (seeds with more than one trial in some step)."""
+    cfg = C.CFG3
+    b = G.make_batch(cfg, [0, 1])
+    seeds = dev(G.make_seeds(cfg, [0, 1], n_seeds=2048))
+    sig, eta, fsig, mh = C.newton_schedule(cfg)
+    runs = []
+    for _ in range(2):
+        out = R.retina_multistart_newton_ex(events_of(b), cfg.model, seeds, sig, eta, fsig, mh, cfg.box_lo,
+                                            cfg.box_hi)
+        torch.cuda.synchronize()
+        runs.append([x.clone() for x in out])
+    for x, y in zip(*runs):
+        assert torch.equal(x, y)
+    ne = runs[0][3]
+    assert int((ne > 2 * len(sig) + 1).sum()) > 0  # some seeds needed halvings (queue path)
+
+
 def test_newton_identities():
     cfg = C.CFG2
     b = G.make_batch(cfg, [0])
