@@ -155,6 +155,9 @@ def run_reference(a):
     rank, world, _ = (int(os.environ.get(k, d)) for k, d in (("RANK", 0), ("WORLD_SIZE", 1), ("LOCAL_RANK", 0)))
     if rank != 0:
         return
+    # torchrun exports OMP_NUM_THREADS=1 to every rank; rank 0 alone runs the oracle here, on all
+    # the host's cores (read by OpenMP when the oracle library is first loaded, just below)
+    os.environ["OMP_NUM_THREADS"] = str(len(os.sched_getaffinity(0)))
     cfg = C.get_config(a.config)
     steps = []
     for _ in range(a.warmup + a.steps):
