@@ -342,11 +342,11 @@ def main():
         pairs_s = per_launch / (avg_ms * 1e-3)
         if ph == "grid" and cfg.model in (C.SLOPE2, C.SLOPE3):
             # tcgen05 fp16-split contraction (RETINA_GRID_AUTO = RETINA_GRID_TENSOR_F16): 2 algorithmic
-            # flops per (unit, hit) pair, executed as 3 kind::f16 products (hi.hi, hi.lo, lo.hi); the
+            # flops per (unit, hit) pair, executed as 3 kind::f16 products (h.h, h.l, l.h); the
             # fp32-accurate tensor peak is the measured dense bf16/f16 peak / 3
             peak = float(pk.get("bf16_tflops", 1590.0)) * 1e12 / 3.0
             r = {"bound": "tensor",
-                 "kernel": "grid_tensor16x2_kernel (tcgen05.mma cta_group::2 kind::f16, fp16 hi/lo split)",
+                 "kernel": "grid_tensor16pp_kernel (persistent, tcgen05.mma cta_group::2 kind::f16, fp16 hi/lo split)",
                  "achieved": 2.0 * pairs_s / 1e12, "peak": peak / 1e12, "unit": "TFLOP/s",
                  "frac": 2.0 * pairs_s / peak,
                  "peak_basis": "MEASURED_PEAKS.json bf16_tflops (burst; f16 = bf16 rate) / 3 (three f16 products "

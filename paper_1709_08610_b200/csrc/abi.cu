@@ -83,7 +83,7 @@ int retina_grid_response(const retina_events *ev, int model, float sigma, const 
 }
 
 #ifndef RETINA_T16_PERSISTENT
-#define RETINA_T16_PERSISTENT 0  // 1: experimental persistent fp16 kernel (measured slower, grid_tensor16p.cu)
+#define RETINA_T16_PERSISTENT 1  // persistent CTA-pair fp16 kernel (grid_tensor16p.cu); 0: one tile per CTA (pair)
 #endif
 
 #ifndef RETINA_T16_PAIR

@@ -446,15 +446,6 @@ static_assert(T16_NR >= 1 && 4 % T16_NR == 0, "warps / k-blocks must divide the 
 static_assert(T16_KC % 16 == 0, "K = 16 per kind::f16 MMA");
 static_assert(T16_NS * T16_STAGE_BYTES + 1024 + 64 * 16 <= 227 * 1024, "operand ring must leave room for hits");
 
-__device__ __forceinline__ uint32_t pack_h2(float a, float b) {
-    const __half2 h = __floats2half2_rn(a, b);
-    return *reinterpret_cast<const uint32_t *>(&h);
-}
-
-__device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
-    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
-}
-
 template <int MODEL, bool ZREF>
 __global__ void __launch_bounds__(32 * (T16_WARPS + 1), 1) grid_tensor16_kernel(GridArgs a) {
     extern __shared__ __align__(1024) uint8_t s_raw[];
@@ -631,52 +622,7 @@ constexpr int X2_STAGE = 4 * X2_PART;                  // A hi, A lo, B hi, B lo
 constexpr int X2_WARPS = 16;                           // generating warps (+1 MMA warp)
 constexpr int X2_NR = X2_WARPS / X2_KB;                // row sets per k-block (2)
 constexpr int X2_NA = 4 / X2_NR, X2_NB = 4 / X2_NR;   // A and B rows per lane per chunk (2, 2)
-constexpr uint32_t kTcIdescF16M256 =
-    (1u << 4) | ((uint32_t)(TC_N >> 3) << 17) | ((uint32_t)(256 >> 4) << 24);  // M = 256 (pair)
 static_assert(X2_NS * X2_STAGE + 1024 + 64 * 16 <= 227 * 1024, "operand ring must leave room for hits");
-
-__device__ __forceinline__ uint32_t cluster_rank() {
-    uint32_t r;
-    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
-    return r;
-}
-__device__ __forceinline__ void cluster_sync_all() {
-    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
-}
-__device__ __forceinline__ uint32_t mapa_rank0(uint32_t saddr) {
-    uint32_t r;
-    asm volatile("mapa.shared::cluster.u32 %0, %1, 0;" : "=r"(r) : "r"(saddr));
-    return r;
-}
-__device__ __forceinline__ void mbar_arrive_remote(uint32_t cluster_addr) {
-    asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
-}
-__device__ __forceinline__ void mbar_wait_cluster(uint64_t *bar, uint32_t parity) {
-    uint32_t done;
-    do {
-        asm volatile(
-            "{\n\t.reg .pred p;\n\t"
-            "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2;\n\t"
-            "selp.u32 %0, 1, 0, p;\n\t}"
-            : "=r"(done)
-            : "r"(smem_u32(bar)), "r"(parity)
-            : "memory");
-    } while (!done);
-}
-__device__ __forceinline__ void tc2_mma_f16(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t accumulate) {
-    asm volatile(
-        "{\n\t.reg .pred p;\n\t"
-        "setp.ne.b32 p, %4, 0;\n\t"
-        "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
-        "l"(da), "l"(db), "r"(kTcIdescF16M256), "r"(accumulate));
-}
-__device__ __forceinline__ void tc2_commit_both(uint64_t *bar) {
-    asm volatile(
-        "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
-            smem_u32(bar)),
-        "h"((unsigned short)3)
-        : "memory");
-}
 
 template <int MODEL, bool ZREF>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(32 * (X2_WARPS + 1), 1)

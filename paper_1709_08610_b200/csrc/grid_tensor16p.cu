@@ -1,247 +1,278 @@
-// grid_tensor16p.cu -- EXPERIMENTAL persistent variant of the fp16-split grid kernel
-// (-DRETINA_T16_PERSISTENT=1; default off).  Eq. (2) as a dense contraction over hits on the
-// tcgen05 tensor cores with fp16 operands (kind::f16), persistent and warp-specialised.
-// Measured (parity green on every tensor test) but SLOWER than the one-CTA-per-tile kernel
-// grid_tensor16_kernel: cfg3 10.6 vs 7.4 ms, cfg4 38 vs 15.4 ms per 1000 / 50 events -- the
-// third fp16 part adds generation work where generation, not the tensor pipe, is the limit, and
-// SLOPE3's z0-fastest 4-byte stores no longer meet in L2 across concurrently running CTAs.
+// grid_tensor16p.cu -- K1h, the default grid kernel for SLOPE2 / SLOPE3: persistent CTA-pair
+// variant of the fp16-split grid kernel (RETINA_T16_PERSISTENT, default 1).  Eq. (2) as a dense contraction over hits on the tcgen05 tensor
+// cores (kind::f16, cta_group::2, M = 256), with the per-tile prologue and epilogue taken off the
+// MMA critical path:
 //
 //     R[i][j] = sum_k EX[i][k] EY[j][k],  EX = 2^(-K (x - tx z)^2),  EY = 2^(-K (y - ty z)^2)
 //
 // (the exact factorisation of exp(-s^2/sigma^2) for the in-plane distance).
 //
-// Exact fp16 split with ONE accumulator.  Every factor v in [0, 1] is written as
+// Exact fp16 split with ONE accumulator, so that two accumulators fit TMEM and the epilogue of
+// tile i overlaps the MMAs of tile i+1.  Every factor v in [0, 1] is written as
 //     v = h + l,   h = fp16_rn(v 2^15) 2^-15 (exact back in fp32),   l = v - h (exact, |l| <= 2^-12 v),
-// and each operand row carries three fp16 parts, scaled so that all three products land on the
-// same scale 2^30 and accumulate into one fp32 TMEM accumulator:
+// and each operand row carries three fp16 parts, scaled so that the three products share the
+// scale 2^30 and accumulate into one fp32 TMEM accumulator:
 //     A = [h 2^15 | h 2^9  | l 2^21],   B = [h 2^15 | l 2^21 | h 2^9]
 //     A.B = 2^30 (h_x h_y + h_x l_y + l_x h_y)            R = D 2^-30.
-// Dropped: l_x l_y (<= 2^-24 relative).  fp16 rounding of l 2^21: <= 2^-24 relative of v, and where
-// a part falls below the fp16 normal range the absolute error stays <= 2^-45 per term (h 2^9 is
-// normal for h >= 2^-23, l 2^21 for l >= 2^-35) -- far below the T1 floor (1e-11 per cell).
+// Dropped: l_x l_y (<= 2^-24 relative).  fp16 rounding of l 2^21: <= 2^-24 relative of v; where a
+// part falls below the fp16 normal range (h 2^9 for h < 2^-23, l 2^21 for l < 2^-35) the absolute
+// error stays <= 2^-45 per term -- far below the T1 floor (1e-11 per cell).
 //
-// Persistent CTA per SM over a contiguous range of (event, tile[, z0]) work items (z0 fastest, so
-// one CTA writes neighbouring z0 values of the same cells back to back):
-//   warps 0-15  generate: per 32-hit chunk, warp w writes the 8-hit k-block w % 4 (16 B per row
-//               and part) of 1 A row and 2 B rows per lane into stage c % NS, then arrives on
-//               full[stage]; hits are read straight from global memory (L1-resident per event);
-//   warp  16    issues the 6 MMAs (M=128, N=256, K=16) of each chunk into the tile's accumulator
-//               buffer and commits them to empty[stage]; at the end of a tile it commits acc_full;
-//   warps 17-20 epilogue: TMEM -> registers (tcgen05.ld 32x32b.x16) -> global, then acc_empty.
-// TMEM: two 128 x 256 fp32 accumulators (all 512 columns), so the epilogue of tile i overlaps the
-// MMAs of tile i+1.
+// A cluster of two CTAs (one TPC) loops over (event, 256 x 256 pair tile [, z0]) work items: a
+// contiguous range for SLOPE2 (one hit load per event), round-robin for SLOPE3 (concurrent clusters
+// write neighbouring z0, the fastest output axis, so L2 merges their 4-byte stores).  Per CTA (rank r):
+//   warps 0-15  generate its 128 A rows (tx) and its half of B (128 ty rows) per 64-hit chunk
+//               into stage c % NS, then arrive on the even CTA's full[stage] (cluster arrive);
+//               hits live in shared memory, reloaded only when the event changes (or windowed
+//               when an event exceeds the stage);
+//   warp  16    (even CTA) issues the chunk's 6 MMAs (M = 256, N = 256, K = 16) into the tile's
+//               accumulator buffer, commits empty[stage] to both CTAs, and acc_full at tile end;
+//   warps 17-20 epilogue of its 128 rows: TMEM -> registers -> global, then a cluster arrive on
+//               the even CTA's acc_empty[buffer].
 #include "common.cuh"
 #include "kernels.cuh"
 #include "tcgen05.cuh"
-
-#include <cuda_fp16.h>
 
 #include <algorithm>
 
 namespace retina {
 
-#ifndef RETINA_P16_NS
-#define RETINA_P16_NS 2
+#ifndef RETINA_PP_KC
+#define RETINA_PP_KC 64
 #endif
-constexpr int P16_KC = 32;                           // hits per chunk
-constexpr int P16_NS = RETINA_P16_NS;                // operand stages in the ring
-constexpr int P16_KB = P16_KC / 8;                   // 8-hit k-blocks per chunk
-constexpr int P16_PART_A = TC_M * P16_KC * 2;        // one fp16 part of A: 8 KB
-constexpr int P16_PART_B = TC_N * P16_KC * 2;        // one fp16 part of B: 16 KB
-constexpr int P16_STAGE = 3 * P16_PART_A + 3 * P16_PART_B;  // 72 KB
-constexpr int P16_GEN_WARPS = 16;
-constexpr int P16_MMA_WARP = P16_GEN_WARPS;
-constexpr int P16_WARPS = P16_GEN_WARPS + 1 + 4;
-constexpr int P16_NR = P16_GEN_WARPS / P16_KB;       // row sets per k-block (4)
-constexpr int P16_NA = 4 / P16_NR, P16_NB = 8 / P16_NR;  // A and B rows per lane per chunk (1, 2)
-static_assert(P16_NS * P16_STAGE + 1024 <= 227 * 1024, "operand ring exceeds shared memory");
+#ifndef RETINA_PP_NS
+#define RETINA_PP_NS 2
+#endif
+constexpr int PP_KC = RETINA_PP_KC;                 // hits per chunk
+constexpr int PP_NS = RETINA_PP_NS;                 // operand stages in the ring
+constexpr int PP_KB = PP_KC / 8;                    // 8-hit k-blocks per chunk
+constexpr int PP_PART = 128 * PP_KC * 2;            // one fp16 part of A or of this CTA's B half
+constexpr int PP_STAGE = 6 * PP_PART;               // A: 3 parts, B half: 3 parts
+constexpr int PP_GEN_WARPS = 16;
+constexpr int PP_MMA_WARP = PP_GEN_WARPS;
+constexpr int PP_WARPS = PP_GEN_WARPS + 1 + 4;
+constexpr int PP_NR = PP_GEN_WARPS / PP_KB;         // row sets per k-block
+constexpr int PP_NA = 4 / PP_NR, PP_NB = 4 / PP_NR; // A and B rows per lane per chunk
+static_assert(PP_NR >= 1 && 4 % PP_NR == 0, "warps / k-blocks must divide the 4 row groups");
+static_assert(PP_KC % 16 == 0, "K = 16 per kind::f16 MMA");
+static_assert(PP_NS * PP_STAGE + 2048 + 64 * 16 <= 227 * 1024, "operand ring must leave room for hits");
 
-__device__ __forceinline__ void mbar_arrive1(uint64_t *bar) {
-    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
-}
-
-struct TileCoord {
-    int e, l, t_m, t_n;
+struct PairCoord {
+    int e, l, t_m, t_n;  // event (of this launch), z0 index, 128-row block of tx, 256-column block of ty
 };
 
-__device__ __forceinline__ TileCoord decode_tile(int t, int tpe, int nl, int tn) {
-    TileCoord c;
-    c.e = t / tpe;
-    const int r = t - c.e * tpe;
+__device__ __forceinline__ PairCoord decode_pair(int t, int ppe, int nl, int tn, int rank) {
+    PairCoord c;
+    c.e = t / ppe;
+    const int r = t - c.e * ppe;
     c.l = r % nl;
     const int tile = r / nl;
     c.t_n = tile % tn;
-    c.t_m = tile / tn;
+    c.t_m = 2 * (tile / tn) + rank;
     return c;
 }
 
+__device__ __forceinline__ void gen_bar_sync() {  // the 16 generating warps only
+    asm volatile("bar.sync 1, %0;" ::"n"(32 * PP_GEN_WARPS) : "memory");
+}
+
 template <int MODEL, bool ZREF>
-__global__ void __launch_bounds__(32 * P16_WARPS, 1) grid_tensor16p_kernel(GridArgs a, int n_items) {
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(32 * PP_WARPS, 1)
+    grid_tensor16pp_kernel(GridArgs a, int n_items) {
     extern __shared__ __align__(1024) uint8_t s_raw[];
-    __shared__ __align__(8) uint64_t s_full[P16_NS];
-    __shared__ __align__(8) uint64_t s_empty[P16_NS];
-    __shared__ __align__(8) uint64_t s_acc_full[2];
-    __shared__ __align__(8) uint64_t s_acc_empty[2];
+    __shared__ __align__(8) uint64_t s_full[PP_NS];     // even CTA: 2 x 16 generating warps arrive
+    __shared__ __align__(8) uint64_t s_empty[PP_NS];    // both CTAs: multicast MMA commit
+    __shared__ __align__(8) uint64_t s_acc_full[2];     // both CTAs: multicast commit at tile end
+    __shared__ __align__(8) uint64_t s_acc_empty[2];    // even CTA: 2 x 4 epilogue warps arrive
+    __shared__ __align__(8) uint64_t s_hbar;            // hit loads (TMA bulk copy)
     __shared__ uint32_t s_tmem;
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    const int tn = (a.n1 + TC_N - 1) / TC_N, tm = (a.n0 + TC_M - 1) / TC_M;
+    const uint32_t rank = cluster_rank();
+    const int tn = (a.n1 + TC_N - 1) / TC_N, pm = (a.n0 + 255) / 256;
     const int nl = (MODEL == kSlope3) ? a.n2 : 1;
-    const int tpe = tm * tn * nl;  // work items per event
-    const int t0 = (int)((long long)blockIdx.x * n_items / gridDim.x);
-    const int t1 = (int)((long long)(blockIdx.x + 1) * n_items / gridDim.x);
+    const int ppe = pm * tn * nl;  // pair work items per event
+    const int cl = blockIdx.x >> 1, ncl = gridDim.x >> 1;
+    // SLOPE2: a contiguous range of items per cluster (the event's hits stay in shared memory);
+    // SLOPE3: items dealt round-robin, so the clusters running at the same time write neighbouring
+    // z0 values of the same cells (z0 is the fastest output axis) and L2 merges their 4-byte stores
+    const bool rr = MODEL == kSlope3;
+    const int t0 = rr ? cl : (int)((long long)cl * n_items / ncl);
+    const int t1 = rr ? n_items : (int)((long long)(cl + 1) * n_items / ncl);
+    const int dt = rr ? ncl : 1;
+    float4 *s_hits = reinterpret_cast<float4 *>(s_raw + PP_NS * PP_STAGE);
 
-    if (warp == 0) {  // two accumulator buffers: 128 lanes x (256 + 256) fp32 columns
-        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&s_tmem)),
+    if (warp == 0) {  // two accumulator buffers of 128 lanes x 256 fp32 columns, in both CTAs
+        asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&s_tmem)),
                      "r"(2 * TC_N));
-        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
         tc_fence_before();
     }
     if (tid == 0) {
-        for (int i = 0; i < P16_NS; ++i) {
-            mbar_init(&s_full[i], P16_GEN_WARPS);
+        for (int i = 0; i < PP_NS; ++i) {
+            mbar_init(&s_full[i], 2 * PP_GEN_WARPS);
             mbar_init(&s_empty[i], 1);
         }
         for (int i = 0; i < 2; ++i) {
             mbar_init(&s_acc_full[i], 1);
-            mbar_init(&s_acc_empty[i], 4);
+            mbar_init(&s_acc_empty[i], 8);
         }
+        mbar_init(&s_hbar, 1);
         fence_mbar_init();
     }
     __syncthreads();
+    cluster_sync_all();  // the peer's barriers exist before any remote arrive
     tc_fence_after();
     const uint32_t tmem = s_tmem;
     const uint32_t stage_saddr = smem_u32(s_raw);
     constexpr bool EXACT_D = ZREF || MODEL == kSlope3;
 
-    if (warp < P16_GEN_WARPS) {
+    if (warp < PP_GEN_WARPS) {
         // ------------------------------------------------------------------ generating warps
-        const int kb = warp % P16_KB, rset = warp / P16_KB;
+        const int kb = warp % PP_KB, rset = warp / PP_KB;
         const float2 nk2 = make_float2(a.negK, a.negK);
-        const __half2 h2m6 = __float2half2_rn(0.015625f);  // 2^-6: h 2^15 -> h 2^9 (exact in range)
-        uint32_t cg = 0;                                   // chunk counter (ring position)
-        for (int t = t0; t < t1; ++t) {
-            const TileCoord c = decode_tile(t, tpe, nl, tn);
+        const __half2 h2m6 = __float2half2_rn(0.015625f);  // 2^-6: h 2^15 -> h 2^9
+        uint32_t cg = 0, loads = 0;                        // chunk counter, hit loads issued
+        int have_e = -1, have_w0 = -1;                     // hit window now in shared memory
+        const uint32_t full_addr0 = mapa_rank0(smem_u32(&s_full[0]));
+        for (int t = t0; t < t1; t += dt) {
+            const PairCoord c = decode_pair(t, ppe, nl, tn, (int)rank);
             const int start = a.offsets[c.e], n = a.offsets[c.e + 1] - start;
-            if (n <= 0) continue;
-            const float4 *hg = a.hits + start;
-            float p[P16_NA + P16_NB];
+            float p[PP_NA + PP_NB];
 #pragma unroll
-            for (int u = 0; u < P16_NA; ++u)
-                p[u] = __ldg(a.nodes0 + min(c.t_m * TC_M + lane + 32 * (u * P16_NR + rset), a.n0 - 1));
+            for (int u = 0; u < PP_NA; ++u)
+                p[u] = __ldg(a.nodes0 + min(c.t_m * 128 + lane + 32 * (u * PP_NR + rset), a.n0 - 1));
 #pragma unroll
-            for (int u = 0; u < P16_NB; ++u)
-                p[P16_NA + u] = __ldg(a.nodes1 + min(c.t_n * TC_N + lane + 32 * (u * P16_NR + rset), a.n1 - 1));
+            for (int u = 0; u < PP_NB; ++u)  // this CTA's half of the pair tile's 256 ty columns
+                p[PP_NA + u] =
+                    __ldg(a.nodes1 + min(c.t_n * TC_N + (int)rank * 128 + lane + 32 * (u * PP_NR + rset), a.n1 - 1));
             const float zref = (MODEL == kSlope3) ? __ldg(a.nodes2 + c.l) : a.z_ref;
-            for (int k0 = 0; k0 < n; k0 += P16_KC, ++cg) {
-                const int s = (int)(cg % P16_NS);
-                // hits of this warp's k-block as pairs (q, q+1); a missing hit gets a huge
-                // coordinate so its factor is exactly ex2(-inf) = 0
-                float2 hx[4], hy[4], hz[4], hzl[4];
-#pragma unroll
-                for (int q = 0; q < 8; ++q) {
-                    const int k = k0 + kb * 8 + q;
-                    const bool ok = k < n;
-                    const float4 hk = __ldg(hg + (ok ? k : 0));
-                    float zh = hk.z, zl = 0.f;
-                    if (EXACT_D) two_sum(hk.z, -zref, zh, zl);
-                    const float xv = ok ? hk.x : 1e30f, yv = ok ? hk.y : 1e30f;
-                    if (q & 1) {
-                        hx[q >> 1].y = xv; hy[q >> 1].y = yv; hz[q >> 1].y = zh; hzl[q >> 1].y = zl;
-                    } else {
-                        hx[q >> 1].x = xv; hy[q >> 1].x = yv; hz[q >> 1].x = zh; hzl[q >> 1].x = zl;
+            for (int w0 = 0; w0 < n; w0 += a.cap) {
+                const int wlen = min(a.cap, n - w0);
+                if (have_e != c.e || have_w0 != w0) {  // (re)load the window; uniform over the 16 warps
+                    gen_bar_sync();                     // nobody still reads the old window
+                    if (tid == 0) {
+                        fence_proxy_async();
+                        mbar_arrive_expect_tx(&s_hbar, (uint32_t)wlen * 16u);
+                        bulk_g2s(s_hits, a.hits + start + w0, (uint32_t)wlen * 16u, &s_hbar);
                     }
+                    mbar_wait(&s_hbar, loads & 1u);
+                    ++loads;
+                    have_e = c.e;
+                    have_w0 = w0;
                 }
-                if (cg >= P16_NS) mbar_wait(&s_empty[s], ((cg / P16_NS) - 1) & 1u);  // MMAs of cg-NS done
-                uint8_t *sb = s_raw + s * P16_STAGE;
+                const float4 *h = s_hits;
+                for (int k0 = 0; k0 < wlen; k0 += PP_KC, ++cg) {
+                    const int s = (int)(cg % PP_NS);
+                    float2 hx[4], hy[4], hz[4], hzl[4];
 #pragma unroll
-                for (int u = 0; u < P16_NA + P16_NB; ++u) {
-                    const bool isA = u < P16_NA;
-                    const float2 mp = make_float2(-p[u], -p[u]);
-                    uint32_t w15[4], wlo[4], w9[4];
-#pragma unroll
-                    for (int q = 0; q < 4; ++q) {
-                        const float2 cc = isA ? hx[q] : hy[q];
-                        const float2 sres =
-                            EXACT_D ? __ffma2_rn(mp, hzl[q], __ffma2_rn(mp, hz[q], cc)) : __ffma2_rn(mp, hz[q], cc);
-                        const float2 arg = __fmul2_rn(__fmul2_rn(sres, sres), nk2);
-                        const float2 v = make_float2(ex2_approx(arg.x), ex2_approx(arg.y));
-                        const float2 vs = __fmul2_rn(v, make_float2(0x1p15f, 0x1p15f));
-                        const __half2 hh = __floats2half2_rn(vs.x, vs.y);
-                        const float2 hf = __half22float2(hh);                                    // exact
-                        const float2 lo = __ffma2_rn(hf, make_float2(-0x1p-15f, -0x1p-15f), v);  // exact
-                        const float2 ls = __fmul2_rn(lo, make_float2(0x1p21f, 0x1p21f));
-                        const __half2 hl = __floats2half2_rn(ls.x, ls.y);
-                        const __half2 h9 = __hmul2(hh, h2m6);
-                        w15[q] = *reinterpret_cast<const uint32_t *>(&hh);
-                        wlo[q] = *reinterpret_cast<const uint32_t *>(&hl);
-                        w9[q] = *reinterpret_cast<const uint32_t *>(&h9);
+                    for (int q = 0; q < 8; ++q) {
+                        const int k = k0 + kb * 8 + q;
+                        const bool ok = k < wlen;
+                        const float4 hk = h[ok ? k : 0];
+                        float zh = hk.z, zl = 0.f;
+                        if (EXACT_D) two_sum(hk.z, -zref, zh, zl);
+                        const float xv = ok ? hk.x : 1e30f, yv = ok ? hk.y : 1e30f;
+                        if (q & 1) {
+                            hx[q >> 1].y = xv; hy[q >> 1].y = yv; hz[q >> 1].y = zh; hzl[q >> 1].y = zl;
+                        } else {
+                            hx[q >> 1].x = xv; hy[q >> 1].x = yv; hz[q >> 1].x = zh; hzl[q >> 1].x = zl;
+                        }
                     }
-                    // K-major no-swizzle canonical layout: k-block kb of 8 fp16, row r at 16 B
-                    const int r = lane + 32 * ((isA ? u : u - P16_NA) * P16_NR + rset);
-                    const int rows = isA ? TC_M : TC_N;
-                    const int part = isA ? P16_PART_A : P16_PART_B;
-                    uint8_t *d0 = sb + (isA ? 0 : 3 * P16_PART_A) + (size_t)(kb * rows + r) * 16;
-                    // A = [h 2^15 | h 2^9 | l 2^21],  B = [h 2^15 | l 2^21 | h 2^9]
-                    *reinterpret_cast<uint4 *>(d0) = make_uint4(w15[0], w15[1], w15[2], w15[3]);
-                    *reinterpret_cast<uint4 *>(d0 + part) =
-                        isA ? make_uint4(w9[0], w9[1], w9[2], w9[3]) : make_uint4(wlo[0], wlo[1], wlo[2], wlo[3]);
-                    *reinterpret_cast<uint4 *>(d0 + 2 * part) =
-                        isA ? make_uint4(wlo[0], wlo[1], wlo[2], wlo[3]) : make_uint4(w9[0], w9[1], w9[2], w9[3]);
+                    if (cg >= PP_NS) mbar_wait(&s_empty[s], ((cg / PP_NS) - 1) & 1u);  // MMAs of cg-NS done
+                    uint8_t *sb = s_raw + s * PP_STAGE;
+#pragma unroll
+                    for (int u = 0; u < PP_NA + PP_NB; ++u) {
+                        const bool isA = u < PP_NA;
+                        const float2 mp = make_float2(-p[u], -p[u]);
+                        uint32_t w15[4], wlo[4], w9[4];
+#pragma unroll
+                        for (int q = 0; q < 4; ++q) {
+                            const float2 cc = isA ? hx[q] : hy[q];
+                            const float2 sres = EXACT_D ? __ffma2_rn(mp, hzl[q], __ffma2_rn(mp, hz[q], cc))
+                                                        : __ffma2_rn(mp, hz[q], cc);
+                            const float2 arg = __fmul2_rn(__fmul2_rn(sres, sres), nk2);
+                            const float2 v = make_float2(ex2_approx(arg.x), ex2_approx(arg.y));
+                            const float2 vs = __fmul2_rn(v, make_float2(0x1p15f, 0x1p15f));
+                            const __half2 hh = __floats2half2_rn(vs.x, vs.y);
+                            const float2 hf = __half22float2(hh);                                    // exact
+                            const float2 lo = __ffma2_rn(hf, make_float2(-0x1p-15f, -0x1p-15f), v);  // exact
+                            const float2 ls = __fmul2_rn(lo, make_float2(0x1p21f, 0x1p21f));
+                            const __half2 hl = __floats2half2_rn(ls.x, ls.y);
+                            const __half2 h9 = __hmul2(hh, h2m6);
+                            w15[q] = *reinterpret_cast<const uint32_t *>(&hh);
+                            wlo[q] = *reinterpret_cast<const uint32_t *>(&hl);
+                            w9[q] = *reinterpret_cast<const uint32_t *>(&h9);
+                        }
+                        // K-major no-swizzle canonical layout: k-block kb of 8 fp16, row r at 16 B
+                        const int r = lane + 32 * ((isA ? u : u - PP_NA) * PP_NR + rset);
+                        uint8_t *d0 = sb + (isA ? 0 : 3 * PP_PART) + (size_t)(kb * 128 + r) * 16;
+                        // A = [h 2^15 | h 2^9 | l 2^21],  B = [h 2^15 | l 2^21 | h 2^9]
+                        *reinterpret_cast<uint4 *>(d0) = make_uint4(w15[0], w15[1], w15[2], w15[3]);
+                        *reinterpret_cast<uint4 *>(d0 + PP_PART) =
+                            isA ? make_uint4(w9[0], w9[1], w9[2], w9[3]) : make_uint4(wlo[0], wlo[1], wlo[2], wlo[3]);
+                        *reinterpret_cast<uint4 *>(d0 + 2 * PP_PART) =
+                            isA ? make_uint4(wlo[0], wlo[1], wlo[2], wlo[3]) : make_uint4(w9[0], w9[1], w9[2], w9[3]);
+                    }
+                    fence_proxy_async();  // this thread's generic-proxy stores -> visible to the tensor core
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive_remote(full_addr0 + (uint32_t)(s * sizeof(uint64_t)));
                 }
-                fence_proxy_async();  // this thread's generic-proxy stores -> visible to the tensor core
-                __syncwarp();
-                if (lane == 0) mbar_arrive1(&s_full[s]);
             }
         }
-    } else if (warp == P16_MMA_WARP) {
-        // ------------------------------------------------------------------ MMA issuer
-        if (lane == 0) {
+    } else if (warp == PP_MMA_WARP) {
+        // ------------------------------------------------------------------ MMA issuer (even CTA)
+        if (rank == 0 && lane == 0) {
             uint32_t cg = 0;
             int ti = 0;
-            for (int t = t0; t < t1; ++t, ++ti) {
-                const TileCoord c = decode_tile(t, tpe, nl, tn);
+            const uint32_t peer_acc_full = mapa_rank(smem_u32(&s_acc_full[0]), 1);
+            for (int t = t0; t < t1; t += dt, ++ti) {
+                const PairCoord c = decode_pair(t, ppe, nl, tn, 0);
                 const int n = a.offsets[c.e + 1] - a.offsets[c.e];
                 const int b = ti & 1;
-                if (ti >= 2) mbar_wait(&s_acc_empty[b], ((ti >> 1) - 1) & 1);  // epilogue of tile ti-2 done
+                if (ti >= 2) mbar_wait_cluster(&s_acc_empty[b], ((ti >> 1) - 1) & 1);  // both epilogues done
                 tc_fence_after();
                 const uint32_t acc = tmem + (uint32_t)(b * TC_N);
-                const int nck = n > 0 ? (n + P16_KC - 1) / P16_KC : 0;
+                int nck = 0;  // chunks of this tile: every window is cut into 64-hit chunks
+                for (int w0 = 0; w0 < n; w0 += a.cap) nck += (min(a.cap, n - w0) + PP_KC - 1) / PP_KC;
                 for (int ck = 0; ck < nck; ++ck, ++cg) {
-                    const int s = (int)(cg % P16_NS);
-                    mbar_wait(&s_full[s], (cg / P16_NS) & 1u);
+                    const int s = (int)(cg % PP_NS);
+                    mbar_wait_cluster(&s_full[s], (cg / PP_NS) & 1u);
                     tc_fence_after();
-                    const uint32_t A0 = stage_saddr + s * P16_STAGE, B0 = A0 + 3 * P16_PART_A;
+                    const uint32_t A0 = stage_saddr + s * PP_STAGE, B0 = A0 + 3 * PP_PART;
 #pragma unroll
-                    for (int j = 0; j < P16_KC / 16; ++j) {  // K = 16 fp16 per MMA = 2 k-blocks
-                        const uint32_t oa = j * 2 * (TC_M * 16), ob = j * 2 * (TC_N * 16);
+                    for (int j = 0; j < PP_KC / 16; ++j) {  // K = 16 fp16 per MMA = 2 k-blocks
+                        const uint32_t o = j * 2 * (128 * 16);
 #pragma unroll
                         for (int pp = 0; pp < 3; ++pp)
-                            tc_mma_f16(acc, umma_desc(A0 + pp * P16_PART_A + oa, TC_M * 16, 128),
-                                       umma_desc(B0 + pp * P16_PART_B + ob, TC_N * 16, 128),
-                                       (ck > 0 || j > 0 || pp > 0) ? 1u : 0u);
+                            tc2_mma_f16(acc, umma_desc(A0 + pp * PP_PART + o, 128 * 16, 128),
+                                        umma_desc(B0 + pp * PP_PART + o, 128 * 16, 128),
+                                        (ck > 0 || j > 0 || pp > 0) ? 1u : 0u);
                     }
-                    tc_commit(&s_empty[s]);
+                    tc2_commit_both(&s_empty[s]);
                 }
-                if (nck > 0)
-                    tc_commit(&s_acc_full[b]);  // arrives when every MMA of this tile is complete
-                else
-                    mbar_arrive1(&s_acc_full[b]);
+                if (nck > 0) {
+                    tc2_commit_both(&s_acc_full[b]);  // both CTAs: every MMA of this tile complete
+                } else {
+                    mbar_arrive(&s_acc_full[b]);
+                    mbar_arrive_remote(peer_acc_full + (uint32_t)(b * sizeof(uint64_t)));
+                }
             }
         }
         __syncwarp();
     } else {
         // ------------------------------------------------------------------ epilogue warps
         const int q = warp & 3;  // TMEM lane quarter this warp may access
+        const uint32_t acc_empty0 = mapa_rank0(smem_u32(&s_acc_empty[0]));
+        const int64_t cells = (int64_t)a.n0 * a.n1 * nl;
         int ti = 0;
-        for (int t = t0; t < t1; ++t, ++ti) {
-            const TileCoord c = decode_tile(t, tpe, nl, tn);
+        for (int t = t0; t < t1; t += dt, ++ti) {
+            const PairCoord c = decode_pair(t, ppe, nl, tn, (int)rank);
             const int n = a.offsets[c.e + 1] - a.offsets[c.e];
             const int b = ti & 1;
             mbar_wait(&s_acc_full[b], (ti >> 1) & 1);
             tc_fence_after();
-            const int i = c.t_m * TC_M + q * 32 + lane;
-            const int64_t cells = (int64_t)a.n0 * a.n1 * nl;
+            const int i = c.t_m * 128 + q * 32 + lane;
             float *out = a.R + (int64_t)(a.e_base + c.e) * cells + (int64_t)i * a.n1 * nl;
 #pragma unroll 1
             for (int cc = 0; cc < TC_N / 16; ++cc) {
@@ -284,13 +315,15 @@ __global__ void __launch_bounds__(32 * P16_WARPS, 1) grid_tensor16p_kernel(GridA
             }
             tc_fence_before();
             __syncwarp();
-            if (lane == 0) mbar_arrive1(&s_acc_empty[b]);
+            if (lane == 0) mbar_arrive_remote(acc_empty0 + (uint32_t)(b * sizeof(uint64_t)));
         }
     }
+    tc_fence_before();
     __syncthreads();
+    cluster_sync_all();  // both CTAs are done with TMEM before the pair deallocates
     if (warp == 0) {
         tc_fence_after();
-        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(2 * TC_N));
+        asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(2 * TC_N));
     }
 }
 
@@ -298,8 +331,8 @@ static int sm_count() {
     static int n = 0;
     if (n == 0) {
         int dev = 0, v = 0;
-        if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) ==
-                                                       cudaSuccess)
+        if (cudaGetDevice(&dev) == cudaSuccess &&
+            cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) == cudaSuccess)
             n = v;
         if (n <= 0) n = 148;
     }
@@ -307,23 +340,25 @@ static int sm_count() {
 }
 
 template <int MODEL, bool ZREF>
-static cudaError_t launch_p16(const GridArgs &a0, int n_events, cudaStream_t stream) {
-    auto kern = grid_tensor16p_kernel<MODEL, ZREF>;
-    const size_t smem = (size_t)P16_NS * P16_STAGE;
+static cudaError_t launch_pp(const GridArgs &a0, int n_events, cudaStream_t stream) {
+    auto kern = grid_tensor16pp_kernel<MODEL, ZREF>;
+    GridArgs a = a0;
+    const int cap_max = (227 * 1024 - PP_NS * PP_STAGE - 2048) / 16;
+    a.cap = std::max(PP_KC, (std::min(a.cap, cap_max) / PP_KC) * PP_KC);  // windows are whole chunks
+    const size_t smem = (size_t)PP_NS * PP_STAGE + (size_t)a.cap * sizeof(float4);
     cudaError_t err = ensure_dynamic_smem(kern, smem);
     if (err != cudaSuccess) return err;
     const long long per_event =
-        (long long)((a0.n0 + TC_M - 1) / TC_M) * ((a0.n1 + TC_N - 1) / TC_N) * (MODEL == kSlope3 ? a0.n2 : 1);
-    // work items are int32: split the batch into launches of at most 2^31-1 items
+        (long long)((a0.n0 + 255) / 256) * ((a0.n1 + TC_N - 1) / TC_N) * (MODEL == kSlope3 ? a0.n2 : 1);
     const int ev_per_launch = (int)std::max(1LL, std::min((long long)n_events, 0x7fffffffLL / per_event));
     for (int e0 = 0; e0 < n_events; e0 += ev_per_launch) {
-        GridArgs a = a0;
+        GridArgs b = a;
         const int ne = std::min(ev_per_launch, n_events - e0);
-        a.offsets = a0.offsets + e0;  // event e of this launch = e0 + e of the batch
-        a.e_base = e0;
+        b.offsets = a.offsets + e0;  // event e of this launch = e0 + e of the batch
+        b.e_base = e0;
         const int items = (int)(per_event * ne);
-        const int grid = std::min(items, sm_count());
-        kern<<<grid, 32 * P16_WARPS, smem, stream>>>(a, items);
+        const int clusters = std::max(1, std::min(items, sm_count() / 2));
+        kern<<<2 * clusters, 32 * PP_WARPS, smem, stream>>>(b, items);
         err = cudaGetLastError();
         if (err != cudaSuccess) return err;
     }
@@ -332,10 +367,10 @@ static cudaError_t launch_p16(const GridArgs &a0, int n_events, cudaStream_t str
 
 cudaError_t launch_grid_tensor16p(int model, const GridArgs &a, int n_events, cudaStream_t stream) {
     if (n_events == 0) return cudaSuccess;
-    if (model == kSlope3) return launch_p16<kSlope3, false>(a, n_events, stream);
+    if (model == kSlope3) return launch_pp<kSlope3, false>(a, n_events, stream);
     if (model != kSlope2) return cudaErrorInvalidValue;
-    return (a.z_ref == 0.f) ? launch_p16<kSlope2, false>(a, n_events, stream)
-                            : launch_p16<kSlope2, true>(a, n_events, stream);
+    return (a.z_ref == 0.f) ? launch_pp<kSlope2, false>(a, n_events, stream)
+                            : launch_pp<kSlope2, true>(a, n_events, stream);
 }
 
 }  // namespace retina

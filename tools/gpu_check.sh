@@ -10,7 +10,7 @@ SMALL="python bench.py --events-per-rank 296 --steps 1 --warmup 3 --no-cpu-basel
 $SMALL > gpurun_out/small.json 2>&1 && \
 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv $SMALL \
     > gpurun_out/ncu_launches.log 2>&1 && \
-ncu --set full --clock-control none --import-source on -k regex:"multistart|grid_tensor16" -s 4 -c 2 \
+ncu --set full --clock-control none --import-source on -k regex:"multistart|grid_tensor16pp" -s 4 -c 2 \
     -o gpurun_out/prof $SMALL > gpurun_out/ncu_full.log 2>&1
 echo "ncu rc=$?"
 cat gpurun_out/pytest_gpu.txt
