@@ -149,6 +149,8 @@ def make_seeds(cfg: Config, event_ids: Optional[Sequence[int]] = None,
     lo = np.asarray(cfg.box_lo, np.float64)
     hi = np.asarray(cfg.box_hi, np.float64)
     out = np.empty((len(list(event_ids)), n, cfg.P), np.float32)
+    if n == 0 or len(cfg.box_lo) == 0:  # grid-only configs (cfg1) draw no seeds
+        return np.zeros((out.shape[0], n, cfg.P), np.float32)
     for i, e in enumerate(event_ids):
         rng = _rng(cfg.seed, STREAM_SEEDS, int(e))
         u = rng.random((n, cfg.P))
