@@ -255,7 +255,9 @@ def _newton(ex, events, model, seeds, sigmas, etas, final_sigma, max_halvings, b
             out = out + (torch.empty((E, S), dtype=torch.int32, device=seeds.device),)
     th, R, g = out[:3]
     if ex:
-        ne = out[3]
+        ne = out[3] if len(out) > 3 and out[3] is not None else torch.empty((E, S), dtype=torch.int32,
+                                                                           device=seeds.device)
+        _dev(ne, torch.int32)
         _check("retina_multistart_newton_ex",
                lib().retina_multistart_newton_ex(ctypes.byref(events.c), model, S, _ptr(seeds), len(sigmas), sg, et,
                                                  float(final_sigma), int(max_halvings), lo, hi, _ptr(th), _ptr(R),
