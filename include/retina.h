@@ -190,7 +190,10 @@ int retina_multistart_newton(const retina_events *ev, int model, int32_t n_seeds
  * units of one response evaluation): evals_out, device int32 [n_events][n_seeds] or NULL,
  * receives per seed the response evaluations Algorithm 1 spent on it -- n_steps evaluations
  * with gradient and Hessian, every line-search trial, and the final evaluation
- * (= n_steps + sum_j trials_j + 1).  Identical results otherwise. */
+ * (= n_steps + sum_j trials_j + 1).  When grad_out is NULL and final_sigma equals
+ * sigmas[n_steps-1], R(theta^q) is the value the last step already computed at that point (its
+ * accepted trial, or its Hessian-mode evaluation when no trial was accepted): no final pass runs
+ * and the count has no final term.  Identical results otherwise. */
 int retina_multistart_newton_ex(const retina_events *ev, int model, int32_t n_seeds, const float *seeds,
                                 int32_t n_steps, const float *sigmas, const float *etas, float final_sigma,
                                 int32_t max_halvings, const float *box_lo, const float *box_hi,

@@ -421,7 +421,10 @@ static void tn_direction(int P, const double *g, const double *H, double eta, do
  * R_0 for the Armijo tests and |d^T H d| / (|d|^2 max|H|) for the CG curvature tests.
  * evals_out (nullable): per seed, the response evaluations Algorithm 1 spent on it, in the
  * paper's cost unit: q evaluations with gradient and Hessian, every line-search
- * trial, and the final evaluation, i.e. q + sum_j (trials of step j) + 1. */
+ * trial, and the final evaluation, i.e. q + sum_j (trials of step j) + 1 -- without the final one
+ * when it would repeat an evaluation already made (no gradient wanted, grad_out == NULL, and
+ * final_sigma == sigmas[q-1]: R(theta^q) at that sigma is the last accepted trial's value, or the
+ * last Hessian-mode evaluation's if no trial was accepted; Z36). */
 void ora_newton(int model, int n_events, const int32_t *offsets, const float *hits, double z_ref, int n_seeds,
                 const float *seeds, int n_steps, const double *sigmas, const double *etas, double final_sigma,
                 int max_halvings, const double *box_lo, const double *box_hi, double *theta_out,
@@ -468,7 +471,10 @@ void ora_newton(int model, int n_events, const int32_t *offsets, const float *hi
             if (grad_out)
                 for (int a = 0; a < P; ++a) grad_out[id * P + a] = g[a];
             if (margin_out) margin_out[id] = margin;
-            if (evals_out) evals_out[id] = evals + 1;
+            if (evals_out) {
+                const int reuse = !grad_out && n_steps > 0 && (float)sigmas[n_steps - 1] == (float)final_sigma;
+                evals_out[id] = evals + (reuse ? 0 : 1);
+            }
         }
     }
 }

@@ -359,6 +359,7 @@ int retina_multistart_newton_ex(const retina_events *ev, int model, int32_t n_se
     a.R_out = response_out;
     a.grad_out = grad_out;
     a.evals_out = evals_out;
+    a.reuse_final = (grad_out == nullptr && n_steps > 0 && a.negK[n_steps - 1] == a.final_negK) ? 1 : 0;
     a.cap = stage_cap(ev->max_event_hits, 4096);
     const cudaError_t err = retina::launch_newton(model, a, ev->n_events, (cudaStream_t)stream);
     if (err != cudaSuccess) return cuda_fail(err, "retina_multistart_newton");

@@ -51,7 +51,8 @@ struct NewtonArgs {
     int max_halvings;
     float lo[3], hi[3];
     float *theta_out, *R_out, *grad_out;
-    int32_t *evals_out;  // nullable: response evaluations per seed (q + line-search trials + 1)
+    int32_t *evals_out;  // nullable: response evaluations per seed (q + line-search trials [+ 1 final])
+    int reuse_final;     // no final pass: final sigma == last sigma and no gradient output
     int cap;
     int e_base;
 };

@@ -410,8 +410,10 @@ struct LineSearchSmem {
     float base[kNtThreads * S][P];  // theta before the step; the accepted trial overwrites it
     float dir[kNtThreads * S][P];
     float R0[kNtThreads * S], slope[kNtThreads * S];
-    int ntrial[kNtThreads * S];  // halvings tried (k of the accepted trial, else max_halvings)
-    int kmin[kNtThreads * S];    // smallest halving k of the current round that passed Armijo
+    // (k << 32) | bits(R_t) of the smallest halving k of the current round that passed Armijo:
+    // one 64-bit atomicMin keeps both the decision and that trial's response
+    // (all ones: no halving accepted yet); also gives the halvings tried and the final response
+    unsigned long long kmin[kNtThreads * S];
     int q[2][kNtThreads * S];
     int nq[2];
 };
@@ -430,7 +432,7 @@ template <int MODEL, int S, bool ZREF>
 __device__ __forceinline__ void nt_line_search_queue(HitStage &st, const NewtonArgs &a, float negK, float (&th)[S][3],
                                                      const float (&p)[S][3], const float (&R0)[S],
                                                      const float (&slope)[S], const bool (&active)[S], int (&nev)[S],
-                                                     LineSearchSmem<S, (MODEL == kSlope3) ? 3 : 2> &ls) {
+                                                     float (&rcur)[S], LineSearchSmem<S, (MODEL == kSlope3) ? 3 : 2> &ls) {
     constexpr int P = (MODEL == kSlope3) ? 3 : 2;
     constexpr int SQ = RETINA_NT_SQ < S ? RETINA_NT_SQ : S;
     const int tid = threadIdx.x, lane = tid & 31, wbase = (tid >> 5) * 32 * SQ;
@@ -448,8 +450,7 @@ __device__ __forceinline__ void nt_line_search_queue(HitStage &st, const NewtonA
         }
         ls.R0[slot] = R0[s];
         ls.slope[slot] = slope[s];
-        ls.ntrial[slot] = a.max_halvings;
-        ls.kmin[slot] = 0x7fffffff;
+        ls.kmin[slot] = ~0ull;
         ls.q[0][atomicAdd(&ls.nq[0], 1)] = slot;
     }
     __syncthreads();
@@ -487,18 +488,20 @@ __device__ __forceinline__ void nt_line_search_queue(HitStage &st, const NewtonA
                 if (slot[s] < 0) continue;
                 const int sl = slot[s];
                 const float alpha = __int_as_float((127 - kk[s]) << 23);
-                if (Rt[s] >= __fmaf_rn(1e-4f * alpha, ls.slope[sl], ls.R0[sl])) atomicMin(&ls.kmin[sl], kk[s]);
+                if (Rt[s] >= __fmaf_rn(1e-4f * alpha, ls.slope[sl], ls.R0[sl]))
+                    atomicMin(&ls.kmin[sl], ((unsigned long long)kk[s] << 32) | __float_as_uint(Rt[s]));
             }
         }
         __syncthreads();  // every trial of the round is decided
         for (int i = tid; i < n; i += kNtThreads) {
-            const int sl = ls.q[cur][i], km = ls.kmin[sl];
+            const int sl = ls.q[cur][i];
+            const unsigned long long kr = ls.kmin[sl];
+            const int km = (kr == ~0ull) ? 0x7fffffff : (int)(kr >> 32);
             if (km < k0 + nb) {  // accepted: recompute the trial point (same operations, same bits)
                 const float alpha = __int_as_float((127 - km) << 23);
 #pragma unroll
                 for (int d = 0; d < P; ++d)
                     ls.base[sl][d] = fminf(fmaxf(__fmaf_rn(alpha, ls.dir[sl][d], ls.base[sl][d]), a.lo[d]), a.hi[d]);
-                ls.ntrial[sl] = km;
             } else {
                 ls.q[cur ^ 1][atomicAdd(&ls.nq[cur ^ 1], 1)] = sl;
             }
@@ -515,7 +518,13 @@ __device__ __forceinline__ void nt_line_search_queue(HitStage &st, const NewtonA
         const int slot = s * kNtThreads + tid;
 #pragma unroll
         for (int i = 0; i < P; ++i) th[s][i] = ls.base[slot][i];
-        nev[s] += ls.ntrial[slot];
+        const unsigned long long kr = ls.kmin[slot];
+        if (kr == ~0ull) {
+            nev[s] += a.max_halvings;  // every halving tried, none accepted: theta and R(theta) stay
+        } else {
+            nev[s] += (int)(kr >> 32);
+            rcur[s] = __uint_as_float((uint32_t)kr);  // response at the accepted trial point
+        }
     }
 }
 
@@ -543,9 +552,13 @@ __global__ void __launch_bounds__(kNtThreads, RETINA_NT_MINB) newton_kernel(Newt
     __shared__ LineSearchSmem<S, P> ls;
     HessSums hs[S];
     float R[S], G[S][4];
-    int nev[S];  // response evaluations per seed (PAPER.md:200-201 cost unit)
+    int nev[S];     // response evaluations per seed (PAPER.md:200-201 cost unit)
+    float Rcur[S];  // R(theta) at the current step's sigma: the last evaluation at the current point
 #pragma unroll
-    for (int s = 0; s < S; ++s) nev[s] = a.n_steps + 1;  // q Hessian-mode passes + the final one
+    for (int s = 0; s < S; ++s) {
+        nev[s] = a.n_steps + (a.reuse_final ? 0 : 1);  // q Hessian-mode passes (+ the final one)
+        Rcur[s] = 0.f;
+    }
     for (int j = 0; j < a.n_steps; ++j) {
         const float c = a.c2[j], negK = a.negK[j];
         if constexpr (RETINA_NT_X2 && S % 2 == 0)
@@ -560,6 +573,7 @@ __global__ void __launch_bounds__(kNtThreads, RETINA_NT_MINB) newton_kernel(Newt
             const float c2 = __fmul_rn(c, c);
             float g[3], H[3][3];
             R0[s] = hs[s].s1[0];
+            Rcur[s] = R0[s];
             const float *s1 = hs[s].s1, *sd = hs[s].sd, *sd2 = hs[s].sd2;
             g[0] = __fmul_rn(c, sd[1]);
             g[1] = __fmul_rn(c, sd[2]);
@@ -612,6 +626,7 @@ __global__ void __launch_bounds__(kNtThreads, RETINA_NT_MINB) newton_kernel(Newt
 #pragma unroll
             for (int s = 0; s < S; ++s) {
                 if (active[s] && Rt[s] >= __fmaf_rn(1e-4f * alpha, slope[s], R0[s])) {
+                    Rcur[s] = Rt[s];
 #pragma unroll
                     for (int i = 0; i < 3; ++i) th[s][i] = tt[s][i];
                     active[s] = false;
@@ -619,7 +634,7 @@ __global__ void __launch_bounds__(kNtThreads, RETINA_NT_MINB) newton_kernel(Newt
             }
         }
         if (st.resident && a.max_halvings > 0)
-            nt_line_search_queue<MODEL, S, ZREF>(st, a, negK, th, p, R0, slope, active, nev, ls);
+            nt_line_search_queue<MODEL, S, ZREF>(st, a, negK, th, p, R0, slope, active, nev, Rcur, ls);
     }
     float g[S][3];
     if (a.grad_out) {
@@ -635,6 +650,12 @@ __global__ void __launch_bounds__(kNtThreads, RETINA_NT_MINB) newton_kernel(Newt
                           ? -__fmul_rn(a.final_c2, __fmaf_rn(th[s][0], G[s][2], __fmul_rn(th[s][1], G[s][3])))
                           : 0.f;
         }
+    } else if (a.reuse_final) {
+        // final sigma == last step's sigma and no gradient wanted: R(theta^q) is the response of
+        // the last step's accepted trial (same point, same sigma, same arithmetic as a final
+        // pass) or, with no trial accepted, the last Hessian pass's R at the unchanged theta
+#pragma unroll
+        for (int s = 0; s < S; ++s) R[s] = Rcur[s];
     } else {
         if constexpr (RETINA_NT_X2 && S % 2 == 0)
             nt_pass_r_x2<MODEL, S, ZREF, false>(st, th, a.final_negK, a.z_ref, R, G);

@@ -569,6 +569,14 @@ def test_P17_newton_evaluation_count():
     *_, ne = ora.newton(cfg.model, [0, 0], np.zeros((0, 4), np.float32), seeds, sig, eta, cfg.sigma, 8,
                         cfg.box_lo, cfg.box_hi, want_evals=True)
     assert np.all(ne == 2 * 2 + 1)
+    # no gradient wanted and the final sigma is the last step's: the final evaluation repeats the
+    # last step's value at that point and is not counted again (Z36); a different final sigma is
+    th, R, _, ne = ora.newton(cfg.model, [0, 0], np.zeros((0, 4), np.float32), seeds, sig, eta, cfg.sigma, 8,
+                              cfg.box_lo, cfg.box_hi, want_grad=False, want_evals=True)
+    assert np.all(ne == 2 * 2)
+    *_, ne = ora.newton(cfg.model, [0, 0], np.zeros((0, 4), np.float32), seeds, sig, eta, 2 * cfg.sigma, 8,
+                        cfg.box_lo, cfg.box_hi, want_grad=False, want_evals=True)
+    assert np.all(ne == 2 * 2 + 1)
     # seed on the box edge with the (fallback) ascent direction pointing out of the box: every
     # clamped trial equals the start, Armijo fails at every halving -> q (M + 1) + q + 1
     d = 300.0

@@ -589,6 +589,32 @@ def test_newton_line_search_queue_deterministic():
     assert int((ne > 2 * len(sig) + 1).sum()) > 0  # some seeds needed halvings (queue path)
 
 
+def test_newton_final_pass_reuse():
+    """With no gradient wanted and the final sigma equal to the last step's, R(theta^q) comes from
+    the last step's own evaluation at theta^q (its accepted trial, else its Hessian-mode pass):
+    same trajectory bit for bit, one evaluation fewer per seed, R within T1 of a final pass (and
+    bitwise equal to it wherever the value came from an accepted trial)."""
+    cfg = C.CFG3
+    b = G.make_batch(cfg, [3, 4])
+    seeds = dev(G.make_seeds(cfg, [3, 4], n_seeds=2048))
+    sig, eta, fsig, mh = C.newton_schedule(cfg)
+    assert np.float32(sig[-1]) == np.float32(fsig)
+    t1, r1, _, n1 = R.retina_multistart_newton_ex(events_of(b), cfg.model, seeds, sig, eta, fsig, mh, cfg.box_lo,
+                                                  cfg.box_hi, want_grad=True)
+    t0, r0, g0, n0 = R.retina_multistart_newton_ex(events_of(b), cfg.model, seeds, sig, eta, fsig, mh, cfg.box_lo,
+                                                   cfg.box_hi, want_grad=False)
+    torch.cuda.synchronize()
+    assert g0 is None and torch.equal(t0, t1) and torch.equal(n0, n1 - 1)
+    a, c = r0.cpu().numpy().astype(np.float64), r1.cpu().numpy().astype(np.float64)
+    assert np.all(np.abs(a - c) <= 1e-5 * np.maximum(c, 1e-6))
+    assert (a == c).mean() >= 0.5
+    th = t0.cpu().numpy()
+    for e in range(2):
+        for s in range(0, 2048, 211):
+            r, _, _ = ora.point(cfg.model, b.event_hits(e), th[e, s].astype(np.float64), fsig)
+            assert PU.t1_response(float(a[e, s]), r)[0]
+
+
 def test_newton_identities():
     cfg = C.CFG2
     b = G.make_batch(cfg, [0])
