@@ -53,6 +53,9 @@ def args_():
     ap.add_argument("--config", default="cfg3")
     ap.add_argument("--events-per-rank", type=int, default=None)
     ap.add_argument("--chunk-events", type=int, default=256)
+    ap.add_argument("--dense", action="store_true",
+                    help="Z12 'dense' variant: every downstream plane hit (no acceptance cut), ~4,100 hits/event "
+                         "for cfg3 as the config text states")
     ap.add_argument("--overlap-peaks", action="store_true",
                     help="peak scan of grid chunk c on a second stream while chunk c+1 is computed")
     ap.add_argument("--e2e-steps", type=int, default=None)
@@ -158,7 +161,7 @@ def run_reference(a):
     # torchrun exports OMP_NUM_THREADS=1 to every rank; rank 0 alone runs the oracle here, on all
     # the host's cores (read by OpenMP when the oracle library is first loaded, just below)
     os.environ["OMP_NUM_THREADS"] = str(len(os.sched_getaffinity(0)))
-    cfg = C.get_config(a.config)
+    cfg = C.get_config(a.config, dense=True) if a.dense else C.get_config(a.config)
     steps = []
     for _ in range(a.warmup + a.steps):
         steps.append(oracle_sample(cfg, a.cpu_sample_events))
@@ -192,7 +195,7 @@ def main():
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     RT.lib()  # fail loudly if the native library is missing
-    cfg = C.get_config(a.config)
+    cfg = C.get_config(a.config, dense=True) if a.dense else C.get_config(a.config)
     E = a.events_per_rank or cfg.n_events
     ev_ids = range(rank * E, (rank + 1) * E)  # weak scaling: distinct events per rank
     t0 = time.perf_counter()
@@ -381,7 +384,8 @@ def main():
         "steps": a.steps, "warmup": a.warmup, "ms_per_step": ms_step, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
         "events_per_s": E * world / (ms_step * 1e-3),
-        "config": {"workload": f"{cfg.name}: BASELINE.json configs[{cfg.name[-1]}], {E} events per GPU "
+        "config": {"workload": f"{cfg.name}{' dense (Z12: no acceptance cut)' if a.dense else ''}: "
+                               f"BASELINE.json configs[{cfg.name[-1]}], {E} events per GPU "
                                f"(ids rank*{E}..), {'x'.join(str(x[2]) for x in cfg.axes)} "
                                f"{C.MODEL_NAME[cfg.model].upper()} grid + {'x'.join(['3'] * cfg.P)} peaks "
                                f"(R0={cfg.peak_threshold}) + sub-cell estimates, "

@@ -296,8 +296,10 @@ __device__ __forceinline__ void ms_gradient(const float (&th)[S][3], const float
     }
 }
 
-template <int MODEL, int S, bool ZREF>
-__global__ void __launch_bounds__(kMsThreads, (MODEL == kSlope3) ? RETINA_MS3_MINB : RETINA_MS_MINB)
+// T threads per CTA (128 by default; 256 / 512 when an event's hits are so many that shared
+// memory would otherwise cut the CTAs per SM below the 6 x 4 warps the register budget allows)
+template <int MODEL, int S, bool ZREF, int T>
+__global__ void __launch_bounds__(T, ((MODEL == kSlope3) ? RETINA_MS3_MINB : RETINA_MS_MINB) * kMsThreads / T)
 multistart_kernel(MultistartArgs a) {
     extern __shared__ __align__(16) float4 s_hits[];
     __shared__ __align__(8) uint64_t s_bar[2];
@@ -312,7 +314,7 @@ multistart_kernel(MultistartArgs a) {
     float th[S][3];
 #pragma unroll
     for (int s = 0; s < S; ++s) {
-        sid[s] = blockIdx.x * (kMsThreads * S) + s * kMsThreads + threadIdx.x;
+        sid[s] = blockIdx.x * (T * S) + s * T + threadIdx.x;
         const int64_t src = ((int64_t)e * a.n_seeds + min(sid[s], a.n_seeds - 1)) * P;
 #pragma unroll
         for (int i = 0; i < 3; ++i) th[s][i] = (i < P) ? __ldg(a.seeds + src + i) : 0.f;
@@ -348,26 +350,37 @@ multistart_kernel(MultistartArgs a) {
     }
 }
 
-template <int MODEL, bool ZREF>
-static cudaError_t launch_ms(const MultistartArgs &a0, int n_events, cudaStream_t stream) {
 #ifndef RETINA_MS_SEEDS
 #define RETINA_MS_SEEDS 8
 #endif
+template <int MODEL, bool ZREF, int T>
+static cudaError_t launch_ms_t(const MultistartArgs &a0, int n_events, cudaStream_t stream) {
     constexpr int S = (MODEL == kSlope3) ? RETINA_MS3_SEEDS : RETINA_MS_SEEDS;
-    auto kern = multistart_kernel<MODEL, S, ZREF>;
+    auto kern = multistart_kernel<MODEL, S, ZREF, T>;
     const size_t smem = (size_t)a0.cap * sizeof(float4);
     cudaError_t err = ensure_dynamic_smem(kern, smem);
     if (err != cudaSuccess) return err;
-    const int blocks = (a0.n_seeds + kMsThreads * S - 1) / (kMsThreads * S);
+    const int blocks = (a0.n_seeds + T * S - 1) / (T * S);
     for (int e0 = 0; e0 < n_events; e0 += 65535) {
         MultistartArgs a = a0;
         a.e_base = e0;
         const int ne = min(65535, n_events - e0);
-        kern<<<dim3(blocks, ne), kMsThreads, smem, stream>>>(a);
+        kern<<<dim3(blocks, ne), T, smem, stream>>>(a);
         err = cudaGetLastError();
         if (err != cudaSuccess) return err;
     }
     return cudaSuccess;
+}
+
+template <int MODEL, bool ZREF>
+static cudaError_t launch_ms(const MultistartArgs &a, int n_events, cudaStream_t stream) {
+    // resident 128-thread CTAs the hit stage allows per SM (227 KB of shared memory)
+    const size_t per_cta = (size_t)a.cap * sizeof(float4) + 1024;
+    const int fit = (int)((227 * 1024) / per_cta);
+    const int want = (MODEL == kSlope3) ? RETINA_MS3_MINB : RETINA_MS_MINB;
+    if (fit >= want || MODEL == kLine2D) return launch_ms_t<MODEL, ZREF, kMsThreads>(a, n_events, stream);
+    if (2 * fit >= want) return launch_ms_t<MODEL, ZREF, 2 * kMsThreads>(a, n_events, stream);
+    return launch_ms_t<MODEL, ZREF, 4 * kMsThreads>(a, n_events, stream);
 }
 
 cudaError_t launch_multistart(int model, const MultistartArgs &a, int n_events, cudaStream_t stream) {
