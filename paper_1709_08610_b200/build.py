@@ -32,19 +32,37 @@ def stale() -> bool:
 
 
 def build(force: bool = False, verbose: bool = False, out: str = LIB, defines=()) -> str:
-    """Compile every csrc/*.cu into one shared library (`defines` only for experiments)."""
+    """Compile every csrc/*.cu (one nvcc process per file, in parallel) and link them into one
+    shared library (`defines` only for experiments)."""
     if out == LIB and not defines and not force and not stale():
         return LIB
-    cmd = [NVCC, *ARCH, *FLAGS, *[f"-D{d}" for d in defines], "-shared", "-o", out, *sources()]
-    res = subprocess.run(cmd, capture_output=True, text=True)
-    if res.returncode != 0:
-        sys.stderr.write(res.stdout + res.stderr)
-        raise RuntimeError("nvcc failed building libretina.so")
+    import concurrent.futures
+    import tempfile
+    dflags = [f"-D{d}" for d in defines]
+    with tempfile.TemporaryDirectory(prefix="retina_build_") as tmp:
+        objs = [os.path.join(tmp, os.path.basename(src) + ".o") for src in sources()]
+
+        def compile_one(src_obj):
+            src, obj = src_obj
+            return subprocess.run([NVCC, *ARCH, *FLAGS, *dflags, "-c", "-o", obj, src], capture_output=True,
+                                  text=True)
+
+        with concurrent.futures.ThreadPoolExecutor(max_workers=min(8, len(objs))) as pool:
+            results = list(pool.map(compile_one, zip(sources(), objs)))
+        log = "".join(r.stderr for r in results)
+        if any(r.returncode != 0 for r in results):
+            sys.stderr.write("".join(r.stdout + r.stderr for r in results if r.returncode != 0))
+            raise RuntimeError("nvcc failed building libretina.so")
+        res = subprocess.run([NVCC, *ARCH, "-shared", "-Xcompiler", "-fPIC", "-o", out, *objs], capture_output=True,
+                             text=True)
+        if res.returncode != 0:
+            sys.stderr.write(res.stdout + res.stderr)
+            raise RuntimeError("nvcc failed linking libretina.so")
     if out == LIB:
         with open(os.path.join(PKG, "ptxas.log"), "w") as f:
-            f.write(res.stderr)
+            f.write(log)
     if verbose:
-        sys.stderr.write(res.stderr)
+        sys.stderr.write(log)
     return out
 
 
