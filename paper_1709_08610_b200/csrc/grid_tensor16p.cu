@@ -80,7 +80,8 @@ template <int MODEL, bool ZREF>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(32 * PP_WARPS, 1)
     grid_tensor16pp_kernel(GridArgs a, int n_items) {
     extern __shared__ __align__(1024) uint8_t s_raw[];
-    __shared__ __align__(8) uint64_t s_full[PP_NS];     // even CTA: 2 x 16 generating warps arrive
+    __shared__ __align__(8) uint64_t s_full[PP_NS];     // even CTA: its 16 generating warps + the odd CTA's relay
+    __shared__ __align__(8) uint64_t s_pfull[PP_NS];    // odd CTA: its 16 generating warps (relayed once)
     __shared__ __align__(8) uint64_t s_empty[PP_NS];    // both CTAs: multicast MMA commit
     __shared__ __align__(8) uint64_t s_acc_full[2];     // both CTAs: multicast commit at tile end
     __shared__ __align__(8) uint64_t s_acc_empty[2];    // even CTA: 2 x 4 epilogue warps arrive
@@ -110,7 +111,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(32 * PP_WARPS, 1)
     }
     if (tid == 0) {
         for (int i = 0; i < PP_NS; ++i) {
-            mbar_init(&s_full[i], 2 * PP_GEN_WARPS);
+            mbar_init(&s_full[i], PP_GEN_WARPS + 1);
+            mbar_init(&s_pfull[i], PP_GEN_WARPS);
             mbar_init(&s_empty[i], 1);
         }
         for (int i = 0; i < 2; ++i) {
@@ -134,7 +136,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(32 * PP_WARPS, 1)
         const __half2 h2m6 = __float2half2_rn(0.015625f);  // 2^-6: h 2^15 -> h 2^9
         uint32_t cg = 0, loads = 0;                        // chunk counter, hit loads issued
         int have_e = -1, have_w0 = -1;                     // hit window now in shared memory
-        const uint32_t full_addr0 = mapa_rank0(smem_u32(&s_full[0]));
+        // each warp arrives on a barrier of its own CTA (CTA-scope release: cheap); the odd CTA's
+        // arrivals are relayed to the even CTA by one cluster-scope release per chunk (MMA warp)
+        uint64_t *arrive_bar = (rank == 0) ? s_full : s_pfull;
         for (int t = t0; t < t1; t += dt) {
             const PairCoord c = decode_pair(t, ppe, nl, tn, (int)rank);
             const int start = a.offsets[c.e], n = a.offsets[c.e + 1] - start;
@@ -216,12 +220,30 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(32 * PP_WARPS, 1)
                     }
                     fence_proxy_async();  // this thread's generic-proxy stores -> visible to the tensor core
                     __syncwarp();
-                    if (lane == 0) mbar_arrive_remote(full_addr0 + (uint32_t)(s * sizeof(uint64_t)));
+                    if (lane == 0) mbar_arrive(&arrive_bar[s]);
                 }
             }
         }
     } else if (warp == PP_MMA_WARP) {
         // ------------------------------------------------------------------ MMA issuer (even CTA)
+        if (rank == 1 && lane == 0) {
+            // relay: once all 16 local warps have filled stage s, one release.cluster arrive on the
+            // even CTA's full[s] publishes them (their stores precede their local arrivals, which
+            // this thread acquires) -- one GPU-scope fence per chunk instead of sixteen
+            const uint32_t full_addr0 = mapa_rank0(smem_u32(&s_full[0]));
+            uint32_t cg = 0;
+            for (int t = t0; t < t1; t += dt) {
+                const PairCoord c = decode_pair(t, ppe, nl, tn, 1);
+                const int n = a.offsets[c.e + 1] - a.offsets[c.e];
+                int nck = 0;
+                for (int w0 = 0; w0 < n; w0 += a.cap) nck += (min(a.cap, n - w0) + PP_KC - 1) / PP_KC;
+                for (int ck = 0; ck < nck; ++ck, ++cg) {
+                    const int s = (int)(cg % PP_NS);
+                    mbar_wait(&s_pfull[s], (cg / PP_NS) & 1u);
+                    mbar_arrive_remote(full_addr0 + (uint32_t)(s * sizeof(uint64_t)));
+                }
+            }
+        }
         if (rank == 0 && lane == 0) {
             uint32_t cg = 0;
             int ti = 0;
