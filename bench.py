@@ -363,8 +363,9 @@ def main():
                  "achieved": pairs_s / 1e9, "peak": peak / 1e9, "unit": "Gpair/s (1 MUFU.EX2 per pair)",
                  "frac": pairs_s / peak,
                  "peak_basis": f"{N_SM} SMs x {MUFU_PER_SM_CLK} MUFU.EX2/clk/SM (measured 15.95) x sm_max_mhz "
-                               f"{fmax / 1e6:.0f} (MEASURED_PEAKS.json); FMA pipe gives the same 16 pairs/clk/SM "
-                               "at 8 lane-ops per pair",
+                               f"{fmax / 1e6:.0f} (MEASURED_PEAKS.json); the loop's 7 FMA-pipe lane-ops per pair make "
+                               "the FMA pipe a co-limit (~14 pairs/clk/SM at the 97 lanes/clk measured for "
+                               "FFMA2 with register operands, tools/pipe_microbench.cu)",
                  "frac_at_measured_clock": (pairs_s / (N_SM * MUFU_PER_SM_CLK * clk["sm_mhz"] * 1e6)
                                             if clk.get("sm_mhz") else None)}
         r.update({"launch_ms": avg_ms, "pairs_per_launch": per_launch, "pairs_per_s": pairs_s,
