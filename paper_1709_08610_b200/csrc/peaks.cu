@@ -99,9 +99,17 @@ __device__ __forceinline__ int scan_range(const PeakArgs &a, const float *g, int
                 vv[u + 2] = q.z;
                 vv[u + 3] = q.w;
             }
+            // neighbours along the fastest axis that are the thread's own cells are compared first,
+            // from registers: a candidate on a slope along that axis is rejected with no load
+            const int nlast = (P == 3) ? a.n2 : a.n1;
 #pragma unroll
-            for (int v = 0; v < kPeakV; ++v)
-                if (vv[v] >= a.threshold && beats_neighbours<P>(g, c0 + v, vv[v], a.n0, a.n1, a.n2)) mask |= 1u << v;
+            for (int v = 0; v < kPeakV; ++v) {
+                if (!(vv[v] >= a.threshold)) continue;
+                const int pos = (c0 + v) % nlast;  // position along the fastest axis (rows may wrap)
+                if (v > 0 && pos > 0 && !(vv[v] > vv[v - 1])) continue;
+                if (v + 1 < kPeakV && pos + 1 < nlast && !(vv[v] > vv[v + 1])) continue;
+                if (beats_neighbours<P>(g, c0 + v, vv[v], a.n0, a.n1, a.n2)) mask |= 1u << v;
+            }
         } else {
 #pragma unroll
             for (int v = 0; v < kPeakV; ++v) {
