@@ -204,6 +204,8 @@ def main():
     gen_s = time.perf_counter() - t0
     spec = make_spec(cfg)
     if a.update == "newton":
+        if cfg.model == C.LINE2D or not cfg.n_seeds:
+            raise SystemExit(f"--update newton needs a SLOPE2/SLOPE3 config with seeds ({cfg.name} has none)")
         spec.newton = C.newton_schedule(cfg)
     pipe = RetinaPipeline(spec, E, chunk_events=a.chunk_events, overlap_peaks=a.overlap_peaks)
     stream = torch.cuda.current_stream()
