@@ -52,7 +52,8 @@ def args_():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="cfg3")
     ap.add_argument("--events-per-rank", type=int, default=None)
-    ap.add_argument("--chunk-events", type=int, default=256)
+    ap.add_argument("--chunk-events", type=int, default=1024)
+    ap.add_argument("--grid-buffer-gb", type=float, default=5.0, help="device memory for the per-chunk response grids")
     ap.add_argument("--dense", action="store_true",
                     help="Z12 'dense' variant: every downstream plane hit (no acceptance cut), ~4,100 hits/event "
                          "for cfg3 as the config text states")
@@ -207,7 +208,8 @@ def main():
         if cfg.model == C.LINE2D or not cfg.n_seeds:
             raise SystemExit(f"--update newton needs a SLOPE2/SLOPE3 config with seeds ({cfg.name} has none)")
         spec.newton = C.newton_schedule(cfg)
-    pipe = RetinaPipeline(spec, E, chunk_events=a.chunk_events, overlap_peaks=a.overlap_peaks)
+    pipe = RetinaPipeline(spec, E, chunk_events=a.chunk_events, overlap_peaks=a.overlap_peaks,
+                          grid_bytes_budget=a.grid_buffer_gb * 1e9)
     stream = torch.cuda.current_stream()
     dbatch = upload(batch.offsets, batch.hits, seeds)
     if a.update == "newton":  # the pairs count comes from the kernel's per-seed evaluation counts
