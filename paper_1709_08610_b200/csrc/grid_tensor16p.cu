@@ -349,16 +349,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(32 * PP_WARPS, 1)
     }
 }
 
-static int sm_count() {
-    static int n = 0;
-    if (n == 0) {
-        int dev = 0, v = 0;
-        if (cudaGetDevice(&dev) == cudaSuccess &&
-            cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) == cudaSuccess)
-            n = v;
-        if (n <= 0) n = 148;
-    }
-    return n;
+static int sm_count() {  // of the current device (a cheap attribute query, legal during graph capture)
+    int dev = 0, v = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) !=
+                                                  cudaSuccess || v <= 0)
+        return 148;
+    return v;
 }
 
 template <int MODEL, bool ZREF>
