@@ -10,9 +10,11 @@
 //   2. bitonic sort of the keys in shared memory; exact R ties fall back to the theta
 //      lexicographic comparison (loaded from global) and then to the seed index, so the
 //      order is total and matches the oracle's comparator;
-//   3. warp 0 scans the sorted list; each candidate is tested against 32 leaders per step
-//      (ballot -> first match).  Leader records (size << 32 | seed) overwrite key slots that
-//      have already been consumed (leader l is founded by an item at position >= l).
+//   3. the greedy scan in rounds of 32 candidates: all 16 warps match the round's candidates
+//      against the leaders founded before the round (smallest index per candidate), then warp 0
+//      settles the round in order against the leaders founded within it.  Leader records
+//      (size << 32 | seed) overwrite key slots that have already been consumed (leader l is
+//      founded by an item at position >= l).
 #include "common.cuh"
 #include "kernels.cuh"
 
@@ -56,12 +58,15 @@ __global__ void __launch_bounds__(kMergeThreads) merge_kernel(MergeArgs a) {
     __shared__ int s_warp[kMergeThreads / 32];
     __shared__ float s_lt[kLeaderCache * 3];
     __shared__ int s_m;
+    __shared__ int s_csid[32], s_cmin[32];  // the round's candidates: seed, smallest matching old leader
+    __shared__ float s_ct[32 * 3];           // the round's candidates: theta
 
     const int e = a.e_base + blockIdx.x;
     const int P = a.P, n = a.n_seeds;
     const float *th = a.theta + (int64_t)e * n * P;
     const float *rr = a.R + (int64_t)e * n;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const double r0 = a.radius[0], r1 = a.radius[1], r2 = a.radius[2];
 
     // 1. ordered compaction of R >= threshold
     int total = 0;
@@ -109,20 +114,33 @@ __global__ void __launch_bounds__(kMergeThreads) merge_kernel(MergeArgs a) {
         }
     }
 
-    // 3. greedy leader clustering by warp 0
-    if (warp == 0) {
-        const double r0 = a.radius[0], r1 = a.radius[1], r2 = a.radius[2];
+    // 3. greedy leader clustering, exactly the sequential rule, in rounds of 32 candidates (sorted
+    //    order): (a) every warp compares the round's candidates (one per lane) with a strided share
+    //    of the leaders that existed when the round began, and the smallest matching leader index
+    //    per candidate is reduced in shared memory; (b) warp 0 then walks the round in order: a
+    //    candidate with such a match joins it (an older leader is always the earliest), otherwise
+    //    it is compared with the leaders founded earlier in this round (one per lane), joins the
+    //    first, or founds a new leader.  Leader records overwrite key slots <= the current
+    //    candidate, whose keys the round already copied.
+    {
         int L = 0;
-        for (int q = 0; q < m; ++q) {
-            const uint64_t key = s_key[q];
-            const int sidx = (int)(uint32_t)key;
-            const float t0 = __ldg(th + (int64_t)sidx * P), t1 = __ldg(th + (int64_t)sidx * P + 1);
-            const float t2 = (P == 3) ? __ldg(th + (int64_t)sidx * P + 2) : 0.f;
-            int found = -1;
-            for (int b = 0; b < L && found < 0; b += 32) {
-                const int l = b + lane;
-                bool in = false;
-                if (l < L) {
+        for (int q0 = 0; q0 < m; q0 += 32) {
+            const int nb = min(32, m - q0);
+            if (warp == 0) {
+                if (lane < nb) {
+                    const int sidx = (int)(uint32_t)s_key[q0 + lane];
+                    s_csid[lane] = sidx;
+                    s_ct[lane * 3] = __ldg(th + (int64_t)sidx * P);
+                    s_ct[lane * 3 + 1] = __ldg(th + (int64_t)sidx * P + 1);
+                    s_ct[lane * 3 + 2] = (P == 3) ? __ldg(th + (int64_t)sidx * P + 2) : 0.f;
+                }
+                s_cmin[lane] = 0x7fffffff;
+            }
+            __syncthreads();
+            const int L0 = L;  // leaders founded before this round (uniform)
+            if (lane < nb && L0 > 0) {
+                const double t0 = s_ct[lane * 3], t1 = s_ct[lane * 3 + 1], t2 = s_ct[lane * 3 + 2];
+                for (int l = warp; l < L0; l += kMergeThreads / 32) {
                     float l0, l1, l2 = 0.f;
                     if (l < kLeaderCache) {
                         l0 = s_lt[l * 3];
@@ -134,29 +152,62 @@ __global__ void __launch_bounds__(kMergeThreads) merge_kernel(MergeArgs a) {
                         l1 = __ldg(th + (int64_t)ls * P + 1);
                         if (P == 3) l2 = __ldg(th + (int64_t)ls * P + 2);
                     }
-                    in = fabs((double)t0 - (double)l0) <= r0 && fabs((double)t1 - (double)l1) <= r1 &&
-                         (P != 3 || fabs((double)t2 - (double)l2) <= r2);
-                }
-                const unsigned bal = __ballot_sync(0xffffffffu, in);
-                if (bal) found = b + __ffs(bal) - 1;
-            }
-            __syncwarp();
-            if (lane == 0) {
-                if (found >= 0) {
-                    s_key[found] += (1ull << 32);
-                } else {
-                    s_key[L] = (1ull << 32) | (uint32_t)sidx;
-                    if (L < kLeaderCache) {
-                        s_lt[L * 3] = t0;
-                        s_lt[L * 3 + 1] = t1;
-                        s_lt[L * 3 + 2] = t2;
+                    if (fabs(t0 - (double)l0) <= r0 && fabs(t1 - (double)l1) <= r1 &&
+                        (P != 3 || fabs(t2 - (double)l2) <= r2)) {
+                        atomicMin(&s_cmin[lane], l);  // first match of this warp's share = its smallest
+                        break;
                     }
                 }
             }
-            if (found < 0) ++L;
-            __syncwarp();
+            __syncthreads();
+            if (warp == 0) {
+                for (int j = 0; j < nb; ++j) {
+                    int found = s_cmin[j];
+                    if (found == 0x7fffffff) {
+                        found = -1;
+                        const int nn = L - L0;  // leaders founded earlier in this round (< 32)
+                        bool in = false;
+                        if (lane < nn) {
+                            const int l = L0 + lane;
+                            float l0, l1, l2 = 0.f;
+                            if (l < kLeaderCache) {
+                                l0 = s_lt[l * 3];
+                                l1 = s_lt[l * 3 + 1];
+                                l2 = s_lt[l * 3 + 2];
+                            } else {
+                                const int ls = (int)(uint32_t)s_key[l];
+                                l0 = __ldg(th + (int64_t)ls * P);
+                                l1 = __ldg(th + (int64_t)ls * P + 1);
+                                if (P == 3) l2 = __ldg(th + (int64_t)ls * P + 2);
+                            }
+                            in = fabs((double)s_ct[j * 3] - (double)l0) <= r0 &&
+                                 fabs((double)s_ct[j * 3 + 1] - (double)l1) <= r1 &&
+                                 (P != 3 || fabs((double)s_ct[j * 3 + 2] - (double)l2) <= r2);
+                        }
+                        const unsigned bal = __ballot_sync(0xffffffffu, in);
+                        if (bal) found = L0 + __ffs(bal) - 1;
+                    }
+                    if (lane == 0) {
+                        if (found >= 0) {
+                            s_key[found] += (1ull << 32);
+                        } else {
+                            s_key[L] = (1ull << 32) | (uint32_t)s_csid[j];
+                            if (L < kLeaderCache) {
+                                s_lt[L * 3] = s_ct[j * 3];
+                                s_lt[L * 3 + 1] = s_ct[j * 3 + 1];
+                                s_lt[L * 3 + 2] = s_ct[j * 3 + 2];
+                            }
+                        }
+                    }
+                    if (found < 0) ++L;
+                    __syncwarp();
+                }
+                if (lane == 0) s_m = L;
+            }
+            __syncthreads();
+            L = s_m;  // every thread learns the round's leader count
         }
-        if (lane == 0) s_m = L;
+        if (m == 0 && threadIdx.x == 0) s_m = 0;
     }
     __syncthreads();
 
