@@ -401,7 +401,11 @@ def main():
                    "pairs_grid_per_rank": pairs_grid, "pairs_multistart_per_rank": pairs_ms,
                    "l2": "inputs > L2 (hits %.0f MB, seeds %.0f MB, grid writes %.1f GB per step)" % (
                        batch.hits.nbytes / 1e6, seeds.nbytes / 1e6, 4.0 * cfg.n_units * E / 1e9),
-                   "parallelism": f"dp{world} (events sharded, 1 all_gather of results)"},
+                   "parallelism": f"dp{world} (events sharded, 1 all_gather of results)",
+                   "arithmetic": ("fp32; the grid contraction as three fp16 tensor-core products of an exact "
+                                  "hi/lo split of each fp32 factor, accumulated in fp32 (fp32-level accuracy, "
+                                  "T1 1e-5)" if cfg.model in (C.SLOPE2, C.SLOPE3) else "fp32"),
+                   "grid_chunk_events": pipe.chunk},
         "phases_ms_per_step": {k: v / a.steps for k, v in phase_ms.items()},
         "roofline": roof,
         "roofline_kernels": roofs,
