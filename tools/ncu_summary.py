@@ -22,6 +22,7 @@ METRICS = [
     "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active",
     "dram__bytes_read.sum",
     "dram__bytes_write.sum",
+    "dram__bytes_write.sum.per_second",
     "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed",
     "launch__registers_per_thread",
     "launch__grid_size",
