@@ -12,7 +12,7 @@ not 42 GB), and counts the algorithmic work (unit.hit pairs) for the report.
 from __future__ import annotations
 
 import dataclasses
-from typing import List, Optional, Sequence
+from typing import Optional, Sequence
 
 import numpy as np
 import torch

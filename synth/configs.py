@@ -33,8 +33,7 @@ size rule (a property of the plane positions, not of any event).
 from __future__ import annotations
 
 import dataclasses
-import math
-from typing import Optional, Tuple
+from typing import Tuple
 
 import numpy as np
 

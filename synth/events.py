@@ -16,7 +16,7 @@ from typing import List, Optional, Sequence
 
 import numpy as np
 
-from .configs import (LINE2D, SLOPE2, SLOPE3, TOY_PLANES, TOY_SMEAR, VELO_PLANES,
+from .configs import (LINE2D, SLOPE3, TOY_PLANES, TOY_SMEAR, VELO_PLANES,
                       VELO_R_MAX, VELO_R_MIN, VELO_SMEAR, Config)
 
 STREAM_HITS, STREAM_SEEDS = 1, 2

@@ -5,7 +5,6 @@ follows.  None of them re-types oracle.c's formula: they use closed forms,
 invariants, special cases, independent numerical differentiation, library
 routines (scipy.ndimage) and brute force on tiny inputs.
 """
-import itertools
 import math
 import os
 

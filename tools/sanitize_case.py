@@ -4,7 +4,6 @@ hit stages, peaks, multi-start with/without grad, merge) for compute-sanitizer r
 import os
 import sys
 
-import numpy as np
 import torch
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
