@@ -1,7 +1,7 @@
 /* retina.h -- C ABI of the B200 (sm_100a) Artificial Retina hot path.
  *
  * arXiv 1709.08610, "Numerical optimization for Artificial Retina Algorithm".
- * Four entry points, one per step of the method on the hot path:
+ * The four entry points of the hot path, one per step of the method:
  *
  *   retina_grid_response        Eq. (1)-(2), PAPER.md:36-39 (Sec. 2) and step (ii),
  *                               R_ij = sum_k exp(-s(x_k, theta_ij)^2 / sigma^2)
@@ -15,6 +15,12 @@
  *   retina_merge_tracks         Algorithm 1: "cluster solutions; for each
  *                               cluster select solution with highest response and above
  *                               threshold R0" (Z9, Z10).
+ * and the "next" rows built on them:
+ *   retina_grid_response_ex     the same grid with an explicit kernel choice;
+ *   retina_find_peaks_ws        step (iii) by many CTAs per event (caller workspace);
+ *   retina_estimate_peaks       step (iv): sub-cell parameter estimate per peak;
+ *   retina_multistart_newton    Algorithm 1 with the paper's Truncated-Newton update and sigma
+ *   (_ex)                       schedule, PAPER.md:213-216 (+ per-seed evaluation counts).
  *
  * Track models and the distance s:
  *   RETINA_LINE2D  P=2, theta=(a, b),       hit (x, y, -, -):  s   = y - (a x + b)
@@ -43,7 +49,9 @@
  *  - Precision: fp32 storage and arithmetic, exp lowered to ex2.approx with the
  *    log2(e)/sigma^2 scale applied after squaring; residuals formed with exact
  *    products (FMA) and, where a difference of coordinates is inexact (z - z_ref,
- *    z - z0, y - a x), as double-float pairs.
+ *    z - z0, y - a x), as double-float pairs.  The tensor-core grid kernels
+ *    split every fp32 factor exactly into tf32 or scaled fp16 parts and accumulate the
+ *    products in fp32, for fp32-level accuracy.
  *  - There is no CPU fallback: without a CUDA device every call returns RETINA_ECUDA.
  */
 #ifndef RETINA_H
