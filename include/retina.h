@@ -112,11 +112,15 @@ int retina_grid_response(const retina_events *ev, int model, float sigma,
  *                          residual does not split);
  *   RETINA_GRID_TENSOR     SLOPE2 / SLOPE3 (one GEMM per z0): the same contraction on the tcgen05 tensor cores with a
  *                          3xTF32 split (fp32-level accuracy), accumulators in TMEM;
- *   RETINA_GRID_TENSOR_F16 SLOPE2 / SLOPE3: the same contraction on kind::f16 with an exact scaled fp16 hi/lo split
- *                          of every factor (hi.hi and hi.lo + lo.hi in two TMEM accumulators, fp32-level accuracy,
- *                          half the MMA work of 3xTF32). */
+ *   RETINA_GRID_TENSOR_F16 SLOPE2 / SLOPE3: the same contraction on kind::f16 with an exact scaled fp16 hi/lo
+ *                          split of every factor (fp32-level accuracy, half the MMA work of 3xTF32), by
+ *                          persistent CTA pairs (cta_group::2, M = 256) with double-buffered TMEM
+ *                          accumulators (a three-part split gives one accumulator per tile);
+ *   RETINA_GRID_TENSOR_F16_PAIR    the same split by one CTA pair per 256 x 256 tile (two accumulators:
+ *                          hi.hi and hi.lo + lo.hi), non-persistent;
+ *   RETINA_GRID_TENSOR_F16_SINGLE  the same by one CTA per 128 x 256 tile (no cluster). */
 enum { RETINA_GRID_AUTO = 0, RETINA_GRID_DIRECT = 1, RETINA_GRID_SEPARABLE = 2, RETINA_GRID_TENSOR = 3,
-       RETINA_GRID_TENSOR_F16 = 4 };
+       RETINA_GRID_TENSOR_F16 = 4, RETINA_GRID_TENSOR_F16_PAIR = 5, RETINA_GRID_TENSOR_F16_SINGLE = 6 };
 int retina_grid_response_ex(const retina_events *ev, int model, float sigma,
                             const int32_t *axis_len, const float *const *axis_nodes,
                             float *response, int algorithm, void *stream);

@@ -82,14 +82,6 @@ int retina_grid_response(const retina_events *ev, int model, float sigma, const 
     return retina_grid_response_ex(ev, model, sigma, axis_len, axis_nodes, response, RETINA_GRID_AUTO, stream);
 }
 
-#ifndef RETINA_T16_PERSISTENT
-#define RETINA_T16_PERSISTENT 1  // persistent CTA-pair fp16 kernel (grid_tensor16p.cu); 0: one tile per CTA (pair)
-#endif
-
-#ifndef RETINA_T16_PAIR
-#define RETINA_T16_PAIR 1  // CTA-pair (cta_group::2) fp16 kernel (0: one CTA per 128x256 tile)
-#endif
-
 int retina_grid_response_ex(const retina_events *ev, int model, float sigma, const int32_t *axis_len,
                             const float *const *axis_nodes, float *response, int algorithm, void *stream) {
     g_last_error[0] = 0;
@@ -107,11 +99,11 @@ int retina_grid_response_ex(const retina_events *ev, int model, float sigma, con
     }
     if (cells > 0x7fffffffLL) return fail(RETINA_EUNSUPPORTED, "more than 2^31-1 cells per event");
     if (ev->n_events > 0 && !response) return fail(RETINA_EINVAL, "response is NULL");
-    if (algorithm < RETINA_GRID_AUTO || algorithm > RETINA_GRID_TENSOR_F16)
+    if (algorithm < RETINA_GRID_AUTO || algorithm > RETINA_GRID_TENSOR_F16_SINGLE)
         return fail(RETINA_EINVAL, "unknown grid algorithm %d", algorithm);
     if (algorithm == RETINA_GRID_SEPARABLE && model == RETINA_LINE2D)
         return fail(RETINA_EUNSUPPORTED, "LINE2D residual does not factorise: no separable grid");
-    if ((algorithm == RETINA_GRID_TENSOR || algorithm == RETINA_GRID_TENSOR_F16) && model == RETINA_LINE2D)
+    if (algorithm >= RETINA_GRID_TENSOR && model == RETINA_LINE2D)
         return fail(RETINA_EUNSUPPORTED, "LINE2D residual does not factorise: no tensor-core grid");
     if (algorithm == RETINA_GRID_AUTO)
         algorithm = (model == RETINA_LINE2D)   ? RETINA_GRID_DIRECT
@@ -133,9 +125,11 @@ int retina_grid_response_ex(const retina_events *ev, int model, float sigma, con
     if (algorithm == RETINA_GRID_TENSOR)
         err = retina::launch_grid_tensor(model, a, ev->n_events, (cudaStream_t)stream);
     else if (algorithm == RETINA_GRID_TENSOR_F16)
-        err = RETINA_T16_PERSISTENT ? retina::launch_grid_tensor16p(model, a, ev->n_events, (cudaStream_t)stream)
-              : RETINA_T16_PAIR     ? retina::launch_grid_tensor16x2(model, a, ev->n_events, (cudaStream_t)stream)
-                                    : retina::launch_grid_tensor16(model, a, ev->n_events, (cudaStream_t)stream);
+        err = retina::launch_grid_tensor16p(model, a, ev->n_events, (cudaStream_t)stream);
+    else if (algorithm == RETINA_GRID_TENSOR_F16_PAIR)
+        err = retina::launch_grid_tensor16x2(model, a, ev->n_events, (cudaStream_t)stream);
+    else if (algorithm == RETINA_GRID_TENSOR_F16_SINGLE)
+        err = retina::launch_grid_tensor16(model, a, ev->n_events, (cudaStream_t)stream);
     else if (algorithm == RETINA_GRID_SEPARABLE)
         err = retina::launch_grid_separable(model, a, ev->n_events, (cudaStream_t)stream);
     else

@@ -1,7 +1,7 @@
-// grid_tensor16p.cu -- K1h, the default grid kernel for SLOPE2 / SLOPE3: persistent CTA-pair
-// variant of the fp16-split grid kernel (RETINA_T16_PERSISTENT, default 1).  Eq. (2) as a dense contraction over hits on the tcgen05 tensor
-// cores (kind::f16, cta_group::2, M = 256), with the per-tile prologue and epilogue taken off the
-// MMA critical path:
+// grid_tensor16p.cu -- K1h, the default grid kernel for SLOPE2 / SLOPE3 (RETINA_GRID_TENSOR_F16,
+// what RETINA_GRID_AUTO runs): persistent CTA-pair variant of the fp16-split grid kernel.  Eq. (2)
+// as a dense contraction over hits on the tcgen05 tensor cores (kind::f16, cta_group::2, M = 256),
+// with the per-tile prologue and epilogue taken off the MMA critical path:
 //
 //     R[i][j] = sum_k EX[i][k] EY[j][k],  EX = 2^(-K (x - tx z)^2),  EY = 2^(-K (y - ty z)^2)
 //

@@ -74,12 +74,14 @@ def test_grid_response_validation(L):
     big = _i(65536, 65536)
     assert g(ctypes.byref(ev), 1, 0.5, big, nodes, 16, None) == rt.RETINA_EUNSUPPORTED
     gx = L.retina_grid_response_ex
-    assert gx(ctypes.byref(ev), 1, 0.5, alen, nodes, 16, 5, None) == rt.RETINA_EINVAL  # unknown algorithm
+    assert gx(ctypes.byref(ev), 1, 0.5, alen, nodes, 16, 7, None) == rt.RETINA_EINVAL  # unknown algorithm
     assert gx(ctypes.byref(ev), 1, 0.5, alen, nodes, 16, -1, None) == rt.RETINA_EINVAL
-    for algo in (rt.GRID_TENSOR, rt.GRID_TENSOR_F16, rt.GRID_SEPARABLE):  # LINE2D does not factorise
+    for algo in (rt.GRID_TENSOR, rt.GRID_TENSOR_F16, rt.GRID_TENSOR_F16_PAIR, rt.GRID_TENSOR_F16_SINGLE,
+                 rt.GRID_SEPARABLE):  # LINE2D does not factorise
         assert gx(ctypes.byref(ev), 0, 0.5, alen, nodes, 16, algo, None) == rt.RETINA_EUNSUPPORTED
     e0 = _ev(n=0)  # nothing to launch: every algorithm accepts an empty batch
-    for algo in (rt.GRID_AUTO, rt.GRID_DIRECT, rt.GRID_SEPARABLE, rt.GRID_TENSOR, rt.GRID_TENSOR_F16):
+    for algo in (rt.GRID_AUTO, rt.GRID_DIRECT, rt.GRID_SEPARABLE, rt.GRID_TENSOR, rt.GRID_TENSOR_F16,
+                 rt.GRID_TENSOR_F16_PAIR, rt.GRID_TENSOR_F16_SINGLE):
         assert gx(ctypes.byref(e0), 1, 0.5, alen, nodes, 16, algo, None) == rt.RETINA_OK
 
 

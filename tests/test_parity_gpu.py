@@ -414,7 +414,8 @@ def test_direct_and_separable_agree_cfg3_batch():
 
 # --------------------------------------------------------------------------- tensor-core grid (SLOPE2)
 TENSOR = R.retina.GRID_TENSOR
-TENSORS = [R.retina.GRID_TENSOR, R.retina.GRID_TENSOR_F16]  # 3xTF32 and fp16-split kernels
+TENSORS = [R.retina.GRID_TENSOR, R.retina.GRID_TENSOR_F16,  # 3xTF32 and the fp16-split kernels (default:
+           R.retina.GRID_TENSOR_F16_PAIR, R.retina.GRID_TENSOR_F16_SINGLE]  # persistent pairs; per-tile pair, single)
 
 
 @pytest.mark.parametrize("tensor", TENSORS)
