@@ -212,7 +212,10 @@ static int merge_cmp(const void *pa, const void *pb, void *vctx) {
 
 void ora_merge(int n_events, int n_seeds, int P, const double *theta, const double *R,
                const double *radius, double threshold, int capacity, double *track_theta,
-               double *track_R, int32_t *track_seed, int32_t *track_size, int32_t *track_count) {
+               double *track_R, int32_t *track_seed, int32_t *track_size, int32_t *track_count,
+               int32_t *member) {
+    /* member (may be NULL): [n_events][n_seeds], the creation ordinal of the leader each seed
+     * joined, -1 below the threshold (bookkeeping for the T6 comparator; no arithmetic). */
 #pragma omp parallel for schedule(dynamic)
     for (int e = 0; e < n_events; ++e) {
         const double *th = theta + (int64_t)e * n_seeds * P;
@@ -221,8 +224,11 @@ void ora_merge(int n_events, int n_seeds, int P, const double *theta, const doub
         int32_t *leader = (int32_t *)malloc(sizeof(int32_t) * (n_seeds > 0 ? n_seeds : 1));
         int32_t *size = (int32_t *)malloc(sizeof(int32_t) * (n_seeds > 0 ? n_seeds : 1));
         int m = 0;
-        for (int s = 0; s < n_seeds; ++s)
+        int32_t *mem = member ? member + (int64_t)e * n_seeds : NULL;
+        for (int s = 0; s < n_seeds; ++s) {
+            if (mem) mem[s] = -1;
             if (r[s] >= threshold) items[m++] = s;
+        }
         merge_ctx ctx = {th, r, P};
         qsort_r(items, m, sizeof(int32_t), merge_cmp, &ctx);
         int L = 0;
@@ -240,8 +246,9 @@ void ora_merge(int n_events, int n_seeds, int P, const double *theta, const doub
             } else {
                 leader[L] = s;
                 size[L] = 1;
-                ++L;
+                found = L++;
             }
+            if (mem) mem[s] = found;
         }
         for (int l = 0; l < L && l < capacity; ++l) {
             const int64_t o = (int64_t)e * capacity + l;
@@ -366,7 +373,35 @@ void ora_point_hess(int model, const float *hits, int n, double z_ref, const dou
  * (-H) p = g, at most P iterations (exact for a positive-definite -H), stopped at a direction
  * of non-positive curvature d^T (-H) d <= 0: the iterate built so far is kept, or, at the first
  * iteration, the fixed-step gradient direction p = eta g (reading Z24). */
-static void tn_direction(int P, const double *g, const double *H, double eta, double *p, double *margin) {
+/* splitmix64 of (key, seed, counter) mapped to a uniform double in [-1, 1] (test perturbations) */
+static double unit_hash(uint64_t key, int64_t id, uint64_t c) {
+    uint64_t z = key * 0x9E3779B97F4A7C15ull ^ ((uint64_t)id * 0xBF58476D1CE4E5B9ull) ^ (c * 0x94D049BB133111EBull);
+    z += 0x9E3779B97F4A7C15ull;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    z ^= z >> 31;
+    return (double)(z >> 11) * (2.0 / 9007199254740992.0) - 1.0;
+}
+
+typedef struct {        /* per-seed decision bookkeeping (T5n attribution; no effect by default) */
+    double *margin;     /* smallest relative margin of any decision taken                       */
+    double *log;        /* nullable: margin of decision k at log[k], k < log_len                 */
+    int log_len;
+    int count;          /* decisions taken so far                                               */
+    const uint8_t *flip; /* nullable: decision k's outcome is inverted when flip[k] != 0, k < log_len */
+} decisions;
+
+/* Records one discrete decision's relative margin m and returns its outcome, inverted when it
+ * is the decision the caller asked to flip (test attribution of fp32/fp64 near-ties). */
+static int decide(decisions *dc, int outcome, double m) {
+    if (m < *dc->margin) *dc->margin = m;
+    if (dc->log && dc->count < dc->log_len) dc->log[dc->count] = m;
+    const int flip = dc->flip && dc->count < dc->log_len && dc->flip[dc->count];
+    dc->count++;
+    return flip ? !outcome : outcome;
+}
+
+static void tn_direction(int P, const double *g, const double *H, double eta, double *p, decisions *dc) {
     double x[3] = {0, 0, 0}, r[3], d[3], Ad[3];
     double hs = 0.0;  /* scale of H for the curvature-decision margin (diagnostic only) */
     for (int a = 0; a < P * P; ++a) hs = fabs(H[a]) > hs ? fabs(H[a]) : hs;
@@ -385,13 +420,11 @@ static void tn_direction(int P, const double *g, const double *H, double eta, do
             for (int b = 0; b < P; ++b) Ad[a] -= H[a * P + b] * d[b];
             curv += d[a] * Ad[a];
         }
-        {
-            double dd = 0.0;
-            for (int a = 0; a < P; ++a) dd += d[a] * d[a];
-            const double m = (dd > 0.0 && hs > 0.0) ? fabs(curv) / (dd * hs) : 1.0;
-            if (m < *margin) *margin = m;
-        }
-        if (!(curv > 0.0)) {
+        double dd = 0.0;
+        for (int a = 0; a < P; ++a) dd += d[a] * d[a];
+        const double m = (dd > 0.0 && hs > 0.0) ? fabs(curv) / (dd * hs) : 1.0;
+        /* a flipped decision never divides by a zero curvature */
+        if (!decide(dc, curv > 0.0, m) || curv == 0.0) {
             if (it == 0)
                 for (int a = 0; a < P; ++a) x[a] = eta * g[a];
             break;
@@ -416,6 +449,12 @@ static void tn_direction(int P, const double *g, const double *H, double eta, do
  * backtracking on R (reading Z25: c1 = 1e-4, alpha = 1, 1/2, ..., at most max_halvings
  * halvings; theta is clamped to the prior box at every trial; no accepted trial leaves theta
  * unchanged).  Returns theta^q, R(theta^q) and grad R(theta^q) at final_sigma.
+ * perturb_eps > 0 (test attribution only): every evaluated R, grad R and H entry is multiplied by
+ * 1 + perturb_eps u, u uniform in [-1, 1] from a counter hash of (perturb_key, seed, evaluation),
+ * i.e. the oracle runs with arithmetic errors of the GPU's size (T5n "arithmetic sensitivity").
+ * flip (nullable; test attribution only): [seed][log_len] flags; decision k of a seed (CG curvature
+ * tests and Armijo tests, numbered in the order taken) has its outcome inverted when flag k is set;
+ * decision_log (nullable) receives each decision's relative margin ([seed][log_len], -1 = unused).
  * margin_out (nullable; diagnostic for the T5 near-tie rule, no effect on the result): per seed,
  * the smallest relative margin of any discrete decision taken -- |R_t - (R_0 + c1 alpha g.p)| /
  * R_0 for the Armijo tests and |d^T H d| / (|d|^2 max|H|) for the CG curvature tests.
@@ -428,7 +467,8 @@ static void tn_direction(int P, const double *g, const double *H, double eta, do
 void ora_newton(int model, int n_events, const int32_t *offsets, const float *hits, double z_ref, int n_seeds,
                 const float *seeds, int n_steps, const double *sigmas, const double *etas, double final_sigma,
                 int max_halvings, const double *box_lo, const double *box_hi, double *theta_out,
-                double *R_out, double *grad_out, double *margin_out, int32_t *evals_out) {
+                double *R_out, double *grad_out, double *margin_out, int32_t *evals_out, const uint8_t *flip,
+                double *decision_log, int log_len, double perturb_eps, uint64_t perturb_key) {
     const int P = model_P(model);
 #pragma omp parallel for collapse(2) schedule(dynamic, 16)
     for (int64_t e = 0; e < n_events; ++e) {
@@ -438,11 +478,25 @@ void ora_newton(int model, int n_events, const int32_t *offsets, const float *hi
             const int64_t id = e * n_seeds + s;
             double th[3] = {0, 0, 0}, g[3], H[9], p[3], R0, Rt, tt[3], margin = 1.0;
             int32_t evals = 0;
+            decisions dc = {&margin, decision_log ? decision_log + id * log_len : NULL, log_len, 0,
+                            flip ? flip + id * log_len : NULL};
+            if (dc.log)
+                for (int k = 0; k < log_len; ++k) dc.log[k] = -1.0;
             for (int a = 0; a < P; ++a) th[a] = seeds[id * P + a];
+            uint64_t pc = 0; /* perturbation counter of this seed */
             for (int j = 0; j < n_steps; ++j) {
                 ora_point_hess(model, h, n, z_ref, th, sigmas[j], &R0, g, H);
                 ++evals;
-                tn_direction(P, g, H, etas[j], p, &margin);
+                if (perturb_eps > 0.0) {
+                    R0 *= 1.0 + perturb_eps * unit_hash(perturb_key, id, pc++);
+                    for (int a = 0; a < P; ++a) g[a] *= 1.0 + perturb_eps * unit_hash(perturb_key, id, pc++);
+                    for (int a = 0; a < P; ++a)
+                        for (int b = a; b < P; ++b) {
+                            H[a * P + b] *= 1.0 + perturb_eps * unit_hash(perturb_key, id, pc++);
+                            H[b * P + a] = H[a * P + b];
+                        }
+                }
+                tn_direction(P, g, H, etas[j], p, &dc);
                 double slope = 0.0;
                 for (int a = 0; a < P; ++a) slope += g[a] * p[a];
                 double alpha = 1.0;
@@ -455,11 +509,9 @@ void ora_newton(int model, int n_events, const int32_t *offsets, const float *hi
                     }
                     ora_point_hess(model, h, n, z_ref, tt, sigmas[j], &Rt, NULL, NULL);
                     ++evals;
-                    {
-                        const double m = fabs(Rt - (R0 + 1e-4 * alpha * slope)) / (R0 > 1e-6 ? R0 : 1e-6);
-                        if (m < margin) margin = m;
-                    }
-                    if (Rt >= R0 + 1e-4 * alpha * slope) {
+                    if (perturb_eps > 0.0) Rt *= 1.0 + perturb_eps * unit_hash(perturb_key, id, pc++);
+                    const double m = fabs(Rt - (R0 + 1e-4 * alpha * slope)) / (R0 > 1e-6 ? R0 : 1e-6);
+                    if (decide(&dc, Rt >= R0 + 1e-4 * alpha * slope, m)) {
                         for (int a = 0; a < P; ++a) th[a] = tt[a];
                         break;
                     }

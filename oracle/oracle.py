@@ -42,10 +42,10 @@ def lib():
         L.ora_grid.argtypes = [i, i, P, P, d, d, P, P, P, P, P]
         L.ora_peaks.argtypes = [P, i, i, P, d, i, P, P, P]
         L.ora_multistart.argtypes = [i, i, P, P, d, d, i, P, i, d, P, P, P, P, P]
-        L.ora_merge.argtypes = [i, i, i, P, P, P, d, i, P, P, P, P, P]
+        L.ora_merge.argtypes = [i, i, i, P, P, P, d, i, P, P, P, P, P, P]
         L.ora_estimate.argtypes = [P, i, i, P, P, P, P, P, P, i, P]
         L.ora_point_hess.argtypes = [i, P, i, d, P, d, P, P, P]
-        L.ora_newton.argtypes = [i, i, P, P, d, i, P, i, P, P, d, i, P, P, P, P, P, P, P]
+        L.ora_newton.argtypes = [i, i, P, P, d, i, P, i, P, P, d, i, P, P, P, P, P, P, P, P, P, i, d, ctypes.c_uint64]
         for f in (L.ora_point, L.ora_grid, L.ora_peaks, L.ora_multistart, L.ora_merge, L.ora_estimate,
                   L.ora_point_hess, L.ora_newton):
             f.restype = None
@@ -132,9 +132,10 @@ def multistart(model: int, offsets, hits, seeds, sigma: float, n_iters: int, ste
     return th, R, g
 
 
-def merge(theta, R, radius, threshold: float, capacity: int):
+def merge(theta, R, radius, threshold: float, capacity: int, want_members: bool = False):
     """Algorithm 1 "cluster ... select highest response above R0" (readings Z9/Z10).
-    Returns (track_theta[E,cap,P], track_R[E,cap], seed[E,cap], size[E,cap], count[E])."""
+    Returns (track_theta[E,cap,P], track_R[E,cap], seed[E,cap], size[E,cap], count[E]), plus
+    with want_members the leader ordinal each seed joined ([E,S], -1 below the threshold)."""
     th = np.ascontiguousarray(np.asarray(theta, np.float64))
     r = np.ascontiguousarray(np.asarray(R, np.float64))
     E, S, P = th.shape
@@ -145,9 +146,11 @@ def merge(theta, R, radius, threshold: float, capacity: int):
     ts = np.full((E, cap), -1, np.int32)
     tz = np.zeros((E, cap), np.int32)
     tc = np.zeros(E, np.int32)
+    mem = np.zeros((E, S), np.int32) if want_members else None
     lib().ora_merge(E, S, P, _p(th), _p(r), _p(rad), _f(threshold), int(capacity),
-                    _p(tt), _p(tr), _p(ts), _p(tz), _p(tc))
-    return tt[:, :capacity], tr[:, :capacity], ts[:, :capacity], tz[:, :capacity], tc
+                    _p(tt), _p(tr), _p(ts), _p(tz), _p(tc), _p(mem))
+    res = (tt[:, :capacity], tr[:, :capacity], ts[:, :capacity], tz[:, :capacity], tc)
+    return res + ((mem,) if want_members else ())
 
 
 def estimate(grid_values, nodes: Sequence[np.ndarray], peak_index, peak_count, capacity: int):
@@ -179,10 +182,14 @@ def point_hess(model: int, hits, theta, sigma: float, z_ref: float = 0.0):
 
 def newton(model: int, offsets, hits, seeds, sigmas, etas, final_sigma: float, max_halvings: int,
            box_lo, box_hi, z_ref: float = 0.0, want_grad: bool = True, want_margin: bool = False,
-           want_evals: bool = False):
+           want_evals: bool = False, flip=None, log_len: int = 0, perturb: float = 0.0, perturb_key: int = 0):
     """Algorithm 1 with Truncated-Newton updates and a sigma schedule (readings Z22-Z25).
     Returns (theta, R, grad), plus margin with want_margin, plus the per-seed response
-    evaluation count (q + line-search trials + 1) with want_evals."""
+    evaluation count (q + line-search trials + 1) with want_evals.  Test attribution only:
+    `flip` ([E,S,log_len] bool) inverts the outcomes of the flagged numbered discrete decisions of
+    each seed, and log_len > 0 appends each seed's per-decision margins ([E,S,log_len], -1 = unused);
+    perturb > 0 multiplies every evaluated R, grad R and H entry by 1 + perturb u, u ~ U[-1, 1]
+    keyed by perturb_key."""
     off = np.ascontiguousarray(np.asarray(offsets, np.int32))
     h = _f32(hits).reshape(-1, 4)
     sd = _f32(seeds)
@@ -197,7 +204,12 @@ def newton(model: int, offsets, hits, seeds, sigmas, etas, final_sigma: float, m
     g = np.zeros((E, S, P)) if want_grad else None
     m = np.zeros((E, S)) if want_margin else None
     ne = np.zeros((E, S), np.int32) if want_evals else None
+    assert flip is None or log_len > 0
+    fl = None if flip is None else np.ascontiguousarray(np.broadcast_to(np.asarray(flip, np.uint8), (E, S, log_len)))
+    lg = np.zeros((E, S, log_len)) if log_len > 0 else None
     lib().ora_newton(model, E, _p(off), _p(h), _f(z_ref), S, _p(sd), len(sg), _p(sg), _p(et), _f(final_sigma),
-                     int(max_halvings), _p(lo), _p(hi), _p(th), _p(R), _p(g), _p(m), _p(ne))
-    res = (th, R, g) + ((m,) if want_margin else ()) + ((ne,) if want_evals else ())
+                     int(max_halvings), _p(lo), _p(hi), _p(th), _p(R), _p(g), _p(m), _p(ne), _p(fl), _p(lg),
+                     int(log_len), float(perturb), int(perturb_key))
+    res = (th, R, g) + ((m,) if want_margin else ()) + ((ne,) if want_evals else ()) + \
+        ((lg,) if log_len > 0 else ())
     return res

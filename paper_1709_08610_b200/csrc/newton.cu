@@ -355,52 +355,57 @@ __device__ __forceinline__ void nt_pass_r_x2(HitStage &st, const float (&th)[S][
 #endif
 
 // Truncated CG on (-H) p = g (maximisation), <= P iterations, fallback eta g (oracle tn_direction).
+// The solve runs in fp64 on the fp32-accumulated g and H: for SLOPE3 the Hessian's scales differ by
+// ~(d / t)^2 ~ 1e7 between the slope and z0 axes, so an fp32 CG loses the z0 component of the
+// Newton direction (round 2: 7.6 % of cfg4 seeds ended > 1e-3 x range from the oracle); in fp64 the
+// only error left is the elementwise-relative accumulation error of g and H, which the scaling does
+// not amplify.  P <= 3: a few dozen DFMA per seed per Newton step, nothing next to its hit passes.
 template <int P>
 __device__ __forceinline__ void nt_direction(const float (&g)[3], const float (&H)[3][3], float eta, float (&p)[3]) {
-    float x[3] = {0.f, 0.f, 0.f}, r[3], d[3], Ad[3];
-    float rr = 0.f;
+    double x[3] = {0.0, 0.0, 0.0}, r[3], d[3], Ad[3];
+    double rr = 0.0;
 #pragma unroll
     for (int a = 0; a < P; ++a) {
         r[a] = g[a];
         d[a] = g[a];
-        rr = __fmaf_rn(g[a], g[a], rr);
+        rr = fma((double)g[a], (double)g[a], rr);
     }
-    const float rr0 = rr;
+    const double rr0 = rr;
 #pragma unroll
     for (int it = 0; it < P; ++it) {
-        if (!(rr > 0.f)) break;
-        float curv = 0.f;
+        if (!(rr > 0.0)) break;
+        double curv = 0.0;
 #pragma unroll
         for (int a = 0; a < P; ++a) {
-            float v = 0.f;
+            double v = 0.0;
 #pragma unroll
-            for (int b = 0; b < P; ++b) v = __fmaf_rn(-H[a][b], d[b], v);
+            for (int b = 0; b < P; ++b) v = fma(-(double)H[a][b], d[b], v);
             Ad[a] = v;
-            curv = __fmaf_rn(d[a], v, curv);
+            curv = fma(d[a], v, curv);
         }
-        if (!(curv > 0.f)) {
+        if (!(curv > 0.0)) {
             if (it == 0) {
 #pragma unroll
-                for (int a = 0; a < P; ++a) x[a] = __fmul_rn(eta, g[a]);
+                for (int a = 0; a < P; ++a) x[a] = (double)eta * (double)g[a];
             }
             break;
         }
-        const float alpha = __fdiv_rn(rr, curv);
-        float rr_new = 0.f;
+        const double alpha = rr / curv;
+        double rr_new = 0.0;
 #pragma unroll
         for (int a = 0; a < P; ++a) {
-            x[a] = __fmaf_rn(alpha, d[a], x[a]);
-            r[a] = __fmaf_rn(-alpha, Ad[a], r[a]);
-            rr_new = __fmaf_rn(r[a], r[a], rr_new);
+            x[a] = fma(alpha, d[a], x[a]);
+            r[a] = fma(-alpha, Ad[a], r[a]);
+            rr_new = fma(r[a], r[a], rr_new);
         }
-        if (rr_new <= 1e-14f * rr0) break;
-        const float beta = __fdiv_rn(rr_new, rr);
+        if (rr_new <= 1e-24 * rr0) break;
+        const double beta = rr_new / rr;
 #pragma unroll
-        for (int a = 0; a < P; ++a) d[a] = __fmaf_rn(beta, d[a], r[a]);
+        for (int a = 0; a < P; ++a) d[a] = fma(beta, d[a], r[a]);
         rr = rr_new;
     }
 #pragma unroll
-    for (int a = 0; a < 3; ++a) p[a] = (a < P) ? x[a] : 0.f;
+    for (int a = 0; a < 3; ++a) p[a] = (a < P) ? (float)x[a] : 0.f;
 }
 
 // Shared state of the compacted line search: per seed slot (owner thread t, seed s -> slot

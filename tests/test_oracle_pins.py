@@ -319,6 +319,42 @@ def test_P11_single_hit_trajectory_is_a_straight_contraction():
         assert np.dot(v0, v1) > 0
 
 
+def test_P11_single_hit_one_step_closed_form():
+    """One fixed-step update on one SLOPE2 hit, in closed form: with u = (x, y)/d,
+    R(t) = exp(-d^2 |t - u|^2 / sigma^2) and grad R = (2 d^2 / sigma^2) R(t) (u - t), so
+    t^1 = t^0 + eta (2 d^2 / sigma^2) R(t^0) (u - t^0)   (Alg. 1 update, reading Z7).
+    Also with z_ref != 0 (d = z - z_ref) and for SLOPE3 at fixed z0 (d = z - z0; the z0 component
+    of the step is then -eta (2/sigma^2) R sum (s_x tx + s_y ty), checked in closed form too)."""
+    x, y, z = np.float32(7.25), np.float32(-4.5), np.float32(330.0)
+    h = h4([(x, y, z)])
+    sig = np.float32(1.5)
+    eta = np.float32(3e-7)
+    for z_ref in (0.0, 30.0):
+        d = float(z) - z_ref
+        u = np.array([float(x), float(y)]) / d
+        seeds = np.array([[[0.0213, -0.0141], [0.026, -0.011], [-0.2, 0.25]]], np.float32)
+        th, R, _ = ora.multistart(C.SLOPE2, [0, 1], h, seeds, float(sig), 1, float(eta), (-.3, -.3), (.3, .3),
+                                  z_ref=z_ref)
+        for s in range(seeds.shape[1]):
+            t0 = seeds[0, s].astype(np.float64)
+            R0 = math.exp(-d * d * float(np.sum((t0 - u) ** 2)) / float(sig) ** 2)
+            t1 = t0 + float(eta) * (2 * d * d / float(sig) ** 2) * R0 * (u - t0)
+            assert np.allclose(th[0, s], t1, rtol=0, atol=1e-15), (s, th[0, s], t1)
+            if s < 2:
+                assert np.linalg.norm(th[0, s] - t0) > 1e-6   # the step is not negligible
+    # SLOPE3: theta = (tx, ty, z0); d = z - z0, s = (x - tx d, y - ty d)
+    t0 = np.array([0.0215, -0.0138, 4.0])
+    seeds = t0.astype(np.float32)[None, None]
+    t0 = seeds[0, 0].astype(np.float64)
+    th, _, _ = ora.multistart(C.SLOPE3, [0, 1], h, seeds, float(sig), 1, float(eta), (-.3, -.3, -150.), (.3, .3, 150.))
+    d = float(z) - t0[2]
+    sx, sy = float(x) - t0[0] * d, float(y) - t0[1] * d
+    R0 = math.exp(-(sx * sx + sy * sy) / float(sig) ** 2)
+    c = 2 / float(sig) ** 2 * R0
+    t1 = t0 + float(eta) * c * np.array([sx * d, sy * d, -(sx * t0[0] + sy * t0[1])])
+    assert np.allclose(th[0, 0], t1, rtol=0, atol=1e-13), (th[0, 0], t1)
+
+
 # ---------------------------------------------------------------- P12 (SPEC.md:379-381, 388)
 def _merge_cluster_all_then_select(theta, R, radius, thr):
     """Alternative formulation of PAPER.md:154-155: greedy leader clustering of

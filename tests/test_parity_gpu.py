@@ -274,6 +274,15 @@ def _run_multistart(cfg, ev_ids, n_seeds, n_iters=None, step=None, z_ref=0.0):
     return b, seeds, th, Rg, gg
 
 
+# Bounds on the fraction of seeds (T5) / oracle tracks (T6) the oracle-side rules may excuse per
+# config: about twice what the measured runs excuse (PARITY-STATS lines), so a
+# kernel regression that moved many sensitive seeds (or dissolved tracks) still fails.
+T5_EXCUSE_BOUND = {("cfg2", 1.0): 0.002, ("cfg2", 20.0): 0.005, ("cfg3", 1.0): 0.002, ("cfg4", 1.0): 0.002,
+                   ("cfg0", 1e3): 0.12}   # measured (round 2): 0, 0.0020, 0, 0, 0.0625
+T6_EXCUSE_BOUND = {("cfg2", 1.0): 0.03, ("cfg2", 20.0): 0.05, ("cfg3", 1.0): 0.03, ("cfg4", 1.0): 0.03}
+# measured: 0/38, 1/48 (all members sensitive), 0/2, 0/1 and 0/96 oracle tracks excused
+
+
 @pytest.mark.parametrize("name,n_ev,n_seeds,step_mult", [("cfg2", 4, 1024, 1.0), ("cfg2", 2, 512, 20.0),
                                                           ("cfg3", 2, 8192, 1.0),  # bench launch config
                                                           ("cfg4", 1, 256, 1.0), ("cfg4", 1, 16384, 1.0),
@@ -288,14 +297,13 @@ def test_T5_T6_T7_multistart_and_merge(name, n_ev, n_seeds, step_mult):
     rth, rR, rg = ora.multistart(cfg.model, b.offsets, b.hits, seeds, cfg.sigma, n_iters, step,
                                  cfg.box_lo, cfg.box_hi)
     ranges = np.array(cfg.box_hi, np.float64) - np.array(cfg.box_lo, np.float64)
-    # T5: states within 1e-3 x range unless the seed is sensitive (oracle-side rule)
-    dev_rel = np.max(np.abs(th.astype(np.float64) - rth) / ranges, axis=2)
-    bad = np.argwhere(dev_rel > 1e-3)
-    if len(bad):
-        sens = PU.sensitive_seeds(cfg.model, b.offsets, b.hits, seeds, cfg.sigma, n_iters, step,
-                                  cfg.box_lo, cfg.box_hi, rth, ranges, [tuple(x) for x in bad])
-        assert sens.all(), f"{(~sens).sum()} non-sensitive seeds off by > 1e-3 range"
-    assert len(bad) <= 0.25 * th.shape[0] * th.shape[1]  # gross-bug guard; sensitivity excuses the rest
+    tag = f"T5/T6 {name} E={n_ev} S={n_seeds} step x{step_mult:g}"
+    # T5: states within 1e-3 x range unless the seed is sensitive (the one oracle-side rule)
+    unexcused, st5, sens_cache = PU.t5_states(cfg.model, b.offsets, b.hits, seeds, cfg.sigma, n_iters, step,
+                                              cfg.box_lo, cfg.box_hi, th, rth, ranges)
+    PU.report(tag, **st5)
+    assert not unexcused, f"{len(unexcused)} non-sensitive seeds off by > 1e-3 range: {unexcused[:5]}"
+    assert st5["excused_frac"] <= T5_EXCUSE_BOUND[(name, step_mult)], st5
     assert np.all(th >= np.float32(cfg.box_lo)) and np.all(th <= np.float32(cfg.box_hi))
     # T1 on the final responses: response_out = R(theta_out), checked at the GPU's own theta_out
     rng = np.random.default_rng(0)
@@ -311,28 +319,33 @@ def test_T5_T6_T7_multistart_and_merge(name, n_ev, n_seeds, step_mult):
     tt, tr, ts, tz, tc = R.retina_merge_tracks(th_d, R_d, cfg.merge_radius, cfg.track_threshold, cap)
     torch.cuda.synchronize()
     ts, tz, tc = ts.cpu().numpy(), tz.cpu().numpy(), tc.cpu().numpy()
-    ott, otr, ots, otz, otc = ora.merge(th.astype(np.float64), Rg.astype(np.float64), cfg.merge_radius,
-                                        cfg.track_threshold, cap)
+    ott, otr, ots, otz, otc, gmem = ora.merge(th.astype(np.float64), Rg.astype(np.float64), cfg.merge_radius,
+                                              cfg.track_threshold, cap, want_members=True)
     assert np.array_equal(tc, otc)
     for e in range(len(ev_ids)):
         k = min(tc[e], cap)
         assert np.array_equal(ts[e, :k], ots[e, :k]) and np.array_equal(tz[e, :k], otz[e, :k])
     assert np.array_equal(tt.cpu().numpy()[0, :min(tc[0], cap)], th[0, ts[0, :min(tc[0], cap)]])
-    # T6: merged track sets from GPU and oracle pipelines match within 1e-3 range,
-    # excusing tracks near R0, near the merge radius, or made only of sensitive seeds
-    _, _, ots64, _, otc64 = ora.merge(rth, rR, cfg.merge_radius, cfg.track_threshold, cap)
+    # T6: merged track sets of the GPU and oracle pipelines match one to one within 1e-3 range;
+    # an unmatched track is excused only by a named oracle-side rule (near R0, near the merge
+    # radius, all members sensitive)
+    _, _, ots64, _, otc64, rmem = ora.merge(rth, rR, cfg.merge_radius, cfg.track_threshold, cap, want_members=True)
+    assert np.all(otc64 <= cap) and np.all(tc <= cap)
+    tot = {}
     for e in range(len(ev_ids)):
-        A = th[e, ts[e, :min(tc[e], cap)]].astype(np.float64)
-        B = rth[e, ots64[e, :min(otc64[e], cap)]]
-        unmatched = 0
-        for X, Y, RX in ((A, B, Rg[e, ts[e, :min(tc[e], cap)]]), (B, A, rR[e, ots64[e, :min(otc64[e], cap)]])):
-            for x, rx in zip(X, RX):
-                if len(Y) and np.min(np.max(np.abs(Y - x) / ranges, axis=1)) <= 1e-3:
-                    continue
-                if abs(rx - cfg.track_threshold) <= 1e-5 * cfg.track_threshold:
-                    continue
-                unmatched += 1
-        assert unmatched <= max(1, 0.02 * max(len(A), len(B))), (e, unmatched, len(A), len(B))
+        def sensitive(s, e=e):
+            if (e, s) not in sens_cache:
+                sens_cache[(e, s)] = bool(PU.sensitive_seeds(cfg.model, b.offsets, b.hits, seeds, cfg.sigma, n_iters,
+                                                             step, cfg.box_lo, cfg.box_hi, rth, ranges, [(e, s)])[0])
+            return sens_cache[(e, s)]
+        bad, cnt = PU.t6_tracks((th[e], Rg[e], ts[e, :tc[e]], gmem[e]), (rth[e], rR[e], ots64[e, :otc64[e]], rmem[e]),
+                                ranges, cfg.merge_radius, cfg.track_threshold, sensitive)
+        assert not bad, (e, bad, cnt)
+        for k, v in cnt.items():
+            tot[k] = tot.get(k, 0) + v
+    excused = tot["near_R0"] + tot["near_radius"] + tot["sensitive"]
+    PU.report(tag + " T6", **tot, excused_frac=excused / max(1, tot["tracks_ref"]))
+    assert excused <= max(1, T6_EXCUSE_BOUND[(name, step_mult)] * tot["tracks_ref"]), tot
 
 
 def test_T7_merge_synthetic_ties_and_capacity():
@@ -504,22 +517,13 @@ def test_estimate_peaks_vs_oracle(name, ev):
 
 
 # --------------------------------------------------------------------------- NEXT #1: Truncated Newton
-def _newton_seed_sensitive(cfg, h, seed, end, ranges, sig, eta, fsig, mh, evals=None):
-    """T5n sensitivity (oracle-side): the oracle run from the seed perturbed at fp32 resolution --
-    +-1 ulp on every axis, or 4 random-sign draws of 1e-7 x range per axis -- ends more than
-    1e-4 x range from its unperturbed end point (or, with `evals`, spends another number of
-    response evaluations).  fp32 arithmetic perturbs the GPU trajectory by that much, so such a
-    seed may legitimately end elsewhere."""
-    rng = np.random.default_rng(int(np.float32(seed).view(np.uint32).sum()))
-    trials = [np.nextafter(seed, np.float32(sgn * np.inf)).astype(np.float32) for sgn in (+1, -1)]
-    trials += [(seed.astype(np.float64) + rng.choice([-1.0, 1.0], len(ranges)) * 1e-7 * ranges).astype(np.float32)
-               for _ in range(4)]
-    for t in trials:
-        t2, _, _, n2 = ora.newton(cfg.model, [0, len(h)], h, t[None, None], sig, eta, fsig, mh, cfg.box_lo,
-                                  cfg.box_hi, want_grad=False, want_evals=True)
-        if np.any(np.abs(t2[0, 0] - end) > 1e-4 * ranges) or (evals is not None and n2[0, 0] != evals):
-            return True
-    return False
+T5N_EXCUSE_BOUND = {"cfg2": 0.012, "cfg3": 0.02, "cfg4": 0.05}  # see T5_EXCUSE_BOUND
+# measured (round 2, fp64 CG): cfg2 0.0054, cfg3 0.0068 / 0.0096 (512 / 8192 seeds), cfg4 0.027 / 0.018
+# (256 / 16,384 seeds), most by the near-tie flip rule (seeds in empty regions whose Armijo tests
+# compare R ~ 1e-200 in fp64 with R = 0 in fp32)
+T6N_EXCUSE_BOUND = {"cfg2": 0.05, "cfg3": 0.05, "cfg4": 0.12}
+# measured: 0/48, 0/0, 0/3; cfg4 1/6 and 19/331 -- cfg4's q = 3 Newton steps leave every candidate a
+# single-seed cluster, so each excused far seed with R >= R0 is an unmatched track on both sides
 
 
 @pytest.mark.parametrize("name,n_ev,n_seeds", [("cfg2", 4, 512), ("cfg3", 2, 512), ("cfg3", 2, 8192),
@@ -543,23 +547,11 @@ def test_newton_multistart_vs_oracle(name, n_ev, n_seeds):
     ne = ne_d.cpu().numpy()
     assert np.all(ne >= 2 * len(sig) + 1) and np.all(ne <= len(sig) * (mh + 2) + 1)
     ranges = np.array(cfg.box_hi, np.float64) - np.array(cfg.box_lo, np.float64)
-    mism = np.argwhere((ne != rne) & (margin > 1e-4))
-    assert len(mism) <= 0.05 * ne.size, len(mism)
-    for e, s in mism:
-        assert _newton_seed_sensitive(cfg, b.event_hits(e), seeds[e, s], rth[e, s], ranges, sig, eta, fsig, mh,
-                                      evals=rne[e, s]), (e, s, ne[e, s], rne[e, s], margin[e, s])
-    dev_rel = np.max(np.abs(th.astype(np.float64) - rth) / ranges, axis=2)
-    bad = np.argwhere(dev_rel > 1e-3)
-    for e, s in bad:
-        # T5 near-tie rule for the Newton path: a seed may differ when one of its
-        # discrete decisions (Armijo accept / CG curvature sign) was within 1e-4 relative in the
-        # oracle -- inside what fp32 R (T1: 1e-5) and fp32 H can move -- or when the oracle end
-        # point itself moves under a +-1 ulp nudge of the seed
-        if margin[e, s] <= 1e-4:
-            continue
-        assert _newton_seed_sensitive(cfg, b.event_hits(e), seeds[e, s], rth[e, s], ranges, sig, eta, fsig, mh), \
-            (e, s, th[e, s], rth[e, s], margin[e, s])
-    assert len(bad) <= 0.10 * th.shape[0] * th.shape[1]  # gross-bug guard; every one is excused above
+    unexcused, st, excused_set = PU.t5n_states(cfg.model, cfg.box_lo, cfg.box_hi, b, seeds, sig, eta, fsig, mh, th,
+                                               rth, ranges, ne, rne, R_ref=rR, R0=cfg.track_threshold)
+    PU.report(f"T5n {name} E={n_ev} S={n_seeds}", **st)
+    assert not unexcused, unexcused[:5]
+    assert st["excused_frac"] <= T5N_EXCUSE_BOUND[name], st
     assert np.all(th >= np.float32(cfg.box_lo)) and np.all(th <= np.float32(cfg.box_hi))
     rng = np.random.default_rng(1)
     for e in range(n_ev):
@@ -575,6 +567,30 @@ def test_newton_multistart_vs_oracle(name, n_ev, n_seeds):
     assert np.array_equal(tc.cpu().numpy(), otc)
     if name == "cfg2":  # vertex at the origin: the pattern model is exact and tracks are found
         assert np.all(otc > 0)
+    # T6 on the Newton path: GPU and oracle track sets match one to one; a track is excused only
+    # by the named rules (near R0, near the radius, all members excused by the T5n rules)
+    tc = tc.cpu().numpy()
+    _, _, gts, _, gtc, gmem = ora.merge(th.astype(np.float64), Rg.astype(np.float64), cfg.merge_radius,
+                                        cfg.track_threshold, cfg.track_capacity, want_members=True)
+    _, _, rts, _, rtc, rmem = ora.merge(rth, rR, cfg.merge_radius, cfg.track_threshold, cfg.track_capacity,
+                                        want_members=True)
+    tot = {}
+    for e in range(n_ev):
+        def excused_seed(s, e=e):
+            if (e, s) in excused_set:      # already attributed by T5n (flip or sensitivity)
+                return True
+            ok, _ = PU.newton_flip_explains(cfg.model, cfg.box_lo, cfg.box_hi, b.event_hits(e), seeds[e, s:s + 1],
+                                            th[e, s:s + 1], None, ranges, sig, eta, fsig, mh)
+            return bool(ok[0]) or PU.newton_sensitive(cfg.model, cfg.box_lo, cfg.box_hi, b.event_hits(e), seeds[e, s],
+                                                      rth[e, s], ranges, sig, eta, fsig, mh)
+        bad, cnt = PU.t6_tracks((th[e], Rg[e], gts[e, :gtc[e]], gmem[e]), (rth[e], rR[e], rts[e, :rtc[e]], rmem[e]),
+                                ranges, cfg.merge_radius, cfg.track_threshold, excused_seed)
+        assert not bad, (e, bad, cnt)
+        for k, v in cnt.items():
+            tot[k] = tot.get(k, 0) + v
+    excused = tot["near_R0"] + tot["near_radius"] + tot["sensitive"]
+    PU.report(f"T6n {name} E={n_ev} S={n_seeds}", **tot)
+    assert excused <= max(1, T6N_EXCUSE_BOUND[name] * tot["tracks_ref"]), tot
 
 
 def test_newton_line_search_queue_deterministic():
@@ -782,3 +798,89 @@ def test_many_events_launch_chunking():
     for s in range(3):
         r, _, _ = ora.point(C.SLOPE2, hits[off[e]:off[e + 1]], seeds[e, s].astype(np.float64), 0.44)
         assert PU.t1_response(float(Rr[e, s]), r)[0]
+
+
+# --------------------------------------------------------------------------- T1/T3/T4 at full BASELINE size vs fp64
+def _t4_restricted(gpu_idx, ref_idx, tie_mask, keep):
+    """Symmetric difference of two sets of flat indices restricted by `keep` (flat bool mask),
+    excusing oracle near-tie cells.  Returns (n_diff, n_excused, unexcused list)."""
+    a = {int(c) for c in gpu_idx if keep[c]}
+    b = {int(c) for c in ref_idx if keep[c]}
+    diff = a ^ b
+    bad = [c for c in diff if not tie_mask[c]]
+    return len(diff), len(diff) - len(bad), bad
+
+
+def test_T1_T3_T4_full_cfg3_events_vs_fp64_oracle():
+    """Whole 1024 x 1024 cfg3 grids (steps ii-iii; SURVEY §8(d) parity sample)
+    from the default grid kernel, compared with the full fp64 oracle grid: T1 on every cell, T3
+    bit-exact peaks both ways (GPU grid and oracle grid rounded to fp32), T4 peak sets from the
+    fp32 and fp64 grids equal up to oracle near-ties, at R0 = 2.5 and R0 = 0."""
+    cfg = C.CFG3
+    ev = [0, 4999, 9998]
+    b = G.make_batch(cfg, ev)
+    nodes = G.axis_nodes(cfg)
+    g = gpu_grid(b, cfg, nodes)                                     # AUTO: the bench's kernel
+    ref = ora.grid(cfg.model, b.offsets, b.hits, nodes, cfg.sigma)  # 3 x 1.05e9 pairs in fp64
+    ok, worst = PU.t1_response(g, ref)
+    assert ok, worst
+    stats = {"cells": int(ref.size), "t1_worst": worst}
+    for thr, cap in ((cfg.peak_threshold, cfg.peak_capacity), (0.0, 1 << 20)):
+        idx, val, cnt = R.retina_find_peaks(dev(g), 2, thr, cap)
+        r32 = ref.astype(np.float32)
+        idx2, val2, cnt2 = R.retina_find_peaks(dev(r32), 2, thr, cap)
+        torch.cuda.synchronize()
+        idx, cnt, idx2, cnt2 = idx.cpu().numpy(), cnt.cpu().numpy(), idx2.cpu().numpy(), cnt2.cpu().numpy()
+        for grid32, i_, c_ in ((g, idx, cnt), (r32, idx2, cnt2)):         # T3 both ways
+            ri, rv, rc = ora.peaks(grid32.astype(np.float64), 2, thr, cap)
+            assert np.array_equal(c_, rc)
+            for e in range(len(ev)):
+                assert np.array_equal(i_[e, :min(rc[e], cap)], ri[e, :min(rc[e], cap)])
+        n_diff = n_exc = n_pk = 0
+        for e in range(len(ev)):
+            assert cnt[e] <= cap
+            ok, nd, ne = PU.t4_peak_sets(idx[e], cnt[e], ref[e], 2, thr, cap)
+            assert ok, (e, thr, nd, ne)
+            n_diff, n_exc, n_pk = n_diff + nd, n_exc + ne, n_pk + int(cnt[e])
+        stats[f"R0={thr}"] = {"peaks": n_pk, "sym_diff": n_diff, "excused_near_tie": n_exc}
+        if thr > 0:
+            assert n_pk > 20   # 52 strict maxima with R >= 2.5 in these three events
+    PU.report("T1/T3/T4 cfg3 full 1024^2 x 3 events", **stats)
+
+
+def test_T1_T4_full_cfg4_slab_vs_fp64_oracle():
+    """cfg4 (256^3 SLOPE3): the default grid kernel's full grid, compared on a 256 x 256 x 34 slab
+    of z0 nodes around a true vertex with the fp64 oracle: T1 on every slab cell; T4 (3 x 3 x 3
+    strict maxima from the fp32 and fp64 grids) on the slab's 32 interior z0 planes, where every
+    cell's 26 neighbours lie inside the slab."""
+    cfg = C.CFG4
+    nodes = G.axis_nodes(cfg)
+    stats = {}
+    for e_id in (0, 1):
+        b = G.make_batch(cfg, [e_id])
+        g = gpu_grid(b, cfg, nodes)[0]
+        z0 = float(b.truth[0][0, 2])
+        kc = int(np.clip(np.argmin(np.abs(nodes[2] - z0)), 17, len(nodes[2]) - 18))
+        k0, k1 = kc - 17, kc + 17                                     # slab node range [k0, k1)
+        ref = ora.grid(cfg.model, b.offsets, b.hits, [nodes[0], nodes[1], nodes[2][k0:k1]], cfg.sigma)[0]
+        ok, worst = PU.t1_response(g[:, :, k0:k1], ref)
+        assert ok, (e_id, worst)
+        cap = 1 << 20
+        for thr in (cfg.peak_threshold, 0.0):
+            idx, _, cnt = R.retina_find_peaks(dev(g[None]), 3, thr, cap)
+            torch.cuda.synchronize()
+            gi = idx.cpu().numpy()[0, :int(cnt[0])]
+            ci = np.array(np.unravel_index(gi, g.shape)).T
+            inside = (ci[:, 2] >= k0 + 1) & (ci[:, 2] < k1 - 1)
+            # GPU peaks in the interior planes, as flat indices of the slab
+            gpu_slab = np.ravel_multi_index((ci[inside, 0], ci[inside, 1], ci[inside, 2] - k0), ref.shape)
+            ri, _, rc = ora.peaks(ref[None], 3, thr, cap)
+            keep = np.zeros(ref.shape, bool)
+            keep[:, :, 1:-1] = True
+            tie = PU.near_tie_cells(ref, 3, thr).ravel()
+            nd, ne, bad = _t4_restricted(gpu_slab, ri[0, :rc[0]], tie, keep.ravel())
+            assert not bad, (e_id, thr, nd, ne, bad[:5])
+            stats[f"event {e_id} R0={thr}"] = {"peaks_interior": int(inside.sum()), "sym_diff": nd,
+                                               "excused_near_tie": ne}
+        stats[f"event {e_id} t1_worst"] = worst
+    PU.report("T1/T4 cfg4 256x256x34 slab", **stats)
