@@ -2,22 +2,29 @@
 """Benchmark of the Artificial Retina hot path on B200 (one process per GPU).
 
 A step = one pass of the whole hot path over this rank's
-event batch: grid response + peak finding (grid AR) and multi-start
-fixed-step ascent + merging (Algorithm 1), then the one result gather.
+event batch: grid response + peak finding + sub-cell estimates (grid AR) and
+multi-start fixed-step ascent + merging (Algorithm 1), then the rank's result
+record (retina_pack_results) and the one all_gather.
 
-Workload (default): BASELINE.json configs[3] ("Run-3-like batch"), 10,000 events per
-rank with distinct event ids (weak scaling: per-GPU work fixed as N grows), 1024^2 grid,
-8192 seeds x 50 iterations.  Metric: unit.hit evaluations/s (whole job), plus events/s.
+Workload (default): BASELINE.json configs[3] ("Run-3-like batch"): 10,000 events, 1024^2 grid,
+8192 seeds x 50 iterations.  At N GPUs the SAME 10,000 events are sharded (strong scaling,
+SURVEY.md §8(e): rank r owns [r E / N, (r + 1) E / N)); --scaling weak gives every rank its own
+--events-per-rank events instead.  Metric: unit.hit evaluations/s (whole job), plus events/s.
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--scaling strong|weak]
     python -m torch.distributed.run --nproc-per-node N --master-addr 127.0.0.1 bench.py --gpus N
+
+`--gpus N` without a torchrun environment launches the N ranks itself (torch.distributed.run,
+127.0.0.1); NCCL's INIT log is left on (stderr) so the communicator lines show the N ranks.
 """
 from __future__ import annotations
 
 import argparse
 import json
 import os
+import socket
 import statistics
+import subprocess
 import sys
 import threading
 import time
@@ -51,7 +58,11 @@ def args_():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="cfg3")
-    ap.add_argument("--events-per-rank", type=int, default=None)
+    ap.add_argument("--scaling", default="strong", choices=["strong", "weak"],
+                    help="strong: the config's batch sharded over the ranks (default); weak: --events-per-rank "
+                         "events on every rank")
+    ap.add_argument("--events", type=int, default=None, help="strong scaling: total events (default: the config's)")
+    ap.add_argument("--events-per-rank", type=int, default=None, help="weak scaling: events per rank")
     ap.add_argument("--chunk-events", type=int, default=1024)
     ap.add_argument("--grid-buffer-gb", type=float, default=5.0, help="device memory for the per-chunk response grids")
     ap.add_argument("--dense", action="store_true",
@@ -61,12 +72,79 @@ def args_():
                     help="peak scan of grid chunk c on a second stream while chunk c+1 is computed")
     ap.add_argument("--e2e-steps", type=int, default=None)
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--cpu-sample-events", type=int, default=3)
+    ap.add_argument("--cpu-sample-events", type=int, default=3, help="--impl reference: events per step")
+    ap.add_argument("--cpu-plan", default="declared", choices=["declared", "quick"],
+                    help="cpu_baseline sample: the SURVEY.md §8(d) declared subsample, or 1 event per phase (tests)")
     ap.add_argument("--no-graph", dest="graph", action="store_false",
                     help="skip the CUDA-graph replay measurement")
     ap.add_argument("--update", default="gradient", choices=["gradient", "newton"],
                     help="multi-start update: BASELINE fixed-step ascent, or the paper's Truncated Newton")
+    ap.add_argument("--dist-check", action="store_true",
+                    help="no GPU work: initialise the process group (gloo without CUDA), shard the batch, "
+                         "all_gather each rank's event range and hit count, rank 0 prints them (launcher test)")
     return ap.parse_args()
+
+
+def _free_port() -> int:
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def maybe_spawn(a):
+    """`--gpus N` outside torchrun: launch N ranks with torch.distributed.run and return its exit
+    code; inside torchrun the world size must equal --gpus.  Returns None when this process is a rank."""
+    ws = os.environ.get("WORLD_SIZE")
+    if ws is None:
+        if a.gpus <= 1:
+            return None
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={a.gpus}",
+               "--master-addr", "127.0.0.1", f"--master-port={_free_port()}", os.path.abspath(__file__)] + sys.argv[1:]
+        env = dict(os.environ)
+        env.setdefault("NCCL_DEBUG", "INFO")
+        env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+        return subprocess.call(cmd, env=env)
+    if int(ws) != a.gpus:
+        raise SystemExit(f"--gpus {a.gpus} but WORLD_SIZE={ws}: launch one rank per GPU")
+    return None
+
+
+def rank_events(a, cfg, rank: int, world: int):
+    """This rank's event ids and the scaling mode."""
+    from paper_1709_08610_b200 import dist as D
+    if a.scaling == "weak":
+        E = a.events_per_rank or cfg.n_events
+        return range(rank * E, (rank + 1) * E), "weak"
+    n_total = a.events or cfg.n_events
+    if n_total < world:  # single-event configs (cfg0, cfg1): replicas only
+        return range(n_total), "replicas"
+    return range(*D.shard(n_total, rank, world)), "strong"
+
+
+def dist_check(a):
+    import torch
+    import torch.distributed as dist
+    from paper_1709_08610_b200 import dist as D
+    rank, world, _ = D.env()
+    if world > 1:
+        dist.init_process_group("gloo")
+    cfg = C.get_config(a.config)
+    ids, mode = rank_events(a, cfg, rank, world)
+    b = G.make_batch(cfg, ids)
+    mine = torch.tensor([rank, ids.start, ids.stop, b.n_hits], dtype=torch.int64)
+    allr = [torch.zeros_like(mine) for _ in range(world)]
+    if world > 1:
+        dist.all_gather(allr, mine)
+    else:
+        allr = [mine]
+    if rank == 0:
+        print(json.dumps({"dist_check": True, "world": world, "scaling": mode,
+                          "shards": [x.tolist() for x in allr]}), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
 
 
 def make_spec(cfg):
@@ -128,6 +206,13 @@ class ClockSampler:
 
 
 # ----------------------------------------------------------------------------- CPU oracle
+def _grid_plan(cfg, n_events, z_planes=None):
+    nodes = G.axis_nodes(cfg)
+    if z_planes is not None and cfg.P == 3:  # a bounded slab of the z0 axis (1-core cfg4 sample)
+        nodes = nodes[:2] + [nodes[2][:z_planes]]
+    return nodes
+
+
 def oracle_sample(cfg, n_events: int):
     """The fp64 oracle, as it stands, on a bounded sample of the same workload: the full
     grid + peaks of `n_events` events and their full multi-start + merge."""
@@ -155,6 +240,80 @@ def oracle_sample(cfg, n_events: int):
                       f"peaks and {cfg.n_seeds} seeds x {cfg.n_iters + 1} passes + merge; {pairs:.3e} pairs"}
 
 
+# SURVEY.md §8(d) "Oracle timing": declared subsamples (events for the grid phase, events for the
+# multi-start phase) on all cores and on 1 core; cfg0-2 run in full on all cores.
+CPU_PLAN = {"cfg0": ((1, 1), (1, 1, None)), "cfg1": ((1, 0), (1, 0, None)), "cfg2": ((0, 200), (0, 16, None)),
+            "cfg3": ((16, 64), (1, 4, None)), "cfg4": ((2, 16), (1, 1, 16))}
+
+
+def cpu_model() -> str:
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def oracle_phases(cfg, grid_events: int, ms_events: int, threads: int, z_planes=None):
+    """Times the oracle's grid+peaks phase and multi-start+merge phase on `threads` OpenMP threads."""
+    from oracle import oracle as ora
+    ora.set_num_threads(threads)
+    out = {"threads": threads}
+    if grid_events and cfg.axes:
+        ev = list(range(grid_events))
+        b = G.make_batch(cfg, ev)
+        nodes = _grid_plan(cfg, grid_events, z_planes)
+        cells = int(np.prod([len(n) for n in nodes]))
+        t0 = time.perf_counter()
+        g = ora.grid(cfg.model, b.offsets, b.hits, nodes, cfg.sigma)
+        ora.peaks(g, cfg.P, cfg.peak_threshold, cfg.peak_capacity)
+        dt = time.perf_counter() - t0
+        pairs = float(b.n_hits) * cells
+        out["grid"] = {"events": grid_events, "cells_per_event": cells, "pairs": pairs, "seconds": dt,
+                       "pairs_per_s": pairs / dt, "pairs_per_s_per_core": pairs / dt / threads,
+                       "seconds_per_full_event": dt / grid_events * cfg.n_units / cells}
+    if ms_events and cfg.n_seeds:
+        ev = list(range(ms_events))
+        b = G.make_batch(cfg, ev)
+        seeds = G.make_seeds(cfg, ev)
+        t0 = time.perf_counter()
+        th, R, _ = ora.multistart(cfg.model, b.offsets, b.hits, seeds, cfg.sigma, cfg.n_iters, cfg.step,
+                                  cfg.box_lo, cfg.box_hi, want_grad=False)
+        ora.merge(th, R, cfg.merge_radius, cfg.track_threshold, cfg.track_capacity)
+        dt = time.perf_counter() - t0
+        pairs = float(b.n_hits) * cfg.n_seeds * (cfg.n_iters + 1)
+        out["multistart"] = {"events": ms_events, "pairs": pairs, "seconds": dt, "pairs_per_s": pairs / dt,
+                             "pairs_per_s_per_core": pairs / dt / threads, "seconds_per_event": dt / ms_events}
+    ph = [out[k] for k in ("grid", "multistart") if k in out]
+    out["pairs_per_s"] = sum(p["pairs"] for p in ph) / sum(p["seconds"] for p in ph)
+    # whole-config events/s extrapolated from the per-event phase times
+    per_ev = (out["grid"]["seconds_per_full_event"] if "grid" in out else 0.0) + \
+             (out["multistart"]["seconds_per_event"] if "multistart" in out else 0.0)
+    out["events_per_s"] = 1.0 / per_ev
+    return out
+
+
+def cpu_baseline(cfg, plan: str = "declared"):
+    all_cores = len(os.sched_getaffinity(0))
+    (ga, ma), (g1, m1, zp) = CPU_PLAN.get(cfg.name, ((1, 1), (1, 1, None)))
+    if plan == "quick":
+        ga, ma, g1, m1, zp = min(ga, 1), min(ma, 1), 0, min(m1, 1), None
+    full = oracle_phases(cfg, ga, ma, all_cores)
+    one = oracle_phases(cfg, g1, m1, 1, z_planes=zp)
+    desc = []
+    if "grid" in full:
+        desc.append(f"grid+peaks: {ga} full event(s) on {all_cores} threads, "
+                    f"{g1} event(s){f' x {zp} z0 planes' if zp else ''} on 1")
+    if "multistart" in full:
+        desc.append(f"multi-start ({cfg.n_seeds} seeds x {cfg.n_iters + 1} passes) + merge: {ma} event(s) on "
+                    f"{all_cores} threads, {m1} on 1")
+    return {"value": full["pairs_per_s"], "unit": UNIT, "cores": all_cores, "kind": "oracle",
+            "sample": f"{cfg.name} (SURVEY.md §8(d) declared subsample): " + "; ".join(desc),
+            "cpu_model": cpu_model(), "events_per_s": full["events_per_s"], "all_cores": full, "one_core": one}
+
+
 def run_reference(a):
     rank, world, _ = (int(os.environ.get(k, d)) for k, d in (("RANK", 0), ("WORLD_SIZE", 1), ("LOCAL_RANK", 0)))
     if rank != 0:
@@ -163,6 +322,8 @@ def run_reference(a):
     # the host's cores (read by OpenMP when the oracle library is first loaded, just below)
     os.environ["OMP_NUM_THREADS"] = str(len(os.sched_getaffinity(0)))
     cfg = C.get_config(a.config, dense=True) if a.dense else C.get_config(a.config)
+    from oracle import oracle as ora
+    ora.set_num_threads(len(os.sched_getaffinity(0)))
     steps = []
     for _ in range(a.warmup + a.steps):
         steps.append(oracle_sample(cfg, a.cpu_sample_events))
@@ -170,11 +331,12 @@ def run_reference(a):
     value = statistics.median(s["value"] for s in timed)
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": a.gpus,
             "steps": a.steps, "warmup": a.warmup, "ms_per_step": 1e3 * statistics.median(s["seconds"] for s in timed),
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "higher_is_better": True, "scaling": a.scaling, "vs_baseline": None, "dtype": "f64",
             "data": "synthetic", "config": {"workload": f"{cfg.name} (bounded sample, CPU oracle)",
                                             "events_per_step": a.cpu_sample_events},
             "events_per_s": statistics.median(s["events_per_s"] for s in timed),
-            "cpu_baseline": {k: timed[-1][k] for k in ("kind", "cores", "sample")} | {"value": value, "unit": UNIT},
+            "cpu_baseline": {k: timed[-1][k] for k in ("kind", "cores", "sample")} | {"value": value, "unit": UNIT,
+                                                                                  "cpu_model": cpu_model()},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -184,6 +346,11 @@ def main():
     a = args_()
     if a.impl == "reference":
         return run_reference(a)
+    rc = maybe_spawn(a)
+    if rc is not None:
+        sys.exit(rc)
+    if a.dist_check:
+        return dist_check(a)
     import torch
     import torch.distributed as dist
 
@@ -194,11 +361,13 @@ def main():
     rank, world, local = D.env()
     torch.cuda.set_device(local)
     if world > 1:
+        os.environ.setdefault("NCCL_DEBUG", "INFO")   # communicator INIT lines (stderr) show the ranks
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     RT.lib()  # fail loudly if the native library is missing
     cfg = C.get_config(a.config, dense=True) if a.dense else C.get_config(a.config)
-    E = a.events_per_rank or cfg.n_events
-    ev_ids = range(rank * E, (rank + 1) * E)  # weak scaling: distinct events per rank
+    ev_ids, scaling = rank_events(a, cfg, rank, world)
+    E = len(ev_ids)
     t0 = time.perf_counter()
     batch = G.make_batch(cfg, ev_ids)
     seeds = G.make_seeds(cfg, ev_ids)
@@ -217,12 +386,15 @@ def main():
         torch.cuda.synchronize()
     pairs_grid, pairs_ms = pipe.pairs(dbatch)
     keep = 64
+    hdr = D.header_words(rank, ev_ids.start, E, pairs_grid, pairs_ms)
+    pack_out = torch.empty((RT.PACK_HEADER + E * D.record_width(spec.P, keep),), dtype=torch.int32, device="cuda")
 
-    def step(b, timer=None, t_ms=0.0):
+    def step(b, timer=None):
         pipe.run(b, stream=stream, timer=timer)
+        # the rank's result record, written on the device (retina_pack_results), then THE gather
         buf = D.pack(pipe.peak_idx[:E], pipe.peak_val[:E], pipe.peak_cnt[:E], pipe.t_theta[:E], pipe.t_resp[:E],
-                     pipe.t_size[:E], pipe.t_count[:E], keep,
-                     [rank, rank * E, E, 0, 0, t_ms, pairs_grid / 1e9, pairs_ms / 1e9])
+                     pipe.t_size[:E], pipe.t_count[:E], keep, hdr, out=pack_out, stream=stream)
+        pipe.launches += 2
         return D.gather(buf, world)
 
     for _ in range(a.warmup):
@@ -238,19 +410,30 @@ def main():
         ev0.record(stream)
         for _ in range(a.steps):
             gathered = step(dbatch, timer)
+            timer.next_step()
         ev1.record(stream)
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
     ms = ev0.elapsed_time(ev1)
     launches = pipe.launches
-    phase_ms = timer.totals_ms()
+    per_step = timer.per_step_ms()
+    phase_med = {k: statistics.median(v) for k, v in per_step.items()}
     phase_n = timer.counts()
-    t = torch.tensor([ms], device="cuda")
+
+    # ---- per-rank timings and work, gathered once after the timed region; the step time is the max
+    mine = torch.tensor([float(rank), float(E), ms, pairs_grid, pairs_ms]
+                        + [phase_med.get(k, 0.0) for k in ("grid", "peaks", "multistart", "merge")],
+                        dtype=torch.float64, device="cuda")
+    ranks = [mine]
     if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    ms_max = float(t.item())
+        ranks = [torch.empty_like(mine) for _ in range(world)]
+        dist.all_gather(ranks, mine)
+    ranks = [r.cpu().tolist() for r in ranks]
+    ms_max = max(r[2] for r in ranks)
     ms_step = ms_max / a.steps
+    pairs_all = sum(r[3] + r[4] for r in ranks)
+    events_all = sum(r[1] for r in ranks)
 
     # ---- the same hot path replayed from a CUDA graph (all kernel launches of one pass)
     graph_ms = None
@@ -275,7 +458,7 @@ def main():
     off_h = torch.from_numpy(batch.offsets).pin_memory()
     hits_h = torch.from_numpy(batch.hits).pin_memory()
     seeds_h = torch.from_numpy(seeds).pin_memory()
-    res_h = torch.empty(gathered.shape, dtype=torch.float32).pin_memory()
+    res_h = torch.empty(gathered.shape, dtype=gathered.dtype).pin_memory()
     h2d = off_h.numel() * 4 + hits_h.numel() * 4 + seeds_h.numel() * 4
     d2h = res_h.numel() * 4
     # two device copies of the inputs: the H2D copy of step i+1 (copy stream) overlaps the
@@ -322,6 +505,8 @@ def main():
     if world > 1:
         dist.all_reduce(t2, op=dist.ReduceOp.MAX)
     e2e_ms_step = float(t2.item()) / e2e_steps
+    # the gathered records decode to every rank's event range (checked on rank 0)
+    dec = D.unpack(gathered.cpu().numpy(), spec.P, keep)
 
     if rank != 0:
         if world > 1:
@@ -342,9 +527,9 @@ def main():
             traffic = {}
     work = {"grid": pairs_grid, "multistart": pairs_ms}
     roofs = {}
-    for ph in (k for k in phase_ms if k in work):
+    for ph in (k for k in phase_med if k in work):
         n_launch = phase_n[ph] / a.steps
-        avg_ms = phase_ms[ph] / phase_n[ph]
+        avg_ms = phase_med[ph] / n_launch
         per_launch = work[ph] / n_launch
         pairs_s = per_launch / (avg_ms * 1e-3)
         if ph == "grid" and cfg.model in (C.SLOPE2, C.SLOPE3):
@@ -373,7 +558,8 @@ def main():
                  "frac_at_measured_clock": (pairs_s / (N_SM * MUFU_PER_SM_CLK * clk["sm_mhz"] * 1e6)
                                             if clk.get("sm_mhz") else None)}
         r.update({"launch_ms": avg_ms, "pairs_per_launch": per_launch, "pairs_per_s": pairs_s,
-                  "share_of_step": phase_ms[ph] / a.steps / ms_step, "traffic": None})
+                  "share_of_step": phase_med[ph] / ms_step, "traffic": None,
+                  "timing": f"median over {a.steps} steps of the phase's CUDA-event time per step"})
         if ph == "multistart" and a.update == "newton":
             r["work_basis"] = ("pairs = sum over seeds of response evaluations (q Hessian-mode + line-search "
                                "trials + final; counted by the kernel, PAPER.md:200-201 cost unit) x event hits")
@@ -383,34 +569,46 @@ def main():
         roofs[ph] = r
     dom = max(roofs, key=lambda k: roofs[k]["share_of_step"])
     roof = dict(roofs[dom])
-    total_pairs = (pairs_grid + pairs_ms) * world
+    n_total = a.events or cfg.n_events
+    workload = (f"{cfg.name}{' dense (Z12: no acceptance cut)' if a.dense else ''}: BASELINE.json configs[{cfg.name[-1]}], "
+                + (f"{n_total} events sharded over {world} GPU(s)" if scaling == "strong" else
+                   f"{E} events per GPU (ids rank*{E}..)" if scaling == "weak" else
+                   f"{E} event(s) replicated on each of {world} GPU(s)")
+                + (f", {'x'.join(str(x[2]) for x in cfg.axes)} {C.MODEL_NAME[cfg.model].upper()} grid + "
+                   f"{'x'.join(['3'] * cfg.P)} peaks (R0={cfg.peak_threshold}) + sub-cell estimates" if cfg.axes else "")
+                + ((", " + (f"{cfg.n_seeds} seeds x {cfg.n_iters} fixed-step iterations + merge"
+                            if a.update == "gradient" else
+                            f"{cfg.n_seeds} seeds x q=3 Truncated-Newton steps (sigma schedule) + merge"))
+                   if cfg.n_seeds else ""))
     line = {
-        "metric": METRIC, "value": total_pairs / (ms_step * 1e-3), "unit": UNIT, "n_gpus": world,
+        "metric": METRIC, "value": pairs_all / (ms_step * 1e-3), "unit": UNIT, "n_gpus": world,
         "steps": a.steps, "warmup": a.warmup, "ms_per_step": ms_step, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-        "events_per_s": E * world / (ms_step * 1e-3),
-        "config": {"workload": f"{cfg.name}{' dense (Z12: no acceptance cut)' if a.dense else ''}: "
-                               f"BASELINE.json configs[{cfg.name[-1]}], {E} events per GPU "
-                               f"(ids rank*{E}..), {'x'.join(str(x[2]) for x in cfg.axes)} "
-                               f"{C.MODEL_NAME[cfg.model].upper()} grid + {'x'.join(['3'] * cfg.P)} peaks "
-                               f"(R0={cfg.peak_threshold}) + sub-cell estimates, "
-                               + (f"{cfg.n_seeds} seeds x {cfg.n_iters} fixed-step iterations + merge"
-                                  if a.update == "gradient" else
-                                  f"{cfg.n_seeds} seeds x q=3 Truncated-Newton steps (sigma schedule) + merge"),
-                   "events_per_rank": E, "hits_per_event_mean": float(batch.n_hits) / E,
+        "scaling": scaling, "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "events_per_s": events_all / (ms_step * 1e-3),
+        "config": {"workload": workload,
+                   "events_total": int(events_all), "events_per_rank": [int(r[1]) for r in ranks],
+                   "hits_per_event_mean": float(batch.n_hits) / max(E, 1),
                    "pairs_grid_per_rank": pairs_grid, "pairs_multistart_per_rank": pairs_ms,
-                   "l2": "inputs > L2 (hits %.0f MB, seeds %.0f MB, grid writes %.1f GB per step)" % (
+                   "l2": "inputs > L2 (hits %.0f MB, seeds %.0f MB, grid writes %.1f GB per step per rank)" % (
                        batch.hits.nbytes / 1e6, seeds.nbytes / 1e6, 4.0 * cfg.n_units * E / 1e9),
-                   "parallelism": f"dp{world} (events sharded, 1 all_gather of results)",
+                   "parallelism": f"dp{world} (events sharded, 1 all_gather of device-packed results)",
                    "arithmetic": ("fp32; the grid contraction as three fp16 tensor-core products of an exact "
                                   "hi/lo split of each fp32 factor, accumulated in fp32 (fp32-level accuracy, "
                                   "T1 1e-5)" if cfg.model in (C.SLOPE2, C.SLOPE3) else "fp32"),
                    "grid_chunk_events": pipe.chunk},
-        "phases_ms_per_step": {k: v / a.steps for k, v in phase_ms.items()},
+        "phases_ms_per_step": phase_med,
+        "phases_ms_per_step_all_steps": per_step,
+        "per_rank": [{"rank": int(r[0]), "events": int(r[1]), "ms_per_step": r[2] / a.steps,
+                      "pairs": r[3] + r[4], "phases_ms": dict(zip(("grid", "peaks", "multistart", "merge"), r[5:]))}
+                     for r in ranks],
+        "gathered": {"ranks": [d["rank"] for d in dec], "event_base": [d["event_base"] for d in dec],
+                     "peaks_total": sum(d["peaks_total"] for d in dec),
+                     "tracks_total": sum(d["tracks_total"] for d in dec),
+                     "record_bytes_per_rank": int(pack_out.numel() * 4)},
         "roofline": roof,
         "roofline_kernels": roofs,
         "clocks": clk,
-        "e2e": {"value": total_pairs / (e2e_ms_step * 1e-3), "unit": UNIT, "h2d_bytes_per_step": h2d,
+        "e2e": {"value": pairs_all / (e2e_ms_step * 1e-3), "unit": UNIT, "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms_step},
         "gpu_launches": launches,
         "cuda_graph": (None if graph_ms is None else
@@ -420,7 +618,7 @@ def main():
         "gen_seconds": gen_s,
     }
     if world == 1 and not a.no_cpu_baseline:
-        line["cpu_baseline"] = oracle_sample(cfg, a.cpu_sample_events)
+        line["cpu_baseline"] = cpu_baseline(cfg, a.cpu_plan)
     print(json.dumps(line), flush=True)
     if world > 1:
         dist.barrier()

@@ -20,7 +20,8 @@
  *   retina_find_peaks_ws        step (iii) by many CTAs per event (caller workspace);
  *   retina_estimate_peaks       step (iv): sub-cell parameter estimate per peak;
  *   retina_multistart_newton    Algorithm 1 with the paper's Truncated-Newton update and sigma
- *   (_ex)                       schedule, PAPER.md:213-216 (+ per-seed evaluation counts).
+ *   (_ex)                       schedule, PAPER.md:213-216 (+ per-seed evaluation counts);
+ *   retina_pack_results         the per-rank record of the one multi-GPU result gather.
  *
  * Track models and the distance s:
  *   RETINA_LINE2D  P=2, theta=(a, b),       hit (x, y, -, -):  s   = y - (a x + b)
@@ -230,6 +231,29 @@ int retina_merge_tracks(int32_t n_events, int32_t n_seeds, int32_t P, const floa
                         int32_t capacity, float *track_theta, float *track_response,
                         int32_t *track_seed, int32_t *track_size, int32_t *track_count,
                         void *stream);
+
+/* The per-rank result record of the one multi-GPU gather (north
+ * star: "one NCCL gather over NVLink for found tracks and timings only"): packs the first
+ * `keep` peaks and tracks of every event and the rank's header into a fixed-size buffer of
+ * 32-bit words that the caller all-gathers (fp32 fields as bit patterns, so the record is exact):
+ *   out[0 .. RETINA_PACK_HEADER): header[] as given, except out[3] = sum of peak_count and
+ *       out[4] = sum of track_count (computed on the device; saturate at 2^32 - 1);
+ *   then per event e, RETINA_PACK_WORDS(P, keep) words: peak_count[e], track_count[e],
+ *       keep peak indices (-1 past min(count, capacity)), keep peak values (fp32 bits, 0 past),
+ *       keep x (track_theta[P], track_response (fp32 bits), track_size) (0 past).
+ *   n_events >= 0, P in {2, 3}, keep >= 0, capacities >= 0; peak_* / track_* are the device
+ *   outputs of retina_find_peaks and retina_merge_tracks (layouts as there); header: host
+ *   [RETINA_PACK_HEADER] (rank, event base, n_events, -, -, pairs_grid/1e9 and
+ *   pairs_multistart/1e9 as fp32 bits, 0); out: device, RETINA_PACK_HEADER +
+ *   n_events * RETINA_PACK_WORDS(P, keep) words, caller-owned.  NULL pointers or negative sizes
+ *   -> RETINA_EINVAL.  Deterministic. */
+#define RETINA_PACK_HEADER 8
+#define RETINA_PACK_WORDS(P, keep) (2 + 2 * (keep) + (keep) * ((P) + 2))
+int retina_pack_results(int32_t n_events, int32_t P, int32_t keep, const int32_t *peak_index,
+                        const float *peak_value, const int32_t *peak_count, int32_t peak_capacity,
+                        const float *track_theta, const float *track_response, const int32_t *track_size,
+                        const int32_t *track_count, int32_t track_capacity, const uint32_t *header,
+                        uint32_t *out, void *stream);
 
 /* Static description of a status code. */
 const char *retina_status_string(int status);

@@ -49,6 +49,16 @@ int ora_num_threads(void) {
 #endif
 }
 
+/* Thread count of the following parallel loops (bench.py times the oracle on 1 core and on
+ * all cores); no effect on any result. */
+void ora_set_num_threads(int n) {
+#ifdef _OPENMP
+    if (n > 0) omp_set_num_threads(n);
+#else
+    (void)n;
+#endif
+}
+
 /* R, grad R and A_i = sum_k |d_i t_k| at one theta (Eq. 1 and its gradient).
  *
  * With t_k = exp(-s_k^2 / sigma^2):

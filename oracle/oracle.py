@@ -38,6 +38,8 @@ def lib():
         P = ctypes.c_void_p
         i, d = ctypes.c_int, ctypes.c_double
         L.ora_num_threads.restype = i
+        L.ora_set_num_threads.argtypes = [i]
+        L.ora_set_num_threads.restype = None
         L.ora_point.argtypes = [i, P, i, d, P, d, P, P, P]
         L.ora_grid.argtypes = [i, i, P, P, d, d, P, P, P, P, P]
         L.ora_peaks.argtypes = [P, i, i, P, d, i, P, P, P]
@@ -72,6 +74,11 @@ def _P(model: int) -> int:
 
 def num_threads() -> int:
     return int(lib().ora_num_threads())
+
+
+def set_num_threads(n: int) -> None:
+    """OpenMP threads of the following oracle calls (timing only; results do not depend on it)."""
+    lib().ora_set_num_threads(int(n))
 
 
 def point(model: int, hits, theta, sigma: float, z_ref: float = 0.0):

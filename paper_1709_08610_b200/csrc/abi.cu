@@ -398,4 +398,39 @@ int retina_merge_tracks(int32_t n_events, int32_t n_seeds, int32_t P, const floa
     return RETINA_OK;
 }
 
+int retina_pack_results(int32_t n_events, int32_t P, int32_t keep, const int32_t *peak_index,
+                        const float *peak_value, const int32_t *peak_count, int32_t peak_capacity,
+                        const float *track_theta, const float *track_response, const int32_t *track_size,
+                        const int32_t *track_count, int32_t track_capacity, const uint32_t *header,
+                        uint32_t *out, void *stream) {
+    g_last_error[0] = 0;
+    if (n_events < 0) return fail(RETINA_EINVAL, "n_events < 0");
+    if (P != 2 && P != 3) return fail(RETINA_EINVAL, "P must be 2 or 3 (got %d)", P);
+    if (keep < 0 || peak_capacity < 0 || track_capacity < 0) return fail(RETINA_EINVAL, "negative keep/capacity");
+    if (!header || !out) return fail(RETINA_EINVAL, "header or out is NULL");
+    if (n_events > 0 && (!peak_count || !track_count)) return fail(RETINA_EINVAL, "NULL count pointer");
+    if (n_events > 0 && keep > 0 &&
+        ((peak_capacity > 0 && (!peak_index || !peak_value)) ||
+         (track_capacity > 0 && (!track_theta || !track_response || !track_size))))
+        return fail(RETINA_EINVAL, "NULL device pointer");
+    retina::PackArgs a{};
+    a.n_events = n_events;
+    a.P = P;
+    a.keep = keep;
+    a.peak_index = peak_index;
+    a.peak_value = peak_value;
+    a.peak_count = peak_count;
+    a.peak_cap = peak_capacity;
+    a.track_theta = track_theta;
+    a.track_response = track_response;
+    a.track_size = track_size;
+    a.track_count = track_count;
+    a.track_cap = track_capacity;
+    for (int i = 0; i < RETINA_PACK_HEADER; ++i) a.header[i] = header[i];
+    a.out = out;
+    const cudaError_t err = retina::launch_pack(a, (cudaStream_t)stream);
+    if (err != cudaSuccess) return cuda_fail(err, "retina_pack_results");
+    return RETINA_OK;
+}
+
 }  // extern "C"

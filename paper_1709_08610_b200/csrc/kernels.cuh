@@ -97,6 +97,22 @@ struct EstimateArgs {
     float *theta;
 };
 
+struct PackArgs {
+    int n_events, P, keep;
+    const int32_t *peak_index;
+    const float *peak_value;
+    const int32_t *peak_count;
+    int peak_cap;
+    const float *track_theta;
+    const float *track_response;
+    const int32_t *track_size;
+    const int32_t *track_count;
+    int track_cap;
+    uint32_t header[8];  // RETINA_PACK_HEADER words from the caller; [3], [4] are filled on the device
+    uint32_t *out;
+};
+
+cudaError_t launch_pack(const PackArgs &a, cudaStream_t stream);
 cudaError_t launch_estimate(const EstimateArgs &a, cudaStream_t stream);
 cudaError_t launch_grid_response(int model, const GridArgs &a, int n_events, cudaStream_t stream);
 cudaError_t launch_grid_separable(int model, const GridArgs &a, int n_events, cudaStream_t stream);

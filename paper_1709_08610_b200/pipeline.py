@@ -92,7 +92,8 @@ class RetinaPipeline:
         E, P = max_events, spec.P
         self.peak_idx = torch.empty((E, spec.peak_capacity), dtype=torch.int32, device=self.device)
         self.peak_val = torch.empty((E, spec.peak_capacity), dtype=torch.float32, device=self.device)
-        self.peak_cnt = torch.empty((E,), dtype=torch.int32, device=self.device)
+        # counts start at zero: a config without a grid (or without seeds) reports no peaks (tracks)
+        self.peak_cnt = torch.zeros((E,), dtype=torch.int32, device=self.device)
         self.peak_theta = torch.empty((E, spec.peak_capacity, spec.P), dtype=torch.float32, device=self.device)
         S = spec.n_seeds
         self.theta = torch.empty((E, S, P), dtype=torch.float32, device=self.device)
@@ -103,7 +104,7 @@ class RetinaPipeline:
         self.t_resp = torch.empty((E, spec.track_capacity), dtype=torch.float32, device=self.device)
         self.t_seed = torch.empty((E, spec.track_capacity), dtype=torch.int32, device=self.device)
         self.t_size = torch.empty((E, spec.track_capacity), dtype=torch.int32, device=self.device)
-        self.t_count = torch.empty((E,), dtype=torch.int32, device=self.device)
+        self.t_count = torch.zeros((E,), dtype=torch.int32, device=self.device)
         self.launches = 0
 
     # ------------------------------------------------------------------ accounting
@@ -214,12 +215,17 @@ class RetinaPipeline:
 
 
 class PhaseTimer:
-    """CUDA-event timer per phase on a given stream (sums over launches)."""
+    """CUDA-event timer per phase on a given stream: per step, the sum over the phase's launches;
+    reported as the median over steps (median of >= 5 timed repetitions)."""
 
     def __init__(self, stream):
         self.stream = stream
         self.pending = {}
         self.events: dict = {}
+        self.cur = 0
+
+    def next_step(self):
+        self.cur += 1
 
     def start(self, name, stream=None):
         ev = torch.cuda.Event(enable_timing=True)
@@ -229,10 +235,20 @@ class PhaseTimer:
     def stop(self, name, stream=None):
         ev = torch.cuda.Event(enable_timing=True)
         ev.record(stream or self.stream)
-        self.events.setdefault(name, []).append((self.pending.pop(name), ev))
+        self.events.setdefault(name, []).append((self.pending.pop(name), ev, self.cur))
+
+    def per_step_ms(self):
+        """{phase: [ms of step 0, step 1, ...]} (sum over the phase's launches in each step)."""
+        out = {}
+        for k, v in self.events.items():
+            steps = {}
+            for a, b, st in v:
+                steps[st] = steps.get(st, 0.0) + a.elapsed_time(b)
+            out[k] = [steps[st] for st in sorted(steps)]
+        return out
 
     def totals_ms(self):
-        return {k: sum(a.elapsed_time(b) for a, b in v) for k, v in self.events.items()}
+        return {k: sum(v) for k, v in self.per_step_ms().items()}
 
     def counts(self):
         return {k: len(v) for k, v in self.events.items()}
@@ -240,6 +256,7 @@ class PhaseTimer:
     def reset(self):
         self.events = {}
         self.pending = {}
+        self.cur = 0
 
 
 def upload(offsets: np.ndarray, hits: np.ndarray, seeds: np.ndarray, device="cuda",

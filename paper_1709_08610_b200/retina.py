@@ -25,8 +25,14 @@ GRID_TENSOR_F16_PAIR, GRID_TENSOR_F16_SINGLE = 5, 6
 EXPORTED = ("retina_grid_response", "retina_grid_response_ex", "retina_estimate_peaks", "retina_find_peaks",
             "retina_find_peaks_ws", "retina_find_peaks_workspace_size",
             "retina_multistart_optimize", "retina_multistart_newton", "retina_multistart_newton_ex",
-            "retina_merge_tracks",
+            "retina_merge_tracks", "retina_pack_results",
             "retina_status_string", "retina_last_error", "retina_version")
+PACK_HEADER = 8
+
+
+def pack_words(P: int, keep: int) -> int:
+    """RETINA_PACK_WORDS(P, keep): 32-bit words per event in a retina_pack_results record."""
+    return 2 + 2 * keep + keep * (P + 2)
 
 
 class RetinaError(RuntimeError):
@@ -69,9 +75,10 @@ def lib() -> ctypes.CDLL:
         L.retina_multistart_newton_ex.argtypes = [ctypes.POINTER(retina_events), ctypes.c_int, i32, vp, i32, vp,
                                                   vp, f32, i32, vp, vp, vp, vp, vp, vp, vp]
         L.retina_merge_tracks.argtypes = [i32, i32, i32, vp, vp, vp, f32, i32, vp, vp, vp, vp, vp, vp]
+        L.retina_pack_results.argtypes = [i32, i32, i32, vp, vp, vp, i32, vp, vp, vp, vp, i32, vp, vp, vp]
         for f in (L.retina_grid_response, L.retina_grid_response_ex, L.retina_find_peaks, L.retina_estimate_peaks,
                   L.retina_multistart_optimize, L.retina_multistart_newton, L.retina_multistart_newton_ex,
-                  L.retina_merge_tracks):
+                  L.retina_merge_tracks, L.retina_pack_results):
             f.restype = ctypes.c_int
         L.retina_status_string.argtypes = [ctypes.c_int]
         L.retina_status_string.restype = ctypes.c_char_p
@@ -113,6 +120,20 @@ def _dev(t: torch.Tensor, dtype) -> torch.Tensor:
     return t
 
 
+def _out(name: str, t: Optional[torch.Tensor], dtype, shape, device) -> Optional[torch.Tensor]:
+    """Checks a caller-supplied output buffer before its raw pointer reaches a kernel: CUDA,
+    contiguous, the expected dtype, shape and device (a narrower buffer would be written out
+    of bounds, not rejected, by the device code)."""
+    if t is None:
+        return None
+    _dev(t, dtype)
+    if tuple(t.shape) != tuple(shape):
+        raise ValueError(f"{name}: shape {tuple(t.shape)} expected {tuple(shape)}")
+    if t.device != device:
+        raise ValueError(f"{name}: on {t.device}, inputs on {device}")
+    return t
+
+
 class Events:
     """A device-resident CSR batch: offsets int32 [E+1], hits float32 [N, 4]."""
 
@@ -143,9 +164,10 @@ def retina_grid_response(events: Events, model: int, sigma: float, nodes: Sequen
     nodes = [_dev(n, torch.float32) for n in nodes]
     alen, _k1 = _arr(ctypes.c_int32, [n.numel() for n in nodes])
     nptr, _k2 = _arr(ctypes.c_void_p, [n.data_ptr() for n in nodes])
+    shape = (events.n_events,) + tuple(n.numel() for n in nodes)
     if out is None:
-        out = torch.empty((events.n_events,) + tuple(n.numel() for n in nodes), device=events.hits.device,
-                          dtype=torch.float32)
+        out = torch.empty(shape, device=events.hits.device, dtype=torch.float32)
+    _out("response", out, torch.float32, shape, events.hits.device)
     _check("retina_grid_response_ex",
            lib().retina_grid_response_ex(ctypes.byref(events.c), model, float(sigma), alen, nptr,
                                          _ptr(_dev(out, torch.float32)), int(algorithm), _stream(stream)))
@@ -173,7 +195,13 @@ def retina_find_peaks(response: torch.Tensor, P: int, threshold: float, capacity
                torch.empty((E, capacity), dtype=torch.float32, device=dev),
                torch.empty((E,), dtype=torch.int32, device=dev))
     idx, val, cnt = out
+    _out("peak_index", idx, torch.int32, (E, capacity), response.device)
+    _out("peak_value", val, torch.float32, (E, capacity), response.device)
+    _out("peak_count", cnt, torch.int32, (E,), response.device)
     if workspace is not None:
+        _dev(workspace, workspace.dtype)
+        if workspace.device != response.device:
+            raise ValueError("workspace on another device")
         nbytes = workspace.numel() * workspace.element_size()
         _check("retina_find_peaks_ws",
                lib().retina_find_peaks_ws(_ptr(response), E, P, alen, float(threshold), int(capacity), _ptr(idx),
@@ -195,8 +223,12 @@ def retina_estimate_peaks(response: torch.Tensor, nodes: Sequence[torch.Tensor],
     E, cap = peak_index.shape
     alen, _k1 = _arr(ctypes.c_int32, [n.numel() for n in nodes])
     nptr, _k2 = _arr(ctypes.c_void_p, [n.data_ptr() for n in nodes])
+    if response.dim() != P + 1 or response.shape[0] != E:
+        raise ValueError("response must be [E, n0, ..] with E = peak_index.shape[0]")
+    _out("peak_count", _dev(peak_count, torch.int32), torch.int32, (E,), response.device)
     if out is None:
         out = torch.zeros((E, cap, P), dtype=torch.float32, device=response.device)
+    _out("theta", out, torch.float32, (E, cap, P), response.device)
     _check("retina_estimate_peaks",
            lib().retina_estimate_peaks(_ptr(response), E, P, alen, nptr, _ptr(_dev(peak_index, torch.int32)),
                                        _ptr(_dev(peak_count, torch.int32)), int(cap), _ptr(out), _stream(stream)))
@@ -217,6 +249,9 @@ def retina_multistart_optimize(events: Events, model: int, sigma: float, seeds: 
         out = (torch.empty_like(seeds), torch.empty((E, S), dtype=torch.float32, device=seeds.device),
                torch.empty_like(seeds) if want_grad else None)
     th, R, g = out
+    _out("theta_out", th, torch.float32, (E, S, P), seeds.device)
+    _out("response_out", R, torch.float32, (E, S), seeds.device)
+    _out("grad_out", g, torch.float32, (E, S, P), seeds.device)
     _check("retina_multistart_optimize",
            lib().retina_multistart_optimize(ctypes.byref(events.c), model, float(sigma), S, _ptr(seeds),
                                             int(n_iters), float(step), lo, hi, _ptr(th), _ptr(R), _ptr(g),
@@ -255,10 +290,13 @@ def _newton(ex, events, model, seeds, sigmas, etas, final_sigma, max_halvings, b
         if ex:
             out = out + (torch.empty((E, S), dtype=torch.int32, device=seeds.device),)
     th, R, g = out[:3]
+    _out("theta_out", th, torch.float32, (E, S, P), seeds.device)
+    _out("response_out", R, torch.float32, (E, S), seeds.device)
+    _out("grad_out", g, torch.float32, (E, S, P), seeds.device)
     if ex:
         ne = out[3] if len(out) > 3 and out[3] is not None else torch.empty((E, S), dtype=torch.int32,
                                                                            device=seeds.device)
-        _dev(ne, torch.int32)
+        _out("evals_out", ne, torch.int32, (E, S), seeds.device)
         _check("retina_multistart_newton_ex",
                lib().retina_multistart_newton_ex(ctypes.byref(events.c), model, S, _ptr(seeds), len(sigmas), sg, et,
                                                  float(final_sigma), int(max_halvings), lo, hi, _ptr(th), _ptr(R),
@@ -286,7 +324,43 @@ def retina_merge_tracks(theta: torch.Tensor, response: torch.Tensor, radius, thr
                torch.empty((E, capacity), dtype=torch.int32, device=dev),
                torch.empty((E,), dtype=torch.int32, device=dev))
     tt, tr, ts, tz, tc = out
+    for nm, t, dt, shp in (("track_theta", tt, torch.float32, (E, capacity, P)),
+                           ("track_response", tr, torch.float32, (E, capacity)),
+                           ("track_seed", ts, torch.int32, (E, capacity)), ("track_size", tz, torch.int32, (E, capacity)),
+                           ("track_count", tc, torch.int32, (E,))):
+        _out(nm, t, dt, shp, theta.device)
     _check("retina_merge_tracks",
            lib().retina_merge_tracks(E, S, P, _ptr(theta), _ptr(response), rad, float(threshold), int(capacity),
                                      _ptr(tt), _ptr(tr), _ptr(ts), _ptr(tz), _ptr(tc), _stream(stream)))
     return tt, tr, ts, tz, tc
+
+
+def retina_pack_results(peak_index: torch.Tensor, peak_value: torch.Tensor, peak_count: torch.Tensor,
+                        track_theta: torch.Tensor, track_response: torch.Tensor, track_size: torch.Tensor,
+                        track_count: torch.Tensor, keep: int, header, out: Optional[torch.Tensor] = None,
+                        stream=None) -> torch.Tensor:
+    """The per-rank record of the one result gather: int32 [PACK_HEADER + E * pack_words(P, keep)]
+    (fp32 fields as bit patterns).  `header`: PACK_HEADER uint32 words (see dist.header_words)."""
+    E, pcap = peak_index.shape
+    _, tcap, P = track_theta.shape
+    dev = peak_index.device
+    _out("peak_index", peak_index, torch.int32, (E, pcap), dev)
+    _out("peak_value", peak_value, torch.float32, (E, pcap), dev)
+    _out("peak_count", peak_count, torch.int32, (E,), dev)
+    _out("track_theta", track_theta, torch.float32, (E, tcap, P), dev)
+    _out("track_response", track_response, torch.float32, (E, tcap), dev)
+    _out("track_size", track_size, torch.int32, (E, tcap), dev)
+    _out("track_count", track_count, torch.int32, (E,), dev)
+    n = PACK_HEADER + E * pack_words(P, keep)
+    if out is None:
+        out = torch.empty((n,), dtype=torch.int32, device=dev)
+    _out("out", out, torch.int32, (n,), dev)
+    hdr = list(header)
+    if len(hdr) != PACK_HEADER:
+        raise ValueError(f"header needs {PACK_HEADER} words")
+    h, _k = _arr(ctypes.c_uint32, [int(v) & 0xFFFFFFFF for v in hdr])
+    _check("retina_pack_results",
+           lib().retina_pack_results(E, P, int(keep), _ptr(peak_index), _ptr(peak_value), _ptr(peak_count), pcap,
+                                     _ptr(track_theta), _ptr(track_response), _ptr(track_size), _ptr(track_count),
+                                     tcap, h, _ptr(out), _stream(stream)))
+    return out

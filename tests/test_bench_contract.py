@@ -32,10 +32,12 @@ def test_reference_arm_json_line():
 
 @pytest.mark.gpu
 def test_gpu_arm_json_line():
-    d = _run(["--events-per-rank", "40", "--steps", "1", "--warmup", "3", "--cpu-sample-events", "1",
-              "--e2e-steps", "1"])
+    d = _run(["--events", "40", "--steps", "5", "--warmup", "3", "--cpu-plan", "quick", "--e2e-steps", "1"])
     assert BASE_KEYS <= set(d) and "impl" not in d
-    assert d["n_gpus"] == 1 and d["steps"] == 1 and d["warmup"] == 3 and d["scaling"] == "weak"
+    assert d["n_gpus"] == 1 and d["steps"] == 5 and d["warmup"] == 3 and d["scaling"] == "strong"
+    assert d["config"]["events_total"] == 40 and d["gathered"]["ranks"] == [0]
+    assert d["gathered"]["event_base"] == [0] and d["per_rank"][0]["events"] == 40
+    assert all(len(v) == 5 for v in d["phases_ms_per_step_all_steps"].values())
     assert d["value"] > 0 and d["ms_per_step"] > 0 and d["dtype"] == "f32" and d["data"] == "synthetic"
     r = d["roofline"]
     assert r["bound"] in ("alu", "tensor", "hbm") and 0 < r["frac"] <= 1.0 and r["peak"] > 0
@@ -44,5 +46,25 @@ def test_gpu_arm_json_line():
     assert e["value"] > 0 and e["h2d_bytes_per_step"] > 0 and e["d2h_bytes_per_step"] > 0
     assert d["gpu_launches"] > 0 and set(d["clocks"]) >= {"sm_mhz", "sm_max_mhz", "reasons"}
     cb = d["cpu_baseline"]
-    assert cb["kind"] == "oracle" and cb["cores"] >= 1 and cb["value"] > 0
+    assert cb["kind"] == "oracle" and cb["cores"] >= 1 and cb["value"] > 0 and cb["cpu_model"]
+    assert cb["all_cores"]["threads"] == cb["cores"] and cb["one_core"]["threads"] == 1
     assert d["config"]["workload"].startswith("cfg3")
+
+
+def test_gpus_n_spawns_ranks_and_shards_the_batch():
+    """`bench.py --gpus 2` outside torchrun launches 2 ranks itself (torch.distributed.run on
+    127.0.0.1); each rank takes its contiguous block of the SAME batch (strong scaling, SURVEY.md
+    §8(e)).  --dist-check does no GPU work: gloo all_gather of the shard bounds and hit counts."""
+    from synth import configs as C
+    from synth import events as G
+    d = _run(["--gpus", "2", "--dist-check", "--config", "cfg2"], timeout=900)
+    assert d["world"] == 2 and d["scaling"] == "strong"
+    sh = sorted(d["shards"])
+    assert [s[0] for s in sh] == [0, 1] and sh[0][1] == 0 and sh[0][2] == sh[1][1] and sh[1][2] == 200
+    full = G.make_batch(C.CFG2, range(200))
+    assert sum(s[3] for s in sh) == full.n_hits
+    w = _run(["--gpus", "2", "--dist-check", "--config", "cfg2", "--scaling", "weak", "--events-per-rank", "7"],
+             timeout=900)
+    assert sorted(s[1:3] for s in w["shards"]) == [[0, 7], [7, 14]] and w["scaling"] == "weak"
+    r = _run(["--gpus", "2", "--dist-check", "--config", "cfg1"], timeout=900)
+    assert r["scaling"] == "replicas" and all(s[1:3] == [0, 1] for s in r["shards"])

@@ -11,6 +11,7 @@ import torch.multiprocessing as mp
 from paper_1709_08610_b200 import dist as D
 from synth import configs as C
 from synth import events as G
+from tests.pack_ref import pack_ref
 
 
 def _free_port():
@@ -46,7 +47,10 @@ def _worker(rank, world, port, out_path):
     dist.init_process_group("gloo", rank=rank, world_size=world)
     E, P, cap, keep = 5, 3, 6, 4
     res = _fake_results(rank, E, P, cap, 0)
-    buf = D.pack(*res, keep=keep, header=[rank, rank * E, E, 0, 0, 12.5 + rank, 1.0, 2.0])
+    # the record as retina_pack_results lays it out (the device kernel is checked against the same
+    # reference word for word in tests/test_parity_gpu.py); here gloo moves it
+    buf = torch.from_numpy(pack_ref(*(x.numpy() for x in res), keep,
+                                    D.header_words(rank, rank * E, E, 1.5e9 * (rank + 1), 2.5e9)))
     gathered = D.gather(buf, world)
     if rank == 0:
         np.save(out_path, gathered.numpy())
@@ -63,7 +67,8 @@ def test_pack_gather_unpack_gloo_world2(tmp_path):
     assert [d["rank"] for d in dec] == [0, 1]
     for r, d in enumerate(dec):
         pi, pv, pc, tt, tr, tz, tc = (x.numpy() for x in _fake_results(r, 5, 3, 6, 0))
-        assert d["event_base"] == 5 * r and d["t_ms"] == 12.5 + r
+        assert d["event_base"] == 5 * r and d["n_events"] == 5
+        assert d["pairs_grid"] == np.float32(1.5 * (r + 1)) * 1e9 and d["pairs_ms"] == np.float32(2.5) * 1e9
         assert np.array_equal(d["n_peaks"], pc) and np.array_equal(d["n_tracks"], tc)
         assert d["peaks_total"] == pc.sum() and d["tracks_total"] == tc.sum()
         for e in range(5):
