@@ -177,7 +177,7 @@ size_t retina_find_peaks_workspace_size(int32_t n_events, int32_t P, const int32
     long long cells = 1;
     for (int i = 0; i < P; ++i) cells *= (axis_len[i] > 0 ? axis_len[i] : 0);
     if (cells <= 0 || cells > 0x7fffffffLL) return 0;
-    return retina::peaks_workspace_bytes(n_events, (int)cells);
+    return retina::peaks_workspace_bytes(n_events, P, axis_len[0], axis_len[1], P == 3 ? axis_len[2] : 1);
 }
 
 int retina_find_peaks_ws(const float *response, int32_t n_events, int32_t P, const int32_t *axis_len,

@@ -125,7 +125,10 @@ cudaError_t launch_multistart(int model, const MultistartArgs &a, int n_events, 
 cudaError_t launch_find_peaks(const PeakArgs &a, int n_events, cudaStream_t stream);
 cudaError_t launch_find_peaks_ws(const PeakArgs &a, int n_events, int32_t *ws, cudaStream_t stream);
 int peaks_slabs(int cells);
-size_t peaks_workspace_bytes(long long n_events, int cells);
+size_t peaks_workspace_bytes(long long n_events, int P, int n0, int n1, int n2);
+bool peaks3_brick_ok(int n0, int n1, int n2);
+size_t peaks3_workspace_bytes(long long n_events, int n0, int n1, int n2);
+cudaError_t launch_find_peaks3_brick(const PeakArgs &a, int n_events, int32_t *ws, cudaStream_t stream);
 cudaError_t launch_merge(const MergeArgs &a, int n_events, cudaStream_t stream);
 
 }  // namespace retina

@@ -238,12 +238,15 @@ cudaError_t launch_find_peaks(const PeakArgs &a0, int n_events, cudaStream_t str
 
 int peaks_slabs(int cells) { return (cells + kSlabCells - 1) / kSlabCells; }
 
-size_t peaks_workspace_bytes(long long n_events, int cells) {
-    const long long lists = n_events * peaks_slabs(cells);
+size_t peaks_workspace_bytes(long long n_events, int P, int n0, int n1, int n2) {
+    if (P == 3 && peaks3_brick_ok(n0, n1, n2)) return peaks3_workspace_bytes(n_events, n0, n1, n2);
+    const long long lists = n_events * peaks_slabs(n0 * n1 * n2);
     return (size_t)lists * (sizeof(int32_t) + (size_t)kSlabList * (sizeof(int32_t) + sizeof(float)));
 }
 
 cudaError_t launch_find_peaks_ws(const PeakArgs &a0, int n_events, int32_t *ws, cudaStream_t stream) {
+    if (a0.P == 3 && peaks3_brick_ok(a0.n0, a0.n1, a0.n2))  // plane blocks staged by TMA (peaks3.cu)
+        return launch_find_peaks3_brick(a0, n_events, ws, stream);
     const int cells = a0.n0 * a0.n1 * a0.n2;
     const int n_slabs = peaks_slabs(cells);
     for (int e0 = 0; e0 < n_events; e0 += 65535) {

@@ -56,14 +56,10 @@ __device__ __forceinline__ void tc_mma_f16(uint32_t tmem_d, uint64_t da, uint64_
 }
 
 
-// ---- fp16 packing, mbarrier arrive, and the CTA-pair (cluster of 2) helpers
+// ---- fp16 packing and the CTA-pair (cluster of 2) helpers
 __device__ __forceinline__ uint32_t pack_h2(float a, float b) {
     const __half2 h = __floats2half2_rn(a, b);
     return *reinterpret_cast<const uint32_t *>(&h);
-}
-
-__device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
-    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 
 constexpr uint32_t kTcIdescF16M256 =

@@ -192,7 +192,12 @@ def test_T3_peaks_bitexact_planted_ties(P, shape):
 
 
 @pytest.mark.parametrize("P,shape", [(2, (3, 1024, 1024)), (2, (5, 37, 61)), (3, (2, 64, 64, 64)),
-                                     (3, (1, 256, 256, 256)), (2, (2, 700, 900))])
+                                     (3, (1, 256, 256, 256)), (2, (2, 700, 900)),
+                                     # P = 3 plane-block (TMA ring) path: small rows, one block, max row
+                                     # length, ragged last block, and a row length that is not a multiple
+                                     # of 4 (slab path)
+                                     (3, (2, 19, 23, 28)), (3, (1, 9, 300, 12)), (3, (1, 5, 7, 2048)),
+                                     (3, (2, 4, 70, 36)), (3, (3, 40, 33, 200)), (3, (2, 33, 17, 29))])
 def test_T3_peaks_workspace_path_identical(P, shape):
     """retina_find_peaks_ws (many CTAs per event) == retina_find_peaks (one CTA per event) ==
     the oracle rule, bit for bit, including ties and capacity overflow."""
@@ -209,9 +214,13 @@ def test_T3_peaks_workspace_path_identical(P, shape):
         for e in range(shape[0]):
             k = min(int(a[2][e]), cap)
             assert torch.equal(a[0][e, :k], b[0][e, :k]) and torch.equal(a[1][e, :k], b[1][e, :k])
-        if shape[1] <= 256:
+        if np.prod(shape) <= 2e7:
             ri, rv, rc = ora.peaks(g.astype(np.float64), P, thr, cap)
             assert np.array_equal(b[2].cpu().numpy(), rc)
+            for e in range(shape[0]):
+                k = min(int(rc[e]), cap)
+                assert np.array_equal(b[0][e, :k].cpu().numpy(), ri[e, :k])
+                assert np.array_equal(b[1][e, :k].cpu().numpy().astype(np.float64), rv[e, :k])
 
 
 @pytest.mark.parametrize("P,shape", [(2, (3, 1024, 1024)), (3, (2, 96, 96, 96))])
