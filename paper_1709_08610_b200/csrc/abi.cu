@@ -40,6 +40,9 @@ float c2_of(float sigma) {
     const double s = sigma;
     return (float)(2.0 / (s * s));
 }
+// sqrt(log2(e)) / sigma and (2 / sigma^2) / that, in fp64, rounded once (SLOPE3 multi-start)
+float sk_of(float sigma) { return (float)(1.2011224087864498 / (double)sigma); }
+float c2s_of(float sigma) { return (float)(2.0 / ((double)sigma * 1.2011224087864498)); }
 
 int stage_cap(int32_t hint, int dflt) {
     if (hint <= 0) return dflt;
@@ -280,6 +283,8 @@ int retina_multistart_optimize(const retina_events *ev, int model, float sigma, 
     a.z_ref = ev->z_ref;
     a.negK = neg_k(sigma);
     a.c2 = c2_of(sigma);
+    a.sk = sk_of(sigma);
+    a.c2s = c2s_of(sigma);
     a.step = step;
     for (int i = 0; i < 3; ++i) {
         a.lo[i] = (i < P) ? box_lo[i] : 0.f;

@@ -50,32 +50,6 @@ __device__ __forceinline__ float ex2_approx(float x) {
     return y;
 }
 
-// 2^a for a pair of arguments a <= 0 on the FMA pipe instead of MUFU:
-// a = n + f with n = rint(a) (magic-constant rounding, |a| < 2^22) and |f| <= 1/2 exact
-// (Sterbenz); 2^f by a degree-5 minimax polynomial in Horner form (max relative error
-// 2.1e-7 evaluated in fp32, the size of ex2.approx's own 2^-22); 2^n by adding n to the
-// exponent field (integer pipe).  a is clamped at -125 so the exponent never underflows: the
-// result there is <= 2^-124.5 where ex2.approx.ftz gives 0 or a denormal-flushed 0
-// (absolute difference < 3e-38, far below every parity floor).  8 FMA-pipe lane-ops per
-// exponential (3 FADD + 5 FFMA), packed two per instruction.
-__device__ __forceinline__ float2 ex2_poly2(float2 a) {
-    a.x = fmaxf(a.x, -125.f);
-    a.y = fmaxf(a.y, -125.f);
-    const float2 M = make_float2(12582912.f, 12582912.f);  // 1.5 * 2^23
-    const float2 j = __fadd2_rn(a, M);                      // low mantissa bits = rint(a)
-    const float2 n = __fadd2_rn(j, make_float2(-M.x, -M.y));
-    const float2 f = __fadd2_rn(a, make_float2(-n.x, -n.y));
-    float2 p = make_float2(1.327647129073739e-3f, 1.327647129073739e-3f);
-    p = __ffma2_rn(p, f, make_float2(9.675540961325169e-3f, 9.675540961325169e-3f));
-    p = __ffma2_rn(p, f, make_float2(5.550713092088699e-2f, 5.550713092088699e-2f));
-    p = __ffma2_rn(p, f, make_float2(2.4022120237350464e-1f, 2.4022120237350464e-1f));
-    p = __ffma2_rn(p, f, make_float2(6.931469440460205e-1f, 6.931469440460205e-1f));
-    p = __ffma2_rn(p, f, make_float2(1.0000001192092896f, 1.0000001192092896f));
-    // bits(j) = 0x4B400000 + n, so bits(j) << 23 = n << 23 (mod 2^32)
-    return make_float2(__int_as_float(__float_as_int(p.x) + (__float_as_int(j.x) << 23)),
-                       __int_as_float(__float_as_int(p.y) + (__float_as_int(j.y) << 23)));
-}
-
 // Knuth TwoSum: hi + lo == a + b exactly (round-to-nearest fp32, no FTZ issues for
 // the magnitudes used here: mm coordinates).
 __device__ __forceinline__ void two_sum(float a, float b, float &hi, float &lo) {

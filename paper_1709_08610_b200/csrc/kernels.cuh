@@ -25,6 +25,8 @@ struct MultistartArgs {
     float z_ref;
     float negK;   // -log2(e) / sigma^2
     float c2;     // 2 / sigma^2 (gradient prefactor)
+    float sk;     // sqrt(log2(e)) / sigma (SLOPE3: residuals are formed already scaled by it)
+    float c2s;    // c2 / sk (SLOPE3 gradient prefactor for the scaled residual sums)
     float step;
     float lo[3], hi[3];
     int n_seeds;

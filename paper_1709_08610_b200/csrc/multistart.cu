@@ -33,13 +33,6 @@ namespace retina {
 #define RETINA_MS3_MINB 6
 #endif
 constexpr int kMsThreads = RETINA_MS_THREADS;
-#ifndef RETINA_MS_POLY  // bit u*NP+p: seed pair p of the u-th hit of each two takes ex2_poly2 (FMA pipe)
-#define RETINA_MS_POLY 0   // measured slower (profiles/r1_k4_fma_exp_offload.jsonl): off
-#endif
-constexpr unsigned kPolyMask = RETINA_MS_POLY;
-#ifndef RETINA_MS3_CX
-#define RETINA_MS3_CX 1  // SLOPE3: per-plane -t d_lo folded by FADD2 (+3 % measured on cfg4)
-#endif
 
 template <int MODEL, int S, bool ZREF, bool GRAD>
 __device__ __forceinline__ void ms_pass(HitStage &st, const float (&th)[S][3], float negK, float zref,
@@ -150,23 +143,21 @@ __device__ __forceinline__ void ms_pass(HitStage &st, const float (&th)[S][3], f
 // is an independent IEEE round-to-nearest operation, so results are bit-identical to the
 // scalar ms_pass.  Per (seed, hit): 8 FMA-pipe lane-ops + 1 MUFU.EX2, i.e. the loop is
 // balanced between the FMA pipe (128 lanes/clk/SM) and MUFU (16/clk/SM).
-template <int V>
-struct IC {
-    static constexpr int v = V;
-};
-
 template <int MODEL, int S, bool ZREF, bool GRAD, bool WANT_R>
 __device__ __forceinline__ void ms_pass_x2(HitStage &st, const float (&th)[S][3], float negK, float zref,
-                                           float (&R)[S], float (&G)[S][4]) {
+                                           float (&R)[S], float (&G)[S][4], float sk = 0.f) {
     static_assert(S % 2 == 0, "seed pairs");
     constexpr int NP = S / 2;
     float2 mtx[NP], mty[NP], r2[NP], qx[NP], qy[NP], gx[NP], gy[NP], ax[NP], ay[NP], dh[NP], dl[NP];
     const float2 zero = make_float2(0.f, 0.f);
-#if RETINA_MS3_CX
-    float2 cx[NP], cy[NP];
+    // SLOPE3, per plane and seed: c = t (z - z0) as chx + clx (clx ~ 1e-5 of an ulp-level tail), and
+    // the tail pre-scaled by -sk; per hit s' = sk s = fma(sk, x - chx, -sk clx): x - chx is exact for
+    // every hit near the track (Sterbenz) and one rounding relative to |s| otherwise, and the scale
+    // rides on the correction FMA, so a = s'_x^2 + s'_y^2 needs no separate multiply by K
+    float2 chx[NP], chy[NP], cx[NP], cy[NP];
 #pragma unroll
-    for (int p = 0; p < NP; ++p) cx[p] = cy[p] = zero;
-#endif
+    for (int p = 0; p < NP; ++p) chx[p] = chy[p] = cx[p] = cy[p] = zero;
+    const float2 SK = make_float2(sk, sk);
 #pragma unroll
     for (int p = 0; p < NP; ++p) {
         mtx[p] = make_float2(-th[2 * p][0], -th[2 * p + 1][0]);
@@ -189,9 +180,8 @@ __device__ __forceinline__ void ms_pass_x2(HitStage &st, const float (&th)[S][3]
             qx[p] = qy[p] = zero;
         }
     };
-    // one hit; U = position of the hit in its group of two (selects the FMA-pipe exponentials of
-    // the opt-in RETINA_MS_POLY variant; with the mask 0 every exponential is MUFU.EX2)
-    auto hit = [&](const float4 hk, auto U) {
+    // one hit against every seed pair of the thread
+    auto hit = [&](const float4 hk) {
         if (hk.z != zprev) {  // warp-uniform plane change
             if (GRAD) flush();
             zprev = hk.z;
@@ -200,10 +190,14 @@ __device__ __forceinline__ void ms_pass_x2(HitStage &st, const float (&th)[S][3]
                 for (int p = 0; p < NP; ++p) {
                     two_sum(hk.z, -th[2 * p][2], dh[p].x, dl[p].x);
                     two_sum(hk.z, -th[2 * p + 1][2], dh[p].y, dl[p].y);
-#if RETINA_MS3_CX
-                    cx[p] = __fmul2_rn(mtx[p], dl[p]);  // -t d_lo: constant over the plane
-                    cy[p] = __fmul2_rn(mty[p], dl[p]);
-#endif
+                    // t d = (t d_hi) + (t d_lo): ch = fl(t d_hi), its FMA residual + t d_lo as the tail
+                    const float2 tx = make_float2(-mtx[p].x, -mtx[p].y), ty = make_float2(-mty[p].x, -mty[p].y);
+                    chx[p] = __fmul2_rn(tx, dh[p]);
+                    chy[p] = __fmul2_rn(ty, dh[p]);
+                    const float2 lx = __ffma2_rn(tx, dl[p], __ffma2_rn(tx, dh[p], make_float2(-chx[p].x, -chx[p].y)));
+                    const float2 ly = __ffma2_rn(ty, dl[p], __ffma2_rn(ty, dh[p], make_float2(-chy[p].x, -chy[p].y)));
+                    cx[p] = __fmul2_rn(make_float2(-sk, -sk), lx);  // -sk x tail: constant over the plane
+                    cy[p] = __fmul2_rn(make_float2(-sk, -sk), ly);
                 }
             } else if (ZREF) {
                 two_sum(hk.z, -zref, dprev, dlprev);
@@ -216,15 +210,9 @@ __device__ __forceinline__ void ms_pass_x2(HitStage &st, const float (&th)[S][3]
         for (int p = 0; p < NP; ++p) {
             float2 sx, sy;
             if (MODEL == kSlope3) {
-#if RETINA_MS3_CX
-                // (x - t d_hi) rounded once (error relative to |s + t d_lo| ~ |s|), then the
-                // per-plane constant -t d_lo: an FADD2 of two pairs instead of a 3-pair FFMA2
-                sx = __fadd2_rn(__ffma2_rn(mtx[p], dh[p], X), cx[p]);
-                sy = __fadd2_rn(__ffma2_rn(mty[p], dh[p], Y), cy[p]);
-#else
-                sx = __ffma2_rn(mtx[p], dl[p], __ffma2_rn(mtx[p], dh[p], X));
-                sy = __ffma2_rn(mty[p], dl[p], __ffma2_rn(mty[p], dh[p], Y));
-#endif
+                // scaled residuals s' = sk s (see the plane setup above)
+                sx = __ffma2_rn(SK, __fadd2_rn(X, make_float2(-chx[p].x, -chx[p].y)), cx[p]);
+                sy = __ffma2_rn(SK, __fadd2_rn(Y, make_float2(-chy[p].x, -chy[p].y)), cy[p]);
             } else if (ZREF) {
                 const float2 D = make_float2(dprev, dprev), DL = make_float2(dlprev, dlprev);
                 sx = __ffma2_rn(mtx[p], DL, __ffma2_rn(mtx[p], D, X));
@@ -234,10 +222,14 @@ __device__ __forceinline__ void ms_pass_x2(HitStage &st, const float (&th)[S][3]
                 sx = __ffma2_rn(mtx[p], Z, X);
                 sy = __ffma2_rn(mty[p], Z, Y);
             }
-            const float2 a = __fmul2_rn(__ffma2_rn(sx, sx, __fmul2_rn(sy, sy)), nk);
-            const float2 w = ((kPolyMask >> (decltype(U)::v * NP + p)) & 1)
-                                 ? ex2_poly2(a)
-                                 : make_float2(ex2_approx(a.x), ex2_approx(a.y));
+            float2 w;
+            if (MODEL == kSlope3) {  // already scaled: 2^-(s'_x^2 + s'_y^2)
+                const float2 a = __ffma2_rn(sx, sx, __fmul2_rn(sy, sy));
+                w = make_float2(ex2_approx(-a.x), ex2_approx(-a.y));
+            } else {
+                const float2 a = __fmul2_rn(__ffma2_rn(sx, sx, __fmul2_rn(sy, sy)), nk);
+                w = make_float2(ex2_approx(a.x), ex2_approx(a.y));
+            }
             if (WANT_R) r2[p] = __fadd2_rn(r2[p], w);  // iterations only need grad R
             if (GRAD) {
                 qx[p] = __ffma2_rn(w, sx, qx[p]);
@@ -246,17 +238,8 @@ __device__ __forceinline__ void ms_pass_x2(HitStage &st, const float (&th)[S][3]
         }
     };
     st.pass([&](const float4 *h, int len) {
-        if constexpr (kPolyMask == 0) {
 #pragma unroll 2
-            for (int k = 0; k < len; ++k) hit(h[k], IC<0>{});
-        } else {
-            int k = 0;
-            for (; k + 1 < len; k += 2) {
-                hit(h[k], IC<0>{});
-                hit(h[k + 1], IC<1>{});
-            }
-            if (k < len) hit(h[k], IC<0>{});
-        }
+        for (int k = 0; k < len; ++k) hit(h[k]);
     });
     if (GRAD) flush();
 #pragma unroll
@@ -276,11 +259,11 @@ __device__ __forceinline__ void ms_pass_x2(HitStage &st, const float (&th)[S][3]
 
 template <int MODEL, int S, bool ZREF, bool GRAD, bool WANT_R>
 __device__ __forceinline__ void ms_eval(HitStage &st, const float (&th)[S][3], float negK, float zref,
-                                        float (&R)[S], float (&G)[S][4]) {
+                                        float (&R)[S], float (&G)[S][4], float sk) {
     if constexpr (MODEL == kLine2D)
         ms_pass<MODEL, S, ZREF, GRAD>(st, th, negK, zref, R, G);
     else
-        ms_pass_x2<MODEL, S, ZREF, GRAD, WANT_R>(st, th, negK, zref, R, G);
+        ms_pass_x2<MODEL, S, ZREF, GRAD, WANT_R>(st, th, negK, zref, R, G, sk);
 }
 
 template <int MODEL, int S>
@@ -322,8 +305,8 @@ multistart_kernel(MultistartArgs a) {
 
     float R[S], G[S][4], g[S][3];
     for (int it = 0; it < a.n_iters; ++it) {
-        ms_eval<MODEL, S, ZREF, true, false>(st, th, a.negK, a.z_ref, R, G);
-        ms_gradient<MODEL, S>(th, G, a.c2, g);
+        ms_eval<MODEL, S, ZREF, true, false>(st, th, a.negK, a.z_ref, R, G, a.sk);
+        ms_gradient<MODEL, S>(th, G, (MODEL == kSlope3) ? a.c2s : a.c2, g);
 #pragma unroll
         for (int s = 0; s < S; ++s)
 #pragma unroll
@@ -331,10 +314,10 @@ multistart_kernel(MultistartArgs a) {
                 th[s][i] = fminf(fmaxf(__fmaf_rn(a.step, g[s][i], th[s][i]), a.lo[i]), a.hi[i]);
     }
     if (a.grad_out) {
-        ms_eval<MODEL, S, ZREF, true, true>(st, th, a.negK, a.z_ref, R, G);
-        ms_gradient<MODEL, S>(th, G, a.c2, g);
+        ms_eval<MODEL, S, ZREF, true, true>(st, th, a.negK, a.z_ref, R, G, a.sk);
+        ms_gradient<MODEL, S>(th, G, (MODEL == kSlope3) ? a.c2s : a.c2, g);
     } else {
-        ms_eval<MODEL, S, ZREF, false, true>(st, th, a.negK, a.z_ref, R, G);
+        ms_eval<MODEL, S, ZREF, false, true>(st, th, a.negK, a.z_ref, R, G, a.sk);
     }
 #pragma unroll
     for (int s = 0; s < S; ++s) {
