@@ -246,172 +246,6 @@ __global__ void __launch_bounds__(32 * TC_WARPS, RETINA_TC_MINB) grid_tensor_ker
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TC_TMEM_COLS));
 }
 
-// ------------------------------------------------------------------------------------------------
-// TS variant: the A operand (EX, 128 tx rows) lives in TENSOR MEMORY, written by tcgen05.st from
-// the generating warps, and only B (EY, 256 ty rows) goes through shared memory.  The SS kernel
-// moves ~156 B/clk through shared memory per SM at full MMA rate (A and B written once, read by
-// three MMAs each) -- above the 128 B/clk the SM's shared memory delivers; keeping A in TMEM
-// drops that to ~106 B/clk.  TMEM: accumulator columns [0, 256), A stage s at 256 + 64 s
-// (hi: 32 columns = 32 hits, lo: the next 32).  16 warps: warp w writes A rows 32 (w % 4) + lane
-// (its TMEM lane quarter) for hits 8 (w / 4) .. +7, and B rows lane + 32 (2 t + w / 8), t < 4,
-// for the 4-hit block w % 8.
-constexpr int TS_B_STAGE_BYTES = 2 * TC_B_BYTES;  // B hi + lo: 64 KB
-constexpr int TS_TMEM_COLS = 512;
-
-__device__ __forceinline__ void tc_mma_ts(uint32_t tmem_d, uint32_t tmem_a, uint64_t db, uint32_t accumulate) {
-    asm volatile(
-        "{\n\t.reg .pred p;\n\t"
-        "setp.ne.b32 p, %4, 0;\n\t"
-        "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n\t}" ::"r"(tmem_d),
-        "r"(tmem_a), "l"(db), "r"(kTcIdescTf32), "r"(accumulate));
-}
-
-__device__ __forceinline__ void tmem_st8(uint32_t taddr, const float (&v)[8]) {
-    asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(taddr),
-                 "r"(__float_as_uint(v[0])), "r"(__float_as_uint(v[1])), "r"(__float_as_uint(v[2])),
-                 "r"(__float_as_uint(v[3])), "r"(__float_as_uint(v[4])), "r"(__float_as_uint(v[5])),
-                 "r"(__float_as_uint(v[6])), "r"(__float_as_uint(v[7]))
-                 : "memory");
-}
-
-template <int MODEL, bool ZREF>
-__global__ void __launch_bounds__(512, 1) grid_tensor_ts_kernel(GridArgs a) {
-    extern __shared__ __align__(1024) uint8_t s_raw[];
-    __shared__ __align__(8) uint64_t s_bar[2];
-    __shared__ __align__(8) uint64_t s_empty[2];
-    __shared__ uint32_t s_tmem;
-
-    uint8_t *stage_base = s_raw;                                                  // 2 x 64 KB (B)
-    float4 *s_hits = reinterpret_cast<float4 *>(s_raw + 2 * TS_B_STAGE_BYTES);
-
-    const int e = a.e_base + blockIdx.y;
-    const int tn = (a.n1 + TC_N - 1) / TC_N;
-    const int nl = (MODEL == kSlope3) ? a.n2 : 1;
-    const int l = blockIdx.x % nl, tile = blockIdx.x / nl;
-    const int t_n = tile % tn, t_m = tile / tn;
-    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-
-    if (warp == 0) {
-        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&s_tmem)),
-                     "r"(TS_TMEM_COLS));
-        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
-        tc_fence_before();
-    }
-    if (tid == 0) {
-        mbar_init(&s_empty[0], 1);
-        mbar_init(&s_empty[1], 1);
-    }
-    const int start = a.offsets[e], nh = a.offsets[e + 1] - start;
-    HitStage st;
-    st.init(s_hits, s_bar, a.hits + start, nh, a.cap);
-    tc_fence_after();
-    const uint32_t tmem = s_tmem;
-
-    const int qd = warp & 3, ka = warp >> 2;   // A: lane quarter, 8-hit block
-    const int kb = warp & 7, rset = warp >> 3;  // B: 4-hit block, row set
-    const float pa = __ldg(a.nodes0 + min(t_m * TC_M + qd * 32 + lane, a.n0 - 1));
-    float pb[4];
-#pragma unroll
-    for (int t = 0; t < 4; ++t) pb[t] = __ldg(a.nodes1 + min(t_n * TC_N + lane + 32 * (2 * t + rset), a.n1 - 1));
-    const float negK = a.negK;
-    const float zref = (MODEL == kSlope3) ? __ldg(a.nodes2 + l) : a.z_ref;
-    const uint32_t stage_saddr = smem_u32(stage_base);
-    constexpr bool EXACT_D = ZREF || MODEL == kSlope3;
-
-    auto factor = [&](float p, float c, float dz, float dzl) -> float {
-        const float sres = EXACT_D ? __fmaf_rn(-p, dzl, __fmaf_rn(-p, dz, c)) : __fmaf_rn(-p, dz, c);
-        return ex2_approx(__fmul_rn(__fmul_rn(sres, sres), negK));
-    };
-
-    int chunk = 0;
-    st.pass([&](const float4 *h, int len) {
-        for (int k0 = 0; k0 < len; k0 += TC_KC, ++chunk) {
-            const int s = chunk & 1;
-            if (chunk >= 2) mbar_wait(&s_empty[s], ((chunk - 2) >> 1) & 1);
-            tc_fence_after();  // the MMAs that read A stage s are complete before we overwrite it
-            // ---- A: 8 hits of this thread's row into TMEM (hi and lo columns)
-            {
-                float vh[8], vl[8];
-#pragma unroll
-                for (int q = 0; q < 8; ++q) {
-                    const int k = k0 + ka * 8 + q;
-                    float v = 0.f;
-                    if (k < len) {
-                        const float4 hk = h[k];
-                        float dz = hk.z, dzl = 0.f;
-                        if (EXACT_D) two_sum(hk.z, -zref, dz, dzl);
-                        v = factor(pa, hk.x, dz, dzl);
-                    }
-                    vh[q] = tf32_trunc(v);
-                    vl[q] = __fsub_rn(v, vh[q]);
-                }
-                const uint32_t ta = tmem + ((uint32_t)(qd * 32) << 16) + (uint32_t)(TC_N + s * 64 + ka * 8);
-                tmem_st8(ta, vh);
-                tmem_st8(ta + 32, vl);
-            }
-            // ---- B: 4 hits (block kb) for 4 rows into the shared-memory stage
-            {
-                float hy[4], hz[4], hzl[4];
-                bool ok[4];
-#pragma unroll
-                for (int q = 0; q < 4; ++q) {
-                    const int k = k0 + kb * 4 + q;
-                    ok[q] = k < len;
-                    const float4 hk = h[ok[q] ? k : 0];
-                    hy[q] = hk.y;
-                    hz[q] = hk.z;
-                    hzl[q] = 0.f;
-                    if (EXACT_D) two_sum(hk.z, -zref, hz[q], hzl[q]);
-                }
-                float *Bhi = reinterpret_cast<float *>(stage_base + s * TS_B_STAGE_BYTES);
-                float *Blo = Bhi + TC_B_BYTES / 4;
-#pragma unroll
-                for (int t = 0; t < 4; ++t) {
-                    float vh[4], vl[4];
-#pragma unroll
-                    for (int q = 0; q < 4; ++q) {
-                        const float v = ok[q] ? factor(pb[t], hy[q], hz[q], hzl[q]) : 0.f;
-                        vh[q] = tf32_trunc(v);
-                        vl[q] = __fsub_rn(v, vh[q]);
-                    }
-                    const int r = lane + 32 * (2 * t + rset);
-                    *reinterpret_cast<float4 *>(Bhi + (kb * TC_N + r) * 4) = make_float4(vh[0], vh[1], vh[2], vh[3]);
-                    *reinterpret_cast<float4 *>(Blo + (kb * TC_N + r) * 4) = make_float4(vl[0], vl[1], vl[2], vl[3]);
-                }
-            }
-            asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
-            tc_fence_before();
-            fence_proxy_async();
-            __syncthreads();
-            if (tid == 0) {
-                tc_fence_after();
-                const uint32_t bH = stage_saddr + s * TS_B_STAGE_BYTES, bL = bH + TC_B_BYTES;
-                const uint32_t aH = tmem + (uint32_t)(TC_N + s * 64), aL = aH + 32;
-#pragma unroll
-                for (int j = 0; j < TC_KC / 8; ++j) {
-                    const uint32_t ob = j * 2 * (TC_N * 16);
-                    const uint32_t acc0 = (chunk > 0 || j > 0) ? 1u : 0u;
-                    tc_mma_ts(tmem, aH + 8 * j, umma_desc(bH + ob, TC_N * 16, 128), acc0);
-                    tc_mma_ts(tmem, aH + 8 * j, umma_desc(bL + ob, TC_N * 16, 128), 1u);
-                    tc_mma_ts(tmem, aL + 8 * j, umma_desc(bH + ob, TC_N * 16, 128), 1u);
-                }
-                tc_commit(&s_empty[s]);
-            }
-        }
-    });
-
-    const int n_chunks = chunk;
-    if (n_chunks > 0) {
-        const int s = (n_chunks - 1) & 1;
-        mbar_wait(&s_empty[s], ((n_chunks - 1) >> 1) & 1);
-    }
-    tc_fence_after();
-    tc_epilogue<MODEL>(a, e, t_m, t_n, l, nl, tmem, n_chunks, warp, lane);
-    tc_fence_before();
-    __syncthreads();
-    if (warp == 0)
-        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TS_TMEM_COLS));
-}
 
 // ------------------------------------------------------------------------------------------------
 // F16 split variant (RETINA_GRID_TENSOR_F16): the same contraction with fp16 operands on
@@ -841,33 +675,6 @@ int tensor_max_stage_hits() {
     return (227 * 1024 / RETINA_TC_MINB - 2 * TC_STAGE_BYTES - 1024) / 16;
 }
 
-int tensor_ts_max_stage_hits() { return (227 * 1024 - 2 * TS_B_STAGE_BYTES - 1024) / 16; }
-
-#ifndef RETINA_TC_TS
-#define RETINA_TC_TS 0  // measured: TS 1.04e14 vs SS 1.06e14 pair/s on cfg3 (SS kept as default)
-#endif
-
-template <int MODEL, bool ZREF>
-static cudaError_t launch_tc_ts(const GridArgs &a0, int n_events, cudaStream_t stream) {
-    auto kern = grid_tensor_ts_kernel<MODEL, ZREF>;
-    GridArgs a = a0;
-    a.cap = min(a.cap, tensor_ts_max_stage_hits()) & ~1;
-    const size_t smem = 2 * (size_t)TS_B_STAGE_BYTES + (size_t)a.cap * sizeof(float4);
-    cudaError_t err = ensure_dynamic_smem(kern, smem);
-    if (err != cudaSuccess) return err;
-    const long long tiles =
-        (long long)((a.n0 + TC_M - 1) / TC_M) * ((a.n1 + TC_N - 1) / TC_N) * (MODEL == kSlope3 ? a.n2 : 1);
-    if (tiles > 0x7fffffffLL) return cudaErrorInvalidConfiguration;
-    for (int e0 = 0; e0 < n_events; e0 += 65535) {
-        a.e_base = e0;
-        const int ne = min(65535, n_events - e0);
-        kern<<<dim3((unsigned)tiles, ne), 512, smem, stream>>>(a);
-        err = cudaGetLastError();
-        if (err != cudaSuccess) return err;
-    }
-    return cudaSuccess;
-}
-
 template <int MODEL, bool ZREF>
 static cudaError_t launch_tc(const GridArgs &a0, int n_events, cudaStream_t stream) {
     auto kern = grid_tensor_kernel<MODEL, ZREF>;
@@ -891,12 +698,6 @@ static cudaError_t launch_tc(const GridArgs &a0, int n_events, cudaStream_t stre
 
 cudaError_t launch_grid_tensor(int model, const GridArgs &a, int n_events, cudaStream_t stream) {
     if (n_events == 0) return cudaSuccess;
-    if (RETINA_TC_TS) {
-        if (model == kSlope3) return launch_tc_ts<kSlope3, false>(a, n_events, stream);
-        if (model != kSlope2) return cudaErrorInvalidValue;
-        return (a.z_ref == 0.f) ? launch_tc_ts<kSlope2, false>(a, n_events, stream)
-                                : launch_tc_ts<kSlope2, true>(a, n_events, stream);
-    }
     if (model == kSlope3) return launch_tc<kSlope3, false>(a, n_events, stream);
     if (model != kSlope2) return cudaErrorInvalidValue;
     return (a.z_ref == 0.f) ? launch_tc<kSlope2, false>(a, n_events, stream)
