@@ -191,8 +191,10 @@ int retina_multistart_optimize(const retina_events *ev, int model, float sigma,
  * (<= P iterations; stopped at non-positive curvature, or p = etas[j] grad R at the first
  * iteration), then backtracking alpha = 1, 1/2, ... (<= max_halvings halvings) accepting the
  * first clamp(theta + alpha p) with R >= R(theta) + 1e-4 alpha grad R . p (else theta stays).
- * Returns theta^q, R(theta^q) and grad R(theta^q) at final_sigma.  SLOPE2 / SLOPE3 only
- * (RETINA_EUNSUPPORTED for LINE2D); n_steps <= 16.
+ * Returns theta^q, R(theta^q) and grad R(theta^q) at final_sigma.  The direction is solved in
+ * fp64 from the fp32-accumulated grad R and H (SLOPE3's Hessian mixes slope and mm scales).
+ * SLOPE2 / SLOPE3 only (RETINA_EUNSUPPORTED for LINE2D); n_steps <= 16; max_halvings <= 126
+ * (RETINA_EUNSUPPORTED above: 2^-k is formed exactly only for normal floats).
  *   sigmas, etas: host fp32 [n_steps]; other arguments as retina_multistart_optimize. */
 int retina_multistart_newton(const retina_events *ev, int model, int32_t n_seeds, const float *seeds,
                              int32_t n_steps, const float *sigmas, const float *etas, float final_sigma,

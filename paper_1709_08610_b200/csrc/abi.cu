@@ -324,6 +324,8 @@ int retina_multistart_newton_ex(const retina_events *ev, int model, int32_t n_se
     if (n_steps < 0) return fail(RETINA_EINVAL, "n_steps < 0");
     if (n_steps > retina::kMaxNewtonSteps) return fail(RETINA_EUNSUPPORTED, "n_steps > %d", retina::kMaxNewtonSteps);
     if (max_halvings < 0) return fail(RETINA_EINVAL, "max_halvings < 0");
+    // the queued line search forms 2^-k from the exponent field: exact for k <= 126 (normal floats)
+    if (max_halvings > 126) return fail(RETINA_EUNSUPPORTED, "max_halvings %d > 126", max_halvings);
     if (n_steps > 0 && (!sigmas || !etas)) return fail(RETINA_EINVAL, "sigmas/etas is NULL");
     for (int j = 0; j < n_steps; ++j) {
         if (!finite_pos(sigmas[j])) return fail(RETINA_EINVAL, "sigmas[%d] must be finite and > 0", j);

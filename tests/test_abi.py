@@ -102,7 +102,12 @@ def test_peaks_workspace_size_and_validation(L):
     # 256 (index, value) pairs (8 B each)
     per_slab = 4 + 256 * 8
     assert sz(10, 2, _i(1024, 1024)) == 10 * 8 * per_slab
-    assert sz(3, 3, _i(256, 256, 256)) == 3 * 128 * per_slab
+    # P = 3 with rows of a multiple of 4 cells (<= 2048): the plane-block path (peaks3.cu): per
+    # segment (plane i, block of 2048 / n2 rows) a count, an offset and 32 (index, value) pairs
+    per_seg = 2 * 4 + 32 * 8
+    assert sz(3, 3, _i(256, 256, 256)) == 3 * (256 * 32) * per_seg
+    assert sz(2, 3, _i(19, 23, 28)) == 2 * (19 * 1) * per_seg           # 73 rows cover the 23 rows: one block
+    assert sz(1, 3, _i(20, 30, 29)) == 1 * 1 * per_slab                  # 29 % 4 != 0: slab path
     assert sz(0, 2, _i(4, 4)) == 0 and sz(1, 4, _i(4, 4)) == 0
     p = L.retina_find_peaks_ws
     p.argtypes = [ctypes.c_void_p, ctypes.c_int32, ctypes.c_int32, ctypes.c_void_p, ctypes.c_float, ctypes.c_int32,
@@ -147,6 +152,7 @@ def test_newton_validation(L):
         assert call(eta=_f(float("nan"), 1.0)) == rt.RETINA_EINVAL
         assert call(fs=-1.0) == rt.RETINA_EINVAL
         assert call(mh=-1) == rt.RETINA_EINVAL
+        assert call(mh=127) == rt.RETINA_EUNSUPPORTED           # 2^-k formed exactly only for k <= 126
         assert call(lo_=hi, hi_=lo) == rt.RETINA_EINVAL
         assert call(th=None) == rt.RETINA_EINVAL
         assert call(S=0, th=None, R=None) == rt.RETINA_OK        # nothing to do
