@@ -60,6 +60,13 @@ def test_eq3_budget_and_matching():
     truth = np.array([[0.2, 0.0], [0.0, -0.1]])
     eff, m, n = EV.match_efficiency([math.tan(a + 9e-4), 0.0], [0.0, -0.1 + 2e-3], truth, 1e-3)
     assert (m, n) == (1, 2) and eff == 0.5
+    # one-to-one: two candidates within eps of ONE truth give 1 match + 1 ghost; the closer one
+    # takes it, so a second truth near the farther candidate can still match it
+    two = [math.tan(a + 3e-4), math.tan(a + 8e-4)]
+    assert EV.match_tracks(two, [0.0, 0.0], truth[:1], 1e-3) == (1, 0, 1)
+    pair = np.array([[0.2, 0.0], [math.tan(a + 1.0e-3), 0.0]])
+    assert EV.match_tracks(two, [0.0, 0.0], pair, 1e-3) == (2, 0, 0)
+    assert EV.match_tracks([], [], truth, 1e-3) == (0, 2, 0)
 
 
 @pytest.mark.gpu

@@ -42,14 +42,31 @@ def seed_budget(alpha: float, n_grid: int, C0: float = 30.0, q: int = 3) -> int:
     return int(math.floor(alpha * n_grid / (C0 * q)))
 
 
-def match_efficiency(found_tx, found_ty, truth: np.ndarray, eps: float = 1e-3):
-    """a true track is reconstructed if some reported candidate lies within
-    eps radians of it.  Returns (efficiency, n_matched, n_true)."""
-    if len(truth) == 0:
-        return 1.0, 0, 0
-    if len(found_tx) == 0:
-        return 0.0, 0, len(truth)
+def match_tracks(found_tx, found_ty, truth: np.ndarray, eps: float = 1e-3):
+    """PAPER.md:197-198 ("a track is reconstructed if the found parameters are within
+    epsilon = 1e-3 radians"), as a one-to-one matching: every (truth,
+    candidate) pair within eps, taken in ascending angle (ties: truth index, then candidate
+    index), matches when neither side is matched yet.  Returns (n_matched, n_missed, n_ghosts)."""
+    n_t, n_f = len(truth), len(found_tx)
+    if n_t == 0 or n_f == 0:
+        return 0, n_t, n_f
     ang = angle_between(truth[:, 0][:, None], truth[:, 1][:, None], np.asarray(found_tx)[None, :],
                         np.asarray(found_ty)[None, :])
-    matched = int(np.sum(ang.min(axis=1) <= eps))
-    return matched / len(truth), matched, len(truth)
+    ti, fi = np.nonzero(ang <= eps)
+    order = np.lexsort((fi, ti, ang[ti, fi]))
+    used_t, used_f = np.zeros(n_t, bool), np.zeros(n_f, bool)
+    m = 0
+    for k in order:
+        if not used_t[ti[k]] and not used_f[fi[k]]:
+            used_t[ti[k]] = used_f[fi[k]] = True
+            m += 1
+    return m, n_t - m, n_f - m
+
+
+def match_efficiency(found_tx, found_ty, truth: np.ndarray, eps: float = 1e-3):
+    """Efficiency = matched / true tracks under the one-to-one matching of match_tracks().
+    Returns (efficiency, n_matched, n_true)."""
+    if len(truth) == 0:
+        return 1.0, 0, 0
+    m, _, _ = match_tracks(found_tx, found_ty, truth, eps)
+    return m / len(truth), m, len(truth)
