@@ -893,3 +893,58 @@ def test_T1_T4_full_cfg4_slab_vs_fp64_oracle():
                                                "excused_near_tie": ne}
         stats[f"event {e_id} t1_worst"] = worst
     PU.report("T1/T4 cfg4 256x256x34 slab", **stats)
+
+
+def test_concurrent_host_threads_on_two_streams_bitwise():
+    """include/retina.h promises calls are safe from several host threads on different streams
+    (no global mutable state besides the once-per-kernel shared-memory attribute cache): two
+    threads, each on its own stream, run cfg2 multi-start + merge and a cfg1 grid + peaks (first
+    calls of their kernels included, so the attribute cache is filled concurrently); every result
+    equals the serial run bit for bit."""
+    import threading
+    cfg, c1 = C.CFG2, C.CFG1
+    jobs = []
+    for k in range(2):
+        b = G.make_batch(cfg, [2 * k, 2 * k + 1])
+        sd = dev(G.make_seeds(cfg, [2 * k, 2 * k + 1], n_seeds=2048))
+        b1 = G.make_batch(c1, [k])
+        jobs.append((events_of(b), sd, events_of(b1), [dev(n) for n in G.axis_nodes(c1)]))
+
+    def work(job, stream=None):
+        ev, sd, ev1, nodes = job
+        with torch.cuda.stream(stream) if stream is not None else torch.cuda.stream(torch.cuda.current_stream()):
+            out = R.retina_multistart_optimize(ev, cfg.model, cfg.sigma, sd, cfg.n_iters, cfg.step, cfg.box_lo,
+                                               cfg.box_hi, stream=stream)
+            m = R.retina_merge_tracks(out[0], out[1], cfg.merge_radius, cfg.track_threshold, 256, stream=stream)
+            g = R.retina_grid_response(ev1, c1.model, c1.sigma, nodes, stream=stream,
+                                       algorithm=R.retina.GRID_TENSOR_F16_SINGLE)
+            p = R.retina_find_peaks(g, 2, c1.peak_threshold, 4096, stream=stream)
+        return list(out) + list(m) + [g] + list(p)
+
+    results = [None, None]
+    streams = [torch.cuda.Stream(), torch.cuda.Stream()]
+
+    def thread_main(k):
+        torch.cuda.set_device(0)
+        results[k] = work(jobs[k], streams[k])
+        streams[k].synchronize()
+
+    ts = [threading.Thread(target=thread_main, args=(k,)) for k in range(2)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    torch.cuda.synchronize()
+    for k in range(2):
+        serial = work(jobs[k])
+        torch.cuda.synchronize()
+        a, b = results[k], serial
+        for i in (0, 1, 2, 7, 8, 11):  # theta, R, grad, track_count, grid, peak_count: whole tensors
+            assert torch.equal(a[i], b[i]), i
+        for e in range(a[7].shape[0]):  # list entries up to the true counts
+            kt, kp = min(int(a[7][e]), 256), min(int(a[11][e]), 4096)
+            for i in (3, 4, 5, 6):
+                assert torch.equal(a[i][e, :kt], b[i][e, :kt])
+            if e < a[11].shape[0]:
+                for i in (9, 10):
+                    assert torch.equal(a[i][e, :kp], b[i][e, :kp])

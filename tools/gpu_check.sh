@@ -6,7 +6,7 @@ set -u
 mkdir -p gpurun_out
 timeout 900 python -m pytest tests -m gpu -q 2>&1 | tail -5 > gpurun_out/pytest_gpu.txt
 timeout 600 python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err
-SMALL="python bench.py --events-per-rank 296 --steps 1 --warmup 3 --no-cpu-baseline --e2e-steps 1"
+SMALL="python bench.py --events 296 --steps 1 --warmup 3 --no-cpu-baseline --e2e-steps 1"
 $SMALL > gpurun_out/small.json 2>&1 && \
 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv $SMALL \
     > gpurun_out/ncu_launches.log 2>&1 && \
