@@ -41,7 +41,17 @@ METRIC = "retina unit·hit evaluations/s (events/s alongside)"
 UNIT = "pairs/s"
 MUFU_PER_SM_CLK = 16      # measured: tools/pipe_microbench (15.95 ex2/clk/SM)
 FMA_PER_SM_CLK = 128      # measured: 121.5 FFMA/clk/SM; FFMA2 does not double it
+FMA_REG_LANES = 97        # measured FMA-pipe lanes/clk/SM for FFMA2 with register operands (85-97)
 N_SM = 148
+# FMA-pipe lane-ops per (seed, hit) pair of the multi-start passes: fixed-step
+# iterations (R not accumulated), Newton Hessian-mode and R-only evaluations
+FMA_OPS = {"slope2_iter": 7, "slope3_iter": 8, "line2d_iter": 9, "hessian": 13, "r_only": 6}
+
+
+def binding_pairs_per_clk(ops: float) -> float:
+    """Pairs/clk/SM of a loop with one MUFU.EX2 and `ops` FMA-pipe lane-ops per pair: the lower
+    of the MUFU rate and the measured register-operand FMA-pipe rate."""
+    return min(MUFU_PER_SM_CLK, FMA_REG_LANES / ops)
 
 
 def peaks_json():
@@ -557,6 +567,23 @@ def main():
                                "FFMA2 with register operands, tools/pipe_microbench.cu)",
                  "frac_at_measured_clock": (pairs_s / (N_SM * MUFU_PER_SM_CLK * clk["sm_mhz"] * 1e6)
                                             if clk.get("sm_mhz") else None)}
+        if ph == "multistart":
+            # the binding pipe of the loop: MUFU or the FMA pipe at its measured register-operand rate
+            if a.update == "newton":
+                q = len(spec.newton[0])
+                ev_mean = pairs_ms / max(1.0, float(batch.n_hits) * cfg.n_seeds)
+                cyc = (q / binding_pairs_per_clk(FMA_OPS["hessian"])
+                       + max(0.0, ev_mean - q) / binding_pairs_per_clk(FMA_OPS["r_only"])) / ev_mean
+                basis = (f"{q} Hessian-mode evaluations (13 FMA-pipe lane-ops/pair) and {ev_mean - q:.2f} R-only "
+                         f"evaluations (6) per seed on average")
+            else:
+                ops = FMA_OPS[{C.SLOPE2: "slope2_iter", C.SLOPE3: "slope3_iter"}.get(cfg.model, "line2d_iter")]
+                cyc = 1.0 / binding_pairs_per_clk(ops)
+                basis = f"{ops} FMA-pipe lane-ops per pair in the iterations"
+            bpeak = N_SM * fmax / cyc
+            r["binding"] = {"peak_pairs_per_s": bpeak, "frac": pairs_s / bpeak,
+                            "basis": basis + f"; FMA pipe at {FMA_REG_LANES} lanes/clk/SM (FFMA2, register operands, "
+                                             "tools/pipe_microbench.cu), MUFU at 16/clk/SM: the lower rate binds"}
         r.update({"launch_ms": avg_ms, "pairs_per_launch": per_launch, "pairs_per_s": pairs_s,
                   "share_of_step": phase_med[ph] / ms_step, "traffic": None,
                   "timing": f"median over {a.steps} steps of the phase's CUDA-event time per step"})
