@@ -148,6 +148,18 @@ struct HitStage {
         bulk_g2s(buf + (slot ? cap / 2 : 0), g + start, bytes, &bar[slot]);
     }
 
+    // Resident mode only: brings the event's hits into shared memory now (every thread waits), so
+    // the caller can index them before the first pass.  Returns whether they are resident.
+    __device__ __forceinline__ bool load_resident() {
+        if (n <= 0 || n > cap) return false;
+        if (!resident) {
+            if (threadIdx.x == 0) issue(0, n, 0);
+            mbar_wait(&bar[0], 0u);
+            resident = true;
+        }
+        return true;
+    }
+
     // Calls body(const float4* hits, int count) for consecutive chunks covering all hits.
     template <class F>
     __device__ __forceinline__ void pass(F &&body) {

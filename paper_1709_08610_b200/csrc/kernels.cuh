@@ -34,6 +34,7 @@ struct MultistartArgs {
     const float *seeds;
     float *theta_out, *R_out, *grad_out;
     int cap;
+    int compact;  // SLOPE3: hits staged as (x, y) pairs + a per-plane z table (cap float2 slots)
     int e_base;
 };
 

@@ -143,9 +143,88 @@ __device__ __forceinline__ void ms_pass(HitStage &st, const float (&th)[S][3], f
 // is an independent IEEE round-to-nearest operation, so results are bit-identical to the
 // scalar ms_pass.  Per (seed, hit): 8 FMA-pipe lane-ops + 1 MUFU.EX2, i.e. the loop is
 // balanced between the FMA pipe (128 lanes/clk/SM) and MUFU (16/clk/SM).
+// Detector planes of a resident event (hits sorted by z: runs of equal z), built once per CTA so
+// the passes loop plane by plane instead of testing every hit for a plane change.
+constexpr int kMaxPlanes = 64;
+struct PlaneTable {
+    const int *start;  // [np + 1]
+    const float *z;    // [np]
+    int np;            // -1: no table (streaming event, or more than kMaxPlanes runs)
+    const float2 *xy;  // compact stage: (x, y) per hit (z from the table); nullptr: float4 hits
+};
+
+// Compact stage (dense SLOPE3 events, whose float4 stage would leave too few CTAs per SM): every
+// thread converts hits to (x, y) pairs in shared memory (8 B instead of 16 per hit), and the warps
+// list the plane starts in order from the z values in global memory (each warp a contiguous run
+// of hits, then a prefix over the warps).  np = -1 when there are more than kMaxPlanes planes.
+__device__ __forceinline__ PlaneTable build_compact(const float4 *__restrict__ gh, int n, float2 *s_xy,
+                                                    int *s_start, float *s_z, int *s_np, int *s_wcnt) {
+    const int nw = blockDim.x >> 5, w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    for (int k = threadIdx.x; k < n; k += blockDim.x) {
+        const float4 h = __ldg(gh + k);
+        s_xy[k] = make_float2(h.x, h.y);
+    }
+    const int seg = (n + nw - 1) / nw, a = min(n, w * seg), b = min(n, a + seg);
+    auto flag = [&](int k) { return k < b && (k == 0 || !(__ldg(&gh[k].z) == __ldg(&gh[k - 1].z))); };
+    int cnt = 0;
+    for (int base = a; base < b; base += 32) cnt += __popc(__ballot_sync(0xffffffffu, flag(base + lane)));
+    if (lane == 0) s_wcnt[w] = cnt;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        int acc = 0;
+        for (int i = 0; i < nw; ++i) {
+            const int c = s_wcnt[i];
+            s_wcnt[i] = acc;
+            acc += c;
+        }
+        s_start[min(acc, kMaxPlanes)] = n;
+        *s_np = (acc <= kMaxPlanes) ? acc : -1;
+    }
+    __syncthreads();
+    int off = s_wcnt[w];
+    for (int base = a; base < b; base += 32) {
+        const int k = base + lane;
+        const bool f = flag(k);
+        const unsigned bal = __ballot_sync(0xffffffffu, f);
+        const int pos = off + __popc(bal & ((1u << lane) - 1u));
+        if (f && pos < kMaxPlanes) {
+            s_start[pos] = k;
+            s_z[pos] = __ldg(&gh[k].z);
+        }
+        off += __popc(bal);
+    }
+    __syncthreads();
+    return PlaneTable{s_start, s_z, *s_np, s_xy};
+}
+
+// warp 0 lists the starts of the runs of equal z in order; every thread returns the table
+__device__ __forceinline__ PlaneTable build_planes(const float4 *h, int n, int *s_start, float *s_z, int *s_np) {
+    if (threadIdx.x < 32) {
+        const int lane = threadIdx.x;
+        int cnt = 0;
+        for (int base = 0; base < n; base += 32) {
+            const int k = base + lane;
+            const bool f = k < n && (k == 0 || !(h[k].z == h[k - 1].z));
+            const unsigned b = __ballot_sync(0xffffffffu, f);
+            const int pos = cnt + __popc(b & ((1u << lane) - 1u));
+            if (f && pos < kMaxPlanes) {
+                s_start[pos] = k;
+                s_z[pos] = h[k].z;
+            }
+            cnt += __popc(b);
+        }
+        if (lane == 0) {
+            s_start[min(cnt, kMaxPlanes)] = n;
+            *s_np = (cnt <= kMaxPlanes) ? cnt : -1;
+        }
+    }
+    __syncthreads();
+    return PlaneTable{s_start, s_z, *s_np, nullptr};
+}
+
 template <int MODEL, int S, bool ZREF, bool GRAD, bool WANT_R>
 __device__ __forceinline__ void ms_pass_x2(HitStage &st, const float (&th)[S][3], float negK, float zref,
-                                           float (&R)[S], float (&G)[S][4], float sk = 0.f) {
+                                           float (&R)[S], float (&G)[S][4], float sk, const PlaneTable &pt) {
     static_assert(S % 2 == 0, "seed pairs");
     constexpr int NP = S / 2;
     float2 mtx[NP], mty[NP], r2[NP], qx[NP], qy[NP], gx[NP], gy[NP], ax[NP], ay[NP], dh[NP], dl[NP];
@@ -180,11 +259,13 @@ __device__ __forceinline__ void ms_pass_x2(HitStage &st, const float (&th)[S][3]
             qx[p] = qy[p] = zero;
         }
     };
-    // one hit against every seed pair of the thread
-    auto hit = [&](const float4 hk) {
-        if (hk.z != zprev) {  // warp-uniform plane change
-            if (GRAD) flush();
-            zprev = hk.z;
+    // a new detector plane at z (the same operations, in the same order, whether found from the
+    // table or by comparing a hit's z with the previous one)
+    auto plane = [&](const float z) {
+        if (GRAD) flush();
+        zprev = z;
+        {
+            const float4 hk = make_float4(0.f, 0.f, z, 0.f);
             if (MODEL == kSlope3) {
 #pragma unroll
                 for (int p = 0; p < NP; ++p) {
@@ -205,6 +286,9 @@ __device__ __forceinline__ void ms_pass_x2(HitStage &st, const float (&th)[S][3]
                 dprev = hk.z;
             }
         }
+    };
+    // one hit against every seed pair of the thread
+    auto body = [&](const float4 hk) {
         const float2 X = make_float2(hk.x, hk.x), Y = make_float2(hk.y, hk.y);
 #pragma unroll
         for (int p = 0; p < NP; ++p) {
@@ -237,10 +321,34 @@ __device__ __forceinline__ void ms_pass_x2(HitStage &st, const float (&th)[S][3]
             }
         }
     };
-    st.pass([&](const float4 *h, int len) {
+    if (pt.np >= 0 && pt.xy) {  // compact stage: (x, y) pairs, plane by plane
+        for (int pl = 0; pl < pt.np; ++pl) {
+            const int k1 = pt.start[pl + 1];
+            plane(pt.z[pl]);
 #pragma unroll 2
-        for (int k = 0; k < len; ++k) hit(h[k]);
-    });
+            for (int k = pt.start[pl]; k < k1; ++k) {
+                const float2 q = pt.xy[k];
+                body(make_float4(q.x, q.y, 0.f, 0.f));  // (SLOPE3's body reads x and y only)
+            }
+        }
+    } else if (pt.np >= 0) {  // resident event: plane by plane
+        const float4 *h = st.buf;
+        for (int pl = 0; pl < pt.np; ++pl) {
+            const int k1 = pt.start[pl + 1];
+            plane(pt.z[pl]);
+#pragma unroll 2
+            for (int k = pt.start[pl]; k < k1; ++k) body(h[k]);
+        }
+    } else {
+        st.pass([&](const float4 *h, int len) {
+#pragma unroll 2
+            for (int k = 0; k < len; ++k) {
+                const float4 hk = h[k];
+                if (hk.z != zprev) plane(hk.z);  // warp-uniform plane change
+                body(hk);
+            }
+        });
+    }
     if (GRAD) flush();
 #pragma unroll
     for (int p = 0; p < NP; ++p) {
@@ -259,11 +367,11 @@ __device__ __forceinline__ void ms_pass_x2(HitStage &st, const float (&th)[S][3]
 
 template <int MODEL, int S, bool ZREF, bool GRAD, bool WANT_R>
 __device__ __forceinline__ void ms_eval(HitStage &st, const float (&th)[S][3], float negK, float zref,
-                                        float (&R)[S], float (&G)[S][4], float sk) {
+                                        float (&R)[S], float (&G)[S][4], float sk, const PlaneTable &pt) {
     if constexpr (MODEL == kLine2D)
         ms_pass<MODEL, S, ZREF, GRAD>(st, th, negK, zref, R, G);
     else
-        ms_pass_x2<MODEL, S, ZREF, GRAD, WANT_R>(st, th, negK, zref, R, G, sk);
+        ms_pass_x2<MODEL, S, ZREF, GRAD, WANT_R>(st, th, negK, zref, R, G, sk, pt);
 }
 
 template <int MODEL, int S>
@@ -291,7 +399,21 @@ multistart_kernel(MultistartArgs a) {
     const int e = a.e_base + blockIdx.y;
     const int start = a.offsets[e], nh = a.offsets[e + 1] - start;
     HitStage st;
-    st.init(s_hits, s_bar, a.hits + start, nh, a.cap);
+    // compact SLOPE3 stage: a.cap float2 slots, i.e. a.cap / 2 float4 slots for the fallback stage
+    st.init(s_hits, s_bar, a.hits + start, nh, (MODEL == kSlope3 && a.compact) ? a.cap / 2 : a.cap);
+    __shared__ int s_pstart[kMaxPlanes + 1], s_np, s_wcnt[T / 32];
+    __shared__ float s_pz[kMaxPlanes];
+    PlaneTable pt{nullptr, nullptr, -1, nullptr};
+    // SLOPE3 only: its plane change (two TwoSums and the scaled tails per seed pair) is the heavy
+    // one; for SLOPE2 the per-hit test measured cheaper than the per-plane loop (cfg3 106.1 vs
+    // 109.5 ms per 1000 events; cfg4 98.5 -> 97.1 ms per 200, cfg4 dense 115.7 -> 109.3 per 50)
+    if (MODEL == kSlope3 && a.compact) {
+        if (nh > 0 && nh <= a.cap)
+            pt = build_compact(a.hits + start, nh, reinterpret_cast<float2 *>(s_hits), s_pstart, s_pz, &s_np, s_wcnt);
+        if (pt.np < 0) pt = PlaneTable{nullptr, nullptr, -1, nullptr};  // too many planes: float4 stage streams
+    } else if (MODEL == kSlope3 && st.load_resident()) {
+        pt = build_planes(st.buf, nh, s_pstart, s_pz, &s_np);
+    }
 
     int sid[S];
     float th[S][3];
@@ -305,7 +427,7 @@ multistart_kernel(MultistartArgs a) {
 
     float R[S], G[S][4], g[S][3];
     for (int it = 0; it < a.n_iters; ++it) {
-        ms_eval<MODEL, S, ZREF, true, false>(st, th, a.negK, a.z_ref, R, G, a.sk);
+        ms_eval<MODEL, S, ZREF, true, false>(st, th, a.negK, a.z_ref, R, G, a.sk, pt);
         ms_gradient<MODEL, S>(th, G, (MODEL == kSlope3) ? a.c2s : a.c2, g);
 #pragma unroll
         for (int s = 0; s < S; ++s)
@@ -314,10 +436,10 @@ multistart_kernel(MultistartArgs a) {
                 th[s][i] = fminf(fmaxf(__fmaf_rn(a.step, g[s][i], th[s][i]), a.lo[i]), a.hi[i]);
     }
     if (a.grad_out) {
-        ms_eval<MODEL, S, ZREF, true, true>(st, th, a.negK, a.z_ref, R, G, a.sk);
+        ms_eval<MODEL, S, ZREF, true, true>(st, th, a.negK, a.z_ref, R, G, a.sk, pt);
         ms_gradient<MODEL, S>(th, G, (MODEL == kSlope3) ? a.c2s : a.c2, g);
     } else {
-        ms_eval<MODEL, S, ZREF, false, true>(st, th, a.negK, a.z_ref, R, G, a.sk);
+        ms_eval<MODEL, S, ZREF, false, true>(st, th, a.negK, a.z_ref, R, G, a.sk, pt);
     }
 #pragma unroll
     for (int s = 0; s < S; ++s) {
@@ -340,7 +462,7 @@ template <int MODEL, bool ZREF, int T>
 static cudaError_t launch_ms_t(const MultistartArgs &a0, int n_events, cudaStream_t stream) {
     constexpr int S = (MODEL == kSlope3) ? RETINA_MS3_SEEDS : RETINA_MS_SEEDS;
     auto kern = multistart_kernel<MODEL, S, ZREF, T>;
-    const size_t smem = (size_t)a0.cap * sizeof(float4);
+    const size_t smem = (size_t)a0.cap * (a0.compact ? sizeof(float2) : sizeof(float4));
     cudaError_t err = ensure_dynamic_smem(kern, smem);
     if (err != cudaSuccess) return err;
     const int blocks = (a0.n_seeds + T * S - 1) / (T * S);
@@ -356,11 +478,14 @@ static cudaError_t launch_ms_t(const MultistartArgs &a0, int n_events, cudaStrea
 }
 
 template <int MODEL, bool ZREF>
-static cudaError_t launch_ms(const MultistartArgs &a, int n_events, cudaStream_t stream) {
-    // resident 128-thread CTAs the hit stage allows per SM (227 KB of shared memory)
-    const size_t per_cta = (size_t)a.cap * sizeof(float4) + 1024;
-    const int fit = (int)((227 * 1024) / per_cta);
+static cudaError_t launch_ms(const MultistartArgs &a0, int n_events, cudaStream_t stream) {
+    MultistartArgs a = a0;
     const int want = (MODEL == kSlope3) ? RETINA_MS3_MINB : RETINA_MS_MINB;
+    // resident 128-thread CTAs the hit stage allows per SM (227 KB of shared memory); a SLOPE3
+    // stage that would allow fewer than `want` is staged compactly ((x, y) + plane table, 8 B/hit)
+    a.compact = (MODEL == kSlope3 && (int)((227 * 1024) / ((size_t)a.cap * sizeof(float4) + 1024)) < want) ? 1 : 0;
+    const size_t per_cta = (size_t)a.cap * (a.compact ? sizeof(float2) : sizeof(float4)) + 1024;
+    const int fit = (int)((227 * 1024) / per_cta);
     if (fit >= want || MODEL == kLine2D) return launch_ms_t<MODEL, ZREF, kMsThreads>(a, n_events, stream);
     if (2 * fit >= want) return launch_ms_t<MODEL, ZREF, 2 * kMsThreads>(a, n_events, stream);
     return launch_ms_t<MODEL, ZREF, 4 * kMsThreads>(a, n_events, stream);

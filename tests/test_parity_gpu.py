@@ -727,6 +727,40 @@ def test_multistart_and_newton_streaming_hits(model, z_ref):
         assert PU.t1_response(Rr[0, s], r)[0]
 
 
+def test_multistart_slope3_compact_stage_and_many_planes():
+    """SLOPE3 events too large for six float4 stages per SM are staged compactly ((x, y) pairs + a
+    plane table): a dense 26-plane event (compact path) and an event whose hits all have distinct
+    z (more than 64 planes: the compact attempt falls back to the float4 stage, streaming) both
+    match the oracle: states (T5, 20 small steps) and R at theta_out (T1)."""
+    rng = np.random.default_rng(8)
+    hs = []
+    for n, planes in ((6000, True), (3000, False)):
+        h = np.zeros((n, 4), np.float32)
+        z = rng.choice(C.VELO_PLANES, n) if planes else rng.uniform(0.0, 750.0, n)
+        t = rng.uniform(-0.3, 0.3, (n, 2))
+        h[:, 0] = t[:, 0] * z + rng.normal(0, 0.5, n)
+        h[:, 1] = t[:, 1] * z + rng.normal(0, 0.5, n)
+        h[:, 2] = z
+        hs.append(h[np.argsort(h[:, 2], kind="stable")])
+    off = np.array([0, len(hs[0]), len(hs[0]) + len(hs[1])], np.int32)
+    hits = np.concatenate(hs)
+    lo, hi = (-0.3, -0.3, -150.0), (0.3, 0.3, 150.0)
+    seeds = np.stack([rng.uniform(l, u, (2, 600)) for l, u in zip(lo, hi)], axis=-1).astype(np.float32)
+    sigma = 0.88
+    step = C.step_slope3(sigma)
+    ev = R.Events.from_numpy(off, hits)
+    th, Rr, _ = R.retina_multistart_optimize(ev, C.SLOPE3, sigma, dev(seeds), 20, step, lo, hi)
+    torch.cuda.synchronize()
+    th, Rr = th.cpu().numpy(), Rr.cpu().numpy()
+    rth, _, _ = ora.multistart(C.SLOPE3, off, hits, seeds, sigma, 20, step, lo, hi, want_grad=False)
+    ranges = np.array(hi) - np.array(lo)
+    assert np.max(np.abs(th - rth) / ranges) <= 1e-3
+    for e in range(2):
+        for s in range(0, 600, 61):
+            r, _, _ = ora.point(C.SLOPE3, hits[off[e]:off[e + 1]], th[e, s].astype(np.float64), sigma)
+            assert PU.t1_response(Rr[e, s], r)[0], (e, s)
+
+
 @pytest.mark.parametrize("name", ["cfg2", "cfg3", "cfg4"])
 def test_pipeline_cuda_graph_replay_bitwise(name):
     """The whole pass captured in a CUDA graph and replayed gives the eager results bit for bit;
