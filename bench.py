@@ -50,8 +50,10 @@ FMA_OPS = {"slope2_iter": 7, "slope3_iter": 8, "line2d_iter": 9, "hessian": 13, 
 
 def binding_pairs_per_clk(ops: float) -> float:
     """Pairs/clk/SM of a loop with one MUFU.EX2 and `ops` FMA-pipe lane-ops per pair: the lower
-    of the MUFU rate and the measured register-operand FMA-pipe rate."""
-    return min(MUFU_PER_SM_CLK, FMA_REG_LANES / ops)
+    of the MUFU rate and the FMA pipe's nominal 128 lanes/clk/SM (measured 121.5 for FFMA with
+    immediate operands; 85-97 for FFMA2 with register operands, so loops near the FMA bound land
+    below 1.0 of it)."""
+    return min(MUFU_PER_SM_CLK, FMA_PER_SM_CLK / ops)
 
 
 def peaks_json():
@@ -582,8 +584,9 @@ def main():
                 basis = f"{ops} FMA-pipe lane-ops per pair in the iterations"
             bpeak = N_SM * fmax / cyc
             r["binding"] = {"peak_pairs_per_s": bpeak, "frac": pairs_s / bpeak,
-                            "basis": basis + f"; FMA pipe at {FMA_REG_LANES} lanes/clk/SM (FFMA2, register operands, "
-                                             "tools/pipe_microbench.cu), MUFU at 16/clk/SM: the lower rate binds"}
+                            "basis": basis + f"; FMA pipe at its nominal {FMA_PER_SM_CLK} lanes/clk/SM (measured "
+                                             f"{FMA_REG_LANES} for FFMA2 with register operands, tools/pipe_microbench.cu), "
+                                             "MUFU at 16/clk/SM: the lower rate binds"}
         r.update({"launch_ms": avg_ms, "pairs_per_launch": per_launch, "pairs_per_s": pairs_s,
                   "share_of_step": phase_med[ph] / ms_step, "traffic": None,
                   "timing": f"median over {a.steps} steps of the phase's CUDA-event time per step"})
