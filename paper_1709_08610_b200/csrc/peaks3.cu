@@ -48,9 +48,15 @@ constexpr int kCThreads = RETINA_P3_THREADS;  // consumer threads of a brick CTA
 constexpr int kDefer = RETINA_P3_DEFER;
 constexpr int kRing = RETINA_P3_RING;  // plane slots: i - 1, i, i + 1 resident, the rest in flight
 constexpr int kSegList = 32;      // peaks a segment keeps from pass 1 (more: pass 2 rescans it)
-constexpr int kQueue = 64;        // 4-cell groups a warp queues for the neighbour tests (>= 2 per lane)
+#ifndef RETINA_P3_QUEUE
+#define RETINA_P3_QUEUE 64
+#endif
 constexpr int kBlockCells = RETINA_P3_CELLS;  // cells of one plane block (TJ rows x n2)
-static_assert(kBlockCells <= 8 * RETINA_P3_THREADS, "two 4-cell groups per consumer thread");
+constexpr int kGroups = (kBlockCells + 4 * RETINA_P3_THREADS - 1) / (4 * RETINA_P3_THREADS);  // 4-cell groups per thread
+static_assert(kGroups >= 1 && kGroups <= 16, "4-cell groups per consumer thread");
+// 4-cell groups a warp queues for the neighbour tests: at least one plane's worth (32 kGroups)
+constexpr int kQueue = RETINA_P3_QUEUE > 32 * kGroups ? RETINA_P3_QUEUE : 32 * kGroups;
+
 constexpr int kMaxSlotFloats = 10240;  // 40 KB per ring slot at most (kRing slots <= 200 KB)
 
 // rows per column block for a given row length (n2 % 4 == 0, n2 <= 2048)
@@ -183,10 +189,10 @@ __global__ void __launch_bounds__(kCThreads + 32) peaks3_brick_kernel(PeakArgs a
         const float thr = a.threshold;
         // this thread's two 4-cell groups of every plane block (fixed over the planes): position and
         // shared-memory offset inside a ring slot
-        int gjj[2], gl[2], goff[2];
-        bool gok[2];
+        int gjj[kGroups], gl[kGroups], goff[kGroups];
+        bool gok[kGroups];
 #pragma unroll
-        for (int gi = 0; gi < 2; ++gi) {
+        for (int gi = 0; gi < kGroups; ++gi) {
             const int q = (gi * kCThreads + threadIdx.x) * 4;
             gok[gi] = q < Q;
             gjj[gi] = q / n2;
@@ -254,7 +260,7 @@ __global__ void __launch_bounds__(kCThreads + 32) peaks3_brick_kernel(PeakArgs a
             // groups with some cell >= R0 (~8 % for cfg4) are queued for the neighbour tests
             unsigned grp = 0u;
 #pragma unroll
-            for (int gi = 0; gi < 2; ++gi) {
+            for (int gi = 0; gi < kGroups; ++gi) {
 #ifdef RETINA_P3_NOCOMPUTE
                 continue;
 #endif
@@ -265,7 +271,7 @@ __global__ void __launch_bounds__(kCThreads + 32) peaks3_brick_kernel(PeakArgs a
             const int nc = __popc(grp);
             const unsigned who = __ballot_sync(0xffffffffu, nc != 0);
             if (who) {
-                const int total = __reduce_add_sync(0xffffffffu, nc);  // <= 64 = kQueue
+                const int total = __reduce_add_sync(0xffffffffu, nc);  // <= 32 kGroups <= kQueue
                 if (nq + total > kQueue) flush();
                 if (nq == 0) q0 = i;
                 // positions by a shared counter: the order inside the queue does not matter
