@@ -21,10 +21,11 @@
 // first kSegList peaks.  Measured on cfg4 (256^3 fp32 grids, B200): 0.44 of HBM per event grid
 // (pure streaming through the same ring: 1.0), from 0.11 for the per-cell global-load scan.
 //
-// Pass 2 (peaks3_gather_kernel, one CTA per event): exclusive scan of the segment counts in
-// segment order (= ascending linear index), each segment's list sorted and copied to its offset
-// (up to `capacity`), and, for a segment with more than kSegList peaks, a rescan of its cells
-// with the same rule.  Integer sums in a fixed order: bit-deterministic, identical to the
+// Pass 2 (peaks3_chunk_sum_kernel + peaks3_gather_kernel, one CTA per chunk of 512 segments and
+// event): exclusive scan of the segment counts in segment order (= ascending linear index; a
+// chunk's offset is the sum of the earlier chunks' totals), each segment's list sorted and copied
+// to its offset (up to `capacity`), and, for a segment with more than kSegList peaks, a rescan of
+// its cells with the same rule.  Integer sums in a fixed order: bit-deterministic, identical to the
 // single-CTA path (T3).
 #include "common.cuh"
 #include "kernels.cuh"
@@ -73,16 +74,21 @@ bool peaks3_brick_ok(int n0, int n1, int n2) {
     return (size_t)(tj + 2) * n2 <= (size_t)kMaxSlotFloats;
 }
 
+// pass 2 works on chunks of kB3Threads consecutive segments (one CTA each)
+__host__ __device__ inline long long b3_chunks(long long nseg) { return (nseg + kB3Threads - 1) / kB3Threads; }
+
 size_t peaks3_workspace_bytes(long long n_events, int n0, int n1, int n2) {
     const int tj = b3_rows(n1, n2);
     const long long nseg = (long long)n0 * ((n1 + tj - 1) / tj);
-    // count, offset, then per segment kSegList indices and values
-    return (size_t)(n_events * nseg) * (2 * sizeof(int32_t) + (size_t)kSegList * (sizeof(int32_t) + sizeof(float)));
+    // count, offset, then per segment kSegList indices and values; per chunk its peak total
+    return (size_t)(n_events * nseg) * (2 * sizeof(int32_t) + (size_t)kSegList * (sizeof(int32_t) + sizeof(float))) +
+           (size_t)(n_events * b3_chunks(nseg)) * sizeof(int32_t);
 }
 
 struct SegWs {
     int32_t *count, *offset, *idx;
     float *val;
+    int32_t *ctot;  // [events][chunks]
     __device__ __forceinline__ static SegWs at(int32_t *ws, long long n_ev, long long nseg) {
         SegWs w;
         const long long n = n_ev * nseg;
@@ -90,6 +96,7 @@ struct SegWs {
         w.offset = ws + n;
         w.idx = ws + 2 * n;
         w.val = reinterpret_cast<float *>(ws + 2 * n + n * kSegList);
+        w.ctot = ws + 2 * n + 2 * n * kSegList;
         return w;
     }
 };
@@ -330,34 +337,61 @@ __device__ int b3_rescan(const PeakArgs &a, const float *g, int32_t *oi, float *
     return total;
 }
 
+__device__ __forceinline__ int b3_block_sum(int v, int *s_warp) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    __syncthreads();
+    if (lane == 0) s_warp[warp] = v;
+    __syncthreads();
+    int t = 0;
+    for (int k = 0; k < kB3Threads / 32; ++k) t += s_warp[k];
+    return t;
+}
+
+// pass 2a: the peak total of every chunk of kB3Threads segments (grid (chunks, events))
+__global__ void __launch_bounds__(kB3Threads) peaks3_chunk_sum_kernel(PeakArgs a, int NJB, int32_t *ws) {
+    __shared__ int s_warp[kB3Threads / 32];
+    const long long nseg = (long long)a.n0 * NJB, nch = b3_chunks(nseg);
+    const SegWs w = SegWs::at(ws, gridDim.y, nseg);
+    const long long s = (long long)blockIdx.x * kB3Threads + threadIdx.x;
+    const int n = (s < nseg) ? w.count[(int64_t)blockIdx.y * nseg + s] : 0;
+    const int t = b3_block_sum(n, s_warp);
+    if (threadIdx.x == 0) w.ctot[(int64_t)blockIdx.y * nch + blockIdx.x] = t;
+}
+
+// pass 2b (grid (chunks, events)): the chunk's offset is the sum of the earlier chunks' totals;
+// a block scan places its segments, whose lists are sorted and copied; a segment with more than
+// kSegList peaks is rescanned in place; the last chunk writes the event's true count
 __global__ void __launch_bounds__(kB3Threads) peaks3_gather_kernel(PeakArgs a, int NJB, const int32_t *ws) {
     __shared__ int s_warp[kB3Threads / 32];
-    const int e = a.e_base + blockIdx.x;
-    const long long nseg = (long long)a.n0 * NJB;
-    const SegWs w = SegWs::at(const_cast<int32_t *>(ws), gridDim.x, nseg);
-    const int64_t sb = (int64_t)blockIdx.x * nseg;
+    const int e = a.e_base + blockIdx.y, c = blockIdx.x;
+    const long long nseg = (long long)a.n0 * NJB, nch = b3_chunks(nseg);
+    const SegWs w = SegWs::at(const_cast<int32_t *>(ws), gridDim.y, nseg);
+    const int64_t sb = (int64_t)blockIdx.y * nseg;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     int32_t *oi = a.idx + (int64_t)e * a.capacity;
     float *ov = a.val + (int64_t)e * a.capacity;
-    int running = 0;
+    int pre = 0;
+    for (long long k = threadIdx.x; k < c; k += kB3Threads) pre += w.ctot[(int64_t)blockIdx.y * nch + k];
+    const int prefix = b3_block_sum(pre, s_warp);
+    __syncthreads();
+    const long long s = (long long)c * kB3Threads + threadIdx.x;
+    const int n = (s < nseg) ? w.count[sb + s] : 0;
+    const int incl = b3_warp_incl_scan(n);
+    if (lane == 31) s_warp[warp] = incl;
+    __syncthreads();
+    if (warp == 0) {
+        int x = (lane < kB3Threads / 32) ? s_warp[lane] : 0;
+        x = b3_warp_incl_scan(x);
+        if (lane < kB3Threads / 32) s_warp[lane] = x;
+    }
+    __syncthreads();
+    const int off = prefix + incl - n + (warp > 0 ? s_warp[warp - 1] : 0);
+    const int chunk_total = s_warp[kB3Threads / 32 - 1];
+    if (c == nch - 1 && threadIdx.x == 0) a.cnt[e] = prefix + chunk_total;
     bool overflow = false;
-    // segments in chunks of kB3Threads (coalesced counts), block exclusive scan per chunk
-    for (long long base = 0; base < nseg; base += kB3Threads) {
-        const long long s = base + threadIdx.x;
-        const int n = (s < nseg) ? w.count[sb + s] : 0;
-        const int incl = b3_warp_incl_scan(n);
-        if (lane == 31) s_warp[warp] = incl;
-        __syncthreads();
-        if (warp == 0) {
-            int x = (lane < kB3Threads / 32) ? s_warp[lane] : 0;
-            x = b3_warp_incl_scan(x);
-            if (lane < kB3Threads / 32) s_warp[lane] = x;
-        }
-        __syncthreads();
-        const int off = running + incl - n + (warp > 0 ? s_warp[warp - 1] : 0);
-        running += s_warp[kB3Threads / 32 - 1];
-        __syncthreads();  // s_warp is rewritten by the next chunk
-        if (s >= nseg) continue;
+    if (s < nseg) {
         w.offset[sb + s] = off;
         if (n > kSegList) {
             overflow = true;
@@ -385,45 +419,36 @@ __global__ void __launch_bounds__(kB3Threads) peaks3_gather_kernel(PeakArgs a, i
             }
         }
     }
-    if (threadIdx.x == 0) a.cnt[e] = running;
-    // segments with more than kSegList peaks: rescan them, in segment order, with the whole block
-    if (__syncthreads_or(overflow)) {
-        __shared__ int s_list[kB3Threads];
-        __shared__ int s_nlist;
-        const int tj = b3_rows(a.n1, a.n2);
-        const float *g = a.R + (int64_t)e * a.n0 * a.n1 * a.n2;
-        for (long long base = 0; base < nseg; base += kB3Threads) {
-            const long long s = base + threadIdx.x;
-            const bool ovf = s < nseg && w.count[sb + s] > kSegList;
-            if (!__syncthreads_or(ovf)) continue;
-            // ordered list of this chunk's overflowing segments
-            const unsigned bal = __ballot_sync(0xffffffffu, ovf);
-            if (lane == 0) s_warp[warp] = __popc(bal);
-            __syncthreads();
-            if (threadIdx.x == 0) {
-                int acc = 0;
-                for (int k = 0; k < kB3Threads / 32; ++k) {
-                    const int c = s_warp[k];
-                    s_warp[k] = acc;
-                    acc += c;
-                }
-                s_nlist = acc;
-            }
-            __syncthreads();
-            if (ovf) s_list[s_warp[warp] + __popc(bal & ((1u << lane) - 1u))] = (int)(s - base);
-            __syncthreads();
-            const int nl = s_nlist;
-            for (int k = 0; k < nl; ++k) {
-                const long long sg = base + s_list[k];
-                const int pos0 = w.offset[sb + sg];
-                if (pos0 >= a.capacity) break;           // uniform: later segments start further on
-                const int i = (int)(sg / NJB), jb = (int)(sg - (long long)i * NJB);
-                const int j0 = jb * tj, j1 = min(a.n1, j0 + tj);
-                const int c0 = (int)(((int64_t)i * a.n1 + j0) * a.n2), c1 = (int)(((int64_t)i * a.n1 + j1) * a.n2);
-                b3_rescan(a, g, oi, ov, c0, c1, pos0, s_warp);
-            }
-            __syncthreads();  // s_list / s_warp are rewritten by the next chunk
+    // this chunk's segments with more than kSegList peaks, in order, rescanned by the whole block
+    const unsigned bal = __ballot_sync(0xffffffffu, overflow);
+    __shared__ int s_list[kB3Threads];
+    __shared__ int s_nlist;
+    if (!__syncthreads_or(overflow)) return;
+    if (lane == 0) s_warp[warp] = __popc(bal);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        int acc = 0;
+        for (int k = 0; k < kB3Threads / 32; ++k) {
+            const int cc = s_warp[k];
+            s_warp[k] = acc;
+            acc += cc;
         }
+        s_nlist = acc;
+    }
+    __syncthreads();
+    if (overflow) s_list[s_warp[warp] + __popc(bal & ((1u << lane) - 1u))] = (int)threadIdx.x;
+    __syncthreads();
+    const int nl = s_nlist;
+    const int tj = b3_rows(a.n1, a.n2);
+    const float *g = a.R + (int64_t)e * a.n0 * a.n1 * a.n2;
+    for (int k = 0; k < nl; ++k) {
+        const long long sg = (long long)c * kB3Threads + s_list[k];
+        const int pos0 = w.offset[sb + sg];
+        if (pos0 >= a.capacity) break;  // uniform: later segments start further on
+        const int i = (int)(sg / NJB), jb = (int)(sg - (long long)i * NJB);
+        const int j0 = jb * tj, j1 = min(a.n1, j0 + tj);
+        const int c0 = (int)(((int64_t)i * a.n1 + j0) * a.n2), c1 = (int)(((int64_t)i * a.n1 + j1) * a.n2);
+        b3_rescan(a, g, oi, ov, c0, c1, pos0, s_warp);
     }
 }
 
@@ -444,7 +469,11 @@ cudaError_t launch_find_peaks3_brick(const PeakArgs &a0, int n_events, int32_t *
         peaks3_brick_kernel<<<dim3(NJB, ne), kCThreads + 32, smem, stream>>>(a, TJ, ws);
         err = cudaGetLastError();
         if (err != cudaSuccess) return err;
-        peaks3_gather_kernel<<<ne, kB3Threads, 0, stream>>>(a, NJB, ws);
+        const unsigned nch = (unsigned)b3_chunks((long long)a0.n0 * NJB);
+        peaks3_chunk_sum_kernel<<<dim3(nch, ne), kB3Threads, 0, stream>>>(a, NJB, ws);
+        err = cudaGetLastError();
+        if (err != cudaSuccess) return err;
+        peaks3_gather_kernel<<<dim3(nch, ne), kB3Threads, 0, stream>>>(a, NJB, ws);
         err = cudaGetLastError();
         if (err != cudaSuccess) return err;
     }
