@@ -77,7 +77,7 @@ __device__ __forceinline__ void gen_bar_sync() {  // the 16 generating warps onl
 }
 
 template <int MODEL, bool ZREF>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(32 * PP_WARPS, 1)
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(32 * PP_WARPS)
     grid_tensor16pp_kernel(GridArgs a, int n_items) {
     extern __shared__ __align__(1024) uint8_t s_raw[];
     __shared__ __align__(8) uint64_t s_full[PP_NS];     // even CTA: its 16 generating warps + the odd CTA's relay
