@@ -348,7 +348,10 @@ __device__ __forceinline__ void nt_pass_r_x2(HitStage &st, const float (&th)[S][
 }
 
 #ifndef RETINA_NT_MINB
-#define RETINA_NT_MINB 5  // CTAs per SM the register allocation must allow
+#define RETINA_NT_MINB 4  // CTAs per SM the register allocation must allow (5: 96 registers + spills, 2 % slower)
+#endif
+#ifndef RETINA_NT3_MINB
+#define RETINA_NT3_MINB 3  // SLOPE3 (4 seeds x 3 parameters per thread: 154 registers, no spills)
 #endif
 #ifndef RETINA_NT_X2
 #define RETINA_NT_X2 1  // packed seed-pair passes (0: scalar reference passes)
@@ -534,7 +537,7 @@ __device__ __forceinline__ void nt_line_search_queue(HitStage &st, const NewtonA
 }
 
 template <int MODEL, int S, bool ZREF>
-__global__ void __launch_bounds__(kNtThreads, RETINA_NT_MINB) newton_kernel(NewtonArgs a) {
+__global__ void __launch_bounds__(kNtThreads, (MODEL == kSlope3) ? RETINA_NT3_MINB : RETINA_NT_MINB) newton_kernel(NewtonArgs a) {
     extern __shared__ __align__(16) float4 s_hits[];
     __shared__ __align__(8) uint64_t s_bar[2];
     constexpr int P = (MODEL == kSlope3) ? 3 : 2;
@@ -682,9 +685,12 @@ __global__ void __launch_bounds__(kNtThreads, RETINA_NT_MINB) newton_kernel(Newt
     }
 }
 
+#ifndef RETINA_NT3_SEEDS
+#define RETINA_NT3_SEEDS 4  // SLOPE3 seeds per thread (2 with 5 CTAs/SM: cfg4 Newton 33.5 vs 30.2 ms per 200 events)
+#endif
 template <int MODEL, bool ZREF>
 static cudaError_t launch_nt(const NewtonArgs &a0, int n_events, cudaStream_t stream) {
-    constexpr int S = (MODEL == kSlope3) ? 2 : 4;
+    constexpr int S = (MODEL == kSlope3) ? RETINA_NT3_SEEDS : 4;
     auto kern = newton_kernel<MODEL, S, ZREF>;
     const size_t smem = (size_t)a0.cap * sizeof(float4);
     cudaError_t err = ensure_dynamic_smem(kern, smem);
