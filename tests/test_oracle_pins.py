@@ -557,6 +557,42 @@ def test_P16_newton_converges_to_the_maximiser_found_by_scipy():
         assert R[0, s] >= -res.fun - 1e-12
 
 
+def test_P16_single_hit_newton_step_closed_form():
+    """One Truncated-Newton step on ONE SLOPE2 hit, in closed form.  With u = (x, y)/d, v = u - t,
+    c = 2 d^2 / sigma^2: grad R = R c v and -H = R c (I - c v v^T).  v is an eigenvector of -H with
+    eigenvalue R c (1 - c |v|^2) > 0 when c |v|^2 < 1, and the gradient lies along it, so CG ends
+    after one iteration with p = v / (1 - c |v|^2) (Z23).  For c |v|^2 = 1/4 the full step lands at
+    u - v/3, closer to u, so Armijo accepts alpha = 1 (Z25):  t^1 = t + v / (1 - c |v|^2)."""
+    x, y, z = np.float32(7.25), np.float32(-4.5), np.float32(330.0)
+    h = h4([(x, y, z)])
+    sig = float(np.float32(2.0))
+    d = float(z)
+    u = np.array([float(x), float(y)]) / d
+    c = 2 * d * d / sig ** 2
+    for direction in ([1.0, 0.0], [0.6, -0.8], [-0.28, 0.96]):
+        v = np.array(direction) * np.sqrt(0.25 / c)          # c |v|^2 = 1/4
+        t0 = (u - v).astype(np.float32)
+        v = u - t0.astype(np.float64)                         # exact v for the fp32 seed
+        th, R, _ = ora.newton(C.SLOPE2, [0, 1], h, t0[None, None], [sig], [C.step_slope2(sig)], sig, 8,
+                              (-.3, -.3), (.3, .3))
+        expect = t0.astype(np.float64) + v / (1.0 - c * float(v @ v))
+        assert np.allclose(th[0, 0], expect, rtol=0, atol=1e-13), (th[0, 0], expect)
+        assert np.linalg.norm(th[0, 0] - u) < np.linalg.norm(t0 - u)   # moved toward the hit
+    # beyond the inflection (c |v|^2 > 1) -H is indefinite along v: the CG curvature test fails at
+    # the first iteration and the step falls back to eta grad R (Z24), i.e. t + eta R c v
+    v = np.array([0.6, -0.8]) * np.sqrt(1.5 / c)
+    t0 = (u - v).astype(np.float32)
+    v = u - t0.astype(np.float64)
+    eta = float(np.float32(C.step_slope2(sig)))
+    th, R, _ = ora.newton(C.SLOPE2, [0, 1], h, t0[None, None], [sig], [eta], sig, 8, (-.3, -.3), (.3, .3))
+    R0 = np.exp(-d * d * float(v @ v) / sig ** 2)
+    step = eta * R0 * c * v
+    # Armijo on the fallback step: alpha = 2^-k for the first k whose trial passes; the
+    # closed-form trial t0 + alpha step must be the result for some k <= 8
+    cands = [t0.astype(np.float64) + 0.5 ** k * step for k in range(9)]
+    assert min(np.abs(th[0, 0] - q).max() for q in cands) <= 1e-13
+
+
 def test_P16_newton_ascent_identities_and_fallback():
     cfg = C.CFG2
     b = G.make_batch(cfg, [0])
