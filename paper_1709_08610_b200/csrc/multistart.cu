@@ -6,9 +6,12 @@
 // Mapping (K4): grid = (seed blocks, events), 128 threads per CTA, each thread
 // owns S = 8 seeds (lanes over consecutive seeds: coalesced seed loads / stores).  The event's
 // hits are staged ONCE in shared memory by a TMA bulk copy and stay resident for all
-// n_iters + 1 passes when they fit (HitStage); otherwise they stream per pass.  Each pass
-// accumulates, per seed, R = sum w and the raw gradient sums in registers, in hit-array order;
-// the 2/sigma^2 factor is applied once per seed.
+// n_iters + 1 passes when they fit (HitStage); otherwise they stream per pass.  SLOPE3 CTAs also
+// build a table of the event's detector planes once and loop plane by plane; a dense SLOPE3
+// event whose float4 stage would limit occupancy is staged as (x, y) pairs + that table.  Each
+// pass accumulates, per seed, R = sum w and the raw gradient sums in registers, in hit-array
+// order; the 2/sigma^2 factor is applied once per seed.  SLOPE3 forms its residuals already
+// scaled by sqrt(K) (see ms_pass_x2), so its gradient factor is c2 / sqrt(K).
 //
 // Gradient (chain rule through s^2):
 //   LINE2D  s = y - a x - b:           dR/da = c2 sum w s x,   dR/db = c2 sum w s
