@@ -82,8 +82,16 @@ __device__ __forceinline__ uint32_t mapa_rank(uint32_t saddr, uint32_t rank) {
     asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(saddr), "r"(rank));
     return r;
 }
+// Arrive on a barrier of the peer CTA.  Every hand-off through these barriers publishes shared-memory
+// (or TMEM) state only -- operand stages, accumulator buffers -- never global memory, so the release
+// is restricted to shared::cta operations: MEMBAR.CTA + FENCE.VIEW.ASYNC instead of the MEMBAR.GPU
+// a plain release.cluster arrive costs (a GPU-scope fence also waits for the epilogue's outstanding
+// global stores).  Pattern: release fence, then a relaxed arrive.
 __device__ __forceinline__ void mbar_arrive_remote(uint32_t cluster_addr) {
-    asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+    asm volatile(
+        "fence.release.sync_restrict::shared::cta.cluster;\n\t"
+        "mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr)
+        : "memory");
 }
 __device__ __forceinline__ void mbar_wait_cluster(uint64_t *bar, uint32_t parity) {
     uint32_t done;
