@@ -102,8 +102,9 @@ void ora_point(int model, const float *hits, int n, double z_ref, const double *
     }
 }
 
-/* Eq. (2): R at every node tuple of every event.  out is [E][n0][n1]([n2]),
- * last axis fastest.  nodes_k are fp32 node tables (reading Z4). */
+/* Eq. (2): R at every node tuple of every event.  out is [E][n0][n1] (P = 2) or
+ * [E][n2][n0][n1] (P = 3: one [n0][n1] plane per z0 node; reading Z37), last axis fastest.
+ * nodes_k are fp32 node tables (reading Z4). */
 void ora_grid(int model, int n_events, const int32_t *offsets, const float *hits, double z_ref,
               double sigma, const int32_t *axis_len, const float *nodes0, const float *nodes1,
               const float *nodes2, double *out) {
@@ -120,7 +121,7 @@ void ora_grid(int model, int n_events, const int32_t *offsets, const float *hits
                     double th[3] = {nodes0[i], nodes1[j], P == 3 ? nodes2[l] : 0.0};
                     double R;
                     ora_point(model, h, n, z_ref, th, sigma, &R, NULL, NULL);
-                    out[e * per_event + (i * n1 + j) * n2 + l] = R;
+                    out[e * per_event + (l * n0 + i) * n1 + j] = R;
                 }
             }
         }
@@ -129,7 +130,9 @@ void ora_grid(int model, int n_events, const int32_t *offsets, const float *hits
 
 /* Step (iii), reading Z6: cell c is a peak iff R_c >= R0 and
  * R_c > R_n for every EXISTING neighbour n (3^P - 1 of them in the interior;
- * boundary cells have fewer).  Peaks are listed in ascending linear index;
+ * boundary cells have fewer).  The rule is symmetric in the axes, so it is applied to the
+ * grid as a dense row-major array: axis_len is its shape in memory order ((n2, n0, n1) for a
+ * P = 3 grid, reading Z37).  Peaks are listed in ascending linear index;
  * count is the true count, entries past `capacity` are dropped. */
 void ora_peaks(const double *grid, int n_events, int P, const int32_t *axis_len, double threshold,
                int capacity, int32_t *peak_index, double *peak_value, int32_t *peak_count) {
@@ -283,15 +286,16 @@ void ora_merge(int n_events, int n_seeds, int P, const double *theta, const doub
 void ora_estimate(const double *grid, int n_events, int P, const int32_t *axis_len, const float *nodes0,
                   const float *nodes1, const float *nodes2, const int32_t *peak_index,
                   const int32_t *peak_count, int capacity, double *theta) {
+    /* axis_len in parameter order (tx, ty[, z0]); cell (i, j[, l]) sits at (l n0 + i) n1 + j (Z37) */
     const int64_t n[3] = {axis_len[0], axis_len[1], P == 3 ? axis_len[2] : 1};
     const int64_t per_event = n[0] * n[1] * n[2];
-    const int64_t stride[3] = {n[1] * n[2], n[2], 1};
+    const int64_t stride[3] = {n[1], 1, n[0] * n[1]};
     const float *nodes[3] = {nodes0, nodes1, nodes2};
     for (int e = 0; e < n_events; ++e) {
         const int cnt = peak_count[e] < capacity ? peak_count[e] : capacity;
         for (int p = 0; p < cnt; ++p) {
             const int64_t c = peak_index[(int64_t)e * capacity + p];
-            const int64_t ci[3] = {c / stride[0], (c / stride[1]) % n[1], c % n[2]};
+            const int64_t ci[3] = {(c / n[1]) % n[0], c % n[1], c / (n[0] * n[1])};
             const double *g = grid + e * per_event;
             for (int i = 0; i < P; ++i) {
                 double t = nodes[i][ci[i]];

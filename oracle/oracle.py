@@ -94,7 +94,7 @@ def point(model: int, hits, theta, sigma: float, z_ref: float = 0.0):
 
 def grid(model: int, offsets, hits, nodes: Sequence[np.ndarray], sigma: float,
          z_ref: float = 0.0) -> np.ndarray:
-    """Eq. (2): float64 [E, n0, n1(, n2)]."""
+    """Eq. (2): float64 [E, n0, n1] (P = 2) or [E, n2, n0, n1] (P = 3, z0 planes; reading Z37)."""
     off = np.ascontiguousarray(np.asarray(offsets, np.int32))
     h = _f32(hits).reshape(-1, 4)
     nd = [_f32(n) for n in nodes]
@@ -102,14 +102,17 @@ def grid(model: int, offsets, hits, nodes: Sequence[np.ndarray], sigma: float,
     assert len(nd) == P
     alen = np.array([len(n) for n in nd], np.int32)
     E = len(off) - 1
-    out = np.zeros((E,) + tuple(alen), np.float64)
+    shape = tuple(alen) if P == 2 else (alen[2], alen[0], alen[1])
+    out = np.zeros((E,) + shape, np.float64)
     lib().ora_grid(model, E, _p(off), _p(h), _f(z_ref), _f(sigma), _p(alen),
                    _p(nd[0]), _p(nd[1]), _p(nd[2]) if P == 3 else None, _p(out))
     return out
 
 
 def peaks(grid_values: np.ndarray, P: int, threshold: float, capacity: int):
-    """Reading Z6 peaks of a [E, n0, n1(, n2)] grid: (index[E,cap], value[E,cap], count[E])."""
+    """Reading Z6 peaks of a [E, d0, d1(, d2)] grid (any axis order: the rule is symmetric; a
+    P = 3 response grid is [E, n2, n0, n1]): (index[E,cap], value[E,cap], count[E]), index =
+    flat offset within the event's grid."""
     g = np.ascontiguousarray(np.asarray(grid_values, np.float64))
     E = g.shape[0]
     alen = np.array(g.shape[1:], np.int32)
@@ -161,7 +164,8 @@ def merge(theta, R, radius, threshold: float, capacity: int, want_members: bool 
 
 
 def estimate(grid_values, nodes: Sequence[np.ndarray], peak_index, peak_count, capacity: int):
-    """Step (iv) quadratic sub-cell estimate (reading Z21): float64 [E, capacity, P]."""
+    """Step (iv) quadratic sub-cell estimate (reading Z21) on a response grid in the Z37 layout
+    ([E, n0, n1] or [E, n2, n0, n1]); nodes in parameter order: float64 [E, capacity, P]."""
     g = np.ascontiguousarray(np.asarray(grid_values, np.float64))
     E = g.shape[0]
     P = g.ndim - 1

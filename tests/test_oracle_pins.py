@@ -247,6 +247,34 @@ def test_P9_noiseless_recovery_grid_and_multistart():
     assert np.all(prev < 0.01 * first)
 
 
+def test_P9_slope3_noiseless_recovery_and_layout():
+    """P = 3 (PAPER.md:47-48 with a free origin z0): noiseless tracks whose (tx, ty, z0) sit on
+    lattice nodes are the grid's peaks, at flat offsets (l n0 + i) n1 + j of the z0-plane layout
+    (reading Z37), and each cell equals the point response at its node tuple."""
+    nodes = [np.linspace(-0.3, 0.3, 31).astype(np.float32), np.linspace(-0.3, 0.3, 29).astype(np.float32),
+             np.linspace(-40.0, 40.0, 9).astype(np.float32)]
+    truth = [(5, 20, 2), (22, 7, 6)]
+    rows = []
+    for (i, j, l) in truth:
+        tx, ty, z0 = (float(nodes[0][i]), float(nodes[1][j]), float(nodes[2][l]))
+        for z in C.VELO_PLANES[1:]:
+            d = z - z0
+            if 5 < math.hypot(tx * d, ty * d) < 40:
+                rows.append((tx * d, ty * d, z))
+    rows.sort(key=lambda r: r[2])
+    h = h4(rows)
+    sig = 0.05
+    Rg = ora.grid(C.SLOPE3, [0, len(h)], h, nodes, sig)
+    assert Rg.shape == (1, 9, 31, 29)
+    idx, _, cnt = ora.peaks(Rg, 3, 2.5, 64)
+    assert sorted(int(v) for v in idx[0, :cnt[0]]) == sorted((l * 31 + i) * 29 + j for i, j, l in truth)
+    rng = np.random.default_rng(7)
+    for _ in range(20):
+        i, j, l = int(rng.integers(31)), int(rng.integers(29)), int(rng.integers(9))
+        R, _, _ = ora.point(C.SLOPE3, h, [nodes[0][i], nodes[1][j], nodes[2][l]], float(np.float32(sig)))
+        assert Rg[0, l, i, j] == R
+
+
 # ---------------------------------------------------------------- P10 (SPEC.md:286-290, 313)
 def _strict_max_scipy(g, thr):
     P = g.ndim
@@ -453,8 +481,11 @@ def test_P14_estimate_exact_on_quadratics(P):
         curv = rng.uniform(0.5, 3.0, P)
         grids = np.meshgrid(*[np.arange(n, dtype=np.float64) for n in shape], indexing="ij")
         g = 100.0 - sum(curv[i] * (grids[i] - (c[i] + off[i])) ** 2 for i in range(P))
+        if P == 3:  # the response layout stores z0 planes outermost (reading Z37)
+            g = np.ascontiguousarray(g.transpose(2, 0, 1))
+        mem_c, mem_shape = (c, shape) if P == 2 else ((c[2], c[0], c[1]), (shape[2], shape[0], shape[1]))
         idx, _, cnt = ora.peaks(g[None], P, 0.0, 16)
-        assert cnt[0] == 1 and idx[0, 0] == np.ravel_multi_index(c, shape)
+        assert cnt[0] == 1 and idx[0, 0] == np.ravel_multi_index(mem_c, mem_shape)
         th = ora.estimate(g[None], nodes, idx, cnt, 16)[0, 0]
         for i in range(P):
             step = float(nodes[i][c[i] + 1]) - float(nodes[i][c[i]])
