@@ -97,7 +97,9 @@ typedef struct {
  *   axis_len:   host int32 [P], each >= 2.
  *   axis_nodes: host array [P] of device fp32 [axis_len[i]] node tables (the caller owns
  *               the node values; they are not recomputed, Z4).
- *   response:   device fp32 [n_events][axis_len[0]]...[axis_len[P-1]], last axis fastest.
+ *   response:   device fp32, last axis fastest: [n_events][axis_len[0]][axis_len[1]] for P = 2;
+ *               [n_events][axis_len[2]][axis_len[0]][axis_len[1]] for P = 3, i.e. one
+ *               (tx, ty) plane per z0 node (Z37; the paper fixes no layout).
  * Returns RETINA_OK, RETINA_EINVAL, RETINA_EUNSUPPORTED or RETINA_ECUDA. */
 int retina_grid_response(const retina_events *ev, int model, float sigma,
                          const int32_t *axis_len, const float *const *axis_nodes,
@@ -130,9 +132,12 @@ int retina_grid_response_ex(const retina_events *ev, int model, float sigma,
  * cell c is reported iff response[c] >= threshold and response[c] > response[n] for every
  * EXISTING neighbour n of its 3^P - 1 neighbourhood (cells on the lattice boundary have
  * fewer neighbours; equal neighbours -- plateaus -- give no peak).
- *   response:    device fp32 [n_events][cells]; P in {2, 3}; axis_len host int32 [P].
+ *   response:    device fp32 [n_events][cells] in the layout retina_grid_response writes; P in
+ *                {2, 3}; axis_len host int32 [P] in parameter order, as there.  The rule is
+ *                symmetric in the axes and is applied in memory order.
  *   capacity:    entries per event of the output lists, >= 0.
- *   peak_index:  device int32 [n_events][capacity], linear cell index, ascending.
+ *   peak_index:  device int32 [n_events][capacity], flat offset of the cell within its event's
+ *                grid ((l n0 + i) n1 + j for P = 3), ascending.
  *   peak_value:  device fp32  [n_events][capacity], response at that cell.
  *   peak_count:  device int32 [n_events], TRUE number of peaks (may exceed capacity). */
 int retina_find_peaks(const float *response, int32_t n_events, int32_t P,

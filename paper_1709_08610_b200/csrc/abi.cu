@@ -141,6 +141,20 @@ int retina_grid_response_ex(const retina_events *ev, int model, float sigma, con
     return RETINA_OK;
 }
 
+// The peak rule is symmetric in the axes, so the finder runs on the grid as a dense array in
+// memory order: (n0, n1) for P = 2, (n2, n0, n1) for P = 3 (z0 planes outermost, Z37).
+static void memory_dims(int P, const int32_t *axis_len, int &d0, int &d1, int &d2) {
+    if (P == 3) {
+        d0 = axis_len[2];
+        d1 = axis_len[0];
+        d2 = axis_len[1];
+    } else {
+        d0 = axis_len[0];
+        d1 = axis_len[1];
+        d2 = 1;
+    }
+}
+
 int retina_find_peaks(const float *response, int32_t n_events, int32_t P, const int32_t *axis_len,
                       float threshold, int32_t capacity, int32_t *peak_index, float *peak_value,
                       int32_t *peak_count, void *stream) {
@@ -161,9 +175,7 @@ int retina_find_peaks(const float *response, int32_t n_events, int32_t P, const 
         return fail(RETINA_EINVAL, "NULL device pointer");
     retina::PeakArgs a{};
     a.R = response;
-    a.n0 = axis_len[0];
-    a.n1 = axis_len[1];
-    a.n2 = (P == 3) ? axis_len[2] : 1;
+    memory_dims(P, axis_len, a.n0, a.n1, a.n2);
     a.P = P;
     a.threshold = threshold;
     a.capacity = capacity;
@@ -180,7 +192,9 @@ size_t retina_find_peaks_workspace_size(int32_t n_events, int32_t P, const int32
     long long cells = 1;
     for (int i = 0; i < P; ++i) cells *= (axis_len[i] > 0 ? axis_len[i] : 0);
     if (cells <= 0 || cells > 0x7fffffffLL) return 0;
-    return retina::peaks_workspace_bytes(n_events, P, axis_len[0], axis_len[1], P == 3 ? axis_len[2] : 1);
+    int d0, d1, d2;
+    memory_dims(P, axis_len, d0, d1, d2);
+    return retina::peaks_workspace_bytes(n_events, P, d0, d1, d2);
 }
 
 int retina_find_peaks_ws(const float *response, int32_t n_events, int32_t P, const int32_t *axis_len,
@@ -206,9 +220,7 @@ int retina_find_peaks_ws(const float *response, int32_t n_events, int32_t P, con
         return fail(RETINA_EINVAL, "workspace of %zu bytes needed (got %zu)", need, workspace_bytes);
     retina::PeakArgs a{};
     a.R = response;
-    a.n0 = axis_len[0];
-    a.n1 = axis_len[1];
-    a.n2 = (P == 3) ? axis_len[2] : 1;
+    memory_dims(P, axis_len, a.n0, a.n1, a.n2);
     a.P = P;
     a.threshold = threshold;
     a.capacity = capacity;

@@ -25,17 +25,12 @@ __global__ void __launch_bounds__(256) estimate_kernel(EstimateArgs a) {
     const int64_t cells = (int64_t)a.n0 * a.n1 * a.n2;
     const float *g = a.R + (int64_t)e * cells;
     const int c = a.idx[(int64_t)e * a.capacity + p];
+    // node indices in parameter order (tx, ty[, z0]); cell (i, j[, l]) at (l n0 + i) n1 + j (Z37)
     int ci[3];
-    if (P == 3) {
-        ci[2] = c % a.n2;
-        ci[1] = (c / a.n2) % a.n1;
-        ci[0] = c / (a.n2 * a.n1);
-    } else {
-        ci[1] = c % a.n1;
-        ci[0] = c / a.n1;
-        ci[2] = 0;
-    }
-    const int stride[3] = {a.n1 * a.n2, a.n2, 1};
+    ci[1] = c % a.n1;
+    ci[0] = (c / a.n1) % a.n0;
+    ci[2] = c / (a.n0 * a.n1);
+    const int stride[3] = {a.n1, 1, a.n0 * a.n1};
     const float r0 = __ldg(g + c);
     const float *nodes[3] = {a.nodes0, a.nodes1, a.nodes2};
     for (int i = 0; i < P; ++i) {

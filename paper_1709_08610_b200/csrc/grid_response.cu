@@ -8,7 +8,8 @@
 //    residual that depends only on the lane's parameter (and the hit) is formed once per
 //    (thread, hit) and reused U times.
 //      LINE2D / SLOPE2: lanes over axis 1, U rows of axis 0.
-//      SLOPE3:          lanes over axis 2 (z0), U rows of axis 1 (ty), one axis-0 value.
+//      SLOPE3:          the same within one z0 plane (layout [n2][n0][n1], Z37): the
+//                       block's z0 node plays SLOPE2's z_ref, d = z - z0 formed exactly once per hit.
 //  * the event's hits are staged in shared memory by TMA bulk copies (HitStage) and read
 //    as warp-uniform LDS.128 broadcasts.
 //  * per (unit, hit): residual by FMA (exact product), s^2, one FMUL by -log2(e)/sigma^2,
@@ -31,39 +32,20 @@ __global__ void __launch_bounds__(256) grid_response_kernel(GridArgs a) {
     HitStage st;
     st.init(s_hits, s_bar, a.hits + start, nh, a.cap);
 
-    int fast, row0, ax0 = 0;  // fast-axis index, first owned slow-axis index, (SLOPE3) axis-0
-    int nfast, nslow;
-    const float *nodes_fast, *nodes_slow;
-    if (MODEL == kSlope3) {
-        const int tl = (a.n2 + 31) / 32, tj = (a.n1 + 8 * U - 1) / (8 * U);
-        int b = blockIdx.x;
-        const int t_l = b % tl;
-        b /= tl;
-        const int t_j = b % tj;
-        ax0 = b / tj;
-        fast = t_l * 32 + lane;
-        row0 = t_j * 8 * U + warp * U;
-        nfast = a.n2;
-        nslow = a.n1;
-        nodes_fast = a.nodes2;
-        nodes_slow = a.nodes1;
-    } else {
-        const int tj = (a.n1 + 31) / 32;
-        const int t_j = blockIdx.x % tj, t_i = blockIdx.x / tj;
-        fast = t_j * 32 + lane;
-        row0 = t_i * 8 * U + warp * U;
-        nfast = a.n1;
-        nslow = a.n0;
-        nodes_fast = a.nodes1;
-        nodes_slow = a.nodes0;
-    }
-    const float pf = __ldg(nodes_fast + min(fast, nfast - 1));
+    // fast-axis index (lanes: axis 1), first owned slow-axis index (axis 0), z0 plane (SLOPE3)
+    const int tj = (a.n1 + 31) / 32, ti = (a.n0 + 8 * U - 1) / (8 * U);
+    const int l = (MODEL == kSlope3) ? (int)(blockIdx.x / (tj * ti)) : 0;
+    const int b = (MODEL == kSlope3) ? (int)(blockIdx.x % (tj * ti)) : (int)blockIdx.x;
+    const int t_j = b % tj, t_i = b / tj;
+    const int fast = t_j * 32 + lane, row0 = t_i * 8 * U + warp * U;
+    const int nfast = a.n1, nslow = a.n0;
+    const float pf = __ldg(a.nodes1 + min(fast, nfast - 1));
     float ps[U];
 #pragma unroll
-    for (int u = 0; u < U; ++u) ps[u] = __ldg(nodes_slow + min(row0 + u, nslow - 1));
-    const float p0 = (MODEL == kSlope3) ? __ldg(a.nodes0 + ax0) : 0.f;  // tx (SLOPE3)
+    for (int u = 0; u < U; ++u) ps[u] = __ldg(a.nodes0 + min(row0 + u, nslow - 1));
     const float negK = a.negK;
-    const float zref = a.z_ref;
+    constexpr bool EXACT_D = ZREF || MODEL == kSlope3;  // d = z - z_ref (or z - z0) as dh + dl
+    const float zref = (MODEL == kSlope3) ? __ldg(a.nodes2 + l) : a.z_ref;
 
     float acc[U];
 #pragma unroll
@@ -73,10 +55,10 @@ __global__ void __launch_bounds__(256) grid_response_kernel(GridArgs a) {
 #pragma unroll 2
         for (int k = 0; k < len; ++k) {
             const float4 hk = h[k];
-            if (MODEL == kSlope2) {
+            if (MODEL == kSlope2 || MODEL == kSlope3) {
                 // lane parameter = ty (axis 1), rows = tx (axis 0)
                 float sy, dh = hk.z, dl = 0.f;
-                if (ZREF) {
+                if (EXACT_D) {
                     two_sum(hk.z, -zref, dh, dl);
                     sy = __fmaf_rn(-pf, dl, __fmaf_rn(-pf, dh, hk.y));
                 } else {
@@ -85,21 +67,9 @@ __global__ void __launch_bounds__(256) grid_response_kernel(GridArgs a) {
                 const float sy2 = __fmul_rn(sy, sy);
 #pragma unroll
                 for (int u = 0; u < U; ++u) {
-                    const float sx = ZREF ? __fmaf_rn(-ps[u], dl, __fmaf_rn(-ps[u], dh, hk.x))
-                                          : __fmaf_rn(-ps[u], hk.z, hk.x);
+                    const float sx = EXACT_D ? __fmaf_rn(-ps[u], dl, __fmaf_rn(-ps[u], dh, hk.x))
+                                             : __fmaf_rn(-ps[u], hk.z, hk.x);
                     const float q = __fmaf_rn(sx, sx, sy2);
-                    acc[u] = __fadd_rn(acc[u], ex2_approx(__fmul_rn(q, negK)));
-                }
-            } else if (MODEL == kSlope3) {
-                // lane parameter = z0 (axis 2), rows = ty (axis 1), block-uniform tx
-                float dh, dl;
-                two_sum(hk.z, -pf, dh, dl);  // d = z - z0 exactly as dh + dl
-                const float sx = __fmaf_rn(-p0, dl, __fmaf_rn(-p0, dh, hk.x));
-                const float sx2 = __fmul_rn(sx, sx);
-#pragma unroll
-                for (int u = 0; u < U; ++u) {
-                    const float sy = __fmaf_rn(-ps[u], dl, __fmaf_rn(-ps[u], dh, hk.y));
-                    const float q = __fmaf_rn(sy, sy, sx2);
                     acc[u] = __fadd_rn(acc[u], ex2_approx(__fmul_rn(q, negK)));
                 }
             } else {  // LINE2D: lane parameter = b (axis 1), rows = a (axis 0)
@@ -121,18 +91,11 @@ __global__ void __launch_bounds__(256) grid_response_kernel(GridArgs a) {
 
     if (fast < nfast) {
         const int64_t cells = (int64_t)a.n0 * a.n1 * (MODEL == kSlope3 ? a.n2 : 1);
-        float *out = a.R + (int64_t)e * cells;
+        float *out = a.R + (int64_t)e * cells + (int64_t)l * a.n0 * a.n1;
 #pragma unroll
         for (int u = 0; u < U; ++u) {
             const int r = row0 + u;
-            if (r < nslow) {
-                int64_t idx;
-                if (MODEL == kSlope3)
-                    idx = ((int64_t)ax0 * a.n1 + r) * a.n2 + fast;
-                else
-                    idx = (int64_t)r * a.n1 + fast;
-                out[idx] = acc[u];
-            }
+            if (r < nslow) out[(int64_t)r * a.n1 + fast] = acc[u];
         }
     }
 }
@@ -143,11 +106,8 @@ static cudaError_t launch_grid(const GridArgs &a0, int n_events, cudaStream_t st
     const size_t smem = (size_t)a0.cap * sizeof(float4);
     cudaError_t err = ensure_dynamic_smem(kern, smem);
     if (err != cudaSuccess) return err;
-    long long tiles;
-    if (MODEL == kSlope3)
-        tiles = (long long)((a0.n2 + 31) / 32) * ((a0.n1 + 8 * U - 1) / (8 * U)) * a0.n0;
-    else
-        tiles = (long long)((a0.n1 + 31) / 32) * ((a0.n0 + 8 * U - 1) / (8 * U));
+    const long long tiles = (long long)((a0.n1 + 31) / 32) * ((a0.n0 + 8 * U - 1) / (8 * U)) *
+                            (MODEL == kSlope3 ? a0.n2 : 1);
     if (tiles > 0x7fffffffLL) return cudaErrorInvalidConfiguration;
     for (int e0 = 0; e0 < n_events; e0 += 65535) {
         GridArgs a = a0;

@@ -107,7 +107,7 @@ __global__ void __launch_bounds__(256, 2) grid_separable_kernel(GridArgs a) {
 
 #define ACC(r, c) (((c) & 1) ? acc[r][(c) >> 1].y : acc[r][(c) >> 1].x)
     const int64_t cells = (int64_t)a.n0 * a.n1 * (MODEL == kSlope3 ? a.n2 : 1);
-    float *out = a.R + (int64_t)e * cells;
+    float *out = a.R + (int64_t)e * cells + (int64_t)l * a.n0 * a.n1;  // z0 plane l (Z37)
 #pragma unroll
     for (int r = 0; r < 8; ++r) {
         const int i = t_m * SB_M + (r < 4 ? tr * 4 + r : 64 + tr * 4 + r - 4);
@@ -115,11 +115,7 @@ __global__ void __launch_bounds__(256, 2) grid_separable_kernel(GridArgs a) {
 #pragma unroll
         for (int half = 0; half < 2; ++half) {
             const int j0 = t_n * SB_N + half * 64 + tc * 4;
-            if (MODEL == kSlope3) {
-#pragma unroll
-                for (int c = 0; c < 4; ++c)
-                    if (j0 + c < a.n1) out[((int64_t)i * a.n1 + j0 + c) * a.n2 + l] = ACC(r, half * 4 + c);
-            } else {
+            {
                 float *p = out + (int64_t)i * a.n1 + j0;
                 if (j0 + 3 < a.n1 && ((reinterpret_cast<uintptr_t>(p) & 15u) == 0)) {
                     *reinterpret_cast<float4 *>(p) =

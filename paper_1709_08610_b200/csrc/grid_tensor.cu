@@ -56,7 +56,7 @@ __device__ __forceinline__ void tc_epilogue(const GridArgs &a, int e, int t_m, i
     const int q = warp & 3, half = warp >> 2;
     const int i = t_m * TC_M + q * 32 + lane;
     const int64_t cells = (int64_t)a.n0 * a.n1 * nl;
-    float *out = a.R + (int64_t)e * cells + (int64_t)i * a.n1 * nl;
+    float *out = a.R + (int64_t)e * cells + ((int64_t)l * a.n0 + i) * a.n1;  // z0 plane l (Z37)
 #pragma unroll 1
     for (int cc = 0; cc < GROUP_COLS / 16; ++cc) {
         const int col = half * GROUP_COLS + cc * 16;
@@ -92,11 +92,7 @@ __device__ __forceinline__ void tc_epilogue(const GridArgs &a, int e, int t_m, i
             for (int x = 0; x < 16; ++x) v[x] = 0u;
         }
         const int j0 = t_n * TC_N + col;
-        if (i < a.n0 && MODEL == kSlope3) {
-#pragma unroll
-            for (int x = 0; x < 16; ++x)
-                if (j0 + x < a.n1) out[(int64_t)(j0 + x) * nl + l] = __uint_as_float(v[x]);
-        } else if (i < a.n0) {
+        if (i < a.n0) {
             if (j0 + 15 < a.n1 && (((uintptr_t)(out + j0)) & 15u) == 0) {
 #pragma unroll
                 for (int x = 0; x < 16; x += 4)
@@ -123,8 +119,7 @@ __global__ void __launch_bounds__(32 * TC_WARPS, RETINA_TC_MINB) grid_tensor_ker
     float4 *s_hits = reinterpret_cast<float4 *>(s_raw + 2 * TC_STAGE_BYTES);  // hit stage after
 
     const int e = a.e_base + blockIdx.y;
-    // block order: z0 index fastest (SLOPE3), so the CTAs resident at once write neighbouring
-    // z0 values of the same (tx, ty) cells and L2 merges their 4-byte stores into full sectors
+    // block order: z0 index fastest (SLOPE3); each block writes row segments of its z0 plane
     const int tn = (a.n1 + TC_N - 1) / TC_N;
     const int nl = (MODEL == kSlope3) ? a.n2 : 1;
     const int l = blockIdx.x % nl, tile = blockIdx.x / nl;

@@ -18,9 +18,10 @@
 // part falls below the fp16 normal range (h 2^9 for h < 2^-23, l 2^21 for l < 2^-35) the absolute
 // error stays <= 2^-45 per term -- far below the T1 floor (1e-11 per cell).
 //
-// A cluster of two CTAs (one TPC) loops over (event, 256 x 256 pair tile [, z0]) work items: a
-// contiguous range for SLOPE2 (one hit load per event), round-robin for SLOPE3 (concurrent clusters
-// write neighbouring z0, the fastest output axis, so L2 merges their 4-byte stores).  Per CTA (rank r):
+// A cluster of two CTAs (one TPC) loops over a contiguous range of (event, [z0 plane,] 256 x 256
+// pair tile) work items, so an event's hits are loaded once per cluster.  Every item writes whole
+// row segments (1 KB per row) of one [n0][n1] plane: a SLOPE3 grid is stored z0 plane by z0 plane
+// (Z37).  Per CTA (rank r):
 //   warps 0-15  generate its 128 A rows (tx) and its half of B (128 ty rows) per 64-hit chunk
 //               into stage c % NS, then arrive on the even CTA's full[stage] (cluster arrive);
 //               hits live in shared memory, reloaded only when the event changes (or windowed
@@ -94,13 +95,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(32 * PP_WARPS)
     const int nl = (MODEL == kSlope3) ? a.n2 : 1;
     const int ppe = pm * tn * nl;  // pair work items per event
     const int cl = blockIdx.x >> 1, ncl = gridDim.x >> 1;
-    // SLOPE2: a contiguous range of items per cluster (the event's hits stay in shared memory);
-    // SLOPE3: items dealt round-robin, so the clusters running at the same time write neighbouring
-    // z0 values of the same cells (z0 is the fastest output axis) and L2 merges their 4-byte stores
-    const bool rr = MODEL == kSlope3;
-    const int t0 = rr ? cl : (int)((long long)cl * n_items / ncl);
-    const int t1 = rr ? n_items : (int)((long long)(cl + 1) * n_items / ncl);
-    const int dt = rr ? ncl : 1;
+    // a contiguous range of items per cluster (the event's hits stay in shared memory)
+    const int t0 = (int)((long long)cl * n_items / ncl), t1 = (int)((long long)(cl + 1) * n_items / ncl);
+    constexpr int dt = 1;
     float4 *s_hits = reinterpret_cast<float4 *>(s_raw + PP_NS * PP_STAGE);
 
     if (warp == 0) {  // two accumulator buffers of 128 lanes x 256 fp32 columns, in both CTAs
@@ -295,7 +292,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(32 * PP_WARPS)
             mbar_wait(&s_acc_full[b], (ti >> 1) & 1);
             tc_fence_after();
             const int i = c.t_m * 128 + q * 32 + lane;
-            float *out = a.R + (int64_t)(a.e_base + c.e) * cells + (int64_t)i * a.n1 * nl;
+            float *out = a.R + (int64_t)(a.e_base + c.e) * cells + ((int64_t)c.l * a.n0 + i) * a.n1;
 #pragma unroll 1
             for (int cc = 0; cc < TC_N / 16; ++cc) {
                 const int col = cc * 16;
@@ -317,11 +314,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(32 * PP_WARPS)
                     for (int x = 0; x < 16; ++x) v[x] = 0u;
                 }
                 const int j0 = c.t_n * TC_N + col;
-                if (i < a.n0 && MODEL == kSlope3) {
-#pragma unroll
-                    for (int x = 0; x < 16; ++x)
-                        if (j0 + x < a.n1) out[(int64_t)(j0 + x) * nl + c.l] = __uint_as_float(v[x]);
-                } else if (i < a.n0) {
+                if (i < a.n0) {
                     if (j0 + 15 < a.n1 && (((uintptr_t)(out + j0)) & 15u) == 0) {
 #pragma unroll
                         for (int x = 0; x < 16; x += 4)

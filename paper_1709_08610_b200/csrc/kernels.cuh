@@ -62,7 +62,7 @@ struct NewtonArgs {
 
 struct PeakArgs {
     const float *R;
-    int n0, n1, n2;  // n2 = 1 for P = 2
+    int n0, n1, n2;  // grid dims in MEMORY order, n2 fastest (P = 3: z0, tx, ty -- DESIGN.md Z37); n2 = 1 for P = 2
     int P;
     float threshold;
     int capacity;
@@ -90,7 +90,7 @@ struct MergeArgs {
 
 struct EstimateArgs {
     const float *R;
-    int n0, n1, n2;  // n2 = 1 for P = 2
+    int n0, n1, n2;  // node counts in parameter order (tx, ty, z0); n2 = 1 for P = 2
     int P;
     int n_events;
     int capacity;

@@ -72,7 +72,7 @@ class RetinaPipeline:
             chunk_events = max(1, min(chunk_events, int(grid_bytes_budget // (4 * cells))))
         self.chunk = min(chunk_events, max(1, max_events))
         self.nodes = [torch.from_numpy(np.ascontiguousarray(n, np.float32)).to(self.device) for n in spec.nodes]
-        shape = tuple(len(n) for n in spec.nodes)
+        shape = R.grid_shape(self.chunk, [len(n) for n in spec.nodes])[1:]  # (n2,) n0, n1: z0 planes outermost
         self.grid_buf = torch.empty((self.chunk,) + shape, dtype=torch.float32, device=self.device) if cells else None
         # With several chunks, the peak scan of chunk c (HBM-bound, small CTAs) runs on a second,
         # higher-priority stream while the tensor-core grid kernel computes chunk c+1 into a second

@@ -157,6 +157,19 @@ class Events:
         return Events(off, h, z_ref, max_event_hits)
 
 
+def grid_shape(n_events: int, axis_len: Sequence[int]) -> tuple:
+    """Shape of a response grid: (E, n0, n1) for P = 2, (E, n2, n0, n1) for P = 3 -- one (tx, ty)
+    plane per z0 node (retina.h; Z37)."""
+    n = [int(v) for v in axis_len]
+    return (int(n_events),) + ((n[2], n[0], n[1]) if len(n) == 3 else tuple(n))
+
+
+def _param_axis_len(grid_dims: Sequence[int]) -> list:
+    """Per-event grid dims (memory order) -> axis_len in parameter order (tx, ty[, z0])."""
+    d = [int(v) for v in grid_dims]
+    return [d[1], d[2], d[0]] if len(d) == 3 else d
+
+
 def retina_grid_response(events: Events, model: int, sigma: float, nodes: Sequence[torch.Tensor],
                          out: Optional[torch.Tensor] = None, stream=None, algorithm: int = GRID_AUTO
                          ) -> torch.Tensor:
@@ -164,7 +177,7 @@ def retina_grid_response(events: Events, model: int, sigma: float, nodes: Sequen
     nodes = [_dev(n, torch.float32) for n in nodes]
     alen, _k1 = _arr(ctypes.c_int32, [n.numel() for n in nodes])
     nptr, _k2 = _arr(ctypes.c_void_p, [n.data_ptr() for n in nodes])
-    shape = (events.n_events,) + tuple(n.numel() for n in nodes)
+    shape = grid_shape(events.n_events, [n.numel() for n in nodes])
     if out is None:
         out = torch.empty(shape, device=events.hits.device, dtype=torch.float32)
     _out("response", out, torch.float32, shape, events.hits.device)
@@ -175,7 +188,9 @@ def retina_grid_response(events: Events, model: int, sigma: float, nodes: Sequen
 
 
 def find_peaks_workspace_size(n_events: int, shape) -> int:
-    alen, _k = _arr(ctypes.c_int32, list(shape))
+    """Workspace bytes of retina_find_peaks_ws for grids of per-event shape `shape` (the response
+    tensor's shape[1:], memory order)."""
+    alen, _k = _arr(ctypes.c_int32, _param_axis_len(shape))
     return int(lib().retina_find_peaks_workspace_size(int(n_events), len(shape), alen))
 
 
@@ -188,7 +203,7 @@ def retina_find_peaks(response: torch.Tensor, P: int, threshold: float, capacity
     E = response.shape[0]
     shape = tuple(response.shape[1:])
     assert len(shape) == P
-    alen, _k = _arr(ctypes.c_int32, list(shape))
+    alen, _k = _arr(ctypes.c_int32, _param_axis_len(shape))
     if out is None:
         dev = response.device
         out = (torch.empty((E, capacity), dtype=torch.int32, device=dev),
@@ -223,8 +238,8 @@ def retina_estimate_peaks(response: torch.Tensor, nodes: Sequence[torch.Tensor],
     E, cap = peak_index.shape
     alen, _k1 = _arr(ctypes.c_int32, [n.numel() for n in nodes])
     nptr, _k2 = _arr(ctypes.c_void_p, [n.data_ptr() for n in nodes])
-    if response.dim() != P + 1 or response.shape[0] != E:
-        raise ValueError("response must be [E, n0, ..] with E = peak_index.shape[0]")
+    if tuple(response.shape) != grid_shape(E, [n.numel() for n in nodes]):
+        raise ValueError("response must be grid_shape(E, node counts) with E = peak_index.shape[0]")
     _out("peak_count", _dev(peak_count, torch.int32), torch.int32, (E,), response.device)
     if out is None:
         out = torch.zeros((E, cap, P), dtype=torch.float32, device=response.device)

@@ -102,13 +102,14 @@ def test_peaks_workspace_size_and_validation(L):
     # 256 (index, value) pairs (8 B each)
     per_slab = 4 + 256 * 8
     assert sz(10, 2, _i(1024, 1024)) == 10 * 8 * per_slab
-    # P = 3 with rows of a multiple of 4 cells (<= 2048): the plane-block path (peaks3.cu): per
-    # segment (plane i, block of 2048 / n2 rows) a count, an offset and 32 (index, value) pairs
-    # (plus one int per chunk of 512 segments for the pass-2 chunk totals)
+    # P = 3 grids are scanned in memory order (n2, n0, n1) (z0 planes outermost, Z37).
+    # Rows (axis_len[1] cells) of a multiple of 4 cells (<= 2048): the plane-block path
+    # (peaks3.cu): per segment (z0 plane, block of 2048 / n1 rows) a count, an offset and 32
+    # (index, value) pairs (plus one int per chunk of 512 segments for the pass-2 chunk totals)
     per_seg = 2 * 4 + 32 * 8
     assert sz(3, 3, _i(256, 256, 256)) == 3 * (256 * 32) * per_seg + 3 * 16 * 4
-    assert sz(2, 3, _i(19, 23, 28)) == 2 * (19 * 1) * per_seg + 2 * 1 * 4  # 73 rows cover the 23: one block
-    assert sz(1, 3, _i(20, 30, 29)) == 1 * 1 * per_slab                  # 29 % 4 != 0: slab path
+    assert sz(2, 3, _i(23, 28, 19)) == 2 * (19 * 1) * per_seg + 2 * 1 * 4  # 73 rows cover the 23: one block
+    assert sz(1, 3, _i(20, 30, 29)) == 1 * 1 * per_slab                  # 30 % 4 != 0: slab path
     assert sz(0, 2, _i(4, 4)) == 0 and sz(1, 4, _i(4, 4)) == 0
     p = L.retina_find_peaks_ws
     p.argtypes = [ctypes.c_void_p, ctypes.c_int32, ctypes.c_int32, ctypes.c_void_p, ctypes.c_float, ctypes.c_int32,

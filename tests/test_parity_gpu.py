@@ -37,6 +37,20 @@ def gpu_grid(batch, cfg, nodes, z_ref=0.0, hint=True, sigma=None, algo=0):
     return out.cpu().numpy()
 
 
+def sub_lattice(g, pick):
+    """Cells of a response grid [E, ...] (memory order: z0 planes outermost for P = 3, DESIGN.md
+    Z37) on the sub-lattice of node subsets `pick` given in parameter order (tx, ty[, z0])."""
+    mem = pick if len(pick) == 2 else [pick[2], pick[0], pick[1]]
+    return g[(slice(None),) + np.ix_(*mem)]
+
+
+def param_cells(flat, grid_dims):
+    """Node indices in parameter order (tx, ty[, z0]) of flat cell offsets in a grid of per-event
+    dims `grid_dims` (memory order)."""
+    c = np.array(np.unravel_index(flat, grid_dims)).T
+    return c if len(grid_dims) == 2 else c[:, [1, 2, 0]]
+
+
 def synthetic_batch(model, counts, seed=0):
     """Events with given hit counts, VELO-like coordinates (or toy for LINE2D)."""
     rng = np.random.default_rng(seed)
@@ -109,7 +123,7 @@ def test_T1_grid_full_size_sampled(name, events, sub, algo):
     pick = [np.sort(rng.choice(len(n), sub, replace=False)) for n in nodes]
     pick = [np.unique(np.concatenate([p, [0, len(n) - 1]])) for p, n in zip(pick, nodes)]
     ref = ora.grid(cfg.model, b.offsets, b.hits, [n[p] for n, p in zip(nodes, pick)], cfg.sigma)
-    sub_gpu = g[(slice(None),) + np.ix_(*pick)]
+    sub_gpu = sub_lattice(g, pick)
     ok, worst = PU.t1_response(sub_gpu, ref)
     assert ok, worst
 
@@ -476,7 +490,7 @@ def test_T1_tensor_grid_cfg3_full_size_sampled(tensor):
     pick = [np.unique(np.concatenate([np.sort(rng.choice(len(n), 48, replace=False)), [0, len(n) - 1]]))
             for n in nodes]
     ref = ora.grid(cfg.model, b.offsets, b.hits, [n[p] for n, p in zip(nodes, pick)], cfg.sigma)
-    ok, worst = PU.t1_response(g[(slice(None),) + np.ix_(*pick)], ref)
+    ok, worst = PU.t1_response(sub_lattice(g, pick), ref)
     assert ok, worst
 
 
@@ -518,7 +532,7 @@ def test_estimate_peaks_vs_oracle(name, ev):
         err = np.abs(th[e, :k].astype(np.float64) - ref[e, :k]) / steps
         assert err.max() <= 1e-3, err.max()  # fp32 vertex arithmetic vs fp64, in grid steps
         # every estimate stays inside its peak's cell (|delta| <= 1/2)
-        cells = np.array(np.unravel_index(idx[e, :k], g64.shape[1:])).T
+        cells = param_cells(idx[e, :k], g64.shape[1:])
         centre = np.stack([nodes[i][cells[:, i]] for i in range(cfg.P)], 1)
         assert np.all(np.abs(th[e, :k] - centre) <= 0.5 * steps * (1 + 1e-5))
         n_checked += k
@@ -687,7 +701,7 @@ def test_T1_tensor_grid_cfg4_full_size_sampled_and_peaks(tensor):
     pick = [np.unique(np.concatenate([np.sort(rng.choice(len(n), 12, replace=False)), [0, len(n) - 1]]))
             for n in nodes]
     ref = ora.grid(cfg.model, b.offsets, b.hits, [n[p] for n, p in zip(nodes, pick)], cfg.sigma)
-    ok, worst = PU.t1_response(g[(slice(None),) + np.ix_(*pick)], ref)
+    ok, worst = PU.t1_response(sub_lattice(g, pick), ref)
     assert ok, worst
     gs = gpu_grid(b, cfg, nodes, algo=R.retina.GRID_SEPARABLE)
     err = np.abs(g.astype(np.float64) - gs) / (2e-5 * np.maximum(gs, 1e-6))
@@ -906,20 +920,20 @@ def test_T1_T4_full_cfg4_slab_vs_fp64_oracle():
         kc = int(np.clip(np.argmin(np.abs(nodes[2] - z0)), 17, len(nodes[2]) - 18))
         k0, k1 = kc - 17, kc + 17                                     # slab node range [k0, k1)
         ref = ora.grid(cfg.model, b.offsets, b.hits, [nodes[0], nodes[1], nodes[2][k0:k1]], cfg.sigma)[0]
-        ok, worst = PU.t1_response(g[:, :, k0:k1], ref)
+        ok, worst = PU.t1_response(g[k0:k1], ref)                     # z0 planes k0..k1-1 (Z37)
         assert ok, (e_id, worst)
         cap = 1 << 20
         for thr in (cfg.peak_threshold, 0.0):
             idx, _, cnt = R.retina_find_peaks(dev(g[None]), 3, thr, cap)
             torch.cuda.synchronize()
             gi = idx.cpu().numpy()[0, :int(cnt[0])]
-            ci = np.array(np.unravel_index(gi, g.shape)).T
-            inside = (ci[:, 2] >= k0 + 1) & (ci[:, 2] < k1 - 1)
+            ci = np.array(np.unravel_index(gi, g.shape)).T                # (l, i, j)
+            inside = (ci[:, 0] >= k0 + 1) & (ci[:, 0] < k1 - 1)
             # GPU peaks in the interior planes, as flat indices of the slab
-            gpu_slab = np.ravel_multi_index((ci[inside, 0], ci[inside, 1], ci[inside, 2] - k0), ref.shape)
+            gpu_slab = np.ravel_multi_index((ci[inside, 0] - k0, ci[inside, 1], ci[inside, 2]), ref.shape)
             ri, _, rc = ora.peaks(ref[None], 3, thr, cap)
             keep = np.zeros(ref.shape, bool)
-            keep[:, :, 1:-1] = True
+            keep[1:-1] = True
             tie = PU.near_tie_cells(ref, 3, thr).ravel()
             nd, ne, bad = _t4_restricted(gpu_slab, ri[0, :rc[0]], tie, keep.ravel())
             assert not bad, (e_id, thr, nd, ne, bad[:5])

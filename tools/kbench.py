@@ -66,7 +66,7 @@ def main():
 
     if cfg.axes and ({"grid", "peaks"} & set(phases)):
         nodes = [torch.from_numpy(n).cuda() for n in G.axis_nodes(cfg)]
-        shape = tuple(len(n) for n in nodes)
+        shape = RT.grid_shape(1, [len(n) for n in nodes])[1:]
         chunk = max(1, min(a.events, int(4e9 // (4 * cfg.n_units))))
         grid = torch.empty((chunk,) + shape, device="cuda")
         cap = cfg.peak_capacity

@@ -30,7 +30,7 @@ seeds = torch.from_numpy(G.make_seeds(cfg, ev_ids)).cuda()
 ev = R.Events.from_numpy(b.offsets, b.hits)
 nodes = [torch.from_numpy(n).cuda() for n in G.axis_nodes(cfg)]
 chunk = max(1, min(a.events, int(2e9 // (4 * cfg.n_units))))
-grid = torch.empty((chunk,) + tuple(len(n) for n in nodes), device="cuda")
+grid = torch.empty(R.retina.grid_shape(chunk, [len(n) for n in nodes]), device="cuda")
 out = (torch.empty_like(seeds), torch.empty(seeds.shape[:2], device="cuda"), None)
 nh = float(b.n_hits)
 
