@@ -86,7 +86,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(32 * PP_WARPS)
     __shared__ __align__(8) uint64_t s_empty[PP_NS];    // both CTAs: multicast MMA commit
     __shared__ __align__(8) uint64_t s_acc_full[2];     // both CTAs: multicast commit at tile end
     __shared__ __align__(8) uint64_t s_acc_empty[2];    // even CTA: 2 x 4 epilogue warps arrive
-    __shared__ __align__(8) uint64_t s_hbar;            // hit loads (TMA bulk copy)
     __shared__ uint32_t s_tmem;
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -98,7 +97,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(32 * PP_WARPS)
     // a contiguous range of items per cluster (the event's hits stay in shared memory)
     const int t0 = (int)((long long)cl * n_items / ncl), t1 = (int)((long long)(cl + 1) * n_items / ncl);
     constexpr int dt = 1;
-    float4 *s_hits = reinterpret_cast<float4 *>(s_raw + PP_NS * PP_STAGE);
+    constexpr bool EXACT_D = ZREF || MODEL == kSlope3;
+    // the hit window, structure of arrays: x, y, z - z_ref (hi) [, lo], a.cap floats each
+    float *s_hx = reinterpret_cast<float *>(s_raw + PP_NS * PP_STAGE);
+    float *s_hy = s_hx + a.cap, *s_hz = s_hy + a.cap, *s_hzl = s_hz + a.cap;
 
     if (warp == 0) {  // two accumulator buffers of 128 lanes x 256 fp32 columns, in both CTAs
         asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&s_tmem)),
@@ -116,7 +118,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(32 * PP_WARPS)
             mbar_init(&s_acc_full[i], 1);
             mbar_init(&s_acc_empty[i], 8);
         }
-        mbar_init(&s_hbar, 1);
         fence_mbar_init();
     }
     __syncthreads();
@@ -124,15 +125,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(32 * PP_WARPS)
     tc_fence_after();
     const uint32_t tmem = s_tmem;
     const uint32_t stage_saddr = smem_u32(s_raw);
-    constexpr bool EXACT_D = ZREF || MODEL == kSlope3;
 
     if (warp < PP_GEN_WARPS) {
         // ------------------------------------------------------------------ generating warps
         const int kb = warp % PP_KB, rset = warp / PP_KB;
-        const float2 nk2 = make_float2(a.negK, a.negK);
+        const int gtid = tid;  // 0 .. 32 * PP_GEN_WARPS - 1
+        // 2^15 is folded into the exponent: v' = 2^(15 - K s^2) = v 2^15 straight from MUFU.EX2
+        const float2 nk2 = make_float2(a.negK, a.negK), c15 = make_float2(15.f, 15.f);
         const __half2 h2m6 = __float2half2_rn(0.015625f);  // 2^-6: h 2^15 -> h 2^9
-        uint32_t cg = 0, loads = 0;                        // chunk counter, hit loads issued
-        int have_e = -1, have_w0 = -1;                     // hit window now in shared memory
+        uint32_t cg = 0;                                   // chunk counter
+        int have_e = -1, have_w0 = -1, have_l = -1;        // hit window (and z0) now in shared memory
         // each warp arrives on a barrier of its own CTA (CTA-scope release: cheap); the odd CTA's
         // arrivals are relayed to the even CTA by one cluster-scope release per chunk (MMA warp)
         uint64_t *arrive_bar = (rank == 0) ? s_full : s_pfull;
@@ -150,34 +152,54 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(32 * PP_WARPS)
             const float zref = (MODEL == kSlope3) ? __ldg(a.nodes2 + c.l) : a.z_ref;
             for (int w0 = 0; w0 < n; w0 += a.cap) {
                 const int wlen = min(a.cap, n - w0);
-                if (have_e != c.e || have_w0 != w0) {  // (re)load the window; uniform over the 16 warps
-                    gen_bar_sync();                     // nobody still reads the old window
-                    if (tid == 0) {
-                        fence_proxy_async();
-                        mbar_arrive_expect_tx(&s_hbar, (uint32_t)wlen * 16u);
-                        bulk_g2s(s_hits, a.hits + start + w0, (uint32_t)wlen * 16u, &s_hbar);
+                if (have_e != c.e || have_w0 != w0 || (MODEL == kSlope3 && have_l != c.l)) {
+                    // (re)stage the window as structure-of-arrays x, y, z - z_ref (exact as zh + zl),
+                    // padded to whole chunks with far-away hits (x = y = 1e30: factor 0), so each
+                    // thread loads its 8 hits' coordinates as aligned float4s straight into the
+                    // register pairs the FFMA2s use; uniform over the 16 warps
+                    gen_bar_sync();  // nobody still reads the old window
+                    const int wpad = (wlen + PP_KC - 1) / PP_KC * PP_KC;
+                    for (int k = gtid; k < wpad; k += 32 * PP_GEN_WARPS) {
+                        float x = 1e30f, y = 1e30f, zh = 0.f, zl = 0.f;
+                        if (k < wlen) {
+                            const float4 hk = __ldg(a.hits + start + w0 + k);
+                            x = hk.x;
+                            y = hk.y;
+                            zh = hk.z;
+                            if (EXACT_D) two_sum(hk.z, -zref, zh, zl);
+                        }
+                        s_hx[k] = x;
+                        s_hy[k] = y;
+                        s_hz[k] = zh;
+                        if (EXACT_D) s_hzl[k] = zl;
                     }
-                    mbar_wait(&s_hbar, loads & 1u);
-                    ++loads;
+                    gen_bar_sync();
                     have_e = c.e;
                     have_w0 = w0;
+                    have_l = c.l;
                 }
-                const float4 *h = s_hits;
                 for (int k0 = 0; k0 < wlen; k0 += PP_KC, ++cg) {
                     const int s = (int)(cg % PP_NS);
+                    const int kk = k0 + kb * 8;
                     float2 hx[4], hy[4], hz[4], hzl[4];
-#pragma unroll
-                    for (int q = 0; q < 8; ++q) {
-                        const int k = k0 + kb * 8 + q;
-                        const bool ok = k < wlen;
-                        const float4 hk = h[ok ? k : 0];
-                        float zh = hk.z, zl = 0.f;
-                        if (EXACT_D) two_sum(hk.z, -zref, zh, zl);
-                        const float xv = ok ? hk.x : 1e30f, yv = ok ? hk.y : 1e30f;
-                        if (q & 1) {
-                            hx[q >> 1].y = xv; hy[q >> 1].y = yv; hz[q >> 1].y = zh; hzl[q >> 1].y = zl;
-                        } else {
-                            hx[q >> 1].x = xv; hy[q >> 1].x = yv; hz[q >> 1].x = zh; hzl[q >> 1].x = zl;
+                    {
+                        const float4 x0 = *reinterpret_cast<const float4 *>(s_hx + kk);
+                        const float4 x1 = *reinterpret_cast<const float4 *>(s_hx + kk + 4);
+                        const float4 y0 = *reinterpret_cast<const float4 *>(s_hy + kk);
+                        const float4 y1 = *reinterpret_cast<const float4 *>(s_hy + kk + 4);
+                        const float4 z0 = *reinterpret_cast<const float4 *>(s_hz + kk);
+                        const float4 z1 = *reinterpret_cast<const float4 *>(s_hz + kk + 4);
+                        hx[0] = make_float2(x0.x, x0.y); hx[1] = make_float2(x0.z, x0.w);
+                        hx[2] = make_float2(x1.x, x1.y); hx[3] = make_float2(x1.z, x1.w);
+                        hy[0] = make_float2(y0.x, y0.y); hy[1] = make_float2(y0.z, y0.w);
+                        hy[2] = make_float2(y1.x, y1.y); hy[3] = make_float2(y1.z, y1.w);
+                        hz[0] = make_float2(z0.x, z0.y); hz[1] = make_float2(z0.z, z0.w);
+                        hz[2] = make_float2(z1.x, z1.y); hz[3] = make_float2(z1.z, z1.w);
+                        if (EXACT_D) {
+                            const float4 l0 = *reinterpret_cast<const float4 *>(s_hzl + kk);
+                            const float4 l1 = *reinterpret_cast<const float4 *>(s_hzl + kk + 4);
+                            hzl[0] = make_float2(l0.x, l0.y); hzl[1] = make_float2(l0.z, l0.w);
+                            hzl[2] = make_float2(l1.x, l1.y); hzl[3] = make_float2(l1.z, l1.w);
                         }
                     }
                     if (cg >= PP_NS) mbar_wait(&s_empty[s], ((cg / PP_NS) - 1) & 1u);  // MMAs of cg-NS done
@@ -192,13 +214,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(32 * PP_WARPS)
                             const float2 cc = isA ? hx[q] : hy[q];
                             const float2 sres = EXACT_D ? __ffma2_rn(mp, hzl[q], __ffma2_rn(mp, hz[q], cc))
                                                         : __ffma2_rn(mp, hz[q], cc);
-                            const float2 arg = __fmul2_rn(__fmul2_rn(sres, sres), nk2);
-                            const float2 v = make_float2(ex2_approx(arg.x), ex2_approx(arg.y));
-                            const float2 vs = __fmul2_rn(v, make_float2(0x1p15f, 0x1p15f));
+                            const float2 arg = __ffma2_rn(__fmul2_rn(sres, sres), nk2, c15);
+                            const float2 vs = make_float2(ex2_approx(arg.x), ex2_approx(arg.y));  // v 2^15
                             const __half2 hh = __floats2half2_rn(vs.x, vs.y);
-                            const float2 hf = __half22float2(hh);                                    // exact
-                            const float2 lo = __ffma2_rn(hf, make_float2(-0x1p-15f, -0x1p-15f), v);  // exact
-                            const float2 ls = __fmul2_rn(lo, make_float2(0x1p21f, 0x1p21f));
+                            const float2 hf = __half22float2(hh);                                  // exact
+                            const float2 lo = __ffma2_rn(hf, make_float2(-1.f, -1.f), vs);         // exact
+                            const float2 ls = __fmul2_rn(lo, make_float2(0x1p6f, 0x1p6f));       // l 2^21
                             const __half2 hl = __floats2half2_rn(ls.x, ls.y);
                             const __half2 h9 = __hmul2(hh, h2m6);
                             w15[q] = *reinterpret_cast<const uint32_t *>(&hh);
@@ -354,9 +375,11 @@ template <int MODEL, bool ZREF>
 static cudaError_t launch_pp(const GridArgs &a0, int n_events, cudaStream_t stream) {
     auto kern = grid_tensor16pp_kernel<MODEL, ZREF>;
     GridArgs a = a0;
-    const int cap_max = (227 * 1024 - PP_NS * PP_STAGE - 2048) / 16;
-    a.cap = std::max(PP_KC, (std::min(a.cap, cap_max) / PP_KC) * PP_KC);  // windows are whole chunks
-    const size_t smem = (size_t)PP_NS * PP_STAGE + (size_t)a.cap * sizeof(float4);
+    // hit window: x, y, z (+ the low part of z - z_ref) as floats; whole chunks
+    constexpr int n_arr = (ZREF || MODEL == kSlope3) ? 4 : 3;
+    const int cap_max = (227 * 1024 - PP_NS * PP_STAGE - 2048) / (4 * n_arr);
+    a.cap = std::max(PP_KC, (std::min(std::max(a.cap, PP_KC), cap_max) / PP_KC) * PP_KC);
+    const size_t smem = (size_t)PP_NS * PP_STAGE + (size_t)a.cap * 4 * n_arr;
     cudaError_t err = ensure_dynamic_smem(kern, smem);
     if (err != cudaSuccess) return err;
     const long long per_event =
