@@ -34,6 +34,9 @@
 #include "kernels.cuh"
 #include "tcgen05.cuh"
 
+#include <cuda.h>           // CUtensorMap (the encoder is fetched from the driver at run time)
+#include <cudaTypedefs.h>   // PFN_cuTensorMapEncodeTiled
+
 #include <algorithm>
 
 namespace retina {
@@ -77,9 +80,15 @@ __device__ __forceinline__ void gen_bar_sync() {  // the 16 generating warps onl
     asm volatile("bar.sync 1, %0;" ::"n"(32 * PP_GEN_WARPS) : "memory");
 }
 
-template <int MODEL, bool ZREF>
+// Epilogue staging for the TMA tensor store: per epilogue warp two 32-row x 16-column fp32 boxes
+// (2 KB each, 64-byte swizzle: 16-byte chunk c of row r at r 64 + ((c ^ ((r >> 1) & 3)) << 4), so the
+// warp's row-per-lane STS.128s are bank-conflict-free).
+constexpr int PP_EPI_BOX = 32 * 16 * 4;
+constexpr int PP_EPI_BYTES = 4 * 2 * PP_EPI_BOX;
+
+template <int MODEL, bool ZREF, bool TMA_EPI>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(32 * PP_WARPS)
-    grid_tensor16pp_kernel(GridArgs a, int n_items) {
+    grid_tensor16pp_kernel(GridArgs a, int n_items, const __grid_constant__ CUtensorMap out_map) {
     extern __shared__ __align__(1024) uint8_t s_raw[];
     __shared__ __align__(8) uint64_t s_full[PP_NS];     // even CTA: its 16 generating warps + the odd CTA's relay
     __shared__ __align__(8) uint64_t s_pfull[PP_NS];    // odd CTA: its 16 generating warps (relayed once)
@@ -98,8 +107,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(32 * PP_WARPS)
     const int t0 = (int)((long long)cl * n_items / ncl), t1 = (int)((long long)(cl + 1) * n_items / ncl);
     constexpr int dt = 1;
     constexpr bool EXACT_D = ZREF || MODEL == kSlope3;
-    // the hit window, structure of arrays: x, y, z - z_ref (hi) [, lo], a.cap floats each
-    float *s_hx = reinterpret_cast<float *>(s_raw + PP_NS * PP_STAGE);
+    // [operand stages][epilogue boxes (TMA_EPI)][hit window]; the hit window is a structure of
+    // arrays: x, y, z - z_ref (hi) [, lo], a.cap floats each
+    uint8_t *s_epi = s_raw + PP_NS * PP_STAGE;
+    float *s_hx = reinterpret_cast<float *>(s_epi + (TMA_EPI ? PP_EPI_BYTES : 0));
     float *s_hy = s_hx + a.cap, *s_hz = s_hy + a.cap, *s_hzl = s_hz + a.cap;
 
     if (warp == 0) {  // two accumulator buffers of 128 lanes x 256 fp32 columns, in both CTAs
@@ -306,6 +317,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(32 * PP_WARPS)
         const uint32_t acc_empty0 = mapa_rank0(smem_u32(&s_acc_empty[0]));
         const int64_t cells = (int64_t)a.n0 * a.n1 * nl;
         int ti = 0;
+        uint32_t epi_n = 0;  // TMA_EPI: boxes stored so far (two per warp alternate)
         for (int t = t0; t < t1; t += dt, ++ti) {
             const PairCoord c = decode_pair(t, ppe, nl, tn, (int)rank);
             const int n = a.offsets[c.e + 1] - a.offsets[c.e];
@@ -314,6 +326,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(32 * PP_WARPS)
             tc_fence_after();
             const int i = c.t_m * 128 + q * 32 + lane;
             float *out = a.R + (int64_t)(a.e_base + c.e) * cells + ((int64_t)c.l * a.n0 + i) * a.n1;
+            const int plane = (a.e_base + c.e) * nl + c.l;  // [E][n2] planes of [n0][n1] (Z37)
 #pragma unroll 1
             for (int cc = 0; cc < TC_N / 16; ++cc) {
                 const int col = cc * 16;
@@ -335,7 +348,32 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(32 * PP_WARPS)
                     for (int x = 0; x < 16; ++x) v[x] = 0u;
                 }
                 const int j0 = c.t_n * TC_N + col;
-                if (i < a.n0) {
+                if constexpr (TMA_EPI) {
+                    // registers -> swizzled box in shared memory -> one TMA tensor store per warp
+                    // (rows past n0 and columns past n1 are clipped by the tensor map's bounds)
+                    const uint32_t box = smem_u32(s_epi) + (uint32_t)((q * 2 + (epi_n & 1)) * PP_EPI_BOX);
+                    if (epi_n >= 2) {  // the store issued from this box two boxes ago has read it
+                        if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+                        __syncwarp();
+                    }
+                    const uint32_t row = box + (uint32_t)(lane * 64), sw = (uint32_t)((lane >> 1) & 3);
+#pragma unroll
+                    for (int x = 0; x < 4; ++x)
+                        asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(row + (((uint32_t)x ^ sw) << 4)),
+                                     "r"(v[4 * x]), "r"(v[4 * x + 1]), "r"(v[4 * x + 2]), "r"(v[4 * x + 3])
+                                     : "memory");
+                    fence_proxy_async();
+                    __syncwarp();
+                    if (lane == 0) {
+                        asm volatile(
+                            "cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%2, %3, %4}], [%1];" ::"l"(
+                                reinterpret_cast<uint64_t>(&out_map)),
+                            "r"(box), "r"(j0), "r"(c.t_m * 128 + q * 32), "r"(plane)
+                            : "memory");
+                        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+                    }
+                    ++epi_n;
+                } else if (i < a.n0) {
                     if (j0 + 15 < a.n1 && (((uintptr_t)(out + j0)) & 15u) == 0) {
 #pragma unroll
                         for (int x = 0; x < 16; x += 4)
@@ -353,6 +391,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(32 * PP_WARPS)
             __syncwarp();
             if (lane == 0) mbar_arrive_remote(acc_empty0 + (uint32_t)(b * sizeof(uint64_t)));
         }
+        if (TMA_EPI && lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");  // stores done
     }
     tc_fence_before();
     __syncthreads();
@@ -371,15 +410,37 @@ static int sm_count() {  // of the current device (a cheap attribute query, lega
     return v;
 }
 
-template <int MODEL, bool ZREF>
-static cudaError_t launch_pp(const GridArgs &a0, int n_events, cudaStream_t stream) {
-    auto kern = grid_tensor16pp_kernel<MODEL, ZREF>;
+// The output as a 3-D tensor map {n1, n0, planes} (planes = events x z0 nodes) with 16 x 32 x 1
+// boxes, 64-byte swizzle; false if the driver's encoder is unavailable or the layout does not
+// qualify (row pitch n1 * 4 bytes must be a multiple of 16) -- then the epilogue stores directly.
+static bool encode_out_map(CUtensorMap *map, float *R, int n0, int n1, long long planes) {
+    static PFN_cuTensorMapEncodeTiled_v12000 encode = []() -> PFN_cuTensorMapEncodeTiled_v12000 {
+        void *fn = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess)
+            return nullptr;
+        return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+    }();
+    if (!encode || (n1 & 3) || (reinterpret_cast<uintptr_t>(R) & 15u) || planes <= 0) return false;
+    const cuuint64_t dims[3] = {(cuuint64_t)n1, (cuuint64_t)n0, (cuuint64_t)planes};
+    const cuuint64_t strides[2] = {(cuuint64_t)n1 * 4, (cuuint64_t)n1 * n0 * 4};
+    const cuuint32_t box[3] = {16, 32, 1}, estr[3] = {1, 1, 1};
+    return encode(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, R, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                  CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+template <int MODEL, bool ZREF, bool TMA_EPI>
+static cudaError_t launch_pp(const GridArgs &a0, int n_events, const CUtensorMap &map, cudaStream_t stream) {
+    auto kern = grid_tensor16pp_kernel<MODEL, ZREF, TMA_EPI>;
     GridArgs a = a0;
     // hit window: x, y, z (+ the low part of z - z_ref) as floats; whole chunks
     constexpr int n_arr = (ZREF || MODEL == kSlope3) ? 4 : 3;
-    const int cap_max = (227 * 1024 - PP_NS * PP_STAGE - 2048) / (4 * n_arr);
+    constexpr int fixed = PP_NS * PP_STAGE + (TMA_EPI ? PP_EPI_BYTES : 0);
+    const int cap_max = (227 * 1024 - fixed - 2048) / (4 * n_arr);
     a.cap = std::max(PP_KC, (std::min(std::max(a.cap, PP_KC), cap_max) / PP_KC) * PP_KC);
-    const size_t smem = (size_t)PP_NS * PP_STAGE + (size_t)a.cap * 4 * n_arr;
+    const size_t smem = (size_t)fixed + (size_t)a.cap * 4 * n_arr;
     cudaError_t err = ensure_dynamic_smem(kern, smem);
     if (err != cudaSuccess) return err;
     const long long per_event =
@@ -392,19 +453,28 @@ static cudaError_t launch_pp(const GridArgs &a0, int n_events, cudaStream_t stre
         b.e_base = e0;
         const int items = (int)(per_event * ne);
         const int clusters = std::max(1, std::min(items, sm_count() / 2));
-        kern<<<2 * clusters, 32 * PP_WARPS, smem, stream>>>(b, items);
+        kern<<<2 * clusters, 32 * PP_WARPS, smem, stream>>>(b, items, map);
         err = cudaGetLastError();
         if (err != cudaSuccess) return err;
     }
     return cudaSuccess;
 }
 
+template <int MODEL, bool ZREF>
+static cudaError_t launch_pp_any(const GridArgs &a, int n_events, cudaStream_t stream) {
+    CUtensorMap map;
+    const long long planes = (long long)n_events * (MODEL == kSlope3 ? a.n2 : 1);
+    if (encode_out_map(&map, a.R, a.n0, a.n1, planes)) return launch_pp<MODEL, ZREF, true>(a, n_events, map, stream);
+    memset(&map, 0, sizeof(map));
+    return launch_pp<MODEL, ZREF, false>(a, n_events, map, stream);
+}
+
 cudaError_t launch_grid_tensor16p(int model, const GridArgs &a, int n_events, cudaStream_t stream) {
     if (n_events == 0) return cudaSuccess;
-    if (model == kSlope3) return launch_pp<kSlope3, false>(a, n_events, stream);
+    if (model == kSlope3) return launch_pp_any<kSlope3, false>(a, n_events, stream);
     if (model != kSlope2) return cudaErrorInvalidValue;
-    return (a.z_ref == 0.f) ? launch_pp<kSlope2, false>(a, n_events, stream)
-                            : launch_pp<kSlope2, true>(a, n_events, stream);
+    return (a.z_ref == 0.f) ? launch_pp_any<kSlope2, false>(a, n_events, stream)
+                            : launch_pp_any<kSlope2, true>(a, n_events, stream);
 }
 
 }  // namespace retina
