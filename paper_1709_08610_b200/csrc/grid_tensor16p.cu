@@ -273,7 +273,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(32 * PP_WARPS)
                 }
             }
         }
-        if (rank == 0 && lane == 0) {
+        if (rank == 0) {  // the whole warp runs the loop; elect.sync picks the issuing lane
             uint32_t cg = 0;
             int ti = 0;
             const uint32_t peer_acc_full = mapa_rank(smem_u32(&s_acc_full[0]), 1);
@@ -290,24 +290,28 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(32 * PP_WARPS)
                     const int s = (int)(cg % PP_NS);
                     mbar_wait_cluster(&s_full[s], (cg / PP_NS) & 1u);
                     tc_fence_after();
-                    const uint32_t A0 = stage_saddr + s * PP_STAGE, B0 = A0 + 3 * PP_PART;
+                    // descriptor of the stage's first A / B part; offsets inside the stage are added
+                    // to the 14-bit start-address field (address >> 4) directly
+                    const uint64_t dA = umma_desc(stage_saddr + s * PP_STAGE, 128 * 16, 128);
+                    const uint64_t dB = dA + (uint64_t)((3 * PP_PART) >> 4);
 #pragma unroll
                     for (int j = 0; j < PP_KC / 16; ++j) {  // K = 16 fp16 per MMA = 2 k-blocks
                         const uint32_t o = j * 2 * (128 * 16);
 #pragma unroll
                         for (int pp = 0; pp < 3; ++pp)
-                            tc2_mma_f16(acc, umma_desc(A0 + pp * PP_PART + o, 128 * 16, 128),
-                                        umma_desc(B0 + pp * PP_PART + o, 128 * 16, 128),
-                                        (ck > 0 || j > 0 || pp > 0) ? 1u : 0u);
+                            tc2_mma_f16_warp(acc, dA + (uint64_t)((pp * PP_PART + o) >> 4),
+                                             dB + (uint64_t)((pp * PP_PART + o) >> 4),
+                                             (ck > 0 || j > 0 || pp > 0) ? 1u : 0u);
                     }
-                    tc2_commit_both(&s_empty[s]);
+                    tc2_commit_both_warp(&s_empty[s]);
                 }
                 if (nck > 0) {
-                    tc2_commit_both(&s_acc_full[b]);  // both CTAs: every MMA of this tile complete
-                } else {
+                    tc2_commit_both_warp(&s_acc_full[b]);  // both CTAs: every MMA of this tile complete
+                } else if (lane == 0) {
                     mbar_arrive(&s_acc_full[b]);
                     mbar_arrive_remote(peer_acc_full + (uint32_t)(b * sizeof(uint64_t)));
                 }
+                __syncwarp();
             }
         }
         __syncwarp();

@@ -112,6 +112,26 @@ __device__ __forceinline__ void tc2_mma_f16(uint32_t tmem_d, uint64_t da, uint64
         "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
         "l"(da), "l"(db), "r"(kTcIdescF16M256), "r"(accumulate));
 }
+// Warp-converged forms: the whole warp executes them with warp-uniform operands and one lane,
+// chosen by elect.sync, issues -- no divergent single-lane region, so the descriptors stay in
+// uniform registers instead of being broadcast per instruction (R2UR + BRA.U.ANY loop).
+__device__ __forceinline__ void tc2_mma_f16_warp(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p, e;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "elect.sync _|e, 0xffffffff;\n\t"
+        "@e tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+        "l"(da), "l"(db), "r"(kTcIdescF16M256), "r"(accumulate));
+}
+__device__ __forceinline__ void tc2_commit_both_warp(uint64_t *bar) {
+    asm volatile(
+        "{\n\t.reg .pred e;\n\t"
+        "elect.sync _|e, 0xffffffff;\n\t"
+        "@e tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;\n\t}" ::"r"(
+            smem_u32(bar)),
+        "h"((unsigned short)3)
+        : "memory");
+}
 __device__ __forceinline__ void tc2_commit_both(uint64_t *bar) {
     asm volatile(
         "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
