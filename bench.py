@@ -593,8 +593,9 @@ def main():
         if ph == "multistart" and a.update == "newton":
             r["work_basis"] = ("pairs = sum over seeds of response evaluations (q Hessian-mode + line-search "
                                "trials + final; counted by the kernel, PAPER.md:200-201 cost unit) x event hits")
-        if ph in traffic and not (ph == "multistart" and a.update == "newton"):
-            r["traffic"] = traffic[ph]["dram_bytes_per_event"] * E / n_launch
+        tcfg = traffic.get(cfg.name, {}) if not a.dense else {}  # per config: the capture's workload
+        if ph in tcfg and not (ph == "multistart" and a.update == "newton"):
+            r["traffic"] = tcfg[ph]["dram_bytes_per_event"] * E / n_launch
             r["traffic_unit"] = "bytes/launch (ncu dram read+write per event x events per launch)"
         roofs[ph] = r
     dom = max(roofs, key=lambda k: roofs[k]["share_of_step"])
