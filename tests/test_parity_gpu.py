@@ -691,6 +691,33 @@ def test_T1_tensor_grid_slope3_ragged(shape, hint, tensor):
     assert ok, worst
 
 
+@pytest.mark.parametrize("model,z_ref,shape", [(C.SLOPE2, 0.0, (300, 516)), (C.SLOPE2, 7.5, (260, 132)),
+                                               (C.SLOPE3, 0.0, (130, 260, 5)), (C.SLOPE3, 0.0, (40, 36, 7))])
+def test_T1_default_grid_tma_store_ragged_tiles(model, z_ref, shape):
+    """The default kernel's TMA-store epilogue (row pitch a multiple of 16 bytes): partial 256 x 256
+    tiles at both edges, clipped by the tensor map's bounds (nothing written past n0 / n1, nor into
+    the next z0 plane or event: the output buffer is pre-filled with a sentinel and the whole grid
+    compared), empty / single-hit events, and an event longer than the hit window."""
+    b = synthetic_batch(model, [700, 0, 1, 5000, 37], seed=21 + len(shape))
+    P = len(shape)
+    nodes = [np.linspace(lo, hi, n).astype(np.float32) for (lo, hi), n in
+             zip([(-0.3, 0.3), (-0.3, 0.3), (-150.0, 150.0)], shape)]
+    sigma = 0.44
+    ev = events_of(b, z_ref)
+    gshape = R.retina.grid_shape(5, shape)
+    n_cells = int(np.prod(gshape))
+    buf = torch.full((n_cells + 4096,), 7.25, device="cuda")   # sentinel tail right after the grid
+    out = buf[:n_cells].view(gshape)
+    R.retina_grid_response(ev, model, sigma, [dev(n) for n in nodes], out=out)
+    torch.cuda.synchronize()
+    g = out.cpu().numpy()
+    ref = ora.grid(model, b.offsets, b.hits, nodes, sigma, z_ref=z_ref)
+    assert g.shape == ref.shape and np.all(g[1] == 0.0)
+    ok, worst = PU.t1_response(g, ref)
+    assert ok, worst
+    assert torch.all(buf[n_cells:] == 7.25)
+
+
 @pytest.mark.parametrize("tensor", TENSORS)
 def test_T1_tensor_grid_cfg4_full_size_sampled_and_peaks(tensor):
     cfg = C.CFG4
