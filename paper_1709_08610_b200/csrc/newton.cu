@@ -432,6 +432,9 @@ struct LineSearchSmem {
 #ifndef RETINA_NT_SQ
 #define RETINA_NT_SQ 1  // queue entries per worker thread (1 measured best: C0 5.3 vs 6.0 (2), 7.8 (4) on cfg3)
 #endif
+#ifndef RETINA_NT3_SQ
+#define RETINA_NT3_SQ 2  // SLOPE3: two entries per worker as one packed seed pair (cfg4 Newton 15.55 -> 15.08 ms per 100 events)
+#endif
 #ifndef RETINA_NT_LSB
 #define RETINA_NT_LSB 4  // halvings evaluated together per queue round (measured: C0 4.9 / 4.0 / 3.8 / 3.8 for 1 / 2 / 4 / 8)
 #endif
@@ -442,7 +445,8 @@ __device__ __forceinline__ void nt_line_search_queue(HitStage &st, const NewtonA
                                                      const float (&slope)[S], const bool (&active)[S], int (&nev)[S],
                                                      float (&rcur)[S], LineSearchSmem<S, (MODEL == kSlope3) ? 3 : 2> &ls) {
     constexpr int P = (MODEL == kSlope3) ? 3 : 2;
-    constexpr int SQ = RETINA_NT_SQ < S ? RETINA_NT_SQ : S;
+    constexpr int SQW = (MODEL == kSlope3) ? RETINA_NT3_SQ : RETINA_NT_SQ;
+    constexpr int SQ = SQW < S ? SQW : S;
     const int tid = threadIdx.x, lane = tid & 31, wbase = (tid >> 5) * 32 * SQ;
     __syncthreads();  // previous users of ls are done
     if (tid == 0) ls.nq[0] = ls.nq[1] = 0;
@@ -490,7 +494,10 @@ __device__ __forceinline__ void nt_line_search_queue(HitStage &st, const NewtonA
                                        : 0.f;
             }
             float Rt[SQ], Gd[SQ][4];
-            nt_pass_r<MODEL, SQ, ZREF, false>(st, tt, negK, a.z_ref, Rt, Gd);
+            if constexpr (RETINA_NT_X2 && SQ % 2 == 0)
+                nt_pass_r_x2<MODEL, SQ, ZREF, false>(st, tt, negK, a.z_ref, Rt, Gd);
+            else
+                nt_pass_r<MODEL, SQ, ZREF, false>(st, tt, negK, a.z_ref, Rt, Gd);
 #pragma unroll
             for (int s = 0; s < SQ; ++s) {
                 if (slot[s] < 0) continue;
