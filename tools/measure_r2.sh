@@ -47,3 +47,15 @@ for f in ("", "_newton", "_cfg4", "_cfg4full", "_dense", "_cfg4dense", "_cfg0", 
     except Exception as exc:  # report and go on: one failed line must not hide the others
         print(f, "FAILED", exc)
 PY
+# repeatability: the default bench twice more on the same box
+for k in 2 3; do timeout 900 python bench.py --no-cpu-baseline > gpurun_out/${P}_bench_rep$k.json 2>/dev/null; done
+python - "$P" <<'PY'
+import json, sys
+p = sys.argv[1]
+for f in ("", "_rep2", "_rep3"):
+    try:
+        d = json.load(open(f"gpurun_out/{p}_bench{f}.json"))
+        print("repeat", f or "_rep1", round(d["ms_per_step"], 2), round(d["roofline"]["frac"], 4))
+    except Exception as exc:
+        print(f, "FAILED", exc)
+PY
