@@ -9,6 +9,15 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+// Bounds checks of the index arithmetic for a debug build (-DRETINA_DEBUG: device-side asserts;
+// compute-sanitizer is not available on this pool); compiled out otherwise.
+#ifdef RETINA_DEBUG
+#include <cassert>
+#define RETINA_ASSERT(cond) assert(cond)
+#else
+#define RETINA_ASSERT(cond) ((void)0)
+#endif
+
 #include <map>
 #include <mutex>
 #include <utility>

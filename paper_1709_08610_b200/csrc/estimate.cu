@@ -25,6 +25,7 @@ __global__ void __launch_bounds__(256) estimate_kernel(EstimateArgs a) {
     const int64_t cells = (int64_t)a.n0 * a.n1 * a.n2;
     const float *g = a.R + (int64_t)e * cells;
     const int c = a.idx[(int64_t)e * a.capacity + p];
+    RETINA_ASSERT(c >= 0 && (int64_t)c < cells);
     // node indices in parameter order (tx, ty[, z0]); cell (i, j[, l]) at (l n0 + i) n1 + j (Z37)
     int ci[3];
     ci[1] = c % a.n1;

@@ -170,6 +170,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(32 * PP_WARPS)
                     // register pairs the FFMA2s use; uniform over the 16 warps
                     gen_bar_sync();  // nobody still reads the old window
                     const int wpad = (wlen + PP_KC - 1) / PP_KC * PP_KC;
+                    RETINA_ASSERT(wpad <= a.cap);
                     for (int k = gtid; k < wpad; k += 32 * PP_GEN_WARPS) {
                         float x = 1e30f, y = 1e30f, zh = 0.f, zl = 0.f;
                         if (k < wlen) {
@@ -192,6 +193,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(32 * PP_WARPS)
                 for (int k0 = 0; k0 < wlen; k0 += PP_KC, ++cg) {
                     const int s = (int)(cg % PP_NS);
                     const int kk = k0 + kb * 8;
+                    RETINA_ASSERT(kk + 8 <= a.cap);
                     float2 hx[4], hy[4], hz[4], hzl[4];
                     {
                         const float4 x0 = *reinterpret_cast<const float4 *>(s_hx + kk);
@@ -331,6 +333,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(32 * PP_WARPS)
             const int i = c.t_m * 128 + q * 32 + lane;
             float *out = a.R + (int64_t)(a.e_base + c.e) * cells + ((int64_t)c.l * a.n0 + i) * a.n1;
             const int plane = (a.e_base + c.e) * nl + c.l;  // [E][n2] planes of [n0][n1] (Z37)
+            RETINA_ASSERT(c.l >= 0 && c.l < nl && c.t_m * 128 < a.n0 + 128 && c.t_n * TC_N < a.n1);
 #pragma unroll 1
             for (int cc = 0; cc < TC_N / 16; ++cc) {
                 const int col = cc * 16;

@@ -214,6 +214,7 @@ __global__ void __launch_bounds__(kCThreads + 32) peaks3_brick_kernel(PeakArgs a
         int released = -1;    // planes <= released are handed back to the producer
         auto check = [&](int2 ent) {  // strict test of one candidate against its other 24 neighbours
             const int i = ent.x, jj = ent.y >> 16, lc = ent.y & 0xffff;
+            RETINA_ASSERT(i >= 0 && i < n0 && jj >= 0 && jj < j1 - j0 && lc >= 0 && lc < n2);
             const int r = jj + 1, jg = j0 + jj;
             const float *pc = ring + (i % kRing) * slot;
             const float *pm = (i > 0) ? ring + ((i - 1) % kRing) * slot : pc;  // pc: a dummy, masked
