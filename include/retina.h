@@ -19,6 +19,8 @@
  *   retina_grid_response_ex     the same grid with an explicit kernel choice;
  *   retina_find_peaks_ws        step (iii) by many CTAs per event (caller workspace);
  *   retina_estimate_peaks       step (iv): sub-cell parameter estimate per peak;
+ *   retina_multistart_optimize_ex  the same update loop, optionally evaluating only the pairs that
+ *                               can contribute (bit-identical results; RETINA_MS_CULLED);
  *   retina_multistart_newton    Algorithm 1 with the paper's Truncated-Newton update and sigma
  *   (_ex)                       schedule, PAPER.md:213-216 (+ per-seed evaluation counts);
  *   retina_pack_results         the per-rank record of the one multi-GPU result gather.
@@ -189,6 +191,31 @@ int retina_multistart_optimize(const retina_events *ev, int model, float sigma,
                                float step, const float *box_lo, const float *box_hi,
                                float *theta_out, float *response_out, float *grad_out,
                                void *stream);
+
+/* retina_multistart_optimize with an explicit algorithm:
+ *   RETINA_MS_DENSE   evaluates every (seed, hit) pair of every pass (what retina_multistart_optimize
+ *                     does; workspace unused);
+ *   RETINA_MS_CULLED  SLOPE2 only (RETINA_EUNSUPPORTED otherwise): the SAME results bit for bit,
+ *                     evaluating only the pairs that can contribute.  With ex2.approx.ftz a pair
+ *                     whose exponent -K s^2 is below -126 adds exactly +0 to R and to the gradient
+ *                     sums; the seeds of each event are ordered along a Morton curve of (tx, ty) so
+ *                     that every warp's 256 seeds cover a small box, and per pass each warp skips the
+ *                     hits that a conservative bound puts beyond K s^2 > 128 for all of them, visiting
+ *                     the others in hit order with K4's arithmetic.  Needs a DEVICE workspace of at
+ *                     least retina_multistart_workspace_size() bytes (the per-event permutation;
+ *                     contents on entry do not matter); n_seeds <= 16,384 (the per-event sort runs in
+ *                     shared memory).  Events larger than the hit stage run the dense passes.
+ *   pairs_evaluated:  device uint64 or NULL: the (seed, hit) pairs actually evaluated are ADDED to
+ *                     it (all pairs for RETINA_MS_DENSE).
+ * Other arguments as retina_multistart_optimize. */
+enum { RETINA_MS_DENSE = 0, RETINA_MS_CULLED = 1 };
+size_t retina_multistart_workspace_size(int32_t n_events, int32_t n_seeds, int algorithm);
+int retina_multistart_optimize_ex(const retina_events *ev, int model, float sigma,
+                                  int32_t n_seeds, const float *seeds, int32_t n_iters,
+                                  float step, const float *box_lo, const float *box_hi,
+                                  float *theta_out, float *response_out, float *grad_out,
+                                  int algorithm, void *workspace, size_t workspace_bytes,
+                                  unsigned long long *pairs_evaluated, void *stream);
 
 /* Algorithm 1 with the paper's own update (Z22-Z25): q = n_steps
  * Truncated-Newton steps, step j at bandwidth sigmas[j] with R, grad R and the Hessian H R from

@@ -273,7 +273,30 @@ int retina_multistart_optimize(const retina_events *ev, int model, float sigma, 
                                const float *seeds, int32_t n_iters, float step, const float *box_lo,
                                const float *box_hi, float *theta_out, float *response_out,
                                float *grad_out, void *stream) {
+    return retina_multistart_optimize_ex(ev, model, sigma, n_seeds, seeds, n_iters, step, box_lo, box_hi, theta_out,
+                                         response_out, grad_out, RETINA_MS_DENSE, nullptr, 0, nullptr, stream);
+}
+
+size_t retina_multistart_workspace_size(int32_t n_events, int32_t n_seeds, int algorithm) {
+    if (algorithm != RETINA_MS_CULLED || n_events <= 0 || n_seeds <= 0) return 0;
+    return retina::multistart_culled_workspace_bytes(n_events, n_seeds);
+}
+
+// the dense path's pair count: hits x seeds x (n_iters + 1) passes, added on the device
+__global__ void add_dense_pairs_kernel(const int32_t *offsets, int n_events, long long seeds_passes,
+                                       unsigned long long *pairs) {
+    if (blockIdx.x == 0 && threadIdx.x == 0)
+        atomicAdd(pairs, (unsigned long long)(offsets[n_events] - offsets[0]) * (unsigned long long)seeds_passes);
+}
+
+int retina_multistart_optimize_ex(const retina_events *ev, int model, float sigma, int32_t n_seeds,
+                                  const float *seeds, int32_t n_iters, float step, const float *box_lo,
+                                  const float *box_hi, float *theta_out, float *response_out, float *grad_out,
+                                  int algorithm, void *workspace, size_t workspace_bytes,
+                                  unsigned long long *pairs_evaluated, void *stream) {
     g_last_error[0] = 0;
+    if (algorithm != RETINA_MS_DENSE && algorithm != RETINA_MS_CULLED)
+        return fail(RETINA_EINVAL, "unknown multi-start algorithm %d", algorithm);
     int st = check_events(ev);
     if (st) return st;
     const int P = model_P(model);
@@ -309,7 +332,24 @@ int retina_multistart_optimize(const retina_events *ev, int model, float sigma, 
     a.R_out = response_out;
     a.grad_out = grad_out;
     a.cap = stage_cap(ev->max_event_hits, 4096);
-    const cudaError_t err = retina::launch_multistart(model, a, ev->n_events, (cudaStream_t)stream);
+    cudaError_t err;
+    if (algorithm == RETINA_MS_CULLED) {
+        if (!retina::multistart_culled_ok(model, n_seeds))
+            return fail(RETINA_EUNSUPPORTED, "RETINA_MS_CULLED: SLOPE2 with n_seeds <= 16384 only");
+        const size_t need = retina_multistart_workspace_size(ev->n_events, n_seeds, algorithm);
+        if (!workspace || workspace_bytes < need)
+            return fail(RETINA_EINVAL, "workspace of %zu bytes needed (got %zu)", need, workspace_bytes);
+        err = retina::launch_multistart_culled(a, ev->n_events, static_cast<int32_t *>(workspace), pairs_evaluated,
+                                               (cudaStream_t)stream);
+    } else {
+        err = retina::launch_multistart(model, a, ev->n_events, (cudaStream_t)stream);
+        if (err == cudaSuccess && pairs_evaluated) {
+            add_dense_pairs_kernel<<<1, 32, 0, (cudaStream_t)stream>>>(ev->offsets, ev->n_events,
+                                                                      (long long)n_seeds * (n_iters + 1),
+                                                                      pairs_evaluated);
+            err = cudaGetLastError();
+        }
+    }
     if (err != cudaSuccess) return cuda_fail(err, "retina_multistart_optimize");
     return RETINA_OK;
 }

@@ -21,6 +21,9 @@
 #include "common.cuh"
 #include "kernels.cuh"
 
+#include <algorithm>
+#include <type_traits>
+
 namespace retina {
 
 #ifndef RETINA_MS_THREADS
@@ -504,6 +507,317 @@ cudaError_t launch_multistart(int model, const MultistartArgs &a, int n_events, 
         case kSlope3: return launch_ms<kSlope3, false>(a, n_events, stream);
     }
     return cudaErrorInvalidValue;
+}
+
+// =====================================================================================================
+// K4c: the SLOPE2 multi-start update loop of K4 (Algorithm 1 update loop,
+// PAPER.md:144-153; Z7) computing the SAME results bit for bit while evaluating only the
+// (seed, hit) pairs that can contribute.
+//
+// Why it is exact: w = ex2.approx.ftz(-K s^2) is +0 whenever -K s^2 < -126 (the result would be
+// subnormal and is flushed), and adding w = +0 to R, or w * s_x = +-0 to the gradient sums, leaves
+// them unchanged (the sums never hold -0: they start at +0 and -0 + +0 = +0).  A hit is skipped by a
+// warp only when a conservative bound proves K s^2 > 128 for EVERY seed of the warp; the warp then
+// visits the remaining hits in the original hit order with the same operations as K4 (FFMA2 seed
+// pairs, per-plane gradient sums flushed at each change of z), so every sum sees the same non-zero
+// terms in the same order.
+//
+// Where the speed comes from: seeds are first ordered per event along a Morton curve of (tx, ty)
+// (K4c-sort, one CTA per event; the outputs go back to the caller's seed order), so the 256 seeds of
+// a warp (8 per lane) cover a small box of parameter space.  Per iteration each warp reduces its box,
+// lists (ballot, in order) the hits within reach of the box -- on cfg3 about one hit in ten -- and
+// evaluates only those.  The work actually done is counted (pairs_evaluated).
+#ifndef RETINA_MC_MINB
+#define RETINA_MC_MINB 5  // CTAs per SM the register budget allows (96 registers: no spills)
+#endif
+constexpr int kMcThreads = 128, kMcSeeds = 8, kMcWarps = kMcThreads / 32;
+
+// ---------------------------------------------------------------- K4c-sort: Morton order per event
+// perm[e][q] = caller index of the q-th seed of event e along a Morton curve of (tx, ty) quantised
+// to 16 bits per axis over the prior box.  Bitonic sort of (key << 32 | index) in shared memory.
+__global__ void __launch_bounds__(1024) seed_morton_sort_kernel(const float *seeds, int n_seeds, int np2,
+                                                                float lo0, float hi0, float lo1, float hi1,
+                                                                int32_t *perm, int e_base) {
+    extern __shared__ unsigned long long s_key[];
+    const int e = e_base + blockIdx.x;
+    const float *sd = seeds + (int64_t)e * n_seeds * 2;
+    const float sx = 65535.f / fmaxf(hi0 - lo0, 1e-30f), sy = 65535.f / fmaxf(hi1 - lo1, 1e-30f);
+    for (int i = threadIdx.x; i < np2; i += blockDim.x) {
+        unsigned long long k = ~0ull;
+        if (i < n_seeds) {
+            const uint32_t qx = (uint32_t)fminf(fmaxf((sd[2 * i] - lo0) * sx, 0.f), 65535.f);
+            const uint32_t qy = (uint32_t)fminf(fmaxf((sd[2 * i + 1] - lo1) * sy, 0.f), 65535.f);
+            uint32_t m = 0;
+#pragma unroll
+            for (int b = 0; b < 16; ++b) m |= (((qx >> b) & 1u) << (2 * b)) | (((qy >> b) & 1u) << (2 * b + 1));
+            k = ((unsigned long long)m << 32) | (uint32_t)i;
+        }
+        s_key[i] = k;
+    }
+    __syncthreads();
+    for (int size = 2; size <= np2; size <<= 1)
+        for (int stride = size >> 1; stride > 0; stride >>= 1) {
+            for (int i = threadIdx.x; i < np2; i += blockDim.x) {
+                const int j = i ^ stride;
+                if (j > i) {
+                    const bool up = (i & size) == 0;
+                    const unsigned long long a = s_key[i], b = s_key[j];
+                    if ((a > b) == up) {
+                        s_key[i] = b;
+                        s_key[j] = a;
+                    }
+                }
+            }
+            __syncthreads();
+        }
+    for (int i = threadIdx.x; i < n_seeds; i += blockDim.x)
+        perm[(int64_t)e * n_seeds + i] = (int32_t)(s_key[i] & 0xffffffffull);
+}
+
+// ---------------------------------------------------------------- K4c
+template <bool ZREF, bool GRAD, bool WANT_R>
+__device__ __forceinline__ void mc_pass(const float4 *h, const uint16_t *list, int L, const float (&th)[kMcSeeds][3],
+                                        float negK, float zref, float (&R)[kMcSeeds], float (&G)[kMcSeeds][2]) {
+    constexpr int NP = kMcSeeds / 2;
+    float2 mtx[NP], mty[NP], r2[NP], qx[NP], qy[NP], gx[NP], gy[NP];
+    const float2 zero = make_float2(0.f, 0.f), nk = make_float2(negK, negK);
+#pragma unroll
+    for (int p = 0; p < NP; ++p) {
+        mtx[p] = make_float2(-th[2 * p][0], -th[2 * p + 1][0]);
+        mty[p] = make_float2(-th[2 * p][1], -th[2 * p + 1][1]);
+        r2[p] = qx[p] = qy[p] = gx[p] = gy[p] = zero;
+    }
+    float zprev = __int_as_float(0x7fc00000);
+    float dprev = 0.f, dlprev = 0.f;
+    auto flush = [&]() {
+#pragma unroll
+        for (int p = 0; p < NP; ++p) {
+            const float2 d = make_float2(dprev, dprev);
+            gx[p] = __ffma2_rn(d, qx[p], gx[p]);
+            gy[p] = __ffma2_rn(d, qy[p], gy[p]);
+            qx[p] = qy[p] = zero;
+        }
+    };
+#pragma unroll 2
+    for (int t = 0; t < L; ++t) {
+        const float4 hk = h[list[t]];
+        if (hk.z != zprev) {  // warp-uniform: the list is the warp's
+            if (GRAD) flush();
+            zprev = hk.z;
+            if (ZREF)
+                two_sum(hk.z, -zref, dprev, dlprev);
+            else
+                dprev = hk.z;
+        }
+        const float2 X = make_float2(hk.x, hk.x), Y = make_float2(hk.y, hk.y);
+#pragma unroll
+        for (int p = 0; p < NP; ++p) {
+            float2 sx, sy;
+            if (ZREF) {
+                const float2 D = make_float2(dprev, dprev), DL = make_float2(dlprev, dlprev);
+                sx = __ffma2_rn(mtx[p], DL, __ffma2_rn(mtx[p], D, X));
+                sy = __ffma2_rn(mty[p], DL, __ffma2_rn(mty[p], D, Y));
+            } else {
+                const float2 Z = make_float2(hk.z, hk.z);
+                sx = __ffma2_rn(mtx[p], Z, X);
+                sy = __ffma2_rn(mty[p], Z, Y);
+            }
+            const float2 a = __fmul2_rn(__ffma2_rn(sx, sx, __fmul2_rn(sy, sy)), nk);
+            const float2 w = make_float2(ex2_approx(a.x), ex2_approx(a.y));
+            if (WANT_R) r2[p] = __fadd2_rn(r2[p], w);
+            if (GRAD) {
+                qx[p] = __ffma2_rn(w, sx, qx[p]);
+                qy[p] = __ffma2_rn(w, sy, qy[p]);
+            }
+        }
+    }
+    if (GRAD) flush();
+#pragma unroll
+    for (int p = 0; p < NP; ++p) {
+        R[2 * p] = r2[p].x;
+        R[2 * p + 1] = r2[p].y;
+        G[2 * p][0] = gx[p].x;
+        G[2 * p + 1][0] = gx[p].y;
+        G[2 * p][1] = gy[p].x;
+        G[2 * p + 1][1] = gy[p].y;
+    }
+}
+
+// The warp's list of hits within reach: hit k is kept unless, for every (tx, ty) in the warp's
+// box, K ((x - tx d)^2 + (y - ty d)^2) > 128 (then every seed's ex2 argument is < -126 with room for
+// fp32 rounding: w = +0 exactly).  In hit order; returns the length.
+template <bool ZREF>
+__device__ __forceinline__ int mc_build_list(const float4 *h, int n, const float (&th)[kMcSeeds][3], const bool (&ok)[kMcSeeds],
+                                             float K, float zref, uint16_t *list) {
+    const int lane = threadIdx.x & 31;
+    float a0 = 3.4e38f, b0 = -3.4e38f, a1 = 3.4e38f, b1 = -3.4e38f;
+#pragma unroll
+    for (int s = 0; s < kMcSeeds; ++s)
+        if (ok[s]) {
+            a0 = fminf(a0, th[s][0]);
+            b0 = fmaxf(b0, th[s][0]);
+            a1 = fminf(a1, th[s][1]);
+            b1 = fmaxf(b1, th[s][1]);
+        }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        a0 = fminf(a0, __shfl_xor_sync(0xffffffffu, a0, o));
+        b0 = fmaxf(b0, __shfl_xor_sync(0xffffffffu, b0, o));
+        a1 = fminf(a1, __shfl_xor_sync(0xffffffffu, a1, o));
+        b1 = fmaxf(b1, __shfl_xor_sync(0xffffffffu, b1, o));
+    }
+    if (a0 > b0) return 0;  // no valid seed in this warp
+    int L = 0;
+    for (int k0 = 0; k0 < n; k0 += 32) {
+        const int k = k0 + lane;
+        bool keep = false;
+        if (k < n) {
+            const float4 hk = h[k];
+            const float d = ZREF ? __fsub_rn(hk.z, zref) : hk.z;
+            // s_x over tx in [a0, b0] is monotone: its least |value| is 0 if the ends differ in sign
+            const float ex1 = __fmaf_rn(-a0, d, hk.x), ex2 = __fmaf_rn(-b0, d, hk.x);
+            const float ey1 = __fmaf_rn(-a1, d, hk.y), ey2 = __fmaf_rn(-b1, d, hk.y);
+            const float mx = (ex1 > 0.f) == (ex2 > 0.f) && ex1 != 0.f ? fminf(fabsf(ex1), fabsf(ex2)) : 0.f;
+            const float my = (ey1 > 0.f) == (ey2 > 0.f) && ey1 != 0.f ? fminf(fabsf(ey1), fabsf(ey2)) : 0.f;
+            // shrink by 1e-5 relative (the fp32 rounding of the ends) before the comparison
+            keep = K * __fmaf_rn(mx, mx, my * my) * 0.99999f <= 128.f;
+        }
+        const unsigned b = __ballot_sync(0xffffffffu, keep);
+        if (keep) list[L + __popc(b & ((1u << lane) - 1u))] = (uint16_t)k;
+        L += __popc(b);
+    }
+    __syncwarp();
+    return L;
+}
+
+template <bool ZREF>
+__global__ void __launch_bounds__(kMcThreads, RETINA_MC_MINB) multistart_culled_kernel(MultistartArgs a, const int32_t *perm,
+                                                                         unsigned long long *pairs_evaluated) {
+    extern __shared__ __align__(16) float4 s_hits[];  // [cap] hits, then [warps][cap] uint16 lists
+    __shared__ __align__(8) uint64_t s_bar[2];
+    const int e = a.e_base + blockIdx.y;
+    const int start = a.offsets[e], nh = a.offsets[e + 1] - start;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    HitStage st;
+    st.init(s_hits, s_bar, a.hits + start, nh, a.cap);
+    // an event larger than the stage (max_event_hits is only a hint) runs K4's dense passes, streamed
+    const bool culled = nh <= a.cap && nh <= 65535 && (nh == 0 || st.load_resident());
+    uint16_t *list = reinterpret_cast<uint16_t *>(s_hits + a.cap) + warp * a.cap;
+    const float K = -a.negK;
+
+    // the warp's 256 consecutive seeds of the Morton order (8 per lane, 32 consecutive per s)
+    const int32_t *pe = perm + (int64_t)e * a.n_seeds;
+    const int q0 = blockIdx.x * (kMcThreads * kMcSeeds) + warp * 32 * kMcSeeds + lane;
+    bool ok[kMcSeeds];
+    float th[kMcSeeds][3];
+#pragma unroll
+    for (int s = 0; s < kMcSeeds; ++s) {
+        const int q = q0 + s * 32;
+        ok[s] = q < a.n_seeds;
+        const int64_t src = ((int64_t)e * a.n_seeds + __ldg(pe + min(q, a.n_seeds - 1))) * 2;
+        th[s][0] = __ldg(a.seeds + src);
+        th[s][1] = __ldg(a.seeds + src + 1);
+        th[s][2] = 0.f;
+    }
+    int nvalid = 0;
+#pragma unroll
+    for (int s = 0; s < kMcSeeds; ++s) nvalid += ok[s] ? 1 : 0;
+    nvalid = __reduce_add_sync(0xffffffffu, nvalid);
+    unsigned long long evaluated = 0;
+
+    float R[kMcSeeds], G[kMcSeeds][2], g[kMcSeeds][2];
+    const PlaneTable no_table{nullptr, nullptr, -1, nullptr};
+    auto pass = [&](auto grad_tag, auto want_r_tag) {  // one pass over the hits in reach, or all of them
+        constexpr bool GR = decltype(grad_tag)::value, WR = decltype(want_r_tag)::value;
+        if (culled) {
+            const int L = mc_build_list<ZREF>(st.buf, nh, th, ok, K, a.z_ref, list);
+            evaluated += (unsigned long long)L * nvalid;
+            mc_pass<ZREF, GR, WR>(st.buf, list, L, th, a.negK, a.z_ref, R, G);
+        } else {
+            float G4[kMcSeeds][4];
+            ms_eval<kSlope2, kMcSeeds, ZREF, GR, WR>(st, th, a.negK, a.z_ref, R, G4, a.sk, no_table);
+#pragma unroll
+            for (int s = 0; s < kMcSeeds; ++s) {
+                G[s][0] = G4[s][0];
+                G[s][1] = G4[s][1];
+            }
+            evaluated += (unsigned long long)nh * nvalid;
+        }
+    };
+    for (int it = 0; it < a.n_iters; ++it) {
+        pass(std::true_type{}, std::false_type{});
+#pragma unroll
+        for (int s = 0; s < kMcSeeds; ++s) {
+            g[s][0] = __fmul_rn(a.c2, G[s][0]);
+            g[s][1] = __fmul_rn(a.c2, G[s][1]);
+#pragma unroll
+            for (int i = 0; i < 2; ++i)
+                th[s][i] = fminf(fmaxf(__fmaf_rn(a.step, g[s][i], th[s][i]), a.lo[i]), a.hi[i]);
+        }
+    }
+    if (a.grad_out) {
+        pass(std::true_type{}, std::true_type{});
+#pragma unroll
+        for (int s = 0; s < kMcSeeds; ++s) {
+            g[s][0] = __fmul_rn(a.c2, G[s][0]);
+            g[s][1] = __fmul_rn(a.c2, G[s][1]);
+        }
+    } else {
+        pass(std::false_type{}, std::true_type{});
+    }
+#pragma unroll
+    for (int s = 0; s < kMcSeeds; ++s) {
+        if (!ok[s]) continue;
+        const int64_t o = (int64_t)e * a.n_seeds + __ldg(pe + q0 + s * 32);
+        a.R_out[o] = R[s];
+        a.theta_out[o * 2] = th[s][0];
+        a.theta_out[o * 2 + 1] = th[s][1];
+        if (a.grad_out) {
+            a.grad_out[o * 2] = g[s][0];
+            a.grad_out[o * 2 + 1] = g[s][1];
+        }
+    }
+    if (pairs_evaluated && lane == 0 && evaluated) atomicAdd(pairs_evaluated, evaluated);
+}
+
+size_t multistart_culled_workspace_bytes(long long n_events, int n_seeds) {
+    return (size_t)(n_events * n_seeds) * sizeof(int32_t);
+}
+
+bool multistart_culled_ok(int model, int n_seeds) {
+    // SLOPE2; the sort holds an event's seeds in shared memory
+    int np2 = 1;
+    while (np2 < n_seeds) np2 <<= 1;
+    return model == kSlope2 && n_seeds > 0 && np2 <= 16384;  // 128 KB of (key, index) words
+}
+
+cudaError_t launch_multistart_culled(const MultistartArgs &a0, int n_events, int32_t *perm,
+                                     unsigned long long *pairs_evaluated, cudaStream_t stream) {
+    if (n_events == 0 || a0.n_seeds == 0) return cudaSuccess;
+    int np2 = 1;
+    while (np2 < a0.n_seeds) np2 <<= 1;
+    const size_t sort_smem = (size_t)np2 * sizeof(unsigned long long);
+    cudaError_t err = ensure_dynamic_smem(seed_morton_sort_kernel, sort_smem);
+    if (err != cudaSuccess) return err;
+    MultistartArgs a = a0;
+    a.cap = ((std::max(a0.cap, 2) + 7) / 8) * 8;  // resident stage (events beyond it run dense)
+    const size_t smem = (size_t)a.cap * (sizeof(float4) + kMcWarps * sizeof(uint16_t));
+    auto kern = (a.z_ref == 0.f) ? multistart_culled_kernel<false> : multistart_culled_kernel<true>;
+    err = ensure_dynamic_smem(kern, smem);
+    if (err != cudaSuccess) return err;
+    const int blocks = (a.n_seeds + kMcThreads * kMcSeeds - 1) / (kMcThreads * kMcSeeds);
+    for (int e0 = 0; e0 < n_events; e0 += 65535) {
+        const int ne = std::min(65535, n_events - e0);
+        seed_morton_sort_kernel<<<ne, 1024, sort_smem, stream>>>(a.seeds, a.n_seeds, np2, a.lo[0], a.hi[0], a.lo[1],
+                                                                 a.hi[1], perm, e0);
+        err = cudaGetLastError();
+        if (err != cudaSuccess) return err;
+        a.e_base = e0;
+        kern<<<dim3(blocks, ne), kMcThreads, smem, stream>>>(a, perm, pairs_evaluated);
+        err = cudaGetLastError();
+        if (err != cudaSuccess) return err;
+    }
+    return cudaSuccess;
 }
 
 }  // namespace retina

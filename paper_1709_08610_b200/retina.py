@@ -21,10 +21,12 @@ MERGE_MAX_SEEDS = 16384
 
 GRID_AUTO, GRID_DIRECT, GRID_SEPARABLE, GRID_TENSOR, GRID_TENSOR_F16 = 0, 1, 2, 3, 4
 GRID_TENSOR_F16_PAIR, GRID_TENSOR_F16_SINGLE = 5, 6
+MS_DENSE, MS_CULLED = 0, 1
 
 EXPORTED = ("retina_grid_response", "retina_grid_response_ex", "retina_estimate_peaks", "retina_find_peaks",
             "retina_find_peaks_ws", "retina_find_peaks_workspace_size",
-            "retina_multistart_optimize", "retina_multistart_newton", "retina_multistart_newton_ex",
+            "retina_multistart_optimize", "retina_multistart_optimize_ex", "retina_multistart_workspace_size",
+            "retina_multistart_newton", "retina_multistart_newton_ex",
             "retina_merge_tracks", "retina_pack_results",
             "retina_status_string", "retina_last_error", "retina_version")
 PACK_HEADER = 8
@@ -70,6 +72,11 @@ def lib() -> ctypes.CDLL:
         L.retina_find_peaks_workspace_size.restype = ctypes.c_size_t
         L.retina_multistart_optimize.argtypes = [ctypes.POINTER(retina_events), ctypes.c_int, f32, i32, vp,
                                                  i32, f32, vp, vp, vp, vp, vp, vp]
+        L.retina_multistart_optimize_ex.argtypes = [ctypes.POINTER(retina_events), ctypes.c_int, f32, i32, vp,
+                                                    i32, f32, vp, vp, vp, vp, vp, ctypes.c_int, vp,
+                                                    ctypes.c_size_t, vp, vp]
+        L.retina_multistart_workspace_size.argtypes = [i32, i32, ctypes.c_int]
+        L.retina_multistart_workspace_size.restype = ctypes.c_size_t
         L.retina_multistart_newton.argtypes = [ctypes.POINTER(retina_events), ctypes.c_int, i32, vp, i32, vp, vp,
                                                f32, i32, vp, vp, vp, vp, vp, vp]
         L.retina_multistart_newton_ex.argtypes = [ctypes.POINTER(retina_events), ctypes.c_int, i32, vp, i32, vp,
@@ -77,7 +84,8 @@ def lib() -> ctypes.CDLL:
         L.retina_merge_tracks.argtypes = [i32, i32, i32, vp, vp, vp, f32, i32, vp, vp, vp, vp, vp, vp]
         L.retina_pack_results.argtypes = [i32, i32, i32, vp, vp, vp, i32, vp, vp, vp, vp, i32, vp, vp, vp]
         for f in (L.retina_grid_response, L.retina_grid_response_ex, L.retina_find_peaks, L.retina_estimate_peaks,
-                  L.retina_multistart_optimize, L.retina_multistart_newton, L.retina_multistart_newton_ex,
+                  L.retina_multistart_optimize, L.retina_multistart_optimize_ex, L.retina_multistart_newton,
+                  L.retina_multistart_newton_ex,
                   L.retina_merge_tracks, L.retina_pack_results):
             f.restype = ctypes.c_int
         L.retina_status_string.argtypes = [ctypes.c_int]
@@ -252,8 +260,13 @@ def retina_estimate_peaks(response: torch.Tensor, nodes: Sequence[torch.Tensor],
 
 def retina_multistart_optimize(events: Events, model: int, sigma: float, seeds: torch.Tensor,
                                n_iters: int, step: float, box_lo, box_hi, want_grad: bool = True,
-                               out=None, stream=None):
-    """Returns (theta_out [E,S,P], response_out [E,S], grad_out [E,S,P] or None)."""
+                               out=None, stream=None, algorithm: int = MS_DENSE,
+                               workspace: Optional[torch.Tensor] = None,
+                               pairs_evaluated: Optional[torch.Tensor] = None):
+    """Returns (theta_out [E,S,P], response_out [E,S], grad_out [E,S,P] or None).  algorithm=MS_CULLED
+    (SLOPE2) gives the same results bit for bit evaluating only the pairs that can contribute
+    (retina_multistart_optimize_ex; a workspace is allocated if none is passed); pairs_evaluated, an
+    int64 [1] device tensor, accumulates the pairs actually evaluated."""
     P = MODEL_P[model]
     _dev(seeds, torch.float32)
     E, S, Ps = seeds.shape
@@ -267,11 +280,34 @@ def retina_multistart_optimize(events: Events, model: int, sigma: float, seeds: 
     _out("theta_out", th, torch.float32, (E, S, P), seeds.device)
     _out("response_out", R, torch.float32, (E, S), seeds.device)
     _out("grad_out", g, torch.float32, (E, S, P), seeds.device)
-    _check("retina_multistart_optimize",
-           lib().retina_multistart_optimize(ctypes.byref(events.c), model, float(sigma), S, _ptr(seeds),
-                                            int(n_iters), float(step), lo, hi, _ptr(th), _ptr(R), _ptr(g),
-                                            _stream(stream)))
+    if algorithm == MS_DENSE and workspace is None and pairs_evaluated is None:
+        _check("retina_multistart_optimize",
+               lib().retina_multistart_optimize(ctypes.byref(events.c), model, float(sigma), S, _ptr(seeds),
+                                                int(n_iters), float(step), lo, hi, _ptr(th), _ptr(R), _ptr(g),
+                                                _stream(stream)))
+        return th, R, g
+    if algorithm == MS_CULLED and workspace is None:
+        nbytes = multistart_workspace_size(E, S, algorithm)
+        workspace = torch.empty((max(nbytes, 4) // 4,), dtype=torch.int32, device=seeds.device)
+    nbytes = 0
+    if workspace is not None:
+        _dev(workspace, workspace.dtype)
+        if workspace.device != seeds.device:
+            raise ValueError("workspace on another device")
+        nbytes = workspace.numel() * workspace.element_size()
+    if pairs_evaluated is not None:
+        _out("pairs_evaluated", pairs_evaluated, torch.int64, (1,), seeds.device)
+    _check("retina_multistart_optimize_ex",
+           lib().retina_multistart_optimize_ex(ctypes.byref(events.c), model, float(sigma), S, _ptr(seeds),
+                                               int(n_iters), float(step), lo, hi, _ptr(th), _ptr(R), _ptr(g),
+                                               int(algorithm), _ptr(workspace), ctypes.c_size_t(nbytes),
+                                               _ptr(pairs_evaluated), _stream(stream)))
     return th, R, g
+
+
+def multistart_workspace_size(n_events: int, n_seeds: int, algorithm: int = MS_CULLED) -> int:
+    """Bytes of device workspace retina_multistart_optimize_ex needs (0 for MS_DENSE)."""
+    return int(lib().retina_multistart_workspace_size(int(n_events), int(n_seeds), int(algorithm)))
 
 
 def retina_multistart_newton(events: Events, model: int, seeds: torch.Tensor, sigmas, etas, final_sigma: float,

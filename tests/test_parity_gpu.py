@@ -391,6 +391,70 @@ def test_T7_merge_synthetic_ties_and_capacity():
             assert np.array_equal(tz.cpu().numpy()[e, :k], otz[e, :k])
 
 
+# --------------------------------------------------------------------------- K4c: culled = dense, bit for bit
+@pytest.mark.parametrize("name,n_ev,n_seeds,n_iters,z_ref,want_grad,hint", [
+    ("cfg2", 4, 4096, 50, 0.0, True, None), ("cfg2", 3, 1000, 20, 23.5, True, None),
+    ("cfg3", 2, 8192, 50, 0.0, False, None),  # the bench launch configuration
+    ("cfg3", 2, 8192, 0, 0.0, True, None), ("cfg2", 3, 777, 7, 0.0, True, 64)])  # hint 64: events run dense
+def test_multistart_culled_bitwise_equal_to_dense(name, n_ev, n_seeds, n_iters, z_ref, want_grad, hint):
+    """RETINA_MS_CULLED skips only pairs whose ex2.approx.ftz weight is exactly +0 and visits the
+    others in hit order with K4's arithmetic: theta, R and grad R equal the dense kernel's bit for
+    bit; it evaluates fewer pairs than the dense count (all pairs of all passes)."""
+    cfg = C.CONFIGS[name]
+    ev_ids = list(range(n_ev))
+    b = G.make_batch(cfg, ev_ids)
+    # plus an empty event and a single-hit event
+    off = np.concatenate([b.offsets, [b.offsets[-1], b.offsets[-1] + 1]]).astype(np.int32)
+    hits = np.concatenate([b.hits, b.hits[:1]])
+    seeds = np.concatenate([G.make_seeds(cfg, ev_ids, n_seeds=n_seeds)] * 1 +
+                           [G.make_seeds(cfg, [0, 1], n_seeds=n_seeds)], axis=0)
+    ev = R.Events.from_numpy(off, hits, z_ref=z_ref, max_event_hits=hint)
+    step = cfg.step if cfg.step else C.step_slope2(cfg.sigma)
+    dense = R.retina_multistart_optimize(ev, cfg.model, cfg.sigma, dev(seeds), n_iters, step, cfg.box_lo,
+                                         cfg.box_hi, want_grad=want_grad)
+    pd = torch.zeros(1, dtype=torch.int64, device=DEV)
+    pc = torch.zeros(1, dtype=torch.int64, device=DEV)
+    dense2 = R.retina_multistart_optimize(ev, cfg.model, cfg.sigma, dev(seeds), n_iters, step, cfg.box_lo,
+                                          cfg.box_hi, want_grad=want_grad, pairs_evaluated=pd)
+    culled = R.retina_multistart_optimize(ev, cfg.model, cfg.sigma, dev(seeds), n_iters, step, cfg.box_lo,
+                                          cfg.box_hi, want_grad=want_grad, algorithm=R.retina.MS_CULLED,
+                                          pairs_evaluated=pc)
+    torch.cuda.synchronize()
+    for x, y, z in zip(dense, dense2, culled):
+        if x is None:
+            assert y is None and z is None
+            continue
+        assert torch.equal(x, y)
+        assert torch.equal(x.view(torch.int32), z.view(torch.int32))  # bit for bit, signs of zeros included
+    total = int(off[-1]) * seeds.shape[1] * (n_iters + 1)
+    assert int(pd.item()) == total
+    n_pc = int(pc.item())
+    assert 0 < n_pc <= total
+    if hint is None:
+        assert n_pc < total
+    PU.report(f"K4c {name} S={n_seeds} it={n_iters}", pairs_all=total, pairs_evaluated=n_pc,
+              evaluated_frac=n_pc / total)
+
+
+def test_multistart_culled_unsupported_and_workspace():
+    cfg = C.CFG4
+    b = G.make_batch(cfg, [0])
+    ev = events_of(b)
+    seeds = dev(G.make_seeds(cfg, [0], n_seeds=64))
+    with pytest.raises(R.retina.RetinaError):  # SLOPE3
+        R.retina_multistart_optimize(ev, cfg.model, cfg.sigma, seeds, 1, cfg.step, cfg.box_lo, cfg.box_hi,
+                                     algorithm=R.retina.MS_CULLED)
+    c2 = C.CFG2
+    b2 = G.make_batch(c2, [0])
+    s2 = dev(G.make_seeds(c2, [0], n_seeds=32))
+    ws = torch.empty(1, dtype=torch.int32, device=DEV)  # 4 bytes: too small for 32 seeds
+    with pytest.raises(R.retina.RetinaError):
+        R.retina_multistart_optimize(events_of(b2), c2.model, c2.sigma, s2, 1, c2.step, c2.box_lo, c2.box_hi,
+                                     algorithm=R.retina.MS_CULLED, workspace=ws)
+    assert R.retina.multistart_workspace_size(3, 100) == 3 * 100 * 4
+    assert R.retina.multistart_workspace_size(3, 100, R.retina.MS_DENSE) == 0
+
+
 # --------------------------------------------------------------------------- identities / edges
 def test_multistart_identities_and_determinism():
     cfg = C.CFG2

@@ -98,7 +98,7 @@ def main():
             med, mn = timeit(run_peaks)
             byts = 4.0 * cfg.n_units * chunk * n_chunks
             emit("peaks", med, mn, grid_bytes=byts, gbs=byts / (med * 1e-3) / 1e9, frac_hbm=byts / (med * 1e-3) / 6550.7e9)
-    if "ms" in phases or "newton" in phases:
+    if "ms" in phases or "newton" in phases or "culled" in phases:
         seeds = torch.from_numpy(G.make_seeds(cfg, ev_ids)).cuda()
         th = torch.empty_like(seeds)
         Rr = torch.empty(seeds.shape[:2], device="cuda")
@@ -109,6 +109,23 @@ def main():
             med, mn = timeit(run_ms)
             pairs = nh * cfg.n_seeds * (cfg.n_iters + 1)
             emit("ms", med, mn, pairs=pairs, frac_mufu=pairs / (med * 1e-3) / MUFU)
+        if "culled" in phases:  # K4c: same results, only the pairs that can contribute
+            ws = torch.empty((RT.multistart_workspace_size(len(ev_ids), cfg.n_seeds) // 4 + 1,), dtype=torch.int32,
+                             device="cuda")
+            pc = torch.zeros(1, dtype=torch.int64, device="cuda")
+
+            def run_mc():
+                R.retina_multistart_optimize(ev, cfg.model, cfg.sigma, seeds, cfg.n_iters, cfg.step, cfg.box_lo,
+                                             cfg.box_hi, want_grad=False, out=(th, Rr, None),
+                                             algorithm=RT.MS_CULLED, workspace=ws, pairs_evaluated=pc)
+            med, mn = timeit(run_mc)
+            pc.zero_()
+            run_mc()
+            torch.cuda.synchronize()
+            pairs = nh * cfg.n_seeds * (cfg.n_iters + 1)
+            ev_pairs = float(pc.item())
+            emit("culled", med, mn, pairs=pairs, pairs_evaluated=ev_pairs, evaluated_frac=ev_pairs / pairs,
+                 frac_mufu_evaluated=ev_pairs / (med * 1e-3) / MUFU, events_per_s=len(ev_ids) / (med * 1e-3))
         if "newton" in phases:
             sig, eta, fsig, mh = C.newton_schedule(cfg)
             ne = torch.empty(seeds.shape[:2], dtype=torch.int32, device="cuda")
