@@ -530,7 +530,16 @@ cudaError_t launch_multistart(int model, const MultistartArgs &a, int n_events, 
 #ifndef RETINA_MC_MINB
 #define RETINA_MC_MINB 5  // CTAs per SM the register budget allows (96 registers: no spills)
 #endif
-constexpr int kMcThreads = 128, kMcSeeds = 8, kMcWarps = kMcThreads / 32;
+#ifndef RETINA_MC_MARGIN
+#define RETINA_MC_MARGIN 0.02f  // list box margin, relative to the seeds' box
+#endif
+#ifndef RETINA_MC_MARGIN_ABS
+#define RETINA_MC_MARGIN_ABS 1e-5f
+#endif
+#ifndef RETINA_MC_UNITS
+#define RETINA_MC_UNITS 16  // at most this many units of 256 seeds per block, dealt to its 4 warps
+#endif
+constexpr int kMcThreads = 128, kMcSeeds = 8, kMcWarps = kMcThreads / 32, kMcUnits = RETINA_MC_UNITS;
 
 // ---------------------------------------------------------------- K4c-sort: Morton order per event
 // perm[e][q] = caller index of the q-th seed of event e along a Morton curve of (tx, ty) quantised
@@ -643,30 +652,39 @@ __device__ __forceinline__ void mc_pass(const float4 *h, const uint16_t *list, i
     }
 }
 
-// The warp's list of hits within reach: hit k is kept unless, for every (tx, ty) in the warp's
-// box, K ((x - tx d)^2 + (y - ty d)^2) > 128 (then every seed's ex2 argument is < -126 with room for
-// fp32 rounding: w = +0 exactly).  In hit order; returns the length.
-template <bool ZREF>
-__device__ __forceinline__ int mc_build_list(const float4 *h, int n, const float (&th)[kMcSeeds][3], const bool (&ok)[kMcSeeds],
-                                             float K, float zref, uint16_t *list) {
-    const int lane = threadIdx.x & 31;
-    float a0 = 3.4e38f, b0 = -3.4e38f, a1 = 3.4e38f, b1 = -3.4e38f;
+struct McBox {
+    float a0, b0, a1, b1;  // [a0, b0] x [a1, b1] in (tx, ty); a0 > b0: empty
+};
+
+// the box of the warp's valid seeds (warp-uniform)
+__device__ __forceinline__ McBox mc_warp_box(const float (&th)[kMcSeeds][3], const bool (&ok)[kMcSeeds]) {
+    McBox b{3.4e38f, -3.4e38f, 3.4e38f, -3.4e38f};
 #pragma unroll
     for (int s = 0; s < kMcSeeds; ++s)
         if (ok[s]) {
-            a0 = fminf(a0, th[s][0]);
-            b0 = fmaxf(b0, th[s][0]);
-            a1 = fminf(a1, th[s][1]);
-            b1 = fmaxf(b1, th[s][1]);
+            b.a0 = fminf(b.a0, th[s][0]);
+            b.b0 = fmaxf(b.b0, th[s][0]);
+            b.a1 = fminf(b.a1, th[s][1]);
+            b.b1 = fmaxf(b.b1, th[s][1]);
         }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
-        a0 = fminf(a0, __shfl_xor_sync(0xffffffffu, a0, o));
-        b0 = fmaxf(b0, __shfl_xor_sync(0xffffffffu, b0, o));
-        a1 = fminf(a1, __shfl_xor_sync(0xffffffffu, a1, o));
-        b1 = fmaxf(b1, __shfl_xor_sync(0xffffffffu, b1, o));
+        b.a0 = fminf(b.a0, __shfl_xor_sync(0xffffffffu, b.a0, o));
+        b.b0 = fmaxf(b.b0, __shfl_xor_sync(0xffffffffu, b.b0, o));
+        b.a1 = fminf(b.a1, __shfl_xor_sync(0xffffffffu, b.a1, o));
+        b.b1 = fmaxf(b.b1, __shfl_xor_sync(0xffffffffu, b.b1, o));
     }
-    if (a0 > b0) return 0;  // no valid seed in this warp
+    return b;
+}
+
+// The warp's list of hits within reach of the box B: hit k is kept unless, for every (tx, ty) in
+// B, K ((x - tx d)^2 + (y - ty d)^2) > 128 (then every seed inside B has an ex2 argument < -126,
+// with room for fp32 rounding: w = +0 exactly).  In hit order; returns the length.
+template <bool ZREF>
+__device__ __forceinline__ int mc_build_list(const float4 *h, int n, const McBox &B, float K, float zref,
+                                             uint16_t *list) {
+    const int lane = threadIdx.x & 31;
+    if (B.a0 > B.b0) return 0;  // no valid seed in this warp
     int L = 0;
     for (int k0 = 0; k0 < n; k0 += 32) {
         const int k = k0 + lane;
@@ -675,8 +693,8 @@ __device__ __forceinline__ int mc_build_list(const float4 *h, int n, const float
             const float4 hk = h[k];
             const float d = ZREF ? __fsub_rn(hk.z, zref) : hk.z;
             // s_x over tx in [a0, b0] is monotone: its least |value| is 0 if the ends differ in sign
-            const float ex1 = __fmaf_rn(-a0, d, hk.x), ex2 = __fmaf_rn(-b0, d, hk.x);
-            const float ey1 = __fmaf_rn(-a1, d, hk.y), ey2 = __fmaf_rn(-b1, d, hk.y);
+            const float ex1 = __fmaf_rn(-B.a0, d, hk.x), ex2 = __fmaf_rn(-B.b0, d, hk.x);
+            const float ey1 = __fmaf_rn(-B.a1, d, hk.y), ey2 = __fmaf_rn(-B.b1, d, hk.y);
             const float mx = (ex1 > 0.f) == (ex2 > 0.f) && ex1 != 0.f ? fminf(fabsf(ex1), fabsf(ex2)) : 0.f;
             const float my = (ey1 > 0.f) == (ey2 > 0.f) && ey1 != 0.f ? fminf(fabsf(ey1), fabsf(ey2)) : 0.f;
             // shrink by 1e-5 relative (the fp32 rounding of the ends) before the comparison
@@ -692,89 +710,119 @@ __device__ __forceinline__ int mc_build_list(const float4 *h, int n, const float
 
 template <bool ZREF>
 __global__ void __launch_bounds__(kMcThreads, RETINA_MC_MINB) multistart_culled_kernel(MultistartArgs a, const int32_t *perm,
-                                                                         unsigned long long *pairs_evaluated) {
+                                                                         unsigned long long *pairs_evaluated,
+                                                                         int units_per_cta) {
     extern __shared__ __align__(16) float4 s_hits[];  // [cap] hits, then [warps][cap] uint16 lists
     __shared__ __align__(8) uint64_t s_bar[2];
     const int e = a.e_base + blockIdx.y;
     const int start = a.offsets[e], nh = a.offsets[e + 1] - start;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    __shared__ int s_next;
+    if (threadIdx.x == 0) s_next = 0;
     HitStage st;
-    st.init(s_hits, s_bar, a.hits + start, nh, a.cap);
+    st.init(s_hits, s_bar, a.hits + start, nh, a.cap);  // (its block barrier also publishes s_next)
     // an event larger than the stage (max_event_hits is only a hint) runs K4's dense passes, streamed
     const bool culled = nh <= a.cap && nh <= 65535 && (nh == 0 || st.load_resident());
     uint16_t *list = reinterpret_cast<uint16_t *>(s_hits + a.cap) + warp * a.cap;
     const float K = -a.negK;
 
-    // the warp's 256 consecutive seeds of the Morton order (8 per lane, 32 consecutive per s)
+    // Units of 256 seeds are dealt to the warps: dynamically (a shared counter) when the event is
+    // resident -- the warps' lists differ in length, so a fixed share would leave warps idle -- and
+    // round-robin in lockstep otherwise (the streamed dense passes synchronise the block).
     const int32_t *pe = perm + (int64_t)e * a.n_seeds;
-    const int q0 = blockIdx.x * (kMcThreads * kMcSeeds) + warp * 32 * kMcSeeds + lane;
-    bool ok[kMcSeeds];
-    float th[kMcSeeds][3];
-#pragma unroll
-    for (int s = 0; s < kMcSeeds; ++s) {
-        const int q = q0 + s * 32;
-        ok[s] = q < a.n_seeds;
-        const int64_t src = ((int64_t)e * a.n_seeds + __ldg(pe + min(q, a.n_seeds - 1))) * 2;
-        th[s][0] = __ldg(a.seeds + src);
-        th[s][1] = __ldg(a.seeds + src + 1);
-        th[s][2] = 0.f;
-    }
-    int nvalid = 0;
-#pragma unroll
-    for (int s = 0; s < kMcSeeds; ++s) nvalid += ok[s] ? 1 : 0;
-    nvalid = __reduce_add_sync(0xffffffffu, nvalid);
+    const int cta_seed0 = blockIdx.x * units_per_cta * 32 * kMcSeeds;
+    const int units = min(units_per_cta, (a.n_seeds - cta_seed0 + 32 * kMcSeeds - 1) / (32 * kMcSeeds));
     unsigned long long evaluated = 0;
-
-    float R[kMcSeeds], G[kMcSeeds][2], g[kMcSeeds][2];
-    const PlaneTable no_table{nullptr, nullptr, -1, nullptr};
-    auto pass = [&](auto grad_tag, auto want_r_tag) {  // one pass over the hits in reach, or all of them
-        constexpr bool GR = decltype(grad_tag)::value, WR = decltype(want_r_tag)::value;
+    for (int k = 0;; ++k) {
+        int u;
         if (culled) {
-            const int L = mc_build_list<ZREF>(st.buf, nh, th, ok, K, a.z_ref, list);
-            evaluated += (unsigned long long)L * nvalid;
-            mc_pass<ZREF, GR, WR>(st.buf, list, L, th, a.negK, a.z_ref, R, G);
+            if (lane == 0) u = atomicAdd(&s_next, 1);
+            u = __shfl_sync(0xffffffffu, u, 0);
+            if (u >= units) break;
         } else {
-            float G4[kMcSeeds][4];
-            ms_eval<kSlope2, kMcSeeds, ZREF, GR, WR>(st, th, a.negK, a.z_ref, R, G4, a.sk, no_table);
+            u = warp + kMcWarps * k;
+            if (k >= (units + kMcWarps - 1) / kMcWarps) break;
+        }
+        // a unit = 256 consecutive seeds of the Morton order (8 per lane, 32 consecutive per s)
+        const int q0 = cta_seed0 + u * 32 * kMcSeeds + lane;
+        bool ok[kMcSeeds];
+        float th[kMcSeeds][3];
+#pragma unroll
+        for (int s = 0; s < kMcSeeds; ++s) {
+            const int q = q0 + s * 32;
+            ok[s] = q < a.n_seeds;
+            const int64_t src = ((int64_t)e * a.n_seeds + __ldg(pe + min(q, a.n_seeds - 1))) * 2;
+            th[s][0] = __ldg(a.seeds + src);
+            th[s][1] = __ldg(a.seeds + src + 1);
+            th[s][2] = 0.f;
+        }
+        int nvalid = 0;
+#pragma unroll
+        for (int s = 0; s < kMcSeeds; ++s) nvalid += ok[s] ? 1 : 0;
+        nvalid = __reduce_add_sync(0xffffffffu, nvalid);
+        // The list is built for the seeds' box grown by a margin and rebuilt only when a seed leaves
+        // that box (a list built for a box covers every seed inside it, so reuse stays exact); fixed-
+        // step seeds move little per iteration.
+        McBox lb{1.f, 0.f, 1.f, 0.f};  // empty: build on the first pass
+        int L = 0;
+
+        float R[kMcSeeds], G[kMcSeeds][2], g[kMcSeeds][2];
+        const PlaneTable no_table{nullptr, nullptr, -1, nullptr};
+        auto pass = [&](auto grad_tag, auto want_r_tag) {  // one pass over the hits in reach, or all of them
+            constexpr bool GR = decltype(grad_tag)::value, WR = decltype(want_r_tag)::value;
+            if (culled) {
+                const McBox B = mc_warp_box(th, ok);
+                if (!(B.a0 >= lb.a0 && B.b0 <= lb.b0 && B.a1 >= lb.a1 && B.b1 <= lb.b1) || lb.a0 > lb.b0) {
+                    const float m0 = fmaxf(RETINA_MC_MARGIN_ABS, RETINA_MC_MARGIN * (B.b0 - B.a0));
+                    const float m1 = fmaxf(RETINA_MC_MARGIN_ABS, RETINA_MC_MARGIN * (B.b1 - B.a1));
+                    lb = (B.a0 > B.b0) ? B : McBox{B.a0 - m0, B.b0 + m0, B.a1 - m1, B.b1 + m1};
+                    L = mc_build_list<ZREF>(st.buf, nh, lb, K, a.z_ref, list);
+                }
+                evaluated += (unsigned long long)L * nvalid;
+                mc_pass<ZREF, GR, WR>(st.buf, list, L, th, a.negK, a.z_ref, R, G);
+            } else {
+                float G4[kMcSeeds][4];
+                ms_eval<kSlope2, kMcSeeds, ZREF, GR, WR>(st, th, a.negK, a.z_ref, R, G4, a.sk, no_table);
+#pragma unroll
+                for (int s = 0; s < kMcSeeds; ++s) {
+                    G[s][0] = G4[s][0];
+                    G[s][1] = G4[s][1];
+                }
+                evaluated += (unsigned long long)nh * nvalid;
+            }
+        };
+        for (int it = 0; it < a.n_iters; ++it) {
+            pass(std::true_type{}, std::false_type{});
 #pragma unroll
             for (int s = 0; s < kMcSeeds; ++s) {
-                G[s][0] = G4[s][0];
-                G[s][1] = G4[s][1];
+                g[s][0] = __fmul_rn(a.c2, G[s][0]);
+                g[s][1] = __fmul_rn(a.c2, G[s][1]);
+#pragma unroll
+                for (int i = 0; i < 2; ++i)
+                    th[s][i] = fminf(fmaxf(__fmaf_rn(a.step, g[s][i], th[s][i]), a.lo[i]), a.hi[i]);
             }
-            evaluated += (unsigned long long)nh * nvalid;
         }
-    };
-    for (int it = 0; it < a.n_iters; ++it) {
-        pass(std::true_type{}, std::false_type{});
-#pragma unroll
-        for (int s = 0; s < kMcSeeds; ++s) {
-            g[s][0] = __fmul_rn(a.c2, G[s][0]);
-            g[s][1] = __fmul_rn(a.c2, G[s][1]);
-#pragma unroll
-            for (int i = 0; i < 2; ++i)
-                th[s][i] = fminf(fmaxf(__fmaf_rn(a.step, g[s][i], th[s][i]), a.lo[i]), a.hi[i]);
-        }
-    }
-    if (a.grad_out) {
-        pass(std::true_type{}, std::true_type{});
-#pragma unroll
-        for (int s = 0; s < kMcSeeds; ++s) {
-            g[s][0] = __fmul_rn(a.c2, G[s][0]);
-            g[s][1] = __fmul_rn(a.c2, G[s][1]);
-        }
-    } else {
-        pass(std::false_type{}, std::true_type{});
-    }
-#pragma unroll
-    for (int s = 0; s < kMcSeeds; ++s) {
-        if (!ok[s]) continue;
-        const int64_t o = (int64_t)e * a.n_seeds + __ldg(pe + q0 + s * 32);
-        a.R_out[o] = R[s];
-        a.theta_out[o * 2] = th[s][0];
-        a.theta_out[o * 2 + 1] = th[s][1];
         if (a.grad_out) {
-            a.grad_out[o * 2] = g[s][0];
-            a.grad_out[o * 2 + 1] = g[s][1];
+            pass(std::true_type{}, std::true_type{});
+#pragma unroll
+            for (int s = 0; s < kMcSeeds; ++s) {
+                g[s][0] = __fmul_rn(a.c2, G[s][0]);
+                g[s][1] = __fmul_rn(a.c2, G[s][1]);
+            }
+        } else {
+            pass(std::false_type{}, std::true_type{});
+        }
+#pragma unroll
+        for (int s = 0; s < kMcSeeds; ++s) {
+            if (!ok[s]) continue;
+            const int64_t o = (int64_t)e * a.n_seeds + __ldg(pe + q0 + s * 32);
+            a.R_out[o] = R[s];
+            a.theta_out[o * 2] = th[s][0];
+            a.theta_out[o * 2 + 1] = th[s][1];
+            if (a.grad_out) {
+                a.grad_out[o * 2] = g[s][0];
+                a.grad_out[o * 2 + 1] = g[s][1];
+            }
         }
     }
     if (pairs_evaluated && lane == 0 && evaluated) atomicAdd(pairs_evaluated, evaluated);
@@ -805,7 +853,11 @@ cudaError_t launch_multistart_culled(const MultistartArgs &a0, int n_events, int
     auto kern = (a.z_ref == 0.f) ? multistart_culled_kernel<false> : multistart_culled_kernel<true>;
     err = ensure_dynamic_smem(kern, smem);
     if (err != cudaSuccess) return err;
-    const int blocks = (a.n_seeds + kMcThreads * kMcSeeds - 1) / (kMcThreads * kMcSeeds);
+    // units per block: up to kMcUnits, fewer when the launch would not give ~3 blocks per slot
+    const long long units_all = (long long)n_events * ((a.n_seeds + 32 * kMcSeeds - 1) / (32 * kMcSeeds));
+    int upc = (int)std::min<long long>(kMcUnits, units_all / (3LL * 148 * RETINA_MC_MINB));
+    upc = std::max(upc, kMcWarps);
+    const int blocks = (a.n_seeds + upc * 32 * kMcSeeds - 1) / (upc * 32 * kMcSeeds);
     for (int e0 = 0; e0 < n_events; e0 += 65535) {
         const int ne = std::min(65535, n_events - e0);
         seed_morton_sort_kernel<<<ne, 1024, sort_smem, stream>>>(a.seeds, a.n_seeds, np2, a.lo[0], a.hi[0], a.lo[1],
@@ -813,7 +865,7 @@ cudaError_t launch_multistart_culled(const MultistartArgs &a0, int n_events, int
         err = cudaGetLastError();
         if (err != cudaSuccess) return err;
         a.e_base = e0;
-        kern<<<dim3(blocks, ne), kMcThreads, smem, stream>>>(a, perm, pairs_evaluated);
+        kern<<<dim3(blocks, ne), kMcThreads, smem, stream>>>(a, perm, pairs_evaluated, upc);
         err = cudaGetLastError();
         if (err != cudaSuccess) return err;
     }
