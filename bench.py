@@ -89,6 +89,10 @@ def args_():
                     help="cpu_baseline sample: the SURVEY.md §8(d) declared subsample, or 1 event per phase (tests)")
     ap.add_argument("--no-graph", dest="graph", action="store_false",
                     help="skip the CUDA-graph replay measurement")
+    ap.add_argument("--ms-algo", default="dense", choices=["dense", "culled"],
+                    help="fixed-step multi-start kernel: dense (every pair, the metric's definition) or culled "
+                         "(SLOPE2: the same results bit for bit, evaluating only pairs whose weight can be "
+                         "non-zero; value then counts the pairs actually evaluated)")
     ap.add_argument("--update", default="gradient", choices=["gradient", "newton"],
                     help="multi-start update: BASELINE fixed-step ascent, or the paper's Truncated Newton")
     ap.add_argument("--dist-check", action="store_true",
@@ -389,13 +393,21 @@ def main():
         if cfg.model == C.LINE2D or not cfg.n_seeds:
             raise SystemExit(f"--update newton needs a SLOPE2/SLOPE3 config with seeds ({cfg.name} has none)")
         spec.newton = C.newton_schedule(cfg)
+    elif a.ms_algo == "culled":
+        if cfg.model != C.SLOPE2 or not cfg.n_seeds:
+            raise SystemExit(f"--ms-algo culled needs a SLOPE2 config with seeds ({cfg.name})")
+        spec.ms_algorithm = RT.MS_CULLED
     pipe = RetinaPipeline(spec, E, chunk_events=a.chunk_events, overlap_peaks=a.overlap_peaks,
                           grid_bytes_budget=a.grid_buffer_gb * 1e9)
     stream = torch.cuda.current_stream()
     dbatch = upload(batch.offsets, batch.hits, seeds)
-    if a.update == "newton":  # the pairs count comes from the kernel's per-seed evaluation counts
+    if a.update == "newton" or pipe.pairs_ev is not None:
+        # the pairs count comes from the kernel: per-seed evaluation counts (Newton) or the pairs
+        # the culled kernel evaluated (one counted run, outside the timed region)
+        pipe.count_pairs = pipe.pairs_ev is not None
         pipe.run(dbatch, stream=stream)
         torch.cuda.synchronize()
+        pipe.count_pairs = False
     pairs_grid, pairs_ms = pipe.pairs(dbatch)
     keep = 64
     hdr = D.header_words(rank, ev_ids.start, E, pairs_grid, pairs_ms)
@@ -590,11 +602,15 @@ def main():
         r.update({"launch_ms": avg_ms, "pairs_per_launch": per_launch, "pairs_per_s": pairs_s,
                   "share_of_step": phase_med[ph] / ms_step, "traffic": None,
                   "timing": f"median over {a.steps} steps of the phase's CUDA-event time per step"})
+        if ph == "multistart" and a.ms_algo == "culled" and a.update == "gradient":
+            r["kernel"] = "multistart_culled_kernel"
+            r["work_basis"] = ("pairs = (seed, hit) pairs the culled kernel evaluated (counted on the device); "
+                               "the skipped pairs have weight exactly +0")
         if ph == "multistart" and a.update == "newton":
             r["work_basis"] = ("pairs = sum over seeds of response evaluations (q Hessian-mode + line-search "
                                "trials + final; counted by the kernel, PAPER.md:200-201 cost unit) x event hits")
         tcfg = traffic.get(cfg.name, {}) if not a.dense else {}  # per config: the capture's workload
-        if ph in tcfg and not (ph == "multistart" and a.update == "newton"):
+        if ph in tcfg and not (ph == "multistart" and (a.update == "newton" or a.ms_algo == "culled")):
             r["traffic"] = tcfg[ph]["dram_bytes_per_event"] * E / n_launch
             r["traffic_unit"] = "bytes/launch (ncu dram read+write per event x events per launch)"
         roofs[ph] = r
@@ -608,6 +624,8 @@ def main():
                 + (f", {'x'.join(str(x[2]) for x in cfg.axes)} {C.MODEL_NAME[cfg.model].upper()} grid + "
                    f"{'x'.join(['3'] * cfg.P)} peaks (R0={cfg.peak_threshold}) + sub-cell estimates" if cfg.axes else "")
                 + ((", " + (f"{cfg.n_seeds} seeds x {cfg.n_iters} fixed-step iterations + merge"
+                            + (" (culled multi-start kernel: bit-identical results, pairs = pairs evaluated)"
+                               if a.ms_algo == "culled" else "")
                             if a.update == "gradient" else
                             f"{cfg.n_seeds} seeds x q=3 Truncated-Newton steps (sigma schedule) + merge"))
                    if cfg.n_seeds else ""))

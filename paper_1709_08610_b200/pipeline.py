@@ -39,6 +39,7 @@ class PathSpec:
     z_ref: float = 0.0
     sigma_ms: Optional[float] = None     # multi-start sigma (defaults to sigma)
     newton: Optional[tuple] = None       # (sigmas, etas, final_sigma, max_halvings): Newton update
+    ms_algorithm: int = 0                # R.MS_DENSE, or R.MS_CULLED (SLOPE2: same results, fewer pairs)
 
     @property
     def P(self) -> int:
@@ -100,6 +101,13 @@ class RetinaPipeline:
         self.resp = torch.empty((E, S), dtype=torch.float32, device=self.device)
         # Newton path: response evaluations per seed (the paper's cost unit), counted by the kernel
         self.evals = torch.empty((E, S), dtype=torch.int32, device=self.device) if spec.newton is not None else None
+        # culled fixed-step path: the per-event seed permutation (workspace) and the evaluated-pair count
+        self.ms_ws = self.pairs_ev = None
+        if spec.newton is None and spec.ms_algorithm == R.MS_CULLED and S:
+            nb = R.multistart_workspace_size(E, S, spec.ms_algorithm)
+            self.ms_ws = torch.empty((max(nb, 4) // 4,), dtype=torch.int32, device=self.device)
+            self.pairs_ev = torch.zeros((1,), dtype=torch.int64, device=self.device)
+        self.count_pairs = False  # run(): add the pairs the culled kernel evaluates to pairs_ev
         self.t_theta = torch.empty((E, spec.track_capacity, P), dtype=torch.float32, device=self.device)
         self.t_resp = torch.empty((E, spec.track_capacity), dtype=torch.float32, device=self.device)
         self.t_seed = torch.empty((E, spec.track_capacity), dtype=torch.int32, device=self.device)
@@ -118,6 +126,8 @@ class RetinaPipeline:
             E = batch.n_events
             ev = self.evals[:E].to(torch.float64).sum(dim=1).cpu().numpy()
             return grid, float((n * ev).sum())
+        if self.pairs_ev is not None:  # the pairs the culled kernel evaluated in the counted run
+            return grid, float(self.pairs_ev.item())
         ms = float(n.sum()) * self.spec.n_seeds * (self.spec.n_iters + 1)
         return grid, ms
 
@@ -180,7 +190,9 @@ class RetinaPipeline:
         else:  # BASELINE configs[2..4]: fixed-step gradient ascent
             R.retina_multistart_optimize(ev, sp.model, sp.sigma_ms or sp.sigma, batch.seeds, sp.n_iters, sp.step,
                                          sp.box_lo, sp.box_hi, want_grad=False,
-                                         out=(self.theta[:E], self.resp[:E], None), stream=stream)
+                                         out=(self.theta[:E], self.resp[:E], None), stream=stream,
+                                         algorithm=sp.ms_algorithm, workspace=self.ms_ws,
+                                         pairs_evaluated=self.pairs_ev if self.count_pairs else None)
         if timer is not None:
             timer.stop("multistart")
             timer.start("merge")

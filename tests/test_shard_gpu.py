@@ -14,11 +14,13 @@ from tests.pack_ref import pack_ref
 pytestmark = pytest.mark.gpu
 
 
-def _run(cfg, ids, chunk=4):
+def _run(cfg, ids, chunk=4, ms_algorithm=0):
     import bench
     b = G.make_batch(cfg, ids)
     sd = G.make_seeds(cfg, ids)
-    pipe = RetinaPipeline(bench.make_spec(cfg), len(ids), chunk_events=chunk)
+    spec = bench.make_spec(cfg)
+    spec.ms_algorithm = ms_algorithm
+    pipe = RetinaPipeline(spec, len(ids), chunk_events=chunk)
     pipe.run(upload(b.offsets, b.hits, sd))
     torch.cuda.synchronize()
     return pipe
@@ -47,6 +49,18 @@ def test_pipeline_results_independent_of_the_event_split(name, E, seeds, splits)
                 assert np.array_equal(a, b), (name, e)
         lo = hi
     assert sum(int(x[0][1]) for x in ref) >= 0
+
+
+@pytest.mark.parametrize("name,E,seeds", [("cfg3", 6, 8192), ("cfg2", 5, 4096)])
+def test_pipeline_culled_multistart_gives_the_dense_results(name, E, seeds):
+    """The whole pass with the culled multi-start kernel (RETINA_MS_CULLED) gives every per-event
+    output of the dense pass bit for bit: seeds' end points and responses, and therefore the tracks."""
+    cfg = C.CONFIGS[name].replace(n_seeds=seeds)
+    dense = _run(cfg, range(E))
+    culled = _run(cfg, range(E), ms_algorithm=1)
+    for e in range(E):
+        for a, b in zip(_event_outputs(dense, e), _event_outputs(culled, e)):
+            assert np.array_equal(a.view(np.uint8), b.view(np.uint8)), (name, e)
 
 
 def test_pack_kernel_matches_the_stated_layout():
