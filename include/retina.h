@@ -195,10 +195,10 @@ int retina_multistart_optimize(const retina_events *ev, int model, float sigma,
 /* retina_multistart_optimize with an explicit algorithm:
  *   RETINA_MS_DENSE   evaluates every (seed, hit) pair of every pass (what retina_multistart_optimize
  *                     does; workspace unused);
- *   RETINA_MS_CULLED  SLOPE2 only (RETINA_EUNSUPPORTED otherwise): the SAME results bit for bit,
+ *   RETINA_MS_CULLED  SLOPE2 / SLOPE3 (RETINA_EUNSUPPORTED for LINE2D): the SAME results bit for bit,
  *                     evaluating only the pairs that can contribute.  With ex2.approx.ftz a pair
  *                     whose exponent -K s^2 is below -126 adds exactly +0 to R and to the gradient
- *                     sums; the seeds of each event are ordered along a Morton curve of (tx, ty) so
+ *                     sums; the seeds of each event are ordered along a Morton curve of theta so
  *                     that every warp's 256 seeds cover a small box, and per pass each warp skips the
  *                     hits that a conservative bound puts beyond K s^2 > 128 for all of them, visiting
  *                     the others in hit order with K4's arithmetic.  Needs a DEVICE workspace of at

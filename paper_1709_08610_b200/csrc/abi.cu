@@ -335,12 +335,12 @@ int retina_multistart_optimize_ex(const retina_events *ev, int model, float sigm
     cudaError_t err;
     if (algorithm == RETINA_MS_CULLED) {
         if (!retina::multistart_culled_ok(model, n_seeds))
-            return fail(RETINA_EUNSUPPORTED, "RETINA_MS_CULLED: SLOPE2 with n_seeds <= 16384 only");
+            return fail(RETINA_EUNSUPPORTED, "RETINA_MS_CULLED: SLOPE2 / SLOPE3 with n_seeds <= 16384 only");
         const size_t need = retina_multistart_workspace_size(ev->n_events, n_seeds, algorithm);
         if (!workspace || workspace_bytes < need)
             return fail(RETINA_EINVAL, "workspace of %zu bytes needed (got %zu)", need, workspace_bytes);
-        err = retina::launch_multistart_culled(a, ev->n_events, static_cast<int32_t *>(workspace), pairs_evaluated,
-                                               (cudaStream_t)stream);
+        err = retina::launch_multistart_culled(model, a, ev->n_events, static_cast<int32_t *>(workspace),
+                                               pairs_evaluated, (cudaStream_t)stream);
     } else {
         err = retina::launch_multistart(model, a, ev->n_events, (cudaStream_t)stream);
         if (err == cudaSuccess && pairs_evaluated) {

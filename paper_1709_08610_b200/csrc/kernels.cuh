@@ -128,7 +128,7 @@ cudaError_t launch_multistart(int model, const MultistartArgs &a, int n_events, 
 // K4c (multistart.cu): the same results as K4 for SLOPE2, evaluating only the pairs that can contribute
 bool multistart_culled_ok(int model, int n_seeds);
 size_t multistart_culled_workspace_bytes(long long n_events, int n_seeds);
-cudaError_t launch_multistart_culled(const MultistartArgs &a, int n_events, int32_t *perm,
+cudaError_t launch_multistart_culled(int model, const MultistartArgs &a, int n_events, int32_t *perm,
                                      unsigned long long *pairs_evaluated, cudaStream_t stream);
 cudaError_t launch_find_peaks(const PeakArgs &a, int n_events, cudaStream_t stream);
 cudaError_t launch_find_peaks_ws(const PeakArgs &a, int n_events, int32_t *ws, cudaStream_t stream);

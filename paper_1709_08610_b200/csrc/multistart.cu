@@ -228,9 +228,12 @@ __device__ __forceinline__ PlaneTable build_planes(const float4 *h, int n, int *
     return PlaneTable{s_start, s_z, *s_np, nullptr};
 }
 
+// list != nullptr (K4c): only the resident hits list[0 .. L) are visited, in that (hit) order; a
+// new plane is found by comparing z, which runs the same operations as the plane table would.
 template <int MODEL, int S, bool ZREF, bool GRAD, bool WANT_R>
 __device__ __forceinline__ void ms_pass_x2(HitStage &st, const float (&th)[S][3], float negK, float zref,
-                                           float (&R)[S], float (&G)[S][4], float sk, const PlaneTable &pt) {
+                                           float (&R)[S], float (&G)[S][4], float sk, const PlaneTable &pt,
+                                           const uint16_t *list = nullptr, int L = 0) {
     static_assert(S % 2 == 0, "seed pairs");
     constexpr int NP = S / 2;
     float2 mtx[NP], mty[NP], r2[NP], qx[NP], qy[NP], gx[NP], gy[NP], ax[NP], ay[NP], dh[NP], dl[NP];
@@ -327,7 +330,15 @@ __device__ __forceinline__ void ms_pass_x2(HitStage &st, const float (&th)[S][3]
             }
         }
     };
-    if (pt.np >= 0 && pt.xy) {  // compact stage: (x, y) pairs, plane by plane
+    if (list != nullptr) {  // K4c: the warp's listed hits
+        const float4 *h = st.buf;
+#pragma unroll 2
+        for (int t = 0; t < L; ++t) {
+            const float4 hk = h[list[t]];
+            if (hk.z != zprev) plane(hk.z);  // warp-uniform: the list is the warp's
+            body(hk);
+        }
+    } else if (pt.np >= 0 && pt.xy) {  // compact stage: (x, y) pairs, plane by plane
         for (int pl = 0; pl < pt.np; ++pl) {
             const int k1 = pt.start[pl + 1];
             plane(pt.z[pl]);
@@ -542,23 +553,27 @@ cudaError_t launch_multistart(int model, const MultistartArgs &a, int n_events, 
 constexpr int kMcThreads = 128, kMcSeeds = 8, kMcWarps = kMcThreads / 32, kMcUnits = RETINA_MC_UNITS;
 
 // ---------------------------------------------------------------- K4c-sort: Morton order per event
-// perm[e][q] = caller index of the q-th seed of event e along a Morton curve of (tx, ty) quantised
-// to 16 bits per axis over the prior box.  Bitonic sort of (key << 32 | index) in shared memory.
-__global__ void __launch_bounds__(1024) seed_morton_sort_kernel(const float *seeds, int n_seeds, int np2,
-                                                                float lo0, float hi0, float lo1, float hi1,
-                                                                int32_t *perm, int e_base) {
+// perm[e][q] = caller index of the q-th seed of event e along a Morton curve of the seed's
+// parameters quantised over the prior box (P = 2: 16 bits per axis; P = 3: 10).  Bitonic sort of
+// (key << 32 | index) in shared memory.
+__global__ void __launch_bounds__(1024) seed_morton_sort_kernel(const float *seeds, int n_seeds, int np2, int P,
+                                                                float3 lo, float3 hi, int32_t *perm, int e_base) {
     extern __shared__ unsigned long long s_key[];
     const int e = e_base + blockIdx.x;
-    const float *sd = seeds + (int64_t)e * n_seeds * 2;
-    const float sx = 65535.f / fmaxf(hi0 - lo0, 1e-30f), sy = 65535.f / fmaxf(hi1 - lo1, 1e-30f);
+    const float *sd = seeds + (int64_t)e * n_seeds * P;
+    const int bits = (P == 3) ? 10 : 16;
+    const float qmax = (float)((1 << bits) - 1);
+    const float sc[3] = {qmax / fmaxf(hi.x - lo.x, 1e-30f), qmax / fmaxf(hi.y - lo.y, 1e-30f),
+                         qmax / fmaxf(hi.z - lo.z, 1e-30f)};
+    const float lo3[3] = {lo.x, lo.y, lo.z};
     for (int i = threadIdx.x; i < np2; i += blockDim.x) {
         unsigned long long k = ~0ull;
         if (i < n_seeds) {
-            const uint32_t qx = (uint32_t)fminf(fmaxf((sd[2 * i] - lo0) * sx, 0.f), 65535.f);
-            const uint32_t qy = (uint32_t)fminf(fmaxf((sd[2 * i + 1] - lo1) * sy, 0.f), 65535.f);
             uint32_t m = 0;
-#pragma unroll
-            for (int b = 0; b < 16; ++b) m |= (((qx >> b) & 1u) << (2 * b)) | (((qy >> b) & 1u) << (2 * b + 1));
+            for (int d = 0; d < P; ++d) {
+                const uint32_t q = (uint32_t)fminf(fmaxf((sd[(int64_t)P * i + d] - lo3[d]) * sc[d], 0.f), qmax);
+                for (int b = 0; b < bits; ++b) m |= ((q >> b) & 1u) << (P * b + d);
+            }
             k = ((unsigned long long)m << 32) | (uint32_t)i;
         }
         s_key[i] = k;
@@ -584,120 +599,72 @@ __global__ void __launch_bounds__(1024) seed_morton_sort_kernel(const float *see
 }
 
 // ---------------------------------------------------------------- K4c
-template <bool ZREF, bool GRAD, bool WANT_R>
-__device__ __forceinline__ void mc_pass(const float4 *h, const uint16_t *list, int L, const float (&th)[kMcSeeds][3],
-                                        float negK, float zref, float (&R)[kMcSeeds], float (&G)[kMcSeeds][2]) {
-    constexpr int NP = kMcSeeds / 2;
-    float2 mtx[NP], mty[NP], r2[NP], qx[NP], qy[NP], gx[NP], gy[NP];
-    const float2 zero = make_float2(0.f, 0.f), nk = make_float2(negK, negK);
-#pragma unroll
-    for (int p = 0; p < NP; ++p) {
-        mtx[p] = make_float2(-th[2 * p][0], -th[2 * p + 1][0]);
-        mty[p] = make_float2(-th[2 * p][1], -th[2 * p + 1][1]);
-        r2[p] = qx[p] = qy[p] = gx[p] = gy[p] = zero;
-    }
-    float zprev = __int_as_float(0x7fc00000);
-    float dprev = 0.f, dlprev = 0.f;
-    auto flush = [&]() {
-#pragma unroll
-        for (int p = 0; p < NP; ++p) {
-            const float2 d = make_float2(dprev, dprev);
-            gx[p] = __ffma2_rn(d, qx[p], gx[p]);
-            gy[p] = __ffma2_rn(d, qy[p], gy[p]);
-            qx[p] = qy[p] = zero;
-        }
-    };
-#pragma unroll 2
-    for (int t = 0; t < L; ++t) {
-        const float4 hk = h[list[t]];
-        if (hk.z != zprev) {  // warp-uniform: the list is the warp's
-            if (GRAD) flush();
-            zprev = hk.z;
-            if (ZREF)
-                two_sum(hk.z, -zref, dprev, dlprev);
-            else
-                dprev = hk.z;
-        }
-        const float2 X = make_float2(hk.x, hk.x), Y = make_float2(hk.y, hk.y);
-#pragma unroll
-        for (int p = 0; p < NP; ++p) {
-            float2 sx, sy;
-            if (ZREF) {
-                const float2 D = make_float2(dprev, dprev), DL = make_float2(dlprev, dlprev);
-                sx = __ffma2_rn(mtx[p], DL, __ffma2_rn(mtx[p], D, X));
-                sy = __ffma2_rn(mty[p], DL, __ffma2_rn(mty[p], D, Y));
-            } else {
-                const float2 Z = make_float2(hk.z, hk.z);
-                sx = __ffma2_rn(mtx[p], Z, X);
-                sy = __ffma2_rn(mty[p], Z, Y);
-            }
-            const float2 a = __fmul2_rn(__ffma2_rn(sx, sx, __fmul2_rn(sy, sy)), nk);
-            const float2 w = make_float2(ex2_approx(a.x), ex2_approx(a.y));
-            if (WANT_R) r2[p] = __fadd2_rn(r2[p], w);
-            if (GRAD) {
-                qx[p] = __ffma2_rn(w, sx, qx[p]);
-                qy[p] = __ffma2_rn(w, sy, qy[p]);
-            }
-        }
-    }
-    if (GRAD) flush();
-#pragma unroll
-    for (int p = 0; p < NP; ++p) {
-        R[2 * p] = r2[p].x;
-        R[2 * p + 1] = r2[p].y;
-        G[2 * p][0] = gx[p].x;
-        G[2 * p + 1][0] = gx[p].y;
-        G[2 * p][1] = gy[p].x;
-        G[2 * p + 1][1] = gy[p].y;
-    }
-}
-
 struct McBox {
-    float a0, b0, a1, b1;  // [a0, b0] x [a1, b1] in (tx, ty); a0 > b0: empty
+    float lo[3], hi[3];  // the seeds' parameter box; lo[0] > hi[0]: empty
 };
 
 // the box of the warp's valid seeds (warp-uniform)
-__device__ __forceinline__ McBox mc_warp_box(const float (&th)[kMcSeeds][3], const bool (&ok)[kMcSeeds]) {
-    McBox b{3.4e38f, -3.4e38f, 3.4e38f, -3.4e38f};
+template <int P, int S>
+__device__ __forceinline__ McBox mc_warp_box(const float (&th)[S][3], const bool (&ok)[S]) {
+    McBox b;
 #pragma unroll
-    for (int s = 0; s < kMcSeeds; ++s)
-        if (ok[s]) {
-            b.a0 = fminf(b.a0, th[s][0]);
-            b.b0 = fmaxf(b.b0, th[s][0]);
-            b.a1 = fminf(b.a1, th[s][1]);
-            b.b1 = fmaxf(b.b1, th[s][1]);
-        }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-        b.a0 = fminf(b.a0, __shfl_xor_sync(0xffffffffu, b.a0, o));
-        b.b0 = fmaxf(b.b0, __shfl_xor_sync(0xffffffffu, b.b0, o));
-        b.a1 = fminf(b.a1, __shfl_xor_sync(0xffffffffu, b.a1, o));
-        b.b1 = fmaxf(b.b1, __shfl_xor_sync(0xffffffffu, b.b1, o));
+    for (int i = 0; i < 3; ++i) {
+        b.lo[i] = 3.4e38f;
+        b.hi[i] = -3.4e38f;
     }
+#pragma unroll
+    for (int s = 0; s < S; ++s)
+        if (ok[s])
+#pragma unroll
+            for (int i = 0; i < P; ++i) {
+                b.lo[i] = fminf(b.lo[i], th[s][i]);
+                b.hi[i] = fmaxf(b.hi[i], th[s][i]);
+            }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+        for (int i = 0; i < P; ++i) {
+            b.lo[i] = fminf(b.lo[i], __shfl_xor_sync(0xffffffffu, b.lo[i], o));
+            b.hi[i] = fmaxf(b.hi[i], __shfl_xor_sync(0xffffffffu, b.hi[i], o));
+        }
     return b;
 }
 
-// The warp's list of hits within reach of the box B: hit k is kept unless, for every (tx, ty) in
-// B, K ((x - tx d)^2 + (y - ty d)^2) > 128 (then every seed inside B has an ex2 argument < -126,
-// with room for fp32 rounding: w = +0 exactly).  In hit order; returns the length.
-template <bool ZREF>
+// least |x - t d| over t in [t0, t1] and d in [d0, d1] (0 when the range of t d contains x)
+__device__ __forceinline__ float mc_min_abs(float x, float t0, float t1, float d0, float d1) {
+    const float p00 = t0 * d0, p01 = t0 * d1, p10 = t1 * d0, p11 = t1 * d1;
+    const float pmin = fminf(fminf(p00, p01), fminf(p10, p11)), pmax = fmaxf(fmaxf(p00, p01), fmaxf(p10, p11));
+    // rounded products: widen the range by 1e-6 of its magnitude so it holds every exact t d
+    const float slack = 1e-6f * fmaxf(fabsf(pmin), fabsf(pmax));
+    const float lo = x - (pmax + slack), hi = x - (pmin - slack);  // s ranges over [lo, hi]
+    return (lo > 0.f) ? lo : (hi < 0.f ? -hi : 0.f);
+}
+
+// The warp's list of hits within reach of the box B: hit k is kept unless, for every parameter
+// tuple in B, K ((x - tx d)^2 + (y - ty d)^2) > 128 (then every seed inside B has an ex2 argument
+// < -126, with room for fp32 rounding: w = +0 exactly); d = z - z_ref (SLOPE2) or z - z0 over the
+// box's z0 range (SLOPE3).  In hit order; returns the length.
+template <int MODEL, bool ZREF>
 __device__ __forceinline__ int mc_build_list(const float4 *h, int n, const McBox &B, float K, float zref,
                                              uint16_t *list) {
     const int lane = threadIdx.x & 31;
-    if (B.a0 > B.b0) return 0;  // no valid seed in this warp
+    if (B.lo[0] > B.hi[0]) return 0;  // no valid seed in this warp
     int L = 0;
     for (int k0 = 0; k0 < n; k0 += 32) {
         const int k = k0 + lane;
         bool keep = false;
         if (k < n) {
             const float4 hk = h[k];
-            const float d = ZREF ? __fsub_rn(hk.z, zref) : hk.z;
-            // s_x over tx in [a0, b0] is monotone: its least |value| is 0 if the ends differ in sign
-            const float ex1 = __fmaf_rn(-B.a0, d, hk.x), ex2 = __fmaf_rn(-B.b0, d, hk.x);
-            const float ey1 = __fmaf_rn(-B.a1, d, hk.y), ey2 = __fmaf_rn(-B.b1, d, hk.y);
-            const float mx = (ex1 > 0.f) == (ex2 > 0.f) && ex1 != 0.f ? fminf(fabsf(ex1), fabsf(ex2)) : 0.f;
-            const float my = (ey1 > 0.f) == (ey2 > 0.f) && ey1 != 0.f ? fminf(fabsf(ey1), fabsf(ey2)) : 0.f;
-            // shrink by 1e-5 relative (the fp32 rounding of the ends) before the comparison
+            float d0, d1;  // the range of d, rounded outwards
+            if (MODEL == kSlope3) {
+                d0 = __fsub_rd(hk.z, B.hi[2]);
+                d1 = __fsub_ru(hk.z, B.lo[2]);
+            } else {
+                d0 = ZREF ? __fsub_rd(hk.z, zref) : hk.z;
+                d1 = ZREF ? __fsub_ru(hk.z, zref) : hk.z;
+            }
+            const float mx = mc_min_abs(hk.x, B.lo[0], B.hi[0], d0, d1);
+            const float my = mc_min_abs(hk.y, B.lo[1], B.hi[1], d0, d1);
             keep = K * __fmaf_rn(mx, mx, my * my) * 0.99999f <= 128.f;
         }
         const unsigned b = __ballot_sync(0xffffffffu, keep);
@@ -708,16 +675,18 @@ __device__ __forceinline__ int mc_build_list(const float4 *h, int n, const McBox
     return L;
 }
 
-template <bool ZREF>
-__global__ void __launch_bounds__(kMcThreads, RETINA_MC_MINB) multistart_culled_kernel(MultistartArgs a, const int32_t *perm,
-                                                                         unsigned long long *pairs_evaluated,
-                                                                         int units_per_cta) {
+template <int MODEL, int S, bool ZREF>
+__global__ void __launch_bounds__(kMcThreads, RETINA_MC_MINB)
+    multistart_culled_kernel(MultistartArgs a, const int32_t *perm, unsigned long long *pairs_evaluated,
+                             int units_per_cta) {
+    constexpr int P = (MODEL == kSlope3) ? 3 : 2;
+    constexpr int USEEDS = 32 * S;  // seeds per unit (one warp's)
     extern __shared__ __align__(16) float4 s_hits[];  // [cap] hits, then [warps][cap] uint16 lists
     __shared__ __align__(8) uint64_t s_bar[2];
+    __shared__ int s_next;
     const int e = a.e_base + blockIdx.y;
     const int start = a.offsets[e], nh = a.offsets[e + 1] - start;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    __shared__ int s_next;
     if (threadIdx.x == 0) s_next = 0;
     HitStage st;
     st.init(s_hits, s_bar, a.hits + start, nh, a.cap);  // (its block barrier also publishes s_next)
@@ -725,13 +694,14 @@ __global__ void __launch_bounds__(kMcThreads, RETINA_MC_MINB) multistart_culled_
     const bool culled = nh <= a.cap && nh <= 65535 && (nh == 0 || st.load_resident());
     uint16_t *list = reinterpret_cast<uint16_t *>(s_hits + a.cap) + warp * a.cap;
     const float K = -a.negK;
+    const PlaneTable no_table{nullptr, nullptr, -1, nullptr};
 
-    // Units of 256 seeds are dealt to the warps: dynamically (a shared counter) when the event is
+    // Units of USEEDS seeds are dealt to the warps: dynamically (a shared counter) when the event is
     // resident -- the warps' lists differ in length, so a fixed share would leave warps idle -- and
     // round-robin in lockstep otherwise (the streamed dense passes synchronise the block).
     const int32_t *pe = perm + (int64_t)e * a.n_seeds;
-    const int cta_seed0 = blockIdx.x * units_per_cta * 32 * kMcSeeds;
-    const int units = min(units_per_cta, (a.n_seeds - cta_seed0 + 32 * kMcSeeds - 1) / (32 * kMcSeeds));
+    const int cta_seed0 = blockIdx.x * units_per_cta * USEEDS;
+    const int units = min(units_per_cta, (a.n_seeds - cta_seed0 + USEEDS - 1) / USEEDS);
     unsigned long long evaluated = 0;
     for (int k = 0;; ++k) {
         int u;
@@ -743,85 +713,82 @@ __global__ void __launch_bounds__(kMcThreads, RETINA_MC_MINB) multistart_culled_
             u = warp + kMcWarps * k;
             if (k >= (units + kMcWarps - 1) / kMcWarps) break;
         }
-        // a unit = 256 consecutive seeds of the Morton order (8 per lane, 32 consecutive per s)
-        const int q0 = cta_seed0 + u * 32 * kMcSeeds + lane;
-        bool ok[kMcSeeds];
-        float th[kMcSeeds][3];
+        // a unit = USEEDS consecutive seeds of the Morton order (S per lane, 32 consecutive per s)
+        const int q0 = cta_seed0 + u * USEEDS + lane;
+        bool ok[S];
+        float th[S][3];
 #pragma unroll
-        for (int s = 0; s < kMcSeeds; ++s) {
+        for (int s = 0; s < S; ++s) {
             const int q = q0 + s * 32;
             ok[s] = q < a.n_seeds;
-            const int64_t src = ((int64_t)e * a.n_seeds + __ldg(pe + min(q, a.n_seeds - 1))) * 2;
-            th[s][0] = __ldg(a.seeds + src);
-            th[s][1] = __ldg(a.seeds + src + 1);
-            th[s][2] = 0.f;
+            const int64_t src = ((int64_t)e * a.n_seeds + __ldg(pe + min(q, a.n_seeds - 1))) * P;
+#pragma unroll
+            for (int i = 0; i < 3; ++i) th[s][i] = (i < P) ? __ldg(a.seeds + src + i) : 0.f;
         }
         int nvalid = 0;
 #pragma unroll
-        for (int s = 0; s < kMcSeeds; ++s) nvalid += ok[s] ? 1 : 0;
+        for (int s = 0; s < S; ++s) nvalid += ok[s] ? 1 : 0;
         nvalid = __reduce_add_sync(0xffffffffu, nvalid);
         // The list is built for the seeds' box grown by a margin and rebuilt only when a seed leaves
         // that box (a list built for a box covers every seed inside it, so reuse stays exact); fixed-
         // step seeds move little per iteration.
-        McBox lb{1.f, 0.f, 1.f, 0.f};  // empty: build on the first pass
+        McBox lb;
+        lb.lo[0] = 1.f;
+        lb.hi[0] = 0.f;  // empty: build on the first pass
         int L = 0;
 
-        float R[kMcSeeds], G[kMcSeeds][2], g[kMcSeeds][2];
-        const PlaneTable no_table{nullptr, nullptr, -1, nullptr};
+        float R[S], G[S][4], g[S][3];
         auto pass = [&](auto grad_tag, auto want_r_tag) {  // one pass over the hits in reach, or all of them
             constexpr bool GR = decltype(grad_tag)::value, WR = decltype(want_r_tag)::value;
             if (culled) {
-                const McBox B = mc_warp_box(th, ok);
-                if (!(B.a0 >= lb.a0 && B.b0 <= lb.b0 && B.a1 >= lb.a1 && B.b1 <= lb.b1) || lb.a0 > lb.b0) {
-                    const float m0 = fmaxf(RETINA_MC_MARGIN_ABS, RETINA_MC_MARGIN * (B.b0 - B.a0));
-                    const float m1 = fmaxf(RETINA_MC_MARGIN_ABS, RETINA_MC_MARGIN * (B.b1 - B.a1));
-                    lb = (B.a0 > B.b0) ? B : McBox{B.a0 - m0, B.b0 + m0, B.a1 - m1, B.b1 + m1};
-                    L = mc_build_list<ZREF>(st.buf, nh, lb, K, a.z_ref, list);
+                const McBox B = mc_warp_box<P, S>(th, ok);
+                bool inside = lb.lo[0] <= lb.hi[0];
+#pragma unroll
+                for (int i = 0; i < P; ++i) inside = inside && B.lo[i] >= lb.lo[i] && B.hi[i] <= lb.hi[i];
+                if (!inside) {
+                    lb = B;
+                    if (B.lo[0] <= B.hi[0])
+#pragma unroll
+                        for (int i = 0; i < P; ++i) {
+                            const float m = fmaxf(RETINA_MC_MARGIN_ABS * (i == 2 ? 1e4f : 1.f),
+                                                  RETINA_MC_MARGIN * (B.hi[i] - B.lo[i]));
+                            lb.lo[i] = B.lo[i] - m;
+                            lb.hi[i] = B.hi[i] + m;
+                        }
+                    L = mc_build_list<MODEL, ZREF>(st.buf, nh, lb, K, a.z_ref, list);
                 }
                 evaluated += (unsigned long long)L * nvalid;
-                mc_pass<ZREF, GR, WR>(st.buf, list, L, th, a.negK, a.z_ref, R, G);
+                ms_pass_x2<MODEL, S, ZREF, GR, WR>(st, th, a.negK, a.z_ref, R, G, a.sk, no_table, list, L);
             } else {
-                float G4[kMcSeeds][4];
-                ms_eval<kSlope2, kMcSeeds, ZREF, GR, WR>(st, th, a.negK, a.z_ref, R, G4, a.sk, no_table);
-#pragma unroll
-                for (int s = 0; s < kMcSeeds; ++s) {
-                    G[s][0] = G4[s][0];
-                    G[s][1] = G4[s][1];
-                }
+                ms_eval<MODEL, S, ZREF, GR, WR>(st, th, a.negK, a.z_ref, R, G, a.sk, no_table);
                 evaluated += (unsigned long long)nh * nvalid;
             }
         };
+        const float cg = (MODEL == kSlope3) ? a.c2s : a.c2;
         for (int it = 0; it < a.n_iters; ++it) {
             pass(std::true_type{}, std::false_type{});
+            ms_gradient<MODEL, S>(th, G, cg, g);
 #pragma unroll
-            for (int s = 0; s < kMcSeeds; ++s) {
-                g[s][0] = __fmul_rn(a.c2, G[s][0]);
-                g[s][1] = __fmul_rn(a.c2, G[s][1]);
+            for (int s = 0; s < S; ++s)
 #pragma unroll
-                for (int i = 0; i < 2; ++i)
+                for (int i = 0; i < P; ++i)
                     th[s][i] = fminf(fmaxf(__fmaf_rn(a.step, g[s][i], th[s][i]), a.lo[i]), a.hi[i]);
-            }
         }
         if (a.grad_out) {
             pass(std::true_type{}, std::true_type{});
-#pragma unroll
-            for (int s = 0; s < kMcSeeds; ++s) {
-                g[s][0] = __fmul_rn(a.c2, G[s][0]);
-                g[s][1] = __fmul_rn(a.c2, G[s][1]);
-            }
+            ms_gradient<MODEL, S>(th, G, cg, g);
         } else {
             pass(std::false_type{}, std::true_type{});
         }
 #pragma unroll
-        for (int s = 0; s < kMcSeeds; ++s) {
+        for (int s = 0; s < S; ++s) {
             if (!ok[s]) continue;
             const int64_t o = (int64_t)e * a.n_seeds + __ldg(pe + q0 + s * 32);
             a.R_out[o] = R[s];
-            a.theta_out[o * 2] = th[s][0];
-            a.theta_out[o * 2 + 1] = th[s][1];
-            if (a.grad_out) {
-                a.grad_out[o * 2] = g[s][0];
-                a.grad_out[o * 2 + 1] = g[s][1];
+#pragma unroll
+            for (int i = 0; i < P; ++i) {
+                a.theta_out[o * P + i] = th[s][i];
+                if (a.grad_out) a.grad_out[o * P + i] = g[s][i];
             }
         }
     }
@@ -833,15 +800,16 @@ size_t multistart_culled_workspace_bytes(long long n_events, int n_seeds) {
 }
 
 bool multistart_culled_ok(int model, int n_seeds) {
-    // SLOPE2; the sort holds an event's seeds in shared memory
+    // SLOPE2 / SLOPE3; the sort holds an event's seeds in shared memory
     int np2 = 1;
     while (np2 < n_seeds) np2 <<= 1;
-    return model == kSlope2 && n_seeds > 0 && np2 <= 16384;  // 128 KB of (key, index) words
+    return (model == kSlope2 || model == kSlope3) && n_seeds > 0 && np2 <= 16384;  // 128 KB of (key, index)
 }
 
-cudaError_t launch_multistart_culled(const MultistartArgs &a0, int n_events, int32_t *perm,
-                                     unsigned long long *pairs_evaluated, cudaStream_t stream) {
-    if (n_events == 0 || a0.n_seeds == 0) return cudaSuccess;
+template <int MODEL, int S, bool ZREF>
+static cudaError_t launch_mc(const MultistartArgs &a0, int n_events, int32_t *perm, unsigned long long *pairs_evaluated,
+                             cudaStream_t stream) {
+    constexpr int P = (MODEL == kSlope3) ? 3 : 2;
     int np2 = 1;
     while (np2 < a0.n_seeds) np2 <<= 1;
     const size_t sort_smem = (size_t)np2 * sizeof(unsigned long long);
@@ -850,18 +818,19 @@ cudaError_t launch_multistart_culled(const MultistartArgs &a0, int n_events, int
     MultistartArgs a = a0;
     a.cap = ((std::max(a0.cap, 2) + 7) / 8) * 8;  // resident stage (events beyond it run dense)
     const size_t smem = (size_t)a.cap * (sizeof(float4) + kMcWarps * sizeof(uint16_t));
-    auto kern = (a.z_ref == 0.f) ? multistart_culled_kernel<false> : multistart_culled_kernel<true>;
+    auto kern = multistart_culled_kernel<MODEL, S, ZREF>;
     err = ensure_dynamic_smem(kern, smem);
     if (err != cudaSuccess) return err;
     // units per block: up to kMcUnits, fewer when the launch would not give ~3 blocks per slot
-    const long long units_all = (long long)n_events * ((a.n_seeds + 32 * kMcSeeds - 1) / (32 * kMcSeeds));
+    constexpr int useeds = 32 * S;
+    const long long units_all = (long long)n_events * ((a.n_seeds + useeds - 1) / useeds);
     int upc = (int)std::min<long long>(kMcUnits, units_all / (3LL * 148 * RETINA_MC_MINB));
     upc = std::max(upc, kMcWarps);
-    const int blocks = (a.n_seeds + upc * 32 * kMcSeeds - 1) / (upc * 32 * kMcSeeds);
+    const int blocks = (a.n_seeds + upc * useeds - 1) / (upc * useeds);
+    const float3 lo = make_float3(a.lo[0], a.lo[1], a.lo[2]), hi = make_float3(a.hi[0], a.hi[1], a.hi[2]);
     for (int e0 = 0; e0 < n_events; e0 += 65535) {
         const int ne = std::min(65535, n_events - e0);
-        seed_morton_sort_kernel<<<ne, 1024, sort_smem, stream>>>(a.seeds, a.n_seeds, np2, a.lo[0], a.hi[0], a.lo[1],
-                                                                 a.hi[1], perm, e0);
+        seed_morton_sort_kernel<<<ne, 1024, sort_smem, stream>>>(a.seeds, a.n_seeds, np2, P, lo, hi, perm, e0);
         err = cudaGetLastError();
         if (err != cudaSuccess) return err;
         a.e_base = e0;
@@ -870,6 +839,15 @@ cudaError_t launch_multistart_culled(const MultistartArgs &a0, int n_events, int
         if (err != cudaSuccess) return err;
     }
     return cudaSuccess;
+}
+
+cudaError_t launch_multistart_culled(int model, const MultistartArgs &a, int n_events, int32_t *perm,
+                                     unsigned long long *pairs_evaluated, cudaStream_t stream) {
+    if (n_events == 0 || a.n_seeds == 0) return cudaSuccess;
+    if (model == kSlope3) return launch_mc<kSlope3, RETINA_MS3_SEEDS, false>(a, n_events, perm, pairs_evaluated, stream);
+    if (model != kSlope2) return cudaErrorInvalidValue;
+    return (a.z_ref == 0.f) ? launch_mc<kSlope2, kMcSeeds, false>(a, n_events, perm, pairs_evaluated, stream)
+                            : launch_mc<kSlope2, kMcSeeds, true>(a, n_events, perm, pairs_evaluated, stream);
 }
 
 }  // namespace retina

@@ -395,7 +395,8 @@ def test_T7_merge_synthetic_ties_and_capacity():
 @pytest.mark.parametrize("name,n_ev,n_seeds,n_iters,z_ref,want_grad,hint", [
     ("cfg2", 4, 4096, 50, 0.0, True, None), ("cfg2", 3, 1000, 20, 23.5, True, None),
     ("cfg3", 2, 8192, 50, 0.0, False, None),  # the bench launch configuration
-    ("cfg3", 2, 8192, 0, 0.0, True, None), ("cfg2", 3, 777, 7, 0.0, True, 64)])  # hint 64: events run dense
+    ("cfg3", 2, 8192, 0, 0.0, True, None), ("cfg2", 3, 777, 7, 0.0, True, 64),  # hint 64: events run dense
+    ("cfg4", 1, 16384, 50, 0.0, False, None), ("cfg4", 2, 2000, 10, 0.0, True, None)])  # SLOPE3
 def test_multistart_culled_bitwise_equal_to_dense(name, n_ev, n_seeds, n_iters, z_ref, want_grad, hint):
     """RETINA_MS_CULLED skips only pairs whose ex2.approx.ftz weight is exactly +0 and visits the
     others in hit order with K4's arithmetic: theta, R and grad R equal the dense kernel's bit for
@@ -437,12 +438,12 @@ def test_multistart_culled_bitwise_equal_to_dense(name, n_ev, n_seeds, n_iters, 
 
 
 def test_multistart_culled_unsupported_and_workspace():
-    cfg = C.CFG4
+    cfg = C.CFG0
     b = G.make_batch(cfg, [0])
     ev = events_of(b)
     seeds = dev(G.make_seeds(cfg, [0], n_seeds=64))
-    with pytest.raises(R.retina.RetinaError):  # SLOPE3
-        R.retina_multistart_optimize(ev, cfg.model, cfg.sigma, seeds, 1, cfg.step, cfg.box_lo, cfg.box_hi,
+    with pytest.raises(R.retina.RetinaError):  # LINE2D
+        R.retina_multistart_optimize(ev, cfg.model, cfg.sigma, seeds, 1, 1e-8, (-0.5, -1.0), (0.5, 1.0),
                                      algorithm=R.retina.MS_CULLED)
     c2 = C.CFG2
     b2 = G.make_batch(c2, [0])
