@@ -91,7 +91,7 @@ def args_():
                     help="skip the CUDA-graph replay measurement")
     ap.add_argument("--ms-algo", default="dense", choices=["dense", "culled"],
                     help="fixed-step multi-start kernel: dense (every pair, the metric's definition) or culled "
-                         "(SLOPE2: the same results bit for bit, evaluating only pairs whose weight can be "
+                         "(SLOPE2/SLOPE3: the same results bit for bit, evaluating only pairs whose weight can be "
                          "non-zero; value then counts the pairs actually evaluated)")
     ap.add_argument("--update", default="gradient", choices=["gradient", "newton"],
                     help="multi-start update: BASELINE fixed-step ascent, or the paper's Truncated Newton")
@@ -394,8 +394,8 @@ def main():
             raise SystemExit(f"--update newton needs a SLOPE2/SLOPE3 config with seeds ({cfg.name} has none)")
         spec.newton = C.newton_schedule(cfg)
     elif a.ms_algo == "culled":
-        if cfg.model != C.SLOPE2 or not cfg.n_seeds:
-            raise SystemExit(f"--ms-algo culled needs a SLOPE2 config with seeds ({cfg.name})")
+        if cfg.model not in (C.SLOPE2, C.SLOPE3) or not cfg.n_seeds:
+            raise SystemExit(f"--ms-algo culled needs a SLOPE2/SLOPE3 config with seeds ({cfg.name})")
         spec.ms_algorithm = RT.MS_CULLED
     pipe = RetinaPipeline(spec, E, chunk_events=a.chunk_events, overlap_peaks=a.overlap_peaks,
                           grid_bytes_budget=a.grid_buffer_gb * 1e9)
