@@ -123,9 +123,17 @@ int retina_grid_response(const retina_events *ev, int model, float sigma,
  *                          accumulators (a three-part split gives one accumulator per tile);
  *   RETINA_GRID_TENSOR_F16_PAIR    the same split by one CTA pair per 256 x 256 tile (two accumulators:
  *                          hi.hi and hi.lo + lo.hi), non-persistent;
- *   RETINA_GRID_TENSOR_F16_SINGLE  the same by one CTA per 128 x 256 tile (no cluster). */
+ *   RETINA_GRID_TENSOR_F16_SINGLE  the same by one CTA per 128 x 256 tile (no cluster);
+ *   RETINA_GRID_TENSOR_F16_CULLED  RETINA_GRID_TENSOR_F16 where every 256 x 256 tile contracts only the hits
+ *                          that can reach it: a conservative bound keeps a hit unless K s^2 > 128 for every
+ *                          (tx, ty) of the tile, i.e. unless each of its products e_x e_y is below 2^-128 --
+ *                          below fp32's normal range -- for every cell; the grid stays within the T1
+ *                          tolerance of the dense one, not bit-identical (the tensor-core sums group the
+ *                          remaining hits differently).  Row pitches that are not a multiple of 16 bytes run
+ *                          the dense kernel. */
 enum { RETINA_GRID_AUTO = 0, RETINA_GRID_DIRECT = 1, RETINA_GRID_SEPARABLE = 2, RETINA_GRID_TENSOR = 3,
-       RETINA_GRID_TENSOR_F16 = 4, RETINA_GRID_TENSOR_F16_PAIR = 5, RETINA_GRID_TENSOR_F16_SINGLE = 6 };
+       RETINA_GRID_TENSOR_F16 = 4, RETINA_GRID_TENSOR_F16_PAIR = 5, RETINA_GRID_TENSOR_F16_SINGLE = 6,
+       RETINA_GRID_TENSOR_F16_CULLED = 7 };
 int retina_grid_response_ex(const retina_events *ev, int model, float sigma,
                             const int32_t *axis_len, const float *const *axis_nodes,
                             float *response, int algorithm, void *stream);

@@ -102,7 +102,7 @@ int retina_grid_response_ex(const retina_events *ev, int model, float sigma, con
     }
     if (cells > 0x7fffffffLL) return fail(RETINA_EUNSUPPORTED, "more than 2^31-1 cells per event");
     if (ev->n_events > 0 && !response) return fail(RETINA_EINVAL, "response is NULL");
-    if (algorithm < RETINA_GRID_AUTO || algorithm > RETINA_GRID_TENSOR_F16_SINGLE)
+    if (algorithm < RETINA_GRID_AUTO || algorithm > RETINA_GRID_TENSOR_F16_CULLED)
         return fail(RETINA_EINVAL, "unknown grid algorithm %d", algorithm);
     if (algorithm == RETINA_GRID_SEPARABLE && model == RETINA_LINE2D)
         return fail(RETINA_EUNSUPPORTED, "LINE2D residual does not factorise: no separable grid");
@@ -127,8 +127,9 @@ int retina_grid_response_ex(const retina_events *ev, int model, float sigma, con
     cudaError_t err;
     if (algorithm == RETINA_GRID_TENSOR)
         err = retina::launch_grid_tensor(model, a, ev->n_events, (cudaStream_t)stream);
-    else if (algorithm == RETINA_GRID_TENSOR_F16)
-        err = retina::launch_grid_tensor16p(model, a, ev->n_events, (cudaStream_t)stream);
+    else if (algorithm == RETINA_GRID_TENSOR_F16 || algorithm == RETINA_GRID_TENSOR_F16_CULLED)
+        err = retina::launch_grid_tensor16p(model, a, ev->n_events, (cudaStream_t)stream,
+                                            algorithm == RETINA_GRID_TENSOR_F16_CULLED);
     else if (algorithm == RETINA_GRID_TENSOR_F16_PAIR)
         err = retina::launch_grid_tensor16x2(model, a, ev->n_events, (cudaStream_t)stream);
     else if (algorithm == RETINA_GRID_TENSOR_F16_SINGLE)

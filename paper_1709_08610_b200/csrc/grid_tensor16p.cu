@@ -86,7 +86,22 @@ __device__ __forceinline__ void gen_bar_sync() {  // the 16 generating warps onl
 constexpr int PP_EPI_BOX = 32 * 16 * 4;
 constexpr int PP_EPI_BYTES = 4 * 2 * PP_EPI_BOX;
 
-template <int MODEL, bool ZREF, bool TMA_EPI>
+// least |x - t d| over t in [t0, t1] and d in [d0, d1] (0 when the range of t d contains x); the
+// products' range is widened by 1e-6 of its magnitude so it holds every exact t d
+__device__ __forceinline__ float pp_min_abs(float x, float t0, float t1, float d0, float d1) {
+    const float p00 = t0 * d0, p01 = t0 * d1, p10 = t1 * d0, p11 = t1 * d1;
+    const float pmin = fminf(fminf(p00, p01), fminf(p10, p11)), pmax = fmaxf(fmaxf(p00, p01), fmaxf(p10, p11));
+    const float slack = 1e-6f * fmaxf(fabsf(pmin), fabsf(pmax));
+    const float lo = x - (pmax + slack), hi = x - (pmin - slack);
+    return (lo > 0.f) ? lo : (hi < 0.f ? -hi : 0.f);
+}
+
+// CULL (RETINA_GRID_TENSOR_F16_CULLED): per pair tile, the hit window holds only the hits that can
+// reach the tile -- a conservative bound puts K s^2 <= 128 for some (tx, ty) of the tile, i.e. a
+// product e_x e_y >= 2^-128 -- in hit order; every other hit's contribution to every cell of the
+// tile is below 2^-128 (fp32's normal range ends at 2^-126).  Windows are then per tile, and each
+// chunk carries a "last of its tile" flag for the MMA warp and the relay.
+template <int MODEL, bool ZREF, bool TMA_EPI, bool CULL = false>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(32 * PP_WARPS)
     grid_tensor16pp_kernel(GridArgs a, int n_items, const __grid_constant__ CUtensorMap out_map) {
     extern __shared__ __align__(1024) uint8_t s_raw[];
@@ -96,6 +111,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(32 * PP_WARPS)
     __shared__ __align__(8) uint64_t s_acc_full[2];     // both CTAs: multicast commit at tile end
     __shared__ __align__(8) uint64_t s_acc_empty[2];    // even CTA: 2 x 4 epilogue warps arrive
     __shared__ uint32_t s_tmem;
+    __shared__ int s_last[PP_NS];                        // CULL: stage holds its tile's last chunk
+    __shared__ int s_wcnt[PP_GEN_WARPS];                 // CULL: kept hits per generating warp, per round
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const uint32_t rank = cluster_rank();
@@ -161,9 +178,74 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(32 * PP_WARPS)
                 p[PP_NA + u] =
                     __ldg(a.nodes1 + min(c.t_n * TC_N + (int)rank * 128 + lane + 32 * (u * PP_NR + rset), a.n1 - 1));
             const float zref = (MODEL == kSlope3) ? __ldg(a.nodes2 + c.l) : a.z_ref;
-            for (int w0 = 0; w0 < n; w0 += a.cap) {
-                const int wlen = min(a.cap, n - w0);
-                if (have_e != c.e || have_w0 != w0 || (MODEL == kSlope3 && have_l != c.l)) {
+            // CULL: the pair tile's parameter box (both CTAs: the same box, so the same lists)
+            float txl = 0.f, txh = 0.f, tyl = 0.f, tyh = 0.f;
+            if (CULL) {
+                const int i0 = (c.t_m & ~1) * 128, j0 = c.t_n * TC_N;
+                const float u0 = __ldg(a.nodes0 + i0), u1 = __ldg(a.nodes0 + min(i0 + 255, a.n0 - 1));
+                const float v0 = __ldg(a.nodes1 + j0), v1 = __ldg(a.nodes1 + min(j0 + TC_N - 1, a.n1 - 1));
+                txl = fminf(u0, u1);
+                txh = fmaxf(u0, u1);
+                tyl = fminf(v0, v1);
+                tyh = fmaxf(v0, v1);
+            }
+            const float K = -a.negK;
+            int r0 = 0;  // CULL: next raw hit of the event to scan
+            for (int w0 = 0; CULL ? (r0 < n) : (w0 < n); w0 += a.cap) {
+                int wlen = min(a.cap, n - w0);
+                if (CULL) {
+                    // scan rounds of 512 raw hits, keeping (in hit order) those within reach of the
+                    // tile, until the window would overflow or the event is done
+                    int L = 0;
+                    while (r0 < n) {
+                        const int k = r0 + gtid;
+                        float4 hk = make_float4(0.f, 0.f, 0.f, 0.f);
+                        bool keep = false;
+                        if (k < n) {
+                            hk = __ldg(a.hits + start + k);
+                            const float d0 = (EXACT_D) ? __fsub_rd(hk.z, zref) : hk.z;
+                            const float d1 = (EXACT_D) ? __fsub_ru(hk.z, zref) : hk.z;
+                            const float mx = pp_min_abs(hk.x, txl, txh, d0, d1);
+                            const float my = pp_min_abs(hk.y, tyl, tyh, d0, d1);
+                            keep = K * __fmaf_rn(mx, mx, my * my) * 0.99999f <= 128.f;
+                        }
+                        const unsigned bal = __ballot_sync(0xffffffffu, keep);
+                        gen_bar_sync();  // the previous round's counts are read
+                        if (lane == 0) s_wcnt[warp] = __popc(bal);
+                        gen_bar_sync();
+                        int off = 0, tot = 0;
+#pragma unroll
+                        for (int w = 0; w < PP_GEN_WARPS; ++w) {
+                            const int cw = s_wcnt[w];
+                            off += (w < warp) ? cw : 0;
+                            tot += cw;
+                        }
+                        if (L + tot > a.cap) break;  // the round goes to the next window
+                        if (keep) {
+                            const int o = L + off + __popc(bal & ((1u << lane) - 1u));
+                            float zh = hk.z, zl = 0.f;
+                            if (EXACT_D) two_sum(hk.z, -zref, zh, zl);
+                            s_hx[o] = hk.x;
+                            s_hy[o] = hk.y;
+                            s_hz[o] = zh;
+                            if (EXACT_D) s_hzl[o] = zl;
+                        }
+                        L += tot;
+                        r0 += 32 * PP_GEN_WARPS;
+                    }
+                    // pad to whole chunks (at least one: an item whose window is empty still runs one
+                    // chunk of far-away hits, so the MMA warp writes its accumulator with zeros)
+                    const int Lpad = max(PP_KC, (L + PP_KC - 1) / PP_KC * PP_KC);
+                    for (int k = L + gtid; k < Lpad; k += 32 * PP_GEN_WARPS) {
+                        s_hx[k] = 1e30f;
+                        s_hy[k] = 1e30f;
+                        s_hz[k] = 0.f;
+                        if (EXACT_D) s_hzl[k] = 0.f;
+                    }
+                    gen_bar_sync();
+                    wlen = max(L, 1);
+                    have_e = -1;  // the dense path's window is gone
+                } else if (have_e != c.e || have_w0 != w0 || (MODEL == kSlope3 && have_l != c.l)) {
                     // (re)stage the window as structure-of-arrays x, y, z - z_ref (exact as zh + zl),
                     // padded to whole chunks with far-away hits (x = y = 1e30: factor 0), so each
                     // thread loads its 8 hits' coordinates as aligned float4s straight into the
@@ -249,6 +331,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(32 * PP_WARPS)
                         *reinterpret_cast<uint4 *>(d0 + 2 * PP_PART) =
                             isA ? make_uint4(wlo[0], wlo[1], wlo[2], wlo[3]) : make_uint4(w9[0], w9[1], w9[2], w9[3]);
                     }
+                    if (CULL && tid == 0) s_last[s] = (r0 >= n && k0 + PP_KC >= wlen) ? 1 : 0;
                     fence_proxy_async();  // this thread's generic-proxy stores -> visible to the tensor core
                     __syncwarp();
                     if (lane == 0) mbar_arrive(&arrive_bar[s]);
@@ -268,10 +351,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(32 * PP_WARPS)
                 const int n = a.offsets[c.e + 1] - a.offsets[c.e];
                 int nck = 0;
                 for (int w0 = 0; w0 < n; w0 += a.cap) nck += (min(a.cap, n - w0) + PP_KC - 1) / PP_KC;
-                for (int ck = 0; ck < nck; ++ck, ++cg) {
+                for (int ck = 0; CULL ? (n > 0) : (ck < nck); ++ck) {
                     const int s = (int)(cg % PP_NS);
                     mbar_wait(&s_pfull[s], (cg / PP_NS) & 1u);
+                    const bool last = CULL && s_last[s];
                     mbar_arrive_remote(full_addr0 + (uint32_t)(s * sizeof(uint64_t)));
+                    ++cg;
+                    if (last) break;
                 }
             }
         }
@@ -288,10 +374,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(32 * PP_WARPS)
                 const uint32_t acc = tmem + (uint32_t)(b * TC_N);
                 int nck = 0;  // chunks of this tile: every window is cut into 64-hit chunks
                 for (int w0 = 0; w0 < n; w0 += a.cap) nck += (min(a.cap, n - w0) + PP_KC - 1) / PP_KC;
-                for (int ck = 0; ck < nck; ++ck, ++cg) {
+                bool last = false;  // CULL: the generating warps flag the tile's last chunk
+                for (int ck = 0; CULL ? (n > 0 && !last) : (ck < nck); ++ck, ++cg) {
                     const int s = (int)(cg % PP_NS);
                     mbar_wait_cluster(&s_full[s], (cg / PP_NS) & 1u);
                     tc_fence_after();
+                    if (CULL) last = s_last[s];
                     // descriptor of the stage's first A / B part; offsets inside the stage are added
                     // to the 14-bit start-address field (address >> 4) directly
                     const uint64_t dA = umma_desc(stage_saddr + s * PP_STAGE, 128 * 16, 128);
@@ -307,7 +395,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(32 * PP_WARPS)
                     }
                     tc2_commit_both_warp(&s_empty[s]);
                 }
-                if (nck > 0) {
+                if (CULL ? n > 0 : nck > 0) {
                     tc2_commit_both_warp(&s_acc_full[b]);  // both CTAs: every MMA of this tile complete
                 } else if (lane == 0) {
                     mbar_arrive(&s_acc_full[b]);
@@ -438,9 +526,9 @@ static bool encode_out_map(CUtensorMap *map, float *R, int n0, int n1, long long
                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-template <int MODEL, bool ZREF, bool TMA_EPI>
+template <int MODEL, bool ZREF, bool TMA_EPI, bool CULL = false>
 static cudaError_t launch_pp(const GridArgs &a0, int n_events, const CUtensorMap &map, cudaStream_t stream) {
-    auto kern = grid_tensor16pp_kernel<MODEL, ZREF, TMA_EPI>;
+    auto kern = grid_tensor16pp_kernel<MODEL, ZREF, TMA_EPI, CULL>;
     GridArgs a = a0;
     // hit window: x, y, z (+ the low part of z - z_ref) as floats; whole chunks
     constexpr int n_arr = (ZREF || MODEL == kSlope3) ? 4 : 3;
@@ -468,20 +556,22 @@ static cudaError_t launch_pp(const GridArgs &a0, int n_events, const CUtensorMap
 }
 
 template <int MODEL, bool ZREF>
-static cudaError_t launch_pp_any(const GridArgs &a, int n_events, cudaStream_t stream) {
+static cudaError_t launch_pp_any(const GridArgs &a, int n_events, bool cull, cudaStream_t stream) {
     CUtensorMap map;
     const long long planes = (long long)n_events * (MODEL == kSlope3 ? a.n2 : 1);
-    if (encode_out_map(&map, a.R, a.n0, a.n1, planes)) return launch_pp<MODEL, ZREF, true>(a, n_events, map, stream);
+    if (encode_out_map(&map, a.R, a.n0, a.n1, planes))  // (culling rides on the TMA-store variant only)
+        return cull ? launch_pp<MODEL, ZREF, true, true>(a, n_events, map, stream)
+                    : launch_pp<MODEL, ZREF, true>(a, n_events, map, stream);
     memset(&map, 0, sizeof(map));
     return launch_pp<MODEL, ZREF, false>(a, n_events, map, stream);
 }
 
-cudaError_t launch_grid_tensor16p(int model, const GridArgs &a, int n_events, cudaStream_t stream) {
+cudaError_t launch_grid_tensor16p(int model, const GridArgs &a, int n_events, cudaStream_t stream, bool cull) {
     if (n_events == 0) return cudaSuccess;
-    if (model == kSlope3) return launch_pp_any<kSlope3, false>(a, n_events, stream);
+    if (model == kSlope3) return launch_pp_any<kSlope3, false>(a, n_events, cull, stream);
     if (model != kSlope2) return cudaErrorInvalidValue;
-    return (a.z_ref == 0.f) ? launch_pp_any<kSlope2, false>(a, n_events, stream)
-                            : launch_pp_any<kSlope2, true>(a, n_events, stream);
+    return (a.z_ref == 0.f) ? launch_pp_any<kSlope2, false>(a, n_events, cull, stream)
+                            : launch_pp_any<kSlope2, true>(a, n_events, cull, stream);
 }
 
 }  // namespace retina

@@ -121,7 +121,7 @@ cudaError_t launch_grid_response(int model, const GridArgs &a, int n_events, cud
 cudaError_t launch_grid_separable(int model, const GridArgs &a, int n_events, cudaStream_t stream);
 cudaError_t launch_grid_tensor(int model, const GridArgs &a, int n_events, cudaStream_t stream);
 cudaError_t launch_grid_tensor16(int model, const GridArgs &a, int n_events, cudaStream_t stream);
-cudaError_t launch_grid_tensor16p(int model, const GridArgs &a, int n_events, cudaStream_t stream);
+cudaError_t launch_grid_tensor16p(int model, const GridArgs &a, int n_events, cudaStream_t stream, bool cull = false);
 cudaError_t launch_grid_tensor16x2(int model, const GridArgs &a, int n_events, cudaStream_t stream);
 cudaError_t launch_newton(int model, const NewtonArgs &a, int n_events, cudaStream_t stream);
 cudaError_t launch_multistart(int model, const MultistartArgs &a, int n_events, cudaStream_t stream);

@@ -20,7 +20,7 @@ RETINA_OK, RETINA_EINVAL, RETINA_EUNSUPPORTED, RETINA_ECUDA = 0, 1, 2, 3
 MERGE_MAX_SEEDS = 16384
 
 GRID_AUTO, GRID_DIRECT, GRID_SEPARABLE, GRID_TENSOR, GRID_TENSOR_F16 = 0, 1, 2, 3, 4
-GRID_TENSOR_F16_PAIR, GRID_TENSOR_F16_SINGLE = 5, 6
+GRID_TENSOR_F16_PAIR, GRID_TENSOR_F16_SINGLE, GRID_TENSOR_F16_CULLED = 5, 6, 7
 MS_DENSE, MS_CULLED = 0, 1
 
 EXPORTED = ("retina_grid_response", "retina_grid_response_ex", "retina_estimate_peaks", "retina_find_peaks",

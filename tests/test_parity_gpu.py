@@ -783,6 +783,50 @@ def test_T1_default_grid_tma_store_ragged_tiles(model, z_ref, shape):
     assert torch.all(buf[n_cells:] == 7.25)
 
 
+@pytest.mark.parametrize("name,ev,model_shape", [
+    ("cfg3", [0, 4999], None), ("cfg1", [0], None),
+    ("ragged2", [700, 0, 1, 5000, 37], (C.SLOPE2, (300, 516))), ("ragged3", [700, 0, 1, 5000, 37], (C.SLOPE3, (130, 260, 5)))])
+def test_T1_culled_tensor_grid_vs_fp64_oracle(name, ev, model_shape):
+    """RETINA_GRID_TENSOR_F16_CULLED (each tile contracts only the hits that can reach it) against the
+    fp64 oracle on whole grids: T1 on every cell; its peaks equal the dense kernel's up to T4 near-ties."""
+    if model_shape is None:
+        cfg = C.CONFIGS[name]
+        b = G.make_batch(cfg, ev)
+        nodes = G.axis_nodes(cfg)
+        sigma, model = cfg.sigma, cfg.model
+    else:
+        model, shape = model_shape
+        b = synthetic_batch(model, ev, seed=5)
+        nodes = [np.linspace(lo, hi, n).astype(np.float32) for (lo, hi), n in
+                 zip([(-0.3, 0.3), (-0.3, 0.3), (-150.0, 150.0)], shape)]
+        sigma = 0.44
+        cfg = C.Config(name="t", model=model, n_events=len(ev), seed=0, n_tracks=0, sigma=sigma)
+    g = gpu_grid(b, cfg, nodes, algo=R.retina.GRID_TENSOR_F16_CULLED)
+    ref = ora.grid(model, b.offsets, b.hits, nodes, sigma)
+    ok, worst = PU.t1_response(g, ref)
+    assert ok, worst
+    P = len(nodes)
+    for e in range(g.shape[0]):
+        idx, _, cnt = R.retina_find_peaks(dev(g[e:e + 1]), P, 2.5, 1 << 16)
+        okp, nd, ne = PU.t4_peak_sets(idx.cpu().numpy()[0], int(cnt[0]), ref[e], P, 2.5, 1 << 16)
+        assert okp, (e, nd, ne)
+    PU.report(f"T1/T4 culled grid {name}", t1_worst=worst)
+
+
+@pytest.mark.parametrize("name,n_ev", [("cfg3", 160), ("cfg4", 12)])
+def test_culled_tensor_grid_many_tiles_per_cluster(name, n_ev):
+    """Many tiles per persistent CTA pair (the per-tile windows, the 'last chunk' flags and the ring
+    phases carried from tile to tile): the culled grid equals the dense one within 2e-5 relative
+    (each within 1e-5 of fp64, T1) on every cell of every event."""
+    cfg = C.CONFIGS[name]
+    b = G.make_batch(cfg, range(n_ev))
+    nodes = G.axis_nodes(cfg)
+    gd = gpu_grid(b, cfg, nodes, algo=R.retina.GRID_TENSOR_F16)
+    gc = gpu_grid(b, cfg, nodes, algo=R.retina.GRID_TENSOR_F16_CULLED)
+    err = np.abs(gc.astype(np.float64) - gd) / (2e-5 * np.maximum(gd.astype(np.float64), 1e-6))
+    assert err.max() <= 1.0, err.max()
+
+
 @pytest.mark.parametrize("tensor", TENSORS)
 def test_T1_tensor_grid_cfg4_full_size_sampled_and_peaks(tensor):
     cfg = C.CFG4
