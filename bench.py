@@ -93,6 +93,10 @@ def args_():
                     help="fixed-step multi-start kernel: dense (every pair, the metric's definition) or culled "
                          "(SLOPE2/SLOPE3: the same results bit for bit, evaluating only pairs whose weight can be "
                          "non-zero; value then counts the pairs actually evaluated)")
+    ap.add_argument("--grid-algo", default="dense", choices=["dense", "culled"],
+                    help="grid kernel: dense (every unit.hit pair) or culled (RETINA_GRID_TENSOR_F16_CULLED: each "
+                         "tile contracts only the hits that can reach it; within T1 of the dense grid; value "
+                         "then counts the pairs actually contracted)")
     ap.add_argument("--update", default="gradient", choices=["gradient", "newton"],
                     help="multi-start update: BASELINE fixed-step ascent, or the paper's Truncated Newton")
     ap.add_argument("--dist-check", action="store_true",
@@ -397,14 +401,18 @@ def main():
         if cfg.model not in (C.SLOPE2, C.SLOPE3) or not cfg.n_seeds:
             raise SystemExit(f"--ms-algo culled needs a SLOPE2/SLOPE3 config with seeds ({cfg.name})")
         spec.ms_algorithm = RT.MS_CULLED
+    if a.grid_algo == "culled":
+        if cfg.model not in (C.SLOPE2, C.SLOPE3) or not cfg.axes:
+            raise SystemExit(f"--grid-algo culled needs a SLOPE2/SLOPE3 grid config ({cfg.name})")
+        spec.grid_algorithm = RT.GRID_TENSOR_F16_CULLED
     pipe = RetinaPipeline(spec, E, chunk_events=a.chunk_events, overlap_peaks=a.overlap_peaks,
                           grid_bytes_budget=a.grid_buffer_gb * 1e9)
     stream = torch.cuda.current_stream()
     dbatch = upload(batch.offsets, batch.hits, seeds)
-    if a.update == "newton" or pipe.pairs_ev is not None:
+    if a.update == "newton" or pipe.pairs_ev is not None or pipe.grid_pairs_ev is not None:
         # the pairs count comes from the kernel: per-seed evaluation counts (Newton) or the pairs
         # the culled kernel evaluated (one counted run, outside the timed region)
-        pipe.count_pairs = pipe.pairs_ev is not None
+        pipe.count_pairs = pipe.pairs_ev is not None or pipe.grid_pairs_ev is not None
         pipe.run(dbatch, stream=stream)
         torch.cuda.synchronize()
         pipe.count_pairs = False

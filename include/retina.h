@@ -16,7 +16,7 @@
  *                               cluster select solution with highest response and above
  *                               threshold R0" (Z9, Z10).
  * and the "next" rows built on them:
- *   retina_grid_response_ex     the same grid with an explicit kernel choice;
+ *   retina_grid_response_ex     the same grid with an explicit kernel choice (_ex2: + pairs contracted);
  *   retina_find_peaks_ws        step (iii) by many CTAs per event (caller workspace);
  *   retina_estimate_peaks       step (iv): sub-cell parameter estimate per peak;
  *   retina_multistart_optimize_ex  the same update loop, optionally evaluating only the pairs that
@@ -137,6 +137,14 @@ enum { RETINA_GRID_AUTO = 0, RETINA_GRID_DIRECT = 1, RETINA_GRID_SEPARABLE = 2, 
 int retina_grid_response_ex(const retina_events *ev, int model, float sigma,
                             const int32_t *axis_len, const float *const *axis_nodes,
                             float *response, int algorithm, void *stream);
+/* retina_grid_response_ex that also ADDS to *pairs_evaluated (device uint64, may be NULL) the
+ * (unit, hit) pairs the kernel contracted: hits x cells for every algorithm but
+ * RETINA_GRID_TENSOR_F16_CULLED, which counts, per tile, its cells x the hits it kept. */
+
+int retina_grid_response_ex2(const retina_events *ev, int model, float sigma,
+                             const int32_t *axis_len, const float *const *axis_nodes,
+                             float *response, int algorithm, unsigned long long *pairs_evaluated,
+                             void *stream);
 
 /* Step (iii) on a response grid (any fp32 grid of that shape):
  * cell c is reported iff response[c] >= threshold and response[c] > response[n] for every

@@ -85,8 +85,20 @@ int retina_grid_response(const retina_events *ev, int model, float sigma, const 
     return retina_grid_response_ex(ev, model, sigma, axis_len, axis_nodes, response, RETINA_GRID_AUTO, stream);
 }
 
+// pairs every grid kernel but the culled one contracts: hits x cells, added on the device
+__global__ void add_grid_pairs_kernel(const int32_t *offsets, int n_events, long long cells, unsigned long long *pairs) {
+    if (blockIdx.x == 0 && threadIdx.x == 0)
+        atomicAdd(pairs, (unsigned long long)(offsets[n_events] - offsets[0]) * (unsigned long long)cells);
+}
+
 int retina_grid_response_ex(const retina_events *ev, int model, float sigma, const int32_t *axis_len,
                             const float *const *axis_nodes, float *response, int algorithm, void *stream) {
+    return retina_grid_response_ex2(ev, model, sigma, axis_len, axis_nodes, response, algorithm, nullptr, stream);
+}
+
+int retina_grid_response_ex2(const retina_events *ev, int model, float sigma, const int32_t *axis_len,
+                             const float *const *axis_nodes, float *response, int algorithm,
+                             unsigned long long *pairs_evaluated, void *stream) {
     g_last_error[0] = 0;
     int st = check_events(ev);
     if (st) return st;
@@ -124,6 +136,7 @@ int retina_grid_response_ex(const retina_events *ev, int model, float sigma, con
     a.nodes2 = (P == 3) ? axis_nodes[2] : nullptr;
     a.R = response;
     a.cap = stage_cap(ev->max_event_hits, 2048);
+    a.pairs = (algorithm == RETINA_GRID_TENSOR_F16_CULLED) ? pairs_evaluated : nullptr;
     cudaError_t err;
     if (algorithm == RETINA_GRID_TENSOR)
         err = retina::launch_grid_tensor(model, a, ev->n_events, (cudaStream_t)stream);
@@ -138,6 +151,10 @@ int retina_grid_response_ex(const retina_events *ev, int model, float sigma, con
         err = retina::launch_grid_separable(model, a, ev->n_events, (cudaStream_t)stream);
     else
         err = retina::launch_grid_response(model, a, ev->n_events, (cudaStream_t)stream);
+    if (err == cudaSuccess && pairs_evaluated && ev->n_events > 0 && !a.pairs) {
+        add_grid_pairs_kernel<<<1, 32, 0, (cudaStream_t)stream>>>(ev->offsets, ev->n_events, cells, pairs_evaluated);
+        err = cudaGetLastError();
+    }
     if (err != cudaSuccess) return cuda_fail(err, "retina_grid_response");
     return RETINA_OK;
 }

@@ -190,7 +190,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(32 * PP_WARPS)
                 tyh = fmaxf(v0, v1);
             }
             const float K = -a.negK;
-            int r0 = 0;  // CULL: next raw hit of the event to scan
+            int r0 = 0;             // CULL: next raw hit of the event to scan
+            long long kept = 0;     // CULL: hits this tile keeps (all windows)
             for (int w0 = 0; CULL ? (r0 < n) : (w0 < n); w0 += a.cap) {
                 int wlen = min(a.cap, n - w0);
                 if (CULL) {
@@ -244,6 +245,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(32 * PP_WARPS)
                     }
                     gen_bar_sync();
                     wlen = max(L, 1);
+                    kept += L;
                     have_e = -1;  // the dense path's window is gone
                 } else if (have_e != c.e || have_w0 != w0 || (MODEL == kSlope3 && have_l != c.l)) {
                     // (re)stage the window as structure-of-arrays x, y, z - z_ref (exact as zh + zl),
@@ -336,6 +338,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(32 * PP_WARPS)
                     __syncwarp();
                     if (lane == 0) mbar_arrive(&arrive_bar[s]);
                 }
+            }
+            if (CULL && a.pairs && rank == 0 && tid == 0 && kept > 0) {  // cells of the pair tile x kept hits
+                const int i0 = (c.t_m & ~1) * 128, j0 = c.t_n * TC_N;
+                const long long cells = (long long)min(256, a.n0 - i0) * min(TC_N, a.n1 - j0);
+                atomicAdd(a.pairs, (unsigned long long)(cells * kept));
             }
         }
     } else if (warp == PP_MMA_WARP) {

@@ -17,6 +17,7 @@ struct GridArgs {
     float *R;
     int cap;     // float4 slots of the shared-memory hit stage
     int e_base;
+    unsigned long long *pairs;  // culled tensor grid: (unit, hit) pairs contracted are added here (or NULL)
 };
 
 struct MultistartArgs {

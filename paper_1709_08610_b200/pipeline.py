@@ -39,7 +39,8 @@ class PathSpec:
     z_ref: float = 0.0
     sigma_ms: Optional[float] = None     # multi-start sigma (defaults to sigma)
     newton: Optional[tuple] = None       # (sigmas, etas, final_sigma, max_halvings): Newton update
-    ms_algorithm: int = 0                # R.MS_DENSE, or R.MS_CULLED (SLOPE2: same results, fewer pairs)
+    ms_algorithm: int = 0                # R.MS_DENSE, or R.MS_CULLED (SLOPE2/3: same results, fewer pairs)
+    grid_algorithm: int = 0              # R.GRID_AUTO, or e.g. R.GRID_TENSOR_F16_CULLED
 
     @property
     def P(self) -> int:
@@ -107,7 +108,11 @@ class RetinaPipeline:
             nb = R.multistart_workspace_size(E, S, spec.ms_algorithm)
             self.ms_ws = torch.empty((max(nb, 4) // 4,), dtype=torch.int32, device=self.device)
             self.pairs_ev = torch.zeros((1,), dtype=torch.int64, device=self.device)
-        self.count_pairs = False  # run(): add the pairs the culled kernel evaluates to pairs_ev
+        # culled grid: the pairs the tiles contracted
+        self.grid_pairs_ev = None
+        if spec.cells and spec.grid_algorithm == R.GRID_TENSOR_F16_CULLED:
+            self.grid_pairs_ev = torch.zeros((1,), dtype=torch.int64, device=self.device)
+        self.count_pairs = False  # run(): add the pairs the culled kernels evaluate to pairs_ev / grid_pairs_ev
         self.t_theta = torch.empty((E, spec.track_capacity, P), dtype=torch.float32, device=self.device)
         self.t_resp = torch.empty((E, spec.track_capacity), dtype=torch.float32, device=self.device)
         self.t_seed = torch.empty((E, spec.track_capacity), dtype=torch.int32, device=self.device)
@@ -122,6 +127,8 @@ class RetinaPipeline:
         kernel's per-seed counts of the last pass (call after one run())."""
         n = batch.n_hits_per_event.astype(np.float64)
         grid = float(n.sum()) * self.spec.cells
+        if self.grid_pairs_ev is not None:  # the pairs the culled grid contracted in the counted run
+            grid = float(self.grid_pairs_ev.item())
         if self.spec.newton is not None:
             E = batch.n_events
             ev = self.evals[:E].to(torch.float64).sum(dim=1).cpu().numpy()
@@ -152,7 +159,9 @@ class RetinaPipeline:
             out = self.grid_bufs[b][: e1 - e0]
             if timer is not None:
                 timer.start("grid", main)
-            R.retina_grid_response(ev, sp.model, sp.sigma, self.nodes, out=out, stream=main)
+            R.retina_grid_response(ev, sp.model, sp.sigma, self.nodes, out=out, stream=main,
+                                   algorithm=sp.grid_algorithm,
+                                   pairs_evaluated=self.grid_pairs_ev if self.count_pairs else None)
             if timer is not None:
                 timer.stop("grid", main)
             if side is not main:

@@ -23,7 +23,8 @@ GRID_AUTO, GRID_DIRECT, GRID_SEPARABLE, GRID_TENSOR, GRID_TENSOR_F16 = 0, 1, 2, 
 GRID_TENSOR_F16_PAIR, GRID_TENSOR_F16_SINGLE, GRID_TENSOR_F16_CULLED = 5, 6, 7
 MS_DENSE, MS_CULLED = 0, 1
 
-EXPORTED = ("retina_grid_response", "retina_grid_response_ex", "retina_estimate_peaks", "retina_find_peaks",
+EXPORTED = ("retina_grid_response", "retina_grid_response_ex", "retina_grid_response_ex2", "retina_estimate_peaks",
+            "retina_find_peaks",
             "retina_find_peaks_ws", "retina_find_peaks_workspace_size",
             "retina_multistart_optimize", "retina_multistart_optimize_ex", "retina_multistart_workspace_size",
             "retina_multistart_newton", "retina_multistart_newton_ex",
@@ -62,6 +63,9 @@ def lib() -> ctypes.CDLL:
         L = ctypes.CDLL(path)
         vp, i32, f32 = ctypes.c_void_p, ctypes.c_int32, ctypes.c_float
         L.retina_grid_response.argtypes = [ctypes.POINTER(retina_events), ctypes.c_int, f32, vp, vp, vp, vp]
+        L.retina_grid_response_ex2.argtypes = [ctypes.POINTER(retina_events), ctypes.c_int, f32, vp, vp, vp,
+                                               ctypes.c_int, vp, vp]
+        L.retina_grid_response_ex2.restype = ctypes.c_int
         L.retina_grid_response_ex.argtypes = [ctypes.POINTER(retina_events), ctypes.c_int, f32, vp, vp, vp,
                                               ctypes.c_int, vp]
         L.retina_find_peaks.argtypes = [vp, i32, i32, vp, f32, i32, vp, vp, vp, vp]
@@ -179,8 +183,10 @@ def _param_axis_len(grid_dims: Sequence[int]) -> list:
 
 
 def retina_grid_response(events: Events, model: int, sigma: float, nodes: Sequence[torch.Tensor],
-                         out: Optional[torch.Tensor] = None, stream=None, algorithm: int = GRID_AUTO
-                         ) -> torch.Tensor:
+                         out: Optional[torch.Tensor] = None, stream=None, algorithm: int = GRID_AUTO,
+                         pairs_evaluated: Optional[torch.Tensor] = None) -> torch.Tensor:
+    """Eq. (2) grid, shape grid_shape(E, node counts).  pairs_evaluated (int64 [1] device tensor)
+    accumulates the (unit, hit) pairs contracted (retina_grid_response_ex2)."""
     P = MODEL_P[model]
     nodes = [_dev(n, torch.float32) for n in nodes]
     alen, _k1 = _arr(ctypes.c_int32, [n.numel() for n in nodes])
@@ -189,6 +195,13 @@ def retina_grid_response(events: Events, model: int, sigma: float, nodes: Sequen
     if out is None:
         out = torch.empty(shape, device=events.hits.device, dtype=torch.float32)
     _out("response", out, torch.float32, shape, events.hits.device)
+    if pairs_evaluated is not None:
+        _out("pairs_evaluated", pairs_evaluated, torch.int64, (1,), events.hits.device)
+        _check("retina_grid_response_ex2",
+               lib().retina_grid_response_ex2(ctypes.byref(events.c), model, float(sigma), alen, nptr,
+                                              _ptr(_dev(out, torch.float32)), int(algorithm), _ptr(pairs_evaluated),
+                                              _stream(stream)))
+        return out
     _check("retina_grid_response_ex",
            lib().retina_grid_response_ex(ctypes.byref(events.c), model, float(sigma), alen, nptr,
                                          _ptr(_dev(out, torch.float32)), int(algorithm), _stream(stream)))

@@ -23,7 +23,7 @@ def L():
 def declared_functions():
     src = open(HEADER).read()
     src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
-    return sorted(set(re.findall(r"\b(retina_[a-z_]+)\s*\(", src)))
+    return sorted(set(re.findall(r"\b(retina_[a-z0-9_]+)\s*\(", src)))
 
 
 def test_exports_every_declared_symbol(L):
@@ -74,7 +74,7 @@ def test_grid_response_validation(L):
     big = _i(65536, 65536)
     assert g(ctypes.byref(ev), 1, 0.5, big, nodes, 16, None) == rt.RETINA_EUNSUPPORTED
     gx = L.retina_grid_response_ex
-    assert gx(ctypes.byref(ev), 1, 0.5, alen, nodes, 16, 7, None) == rt.RETINA_EINVAL  # unknown algorithm
+    assert gx(ctypes.byref(ev), 1, 0.5, alen, nodes, 16, 8, None) == rt.RETINA_EINVAL  # unknown algorithm
     assert gx(ctypes.byref(ev), 1, 0.5, alen, nodes, 16, -1, None) == rt.RETINA_EINVAL
     for algo in (rt.GRID_TENSOR, rt.GRID_TENSOR_F16, rt.GRID_TENSOR_F16_PAIR, rt.GRID_TENSOR_F16_SINGLE,
                  rt.GRID_SEPARABLE):  # LINE2D does not factorise

@@ -825,6 +825,19 @@ def test_culled_tensor_grid_many_tiles_per_cluster(name, n_ev):
     gc = gpu_grid(b, cfg, nodes, algo=R.retina.GRID_TENSOR_F16_CULLED)
     err = np.abs(gc.astype(np.float64) - gd) / (2e-5 * np.maximum(gd.astype(np.float64), 1e-6))
     assert err.max() <= 1.0, err.max()
+    # the pair counters: every pair for the dense kernel, the kept (tile, hit) pairs for the culled one
+    ev = events_of(b)
+    dn = [dev(n) for n in nodes]
+    pd = torch.zeros(1, dtype=torch.int64, device=DEV)
+    pc = torch.zeros(1, dtype=torch.int64, device=DEV)
+    R.retina_grid_response(ev, cfg.model, cfg.sigma, dn, algorithm=R.retina.GRID_TENSOR_F16, pairs_evaluated=pd)
+    R.retina_grid_response(ev, cfg.model, cfg.sigma, dn, algorithm=R.retina.GRID_TENSOR_F16_CULLED,
+                           pairs_evaluated=pc)
+    torch.cuda.synchronize()
+    assert int(pd.item()) == int(b.offsets[-1]) * int(np.prod([len(n) for n in nodes]))
+    assert 0 < int(pc.item()) <= int(pd.item())
+    PU.report(f"culled grid {name} x{n_ev}", pairs_all=int(pd.item()), pairs_contracted=int(pc.item()),
+              frac=int(pc.item()) / int(pd.item()))
 
 
 @pytest.mark.parametrize("tensor", TENSORS)
