@@ -550,7 +550,13 @@ cudaError_t launch_multistart(int model, const MultistartArgs &a, int n_events, 
 #ifndef RETINA_MC_UNITS
 #define RETINA_MC_UNITS 16  // at most this many units of 256 seeds per block, dealt to its 4 warps
 #endif
-constexpr int kMcThreads = 128, kMcSeeds = 8, kMcWarps = kMcThreads / 32, kMcUnits = RETINA_MC_UNITS;
+#ifndef RETINA_MC_SEEDS
+#define RETINA_MC_SEEDS 2  // SLOPE2 seeds per thread in K4c (a unit = 32 x this: small units, tight boxes; 8 / 4 / 2 measured 31.2 / 22.8 / 17.0 ms per 2,000 cfg3 events)
+#endif
+#ifndef RETINA_MC3_SEEDS
+#define RETINA_MC3_SEEDS 4  // SLOPE3 (4 / 2: 39.3 / 37.7 ms per 100 cfg4 events, but 278 / 295 ms on the full 1,000)
+#endif
+constexpr int kMcThreads = 128, kMcSeeds = RETINA_MC_SEEDS, kMcWarps = kMcThreads / 32, kMcUnits = RETINA_MC_UNITS;
 
 // ---------------------------------------------------------------- K4c-sort: Morton order per event
 // perm[e][q] = caller index of the q-th seed of event e along a Morton curve of the seed's
@@ -844,7 +850,7 @@ static cudaError_t launch_mc(const MultistartArgs &a0, int n_events, int32_t *pe
 cudaError_t launch_multistart_culled(int model, const MultistartArgs &a, int n_events, int32_t *perm,
                                      unsigned long long *pairs_evaluated, cudaStream_t stream) {
     if (n_events == 0 || a.n_seeds == 0) return cudaSuccess;
-    if (model == kSlope3) return launch_mc<kSlope3, RETINA_MS3_SEEDS, false>(a, n_events, perm, pairs_evaluated, stream);
+    if (model == kSlope3) return launch_mc<kSlope3, RETINA_MC3_SEEDS, false>(a, n_events, perm, pairs_evaluated, stream);
     if (model != kSlope2) return cudaErrorInvalidValue;
     return (a.z_ref == 0.f) ? launch_mc<kSlope2, kMcSeeds, false>(a, n_events, perm, pairs_evaluated, stream)
                             : launch_mc<kSlope2, kMcSeeds, true>(a, n_events, perm, pairs_evaluated, stream);
