@@ -90,7 +90,7 @@ def args_():
     ap.add_argument("--no-graph", dest="graph", action="store_false",
                     help="skip the CUDA-graph replay measurement")
     ap.add_argument("--ms-algo", default="dense", choices=["dense", "culled"],
-                    help="fixed-step multi-start kernel: dense (every pair, the metric's definition) or culled "
+                    help="multi-start kernel (fixed step, or Newton with --update newton): dense (every pair, the metric's definition) or culled "
                          "(SLOPE2/SLOPE3: the same results bit for bit, evaluating only pairs whose weight can be "
                          "non-zero; value then counts the pairs actually evaluated)")
     ap.add_argument("--grid-algo", default="dense", choices=["dense", "culled"],
@@ -397,7 +397,7 @@ def main():
         if cfg.model == C.LINE2D or not cfg.n_seeds:
             raise SystemExit(f"--update newton needs a SLOPE2/SLOPE3 config with seeds ({cfg.name} has none)")
         spec.newton = C.newton_schedule(cfg)
-    elif a.ms_algo == "culled":
+    if a.ms_algo == "culled":
         if cfg.model not in (C.SLOPE2, C.SLOPE3) or not cfg.n_seeds:
             raise SystemExit(f"--ms-algo culled needs a SLOPE2/SLOPE3 config with seeds ({cfg.name})")
         spec.ms_algorithm = RT.MS_CULLED
@@ -579,7 +579,8 @@ def main():
         else:
             peak = N_SM * MUFU_PER_SM_CLK * fmax  # 1 MUFU.EX2 per pair
             kname = {"grid": "grid_separable/direct",
-                     "multistart": "newton_kernel" if a.update == "newton" else "multistart_kernel"}[ph]
+                     "multistart": ("newton_kernel" + (" (culled)" if a.ms_algo == "culled" else ""))
+                     if a.update == "newton" else "multistart_kernel"}[ph]
             r = {"bound": "alu", "kernel": kname,
                  "achieved": pairs_s / 1e9, "peak": peak / 1e9, "unit": "Gpair/s (1 MUFU.EX2 per pair)",
                  "frac": pairs_s / peak,
@@ -593,7 +594,9 @@ def main():
             # the binding pipe of the loop: MUFU or the FMA pipe at its measured register-operand rate
             if a.update == "newton":
                 q = len(spec.newton[0])
-                ev_mean = pairs_ms / max(1.0, float(batch.n_hits) * cfg.n_seeds)
+                # response evaluations per seed (the kernel's counts; the culled kernel's pairs are not
+                # evaluations x hits)
+                ev_mean = float(pipe.evals[:E].to(torch.float64).mean().item())
                 cyc = (q / binding_pairs_per_clk(FMA_OPS["hessian"])
                        + max(0.0, ev_mean - q) / binding_pairs_per_clk(FMA_OPS["r_only"])) / ev_mean
                 basis = (f"{q} Hessian-mode evaluations (13 FMA-pipe lane-ops/pair) and {ev_mean - q:.2f} R-only "
@@ -614,7 +617,11 @@ def main():
             r["kernel"] = "multistart_culled_kernel"
             r["work_basis"] = ("pairs = (seed, hit) pairs the culled kernel evaluated (counted on the device); "
                                "the skipped pairs have weight exactly +0")
-        if ph == "multistart" and a.update == "newton":
+        if ph == "multistart" and a.update == "newton" and a.ms_algo == "culled":
+            r["work_basis"] = ("pairs = (seed, hit) pairs the culled Newton kernel's passes visited (counted on the "
+                               "device, speculative line-search halvings included); the skipped pairs have weight "
+                               "exactly +0")
+        elif ph == "multistart" and a.update == "newton":
             r["work_basis"] = ("pairs = sum over seeds of response evaluations (q Hessian-mode + line-search "
                                "trials + final; counted by the kernel, PAPER.md:200-201 cost unit) x event hits")
         tcfg = traffic.get(cfg.name, {}) if not a.dense else {}  # per config: the capture's workload
@@ -635,7 +642,9 @@ def main():
                             + (" (culled multi-start kernel: bit-identical results, pairs = pairs evaluated)"
                                if a.ms_algo == "culled" else "")
                             if a.update == "gradient" else
-                            f"{cfg.n_seeds} seeds x q=3 Truncated-Newton steps (sigma schedule) + merge"))
+                            f"{cfg.n_seeds} seeds x q=3 Truncated-Newton steps (sigma schedule) + merge"
+                            + (" (culled Newton kernel: bit-identical results, pairs = pairs visited)"
+                               if a.ms_algo == "culled" else "")))
                    if cfg.n_seeds else ""))
     line = {
         "metric": METRIC, "value": pairs_all / (ms_step * 1e-3), "unit": UNIT, "n_gpus": world,

@@ -22,7 +22,8 @@
  *   retina_multistart_optimize_ex  the same update loop, optionally evaluating only the pairs that
  *                               can contribute (bit-identical results; RETINA_MS_CULLED);
  *   retina_multistart_newton    Algorithm 1 with the paper's Truncated-Newton update and sigma
- *   (_ex)                       schedule, PAPER.md:213-216 (+ per-seed evaluation counts);
+ *   (_ex, _ex2)                 schedule, PAPER.md:213-216 (+ per-seed evaluation counts; _ex2:
+ *                               optionally culled like the update loop, bit-identical results);
  *   retina_pack_results         the per-rank record of the one multi-GPU result gather.
  *
  * Track models and the distance s:
@@ -262,6 +263,28 @@ int retina_multistart_newton_ex(const retina_events *ev, int model, int32_t n_se
                                 int32_t max_halvings, const float *box_lo, const float *box_hi,
                                 float *theta_out, float *response_out, float *grad_out, int32_t *evals_out,
                                 void *stream);
+
+/* retina_multistart_newton_ex with an explicit algorithm (as retina_multistart_optimize_ex):
+ *   RETINA_MS_DENSE   every pass visits every hit (what retina_multistart_newton_ex does);
+ *   RETINA_MS_CULLED  the SAME results bit for bit (theta, R, grad R and evals_out), each warp
+ *                     visiting only the hits that can contribute: the seeds of each event are taken
+ *                     in Morton order of theta, and before every pass (Hessian mode, each line-search
+ *                     trial pass, the final pass) a warp lists, in hit order, the hits a conservative
+ *                     bound keeps within K_j s^2 <= 128 of the box of the points it evaluates (K_j =
+ *                     1/sigma_j^2 of that pass); the others would add exactly +0 under ex2.approx.ftz.
+ *                     Needs a DEVICE workspace of at least retina_multistart_workspace_size(n_events,
+ *                     n_seeds, RETINA_MS_CULLED) bytes; n_seeds <= 16,384.  Events larger than the
+ *                     hit stage run the dense passes.
+ *   pairs_evaluated:  device uint64 or NULL: RETINA_MS_DENSE ADDS evaluations x hits (every
+ *                     evaluation visits every hit); RETINA_MS_CULLED adds the (seed, hit) pairs its
+ *                     passes visited for real seeds (including the line search's speculative
+ *                     halvings, which evals_out does not count). */
+int retina_multistart_newton_ex2(const retina_events *ev, int model, int32_t n_seeds, const float *seeds,
+                                 int32_t n_steps, const float *sigmas, const float *etas, float final_sigma,
+                                 int32_t max_halvings, const float *box_lo, const float *box_hi,
+                                 float *theta_out, float *response_out, float *grad_out, int32_t *evals_out,
+                                 int algorithm, void *workspace, size_t workspace_bytes,
+                                 unsigned long long *pairs_evaluated, void *stream);
 
 /* Algorithm 1 "cluster solutions ... select highest response above R0" per event:
  *   keep seeds with response >= threshold; order them by (response descending, theta

@@ -384,7 +384,20 @@ int retina_multistart_newton_ex(const retina_events *ev, int model, int32_t n_se
                                 int32_t n_steps, const float *sigmas, const float *etas, float final_sigma,
                                 int32_t max_halvings, const float *box_lo, const float *box_hi, float *theta_out,
                                 float *response_out, float *grad_out, int32_t *evals_out, void *stream) {
+    return retina_multistart_newton_ex2(ev, model, n_seeds, seeds, n_steps, sigmas, etas, final_sigma, max_halvings,
+                                        box_lo, box_hi, theta_out, response_out, grad_out, evals_out, RETINA_MS_DENSE,
+                                        nullptr, 0, nullptr, stream);
+}
+
+int retina_multistart_newton_ex2(const retina_events *ev, int model, int32_t n_seeds, const float *seeds,
+                                 int32_t n_steps, const float *sigmas, const float *etas, float final_sigma,
+                                 int32_t max_halvings, const float *box_lo, const float *box_hi, float *theta_out,
+                                 float *response_out, float *grad_out, int32_t *evals_out, int algorithm,
+                                 void *workspace, size_t workspace_bytes, unsigned long long *pairs_evaluated,
+                                 void *stream) {
     g_last_error[0] = 0;
+    if (algorithm != RETINA_MS_DENSE && algorithm != RETINA_MS_CULLED)
+        return fail(RETINA_EINVAL, "unknown multi-start algorithm %d", algorithm);
     int st = check_events(ev);
     if (st) return st;
     const int P = model_P(model);
@@ -432,7 +445,18 @@ int retina_multistart_newton_ex(const retina_events *ev, int model, int32_t n_se
     a.evals_out = evals_out;
     a.reuse_final = (grad_out == nullptr && n_steps > 0 && a.negK[n_steps - 1] == a.final_negK) ? 1 : 0;
     a.cap = stage_cap(ev->max_event_hits, 4096);
-    const cudaError_t err = retina::launch_newton(model, a, ev->n_events, (cudaStream_t)stream);
+    cudaError_t err;
+    if (algorithm == RETINA_MS_CULLED) {
+        if (!retina::multistart_culled_ok(model, n_seeds))
+            return fail(RETINA_EUNSUPPORTED, "RETINA_MS_CULLED: n_seeds <= 16384 only");
+        const size_t need = retina_multistart_workspace_size(ev->n_events, n_seeds, algorithm);
+        if (!workspace || workspace_bytes < need)
+            return fail(RETINA_EINVAL, "workspace of %zu bytes needed (got %zu)", need, workspace_bytes);
+        err = retina::launch_newton_culled(model, a, ev->n_events, static_cast<int32_t *>(workspace), pairs_evaluated,
+                                           (cudaStream_t)stream);
+    } else {
+        err = retina::launch_newton(model, a, ev->n_events, pairs_evaluated, (cudaStream_t)stream);
+    }
     if (err != cudaSuccess) return cuda_fail(err, "retina_multistart_newton");
     return RETINA_OK;
 }

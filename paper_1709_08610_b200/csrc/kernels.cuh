@@ -124,7 +124,15 @@ cudaError_t launch_grid_tensor(int model, const GridArgs &a, int n_events, cudaS
 cudaError_t launch_grid_tensor16(int model, const GridArgs &a, int n_events, cudaStream_t stream);
 cudaError_t launch_grid_tensor16p(int model, const GridArgs &a, int n_events, cudaStream_t stream, bool cull = false);
 cudaError_t launch_grid_tensor16x2(int model, const GridArgs &a, int n_events, cudaStream_t stream);
-cudaError_t launch_newton(int model, const NewtonArgs &a, int n_events, cudaStream_t stream);
+cudaError_t launch_newton(int model, const NewtonArgs &a, int n_events, unsigned long long *pairs_evaluated,
+                          cudaStream_t stream);
+// K6c (newton.cu): the same results as K6, evaluating only the pairs that can contribute; perm is the
+// per-event Morton permutation workspace (multistart_culled_workspace_bytes)
+cudaError_t launch_newton_culled(int model, const NewtonArgs &a, int n_events, int32_t *perm,
+                                 unsigned long long *pairs_evaluated, cudaStream_t stream);
+// K4c-sort: perm[e][q] = caller index of event e's q-th seed along a Morton curve over the box
+cudaError_t launch_seed_morton_sort(const float *seeds, int n_seeds, int P, const float (&lo)[3], const float (&hi)[3],
+                                    int32_t *perm, int n_events, cudaStream_t stream);
 cudaError_t launch_multistart(int model, const MultistartArgs &a, int n_events, cudaStream_t stream);
 // K4c (multistart.cu): the same results as K4 for SLOPE2, evaluating only the pairs that can contribute
 bool multistart_culled_ok(int model, int n_seeds);

@@ -20,6 +20,7 @@
 // with w = exp(-s^2/sigma^2) = ex2(-K s^2), c2 = 2/sigma^2.
 #include "common.cuh"
 #include "kernels.cuh"
+#include "cull.cuh"
 
 #include <algorithm>
 #include <type_traits>
@@ -604,83 +605,7 @@ __global__ void __launch_bounds__(1024) seed_morton_sort_kernel(const float *see
         perm[(int64_t)e * n_seeds + i] = (int32_t)(s_key[i] & 0xffffffffull);
 }
 
-// ---------------------------------------------------------------- K4c
-struct McBox {
-    float lo[3], hi[3];  // the seeds' parameter box; lo[0] > hi[0]: empty
-};
-
-// the box of the warp's valid seeds (warp-uniform)
-template <int P, int S>
-__device__ __forceinline__ McBox mc_warp_box(const float (&th)[S][3], const bool (&ok)[S]) {
-    McBox b;
-#pragma unroll
-    for (int i = 0; i < 3; ++i) {
-        b.lo[i] = 3.4e38f;
-        b.hi[i] = -3.4e38f;
-    }
-#pragma unroll
-    for (int s = 0; s < S; ++s)
-        if (ok[s])
-#pragma unroll
-            for (int i = 0; i < P; ++i) {
-                b.lo[i] = fminf(b.lo[i], th[s][i]);
-                b.hi[i] = fmaxf(b.hi[i], th[s][i]);
-            }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1)
-#pragma unroll
-        for (int i = 0; i < P; ++i) {
-            b.lo[i] = fminf(b.lo[i], __shfl_xor_sync(0xffffffffu, b.lo[i], o));
-            b.hi[i] = fmaxf(b.hi[i], __shfl_xor_sync(0xffffffffu, b.hi[i], o));
-        }
-    return b;
-}
-
-// least |x - t d| over t in [t0, t1] and d in [d0, d1] (0 when the range of t d contains x)
-__device__ __forceinline__ float mc_min_abs(float x, float t0, float t1, float d0, float d1) {
-    const float p00 = t0 * d0, p01 = t0 * d1, p10 = t1 * d0, p11 = t1 * d1;
-    const float pmin = fminf(fminf(p00, p01), fminf(p10, p11)), pmax = fmaxf(fmaxf(p00, p01), fmaxf(p10, p11));
-    // rounded products: widen the range by 1e-6 of its magnitude so it holds every exact t d
-    const float slack = 1e-6f * fmaxf(fabsf(pmin), fabsf(pmax));
-    const float lo = x - (pmax + slack), hi = x - (pmin - slack);  // s ranges over [lo, hi]
-    return (lo > 0.f) ? lo : (hi < 0.f ? -hi : 0.f);
-}
-
-// The warp's list of hits within reach of the box B: hit k is kept unless, for every parameter
-// tuple in B, K ((x - tx d)^2 + (y - ty d)^2) > 128 (then every seed inside B has an ex2 argument
-// < -126, with room for fp32 rounding: w = +0 exactly); d = z - z_ref (SLOPE2) or z - z0 over the
-// box's z0 range (SLOPE3).  In hit order; returns the length.
-template <int MODEL, bool ZREF>
-__device__ __forceinline__ int mc_build_list(const float4 *h, int n, const McBox &B, float K, float zref,
-                                             uint16_t *list) {
-    const int lane = threadIdx.x & 31;
-    if (B.lo[0] > B.hi[0]) return 0;  // no valid seed in this warp
-    int L = 0;
-    for (int k0 = 0; k0 < n; k0 += 32) {
-        const int k = k0 + lane;
-        bool keep = false;
-        if (k < n) {
-            const float4 hk = h[k];
-            float d0, d1;  // the range of d, rounded outwards
-            if (MODEL == kSlope3) {
-                d0 = __fsub_rd(hk.z, B.hi[2]);
-                d1 = __fsub_ru(hk.z, B.lo[2]);
-            } else {
-                d0 = ZREF ? __fsub_rd(hk.z, zref) : hk.z;
-                d1 = ZREF ? __fsub_ru(hk.z, zref) : hk.z;
-            }
-            const float mx = mc_min_abs(hk.x, B.lo[0], B.hi[0], d0, d1);
-            const float my = mc_min_abs(hk.y, B.lo[1], B.hi[1], d0, d1);
-            keep = K * __fmaf_rn(mx, mx, my * my) * 0.99999f <= 128.f;
-        }
-        const unsigned b = __ballot_sync(0xffffffffu, keep);
-        if (keep) list[L + __popc(b & ((1u << lane) - 1u))] = (uint16_t)k;
-        L += __popc(b);
-    }
-    __syncwarp();
-    return L;
-}
-
+// ---------------------------------------------------------------- K4c (box bound and lists: cull.cuh)
 template <int MODEL, int S, bool ZREF>
 __global__ void __launch_bounds__(kMcThreads, RETINA_MC_MINB)
     multistart_culled_kernel(MultistartArgs a, const int32_t *perm, unsigned long long *pairs_evaluated,
@@ -812,14 +737,28 @@ bool multistart_culled_ok(int model, int n_seeds) {
     return (model == kSlope2 || model == kSlope3) && n_seeds > 0 && np2 <= 16384;  // 128 KB of (key, index)
 }
 
+cudaError_t launch_seed_morton_sort(const float *seeds, int n_seeds, int P, const float (&lo)[3], const float (&hi)[3],
+                                    int32_t *perm, int n_events, cudaStream_t stream) {
+    int np2 = 1;
+    while (np2 < n_seeds) np2 <<= 1;
+    const size_t sort_smem = (size_t)np2 * sizeof(unsigned long long);
+    cudaError_t err = ensure_dynamic_smem(seed_morton_sort_kernel, sort_smem);
+    if (err != cudaSuccess) return err;
+    const float3 l3 = make_float3(lo[0], lo[1], lo[2]), h3 = make_float3(hi[0], hi[1], hi[2]);
+    for (int e0 = 0; e0 < n_events; e0 += 65535) {
+        const int ne = std::min(65535, n_events - e0);
+        seed_morton_sort_kernel<<<ne, 1024, sort_smem, stream>>>(seeds, n_seeds, np2, P, l3, h3, perm, e0);
+        err = cudaGetLastError();
+        if (err != cudaSuccess) return err;
+    }
+    return cudaSuccess;
+}
+
 template <int MODEL, int S, bool ZREF>
 static cudaError_t launch_mc(const MultistartArgs &a0, int n_events, int32_t *perm, unsigned long long *pairs_evaluated,
                              cudaStream_t stream) {
     constexpr int P = (MODEL == kSlope3) ? 3 : 2;
-    int np2 = 1;
-    while (np2 < a0.n_seeds) np2 <<= 1;
-    const size_t sort_smem = (size_t)np2 * sizeof(unsigned long long);
-    cudaError_t err = ensure_dynamic_smem(seed_morton_sort_kernel, sort_smem);
+    cudaError_t err = launch_seed_morton_sort(a0.seeds, a0.n_seeds, P, a0.lo, a0.hi, perm, n_events, stream);
     if (err != cudaSuccess) return err;
     MultistartArgs a = a0;
     a.cap = ((std::max(a0.cap, 2) + 7) / 8) * 8;  // resident stage (events beyond it run dense)
@@ -833,12 +772,8 @@ static cudaError_t launch_mc(const MultistartArgs &a0, int n_events, int32_t *pe
     int upc = (int)std::min<long long>(kMcUnits, units_all / (3LL * 148 * RETINA_MC_MINB));
     upc = std::max(upc, kMcWarps);
     const int blocks = (a.n_seeds + upc * useeds - 1) / (upc * useeds);
-    const float3 lo = make_float3(a.lo[0], a.lo[1], a.lo[2]), hi = make_float3(a.hi[0], a.hi[1], a.hi[2]);
     for (int e0 = 0; e0 < n_events; e0 += 65535) {
         const int ne = std::min(65535, n_events - e0);
-        seed_morton_sort_kernel<<<ne, 1024, sort_smem, stream>>>(a.seeds, a.n_seeds, np2, P, lo, hi, perm, e0);
-        err = cudaGetLastError();
-        if (err != cudaSuccess) return err;
         a.e_base = e0;
         kern<<<dim3(blocks, ne), kMcThreads, smem, stream>>>(a, perm, pairs_evaluated, upc);
         err = cudaGetLastError();

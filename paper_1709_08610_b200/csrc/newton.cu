@@ -23,6 +23,9 @@
 //   H_z0z0 = c^2 (tx^2 sum wA^2 + 2 tx ty sum wAB + ty^2 sum wB^2) - c (tx^2 + ty^2) sum w.
 #include "common.cuh"
 #include "kernels.cuh"
+#include "cull.cuh"
+
+#include <algorithm>
 
 namespace retina {
 
@@ -36,9 +39,25 @@ struct HessSums {
     float sd2[6];  // weight d^2
 };
 
+// Visits the event's hits in order: all of them (streamed or resident), or only the resident hits
+// list[0 .. L) (K6c: the warp's list of hits within reach; a skipped hit would add exactly +0).
+template <class F>
+__device__ __forceinline__ void nt_visit(HitStage &st, const uint16_t *list, int L, F &&f) {
+    if (list != nullptr) {
+        const float4 *h = st.buf;
+#pragma unroll 2
+        for (int t = 0; t < L; ++t) f(h[list[t]]);
+    } else {
+        st.pass([&](const float4 *h, int len) {
+#pragma unroll 2
+            for (int k = 0; k < len; ++k) f(h[k]);
+        });
+    }
+}
+
 template <int MODEL, int S, bool ZREF>
 __device__ __forceinline__ void nt_pass_hess(HitStage &st, const float (&th)[S][3], float negK, float zref,
-                                             HessSums (&hs)[S]) {
+                                             HessSums (&hs)[S], const uint16_t *list = nullptr, int L = 0) {
 #pragma unroll
     for (int s = 0; s < S; ++s)
 #pragma unroll
@@ -60,44 +79,40 @@ __device__ __forceinline__ void nt_pass_hess(HitStage &st, const float (&th)[S][
             }
         }
     };
-    st.pass([&](const float4 *h, int len) {
-#pragma unroll 2
-        for (int k = 0; k < len; ++k) {
-            const float4 hk = h[k];
-            if (hk.z != zprev) {  // warp-uniform plane change
-                flush();
-                zprev = hk.z;
-#pragma unroll
-                for (int s = 0; s < S; ++s) {
-                    if (MODEL == kSlope3)
-                        two_sum(hk.z, -th[s][2], dh[s], dl[s]);
-                    else if (ZREF)
-                        two_sum(hk.z, -zref, dh[s], dl[s]);
-                    else {
-                        dh[s] = hk.z;
-                        dl[s] = 0.f;
-                    }
-                }
-            }
+    nt_visit(st, list, L, [&](const float4 hk) {
+        if (hk.z != zprev) {  // warp-uniform plane change
+            flush();
+            zprev = hk.z;
 #pragma unroll
             for (int s = 0; s < S; ++s) {
-                float A, B;
-                if (MODEL == kSlope3 || ZREF) {
-                    A = __fmaf_rn(-th[s][0], dl[s], __fmaf_rn(-th[s][0], dh[s], hk.x));
-                    B = __fmaf_rn(-th[s][1], dl[s], __fmaf_rn(-th[s][1], dh[s], hk.y));
-                } else {
-                    A = __fmaf_rn(-th[s][0], hk.z, hk.x);
-                    B = __fmaf_rn(-th[s][1], hk.z, hk.y);
+                if (MODEL == kSlope3)
+                    two_sum(hk.z, -th[s][2], dh[s], dl[s]);
+                else if (ZREF)
+                    two_sum(hk.z, -zref, dh[s], dl[s]);
+                else {
+                    dh[s] = hk.z;
+                    dl[s] = 0.f;
                 }
-                const float w = ex2_approx(__fmul_rn(__fmaf_rn(A, A, __fmul_rn(B, B)), negK));
-                const float wA = __fmul_rn(w, A), wB = __fmul_rn(w, B);
-                hs[s].p[0] = __fadd_rn(hs[s].p[0], w);
-                hs[s].p[1] = __fadd_rn(hs[s].p[1], wA);
-                hs[s].p[2] = __fadd_rn(hs[s].p[2], wB);
-                hs[s].p[3] = __fmaf_rn(wA, A, hs[s].p[3]);
-                hs[s].p[4] = __fmaf_rn(wA, B, hs[s].p[4]);
-                hs[s].p[5] = __fmaf_rn(wB, B, hs[s].p[5]);
             }
+        }
+#pragma unroll
+        for (int s = 0; s < S; ++s) {
+            float A, B;
+            if (MODEL == kSlope3 || ZREF) {
+                A = __fmaf_rn(-th[s][0], dl[s], __fmaf_rn(-th[s][0], dh[s], hk.x));
+                B = __fmaf_rn(-th[s][1], dl[s], __fmaf_rn(-th[s][1], dh[s], hk.y));
+            } else {
+                A = __fmaf_rn(-th[s][0], hk.z, hk.x);
+                B = __fmaf_rn(-th[s][1], hk.z, hk.y);
+            }
+            const float w = ex2_approx(__fmul_rn(__fmaf_rn(A, A, __fmul_rn(B, B)), negK));
+            const float wA = __fmul_rn(w, A), wB = __fmul_rn(w, B);
+            hs[s].p[0] = __fadd_rn(hs[s].p[0], w);
+            hs[s].p[1] = __fadd_rn(hs[s].p[1], wA);
+            hs[s].p[2] = __fadd_rn(hs[s].p[2], wB);
+            hs[s].p[3] = __fmaf_rn(wA, A, hs[s].p[3]);
+            hs[s].p[4] = __fmaf_rn(wA, B, hs[s].p[4]);
+            hs[s].p[5] = __fmaf_rn(wB, B, hs[s].p[5]);
         }
     });
     flush();
@@ -106,7 +121,7 @@ __device__ __forceinline__ void nt_pass_hess(HitStage &st, const float (&th)[S][
 // R only (line-search trials and the final pass); grad too when GRAD.
 template <int MODEL, int S, bool ZREF, bool GRAD>
 __device__ __forceinline__ void nt_pass_r(HitStage &st, const float (&th)[S][3], float negK, float zref,
-                                          float (&R)[S], float (&G)[S][4]) {
+                                          float (&R)[S], float (&G)[S][4], const uint16_t *list = nullptr, int L = 0) {
 #pragma unroll
     for (int s = 0; s < S; ++s) {
         R[s] = 0.f;
@@ -129,41 +144,37 @@ __device__ __forceinline__ void nt_pass_r(HitStage &st, const float (&th)[S][3],
             }
         }
     };
-    st.pass([&](const float4 *h, int len) {
-#pragma unroll 2
-        for (int k = 0; k < len; ++k) {
-            const float4 hk = h[k];
-            if (hk.z != zprev) {
-                flush();
-                zprev = hk.z;
-#pragma unroll
-                for (int s = 0; s < S; ++s) {
-                    if (MODEL == kSlope3)
-                        two_sum(hk.z, -th[s][2], dh[s], dl[s]);
-                    else if (ZREF)
-                        two_sum(hk.z, -zref, dh[s], dl[s]);
-                    else {
-                        dh[s] = hk.z;
-                        dl[s] = 0.f;
-                    }
-                }
-            }
+    nt_visit(st, list, L, [&](const float4 hk) {
+        if (hk.z != zprev) {
+            flush();
+            zprev = hk.z;
 #pragma unroll
             for (int s = 0; s < S; ++s) {
-                float A, B;
-                if (MODEL == kSlope3 || ZREF) {
-                    A = __fmaf_rn(-th[s][0], dl[s], __fmaf_rn(-th[s][0], dh[s], hk.x));
-                    B = __fmaf_rn(-th[s][1], dl[s], __fmaf_rn(-th[s][1], dh[s], hk.y));
-                } else {
-                    A = __fmaf_rn(-th[s][0], hk.z, hk.x);
-                    B = __fmaf_rn(-th[s][1], hk.z, hk.y);
+                if (MODEL == kSlope3)
+                    two_sum(hk.z, -th[s][2], dh[s], dl[s]);
+                else if (ZREF)
+                    two_sum(hk.z, -zref, dh[s], dl[s]);
+                else {
+                    dh[s] = hk.z;
+                    dl[s] = 0.f;
                 }
-                const float w = ex2_approx(__fmul_rn(__fmaf_rn(A, A, __fmul_rn(B, B)), negK));
-                R[s] = __fadd_rn(R[s], w);
-                if (GRAD) {
-                    qa[s] = __fmaf_rn(w, A, qa[s]);
-                    qb[s] = __fmaf_rn(w, B, qb[s]);
-                }
+            }
+        }
+#pragma unroll
+        for (int s = 0; s < S; ++s) {
+            float A, B;
+            if (MODEL == kSlope3 || ZREF) {
+                A = __fmaf_rn(-th[s][0], dl[s], __fmaf_rn(-th[s][0], dh[s], hk.x));
+                B = __fmaf_rn(-th[s][1], dl[s], __fmaf_rn(-th[s][1], dh[s], hk.y));
+            } else {
+                A = __fmaf_rn(-th[s][0], hk.z, hk.x);
+                B = __fmaf_rn(-th[s][1], hk.z, hk.y);
+            }
+            const float w = ex2_approx(__fmul_rn(__fmaf_rn(A, A, __fmul_rn(B, B)), negK));
+            R[s] = __fadd_rn(R[s], w);
+            if (GRAD) {
+                qa[s] = __fmaf_rn(w, A, qa[s]);
+                qb[s] = __fmaf_rn(w, B, qb[s]);
             }
         }
     });
@@ -175,7 +186,7 @@ __device__ __forceinline__ void nt_pass_r(HitStage &st, const float (&th)[S][3],
 // the results are bit-identical to nt_pass_hess / nt_pass_r with half the issue slots.
 template <int MODEL, int S, bool ZREF>
 __device__ __forceinline__ void nt_pass_hess_x2(HitStage &st, const float (&th)[S][3], float negK, float zref,
-                                                HessSums (&hs)[S]) {
+                                                HessSums (&hs)[S], const uint16_t *list = nullptr, int L = 0) {
     static_assert(S % 2 == 0, "seed pairs");
     constexpr int NP = S / 2;
     const float2 zero = make_float2(0.f, 0.f), nk = make_float2(negK, negK);
@@ -202,50 +213,46 @@ __device__ __forceinline__ void nt_pass_hess_x2(HitStage &st, const float (&th)[
             }
         }
     };
-    st.pass([&](const float4 *h, int len) {
-#pragma unroll 2
-        for (int k = 0; k < len; ++k) {
-            const float4 hk = h[k];
-            if (hk.z != zprev) {  // warp-uniform plane change
-                flush();
-                zprev = hk.z;
-#pragma unroll
-                for (int p = 0; p < NP; ++p) {
-                    if (MODEL == kSlope3) {
-                        two_sum(hk.z, -th[2 * p][2], dh[p].x, dl[p].x);
-                        two_sum(hk.z, -th[2 * p + 1][2], dh[p].y, dl[p].y);
-                    } else if (ZREF) {
-                        float hi, lo;
-                        two_sum(hk.z, -zref, hi, lo);
-                        dh[p] = make_float2(hi, hi);
-                        dl[p] = make_float2(lo, lo);
-                    } else {
-                        dh[p] = make_float2(hk.z, hk.z);
-                    }
-                }
-            }
-            const float2 X = make_float2(hk.x, hk.x), Y = make_float2(hk.y, hk.y);
+    nt_visit(st, list, L, [&](const float4 hk) {
+        if (hk.z != zprev) {  // warp-uniform plane change
+            flush();
+            zprev = hk.z;
 #pragma unroll
             for (int p = 0; p < NP; ++p) {
-                float2 A, B;
-                if (MODEL == kSlope3 || ZREF) {
-                    A = __ffma2_rn(mtx[p], dl[p], __ffma2_rn(mtx[p], dh[p], X));
-                    B = __ffma2_rn(mty[p], dl[p], __ffma2_rn(mty[p], dh[p], Y));
+                if (MODEL == kSlope3) {
+                    two_sum(hk.z, -th[2 * p][2], dh[p].x, dl[p].x);
+                    two_sum(hk.z, -th[2 * p + 1][2], dh[p].y, dl[p].y);
+                } else if (ZREF) {
+                    float hi, lo;
+                    two_sum(hk.z, -zref, hi, lo);
+                    dh[p] = make_float2(hi, hi);
+                    dl[p] = make_float2(lo, lo);
                 } else {
-                    const float2 Z = make_float2(hk.z, hk.z);
-                    A = __ffma2_rn(mtx[p], Z, X);
-                    B = __ffma2_rn(mty[p], Z, Y);
+                    dh[p] = make_float2(hk.z, hk.z);
                 }
-                const float2 a = __fmul2_rn(__ffma2_rn(A, A, __fmul2_rn(B, B)), nk);
-                const float2 w = make_float2(ex2_approx(a.x), ex2_approx(a.y));
-                const float2 wA = __fmul2_rn(w, A), wB = __fmul2_rn(w, B);
-                pp[p][0] = __fadd2_rn(pp[p][0], w);
-                pp[p][1] = __fadd2_rn(pp[p][1], wA);
-                pp[p][2] = __fadd2_rn(pp[p][2], wB);
-                pp[p][3] = __ffma2_rn(wA, A, pp[p][3]);
-                pp[p][4] = __ffma2_rn(wA, B, pp[p][4]);
-                pp[p][5] = __ffma2_rn(wB, B, pp[p][5]);
             }
+        }
+        const float2 X = make_float2(hk.x, hk.x), Y = make_float2(hk.y, hk.y);
+#pragma unroll
+        for (int p = 0; p < NP; ++p) {
+            float2 A, B;
+            if (MODEL == kSlope3 || ZREF) {
+                A = __ffma2_rn(mtx[p], dl[p], __ffma2_rn(mtx[p], dh[p], X));
+                B = __ffma2_rn(mty[p], dl[p], __ffma2_rn(mty[p], dh[p], Y));
+            } else {
+                const float2 Z = make_float2(hk.z, hk.z);
+                A = __ffma2_rn(mtx[p], Z, X);
+                B = __ffma2_rn(mty[p], Z, Y);
+            }
+            const float2 a = __fmul2_rn(__ffma2_rn(A, A, __fmul2_rn(B, B)), nk);
+            const float2 w = make_float2(ex2_approx(a.x), ex2_approx(a.y));
+            const float2 wA = __fmul2_rn(w, A), wB = __fmul2_rn(w, B);
+            pp[p][0] = __fadd2_rn(pp[p][0], w);
+            pp[p][1] = __fadd2_rn(pp[p][1], wA);
+            pp[p][2] = __fadd2_rn(pp[p][2], wB);
+            pp[p][3] = __ffma2_rn(wA, A, pp[p][3]);
+            pp[p][4] = __ffma2_rn(wA, B, pp[p][4]);
+            pp[p][5] = __ffma2_rn(wB, B, pp[p][5]);
         }
     });
     flush();
@@ -264,7 +271,7 @@ __device__ __forceinline__ void nt_pass_hess_x2(HitStage &st, const float (&th)[
 
 template <int MODEL, int S, bool ZREF, bool GRAD>
 __device__ __forceinline__ void nt_pass_r_x2(HitStage &st, const float (&th)[S][3], float negK, float zref,
-                                             float (&R)[S], float (&G)[S][4]) {
+                                             float (&R)[S], float (&G)[S][4], const uint16_t *list = nullptr, int L = 0) {
     static_assert(S % 2 == 0, "seed pairs");
     constexpr int NP = S / 2;
     const float2 zero = make_float2(0.f, 0.f), nk = make_float2(negK, negK);
@@ -290,47 +297,43 @@ __device__ __forceinline__ void nt_pass_r_x2(HitStage &st, const float (&th)[S][
             }
         }
     };
-    st.pass([&](const float4 *h, int len) {
-#pragma unroll 2
-        for (int k = 0; k < len; ++k) {
-            const float4 hk = h[k];
-            if (hk.z != zprev) {
-                flush();
-                zprev = hk.z;
-#pragma unroll
-                for (int p = 0; p < NP; ++p) {
-                    if (MODEL == kSlope3) {
-                        two_sum(hk.z, -th[2 * p][2], dh[p].x, dl[p].x);
-                        two_sum(hk.z, -th[2 * p + 1][2], dh[p].y, dl[p].y);
-                    } else if (ZREF) {
-                        float hi, lo;
-                        two_sum(hk.z, -zref, hi, lo);
-                        dh[p] = make_float2(hi, hi);
-                        dl[p] = make_float2(lo, lo);
-                    } else {
-                        dh[p] = make_float2(hk.z, hk.z);
-                    }
-                }
-            }
-            const float2 X = make_float2(hk.x, hk.x), Y = make_float2(hk.y, hk.y);
+    nt_visit(st, list, L, [&](const float4 hk) {
+        if (hk.z != zprev) {
+            flush();
+            zprev = hk.z;
 #pragma unroll
             for (int p = 0; p < NP; ++p) {
-                float2 A, B;
-                if (MODEL == kSlope3 || ZREF) {
-                    A = __ffma2_rn(mtx[p], dl[p], __ffma2_rn(mtx[p], dh[p], X));
-                    B = __ffma2_rn(mty[p], dl[p], __ffma2_rn(mty[p], dh[p], Y));
+                if (MODEL == kSlope3) {
+                    two_sum(hk.z, -th[2 * p][2], dh[p].x, dl[p].x);
+                    two_sum(hk.z, -th[2 * p + 1][2], dh[p].y, dl[p].y);
+                } else if (ZREF) {
+                    float hi, lo;
+                    two_sum(hk.z, -zref, hi, lo);
+                    dh[p] = make_float2(hi, hi);
+                    dl[p] = make_float2(lo, lo);
                 } else {
-                    const float2 Z = make_float2(hk.z, hk.z);
-                    A = __ffma2_rn(mtx[p], Z, X);
-                    B = __ffma2_rn(mty[p], Z, Y);
+                    dh[p] = make_float2(hk.z, hk.z);
                 }
-                const float2 a = __fmul2_rn(__ffma2_rn(A, A, __fmul2_rn(B, B)), nk);
-                const float2 w = make_float2(ex2_approx(a.x), ex2_approx(a.y));
-                r2[p] = __fadd2_rn(r2[p], w);
-                if (GRAD) {
-                    qa[p] = __ffma2_rn(w, A, qa[p]);
-                    qb[p] = __ffma2_rn(w, B, qb[p]);
-                }
+            }
+        }
+        const float2 X = make_float2(hk.x, hk.x), Y = make_float2(hk.y, hk.y);
+#pragma unroll
+        for (int p = 0; p < NP; ++p) {
+            float2 A, B;
+            if (MODEL == kSlope3 || ZREF) {
+                A = __ffma2_rn(mtx[p], dl[p], __ffma2_rn(mtx[p], dh[p], X));
+                B = __ffma2_rn(mty[p], dl[p], __ffma2_rn(mty[p], dh[p], Y));
+            } else {
+                const float2 Z = make_float2(hk.z, hk.z);
+                A = __ffma2_rn(mtx[p], Z, X);
+                B = __ffma2_rn(mty[p], Z, Y);
+            }
+            const float2 a = __fmul2_rn(__ffma2_rn(A, A, __fmul2_rn(B, B)), nk);
+            const float2 w = make_float2(ex2_approx(a.x), ex2_approx(a.y));
+            r2[p] = __fadd2_rn(r2[p], w);
+            if (GRAD) {
+                qa[p] = __ffma2_rn(w, A, qa[p]);
+                qb[p] = __ffma2_rn(w, B, qb[p]);
             }
         }
     });
@@ -439,11 +442,12 @@ struct LineSearchSmem {
 #define RETINA_NT_LSB 4  // halvings evaluated together per queue round (measured: C0 4.9 / 4.0 / 3.8 / 3.8 for 1 / 2 / 4 / 8)
 #endif
 constexpr int kNtLsBatch = RETINA_NT_LSB;
-template <int MODEL, int S, bool ZREF>
+template <int MODEL, int S, bool ZREF, bool CULL>
 __device__ __forceinline__ void nt_line_search_queue(HitStage &st, const NewtonArgs &a, float negK, float (&th)[S][3],
                                                      const float (&p)[S][3], const float (&R0)[S],
                                                      const float (&slope)[S], const bool (&active)[S], int (&nev)[S],
-                                                     float (&rcur)[S], LineSearchSmem<S, (MODEL == kSlope3) ? 3 : 2> &ls) {
+                                                     float (&rcur)[S], LineSearchSmem<S, (MODEL == kSlope3) ? 3 : 2> &ls,
+                                                     uint16_t *list, unsigned long long &evaluated) {
     constexpr int P = (MODEL == kSlope3) ? 3 : 2;
     constexpr int SQW = (MODEL == kSlope3) ? RETINA_NT3_SQ : RETINA_NT_SQ;
     constexpr int SQ = SQW < S ? SQW : S;
@@ -493,11 +497,26 @@ __device__ __forceinline__ void nt_line_search_queue(HitStage &st, const NewtonA
                                                a.hi[i])
                                        : 0.f;
             }
+            // K6c (list != nullptr): the hits within reach of this worker warp's trial points
+            int L = st.n;
+            if constexpr (CULL) {
+                bool okq[SQ];
+                int nv = 0;
+#pragma unroll
+                for (int s = 0; s < SQ; ++s) {
+                    okq[s] = slot[s] >= 0;
+                    nv += okq[s] ? 1 : 0;
+                }
+                nv = __reduce_add_sync(0xffffffffu, nv);
+                if (list != nullptr)
+                    L = mc_build_list<MODEL, ZREF>(st.buf, st.n, mc_warp_box<P, SQ>(tt, okq), -negK, a.z_ref, list);
+                evaluated += (unsigned long long)L * nv;
+            }
             float Rt[SQ], Gd[SQ][4];
             if constexpr (RETINA_NT_X2 && SQ % 2 == 0)
-                nt_pass_r_x2<MODEL, SQ, ZREF, false>(st, tt, negK, a.z_ref, Rt, Gd);
+                nt_pass_r_x2<MODEL, SQ, ZREF, false>(st, tt, negK, a.z_ref, Rt, Gd, list, L);
             else
-                nt_pass_r<MODEL, SQ, ZREF, false>(st, tt, negK, a.z_ref, Rt, Gd);
+                nt_pass_r<MODEL, SQ, ZREF, false>(st, tt, negK, a.z_ref, Rt, Gd, list, L);
 #pragma unroll
             for (int s = 0; s < SQ; ++s) {
                 if (slot[s] < 0) continue;
@@ -543,23 +562,64 @@ __device__ __forceinline__ void nt_line_search_queue(HitStage &st, const NewtonA
     }
 }
 
-template <int MODEL, int S, bool ZREF>
-__global__ void __launch_bounds__(kNtThreads, (MODEL == kSlope3) ? RETINA_NT3_MINB : RETINA_NT_MINB) newton_kernel(NewtonArgs a) {
-    extern __shared__ __align__(16) float4 s_hits[];
+// CULL (K6c, RETINA_MS_CULLED): the same per-seed arithmetic and decisions, bit for bit, with each
+// warp visiting only the hits within reach of its points (cull.cuh): the seeds are taken in the
+// per-event Morton order perm (a warp holds 32 S consecutive ones, so its points stay in a small
+// box), and every pass -- Hessian mode, the alpha = 1 trial, each line-search worker pass, the
+// final pass -- first lists, in hit order, the resident hits that a conservative bound keeps within
+// K s^2 <= 128 of the box of the points it evaluates.  Events larger than the stage run dense.
+// Both variants add the (seed, hit) pairs their passes evaluate for real seeds to pairs_evaluated.
+template <int MODEL, int S, bool ZREF, bool CULL>
+__global__ void __launch_bounds__(kNtThreads, (MODEL == kSlope3) ? RETINA_NT3_MINB : RETINA_NT_MINB)
+    newton_kernel(NewtonArgs a, const int32_t *perm, unsigned long long *pairs_evaluated) {
+    extern __shared__ __align__(16) float4 s_hits[];  // [cap] hits (K6c: then [warps][cap] uint16 lists)
     __shared__ __align__(8) uint64_t s_bar[2];
     constexpr int P = (MODEL == kSlope3) ? 3 : 2;
 
     const int e = a.e_base + blockIdx.y;
     const int start = a.offsets[e], nh = a.offsets[e + 1] - start;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     HitStage st;
     st.init(s_hits, s_bar, a.hits + start, nh, a.cap);
+    uint16_t *list = nullptr;  // this warp's list (K6c, resident events)
+    if constexpr (CULL) {
+        if (nh <= a.cap && nh <= 65535 && (nh == 0 || st.load_resident()))
+            list = reinterpret_cast<uint16_t *>(s_hits + a.cap) + warp * a.cap;
+    }
+    unsigned long long evaluated = 0;  // (seed, hit) pairs this warp's passes evaluate for real seeds
+    // the hits a pass over points pts (valid where ok) visits: the warp's list, or all of them
+    auto reach = [&](const float (&pts)[S][3], const bool (&ok)[S], float K) {
+        int L = nh;
+        if constexpr (CULL) {
+            int nv = 0;
+#pragma unroll
+            for (int s = 0; s < S; ++s) nv += ok[s] ? 1 : 0;
+            nv = __reduce_add_sync(0xffffffffu, nv);
+            if (list != nullptr)
+                L = mc_build_list<MODEL, ZREF>(st.buf, nh, mc_warp_box<P, S>(pts, ok), K, a.z_ref, list);
+            evaluated += (unsigned long long)L * nv;
+        }
+        return L;
+    };
 
-    int sid[S];
+    int sid[S];  // position in the CTA's seed range (K6c: in the Morton order)
+    bool valid[S];
     float th[S][3];
+    // the caller's index of seed s
+    auto orig = [&](int s) {
+        if constexpr (CULL)
+            return __ldg(perm + (int64_t)e * a.n_seeds + min(sid[s], a.n_seeds - 1));
+        else
+            return min(sid[s], a.n_seeds - 1);
+    };
 #pragma unroll
     for (int s = 0; s < S; ++s) {
-        sid[s] = blockIdx.x * (kNtThreads * S) + s * kNtThreads + threadIdx.x;
-        const int64_t src = ((int64_t)e * a.n_seeds + min(sid[s], a.n_seeds - 1)) * P;
+        if constexpr (CULL)
+            sid[s] = blockIdx.x * (kNtThreads * S) + warp * (32 * S) + s * 32 + lane;
+        else
+            sid[s] = blockIdx.x * (kNtThreads * S) + s * kNtThreads + threadIdx.x;
+        valid[s] = sid[s] < a.n_seeds;
+        const int64_t src = ((int64_t)e * a.n_seeds + orig(s)) * P;
 #pragma unroll
         for (int i = 0; i < 3; ++i) th[s][i] = (i < P) ? __ldg(a.seeds + src + i) : 0.f;
     }
@@ -576,10 +636,13 @@ __global__ void __launch_bounds__(kNtThreads, (MODEL == kSlope3) ? RETINA_NT3_MI
     }
     for (int j = 0; j < a.n_steps; ++j) {
         const float c = a.c2[j], negK = a.negK[j];
-        if constexpr (RETINA_NT_X2 && S % 2 == 0)
-            nt_pass_hess_x2<MODEL, S, ZREF>(st, th, negK, a.z_ref, hs);
-        else
-            nt_pass_hess<MODEL, S, ZREF>(st, th, negK, a.z_ref, hs);
+        {
+            const int L = reach(th, valid, -negK);
+            if constexpr (RETINA_NT_X2 && S % 2 == 0)
+                nt_pass_hess_x2<MODEL, S, ZREF>(st, th, negK, a.z_ref, hs, list, L);
+            else
+                nt_pass_hess<MODEL, S, ZREF>(st, th, negK, a.z_ref, hs, list, L);
+        }
         float R0[S], p[S][3], slope[S], tt[S][3];
         bool active[S];
 #pragma unroll
@@ -611,7 +674,7 @@ __global__ void __launch_bounds__(kNtThreads, (MODEL == kSlope3) ? RETINA_NT3_MI
             slope[s] = 0.f;
 #pragma unroll
             for (int i = 0; i < P; ++i) slope[s] = __fmaf_rn(g[i], p[s][i], slope[s]);
-            active[s] = sid[s] < a.n_seeds;
+            active[s] = valid[s];
         }
         // Trial alpha = 1 for every seed of the CTA (all owners pass over the hits together).
         // With the hits resident in shared memory, the seeds still searching after it are
@@ -634,10 +697,11 @@ __global__ void __launch_bounds__(kNtThreads, (MODEL == kSlope3) ? RETINA_NT3_MI
 #pragma unroll
             for (int s = 0; s < S; ++s) nev[s] += active[s] ? 1 : 0;
             float Rt[S], Gd[S][4];
+            const int L = reach(tt, active, -negK);
             if constexpr (RETINA_NT_X2 && S % 2 == 0)
-                nt_pass_r_x2<MODEL, S, ZREF, false>(st, tt, negK, a.z_ref, Rt, Gd);
+                nt_pass_r_x2<MODEL, S, ZREF, false>(st, tt, negK, a.z_ref, Rt, Gd, list, L);
             else
-                nt_pass_r<MODEL, S, ZREF, false>(st, tt, negK, a.z_ref, Rt, Gd);
+                nt_pass_r<MODEL, S, ZREF, false>(st, tt, negK, a.z_ref, Rt, Gd, list, L);
 #pragma unroll
             for (int s = 0; s < S; ++s) {
                 if (active[s] && Rt[s] >= __fmaf_rn(1e-4f * alpha, slope[s], R0[s])) {
@@ -649,14 +713,16 @@ __global__ void __launch_bounds__(kNtThreads, (MODEL == kSlope3) ? RETINA_NT3_MI
             }
         }
         if (st.resident && a.max_halvings > 0)
-            nt_line_search_queue<MODEL, S, ZREF>(st, a, negK, th, p, R0, slope, active, nev, Rcur, ls);
+            nt_line_search_queue<MODEL, S, ZREF, CULL>(st, a, negK, th, p, R0, slope, active, nev, Rcur, ls, list,
+                                                 evaluated);
     }
     float g[S][3];
     if (a.grad_out) {
+        const int L = reach(th, valid, -a.final_negK);
         if constexpr (RETINA_NT_X2 && S % 2 == 0)
-            nt_pass_r_x2<MODEL, S, ZREF, true>(st, th, a.final_negK, a.z_ref, R, G);
+            nt_pass_r_x2<MODEL, S, ZREF, true>(st, th, a.final_negK, a.z_ref, R, G, list, L);
         else
-            nt_pass_r<MODEL, S, ZREF, true>(st, th, a.final_negK, a.z_ref, R, G);
+            nt_pass_r<MODEL, S, ZREF, true>(st, th, a.final_negK, a.z_ref, R, G, list, L);
 #pragma unroll
         for (int s = 0; s < S; ++s) {
             g[s][0] = __fmul_rn(a.final_c2, G[s][0]);
@@ -672,15 +738,16 @@ __global__ void __launch_bounds__(kNtThreads, (MODEL == kSlope3) ? RETINA_NT3_MI
 #pragma unroll
         for (int s = 0; s < S; ++s) R[s] = Rcur[s];
     } else {
+        const int L = reach(th, valid, -a.final_negK);
         if constexpr (RETINA_NT_X2 && S % 2 == 0)
-            nt_pass_r_x2<MODEL, S, ZREF, false>(st, th, a.final_negK, a.z_ref, R, G);
+            nt_pass_r_x2<MODEL, S, ZREF, false>(st, th, a.final_negK, a.z_ref, R, G, list, L);
         else
-            nt_pass_r<MODEL, S, ZREF, false>(st, th, a.final_negK, a.z_ref, R, G);
+            nt_pass_r<MODEL, S, ZREF, false>(st, th, a.final_negK, a.z_ref, R, G, list, L);
     }
 #pragma unroll
     for (int s = 0; s < S; ++s) {
-        if (sid[s] < a.n_seeds) {
-            const int64_t o = (int64_t)e * a.n_seeds + sid[s];
+        if (valid[s]) {
+            const int64_t o = (int64_t)e * a.n_seeds + orig(s);
             a.R_out[o] = R[s];
             if (a.evals_out) a.evals_out[o] = nev[s];
 #pragma unroll
@@ -690,39 +757,61 @@ __global__ void __launch_bounds__(kNtThreads, (MODEL == kSlope3) ? RETINA_NT3_MI
             }
         }
     }
+    if constexpr (!CULL) {  // every evaluation visits every hit: evaluations x hits
+        int ne = 0;
+#pragma unroll
+        for (int s = 0; s < S; ++s) ne += valid[s] ? nev[s] : 0;
+        evaluated = (unsigned long long)__reduce_add_sync(0xffffffffu, ne) * nh;
+    }
+    if (pairs_evaluated && lane == 0 && evaluated) atomicAdd(pairs_evaluated, evaluated);
 }
 
 #ifndef RETINA_NT3_SEEDS
 #define RETINA_NT3_SEEDS 4  // SLOPE3 seeds per thread (2 with 5 CTAs/SM: cfg4 Newton 33.5 vs 30.2 ms per 200 events)
 #endif
-template <int MODEL, bool ZREF>
-static cudaError_t launch_nt(const NewtonArgs &a0, int n_events, cudaStream_t stream) {
+template <int MODEL, bool ZREF, bool CULL>
+static cudaError_t launch_nt(const NewtonArgs &a0, int n_events, const int32_t *perm,
+                             unsigned long long *pairs_evaluated, cudaStream_t stream) {
     constexpr int S = (MODEL == kSlope3) ? RETINA_NT3_SEEDS : 4;
-    auto kern = newton_kernel<MODEL, S, ZREF>;
-    const size_t smem = (size_t)a0.cap * sizeof(float4);
+    auto kern = newton_kernel<MODEL, S, ZREF, CULL>;
+    NewtonArgs a = a0;
+    if (CULL) a.cap = ((std::max(a0.cap, 2) + 7) / 8) * 8;  // 16-byte aligned lists after the stage
+    const size_t smem = (size_t)a.cap * (sizeof(float4) + (CULL ? (kNtThreads / 32) * sizeof(uint16_t) : 0));
     cudaError_t err = ensure_dynamic_smem(kern, smem);
     if (err != cudaSuccess) return err;
-    const int blocks = (a0.n_seeds + kNtThreads * S - 1) / (kNtThreads * S);
+    const int blocks = (a.n_seeds + kNtThreads * S - 1) / (kNtThreads * S);
     for (int e0 = 0; e0 < n_events; e0 += 65535) {
-        NewtonArgs a = a0;
         a.e_base = e0;
         const int ne = min(65535, n_events - e0);
-        kern<<<dim3(blocks, ne), kNtThreads, smem, stream>>>(a);
+        kern<<<dim3(blocks, ne), kNtThreads, smem, stream>>>(a, perm, pairs_evaluated);
         err = cudaGetLastError();
         if (err != cudaSuccess) return err;
     }
     return cudaSuccess;
 }
 
-cudaError_t launch_newton(int model, const NewtonArgs &a, int n_events, cudaStream_t stream) {
+cudaError_t launch_newton(int model, const NewtonArgs &a, int n_events, unsigned long long *pairs_evaluated,
+                          cudaStream_t stream) {
     if (n_events == 0 || a.n_seeds == 0) return cudaSuccess;
     switch (model) {
         case kSlope2:
-            return (a.z_ref == 0.f) ? launch_nt<kSlope2, false>(a, n_events, stream)
-                                    : launch_nt<kSlope2, true>(a, n_events, stream);
-        case kSlope3: return launch_nt<kSlope3, false>(a, n_events, stream);
+            return (a.z_ref == 0.f) ? launch_nt<kSlope2, false, false>(a, n_events, nullptr, pairs_evaluated, stream)
+                                    : launch_nt<kSlope2, true, false>(a, n_events, nullptr, pairs_evaluated, stream);
+        case kSlope3: return launch_nt<kSlope3, false, false>(a, n_events, nullptr, pairs_evaluated, stream);
     }
     return cudaErrorInvalidValue;
+}
+
+cudaError_t launch_newton_culled(int model, const NewtonArgs &a, int n_events, int32_t *perm,
+                                 unsigned long long *pairs_evaluated, cudaStream_t stream) {
+    if (n_events == 0 || a.n_seeds == 0) return cudaSuccess;
+    const int P = (model == kSlope3) ? 3 : 2;
+    if (model != kSlope2 && model != kSlope3) return cudaErrorInvalidValue;
+    cudaError_t err = launch_seed_morton_sort(a.seeds, a.n_seeds, P, a.lo, a.hi, perm, n_events, stream);
+    if (err != cudaSuccess) return err;
+    if (model == kSlope3) return launch_nt<kSlope3, false, true>(a, n_events, perm, pairs_evaluated, stream);
+    return (a.z_ref == 0.f) ? launch_nt<kSlope2, false, true>(a, n_events, perm, pairs_evaluated, stream)
+                            : launch_nt<kSlope2, true, true>(a, n_events, perm, pairs_evaluated, stream);
 }
 
 }  // namespace retina

@@ -102,9 +102,10 @@ class RetinaPipeline:
         self.resp = torch.empty((E, S), dtype=torch.float32, device=self.device)
         # Newton path: response evaluations per seed (the paper's cost unit), counted by the kernel
         self.evals = torch.empty((E, S), dtype=torch.int32, device=self.device) if spec.newton is not None else None
-        # culled fixed-step path: the per-event seed permutation (workspace) and the evaluated-pair count
+        # culled multi-start (fixed step or Newton): the per-event seed permutation (workspace) and the
+        # evaluated-pair count
         self.ms_ws = self.pairs_ev = None
-        if spec.newton is None and spec.ms_algorithm == R.MS_CULLED and S:
+        if spec.ms_algorithm == R.MS_CULLED and S:
             nb = R.multistart_workspace_size(E, S, spec.ms_algorithm)
             self.ms_ws = torch.empty((max(nb, 4) // 4,), dtype=torch.int32, device=self.device)
             self.pairs_ev = torch.zeros((1,), dtype=torch.int64, device=self.device)
@@ -129,12 +130,12 @@ class RetinaPipeline:
         grid = float(n.sum()) * self.spec.cells
         if self.grid_pairs_ev is not None:  # the pairs the culled grid contracted in the counted run
             grid = float(self.grid_pairs_ev.item())
+        if self.pairs_ev is not None:  # the pairs the culled kernel evaluated in the counted run
+            return grid, float(self.pairs_ev.item())
         if self.spec.newton is not None:
             E = batch.n_events
             ev = self.evals[:E].to(torch.float64).sum(dim=1).cpu().numpy()
             return grid, float((n * ev).sum())
-        if self.pairs_ev is not None:  # the pairs the culled kernel evaluated in the counted run
-            return grid, float(self.pairs_ev.item())
         ms = float(n.sum()) * self.spec.n_seeds * (self.spec.n_iters + 1)
         return grid, ms
 
@@ -195,7 +196,8 @@ class RetinaPipeline:
             sig, eta, fsig, mh = sp.newton
             R.retina_multistart_newton_ex(ev, sp.model, batch.seeds, sig, eta, fsig, mh, sp.box_lo, sp.box_hi,
                                           want_grad=False, out=(self.theta[:E], self.resp[:E], None, self.evals[:E]),
-                                          stream=stream)
+                                          stream=stream, algorithm=sp.ms_algorithm, workspace=self.ms_ws,
+                                          pairs_evaluated=self.pairs_ev if self.count_pairs else None)
         else:  # BASELINE configs[2..4]: fixed-step gradient ascent
             R.retina_multistart_optimize(ev, sp.model, sp.sigma_ms or sp.sigma, batch.seeds, sp.n_iters, sp.step,
                                          sp.box_lo, sp.box_hi, want_grad=False,

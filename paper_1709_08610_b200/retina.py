@@ -27,7 +27,7 @@ EXPORTED = ("retina_grid_response", "retina_grid_response_ex", "retina_grid_resp
             "retina_find_peaks",
             "retina_find_peaks_ws", "retina_find_peaks_workspace_size",
             "retina_multistart_optimize", "retina_multistart_optimize_ex", "retina_multistart_workspace_size",
-            "retina_multistart_newton", "retina_multistart_newton_ex",
+            "retina_multistart_newton", "retina_multistart_newton_ex", "retina_multistart_newton_ex2",
             "retina_merge_tracks", "retina_pack_results",
             "retina_status_string", "retina_last_error", "retina_version")
 PACK_HEADER = 8
@@ -85,11 +85,14 @@ def lib() -> ctypes.CDLL:
                                                f32, i32, vp, vp, vp, vp, vp, vp]
         L.retina_multistart_newton_ex.argtypes = [ctypes.POINTER(retina_events), ctypes.c_int, i32, vp, i32, vp,
                                                   vp, f32, i32, vp, vp, vp, vp, vp, vp, vp]
+        L.retina_multistart_newton_ex2.argtypes = [ctypes.POINTER(retina_events), ctypes.c_int, i32, vp, i32, vp,
+                                                   vp, f32, i32, vp, vp, vp, vp, vp, vp, ctypes.c_int, vp,
+                                                   ctypes.c_size_t, vp, vp]
         L.retina_merge_tracks.argtypes = [i32, i32, i32, vp, vp, vp, f32, i32, vp, vp, vp, vp, vp, vp]
         L.retina_pack_results.argtypes = [i32, i32, i32, vp, vp, vp, i32, vp, vp, vp, vp, i32, vp, vp, vp]
         for f in (L.retina_grid_response, L.retina_grid_response_ex, L.retina_find_peaks, L.retina_estimate_peaks,
                   L.retina_multistart_optimize, L.retina_multistart_optimize_ex, L.retina_multistart_newton,
-                  L.retina_multistart_newton_ex,
+                  L.retina_multistart_newton_ex, L.retina_multistart_newton_ex2,
                   L.retina_merge_tracks, L.retina_pack_results):
             f.restype = ctypes.c_int
         L.retina_status_string.argtypes = [ctypes.c_int]
@@ -331,15 +334,20 @@ def retina_multistart_newton(events: Events, model: int, seeds: torch.Tensor, si
 
 
 def retina_multistart_newton_ex(events: Events, model: int, seeds: torch.Tensor, sigmas, etas, final_sigma: float,
-                                max_halvings: int, box_lo, box_hi, want_grad: bool = True, out=None, stream=None):
+                                max_halvings: int, box_lo, box_hi, want_grad: bool = True, out=None, stream=None,
+                                algorithm: int = MS_DENSE, workspace: Optional[torch.Tensor] = None,
+                                pairs_evaluated: Optional[torch.Tensor] = None):
     """As retina_multistart_newton, plus the per-seed response-evaluation counts (int32 [E, S]):
-    (theta_out, response_out, grad_out or None, evals_out)."""
+    (theta_out, response_out, grad_out or None, evals_out).  algorithm=MS_CULLED (or a
+    pairs_evaluated int64 [1] device tensor) goes through retina_multistart_newton_ex2: the same
+    results bit for bit, each warp visiting only the hits that can contribute (a workspace is
+    allocated if none is passed)."""
     return _newton(True, events, model, seeds, sigmas, etas, final_sigma, max_halvings, box_lo, box_hi, want_grad,
-                   out, stream)
+                   out, stream, algorithm, workspace, pairs_evaluated)
 
 
 def _newton(ex, events, model, seeds, sigmas, etas, final_sigma, max_halvings, box_lo, box_hi, want_grad, out,
-            stream):
+            stream, algorithm=MS_DENSE, workspace=None, pairs_evaluated=None):
     P = MODEL_P[model]
     _dev(seeds, torch.float32)
     E, S, Ps = seeds.shape
@@ -361,6 +369,24 @@ def _newton(ex, events, model, seeds, sigmas, etas, final_sigma, max_halvings, b
         ne = out[3] if len(out) > 3 and out[3] is not None else torch.empty((E, S), dtype=torch.int32,
                                                                            device=seeds.device)
         _out("evals_out", ne, torch.int32, (E, S), seeds.device)
+        if algorithm != MS_DENSE or workspace is not None or pairs_evaluated is not None:
+            if algorithm == MS_CULLED and workspace is None:
+                nbytes = multistart_workspace_size(E, S, algorithm)
+                workspace = torch.empty((max(nbytes, 4) // 4,), dtype=torch.int32, device=seeds.device)
+            nbytes = 0
+            if workspace is not None:
+                _dev(workspace, workspace.dtype)
+                if workspace.device != seeds.device:
+                    raise ValueError("workspace on another device")
+                nbytes = workspace.numel() * workspace.element_size()
+            if pairs_evaluated is not None:
+                _out("pairs_evaluated", pairs_evaluated, torch.int64, (1,), seeds.device)
+            _check("retina_multistart_newton_ex2",
+                   lib().retina_multistart_newton_ex2(ctypes.byref(events.c), model, S, _ptr(seeds), len(sigmas), sg,
+                                                      et, float(final_sigma), int(max_halvings), lo, hi, _ptr(th),
+                                                      _ptr(R), _ptr(g), _ptr(ne), int(algorithm), _ptr(workspace),
+                                                      ctypes.c_size_t(nbytes), _ptr(pairs_evaluated), _stream(stream)))
+            return th, R, g, ne
         _check("retina_multistart_newton_ex",
                lib().retina_multistart_newton_ex(ctypes.byref(events.c), model, S, _ptr(seeds), len(sigmas), sg, et,
                                                  float(final_sigma), int(max_halvings), lo, hi, _ptr(th), _ptr(R),

@@ -740,6 +740,65 @@ def test_newton_identities():
     assert torch.allclose(Rn, R2, rtol=2e-6, atol=1e-6)
 
 
+@pytest.mark.parametrize("name,n_ev,n_seeds,z_ref,want_grad,hint,halvings", [
+    ("cfg2", 3, 4096, 0.0, True, None, None), ("cfg2", 3, 1000, 23.5, False, None, None),
+    ("cfg3", 2, 8192, 0.0, False, None, None),  # the bench's --update newton launch configuration
+    ("cfg3", 2, 2048, 0.0, True, None, 30), ("cfg2", 3, 777, 0.0, True, 64, None),  # hint 64: events run dense
+    ("cfg4", 1, 16384, 0.0, False, None, None), ("cfg4", 2, 2000, 0.0, True, None, None)])  # SLOPE3
+def test_newton_culled_bitwise_equal_to_dense(name, n_ev, n_seeds, z_ref, want_grad, hint, halvings):
+    """K6c (retina_multistart_newton_ex2, RETINA_MS_CULLED) skips only pairs whose ex2.approx.ftz
+    weight is exactly +0 (Hessian-mode, line-search and final passes) and keeps every decision:
+    theta, R, grad R and the per-seed evaluation counts equal the dense kernel's bit for bit; it
+    evaluates fewer pairs than the dense count (evaluations x hits)."""
+    cfg = C.CONFIGS[name]
+    ev_ids = list(range(n_ev))
+    b = G.make_batch(cfg, ev_ids)
+    off = np.concatenate([b.offsets, [b.offsets[-1], b.offsets[-1] + 1]]).astype(np.int32)  # + empty, one hit
+    hits = np.concatenate([b.hits, b.hits[:1]])
+    seeds = np.concatenate([G.make_seeds(cfg, ev_ids, n_seeds=n_seeds), G.make_seeds(cfg, [0, 1], n_seeds=n_seeds)])
+    ev = R.Events.from_numpy(off, hits, z_ref=z_ref, max_event_hits=hint)
+    sig, eta, fsig, mh = C.newton_schedule(cfg)
+    if halvings is not None:
+        mh = halvings
+    pd = torch.zeros(1, dtype=torch.int64, device=DEV)
+    pc = torch.zeros(1, dtype=torch.int64, device=DEV)
+    dense = R.retina_multistart_newton_ex(ev, cfg.model, dev(seeds), sig, eta, fsig, mh, cfg.box_lo, cfg.box_hi,
+                                          want_grad=want_grad, pairs_evaluated=pd)
+    culled = R.retina_multistart_newton_ex(ev, cfg.model, dev(seeds), sig, eta, fsig, mh, cfg.box_lo, cfg.box_hi,
+                                           want_grad=want_grad, algorithm=R.retina.MS_CULLED, pairs_evaluated=pc)
+    plain = R.retina_multistart_newton_ex(ev, cfg.model, dev(seeds), sig, eta, fsig, mh, cfg.box_lo, cfg.box_hi,
+                                          want_grad=want_grad)
+    torch.cuda.synchronize()
+    for x, y, z in zip(plain, dense, culled):
+        if x is None:
+            assert y is None and z is None
+            continue
+        assert torch.equal(x, y)
+        assert torch.equal(x.view(torch.int32), z.view(torch.int32))  # bit for bit, signs of zeros included
+    n_hits = np.diff(off).astype(np.int64)
+    total = int((plain[3].cpu().numpy().astype(np.int64) * n_hits[:, None]).sum())
+    assert int(pd.item()) == total
+    n_pc = int(pc.item())
+    assert n_pc > 0
+    if hint is None:
+        assert n_pc < total
+    PU.report(f"K6c {name} S={n_seeds}", pairs_dense=total, pairs_evaluated=n_pc, evaluated_frac=n_pc / total)
+
+
+def test_newton_culled_unsupported_and_workspace():
+    c2 = C.CFG2
+    b2 = G.make_batch(c2, [0])
+    s2 = dev(G.make_seeds(c2, [0], n_seeds=32))
+    sig, eta, fsig, mh = C.newton_schedule(c2)
+    ws = torch.empty(1, dtype=torch.int32, device=DEV)  # 4 bytes: too small for 32 seeds
+    with pytest.raises(R.retina.RetinaError):
+        R.retina_multistart_newton_ex(events_of(b2), c2.model, s2, sig, eta, fsig, mh, c2.box_lo, c2.box_hi,
+                                      algorithm=R.retina.MS_CULLED, workspace=ws)
+    with pytest.raises(R.retina.RetinaError):  # unknown algorithm
+        R.retina_multistart_newton_ex(events_of(b2), c2.model, s2, sig, eta, fsig, mh, c2.box_lo, c2.box_hi,
+                                      algorithm=5)
+
+
 # --------------------------------------------------------------------------- tensor-core grid (SLOPE3)
 @pytest.mark.parametrize("shape", [(5, 37, 45), (3, 70, 33), (130, 260, 3)])
 @pytest.mark.parametrize("hint", [True, False])

@@ -98,7 +98,7 @@ def main():
             med, mn = timeit(run_peaks)
             byts = 4.0 * cfg.n_units * chunk * n_chunks
             emit("peaks", med, mn, grid_bytes=byts, gbs=byts / (med * 1e-3) / 1e9, frac_hbm=byts / (med * 1e-3) / 6550.7e9)
-    if "ms" in phases or "newton" in phases or "culled" in phases:
+    if "ms" in phases or "newton" in phases or "culled" in phases or "newton_culled" in phases:
         seeds = torch.from_numpy(G.make_seeds(cfg, ev_ids)).cuda()
         th = torch.empty_like(seeds)
         Rr = torch.empty(seeds.shape[:2], device="cuda")
@@ -138,6 +138,26 @@ def main():
             pairs = float((np.diff(b.offsets).astype(np.float64) * nev).sum())
             emit("newton", med, mn, pairs=pairs, frac_mufu=pairs / (med * 1e-3) / MUFU,
                  evals_per_seed=float(nev.sum() / ne.numel()))
+        if "newton_culled" in phases:  # K6c: the same results, only the pairs that can contribute
+            sig, eta, fsig, mh = C.newton_schedule(cfg)
+            ne = torch.empty(seeds.shape[:2], dtype=torch.int32, device="cuda")
+            ws = torch.empty((RT.multistart_workspace_size(len(ev_ids), cfg.n_seeds) // 4 + 1,), dtype=torch.int32,
+                             device="cuda")
+            pc = torch.zeros(1, dtype=torch.int64, device="cuda")
+
+            def run_ntc():
+                R.retina_multistart_newton_ex(ev, cfg.model, seeds, sig, eta, fsig, mh, cfg.box_lo, cfg.box_hi,
+                                              want_grad=False, out=(th, Rr, None, ne), algorithm=RT.MS_CULLED,
+                                              workspace=ws, pairs_evaluated=pc)
+            med, mn = timeit(run_ntc)
+            pc.zero_()
+            run_ntc()
+            torch.cuda.synchronize()
+            nev = ne.to(torch.float64).sum(dim=1).cpu().numpy()
+            pairs = float((np.diff(b.offsets).astype(np.float64) * nev).sum())
+            ev_pairs = float(pc.item())
+            emit("newton_culled", med, mn, pairs=pairs, pairs_evaluated=ev_pairs, evaluated_frac=ev_pairs / pairs,
+                 frac_mufu_evaluated=ev_pairs / (med * 1e-3) / MUFU, events_per_s=len(ev_ids) / (med * 1e-3))
 
 
 if __name__ == "__main__":
