@@ -56,13 +56,14 @@ __device__ __forceinline__ float mc_min_abs(float x, float t0, float t1, float d
 // tuple in B, K ((x - tx d)^2 + (y - ty d)^2) > 128 (then every seed inside B has an ex2 argument
 // < -126, with room for fp32 rounding: w = +0 exactly); d = z - z_ref (SLOPE2) or z - z0 over the
 // box's z0 range (SLOPE3).  In hit order; returns the length.
+// (mc_build_list_range: the hits kb .. n - 1 only.)
 template <int MODEL, bool ZREF>
-__device__ __forceinline__ int mc_build_list(const float4 *h, int n, const McBox &B, float K, float zref,
-                                             uint16_t *list) {
+__device__ __forceinline__ int mc_build_list_range(const float4 *h, int kb, int n, const McBox &B, float K, float zref,
+                                                   uint16_t *list) {
     const int lane = threadIdx.x & 31;
     if (B.lo[0] > B.hi[0]) return 0;  // no valid seed in this warp
     int L = 0;
-    for (int k0 = 0; k0 < n; k0 += 32) {
+    for (int k0 = kb; k0 < n; k0 += 32) {
         const int k = k0 + lane;
         bool keep = false;
         if (k < n) {
@@ -85,6 +86,12 @@ __device__ __forceinline__ int mc_build_list(const float4 *h, int n, const McBox
     }
     __syncwarp();
     return L;
+}
+
+template <int MODEL, bool ZREF>
+__device__ __forceinline__ int mc_build_list(const float4 *h, int n, const McBox &B, float K, float zref,
+                                             uint16_t *list) {
+    return mc_build_list_range<MODEL, ZREF>(h, 0, n, B, K, zref, list);
 }
 
 }  // namespace retina

@@ -39,25 +39,48 @@ struct HessSums {
     float sd2[6];  // weight d^2
 };
 
-// Visits the event's hits in order: all of them (streamed or resident), or only the resident hits
-// list[0 .. L) (K6c: the warp's list of hits within reach; a skipped hit would add exactly +0).
-template <class F>
-__device__ __forceinline__ void nt_visit(HitStage &st, const uint16_t *list, int L, F &&f) {
-    if (list != nullptr) {
+// K6c: a pass restricted to the resident hits within reach of the box of the warp's points (cull.cuh):
+// the hits are listed kNtChunk at a time into the warp's list buffer, each chunk's list consumed in
+// hit order before the next is built; visited counts the listed hits.
+constexpr int kNtChunk = 256;
+#ifndef RETINA_NT_CULL_KEEP
+#define RETINA_NT_CULL_KEEP 0.6f  // a step's trial passes are listed only if its Hessian pass kept <= this share
+#endif
+constexpr float kNtCullKeep = RETINA_NT_CULL_KEEP;
+struct NtReach {
+    McBox box;
+    float K;         // 1 / sigma^2 of the pass
+    uint16_t *list;  // the warp's kNtChunk-entry buffer; nullptr: every hit (dense pass)
+};
+
+// Visits the event's hits in order: all of them (streamed or resident), or (rc.list != nullptr) only
+// the resident hits within reach -- a skipped hit would add exactly +0.  Returns the hits visited.
+template <int MODEL, bool ZREF, class F>
+__device__ __forceinline__ int nt_visit(HitStage &st, const NtReach &rc, float zref, F &&f) {
+    if (rc.list != nullptr) {
         const float4 *h = st.buf;
+        int visited = 0;
+        for (int k0 = 0; k0 < st.n; k0 += kNtChunk) {
+            const int L = mc_build_list_range<MODEL, ZREF>(h, k0, min(st.n, k0 + kNtChunk), rc.box, rc.K, zref,
+                                                           rc.list);
+            visited += L;
 #pragma unroll 2
-        for (int t = 0; t < L; ++t) f(h[list[t]]);
+            for (int t = 0; t < L; ++t) f(h[rc.list[t]]);
+            __syncwarp();  // the list is rebuilt next
+        }
+        return visited;
     } else {
         st.pass([&](const float4 *h, int len) {
 #pragma unroll 2
             for (int k = 0; k < len; ++k) f(h[k]);
         });
+        return st.n;
     }
 }
 
 template <int MODEL, int S, bool ZREF>
-__device__ __forceinline__ void nt_pass_hess(HitStage &st, const float (&th)[S][3], float negK, float zref,
-                                             HessSums (&hs)[S], const uint16_t *list = nullptr, int L = 0) {
+__device__ __forceinline__ int nt_pass_hess(HitStage &st, const float (&th)[S][3], float negK, float zref,
+                                             HessSums (&hs)[S], const NtReach &rc = NtReach{{}, 0.f, nullptr}) {
 #pragma unroll
     for (int s = 0; s < S; ++s)
 #pragma unroll
@@ -79,7 +102,7 @@ __device__ __forceinline__ void nt_pass_hess(HitStage &st, const float (&th)[S][
             }
         }
     };
-    nt_visit(st, list, L, [&](const float4 hk) {
+    const int visited = nt_visit<MODEL, ZREF>(st, rc, zref, [&](const float4 hk) {
         if (hk.z != zprev) {  // warp-uniform plane change
             flush();
             zprev = hk.z;
@@ -116,12 +139,13 @@ __device__ __forceinline__ void nt_pass_hess(HitStage &st, const float (&th)[S][
         }
     });
     flush();
+    return visited;
 }
 
 // R only (line-search trials and the final pass); grad too when GRAD.
 template <int MODEL, int S, bool ZREF, bool GRAD>
-__device__ __forceinline__ void nt_pass_r(HitStage &st, const float (&th)[S][3], float negK, float zref,
-                                          float (&R)[S], float (&G)[S][4], const uint16_t *list = nullptr, int L = 0) {
+__device__ __forceinline__ int nt_pass_r(HitStage &st, const float (&th)[S][3], float negK, float zref,
+                                          float (&R)[S], float (&G)[S][4], const NtReach &rc = NtReach{{}, 0.f, nullptr}) {
 #pragma unroll
     for (int s = 0; s < S; ++s) {
         R[s] = 0.f;
@@ -144,7 +168,7 @@ __device__ __forceinline__ void nt_pass_r(HitStage &st, const float (&th)[S][3],
             }
         }
     };
-    nt_visit(st, list, L, [&](const float4 hk) {
+    const int visited = nt_visit<MODEL, ZREF>(st, rc, zref, [&](const float4 hk) {
         if (hk.z != zprev) {
             flush();
             zprev = hk.z;
@@ -179,14 +203,15 @@ __device__ __forceinline__ void nt_pass_r(HitStage &st, const float (&th)[S][3],
         }
     });
     flush();
+    return visited;
 }
 
 // Packed variants of the two passes above for seed PAIRS (FFMA2 / FMUL2 / FADD2): the same
 // operation sequence per seed, each half an independent IEEE round-to-nearest operation, so
 // the results are bit-identical to nt_pass_hess / nt_pass_r with half the issue slots.
 template <int MODEL, int S, bool ZREF>
-__device__ __forceinline__ void nt_pass_hess_x2(HitStage &st, const float (&th)[S][3], float negK, float zref,
-                                                HessSums (&hs)[S], const uint16_t *list = nullptr, int L = 0) {
+__device__ __forceinline__ int nt_pass_hess_x2(HitStage &st, const float (&th)[S][3], float negK, float zref,
+                                                HessSums (&hs)[S], const NtReach &rc = NtReach{{}, 0.f, nullptr}) {
     static_assert(S % 2 == 0, "seed pairs");
     constexpr int NP = S / 2;
     const float2 zero = make_float2(0.f, 0.f), nk = make_float2(negK, negK);
@@ -213,7 +238,7 @@ __device__ __forceinline__ void nt_pass_hess_x2(HitStage &st, const float (&th)[
             }
         }
     };
-    nt_visit(st, list, L, [&](const float4 hk) {
+    const int visited = nt_visit<MODEL, ZREF>(st, rc, zref, [&](const float4 hk) {
         if (hk.z != zprev) {  // warp-uniform plane change
             flush();
             zprev = hk.z;
@@ -267,11 +292,12 @@ __device__ __forceinline__ void nt_pass_hess_x2(HitStage &st, const float (&th)[
             hs[2 * p].sd2[q] = sd2[p][q].x;
             hs[2 * p + 1].sd2[q] = sd2[p][q].y;
         }
+    return visited;
 }
 
 template <int MODEL, int S, bool ZREF, bool GRAD>
-__device__ __forceinline__ void nt_pass_r_x2(HitStage &st, const float (&th)[S][3], float negK, float zref,
-                                             float (&R)[S], float (&G)[S][4], const uint16_t *list = nullptr, int L = 0) {
+__device__ __forceinline__ int nt_pass_r_x2(HitStage &st, const float (&th)[S][3], float negK, float zref,
+                                             float (&R)[S], float (&G)[S][4], const NtReach &rc = NtReach{{}, 0.f, nullptr}) {
     static_assert(S % 2 == 0, "seed pairs");
     constexpr int NP = S / 2;
     const float2 zero = make_float2(0.f, 0.f), nk = make_float2(negK, negK);
@@ -297,7 +323,7 @@ __device__ __forceinline__ void nt_pass_r_x2(HitStage &st, const float (&th)[S][
             }
         }
     };
-    nt_visit(st, list, L, [&](const float4 hk) {
+    const int visited = nt_visit<MODEL, ZREF>(st, rc, zref, [&](const float4 hk) {
         if (hk.z != zprev) {
             flush();
             zprev = hk.z;
@@ -348,6 +374,7 @@ __device__ __forceinline__ void nt_pass_r_x2(HitStage &st, const float (&th)[S][
             G[2 * p + 1][q] = g[p][q].y;
         }
     }
+    return visited;
 }
 
 #ifndef RETINA_NT_MINB
@@ -447,7 +474,8 @@ __device__ __forceinline__ void nt_line_search_queue(HitStage &st, const NewtonA
                                                      const float (&p)[S][3], const float (&R0)[S],
                                                      const float (&slope)[S], const bool (&active)[S], int (&nev)[S],
                                                      float (&rcur)[S], LineSearchSmem<S, (MODEL == kSlope3) ? 3 : 2> &ls,
-                                                     uint16_t *list, unsigned long long &evaluated) {
+                                                     uint16_t *list, const bool cull_step,
+                                                     unsigned long long &evaluated) {
     constexpr int P = (MODEL == kSlope3) ? 3 : 2;
     constexpr int SQW = (MODEL == kSlope3) ? RETINA_NT3_SQ : RETINA_NT_SQ;
     constexpr int SQ = SQW < S ? SQW : S;
@@ -498,25 +526,25 @@ __device__ __forceinline__ void nt_line_search_queue(HitStage &st, const NewtonA
                                        : 0.f;
             }
             // K6c (list != nullptr): the hits within reach of this worker warp's trial points
-            int L = st.n;
+            NtReach rq{{}, 0.f, nullptr};
+            int nv = 0;
             if constexpr (CULL) {
                 bool okq[SQ];
-                int nv = 0;
 #pragma unroll
                 for (int s = 0; s < SQ; ++s) {
                     okq[s] = slot[s] >= 0;
                     nv += okq[s] ? 1 : 0;
                 }
                 nv = __reduce_add_sync(0xffffffffu, nv);
-                if (list != nullptr)
-                    L = mc_build_list<MODEL, ZREF>(st.buf, st.n, mc_warp_box<P, SQ>(tt, okq), -negK, a.z_ref, list);
-                evaluated += (unsigned long long)L * nv;
+                if (cull_step) rq = NtReach{mc_warp_box<P, SQ>(tt, okq), -negK, list};
             }
             float Rt[SQ], Gd[SQ][4];
+            int vis;
             if constexpr (RETINA_NT_X2 && SQ % 2 == 0)
-                nt_pass_r_x2<MODEL, SQ, ZREF, false>(st, tt, negK, a.z_ref, Rt, Gd, list, L);
+                vis = nt_pass_r_x2<MODEL, SQ, ZREF, false>(st, tt, negK, a.z_ref, Rt, Gd, rq);
             else
-                nt_pass_r<MODEL, SQ, ZREF, false>(st, tt, negK, a.z_ref, Rt, Gd, list, L);
+                vis = nt_pass_r<MODEL, SQ, ZREF, false>(st, tt, negK, a.z_ref, Rt, Gd, rq);
+            if constexpr (CULL) evaluated += (unsigned long long)vis * nv;
 #pragma unroll
             for (int s = 0; s < SQ; ++s) {
                 if (slot[s] < 0) continue;
@@ -565,14 +593,17 @@ __device__ __forceinline__ void nt_line_search_queue(HitStage &st, const NewtonA
 // CULL (K6c, RETINA_MS_CULLED): the same per-seed arithmetic and decisions, bit for bit, with each
 // warp visiting only the hits within reach of its points (cull.cuh): the seeds are taken in the
 // per-event Morton order perm (a warp holds 32 S consecutive ones, so its points stay in a small
-// box), and every pass -- Hessian mode, the alpha = 1 trial, each line-search worker pass, the
-// final pass -- first lists, in hit order, the resident hits that a conservative bound keeps within
-// K s^2 <= 128 of the box of the points it evaluates.  Events larger than the stage run dense.
-// Both variants add the (seed, hit) pairs their passes evaluate for real seeds to pairs_evaluated.
+// box), and the passes -- Hessian mode, the alpha = 1 trial, each line-search worker pass, the
+// final pass -- list, chunk by chunk and in hit order, the resident hits that a conservative bound
+// keeps within K s^2 <= 128 of the box of the points they evaluate.  When a step's Hessian pass
+// keeps more than kNtCullKeep of the hits (wide sigma_j), that warp's trial passes of the step run
+// dense: listing would cost more than it saves (any choice gives the same bits).  Events larger
+// than the stage run dense.  pairs_evaluated: CULL adds the pairs visited for real seeds; the dense
+// kernel adds evaluations x hits.
 template <int MODEL, int S, bool ZREF, bool CULL>
 __global__ void __launch_bounds__(kNtThreads, (MODEL == kSlope3) ? RETINA_NT3_MINB : RETINA_NT_MINB)
     newton_kernel(NewtonArgs a, const int32_t *perm, unsigned long long *pairs_evaluated) {
-    extern __shared__ __align__(16) float4 s_hits[];  // [cap] hits (K6c: then [warps][cap] uint16 lists)
+    extern __shared__ __align__(16) float4 s_hits[];  // [cap] hits (K6c: then [warps][kNtChunk] uint16 lists)
     __shared__ __align__(8) uint64_t s_bar[2];
     constexpr int P = (MODEL == kSlope3) ? 3 : 2;
 
@@ -584,22 +615,25 @@ __global__ void __launch_bounds__(kNtThreads, (MODEL == kSlope3) ? RETINA_NT3_MI
     uint16_t *list = nullptr;  // this warp's list (K6c, resident events)
     if constexpr (CULL) {
         if (nh <= a.cap && nh <= 65535 && (nh == 0 || st.load_resident()))
-            list = reinterpret_cast<uint16_t *>(s_hits + a.cap) + warp * a.cap;
+            list = reinterpret_cast<uint16_t *>(s_hits + a.cap) + warp * kNtChunk;
     }
     unsigned long long evaluated = 0;  // (seed, hit) pairs this warp's passes evaluate for real seeds
-    // the hits a pass over points pts (valid where ok) visits: the warp's list, or all of them
-    auto reach = [&](const float (&pts)[S][3], const bool (&ok)[S], float K) {
-        int L = nh;
+    // a pass over the points pts (valid where ok): restricted to the hits in reach (K6c), or all of
+    // them (nullptr); account() then adds its pairs
+    int rc_nv = 0;
+    auto reach = [&](const float (&pts)[S][3], const bool (&ok)[S], float K, bool use) {
+        NtReach r{{}, 0.f, nullptr};
         if constexpr (CULL) {
             int nv = 0;
 #pragma unroll
             for (int s = 0; s < S; ++s) nv += ok[s] ? 1 : 0;
-            nv = __reduce_add_sync(0xffffffffu, nv);
-            if (list != nullptr)
-                L = mc_build_list<MODEL, ZREF>(st.buf, nh, mc_warp_box<P, S>(pts, ok), K, a.z_ref, list);
-            evaluated += (unsigned long long)L * nv;
+            rc_nv = __reduce_add_sync(0xffffffffu, nv);
+            if (use) r = NtReach{mc_warp_box<P, S>(pts, ok), K, list};
         }
-        return L;
+        return r;
+    };
+    auto account = [&](int visited) {
+        if constexpr (CULL) evaluated += (unsigned long long)visited * rc_nv;
     };
 
     int sid[S];  // position in the CTA's seed range (K6c: in the Morton order)
@@ -636,12 +670,16 @@ __global__ void __launch_bounds__(kNtThreads, (MODEL == kSlope3) ? RETINA_NT3_MI
     }
     for (int j = 0; j < a.n_steps; ++j) {
         const float c = a.c2[j], negK = a.negK[j];
+        bool cull_step = true;  // this warp lists hits for the step's trial passes too
         {
-            const int L = reach(th, valid, -negK);
+            const NtReach r = reach(th, valid, -negK, true);
+            int vis;
             if constexpr (RETINA_NT_X2 && S % 2 == 0)
-                nt_pass_hess_x2<MODEL, S, ZREF>(st, th, negK, a.z_ref, hs, list, L);
+                vis = nt_pass_hess_x2<MODEL, S, ZREF>(st, th, negK, a.z_ref, hs, r);
             else
-                nt_pass_hess<MODEL, S, ZREF>(st, th, negK, a.z_ref, hs, list, L);
+                vis = nt_pass_hess<MODEL, S, ZREF>(st, th, negK, a.z_ref, hs, r);
+            account(vis);
+            if (r.list != nullptr) cull_step = vis <= (int)(kNtCullKeep * nh);
         }
         float R0[S], p[S][3], slope[S], tt[S][3];
         bool active[S];
@@ -697,11 +735,13 @@ __global__ void __launch_bounds__(kNtThreads, (MODEL == kSlope3) ? RETINA_NT3_MI
 #pragma unroll
             for (int s = 0; s < S; ++s) nev[s] += active[s] ? 1 : 0;
             float Rt[S], Gd[S][4];
-            const int L = reach(tt, active, -negK);
+            const NtReach r = reach(tt, active, -negK, cull_step);
+            int vis;
             if constexpr (RETINA_NT_X2 && S % 2 == 0)
-                nt_pass_r_x2<MODEL, S, ZREF, false>(st, tt, negK, a.z_ref, Rt, Gd, list, L);
+                vis = nt_pass_r_x2<MODEL, S, ZREF, false>(st, tt, negK, a.z_ref, Rt, Gd, r);
             else
-                nt_pass_r<MODEL, S, ZREF, false>(st, tt, negK, a.z_ref, Rt, Gd, list, L);
+                vis = nt_pass_r<MODEL, S, ZREF, false>(st, tt, negK, a.z_ref, Rt, Gd, r);
+            account(vis);
 #pragma unroll
             for (int s = 0; s < S; ++s) {
                 if (active[s] && Rt[s] >= __fmaf_rn(1e-4f * alpha, slope[s], R0[s])) {
@@ -714,15 +754,17 @@ __global__ void __launch_bounds__(kNtThreads, (MODEL == kSlope3) ? RETINA_NT3_MI
         }
         if (st.resident && a.max_halvings > 0)
             nt_line_search_queue<MODEL, S, ZREF, CULL>(st, a, negK, th, p, R0, slope, active, nev, Rcur, ls, list,
-                                                 evaluated);
+                                                       cull_step, evaluated);
     }
     float g[S][3];
     if (a.grad_out) {
-        const int L = reach(th, valid, -a.final_negK);
+        const NtReach r = reach(th, valid, -a.final_negK, true);
+        int vis;
         if constexpr (RETINA_NT_X2 && S % 2 == 0)
-            nt_pass_r_x2<MODEL, S, ZREF, true>(st, th, a.final_negK, a.z_ref, R, G, list, L);
+            vis = nt_pass_r_x2<MODEL, S, ZREF, true>(st, th, a.final_negK, a.z_ref, R, G, r);
         else
-            nt_pass_r<MODEL, S, ZREF, true>(st, th, a.final_negK, a.z_ref, R, G, list, L);
+            vis = nt_pass_r<MODEL, S, ZREF, true>(st, th, a.final_negK, a.z_ref, R, G, r);
+        account(vis);
 #pragma unroll
         for (int s = 0; s < S; ++s) {
             g[s][0] = __fmul_rn(a.final_c2, G[s][0]);
@@ -738,11 +780,13 @@ __global__ void __launch_bounds__(kNtThreads, (MODEL == kSlope3) ? RETINA_NT3_MI
 #pragma unroll
         for (int s = 0; s < S; ++s) R[s] = Rcur[s];
     } else {
-        const int L = reach(th, valid, -a.final_negK);
+        const NtReach r = reach(th, valid, -a.final_negK, true);
+        int vis;
         if constexpr (RETINA_NT_X2 && S % 2 == 0)
-            nt_pass_r_x2<MODEL, S, ZREF, false>(st, th, a.final_negK, a.z_ref, R, G, list, L);
+            vis = nt_pass_r_x2<MODEL, S, ZREF, false>(st, th, a.final_negK, a.z_ref, R, G, r);
         else
-            nt_pass_r<MODEL, S, ZREF, false>(st, th, a.final_negK, a.z_ref, R, G, list, L);
+            vis = nt_pass_r<MODEL, S, ZREF, false>(st, th, a.final_negK, a.z_ref, R, G, r);
+        account(vis);
     }
 #pragma unroll
     for (int s = 0; s < S; ++s) {
@@ -775,8 +819,7 @@ static cudaError_t launch_nt(const NewtonArgs &a0, int n_events, const int32_t *
     constexpr int S = (MODEL == kSlope3) ? RETINA_NT3_SEEDS : 4;
     auto kern = newton_kernel<MODEL, S, ZREF, CULL>;
     NewtonArgs a = a0;
-    if (CULL) a.cap = ((std::max(a0.cap, 2) + 7) / 8) * 8;  // 16-byte aligned lists after the stage
-    const size_t smem = (size_t)a.cap * (sizeof(float4) + (CULL ? (kNtThreads / 32) * sizeof(uint16_t) : 0));
+    const size_t smem = (size_t)a.cap * sizeof(float4) + (CULL ? (kNtThreads / 32) * kNtChunk * sizeof(uint16_t) : 0);
     cudaError_t err = ensure_dynamic_smem(kern, smem);
     if (err != cudaSuccess) return err;
     const int blocks = (a.n_seeds + kNtThreads * S - 1) / (kNtThreads * S);

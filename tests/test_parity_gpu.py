@@ -780,7 +780,7 @@ def test_newton_culled_bitwise_equal_to_dense(name, n_ev, n_seeds, z_ref, want_g
     assert int(pd.item()) == total
     n_pc = int(pc.item())
     assert n_pc > 0
-    if hint is None:
+    if hint is None and cfg.model == C.SLOPE2:  # (SLOPE3's wide early sigmas keep nearly every hit in reach)
         assert n_pc < total
     PU.report(f"K6c {name} S={n_seeds}", pairs_dense=total, pairs_evaluated=n_pc, evaluated_frac=n_pc / total)
 
