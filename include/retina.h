@@ -219,9 +219,11 @@ int retina_multistart_optimize(const retina_events *ev, int model, float sigma,
  *                     that every warp's 256 seeds cover a small box, and per pass each warp skips the
  *                     hits that a conservative bound puts beyond K s^2 > 128 for all of them, visiting
  *                     the others in hit order with K4's arithmetic.  Needs a DEVICE workspace of at
- *                     least retina_multistart_workspace_size() bytes (the per-event permutation;
- *                     contents on entry do not matter); n_seeds <= 16,384 (the per-event sort runs in
- *                     shared memory).  Events larger than the hit stage run the dense passes.
+ *                     least retina_multistart_workspace_size() bytes (8 per seed and event: the
+ *                     per-event permutation, and for retina_multistart_newton_ex2 the evaluation
+ *                     counts between its step launches; contents on entry do not matter);
+ *                     n_seeds <= 16,384 (the per-event sort runs in shared memory).  Events larger
+ *                     than the hit stage run the dense passes.
  *   pairs_evaluated:  device uint64 or NULL: the (seed, hit) pairs actually evaluated are ADDED to
  *                     it (all pairs for RETINA_MS_DENSE).
  * Other arguments as retina_multistart_optimize. */
@@ -267,11 +269,12 @@ int retina_multistart_newton_ex(const retina_events *ev, int model, int32_t n_se
 /* retina_multistart_newton_ex with an explicit algorithm (as retina_multistart_optimize_ex):
  *   RETINA_MS_DENSE   every pass visits every hit (what retina_multistart_newton_ex does);
  *   RETINA_MS_CULLED  the SAME results bit for bit (theta, R, grad R and evals_out), each warp
- *                     visiting only the hits that can contribute: the seeds of each event are taken
- *                     in Morton order of theta, and before every pass (Hessian mode, each line-search
- *                     trial pass, the final pass) a warp lists, in hit order, the hits a conservative
- *                     bound keeps within K_j s^2 <= 128 of the box of the points it evaluates (K_j =
- *                     1/sigma_j^2 of that pass); the others would add exactly +0 under ex2.approx.ftz.
+ *                     visiting only the hits that can contribute: one launch per Newton step, before
+ *                     which the seeds of each event are re-ordered along a Morton curve of their
+ *                     current theta; in every pass (Hessian mode, each line-search trial pass, the
+ *                     final pass) a warp lists, in hit order, the hits a conservative bound keeps
+ *                     within K_j s^2 <= 128 of the box of the points it evaluates (K_j = 1/sigma_j^2
+ *                     of that pass); the others would add exactly +0 under ex2.approx.ftz.
  *                     Needs a DEVICE workspace of at least retina_multistart_workspace_size(n_events,
  *                     n_seeds, RETINA_MS_CULLED) bytes; n_seeds <= 16,384.  Events larger than the
  *                     hit stage run the dense passes.

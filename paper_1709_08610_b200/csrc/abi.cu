@@ -297,7 +297,9 @@ int retina_multistart_optimize(const retina_events *ev, int model, float sigma, 
 
 size_t retina_multistart_workspace_size(int32_t n_events, int32_t n_seeds, int algorithm) {
     if (algorithm != RETINA_MS_CULLED || n_events <= 0 || n_seeds <= 0) return 0;
-    return retina::multistart_culled_workspace_bytes(n_events, n_seeds);
+    // one size for both culled paths: K4c needs the permutation, K6c also the evaluation counts
+    return std::max(retina::multistart_culled_workspace_bytes(n_events, n_seeds),
+                    retina::newton_culled_workspace_bytes(n_events, n_seeds));
 }
 
 // the dense path's pair count: hits x seeds x (n_iters + 1) passes, added on the device

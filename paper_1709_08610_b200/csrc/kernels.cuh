@@ -59,6 +59,10 @@ struct NewtonArgs {
     int reuse_final;     // no final pass: final sigma == last sigma and no gradient output
     int cap;
     int e_base;
+    // steps [j_begin, j_end) in this launch; first: theta from seeds (else theta_out) and fresh counts
+    // (else nev_ws); last: the final pass and every output (else theta_out and nev_ws only)
+    int j_begin, j_end, first, last;
+    int32_t *nev_ws;  // K6c: [n_events][n_seeds] evaluation counts between step launches
 };
 
 struct PeakArgs {
@@ -126,9 +130,10 @@ cudaError_t launch_grid_tensor16p(int model, const GridArgs &a, int n_events, cu
 cudaError_t launch_grid_tensor16x2(int model, const GridArgs &a, int n_events, cudaStream_t stream);
 cudaError_t launch_newton(int model, const NewtonArgs &a, int n_events, unsigned long long *pairs_evaluated,
                           cudaStream_t stream);
-// K6c (newton.cu): the same results as K6, evaluating only the pairs that can contribute; perm is the
-// per-event Morton permutation workspace (multistart_culled_workspace_bytes)
-cudaError_t launch_newton_culled(int model, const NewtonArgs &a, int n_events, int32_t *perm,
+// K6c (newton.cu): the same results as K6, evaluating only the pairs that can contribute; ws holds
+// the per-event Morton permutation and the evaluation counts (newton_culled_workspace_bytes)
+size_t newton_culled_workspace_bytes(long long n_events, int n_seeds);
+cudaError_t launch_newton_culled(int model, const NewtonArgs &a, int n_events, int32_t *ws,
                                  unsigned long long *pairs_evaluated, cudaStream_t stream);
 // K4c-sort: perm[e][q] = caller index of event e's q-th seed along a Morton curve over the box
 cudaError_t launch_seed_morton_sort(const float *seeds, int n_seeds, int P, const float (&lo)[3], const float (&hi)[3],

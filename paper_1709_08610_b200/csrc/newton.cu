@@ -42,11 +42,10 @@ struct HessSums {
 // K6c: a pass restricted to the resident hits within reach of the box of the warp's points (cull.cuh):
 // the hits are listed kNtChunk at a time into the warp's list buffer, each chunk's list consumed in
 // hit order before the next is built; visited counts the listed hits.
-constexpr int kNtChunk = 256;
-#ifndef RETINA_NT_CULL_KEEP
-#define RETINA_NT_CULL_KEEP 0.6f  // a step's trial passes are listed only if its Hessian pass kept <= this share
+#ifndef RETINA_NT_CHUNK
+#define RETINA_NT_CHUNK 256  // hits listed per chunk (the list buffer of a warp)
 #endif
-constexpr float kNtCullKeep = RETINA_NT_CULL_KEEP;
+constexpr int kNtChunk = RETINA_NT_CHUNK;
 struct NtReach {
     McBox box;
     float K;         // 1 / sigma^2 of the pass
@@ -474,8 +473,7 @@ __device__ __forceinline__ void nt_line_search_queue(HitStage &st, const NewtonA
                                                      const float (&p)[S][3], const float (&R0)[S],
                                                      const float (&slope)[S], const bool (&active)[S], int (&nev)[S],
                                                      float (&rcur)[S], LineSearchSmem<S, (MODEL == kSlope3) ? 3 : 2> &ls,
-                                                     uint16_t *list, const bool cull_step,
-                                                     unsigned long long &evaluated) {
+                                                     uint16_t *list, unsigned long long &evaluated) {
     constexpr int P = (MODEL == kSlope3) ? 3 : 2;
     constexpr int SQW = (MODEL == kSlope3) ? RETINA_NT3_SQ : RETINA_NT_SQ;
     constexpr int SQ = SQW < S ? SQW : S;
@@ -536,7 +534,7 @@ __device__ __forceinline__ void nt_line_search_queue(HitStage &st, const NewtonA
                     nv += okq[s] ? 1 : 0;
                 }
                 nv = __reduce_add_sync(0xffffffffu, nv);
-                if (cull_step) rq = NtReach{mc_warp_box<P, SQ>(tt, okq), -negK, list};
+                rq = NtReach{mc_warp_box<P, SQ>(tt, okq), -negK, list};
             }
             float Rt[SQ], Gd[SQ][4];
             int vis;
@@ -595,11 +593,13 @@ __device__ __forceinline__ void nt_line_search_queue(HitStage &st, const NewtonA
 // per-event Morton order perm (a warp holds 32 S consecutive ones, so its points stay in a small
 // box), and the passes -- Hessian mode, the alpha = 1 trial, each line-search worker pass, the
 // final pass -- list, chunk by chunk and in hit order, the resident hits that a conservative bound
-// keeps within K s^2 <= 128 of the box of the points they evaluate.  When a step's Hessian pass
-// keeps more than kNtCullKeep of the hits (wide sigma_j), that warp's trial passes of the step run
-// dense: listing would cost more than it saves (any choice gives the same bits).  Events larger
-// than the stage run dense.  pairs_evaluated: CULL adds the pairs visited for real seeds; the dense
-// kernel adds evaluations x hits.
+// keeps within K s^2 <= 128 of the box of the points they evaluate.  K6c runs one launch per
+// Newton step [a.j_begin, a.j_end) with the permutation re-sorted by the seeds' CURRENT theta
+// before each (Newton steps move seeds far; re-sorting keeps every warp's points together), theta
+// and the evaluation count carried in theta_out and the workspace between launches (a.first:
+// theta from seeds; a.last: the final pass and every output).  Events larger than the stage run
+// dense.  pairs_evaluated: CULL adds the pairs visited for real seeds; the dense kernel adds
+// evaluations x hits.
 template <int MODEL, int S, bool ZREF, bool CULL>
 __global__ void __launch_bounds__(kNtThreads, (MODEL == kSlope3) ? RETINA_NT3_MINB : RETINA_NT_MINB)
     newton_kernel(NewtonArgs a, const int32_t *perm, unsigned long long *pairs_evaluated) {
@@ -621,14 +621,14 @@ __global__ void __launch_bounds__(kNtThreads, (MODEL == kSlope3) ? RETINA_NT3_MI
     // a pass over the points pts (valid where ok): restricted to the hits in reach (K6c), or all of
     // them (nullptr); account() then adds its pairs
     int rc_nv = 0;
-    auto reach = [&](const float (&pts)[S][3], const bool (&ok)[S], float K, bool use) {
+    auto reach = [&](const float (&pts)[S][3], const bool (&ok)[S], float K) {
         NtReach r{{}, 0.f, nullptr};
         if constexpr (CULL) {
             int nv = 0;
 #pragma unroll
             for (int s = 0; s < S; ++s) nv += ok[s] ? 1 : 0;
             rc_nv = __reduce_add_sync(0xffffffffu, nv);
-            if (use) r = NtReach{mc_warp_box<P, S>(pts, ok), K, list};
+            r = NtReach{mc_warp_box<P, S>(pts, ok), K, list};
         }
         return r;
     };
@@ -654,8 +654,9 @@ __global__ void __launch_bounds__(kNtThreads, (MODEL == kSlope3) ? RETINA_NT3_MI
             sid[s] = blockIdx.x * (kNtThreads * S) + s * kNtThreads + threadIdx.x;
         valid[s] = sid[s] < a.n_seeds;
         const int64_t src = ((int64_t)e * a.n_seeds + orig(s)) * P;
+        const float *from = a.first ? a.seeds : a.theta_out;  // (written only by this thread, below)
 #pragma unroll
-        for (int i = 0; i < 3; ++i) th[s][i] = (i < P) ? __ldg(a.seeds + src + i) : 0.f;
+        for (int i = 0; i < 3; ++i) th[s][i] = (i < P) ? from[src + i] : 0.f;
     }
 
     __shared__ LineSearchSmem<S, P> ls;
@@ -665,21 +666,20 @@ __global__ void __launch_bounds__(kNtThreads, (MODEL == kSlope3) ? RETINA_NT3_MI
     float Rcur[S];  // R(theta) at the current step's sigma: the last evaluation at the current point
 #pragma unroll
     for (int s = 0; s < S; ++s) {
-        nev[s] = a.n_steps + (a.reuse_final ? 0 : 1);  // q Hessian-mode passes (+ the final one)
+        // q Hessian-mode passes (+ the final one), or the count carried from the previous launch
+        nev[s] = a.first ? a.n_steps + (a.reuse_final ? 0 : 1) : a.nev_ws[(int64_t)e * a.n_seeds + orig(s)];
         Rcur[s] = 0.f;
     }
-    for (int j = 0; j < a.n_steps; ++j) {
+    for (int j = a.j_begin; j < a.j_end; ++j) {
         const float c = a.c2[j], negK = a.negK[j];
-        bool cull_step = true;  // this warp lists hits for the step's trial passes too
         {
-            const NtReach r = reach(th, valid, -negK, true);
+            const NtReach r = reach(th, valid, -negK);
             int vis;
             if constexpr (RETINA_NT_X2 && S % 2 == 0)
                 vis = nt_pass_hess_x2<MODEL, S, ZREF>(st, th, negK, a.z_ref, hs, r);
             else
                 vis = nt_pass_hess<MODEL, S, ZREF>(st, th, negK, a.z_ref, hs, r);
             account(vis);
-            if (r.list != nullptr) cull_step = vis <= (int)(kNtCullKeep * nh);
         }
         float R0[S], p[S][3], slope[S], tt[S][3];
         bool active[S];
@@ -735,7 +735,7 @@ __global__ void __launch_bounds__(kNtThreads, (MODEL == kSlope3) ? RETINA_NT3_MI
 #pragma unroll
             for (int s = 0; s < S; ++s) nev[s] += active[s] ? 1 : 0;
             float Rt[S], Gd[S][4];
-            const NtReach r = reach(tt, active, -negK, cull_step);
+            const NtReach r = reach(tt, active, -negK);
             int vis;
             if constexpr (RETINA_NT_X2 && S % 2 == 0)
                 vis = nt_pass_r_x2<MODEL, S, ZREF, false>(st, tt, negK, a.z_ref, Rt, Gd, r);
@@ -754,11 +754,24 @@ __global__ void __launch_bounds__(kNtThreads, (MODEL == kSlope3) ? RETINA_NT3_MI
         }
         if (st.resident && a.max_halvings > 0)
             nt_line_search_queue<MODEL, S, ZREF, CULL>(st, a, negK, th, p, R0, slope, active, nev, Rcur, ls, list,
-                                                       cull_step, evaluated);
+                                                       evaluated);
+    }
+    if (!a.last) {  // K6c, a step launch before the last: carry theta and the evaluation count
+#pragma unroll
+        for (int s = 0; s < S; ++s) {
+            if (valid[s]) {
+                const int64_t o = (int64_t)e * a.n_seeds + orig(s);
+                a.nev_ws[o] = nev[s];
+#pragma unroll
+                for (int i = 0; i < P; ++i) a.theta_out[o * P + i] = th[s][i];
+            }
+        }
+        if (pairs_evaluated && lane == 0 && evaluated) atomicAdd(pairs_evaluated, evaluated);
+        return;
     }
     float g[S][3];
     if (a.grad_out) {
-        const NtReach r = reach(th, valid, -a.final_negK, true);
+        const NtReach r = reach(th, valid, -a.final_negK);
         int vis;
         if constexpr (RETINA_NT_X2 && S % 2 == 0)
             vis = nt_pass_r_x2<MODEL, S, ZREF, true>(st, th, a.final_negK, a.z_ref, R, G, r);
@@ -780,7 +793,7 @@ __global__ void __launch_bounds__(kNtThreads, (MODEL == kSlope3) ? RETINA_NT3_MI
 #pragma unroll
         for (int s = 0; s < S; ++s) R[s] = Rcur[s];
     } else {
-        const NtReach r = reach(th, valid, -a.final_negK, true);
+        const NtReach r = reach(th, valid, -a.final_negK);
         int vis;
         if constexpr (RETINA_NT_X2 && S % 2 == 0)
             vis = nt_pass_r_x2<MODEL, S, ZREF, false>(st, th, a.final_negK, a.z_ref, R, G, r);
@@ -833,9 +846,13 @@ static cudaError_t launch_nt(const NewtonArgs &a0, int n_events, const int32_t *
     return cudaSuccess;
 }
 
-cudaError_t launch_newton(int model, const NewtonArgs &a, int n_events, unsigned long long *pairs_evaluated,
+cudaError_t launch_newton(int model, const NewtonArgs &a0, int n_events, unsigned long long *pairs_evaluated,
                           cudaStream_t stream) {
-    if (n_events == 0 || a.n_seeds == 0) return cudaSuccess;
+    if (n_events == 0 || a0.n_seeds == 0) return cudaSuccess;
+    NewtonArgs a = a0;  // every step in one launch
+    a.j_begin = 0;
+    a.j_end = a.n_steps;
+    a.first = a.last = 1;
     switch (model) {
         case kSlope2:
             return (a.z_ref == 0.f) ? launch_nt<kSlope2, false, false>(a, n_events, nullptr, pairs_evaluated, stream)
@@ -845,16 +862,35 @@ cudaError_t launch_newton(int model, const NewtonArgs &a, int n_events, unsigned
     return cudaErrorInvalidValue;
 }
 
-cudaError_t launch_newton_culled(int model, const NewtonArgs &a, int n_events, int32_t *perm,
+size_t newton_culled_workspace_bytes(long long n_events, int n_seeds) {
+    return (size_t)(n_events * n_seeds) * 2 * sizeof(int32_t);  // perm, then the evaluation counts
+}
+
+cudaError_t launch_newton_culled(int model, const NewtonArgs &a0, int n_events, int32_t *ws,
                                  unsigned long long *pairs_evaluated, cudaStream_t stream) {
-    if (n_events == 0 || a.n_seeds == 0) return cudaSuccess;
-    const int P = (model == kSlope3) ? 3 : 2;
+    if (n_events == 0 || a0.n_seeds == 0) return cudaSuccess;
     if (model != kSlope2 && model != kSlope3) return cudaErrorInvalidValue;
-    cudaError_t err = launch_seed_morton_sort(a.seeds, a.n_seeds, P, a.lo, a.hi, perm, n_events, stream);
-    if (err != cudaSuccess) return err;
-    if (model == kSlope3) return launch_nt<kSlope3, false, true>(a, n_events, perm, pairs_evaluated, stream);
-    return (a.z_ref == 0.f) ? launch_nt<kSlope2, false, true>(a, n_events, perm, pairs_evaluated, stream)
-                            : launch_nt<kSlope2, true, true>(a, n_events, perm, pairs_evaluated, stream);
+    const int P = (model == kSlope3) ? 3 : 2;
+    int32_t *perm = ws;
+    NewtonArgs a = a0;
+    a.nev_ws = ws + (int64_t)n_events * a.n_seeds;
+    const int launches = a.n_steps > 0 ? a.n_steps : 1;
+    for (int j = 0; j < launches; ++j) {  // one Newton step per launch, the seeds re-sorted by theta first
+        a.j_begin = j;
+        a.j_end = a.n_steps > 0 ? j + 1 : 0;
+        a.first = (j == 0);
+        a.last = (j == launches - 1);
+        cudaError_t err = launch_seed_morton_sort(j == 0 ? a.seeds : a.theta_out, a.n_seeds, P, a.lo, a.hi, perm,
+                                                  n_events, stream);
+        if (err != cudaSuccess) return err;
+        if (model == kSlope3)
+            err = launch_nt<kSlope3, false, true>(a, n_events, perm, pairs_evaluated, stream);
+        else
+            err = (a.z_ref == 0.f) ? launch_nt<kSlope2, false, true>(a, n_events, perm, pairs_evaluated, stream)
+                                   : launch_nt<kSlope2, true, true>(a, n_events, perm, pairs_evaluated, stream);
+        if (err != cudaSuccess) return err;
+    }
+    return cudaSuccess;
 }
 
 }  // namespace retina

@@ -452,7 +452,7 @@ def test_multistart_culled_unsupported_and_workspace():
     with pytest.raises(R.retina.RetinaError):
         R.retina_multistart_optimize(events_of(b2), c2.model, c2.sigma, s2, 1, c2.step, c2.box_lo, c2.box_hi,
                                      algorithm=R.retina.MS_CULLED, workspace=ws)
-    assert R.retina.multistart_workspace_size(3, 100) == 3 * 100 * 4
+    assert R.retina.multistart_workspace_size(3, 100) == 3 * 100 * 8  # permutation + Newton evaluation counts
     assert R.retina.multistart_workspace_size(3, 100, R.retina.MS_DENSE) == 0
 
 
