@@ -66,7 +66,18 @@ __device__ __forceinline__ int mc_build_list_range(const float4 *h, int kb, int 
     for (int k0 = kb; k0 < n; k0 += 32) {
         const int k = k0 + lane;
         bool keep = false;
-        if (k < n) {
+        if (k < n && MODEL == kSlope2 && !ZREF) {
+            // d = z exactly: s_x = x - tx z ranges over [x - hi z, x - lo z] (z >= 0; swapped for
+            // z < 0), so min |s_x| = max(0, x - hi z, lo z - x), each term one FMA (within half an
+            // ulp of the exact value; the 0.99999 below covers it)
+            const float4 hk = h[k];
+            const bool pos = hk.z >= 0.f;
+            const float ax = pos ? B.hi[0] : B.lo[0], bx = pos ? B.lo[0] : B.hi[0];
+            const float ay = pos ? B.hi[1] : B.lo[1], by = pos ? B.lo[1] : B.hi[1];
+            const float mx = fmaxf(0.f, fmaxf(__fmaf_rn(-ax, hk.z, hk.x), __fmaf_rn(bx, hk.z, -hk.x)));
+            const float my = fmaxf(0.f, fmaxf(__fmaf_rn(-ay, hk.z, hk.y), __fmaf_rn(by, hk.z, -hk.y)));
+            keep = K * __fmaf_rn(mx, mx, my * my) * 0.99999f <= 128.f;
+        } else if (k < n) {
             const float4 hk = h[k];
             float d0, d1;  // the range of d, rounded outwards
             if (MODEL == kSlope3) {

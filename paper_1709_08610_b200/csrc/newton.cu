@@ -866,11 +866,16 @@ size_t newton_culled_workspace_bytes(long long n_events, int n_seeds) {
     return (size_t)(n_events * n_seeds) * 2 * sizeof(int32_t);  // perm, then the evaluation counts
 }
 
+// SLOPE3 runs K6 (the dense kernel) under RETINA_MS_CULLED: its wide early sigma_j (x 6, x 3.5 of
+// sigma = 0.88 mm on cfg4) and a warp box's z0 extent keep 80-97 % of the hits in reach
+// (tools/k6c_reach.py), so listing costs more than it saves (cfg4, 100 events: 15.0 ms dense, 16.2
+// culled).  The results are the same either way.
 cudaError_t launch_newton_culled(int model, const NewtonArgs &a0, int n_events, int32_t *ws,
                                  unsigned long long *pairs_evaluated, cudaStream_t stream) {
     if (n_events == 0 || a0.n_seeds == 0) return cudaSuccess;
-    if (model != kSlope2 && model != kSlope3) return cudaErrorInvalidValue;
-    const int P = (model == kSlope3) ? 3 : 2;
+    if (model == kSlope3) return launch_newton(model, a0, n_events, pairs_evaluated, stream);
+    if (model != kSlope2) return cudaErrorInvalidValue;
+    constexpr int P = 2;
     int32_t *perm = ws;
     NewtonArgs a = a0;
     a.nev_ws = ws + (int64_t)n_events * a.n_seeds;
@@ -883,11 +888,8 @@ cudaError_t launch_newton_culled(int model, const NewtonArgs &a0, int n_events, 
         cudaError_t err = launch_seed_morton_sort(j == 0 ? a.seeds : a.theta_out, a.n_seeds, P, a.lo, a.hi, perm,
                                                   n_events, stream);
         if (err != cudaSuccess) return err;
-        if (model == kSlope3)
-            err = launch_nt<kSlope3, false, true>(a, n_events, perm, pairs_evaluated, stream);
-        else
-            err = (a.z_ref == 0.f) ? launch_nt<kSlope2, false, true>(a, n_events, perm, pairs_evaluated, stream)
-                                   : launch_nt<kSlope2, true, true>(a, n_events, perm, pairs_evaluated, stream);
+        err = (a.z_ref == 0.f) ? launch_nt<kSlope2, false, true>(a, n_events, perm, pairs_evaluated, stream)
+                               : launch_nt<kSlope2, true, true>(a, n_events, perm, pairs_evaluated, stream);
         if (err != cudaSuccess) return err;
     }
     return cudaSuccess;
