@@ -588,6 +588,143 @@ __device__ __forceinline__ void nt_line_search_queue(HitStage &st, const NewtonA
     }
 }
 
+// The same halvings with a queue per WARP: the warp's own seeds still searching after the alpha = 1
+// trial are compacted (ballot) into its own part of ls.q, and the warp alone evaluates their
+// (seed, k) entries, 32 SQ per pass: no block barrier, so warps whose passes differ in length (K6c's
+// lists) never wait for each other, and (K6c) a pass's trial points all come from the warp's
+// Morton-neighbouring seeds.  Same entries, same decisions, same bits as the block-wide queue.
+template <int MODEL, int S, bool ZREF, bool CULL>
+__device__ __forceinline__ void nt_line_search_warp(HitStage &st, const NewtonArgs &a, float negK, float (&th)[S][3],
+                                                    const float (&p)[S][3], const float (&R0)[S],
+                                                    const float (&slope)[S], const bool (&active)[S], int (&nev)[S],
+                                                    float (&rcur)[S], LineSearchSmem<S, (MODEL == kSlope3) ? 3 : 2> &ls,
+                                                    uint16_t *list, unsigned long long &evaluated) {
+    constexpr int P = (MODEL == kSlope3) ? 3 : 2;
+    constexpr int SQW = (MODEL == kSlope3) ? RETINA_NT3_SQ : RETINA_NT_SQ;
+    constexpr int SQ = SQW < S ? SQW : S;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const unsigned lt = (1u << lane) - 1u;
+    int *qa = ls.q[0] + warp * 32 * S, *qb = ls.q[1] + warp * 32 * S;  // this warp's two queues
+    __syncwarp();  // the warp's previous reads of ls are done
+    int n = 0;
+#pragma unroll
+    for (int s = 0; s < S; ++s) {
+        const int slot = s * kNtThreads + tid;
+        if (active[s]) {
+#pragma unroll
+            for (int i = 0; i < P; ++i) {
+                ls.base[slot][i] = th[s][i];
+                ls.dir[slot][i] = p[s][i];
+            }
+            ls.R0[slot] = R0[s];
+            ls.slope[slot] = slope[s];
+            ls.kmin[slot] = ~0ull;
+        }
+        const unsigned b = __ballot_sync(0xffffffffu, active[s]);
+        if (active[s]) qa[n + __popc(b & lt)] = slot;
+        n += __popc(b);
+    }
+    __syncwarp();
+    for (int k0 = 1; k0 <= a.max_halvings && n > 0; k0 += kNtLsBatch) {
+        const int nb = min(kNtLsBatch, a.max_halvings - k0 + 1);
+        const int ne = n * nb;
+        for (int wb = 0; wb < ne; wb += 32 * SQ) {
+            int slot[SQ], kk[SQ];
+            float tt[SQ][3];
+#pragma unroll
+            for (int s = 0; s < SQ; ++s) {
+                const int e = wb + s * 32 + lane;
+                const bool valid = e < ne;
+                const int qi = valid ? e / nb : 0;  // padding lanes repeat entry 0
+                kk[s] = k0 + (valid ? e - qi * nb : 0);
+                const int src = qa[qi];
+                slot[s] = valid ? src : -1;
+                const float alpha = __int_as_float((127 - kk[s]) << 23);  // 2^-k, exact
+#pragma unroll
+                for (int i = 0; i < 3; ++i)
+                    tt[s][i] = (i < P) ? fminf(fmaxf(__fmaf_rn(alpha, ls.dir[src][i], ls.base[src][i]), a.lo[i]),
+                                               a.hi[i])
+                                       : 0.f;
+            }
+            NtReach rq{{}, 0.f, nullptr};
+            int nv = 0;
+            if constexpr (CULL) {
+                bool okq[SQ];
+#pragma unroll
+                for (int s = 0; s < SQ; ++s) {
+                    okq[s] = slot[s] >= 0;
+                    nv += okq[s] ? 1 : 0;
+                }
+                nv = __reduce_add_sync(0xffffffffu, nv);
+                rq = NtReach{mc_warp_box<P, SQ>(tt, okq), -negK, list};
+            }
+            float Rt[SQ], Gd[SQ][4];
+            int vis;
+            if constexpr (RETINA_NT_X2 && SQ % 2 == 0)
+                vis = nt_pass_r_x2<MODEL, SQ, ZREF, false>(st, tt, negK, a.z_ref, Rt, Gd, rq);
+            else
+                vis = nt_pass_r<MODEL, SQ, ZREF, false>(st, tt, negK, a.z_ref, Rt, Gd, rq);
+            if constexpr (CULL) evaluated += (unsigned long long)vis * nv;
+#pragma unroll
+            for (int s = 0; s < SQ; ++s) {
+                if (slot[s] < 0) continue;
+                const int sl = slot[s];
+                const float alpha = __int_as_float((127 - kk[s]) << 23);
+                if (Rt[s] >= __fmaf_rn(1e-4f * alpha, ls.slope[sl], ls.R0[sl]))
+                    atomicMin(&ls.kmin[sl], ((unsigned long long)kk[s] << 32) | __float_as_uint(Rt[s]));
+            }
+        }
+        __syncwarp();  // every trial of the round is decided
+        int n2 = 0;
+        for (int i0 = 0; i0 < n; i0 += 32) {
+            const int i = i0 + lane;
+            bool again = false;
+            int sl = 0;
+            if (i < n) {
+                sl = qa[i];
+                const unsigned long long kr = ls.kmin[sl];
+                const int km = (kr == ~0ull) ? 0x7fffffff : (int)(kr >> 32);
+                if (km < k0 + nb) {  // accepted: recompute the trial point (same operations, same bits)
+                    const float alpha = __int_as_float((127 - km) << 23);
+#pragma unroll
+                    for (int d = 0; d < P; ++d)
+                        ls.base[sl][d] =
+                            fminf(fmaxf(__fmaf_rn(alpha, ls.dir[sl][d], ls.base[sl][d]), a.lo[d]), a.hi[d]);
+                } else {
+                    again = true;
+                }
+            }
+            const unsigned b = __ballot_sync(0xffffffffu, again);
+            if (again) qb[n2 + __popc(b & lt)] = sl;
+            n2 += __popc(b);
+        }
+        __syncwarp();
+        int *t = qa;
+        qa = qb;
+        qb = t;
+        n = n2;
+    }
+    __syncwarp();
+#pragma unroll
+    for (int s = 0; s < S; ++s) {
+        if (!active[s]) continue;
+        const int slot = s * kNtThreads + tid;
+#pragma unroll
+        for (int i = 0; i < P; ++i) th[s][i] = ls.base[slot][i];
+        const unsigned long long kr = ls.kmin[slot];
+        if (kr == ~0ull) {
+            nev[s] += a.max_halvings;  // every halving tried, none accepted: theta and R(theta) stay
+        } else {
+            nev[s] += (int)(kr >> 32);
+            rcur[s] = __uint_as_float((uint32_t)kr);  // response at the accepted trial point
+        }
+    }
+}
+
+#ifndef RETINA_NT_WARPQ
+#define RETINA_NT_WARPQ 2  // line-search queue per warp: bit 0 for K6, bit 1 for K6c (else block-wide; K6: cfg4 15.0 vs 16.2 ms per 100 events)
+#endif
+
 // CULL (K6c, RETINA_MS_CULLED): the same per-seed arithmetic and decisions, bit for bit, with each
 // warp visiting only the hits within reach of its points (cull.cuh): the seeds are taken in the
 // per-event Morton order perm (a warp holds 32 S consecutive ones, so its points stay in a small
@@ -726,7 +863,8 @@ __global__ void __launch_bounds__(kNtThreads, (MODEL == kSlope3) ? RETINA_NT3_MI
             bool any = false;
 #pragma unroll
             for (int s = 0; s < S; ++s) any |= active[s];
-            if (!__syncthreads_or(any)) break;
+            // (resident hits: no barrier -- each warp's passes are its own; streamed: block-wide)
+            if (st.resident ? !__any_sync(0xffffffffu, any) : !__syncthreads_or(any)) break;
 #pragma unroll
             for (int s = 0; s < S; ++s)
 #pragma unroll
@@ -752,9 +890,14 @@ __global__ void __launch_bounds__(kNtThreads, (MODEL == kSlope3) ? RETINA_NT3_MI
                 }
             }
         }
-        if (st.resident && a.max_halvings > 0)
-            nt_line_search_queue<MODEL, S, ZREF, CULL>(st, a, negK, th, p, R0, slope, active, nev, Rcur, ls, list,
-                                                       evaluated);
+        if (st.resident && a.max_halvings > 0) {
+            if constexpr ((RETINA_NT_WARPQ >> (CULL ? 1 : 0)) & 1)
+                nt_line_search_warp<MODEL, S, ZREF, CULL>(st, a, negK, th, p, R0, slope, active, nev, Rcur, ls, list,
+                                                          evaluated);
+            else
+                nt_line_search_queue<MODEL, S, ZREF, CULL>(st, a, negK, th, p, R0, slope, active, nev, Rcur, ls, list,
+                                                           evaluated);
+        }
     }
     if (!a.last) {  // K6c, a step launch before the last: carry theta and the evaluation count
 #pragma unroll
