@@ -9,6 +9,8 @@
 #include "common.cuh"
 #include "kernels.cuh"
 
+#include <type_traits>
+
 namespace retina {
 
 struct McBox {
@@ -56,10 +58,10 @@ __device__ __forceinline__ float mc_min_abs(float x, float t0, float t1, float d
 // tuple in B, K ((x - tx d)^2 + (y - ty d)^2) > 128 (then every seed inside B has an ex2 argument
 // < -126, with room for fp32 rounding: w = +0 exactly); d = z - z_ref (SLOPE2) or z - z0 over the
 // box's z0 range (SLOPE3).  In hit order; returns the length.
-// (mc_build_list_range: the hits kb .. n - 1 only.)
-template <int MODEL, bool ZREF>
+// (mc_build_list_range: the hits kb .. n - 1 only; T = float4 lists copies of the hits.)
+template <int MODEL, bool ZREF, class T>
 __device__ __forceinline__ int mc_build_list_range(const float4 *h, int kb, int n, const McBox &B, float K, float zref,
-                                                   uint16_t *list) {
+                                                   T *list) {
     const int lane = threadIdx.x & 31;
     if (B.lo[0] > B.hi[0]) return 0;  // no valid seed in this warp
     int L = 0;
@@ -92,7 +94,12 @@ __device__ __forceinline__ int mc_build_list_range(const float4 *h, int kb, int 
             keep = K * __fmaf_rn(mx, mx, my * my) * 0.99999f <= 128.f;
         }
         const unsigned b = __ballot_sync(0xffffffffu, keep);
-        if (keep) list[L + __popc(b & ((1u << lane) - 1u))] = (uint16_t)k;
+        if (keep) {
+            if constexpr (std::is_same<T, float4>::value)
+                list[L + __popc(b & ((1u << lane) - 1u))] = h[k];  // a copy of the hit (K6c)
+            else
+                list[L + __popc(b & ((1u << lane) - 1u))] = (uint16_t)k;
+        }
         L += __popc(b);
     }
     __syncwarp();

@@ -561,27 +561,32 @@ constexpr int kMcThreads = 128, kMcSeeds = RETINA_MC_SEEDS, kMcWarps = kMcThread
 
 // ---------------------------------------------------------------- K4c-sort: Morton order per event
 // perm[e][q] = caller index of the q-th seed of event e along a Morton curve of the seed's
-// parameters quantised over the prior box (P = 2: 16 bits per axis; P = 3: 10).  Bitonic sort of
-// (key << 32 | index) in shared memory.
+// parameters quantised over the prior box (P = 2: 16 bits per axis; P = 3: 10).  Bitonic sort in
+// shared memory of 32-bit keys: the Morton code's leading 32 - ib bits, then the index (ib bits, n
+// <= 2^ib).  Any order gives the same results (it only groups seeds into warps); this one is
+// deterministic.
 __global__ void __launch_bounds__(1024) seed_morton_sort_kernel(const float *seeds, int n_seeds, int np2, int P,
                                                                 float3 lo, float3 hi, int32_t *perm, int e_base) {
-    extern __shared__ unsigned long long s_key[];
+    extern __shared__ uint32_t s_key[];
     const int e = e_base + blockIdx.x;
     const float *sd = seeds + (int64_t)e * n_seeds * P;
     const int bits = (P == 3) ? 10 : 16;
+    const int ib = 31 - __clz(np2);  // np2 = 2^ib >= n_seeds
+    const int mbits = P * bits, keep = 32 - ib;
     const float qmax = (float)((1 << bits) - 1);
     const float sc[3] = {qmax / fmaxf(hi.x - lo.x, 1e-30f), qmax / fmaxf(hi.y - lo.y, 1e-30f),
                          qmax / fmaxf(hi.z - lo.z, 1e-30f)};
     const float lo3[3] = {lo.x, lo.y, lo.z};
     for (int i = threadIdx.x; i < np2; i += blockDim.x) {
-        unsigned long long k = ~0ull;
+        uint32_t k = 0xffffffffu;  // padding sorts last (a real key has index bits < n - 1 < 2^ib - 1)
         if (i < n_seeds) {
             uint32_t m = 0;
             for (int d = 0; d < P; ++d) {
                 const uint32_t q = (uint32_t)fminf(fmaxf((sd[(int64_t)P * i + d] - lo3[d]) * sc[d], 0.f), qmax);
                 for (int b = 0; b < bits; ++b) m |= ((q >> b) & 1u) << (P * b + d);
             }
-            k = ((unsigned long long)m << 32) | (uint32_t)i;
+            const uint32_t top = (keep >= mbits) ? m : (m >> (mbits - keep));
+            k = (ib == 0) ? 0u : ((top << ib) | (uint32_t)i);
         }
         s_key[i] = k;
     }
@@ -592,7 +597,7 @@ __global__ void __launch_bounds__(1024) seed_morton_sort_kernel(const float *see
                 const int j = i ^ stride;
                 if (j > i) {
                     const bool up = (i & size) == 0;
-                    const unsigned long long a = s_key[i], b = s_key[j];
+                    const uint32_t a = s_key[i], b = s_key[j];
                     if ((a > b) == up) {
                         s_key[i] = b;
                         s_key[j] = a;
@@ -601,8 +606,8 @@ __global__ void __launch_bounds__(1024) seed_morton_sort_kernel(const float *see
             }
             __syncthreads();
         }
-    for (int i = threadIdx.x; i < n_seeds; i += blockDim.x)
-        perm[(int64_t)e * n_seeds + i] = (int32_t)(s_key[i] & 0xffffffffull);
+    const uint32_t imask = (ib >= 32) ? 0xffffffffu : ((1u << ib) - 1u);
+    for (int i = threadIdx.x; i < n_seeds; i += blockDim.x) perm[(int64_t)e * n_seeds + i] = (int32_t)(s_key[i] & imask);
 }
 
 // ---------------------------------------------------------------- K4c (box bound and lists: cull.cuh)
@@ -734,14 +739,14 @@ bool multistart_culled_ok(int model, int n_seeds) {
     // SLOPE2 / SLOPE3; the sort holds an event's seeds in shared memory
     int np2 = 1;
     while (np2 < n_seeds) np2 <<= 1;
-    return (model == kSlope2 || model == kSlope3) && n_seeds > 0 && np2 <= 16384;  // 128 KB of (key, index)
+    return (model == kSlope2 || model == kSlope3) && n_seeds > 0 && np2 <= 16384;  // 64 KB of 32-bit keys
 }
 
 cudaError_t launch_seed_morton_sort(const float *seeds, int n_seeds, int P, const float (&lo)[3], const float (&hi)[3],
                                     int32_t *perm, int n_events, cudaStream_t stream) {
     int np2 = 1;
     while (np2 < n_seeds) np2 <<= 1;
-    const size_t sort_smem = (size_t)np2 * sizeof(unsigned long long);
+    const size_t sort_smem = (size_t)np2 * sizeof(uint32_t);
     cudaError_t err = ensure_dynamic_smem(seed_morton_sort_kernel, sort_smem);
     if (err != cudaSuccess) return err;
     const float3 l3 = make_float3(lo[0], lo[1], lo[2]), h3 = make_float3(hi[0], hi[1], hi[2]);

@@ -40,16 +40,17 @@ struct HessSums {
 };
 
 // K6c: a pass restricted to the resident hits within reach of the box of the warp's points (cull.cuh):
-// the hits are listed kNtChunk at a time into the warp's list buffer, each chunk's list consumed in
-// hit order before the next is built; visited counts the listed hits.
+// the hits are copied kNtChunk at a time into the warp's list buffer, each chunk's list consumed in
+// hit order before the next is built (a copy, not an index: the pass then reads its hits in order,
+// with no dependent shared-memory load per hit).
 #ifndef RETINA_NT_CHUNK
-#define RETINA_NT_CHUNK 256  // hits listed per chunk (the list buffer of a warp)
+#define RETINA_NT_CHUNK 128  // hits listed per chunk (the list buffer of a warp: 2 KB)
 #endif
 constexpr int kNtChunk = RETINA_NT_CHUNK;
 struct NtReach {
     McBox box;
     float K;         // 1 / sigma^2 of the pass
-    uint16_t *list;  // the warp's kNtChunk-entry buffer; nullptr: every hit (dense pass)
+    float4 *list;    // the warp's kNtChunk-entry buffer; nullptr: every hit (dense pass)
 };
 
 // Visits the event's hits in order: all of them (streamed or resident), or (rc.list != nullptr) only
@@ -64,7 +65,7 @@ __device__ __forceinline__ int nt_visit(HitStage &st, const NtReach &rc, float z
                                                            rc.list);
             visited += L;
 #pragma unroll 2
-            for (int t = 0; t < L; ++t) f(h[rc.list[t]]);
+            for (int t = 0; t < L; ++t) f(rc.list[t]);
             __syncwarp();  // the list is rebuilt next
         }
         return visited;
@@ -473,7 +474,7 @@ __device__ __forceinline__ void nt_line_search_queue(HitStage &st, const NewtonA
                                                      const float (&p)[S][3], const float (&R0)[S],
                                                      const float (&slope)[S], const bool (&active)[S], int (&nev)[S],
                                                      float (&rcur)[S], LineSearchSmem<S, (MODEL == kSlope3) ? 3 : 2> &ls,
-                                                     uint16_t *list, unsigned long long &evaluated) {
+                                                     float4 *list, unsigned long long &evaluated) {
     constexpr int P = (MODEL == kSlope3) ? 3 : 2;
     constexpr int SQW = (MODEL == kSlope3) ? RETINA_NT3_SQ : RETINA_NT_SQ;
     constexpr int SQ = SQW < S ? SQW : S;
@@ -598,7 +599,7 @@ __device__ __forceinline__ void nt_line_search_warp(HitStage &st, const NewtonAr
                                                     const float (&p)[S][3], const float (&R0)[S],
                                                     const float (&slope)[S], const bool (&active)[S], int (&nev)[S],
                                                     float (&rcur)[S], LineSearchSmem<S, (MODEL == kSlope3) ? 3 : 2> &ls,
-                                                    uint16_t *list, unsigned long long &evaluated) {
+                                                    float4 *list, unsigned long long &evaluated) {
     constexpr int P = (MODEL == kSlope3) ? 3 : 2;
     constexpr int SQW = (MODEL == kSlope3) ? RETINA_NT3_SQ : RETINA_NT_SQ;
     constexpr int SQ = SQW < S ? SQW : S;
@@ -740,7 +741,7 @@ __device__ __forceinline__ void nt_line_search_warp(HitStage &st, const NewtonAr
 template <int MODEL, int S, bool ZREF, bool CULL>
 __global__ void __launch_bounds__(kNtThreads, (MODEL == kSlope3) ? RETINA_NT3_MINB : RETINA_NT_MINB)
     newton_kernel(NewtonArgs a, const int32_t *perm, unsigned long long *pairs_evaluated) {
-    extern __shared__ __align__(16) float4 s_hits[];  // [cap] hits (K6c: then [warps][kNtChunk] uint16 lists)
+    extern __shared__ __align__(16) float4 s_hits[];  // [cap] hits (K6c: then [warps][kNtChunk] listed hits)
     __shared__ __align__(8) uint64_t s_bar[2];
     constexpr int P = (MODEL == kSlope3) ? 3 : 2;
 
@@ -749,10 +750,10 @@ __global__ void __launch_bounds__(kNtThreads, (MODEL == kSlope3) ? RETINA_NT3_MI
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     HitStage st;
     st.init(s_hits, s_bar, a.hits + start, nh, a.cap);
-    uint16_t *list = nullptr;  // this warp's list (K6c, resident events)
+    float4 *list = nullptr;  // this warp's list (K6c, resident events)
     if constexpr (CULL) {
         if (nh <= a.cap && nh <= 65535 && (nh == 0 || st.load_resident()))
-            list = reinterpret_cast<uint16_t *>(s_hits + a.cap) + warp * kNtChunk;
+            list = s_hits + a.cap + warp * kNtChunk;
     }
     unsigned long long evaluated = 0;  // (seed, hit) pairs this warp's passes evaluate for real seeds
     // a pass over the points pts (valid where ok): restricted to the hits in reach (K6c), or all of
@@ -975,7 +976,7 @@ static cudaError_t launch_nt(const NewtonArgs &a0, int n_events, const int32_t *
     constexpr int S = (MODEL == kSlope3) ? RETINA_NT3_SEEDS : 4;
     auto kern = newton_kernel<MODEL, S, ZREF, CULL>;
     NewtonArgs a = a0;
-    const size_t smem = (size_t)a.cap * sizeof(float4) + (CULL ? (kNtThreads / 32) * kNtChunk * sizeof(uint16_t) : 0);
+    const size_t smem = (size_t)a.cap * sizeof(float4) + (CULL ? (kNtThreads / 32) * kNtChunk * sizeof(float4) : 0);
     cudaError_t err = ensure_dynamic_smem(kern, smem);
     if (err != cudaSuccess) return err;
     const int blocks = (a.n_seeds + kNtThreads * S - 1) / (kNtThreads * S);
