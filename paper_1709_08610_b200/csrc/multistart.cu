@@ -229,6 +229,9 @@ __device__ __forceinline__ PlaneTable build_planes(const float4 *h, int n, int *
     return PlaneTable{s_start, s_z, *s_np, nullptr};
 }
 
+#ifndef RETINA_MC_BATCH
+#define RETINA_MC_BATCH 1  // K4c list loop: 4 listed hits per step (0: one at a time)
+#endif
 // list != nullptr (K4c): only the resident hits list[0 .. L) are visited, in that (hit) order; a
 // new plane is found by comparing z, which runs the same operations as the plane table would.
 template <int MODEL, int S, bool ZREF, bool GRAD, bool WANT_R>
@@ -333,12 +336,25 @@ __device__ __forceinline__ void ms_pass_x2(HitStage &st, const float (&th)[S][3]
     };
     if (list != nullptr) {  // K4c: the warp's listed hits
         const float4 *h = st.buf;
-#pragma unroll 2
-        for (int t = 0; t < L; ++t) {
-            const float4 hk = h[list[t]];
+        auto one = [&](const float4 hk) {
             if (hk.z != zprev) plane(hk.z);  // warp-uniform: the list is the warp's
             body(hk);
+        };
+        int t = 0;
+#if RETINA_MC_BATCH
+        // four indices per 8-byte load, then four independent hit loads: no load waits on the
+        // previous hit's index (the list is 16-byte aligned: cap % 8 == 0)
+        for (; t + 4 <= L; t += 4) {
+            const ushort4 ix = *reinterpret_cast<const ushort4 *>(list + t);
+            const float4 h0 = h[ix.x], h1 = h[ix.y], h2 = h[ix.z], h3 = h[ix.w];
+            one(h0);
+            one(h1);
+            one(h2);
+            one(h3);
         }
+#endif
+#pragma unroll 2
+        for (; t < L; ++t) one(h[list[t]]);
     } else if (pt.np >= 0 && pt.xy) {  // compact stage: (x, y) pairs, plane by plane
         for (int pl = 0; pl < pt.np; ++pl) {
             const int k1 = pt.start[pl + 1];
