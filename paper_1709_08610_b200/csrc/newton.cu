@@ -383,6 +383,12 @@ __device__ __forceinline__ int nt_pass_r_x2(HitStage &st, const float (&th)[S][3
 #ifndef RETINA_NT3_MINB
 #define RETINA_NT3_MINB 3  // SLOPE3 (4 seeds x 3 parameters per thread: 154 registers, no spills)
 #endif
+#ifndef RETINA_NTC_SEEDS
+#define RETINA_NTC_SEEDS 2  // K6c (SLOPE2) seeds per thread (64-seed warps: tighter boxes, 17 % of the pairs instead of 23 %; cfg3 9.63 -> 9.34 ms per 1,000 events)
+#endif
+#ifndef RETINA_NTC_MINB
+#define RETINA_NTC_MINB 5  // K6c CTAs per SM the register allocation must allow (6 / 7: 9.90 / 9.80 ms)
+#endif
 #ifndef RETINA_NT_X2
 #define RETINA_NT_X2 1  // packed seed-pair passes (0: scalar reference passes)
 #endif
@@ -739,7 +745,7 @@ __device__ __forceinline__ void nt_line_search_warp(HitStage &st, const NewtonAr
 // dense.  pairs_evaluated: CULL adds the pairs visited for real seeds; the dense kernel adds
 // evaluations x hits.
 template <int MODEL, int S, bool ZREF, bool CULL>
-__global__ void __launch_bounds__(kNtThreads, (MODEL == kSlope3) ? RETINA_NT3_MINB : RETINA_NT_MINB)
+__global__ void __launch_bounds__(kNtThreads, CULL ? RETINA_NTC_MINB : (MODEL == kSlope3) ? RETINA_NT3_MINB : RETINA_NT_MINB)
     newton_kernel(NewtonArgs a, const int32_t *perm, unsigned long long *pairs_evaluated) {
     extern __shared__ __align__(16) float4 s_hits[];  // [cap] hits (K6c: then [warps][kNtChunk] listed hits)
     __shared__ __align__(8) uint64_t s_bar[2];
@@ -973,7 +979,7 @@ __global__ void __launch_bounds__(kNtThreads, (MODEL == kSlope3) ? RETINA_NT3_MI
 template <int MODEL, bool ZREF, bool CULL>
 static cudaError_t launch_nt(const NewtonArgs &a0, int n_events, const int32_t *perm,
                              unsigned long long *pairs_evaluated, cudaStream_t stream) {
-    constexpr int S = (MODEL == kSlope3) ? RETINA_NT3_SEEDS : 4;
+    constexpr int S = CULL ? RETINA_NTC_SEEDS : (MODEL == kSlope3) ? RETINA_NT3_SEEDS : 4;
     auto kern = newton_kernel<MODEL, S, ZREF, CULL>;
     NewtonArgs a = a0;
     const size_t smem = (size_t)a.cap * sizeof(float4) + (CULL ? (kNtThreads / 32) * kNtChunk * sizeof(float4) : 0);
