@@ -48,12 +48,12 @@ N_SM = 148
 FMA_OPS = {"slope2_iter": 7, "slope3_iter": 8, "line2d_iter": 9, "hessian": 13, "r_only": 6}
 
 
-def binding_pairs_per_clk(ops: float) -> float:
+def binding_pairs_per_clk(ops: float, fma_lanes: float = FMA_PER_SM_CLK) -> float:
     """Pairs/clk/SM of a loop with one MUFU.EX2 and `ops` FMA-pipe lane-ops per pair: the lower
-    of the MUFU rate and the FMA pipe's nominal 128 lanes/clk/SM (measured 121.5 for FFMA with
-    immediate operands; 85-97 for FFMA2 with register operands, so loops near the FMA bound land
-    below 1.0 of it)."""
-    return min(MUFU_PER_SM_CLK, FMA_PER_SM_CLK / ops)
+    of the MUFU rate and the FMA pipe's rate (nominal 128 lanes/clk/SM; measured 121.5 for FFMA
+    with immediate operands, 85-97 for FFMA2 with register operands, so loops near the FMA bound
+    land below 1.0 of the nominal figure -- `fma_lanes` = FMA_REG_LANES gives the measured one)."""
+    return min(MUFU_PER_SM_CLK, fma_lanes / ops)
 
 
 def peaks_json():
@@ -599,14 +599,19 @@ def main():
                 ev_mean = float(pipe.evals[:E].to(torch.float64).mean().item())
                 cyc = (q / binding_pairs_per_clk(FMA_OPS["hessian"])
                        + max(0.0, ev_mean - q) / binding_pairs_per_clk(FMA_OPS["r_only"])) / ev_mean
+                cyc_m = (q / binding_pairs_per_clk(FMA_OPS["hessian"], FMA_REG_LANES)
+                         + max(0.0, ev_mean - q) / binding_pairs_per_clk(FMA_OPS["r_only"], FMA_REG_LANES)) / ev_mean
                 basis = (f"{q} Hessian-mode evaluations (13 FMA-pipe lane-ops/pair) and {ev_mean - q:.2f} R-only "
                          f"evaluations (6) per seed on average")
             else:
                 ops = FMA_OPS[{C.SLOPE2: "slope2_iter", C.SLOPE3: "slope3_iter"}.get(cfg.model, "line2d_iter")]
                 cyc = 1.0 / binding_pairs_per_clk(ops)
+                cyc_m = 1.0 / binding_pairs_per_clk(ops, FMA_REG_LANES)
                 basis = f"{ops} FMA-pipe lane-ops per pair in the iterations"
             bpeak = N_SM * fmax / cyc
+            bpeak_m = N_SM * fmax / cyc_m
             r["binding"] = {"peak_pairs_per_s": bpeak, "frac": pairs_s / bpeak,
+                            "measured_fma_peak_pairs_per_s": bpeak_m, "frac_at_measured_fma": pairs_s / bpeak_m,
                             "basis": basis + f"; FMA pipe at its nominal {FMA_PER_SM_CLK} lanes/clk/SM (measured "
                                              f"{FMA_REG_LANES} for FFMA2 with register operands, tools/pipe_microbench.cu), "
                                              "MUFU at 16/clk/SM: the lower rate binds"}
