@@ -322,7 +322,8 @@ def retina_multistart_optimize(events: Events, model: int, sigma: float, seeds: 
 
 
 def multistart_workspace_size(n_events: int, n_seeds: int, algorithm: int = MS_CULLED) -> int:
-    """Bytes of device workspace retina_multistart_optimize_ex needs (0 for MS_DENSE)."""
+    """Bytes of device workspace retina_multistart_optimize_ex and retina_multistart_newton_ex2 need
+    (0 for MS_DENSE)."""
     return int(lib().retina_multistart_workspace_size(int(n_events), int(n_seeds), int(algorithm)))
 
 

@@ -785,6 +785,28 @@ def test_newton_culled_bitwise_equal_to_dense(name, n_ev, n_seeds, z_ref, want_g
     PU.report(f"K6c {name} S={n_seeds}", pairs_dense=total, pairs_evaluated=n_pc, evaluated_frac=n_pc / total)
 
 
+def test_newton_culled_no_steps_and_aliasing():
+    """K6c with an empty schedule (one launch: the final pass only) and with theta_out aliasing the
+    seeds (each launch reads the theta the previous one wrote) equals K6 bit for bit."""
+    cfg = C.CFG2
+    b = G.make_batch(cfg, [0, 1])
+    seeds = G.make_seeds(cfg, [0, 1], n_seeds=1500)
+    ev = events_of(b)
+    sig, eta, fsig, mh = C.newton_schedule(cfg)
+    for steps in (0, len(sig)):
+        d = R.retina_multistart_newton_ex(ev, cfg.model, dev(seeds), sig[:steps], eta[:steps], fsig, mh, cfg.box_lo,
+                                          cfg.box_hi)
+        sd = dev(seeds)
+        Rc = torch.empty(sd.shape[:2], dtype=torch.float32, device=DEV)
+        gc = torch.empty_like(sd)
+        nc = torch.empty(sd.shape[:2], dtype=torch.int32, device=DEV)
+        c = R.retina_multistart_newton_ex(ev, cfg.model, sd, sig[:steps], eta[:steps], fsig, mh, cfg.box_lo,
+                                          cfg.box_hi, out=(sd, Rc, gc, nc), algorithm=R.retina.MS_CULLED)
+        torch.cuda.synchronize()
+        for x, y in zip(d, c):
+            assert torch.equal(x.view(torch.int32), y.view(torch.int32))
+
+
 def test_newton_culled_unsupported_and_workspace():
     c2 = C.CFG2
     b2 = G.make_batch(c2, [0])
