@@ -21,6 +21,10 @@
 //   H_txz0 = -c^2 (tx sum d wA^2 + ty sum d wAB) + c tx sum d w - c sum wA,
 //   H_tyz0 = -c^2 (tx sum d wAB + ty sum d wB^2) + c ty sum d w - c sum wB,
 //   H_z0z0 = c^2 (tx^2 sum wA^2 + 2 tx ty sum wAB + ty^2 sum wB^2) - c (tx^2 + ty^2) sum w.
+//
+// K6c (CULL, RETINA_MS_CULLED, SLOPE2): the same kernel, each warp visiting only the hits that can
+// contribute (a skipped hit's ex2.approx.ftz weight is exactly +0, cull.cuh), one launch per Newton
+// step with the seeds re-sorted by their current theta before each -- see newton_kernel.
 #include "common.cuh"
 #include "kernels.cuh"
 #include "cull.cuh"
