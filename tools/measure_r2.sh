@@ -34,15 +34,24 @@ run dense --dense --events 2000 --steps 3 --no-cpu-baseline --e2e-steps 1
 run cfg4dense --config cfg4 --dense --events 100 --steps 3 --no-cpu-baseline --e2e-steps 1
 for c in cfg0 cfg1 cfg2; do run $c --config $c --steps 5; done
 run ref --impl reference --steps 1 --warmup 0
+# the opt-in culled kernels (K4c / K6c bit-identical to K4 / K6; the culled grid within T1)
+run culled --ms-algo culled --steps 5 --no-cpu-baseline
+run culled_grid_and_ms --ms-algo culled --grid-algo culled --steps 5 --no-cpu-baseline
+run cfg2_culled --config cfg2 --ms-algo culled --steps 5 --no-cpu-baseline
+run cfg4full_culled --config cfg4 --ms-algo culled --steps 3 --warmup 3 --no-cpu-baseline
+run newton_culled --update newton --ms-algo culled --steps 5 --no-cpu-baseline
+run newton_culled_grid --update newton --ms-algo culled --grid-algo culled --steps 5 --no-cpu-baseline
 timeout 600 python tools/cost_constants.py > gpurun_out/${P}_cost_constants_cfg3.json 2>&1
 tail -2 gpurun_out/${P}_pytest_gpu.txt
 python - "$P" <<'PY'
 import json, sys
 p = sys.argv[1]
-for f in ("", "_newton", "_cfg4", "_cfg4full", "_dense", "_cfg4dense", "_cfg0", "_cfg1", "_cfg2", "_ref"):
+for f in ("", "_newton", "_cfg4", "_cfg4full", "_dense", "_cfg4dense", "_cfg0", "_cfg1", "_cfg2", "_ref", "_culled",
+          "_culled_grid_and_ms", "_cfg2_culled", "_cfg4full_culled", "_newton_culled", "_newton_culled_grid"):
     try:
         d = json.load(open(f"gpurun_out/{p}_bench{f}.json"))
         print(f or "default", "%.4g" % d["value"], round(d["ms_per_step"], 2), d.get("roofline", {}).get("frac"),
+              round(d.get("events_per_s", 0)),
               {k: round(v, 2) for k, v in d.get("phases_ms_per_step", {}).items()})
     except Exception as exc:  # report and go on: one failed line must not hide the others
         print(f, "FAILED", exc)
