@@ -673,7 +673,9 @@ __global__ void __launch_bounds__(kMcThreads, RETINA_MC_MINB)
         for (int s = 0; s < S; ++s) {
             const int q = q0 + s * 32;
             ok[s] = q < a.n_seeds;
-            const int64_t src = ((int64_t)e * a.n_seeds + __ldg(pe + min(q, a.n_seeds - 1))) * P;
+            const int qo = __ldg(pe + min(q, a.n_seeds - 1));
+            RETINA_ASSERT(qo >= 0 && qo < a.n_seeds);
+            const int64_t src = ((int64_t)e * a.n_seeds + qo) * P;
 #pragma unroll
             for (int i = 0; i < 3; ++i) th[s][i] = (i < P) ? __ldg(a.seeds + src + i) : 0.f;
         }

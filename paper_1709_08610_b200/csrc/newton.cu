@@ -67,6 +67,7 @@ __device__ __forceinline__ int nt_visit(HitStage &st, const NtReach &rc, float z
         for (int k0 = 0; k0 < st.n; k0 += kNtChunk) {
             const int L = mc_build_list_range<MODEL, ZREF>(h, k0, min(st.n, k0 + kNtChunk), rc.box, rc.K, zref,
                                                            rc.list);
+            RETINA_ASSERT(L >= 0 && L <= kNtChunk);
             visited += L;
 #pragma unroll 2
             for (int t = 0; t < L; ++t) f(rc.list[t]);
@@ -635,6 +636,7 @@ __device__ __forceinline__ void nt_line_search_warp(HitStage &st, const NewtonAr
         if (active[s]) qa[n + __popc(b & lt)] = slot;
         n += __popc(b);
     }
+    RETINA_ASSERT(n <= 32 * S);
     __syncwarp();
     for (int k0 = 1; k0 <= a.max_halvings && n > 0; k0 += kNtLsBatch) {
         const int nb = min(kNtLsBatch, a.max_halvings - k0 + 1);
@@ -789,10 +791,13 @@ __global__ void __launch_bounds__(kNtThreads, CULL ? RETINA_NTC_MINB : (MODEL ==
     float th[S][3];
     // the caller's index of seed s
     auto orig = [&](int s) {
-        if constexpr (CULL)
-            return __ldg(perm + (int64_t)e * a.n_seeds + min(sid[s], a.n_seeds - 1));
-        else
+        if constexpr (CULL) {
+            const int q = __ldg(perm + (int64_t)e * a.n_seeds + min(sid[s], a.n_seeds - 1));
+            RETINA_ASSERT(q >= 0 && q < a.n_seeds);
+            return q;
+        } else {
             return min(sid[s], a.n_seeds - 1);
+        }
     };
 #pragma unroll
     for (int s = 0; s < S; ++s) {
