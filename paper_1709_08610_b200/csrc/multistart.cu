@@ -577,53 +577,107 @@ constexpr int kMcThreads = 128, kMcSeeds = RETINA_MC_SEEDS, kMcWarps = kMcThread
 
 // ---------------------------------------------------------------- K4c-sort: Morton order per event
 // perm[e][q] = caller index of the q-th seed of event e along a Morton curve of the seed's
-// parameters quantised over the prior box (P = 2: 16 bits per axis; P = 3: 10).  Bitonic sort in
-// shared memory of 32-bit keys: the Morton code's leading 32 - ib bits, then the index (ib bits, n
-// <= 2^ib).  Any order gives the same results (it only groups seeds into warps); this one is
-// deterministic.
-__global__ void __launch_bounds__(1024) seed_morton_sort_kernel(const float *seeds, int n_seeds, int np2, int P,
-                                                                float3 lo, float3 hi, int32_t *perm, int e_base) {
-    extern __shared__ uint32_t s_key[];
-    const int e = e_base + blockIdx.x;
+// parameters quantised over the prior box (P = 2: 16 bits per axis; P = 3: 10).  Bitonic sort of
+// 32-bit keys -- the Morton code's leading 32 - ib bits, then the index (ib bits, N = 2^ib >= n,
+// N >= 1024) -- with E = N / 1024 keys per thread in registers: compare-exchange stages of stride
+// < E run inside a thread, strides < 32 E through warp shuffles, only the wider ones through
+// shared memory (two block barriers each: 15 such stages for N = 8192 instead of 91 in a plain
+// shared-memory network).  Any order gives the same results (it only groups seeds into warps);
+// this one is deterministic.
+__device__ __forceinline__ uint32_t morton_spread2(uint32_t x) {  // 16 bits -> even bit positions
+    x &= 0xffffu;
+    x = (x | (x << 8)) & 0x00ff00ffu;
+    x = (x | (x << 4)) & 0x0f0f0f0fu;
+    x = (x | (x << 2)) & 0x33333333u;
+    return (x | (x << 1)) & 0x55555555u;
+}
+__device__ __forceinline__ uint32_t morton_spread3(uint32_t x) {  // 10 bits -> every third bit
+    x &= 0x3ffu;
+    x = (x | (x << 16)) & 0xff0000ffu;
+    x = (x | (x << 8)) & 0x0300f00fu;
+    x = (x | (x << 4)) & 0x030c30c3u;
+    return (x | (x << 2)) & 0x09249249u;
+}
+
+// compare-exchange of register pairs (r, r ^ ST) of thread t's E consecutive keys
+template <int E, int ST>
+__device__ __forceinline__ void sort_cx_reg(uint32_t (&k)[E], int t, int size) {
+#pragma unroll
+    for (int r = 0; r < E; ++r) {
+        if ((r ^ ST) > r) {
+            const bool up = ((t * E + r) & size) == 0;
+            const uint32_t a = k[r], b = k[r ^ ST];
+            k[r] = up ? min(a, b) : max(a, b);
+            k[r ^ ST] = up ? max(a, b) : min(a, b);
+        }
+    }
+}
+
+template <int E>
+__global__ void __launch_bounds__(1024) seed_morton_sort_kernel(const float *seeds, int n_seeds, int P, float3 lo,
+                                                                float3 hi, int32_t *perm, int e_base) {
+    constexpr int N = 1024 * E;
+    constexpr int ib = 10 + (E >= 2) + (E >= 4) + (E >= 8) + (E >= 16);  // log2(N)
+    extern __shared__ uint32_t s_key[];  // N + N / 32 words (one pad word per 32: no bank conflicts)
+    const int e = e_base + blockIdx.x, t = threadIdx.x;
     const float *sd = seeds + (int64_t)e * n_seeds * P;
     const int bits = (P == 3) ? 10 : 16;
-    const int ib = 31 - __clz(np2);  // np2 = 2^ib >= n_seeds
     const int mbits = P * bits, keep = 32 - ib;
     const float qmax = (float)((1 << bits) - 1);
     const float sc[3] = {qmax / fmaxf(hi.x - lo.x, 1e-30f), qmax / fmaxf(hi.y - lo.y, 1e-30f),
                          qmax / fmaxf(hi.z - lo.z, 1e-30f)};
     const float lo3[3] = {lo.x, lo.y, lo.z};
-    for (int i = threadIdx.x; i < np2; i += blockDim.x) {
-        uint32_t k = 0xffffffffu;  // padding sorts last (a real key has index bits < n - 1 < 2^ib - 1)
+    uint32_t k[E];
+#pragma unroll
+    for (int r = 0; r < E; ++r) {
+        const int i = t * E + r;
+        k[r] = 0xffffffffu;  // padding sorts last (a real key's index bits are < n - 1 < N - 1)
         if (i < n_seeds) {
             uint32_t m = 0;
             for (int d = 0; d < P; ++d) {
                 const uint32_t q = (uint32_t)fminf(fmaxf((sd[(int64_t)P * i + d] - lo3[d]) * sc[d], 0.f), qmax);
-                for (int b = 0; b < bits; ++b) m |= ((q >> b) & 1u) << (P * b + d);
+                m |= (P == 3 ? morton_spread3(q) : morton_spread2(q)) << d;
             }
             const uint32_t top = (keep >= mbits) ? m : (m >> (mbits - keep));
-            k = (ib == 0) ? 0u : ((top << ib) | (uint32_t)i);
+            k[r] = (top << ib) | (uint32_t)i;
         }
-        s_key[i] = k;
     }
-    __syncthreads();
-    for (int size = 2; size <= np2; size <<= 1)
+    auto pad = [](int i) { return i + (i >> 5); };
+    for (int size = 2; size <= N; size <<= 1)
         for (int stride = size >> 1; stride > 0; stride >>= 1) {
-            for (int i = threadIdx.x; i < np2; i += blockDim.x) {
-                const int j = i ^ stride;
-                if (j > i) {
-                    const bool up = (i & size) == 0;
-                    const uint32_t a = s_key[i], b = s_key[j];
-                    if ((a > b) == up) {
-                        s_key[i] = b;
-                        s_key[j] = a;
-                    }
+            if (stride < E) {  // both elements in this thread (compile-time register indices)
+                if (stride == 1) sort_cx_reg<E, 1>(k, t, size);
+                if constexpr (E > 2) if (stride == 2) sort_cx_reg<E, 2>(k, t, size);
+                if constexpr (E > 4) if (stride == 4) sort_cx_reg<E, 4>(k, t, size);
+                if constexpr (E > 8) if (stride == 8) sort_cx_reg<E, 8>(k, t, size);
+            } else if (stride < 32 * E) {  // partner in lane ^ (stride / E), same register
+#pragma unroll
+                for (int r = 0; r < E; ++r) {
+                    const int i = t * E + r;
+                    const uint32_t v = __shfl_xor_sync(0xffffffffu, k[r], stride / E);
+                    const bool keep_min = ((i & stride) == 0) == ((i & size) == 0);
+                    k[r] = keep_min ? min(k[r], v) : max(k[r], v);
                 }
+            } else {  // partner in another warp
+#pragma unroll
+                for (int r = 0; r < E; ++r) s_key[pad(t * E + r)] = k[r];
+                __syncthreads();
+#pragma unroll
+                for (int r = 0; r < E; ++r) {
+                    const int i = t * E + r;
+                    const uint32_t v = s_key[pad(i ^ stride)];
+                    const bool keep_min = ((i & stride) == 0) == ((i & size) == 0);
+                    k[r] = keep_min ? min(k[r], v) : max(k[r], v);
+                }
+                __syncthreads();
             }
-            __syncthreads();
         }
-    const uint32_t imask = (ib >= 32) ? 0xffffffffu : ((1u << ib) - 1u);
-    for (int i = threadIdx.x; i < n_seeds; i += blockDim.x) perm[(int64_t)e * n_seeds + i] = (int32_t)(s_key[i] & imask);
+    const uint32_t imask = (1u << ib) - 1u;
+#pragma unroll
+    for (int r = 0; r < E; ++r) {
+        const int i = t * E + r;
+        if (i < n_seeds) perm[(int64_t)e * n_seeds + i] = (int32_t)(k[r] & imask);
+    }
 }
 
 // ---------------------------------------------------------------- K4c (box bound and lists: cull.cuh)
@@ -760,21 +814,34 @@ bool multistart_culled_ok(int model, int n_seeds) {
     return (model == kSlope2 || model == kSlope3) && n_seeds > 0 && np2 <= 16384;  // 64 KB of 32-bit keys
 }
 
-cudaError_t launch_seed_morton_sort(const float *seeds, int n_seeds, int P, const float (&lo)[3], const float (&hi)[3],
-                                    int32_t *perm, int n_events, cudaStream_t stream) {
-    int np2 = 1;
-    while (np2 < n_seeds) np2 <<= 1;
-    const size_t sort_smem = (size_t)np2 * sizeof(uint32_t);
-    cudaError_t err = ensure_dynamic_smem(seed_morton_sort_kernel, sort_smem);
+template <int E>
+static cudaError_t launch_sort_e(const float *seeds, int n_seeds, int P, float3 lo, float3 hi, int32_t *perm,
+                                 int n_events, cudaStream_t stream) {
+    const size_t smem = (size_t)(1024 * E + 32 * E) * sizeof(uint32_t);
+    cudaError_t err = ensure_dynamic_smem(seed_morton_sort_kernel<E>, smem);
     if (err != cudaSuccess) return err;
-    const float3 l3 = make_float3(lo[0], lo[1], lo[2]), h3 = make_float3(hi[0], hi[1], hi[2]);
     for (int e0 = 0; e0 < n_events; e0 += 65535) {
         const int ne = std::min(65535, n_events - e0);
-        seed_morton_sort_kernel<<<ne, 1024, sort_smem, stream>>>(seeds, n_seeds, np2, P, l3, h3, perm, e0);
+        seed_morton_sort_kernel<E><<<ne, 1024, smem, stream>>>(seeds, n_seeds, P, lo, hi, perm, e0);
         err = cudaGetLastError();
         if (err != cudaSuccess) return err;
     }
     return cudaSuccess;
+}
+
+cudaError_t launch_seed_morton_sort(const float *seeds, int n_seeds, int P, const float (&lo)[3], const float (&hi)[3],
+                                    int32_t *perm, int n_events, cudaStream_t stream) {
+    int np2 = 1024;
+    while (np2 < n_seeds) np2 <<= 1;
+    const float3 l3 = make_float3(lo[0], lo[1], lo[2]), h3 = make_float3(hi[0], hi[1], hi[2]);
+    switch (np2 / 1024) {
+        case 1: return launch_sort_e<1>(seeds, n_seeds, P, l3, h3, perm, n_events, stream);
+        case 2: return launch_sort_e<2>(seeds, n_seeds, P, l3, h3, perm, n_events, stream);
+        case 4: return launch_sort_e<4>(seeds, n_seeds, P, l3, h3, perm, n_events, stream);
+        case 8: return launch_sort_e<8>(seeds, n_seeds, P, l3, h3, perm, n_events, stream);
+        case 16: return launch_sort_e<16>(seeds, n_seeds, P, l3, h3, perm, n_events, stream);
+    }
+    return cudaErrorInvalidValue;  // n_seeds > 16384 (multistart_culled_ok rejects it first)
 }
 
 template <int MODEL, int S, bool ZREF>
