@@ -277,7 +277,8 @@ int retina_multistart_newton_ex(const retina_events *ev, int model, int32_t n_se
  *                     of that pass); the others would add exactly +0 under ex2.approx.ftz.
  *                     Needs a DEVICE workspace of at least retina_multistart_workspace_size(n_events,
  *                     n_seeds, RETINA_MS_CULLED) bytes; n_seeds <= 16,384.  Events larger than the
- *                     hit stage run the dense passes.
+ *                     hit stage run the dense passes, and so does RETINA_SLOPE3 (its wide early
+ *                     sigma_j keep nearly every hit in reach); the results are the same either way.
  *   pairs_evaluated:  device uint64 or NULL: RETINA_MS_DENSE ADDS evaluations x hits (every
  *                     evaluation visits every hit); RETINA_MS_CULLED adds the (seed, hit) pairs its
  *                     passes visited for real seeds (including the line search's speculative
