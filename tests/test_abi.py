@@ -133,8 +133,9 @@ def test_multistart_validation(L):
 
 
 def test_newton_validation(L):
-    for fn in (L.retina_multistart_newton, L.retina_multistart_newton_ex):
-        ex = fn is L.retina_multistart_newton_ex
+    for fn in (L.retina_multistart_newton, L.retina_multistart_newton_ex, L.retina_multistart_newton_ex2):
+        ex = fn is not L.retina_multistart_newton
+        ex2 = fn is L.retina_multistart_newton_ex2
         ev = _ev()
         lo, hi = _f(-1, -1), _f(1, 1)
         sg, et = _f(0.5, 0.2), _f(1e-3, 1e-3)
@@ -143,6 +144,8 @@ def test_newton_validation(L):
             args = [ctypes.byref(ev), model, S, 16, steps, sig, eta, fs, mh, lo_, hi_, th, R, None]
             if ex:
                 args.append(None)
+            if ex2:
+                args += [rt.MS_DENSE, None, ctypes.c_size_t(0), None]
             return fn(*args, None)
 
         assert call(model=0) == rt.RETINA_EUNSUPPORTED          # LINE2D has no Newton kernel
@@ -158,6 +161,28 @@ def test_newton_validation(L):
         assert call(lo_=hi, hi_=lo) == rt.RETINA_EINVAL
         assert call(th=None) == rt.RETINA_EINVAL
         assert call(S=0, th=None, R=None) == rt.RETINA_OK        # nothing to do
+
+
+def test_newton_ex2_algorithm_and_workspace(L):
+    """retina_multistart_newton_ex2: unknown algorithm, a missing or short workspace and too many
+    seeds for the per-event sort are rejected before anything is launched; the workspace size is
+    8 bytes per (event, seed) for RETINA_MS_CULLED (permutation + evaluation counts), 0 for dense."""
+    f = L.retina_multistart_newton_ex2
+    ev = _ev()
+    lo, hi = _f(-1, -1), _f(1, 1)
+    sg, et = _f(0.5, 0.2), _f(1e-3, 1e-3)
+
+    def call(algo, S=8, ws=None, nbytes=0):
+        return f(ctypes.byref(ev), 1, S, 16, 2, sg, et, 0.2, 8, lo, hi, 16, 16, None, None, algo, ws,
+                 ctypes.c_size_t(nbytes), None, None)
+    assert call(2) == rt.RETINA_EINVAL
+    assert call(-1) == rt.RETINA_EINVAL
+    assert call(rt.MS_CULLED) == rt.RETINA_EINVAL                            # no workspace
+    assert call(rt.MS_CULLED, ws=16, nbytes=8) == rt.RETINA_EINVAL           # too small
+    assert call(rt.MS_CULLED, S=16385, ws=16, nbytes=1 << 30) == rt.RETINA_EUNSUPPORTED
+    wsz = L.retina_multistart_workspace_size
+    assert wsz(3, 100, rt.MS_CULLED) == 3 * 100 * 8
+    assert wsz(3, 100, rt.MS_DENSE) == 0 and wsz(0, 100, rt.MS_CULLED) == 0
 
 
 def test_merge_validation(L):
