@@ -520,9 +520,13 @@ static cudaError_t launch_ms(const MultistartArgs &a0, int n_events, cudaStream_
     a.compact = (MODEL == kSlope3 && (int)((227 * 1024) / ((size_t)a.cap * sizeof(float4) + 1024)) < want) ? 1 : 0;
     const size_t per_cta = (size_t)a.cap * (a.compact ? sizeof(float2) : sizeof(float4)) + 1024;
     const int fit = (int)((227 * 1024) / per_cta);
-    if (fit >= want || MODEL == kLine2D) return launch_ms_t<MODEL, ZREF, kMsThreads>(a, n_events, stream);
-    if (2 * fit >= want) return launch_ms_t<MODEL, ZREF, 2 * kMsThreads>(a, n_events, stream);
-    return launch_ms_t<MODEL, ZREF, 4 * kMsThreads>(a, n_events, stream);
+    if constexpr (MODEL == kLine2D) {  // (2-D toy events: always small)
+        return launch_ms_t<MODEL, ZREF, kMsThreads>(a, n_events, stream);
+    } else {
+        if (fit >= want) return launch_ms_t<MODEL, ZREF, kMsThreads>(a, n_events, stream);
+        if (2 * fit >= want) return launch_ms_t<MODEL, ZREF, 2 * kMsThreads>(a, n_events, stream);
+        return launch_ms_t<MODEL, ZREF, 4 * kMsThreads>(a, n_events, stream);
+    }
 }
 
 cudaError_t launch_multistart(int model, const MultistartArgs &a, int n_events, cudaStream_t stream) {
