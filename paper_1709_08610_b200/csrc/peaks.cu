@@ -22,7 +22,10 @@ struct PeakV {
     static constexpr int v = (P == 3) ? 4 : 16;
 };
 constexpr int kSlabCells = 131072;  // cells per CTA in the workspace (two-pass) variant
-constexpr int kSlabList = 256;      // peaks a slab keeps from pass 1 (more: pass 2 rescans it)
+#ifndef RETINA_PK_SLABLIST
+#define RETINA_PK_SLABLIST 1024  // (256: the dense-hit cfg3 variant rescanned most slabs, 6.2 vs 4.5 ms per 1,024 events)
+#endif
+constexpr int kSlabList = RETINA_PK_SLABLIST;  // peaks a slab keeps from pass 1 (more: pass 2 rescans it)
 
 __device__ __forceinline__ int warp_incl_scan(int v) {
     const int lane = threadIdx.x & 31;

@@ -85,10 +85,11 @@ class RetinaPipeline:
         if self.overlap:
             self.grid_bufs.append(torch.empty_like(self.grid_buf))
             self.side = torch.cuda.Stream(self.device, priority=-1)
-        # many-CTA peak finder when a chunk has too few events to fill the GPU with one CTA per
-        # event (large grids, e.g. 256^3); one CTA per event otherwise (single read of the grid)
+        # the many-CTA peak finder (slabs of 131,072 cells, or 3x3x3 plane blocks): one CTA per
+        # event leaves the last wave of a chunk part-empty (cfg3, 2,048 events: 2.50 ms one CTA per
+        # event, 2.20 ms in slabs; the dense-hit variant 5.14 vs 4.52)
         self.peak_ws = None
-        if cells and self.chunk < 2 * 148:
+        if cells:
             ws = R.find_peaks_workspace_size(self.chunk, shape)
             self.peak_ws = torch.empty((max(ws, 4) // 4,), dtype=torch.int32, device=self.device)
         E, P = max_events, spec.P

@@ -240,8 +240,9 @@ def test_T3_peaks_workspace_path_identical(P, shape):
 @pytest.mark.parametrize("P,shape", [(2, (3, 1024, 1024)), (3, (2, 96, 96, 96))])
 def test_T3_peaks_workspace_slab_lists_and_rescans(P, shape):
     """Sparse peaks (kept in the per-slab lists of pass 1 and copied) next to a dense region
-    (more than 256 peaks in a slab: pass 2 rescans it), in the same event: the workspace path
-    equals the single-CTA path and the oracle bit for bit, for several capacities."""
+    (P = 2: ~3,200 strict maxima in one slab, more than its list keeps, so pass 2 rescans it), in
+    the same event: the workspace path equals the single-CTA path and the oracle bit for bit, for
+    several capacities."""
     rng = np.random.default_rng(40 + P)
     g = rng.uniform(0.0, 1.0, shape).astype(np.float32)          # below threshold everywhere
     flat = g.reshape(shape[0], -1)
@@ -250,7 +251,7 @@ def test_T3_peaks_workspace_slab_lists_and_rescans(P, shape):
         pk = rng.choice(cells, 300, replace=False)                 # isolated planted peaks
         flat[e, pk] = rng.uniform(3.0, 9.0, 300).astype(np.float32)
         d0 = 131072 * (e % max(1, cells // 131072))                # one dense slab per event
-        flat[e, d0:d0 + 20000] = rng.integers(2, 9, 20000).astype(np.float32)
+        flat[e, d0:d0 + 60000] = rng.integers(2, 9, 60000).astype(np.float32)
     g = flat.reshape(shape)
     dg = dev(g)
     ws = torch.empty((R.retina.find_peaks_workspace_size(shape[0], shape[1:]) // 4 + 1,), dtype=torch.int32,

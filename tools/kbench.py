@@ -34,6 +34,7 @@ def main():
     ap.add_argument("--dense", action="store_true")
     ap.add_argument("--phases", default="grid,peaks,ms")
     ap.add_argument("--tag", default="")
+    ap.add_argument("--peaks-ws", action="store_true", help="peaks: always the many-CTA workspace path")
     a = ap.parse_args()
     cfg = C.get_config(a.config, dense=True) if a.dense else C.get_config(a.config)
     if a.seeds:
@@ -73,7 +74,7 @@ def main():
         pk = (torch.empty((chunk, cap), dtype=torch.int32, device="cuda"),
               torch.empty((chunk, cap), device="cuda"), torch.empty((chunk,), dtype=torch.int32, device="cuda"))
         ws = None
-        if chunk < 2 * 148:
+        if chunk < 2 * 148 or a.peaks_ws:
             ws = torch.empty((RT.find_peaks_workspace_size(chunk, shape) // 4 + 1,), dtype=torch.int32, device="cuda")
         maxh = int(np.diff(b.offsets).max())
         if "grid" in phases:
