@@ -99,8 +99,8 @@ def test_peaks_workspace_size_and_validation(L):
     sz = L.retina_find_peaks_workspace_size
     sz.restype = ctypes.c_size_t
     # 1024^2 cells -> 8 slabs of 131072 cells per event; per slab a count (4 B) and a list of
-    # 256 (index, value) pairs (8 B each)
-    per_slab = 4 + 256 * 8
+    # 1024 (index, value) pairs (8 B each)
+    per_slab = 4 + 1024 * 8
     assert sz(10, 2, _i(1024, 1024)) == 10 * 8 * per_slab
     # P = 3 grids are scanned in memory order (n2, n0, n1) (z0 planes outermost, Z37).
     # Rows (axis_len[1] cells) of a multiple of 4 cells (<= 2048): the plane-block path
