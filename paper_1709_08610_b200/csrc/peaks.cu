@@ -121,6 +121,8 @@ __device__ __forceinline__ int scan_range(const PeakArgs &a, const float *g, int
             }
         }
         const int cnt = __popc(mask);
+        // most sweeps hold no peak: one barrier decides that, and the block scan is skipped
+        if (!__syncthreads_or(cnt != 0)) continue;
         const int incl = warp_incl_scan(cnt);
         if (lane == 31) s_warp[warp] = incl;
         __syncthreads();
