@@ -72,7 +72,9 @@ class RetinaPipeline:
         cells = spec.cells
         if cells:
             chunk_events = max(1, min(chunk_events, int(grid_bytes_budget // (4 * cells))))
-        self.chunk = min(chunk_events, max(1, max_events))
+        # equal chunks (a short last chunk leaves most of the GPU idle in its grid and peak scan)
+        n_chunks = -(-max(1, max_events) // max(1, chunk_events))
+        self.chunk = -(-max(1, max_events) // n_chunks)
         self.nodes = [torch.from_numpy(np.ascontiguousarray(n, np.float32)).to(self.device) for n in spec.nodes]
         shape = R.grid_shape(self.chunk, [len(n) for n in spec.nodes])[1:]  # (n2,) n0, n1: z0 planes outermost
         self.grid_buf = torch.empty((self.chunk,) + shape, dtype=torch.float32, device=self.device) if cells else None
